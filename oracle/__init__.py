@@ -1,0 +1,143 @@
+"""CPU oracle for arXiv 1202.6575 (stable two-way merge and stable merge sort).
+
+TEST INFRASTRUCTURE ONLY.  Only `tests/`, `__graft_entry__.smoke()` and the
+`cpu_baseline` / `--impl reference` legs of `bench.py` may import this
+package.  The product path (`paper_1202_6575_b200`) never imports it, and this
+package imports nothing from the product path: the two share no code.
+
+Contents
+  oracle.c   O1 merge, O2 sort, rank_low/rank_high, O4 closed-form positions
+             (plain C, single thread, built by `build()` with gcc)
+  plan.py    O3: the paper's Steps 1-4 (block partition, cross ranks,
+             classification into cases (a)-(e)), in plain Python, used to pin
+             the worked example of Fig. 1 and to compare the device plan.
+
+Pins (tests/test_oracle.py, `-m "not gpu"`): Fig. 1 golden values
+(tests/golden/fig1.json), brute-force stable sort of the tagged concatenation,
+Python's stable `sorted`, the closed-form positions, exhaustive small
+instances and the output invariants.  No function here is "parity unpinned".
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "oracle.c")
+_LIB = os.path.join(_HERE, "liboracle.so")
+
+NP_DTYPES = {"u32": np.uint32, "i32": np.int32, "i64": np.int64, "u64": np.uint64}
+_C_KEY = {"u32": ctypes.c_uint32, "i32": ctypes.c_int32, "i64": ctypes.c_int64, "u64": ctypes.c_uint64}
+
+_lib = None
+
+
+def build(force: bool = False) -> str:
+    """Compile oracle.c into liboracle.so (gcc, -O2, no vectorisation tricks)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        subprocess.check_call(["gcc", "-O2", "-std=c99", "-shared", "-fPIC", "-o", _LIB, _SRC])
+    return _LIB
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        build()
+        _lib = ctypes.CDLL(_LIB)
+        P = ctypes.c_void_p
+        I = ctypes.c_int64
+        for kt in NP_DTYPES:
+            getattr(_lib, f"oracle_merge_{kt}").argtypes = [P, P, I, P, P, I, P, P]
+            getattr(_lib, f"oracle_merge_{kt}").restype = None
+            getattr(_lib, f"oracle_sort_{kt}").argtypes = [P, P, I]
+            getattr(_lib, f"oracle_sort_{kt}").restype = ctypes.c_int
+            getattr(_lib, f"oracle_rank_low_{kt}").argtypes = [_C_KEY[kt], P, I]
+            getattr(_lib, f"oracle_rank_low_{kt}").restype = I
+            getattr(_lib, f"oracle_rank_high_{kt}").argtypes = [_C_KEY[kt], P, I]
+            getattr(_lib, f"oracle_rank_high_{kt}").restype = I
+            getattr(_lib, f"oracle_positions_{kt}").argtypes = [P, I, P, I, P, P]
+            getattr(_lib, f"oracle_positions_{kt}").restype = None
+            getattr(_lib, f"oracle_positions_sample_{kt}").argtypes = [P, I, P, I, P, I, P, P, I, P]
+            getattr(_lib, f"oracle_positions_sample_{kt}").restype = None
+    return _lib
+
+
+def _ptr(a):
+    return None if a is None else a.ctypes.data_as(ctypes.c_void_p)
+
+
+def as_np(x, key_type: str = None):
+    """torch CPU tensor / array -> contiguous numpy array.  With `key_type`
+    the bits are viewed in that key type (u32/u64 carried in int32/int64)."""
+    if x is None:
+        return None
+    if hasattr(x, "detach"):
+        x = x.detach().cpu().contiguous().numpy()
+    x = np.ascontiguousarray(x)
+    if key_type is not None:
+        x = x.view(NP_DTYPES[key_type])
+    return x
+
+
+def vals_np(x):
+    """Payload array -> numpy uint32 view."""
+    if x is None:
+        return None
+    return as_np(x).view(np.uint32)
+
+
+def merge(a_keys, a_vals, b_keys, b_vals, key_type: str):
+    """O1: the stable merge of A and B, ties to A.  Returns (c_keys, c_vals)
+    as numpy arrays (c_vals None when the inputs carry no payload)."""
+    a, b = as_np(a_keys, key_type), as_np(b_keys, key_type)
+    va, vb = vals_np(a_vals), vals_np(b_vals)
+    assert (va is None) == (vb is None)
+    n, m = a.size, b.size
+    c = np.empty(n + m, dtype=NP_DTYPES[key_type])
+    vc = None if va is None else np.empty(n + m, dtype=np.uint32)
+    getattr(lib(), f"oracle_merge_{key_type}")(_ptr(a), _ptr(va), n, _ptr(b), _ptr(vb), m, _ptr(c), _ptr(vc))
+    return c, vc
+
+
+def sort(keys, vals, key_type: str):
+    """O2: stable bottom-up merge sort.  Returns sorted copies."""
+    k = as_np(keys, key_type).copy()
+    v = None if vals is None else vals_np(vals).copy()
+    rc = getattr(lib(), f"oracle_sort_{key_type}")(_ptr(k), _ptr(v), k.size)
+    if rc != 0:
+        raise MemoryError("oracle_sort: allocation failed")
+    return k, v
+
+
+def rank_low(x, X, key_type: str) -> int:
+    X = as_np(X, key_type)
+    return int(getattr(lib(), f"oracle_rank_low_{key_type}")(NP_DTYPES[key_type](x).item(), _ptr(X), X.size))
+
+
+def rank_high(x, X, key_type: str) -> int:
+    X = as_np(X, key_type)
+    return int(getattr(lib(), f"oracle_rank_high_{key_type}")(NP_DTYPES[key_type](x).item(), _ptr(X), X.size))
+
+
+def positions(a_keys, b_keys, key_type: str):
+    """O4: closed-form output positions."""
+    a, b = as_np(a_keys, key_type), as_np(b_keys, key_type)
+    pa = np.empty(a.size, dtype=np.int64)
+    pb = np.empty(b.size, dtype=np.int64)
+    getattr(lib(), f"oracle_positions_{key_type}")(_ptr(a), a.size, _ptr(b), b.size, _ptr(pa), _ptr(pb))
+    return pa, pb
+
+
+def positions_sample(a_keys, b_keys, key_type: str, ia, jb):
+    """O4 for sampled indices ia (into A) and jb (into B)."""
+    a, b = as_np(a_keys, key_type), as_np(b_keys, key_type)
+    ia = np.ascontiguousarray(ia, dtype=np.int64)
+    jb = np.ascontiguousarray(jb, dtype=np.int64)
+    pa = np.empty(ia.size, dtype=np.int64)
+    pb = np.empty(jb.size, dtype=np.int64)
+    getattr(lib(), f"oracle_positions_sample_{key_type}")(_ptr(a), a.size, _ptr(b), b.size, _ptr(ia), ia.size,
+                                                          _ptr(pa), _ptr(jb), jb.size, _ptr(pb))
+    return pa, pb

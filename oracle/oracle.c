@@ -1,0 +1,139 @@
+/*
+ * oracle/oracle.c -- plain, slow, obviously correct CPU oracle for the stable
+ * merge and the stable merge sort of arXiv 1202.6575.
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and the
+ * cpu_baseline / --impl reference legs of bench.py may load this library.
+ * It shares no code, header, table or helper with the CUDA path
+ * (paper_1202_6575_b200/csrc) and includes nothing from it.
+ *
+ * The method reaches exactly the plain stable merge (§2, Theorem
+ * L366-371 with the correctness argument L343-357), so the oracle is that
+ * definition written out, not the parallel algorithm:
+ *
+ *   oracle_merge_*   two pointers; emit A[i] when A[i] <= B[j], else B[j]
+ *                    ("all (repeated) elements a from A are ordered before
+ *                    elements a from B").
+ *   oracle_sort_*    bottom-up stable merge sort: runs of width 1, 2, 4, ...
+ *                    merged pairwise with the left run playing A (§3
+ *                    L403-416: the unique stable sort).
+ *   oracle_rank_low_*  / oracle_rank_high_*   rank_low(x,X) = unique i with
+ *                    X[i-1] < x <= X[i]; rank_high(x,X) = unique j with
+ *                    X[j-1] <= x < X[j]  (sentinels
+ *                    X[-1]=-inf, X[len]=+inf, L69-71), by plain binary search.
+ *   oracle_positions_*  the closed form of PAPER.md L158-166: A[i] goes to
+ *                    C[i + rank_low(A[i],B)], B[j] to C[j + rank_high(B[j],A)].
+ *
+ * Keys: u32 / i32 / i64 / u64 with the natural (unsigned or signed) order.
+ * Payloads: uint32, travelling with their key; NULL payload pointers mean
+ * keys only.  Sizes are int64.  No error paths: callers pass valid sizes.
+ */
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+#define DEFINE_ORACLE(SUF, K)                                                         \
+                                                                                      \
+/* Stable two-way merge, ties to A.  vc may be NULL (keys only). */                  \
+void oracle_merge_##SUF(const K *a, const uint32_t *va, int64_t n,                   \
+                        const K *b, const uint32_t *vb, int64_t m,                   \
+                        K *c, uint32_t *vc)                                          \
+{                                                                                     \
+    int64_t i = 0, j = 0, k = 0;                                                     \
+    while (i < n && j < m) {                                                         \
+        if (a[i] <= b[j]) {               /* tie -> A first */                       \
+            c[k] = a[i];                                                             \
+            if (vc) vc[k] = va[i];                                                   \
+            i++;                                                                     \
+        } else {                                                                     \
+            c[k] = b[j];                                                             \
+            if (vc) vc[k] = vb[j];                                                   \
+            j++;                                                                     \
+        }                                                                            \
+        k++;                                                                         \
+    }                                                                                \
+    while (i < n) { c[k] = a[i]; if (vc) vc[k] = va[i]; i++; k++; }                 \
+    while (j < m) { c[k] = b[j]; if (vc) vc[k] = vb[j]; j++; k++; }                 \
+}                                                                                     \
+                                                                                      \
+/* Bottom-up stable merge sort in place (result in keys/vals). */                   \
+int oracle_sort_##SUF(K *keys, uint32_t *vals, int64_t N)                            \
+{                                                                                     \
+    K *src = keys, *dst;                                                             \
+    uint32_t *vsrc = vals, *vdst = NULL;                                             \
+    int64_t width;                                                                   \
+    if (N <= 1) return 0;                                                            \
+    dst = (K *)malloc((size_t)N * sizeof(K));                                        \
+    if (!dst) return -1;                                                             \
+    if (vals) {                                                                      \
+        vdst = (uint32_t *)malloc((size_t)N * sizeof(uint32_t));                     \
+        if (!vdst) { free(dst); return -1; }                                         \
+    }                                                                                \
+    K *kbuf = dst; uint32_t *vbuf = vdst;                                            \
+    for (width = 1; width < N; width *= 2) {                                         \
+        int64_t lo;                                                                  \
+        for (lo = 0; lo < N; lo += 2 * width) {                                      \
+            int64_t mid = lo + width < N ? lo + width : N;                           \
+            int64_t hi = lo + 2 * width < N ? lo + 2 * width : N;                    \
+            /* left run [lo,mid) plays A, right run [mid,hi) plays B */             \
+            oracle_merge_##SUF(src + lo, vsrc ? vsrc + lo : NULL, mid - lo,          \
+                               src + mid, vsrc ? vsrc + mid : NULL, hi - mid,        \
+                               dst + lo, vsrc ? vdst + lo : NULL);                   \
+        }                                                                            \
+        { K *t = src; src = dst; dst = t; }                                          \
+        { uint32_t *t = vsrc; vsrc = vdst; vdst = t; }                               \
+    }                                                                                \
+    if (src != keys) {                                                               \
+        memcpy(keys, src, (size_t)N * sizeof(K));                                    \
+        if (vals) memcpy(vals, vsrc, (size_t)N * sizeof(uint32_t));                  \
+    }                                                                                \
+    free(kbuf);                                                                      \
+    free(vbuf);                                                                      \
+    return 0;                                                                        \
+}                                                                                     \
+                                                                                      \
+/* rank_low(x, X): number of elements of X strictly less than x. */                 \
+int64_t oracle_rank_low_##SUF(K x, const K *X, int64_t len)                          \
+{                                                                                     \
+    int64_t lo = 0, hi = len;       /* answer in [lo, hi] */                        \
+    while (lo < hi) {                                                                \
+        int64_t mid = lo + (hi - lo) / 2;                                            \
+        if (X[mid] < x) lo = mid + 1; else hi = mid;                                 \
+    }                                                                                \
+    return lo;                                                                       \
+}                                                                                     \
+                                                                                      \
+/* rank_high(x, X): number of elements of X less than or equal to x. */             \
+int64_t oracle_rank_high_##SUF(K x, const K *X, int64_t len)                         \
+{                                                                                     \
+    int64_t lo = 0, hi = len;                                                        \
+    while (lo < hi) {                                                                \
+        int64_t mid = lo + (hi - lo) / 2;                                            \
+        if (X[mid] <= x) lo = mid + 1; else hi = mid;                                \
+    }                                                                                \
+    return lo;                                                                       \
+}                                                                                     \
+                                                                                      \
+/* Closed-form output positions. */                             \
+void oracle_positions_##SUF(const K *a, int64_t n, const K *b, int64_t m,            \
+                            int64_t *pos_a, int64_t *pos_b)                          \
+{                                                                                     \
+    int64_t i, j;                                                                    \
+    for (i = 0; i < n; i++) pos_a[i] = i + oracle_rank_low_##SUF(a[i], b, m);        \
+    for (j = 0; j < m; j++) pos_b[j] = j + oracle_rank_high_##SUF(b[j], a, n);       \
+}                                                                                     \
+                                                                                      \
+/* Positions for a sample of indices only (full-size parity checks). */             \
+void oracle_positions_sample_##SUF(const K *a, int64_t n, const K *b, int64_t m,     \
+                                   const int64_t *ia, int64_t na, int64_t *pos_a,    \
+                                   const int64_t *jb, int64_t nb, int64_t *pos_b)    \
+{                                                                                     \
+    int64_t t;                                                                       \
+    for (t = 0; t < na; t++) pos_a[t] = ia[t] + oracle_rank_low_##SUF(a[ia[t]], b, m);\
+    for (t = 0; t < nb; t++) pos_b[t] = jb[t] + oracle_rank_high_##SUF(b[jb[t]], a, n);\
+}
+
+DEFINE_ORACLE(u32, uint32_t)
+DEFINE_ORACLE(i32, int32_t)
+DEFINE_ORACLE(i64, int64_t)
+DEFINE_ORACLE(u64, uint64_t)

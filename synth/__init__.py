@@ -1,0 +1,206 @@
+"""Seeded synthetic inputs shared by the oracle side and the CUDA side.
+
+This module holds NONE of the method's arithmetic (no ranks, no partition, no
+merge): it only draws pseudo-random keys, sorts them with a library sort where
+the workload says "each array sorted", and attaches the source-index payloads
+that make stability observable.  Both `oracle/` (through the tests) and the
+CUDA path (through the tests, `smoke()` and `bench.py`) take their inputs from
+here, so the two sides see the same bits.
+
+Generator: SplitMix64 used as a counter-based generator (DESIGN.md "Input
+recipe"):
+
+    s       = mix64((seed << 8) | stream)
+    r_i     = mix64(s + (i + 1) * 0x9E3779B97F4A7C15)      (mod 2^64)
+    K(r, k) = ((r >> 32) * k) >> 32                        (Lemire, 0 <= K < k)
+
+All arithmetic is done in torch int64 with wrap-around (two's complement) and
+explicit masks after right shifts, so it is device-agnostic: the same tensor
+comes out on the CPU and on `cuda:0`.  Unsigned keys (u32/u64) are carried in
+int32/int64 tensors with the same bit pattern.
+
+Workloads follow BASELINE.json `configs` (C1..C5) with the readings R13/R14 of
+SURVEY.md §8(c):
+  C1  n=m=2^20  u32 key = K(r, 2^16), payload A: i, B: 0x80000000|j
+  C2  n=m=2^26  i32 key = top 32 bits of r (full signed range), keys only
+  C3  n=2^28 m=2^16  i64 key = K(r, 1000), payloads as C1
+  C4  n=2^27 m=2^25  u64 key = 2^63 with probability 0.9 (K(r4,10) < 9) else r
+  C5  N=2^28  u32 key = K(r, 2^20) unsorted, payload = original index
+"""
+from __future__ import annotations
+
+import dataclasses
+from typing import Optional
+
+import torch
+
+BASE_SEED = 0x12026575
+STREAM_A, STREAM_B, STREAM_SORT, STREAM_BERN = 1, 2, 3, 4
+
+_GOLDEN = 0x9E3779B97F4A7C15
+_M1 = 0xBF58476D1CE4E5B9
+_M2 = 0x94D049BB133111EB
+_MASK64 = (1 << 64) - 1
+
+
+def _s64(u: int) -> int:
+    """Unsigned 64-bit constant -> the int64 with the same bits."""
+    u &= _MASK64
+    return u - (1 << 64) if u >= (1 << 63) else u
+
+
+def _lsr(x: torch.Tensor, k: int) -> torch.Tensor:
+    """Logical right shift of int64 bit patterns."""
+    return (x >> k) & ((1 << (64 - k)) - 1)
+
+
+def _mix64(z: torch.Tensor) -> torch.Tensor:
+    z = (z ^ _lsr(z, 30)) * _s64(_M1)
+    z = (z ^ _lsr(z, 27)) * _s64(_M2)
+    return z ^ _lsr(z, 31)
+
+
+def _mix64_int(z: int) -> int:
+    z &= _MASK64
+    z = ((z ^ (z >> 30)) * _M1) & _MASK64
+    z = ((z ^ (z >> 27)) * _M2) & _MASK64
+    return z ^ (z >> 31)
+
+
+def splitmix_stream(seed: int, stream: int, count: int, device="cpu", start: int = 0) -> torch.Tensor:
+    """r_i for i in [start, start+count) as int64 bit patterns (uint64 values)."""
+    s = _mix64_int(((seed << 8) | stream) & _MASK64)
+    i = torch.arange(start + 1, start + count + 1, dtype=torch.int64, device=device)
+    return _mix64(i * _s64(_GOLDEN) + _s64(s))
+
+
+def bounded(r: torch.Tensor, k: int) -> torch.Tensor:
+    """Lemire multiply-shift: uniform-ish integer in [0, k), k <= 2^32."""
+    assert 0 < k <= (1 << 32)
+    return _lsr(_lsr(r, 32) * k, 32)
+
+
+def sort_bits(x: torch.Tensor, unsigned: bool) -> torch.Tensor:
+    """Library sort of keys carried as int32/int64 bit patterns (ascending in
+    the signed or unsigned order)."""
+    if not unsigned:
+        return torch.sort(x, stable=True).values
+    flip = torch.tensor(torch.iinfo(x.dtype).min, dtype=x.dtype, device=x.device)
+    return torch.sort(x ^ flip, stable=True).values ^ flip
+
+
+KEY_TYPES = {
+    # name: (torch carrier dtype, unsigned, key bytes)
+    "u32": (torch.int32, True, 4),
+    "i32": (torch.int32, False, 4),
+    "i64": (torch.int64, False, 8),
+    "u64": (torch.int64, True, 8),
+}
+
+
+@dataclasses.dataclass
+class MergeInput:
+    key_type: str
+    a_keys: torch.Tensor
+    b_keys: torch.Tensor
+    a_vals: Optional[torch.Tensor]
+    b_vals: Optional[torch.Tensor]
+
+    @property
+    def n(self) -> int:
+        return self.a_keys.numel()
+
+    @property
+    def m(self) -> int:
+        return self.b_keys.numel()
+
+    def to(self, device) -> "MergeInput":
+        f = lambda t: None if t is None else t.to(device)
+        return MergeInput(self.key_type, f(self.a_keys), f(self.b_keys), f(self.a_vals), f(self.b_vals))
+
+
+@dataclasses.dataclass
+class SortInput:
+    key_type: str
+    keys: torch.Tensor
+    vals: Optional[torch.Tensor]
+
+    @property
+    def N(self) -> int:
+        return self.keys.numel()
+
+
+def source_payloads(n: int, m: int, device="cpu"):
+    """R13: A[i] -> i, B[j] -> 0x80000000 | j (uint32 bits in int32)."""
+    assert n < (1 << 31) and m < (1 << 31)
+    a = torch.arange(n, dtype=torch.int32, device=device)
+    b = torch.arange(m, dtype=torch.int64, device=device) | (1 << 31)
+    b = b.to(torch.int32) if m == 0 else (b - (1 << 32)).to(torch.int32)
+    return a, b
+
+
+def _keys(dist: str, key_type: str, seed: int, stream: int, count: int, device) -> torch.Tensor:
+    dtype, unsigned, _ = KEY_TYPES[key_type]
+    r = splitmix_stream(seed, stream, count, device)
+    if dist.startswith("bounded:"):
+        k = int(dist.split(":", 1)[1])
+        v = bounded(r, k)
+    elif dist == "full":
+        v = _lsr(r, 32) if dtype == torch.int32 else r
+        if dtype == torch.int32:
+            v = torch.where(v >= (1 << 31), v - (1 << 32), v)
+    elif dist.startswith("mostly:"):
+        # "mostly:<V>:<num>/<den>": key = V with probability num/den, else r.
+        _, vs, frac = dist.split(":")
+        num, den = (int(t) for t in frac.split("/"))
+        V = _s64(int(vs, 0))
+        bern = bounded(splitmix_stream(seed, STREAM_BERN * 16 + stream, count, device), den) < num
+        v = torch.where(bern, torch.full_like(r, V), r)
+    elif dist == "equal":
+        v = torch.zeros(count, dtype=torch.int64, device=device)
+    else:
+        raise ValueError(dist)
+    return v.to(dtype)
+
+
+def merge_input(n: int, m: int, key_type: str, dist: str, seed: int, payload: bool = True,
+                device="cpu") -> MergeInput:
+    """Two independently sorted arrays A (n) and B (m) of `dist` keys."""
+    _, unsigned, _ = KEY_TYPES[key_type]
+    a = sort_bits(_keys(dist, key_type, seed, STREAM_A, n, device), unsigned)
+    b = sort_bits(_keys(dist, key_type, seed, STREAM_B, m, device), unsigned)
+    av = bv = None
+    if payload:
+        av, bv = source_payloads(n, m, device)
+    return MergeInput(key_type, a, b, av, bv)
+
+
+def sort_input(N: int, key_type: str, dist: str, seed: int, payload: bool = True, device="cpu") -> SortInput:
+    keys = _keys(dist, key_type, seed, STREAM_SORT, N, device)
+    vals = torch.arange(N, dtype=torch.int32, device=device) if payload else None
+    return SortInput(key_type, keys, vals)
+
+
+# BASELINE.json configs (index 1..5 as in SURVEY.md §8).  `scale` divides the
+# sizes (power of two) for small parity cases of the same distribution.
+CONFIGS = {
+    1: dict(kind="merge", n=1 << 20, m=1 << 20, key_type="u32", dist="bounded:65536", payload=True),
+    2: dict(kind="merge", n=1 << 26, m=1 << 26, key_type="i32", dist="full", payload=False),
+    3: dict(kind="merge", n=1 << 28, m=1 << 16, key_type="i64", dist="bounded:1000", payload=True),
+    4: dict(kind="merge", n=1 << 27, m=1 << 25, key_type="u64", dist="mostly:0x8000000000000000:9/10",
+            payload=True),
+    5: dict(kind="sort", N=1 << 28, key_type="u32", dist="bounded:1048576", payload=True),
+}
+
+
+def config_input(cfg: int, scale: int = 1, device="cpu"):
+    c = CONFIGS[cfg]
+    seed = BASE_SEED + cfg
+    if c["kind"] == "merge":
+        return merge_input(max(c["n"] // scale, 1), max(c["m"] // scale, 1), c["key_type"], c["dist"], seed,
+                           c["payload"], device)
+    return sort_input(max(c["N"] // scale, 1), c["key_type"], c["dist"], seed, c["payload"], device)
+
+
+def elem_bytes(key_type: str, payload: bool) -> int:
+    return KEY_TYPES[key_type][2] + (4 if payload else 0)
