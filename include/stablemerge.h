@@ -1,0 +1,217 @@
+/*
+ * stablemerge.h -- C ABI of the B200 (sm_100a) stable parallel merge and
+ * stable merge sort of arXiv 1202.6575 (J. L. Traff, "A simple, stable
+ * parallel two-way merge").  Citations are PAPER.md line numbers
+ * and SURVEY.md §8 rows.
+ *
+ * Library: paper_1202_6575_b200/lib/libstablemerge.so (CUDA runtime linked
+ * statically).  No torch types appear here: keys and payloads are plain
+ * pointers, sizes are int64_t, the stream is a cudaStream_t passed as void*.
+ *
+ * ------------------------------------------------------------------------
+ * Problem (§2): A (n elements) and B (m elements) are
+ * non-decreasing under the key order; repeated keys are allowed.  C (n+m
+ * elements) receives the STABLE merge: keys non-decreasing, each input's
+ * order preserved, and every element of A placed before every equal-keyed
+ * element of B (L158-166, L354-357).  Equivalently A[i] lands at
+ * C[i + rank_low(A[i], B)] and B[j] at C[j + rank_high(B[j], A)].  The
+ * paper's "m <= n without loss of generality" (L66) is NOT required: any n, m
+ * (swapping would flip the tie rule).  Sentinels A[-1] = -inf, A[n] = +inf are
+ * virtual and never stored (L69-71).
+ *
+ * Key order: _u32 / _u64 compare unsigned, _i32 / _i64 compare signed
+ * (two's complement).  Payloads are uint32 and travel with their key.
+ *
+ * Memory: every pointer may be DEVICE memory (cudaMalloc / torch CUDA
+ * tensors / managed) or HOST memory (pinned or pageable).  With device
+ * pointers the call is fully asynchronous on `stream`.  If any key/payload
+ * pointer of a call is host memory, the library stages all of that call's
+ * buffers through device memory (cudaMemcpyAsync host->device, the kernels,
+ * device->host) on `stream`; host outputs are valid once `stream` has been
+ * synchronised (for pageable outputs the final copy is synchronous).
+ * Ownership: the caller owns every buffer; the library never frees or
+ * retains them past the stream point of the call.  Scratch (the two
+ * cross-rank arrays of p+1 entries, L373-375; the merge sort's auxiliary
+ * array of N keys + N payloads, §3) comes from
+ * cudaMallocAsync on `stream` and is freed stream-ordered.
+ *
+ * Errors (return value; no host synchronisation is done to detect them):
+ *   SM_OK       success (n = m = 0 / N <= 1: nothing launched)
+ *   SM_EINVAL   negative size; NULL key pointer with a nonzero size; payload
+ *               pointers not all set or all NULL; n + m (or N) > 2^31 - 1
+ *               (32-bit in-kernel indices); invalid options
+ *   SM_EALIAS   output overlaps an input (the merge is not in place)
+ *   SM_ENOMEM   scratch allocation failed
+ *   SM_ECUDA    a CUDA launch or copy failed (see sm_last_error())
+ * Unsorted inputs violate the precondition: the output is then unspecified
+ * (but every write stays inside C).
+ */
+#ifndef STABLEMERGE_H
+#define STABLEMERGE_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    SM_OK = 0,
+    SM_EINVAL = 1,
+    SM_EALIAS = 2,
+    SM_ENOMEM = 3,
+    SM_ECUDA = 4
+} sm_status;
+
+/* ---------------------------------------------------------------------
+ * merge_stable_<K>  -- SURVEY.md §8 rows a0-a7 (§2 Steps 1-4).
+ *
+ *   keys_A[n], vals_A[n]   A, non-decreasing keys (+ uint32 payload)
+ *   keys_B[m], vals_B[m]   B, non-decreasing keys (+ uint32 payload)
+ *   out_keys[n+m], out_vals[n+m]   C
+ *   vals_A, vals_B, out_vals: all three set, or all three NULL (keys only)
+ *   stream: cudaStream_t (NULL = legacy default stream)
+ *
+ * Device path: a cross-rank kernel computes xbar_i = rank_low(A[x_i], B) and
+ * ybar_j = rank_high(B[y_j], A) for the block starts x_i, y_j (L304-309);
+ * stream order is the paper's single synchronisation (L373-375); a task
+ * kernel then classifies each block start into cases (a)-(e) (L310-340) and
+ * copies or stably merges each disjoint subproblem into C[x_i + xbar_i ..]
+ * or C[y_j + ybar_j ..].  Block counts: p_A = ceil(n / T), p_B = ceil(m / T)
+ * with the tile-derived block size T (reading R7 of DESIGN.md).
+ * ------------------------------------------------------------------- */
+sm_status merge_stable_u32(const uint32_t *keys_A, const uint32_t *vals_A, int64_t n,
+                           const uint32_t *keys_B, const uint32_t *vals_B, int64_t m,
+                           uint32_t *out_keys, uint32_t *out_vals, void *stream);
+sm_status merge_stable_i32(const int32_t *keys_A, const uint32_t *vals_A, int64_t n,
+                           const int32_t *keys_B, const uint32_t *vals_B, int64_t m,
+                           int32_t *out_keys, uint32_t *out_vals, void *stream);
+sm_status merge_stable_i64(const int64_t *keys_A, const uint32_t *vals_A, int64_t n,
+                           const int64_t *keys_B, const uint32_t *vals_B, int64_t m,
+                           int64_t *out_keys, uint32_t *out_vals, void *stream);
+sm_status merge_stable_u64(const uint64_t *keys_A, const uint32_t *vals_A, int64_t n,
+                           const uint64_t *keys_B, const uint32_t *vals_B, int64_t m,
+                           uint64_t *out_keys, uint32_t *out_vals, void *stream);
+
+/* ---------------------------------------------------------------------
+ * mergesort_stable_<K>  -- SURVEY.md §8 rows a8-a9 (§3).
+ *
+ *   keys[N], vals[N] (vals may be NULL: keys only), sorted IN PLACE from the
+ *   caller's view; stable: equal keys keep their input order.
+ *
+ * Device path: runs of R consecutive elements are sorted stably inside one
+ * CTA each ("sorting sequentially in parallel p consecutive blocks", L406-407),
+ * then ceil(log2(N/R)) rounds merge run pairs (2k, 2k+1) with the left run
+ * playing A, every pair of a round in one segmented launch of the merge
+ * above ("modifying the merge algorithm to work in parallel on the
+ * ceil(p/2^i) pairs", L413-414); an odd trailing run is copied (L409-410).
+ * One auxiliary array (N keys + N payloads) is ping-ponged.
+ * ------------------------------------------------------------------- */
+sm_status mergesort_stable_u32(uint32_t *keys, uint32_t *vals, int64_t N, void *stream);
+sm_status mergesort_stable_i32(int32_t *keys, uint32_t *vals, int64_t N, void *stream);
+sm_status mergesort_stable_i64(int64_t *keys, uint32_t *vals, int64_t N, void *stream);
+sm_status mergesort_stable_u64(uint64_t *keys, uint32_t *vals, int64_t N, void *stream);
+
+/* ---------------------------------------------------------------------
+ * Test / tuning variants (not the contract).
+ *
+ * sm_options: zero fields mean "default".
+ *   p_A, p_B   explicit block counts (PAPER.md's single p: p_A = p_B = p).
+ *              Every task must then fit one tile:
+ *              ceil(n/p_A) + ceil(m/p_B) <= sm_tile_capacity(key bytes,
+ *              has_vals), else SM_EINVAL.
+ *   block      block size T (elements) when p_A/p_B are 0:
+ *              p_A = ceil(n/T), p_B = ceil(m/T); 2T <= tile capacity.
+ *   sort_run   merge sort initial run length R (0 = default; must equal
+ *              the block-sort tile of the key type, or be rejected)
+ *   flags      bit 0: disable programmatic dependent launch between the
+ *              cross-rank and task kernels.
+ * ------------------------------------------------------------------- */
+typedef struct {
+    int64_t p_A;
+    int64_t p_B;
+    int64_t block;
+    int64_t sort_run;
+    int64_t flags;
+} sm_options;
+
+#define SM_FLAG_NO_PDL 1
+
+sm_status merge_stable_ex_u32(const uint32_t *keys_A, const uint32_t *vals_A, int64_t n,
+                              const uint32_t *keys_B, const uint32_t *vals_B, int64_t m,
+                              uint32_t *out_keys, uint32_t *out_vals, void *stream,
+                              const sm_options *opt);
+sm_status merge_stable_ex_i32(const int32_t *keys_A, const uint32_t *vals_A, int64_t n,
+                              const int32_t *keys_B, const uint32_t *vals_B, int64_t m,
+                              int32_t *out_keys, uint32_t *out_vals, void *stream,
+                              const sm_options *opt);
+sm_status merge_stable_ex_i64(const int64_t *keys_A, const uint32_t *vals_A, int64_t n,
+                              const int64_t *keys_B, const uint32_t *vals_B, int64_t m,
+                              int64_t *out_keys, uint32_t *out_vals, void *stream,
+                              const sm_options *opt);
+sm_status merge_stable_ex_u64(const uint64_t *keys_A, const uint32_t *vals_A, int64_t n,
+                              const uint64_t *keys_B, const uint32_t *vals_B, int64_t m,
+                              uint64_t *out_keys, uint32_t *out_vals, void *stream,
+                              const sm_options *opt);
+
+/* merge_plan_ex_<K>: Steps 1-4 only, dumped for parity with the oracle's plan
+ * (Fig. 1, L73-117).  DEVICE pointers only (host -> SM_EINVAL).
+ *   p_A >= 1, p_B >= 1 (block counts; no tile limit here)
+ *   xbar[p_A+1]  int64: x̄_i = rank_low(A[x_i], B), x̄_{p_A} = m   (L304-306)
+ *   ybar[p_B+1]  int64: ȳ_j = rank_high(B[y_j], A), ȳ_{p_B} = n  (L307-309)
+ *   tasks[(p_A+p_B)*6] int64 rows (side 0=A/1=B, case 0..4 = (a)..(e),
+ *                a0, a1, b0, b1): A-side tasks 0..p_A-1, then B-side.
+ *                The output offset of a task is a0 + b0.                  */
+sm_status merge_plan_ex_u32(const uint32_t *keys_A, int64_t n, const uint32_t *keys_B, int64_t m,
+                            int64_t p_A, int64_t p_B, int64_t *xbar, int64_t *ybar, int64_t *tasks,
+                            void *stream);
+sm_status merge_plan_ex_i32(const int32_t *keys_A, int64_t n, const int32_t *keys_B, int64_t m,
+                            int64_t p_A, int64_t p_B, int64_t *xbar, int64_t *ybar, int64_t *tasks,
+                            void *stream);
+sm_status merge_plan_ex_i64(const int64_t *keys_A, int64_t n, const int64_t *keys_B, int64_t m,
+                            int64_t p_A, int64_t p_B, int64_t *xbar, int64_t *ybar, int64_t *tasks,
+                            void *stream);
+sm_status merge_plan_ex_u64(const uint64_t *keys_A, int64_t n, const uint64_t *keys_B, int64_t m,
+                            int64_t p_A, int64_t p_B, int64_t *xbar, int64_t *ybar, int64_t *tasks,
+                            void *stream);
+
+sm_status mergesort_stable_ex_u32(uint32_t *keys, uint32_t *vals, int64_t N, void *stream,
+                                  const sm_options *opt);
+sm_status mergesort_stable_ex_i32(int32_t *keys, uint32_t *vals, int64_t N, void *stream,
+                                  const sm_options *opt);
+sm_status mergesort_stable_ex_i64(int64_t *keys, uint32_t *vals, int64_t N, void *stream,
+                                  const sm_options *opt);
+sm_status mergesort_stable_ex_u64(uint64_t *keys, uint32_t *vals, int64_t N, void *stream,
+                                  const sm_options *opt);
+
+/* Largest task (elements) one CTA tile holds for this key width / payload
+ * mode: the default block size is T = capacity / 2 (the task bound
+ * ceil(n/p_A) + ceil(m/p_B) <= 2T). */
+int64_t sm_tile_capacity(int32_t key_bytes, int32_t has_vals);
+
+/* Initial run length R of the merge sort for this key width / payload mode. */
+int64_t sm_sort_run(int32_t key_bytes, int32_t has_vals);
+
+/* Human-readable text for a status, and the last CUDA error message seen by
+ * this library in the calling thread ("" if none). */
+const char *sm_status_string(sm_status s);
+const char *sm_last_error(void);
+
+/* Number of kernel launches the last call on this host thread issued. */
+int64_t sm_last_launch_count(void);
+
+/* Profiling (bench.py only).  While enabled, every kernel the library
+ * launches is bracketed by two CUDA events recorded on its launch stream
+ * (this also turns programmatic dependent launch off).  Enabling resets the
+ * record.  sm_profile_read synchronises the recorded events and returns the
+ * summed duration (ms) and launch count of one kernel kind:
+ * 0 = cross ranks (K1), 1 = tasks (K2: classify + copy/merge), 2 = block
+ * sort (K3).  Not thread-safe; process-wide. */
+void sm_profile_enable(int on);
+sm_status sm_profile_read(int kind, double *total_ms, int64_t *launches);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* STABLEMERGE_H */

@@ -1,0 +1,234 @@
+"""B200-native stable parallel merge and stable merge sort (arXiv 1202.6575).
+
+Thin Python binding over the C ABI in include/stablemerge.h
+(paper_1202_6575_b200/lib/libstablemerge.so): argument marshalling only.
+Every step of the path (cross ranks, classification, copy/merge, block sort,
+merge rounds) runs in the library's CUDA kernels.  There is no CPU fallback:
+importing this package fails loudly if the library is missing.
+
+    merge_stable(a_keys, a_vals, b_keys, b_vals, out_keys=None, out_vals=None)
+    mergesort_stable(keys, vals=None)
+    merge_plan(a_keys, b_keys, p_A, p_B)          # Steps 1-4 only (tests)
+
+Tensors may live on a CUDA device (asynchronous on the current stream) or on
+the host (the library stages them; the binding then synchronises the stream
+so host results are ready on return).  Unsigned keys: pass torch.uint32 /
+torch.uint64 tensors, or int32/int64 carriers with key_type="u32"/"u64".
+Payloads are 32-bit (int32 or uint32 tensors, same bits).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Optional
+
+import torch
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "lib", "libstablemerge.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"{LIB_PATH} is not built: run `python build_native.py` "
+                      "(there is no CPU fallback)")
+
+_lib = ctypes.CDLL(LIB_PATH)
+
+KEY_TYPES = ("u32", "i32", "i64", "u64")
+_CT = {"u32": ctypes.c_uint32, "i32": ctypes.c_int32, "i64": ctypes.c_int64, "u64": ctypes.c_uint64}
+_BYTES = {"u32": 4, "i32": 4, "i64": 8, "u64": 8}
+_DTYPE_KT = {torch.int32: "i32", torch.int64: "i64", torch.uint32: "u32", torch.uint64: "u64"}
+_CARRIER = {"u32": (torch.int32, torch.uint32), "i32": (torch.int32,), "i64": (torch.int64,),
+            "u64": (torch.int64, torch.uint64)}
+
+SM_OK, SM_EINVAL, SM_EALIAS, SM_ENOMEM, SM_ECUDA = range(5)
+SM_FLAG_NO_PDL = 1
+
+
+class SmOptions(ctypes.Structure):
+    _fields_ = [("p_A", ctypes.c_int64), ("p_B", ctypes.c_int64), ("block", ctypes.c_int64),
+                ("sort_run", ctypes.c_int64), ("flags", ctypes.c_int64)]
+
+
+_P, _I = ctypes.c_void_p, ctypes.c_int64
+for _kt in KEY_TYPES:
+    for _name, _args in ((f"merge_stable_{_kt}", [_P, _P, _I, _P, _P, _I, _P, _P, _P]),
+                         (f"merge_stable_ex_{_kt}", [_P, _P, _I, _P, _P, _I, _P, _P, _P, ctypes.POINTER(SmOptions)]),
+                         (f"merge_plan_ex_{_kt}", [_P, _I, _P, _I, _I, _I, _P, _P, _P, _P]),
+                         (f"mergesort_stable_{_kt}", [_P, _P, _I, _P]),
+                         (f"mergesort_stable_ex_{_kt}", [_P, _P, _I, _P, ctypes.POINTER(SmOptions)])):
+        _f = getattr(_lib, _name)
+        _f.argtypes = _args
+        _f.restype = ctypes.c_int
+_lib.sm_tile_capacity.argtypes = [ctypes.c_int32, ctypes.c_int32]
+_lib.sm_tile_capacity.restype = ctypes.c_int64
+_lib.sm_sort_run.argtypes = [ctypes.c_int32, ctypes.c_int32]
+_lib.sm_sort_run.restype = ctypes.c_int64
+_lib.sm_status_string.argtypes = [ctypes.c_int]
+_lib.sm_status_string.restype = ctypes.c_char_p
+_lib.sm_last_error.argtypes = []
+_lib.sm_last_error.restype = ctypes.c_char_p
+_lib.sm_last_launch_count.argtypes = []
+_lib.sm_last_launch_count.restype = ctypes.c_int64
+_lib.sm_profile_enable.argtypes = [ctypes.c_int]
+_lib.sm_profile_enable.restype = None
+_lib.sm_profile_read.argtypes = [ctypes.c_int, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int64)]
+_lib.sm_profile_read.restype = ctypes.c_int
+
+PROF_K1, PROF_K2, PROF_K3 = 0, 1, 2
+
+
+class StableMergeError(RuntimeError):
+    def __init__(self, status: int, fn: str):
+        self.status = status
+        msg = _lib.sm_status_string(status).decode()
+        detail = _lib.sm_last_error().decode()
+        super().__init__(f"{fn}: {msg}" + (f" ({detail})" if detail else ""))
+
+
+def _check(status: int, fn: str):
+    if status != SM_OK:
+        raise StableMergeError(status, fn)
+
+
+def _key_type(t: torch.Tensor, key_type: Optional[str]) -> str:
+    if key_type is None:
+        if t.dtype not in _DTYPE_KT:
+            raise TypeError(f"unsupported key dtype {t.dtype}")
+        return _DTYPE_KT[t.dtype]
+    if key_type not in KEY_TYPES:
+        raise ValueError(f"key_type must be one of {KEY_TYPES}")
+    if t.dtype not in _CARRIER[key_type]:
+        raise TypeError(f"key_type {key_type} cannot be carried in {t.dtype}")
+    return key_type
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    if t is None:
+        return None
+    if not t.is_contiguous():
+        raise ValueError("tensors must be contiguous")
+    return t.data_ptr() or None
+
+
+def _vals_ok(t: Optional[torch.Tensor]):
+    if t is not None and t.dtype not in (torch.int32, torch.uint32):
+        raise TypeError("payloads must be 32-bit (int32 / uint32)")
+
+
+def _stream_for(t: torch.Tensor, stream):
+    if stream is not None:
+        return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+    if t.is_cuda:
+        return torch.cuda.current_stream(t.device).cuda_stream
+    return 0
+
+
+def _sync_if_host(t: torch.Tensor, stream_handle):
+    if not t.is_cuda:
+        torch.cuda.synchronize() if stream_handle == 0 else \
+            torch.cuda.ExternalStream(stream_handle).synchronize()
+
+
+def tile_capacity(key_type: str = "u32", has_vals: bool = True) -> int:
+    return int(_lib.sm_tile_capacity(_BYTES[key_type], int(has_vals)))
+
+
+def sort_run(key_type: str = "u32", has_vals: bool = True) -> int:
+    return int(_lib.sm_sort_run(_BYTES[key_type], int(has_vals)))
+
+
+def last_launch_count() -> int:
+    """Kernel launches issued by the last library call on this thread."""
+    return int(_lib.sm_last_launch_count())
+
+
+def profile_enable(on: bool = True):
+    """Bracket every library kernel launch with CUDA events on its stream."""
+    _lib.sm_profile_enable(int(on))
+
+
+def profile_read(kind: int):
+    """(total ms, launches) of one kernel kind since profile_enable()."""
+    t = ctypes.c_double(0.0)
+    c = ctypes.c_int64(0)
+    _check(_lib.sm_profile_read(kind, ctypes.byref(t), ctypes.byref(c)), "sm_profile_read")
+    return t.value, c.value
+
+
+def _options(p_A, p_B, block, flags, sort_run_=None):
+    if p_A is None and p_B is None and block is None and not flags and sort_run_ is None:
+        return None
+    return SmOptions(p_A or 0, p_B or 0, block or 0, sort_run_ or 0, flags or 0)
+
+
+def merge_stable(a_keys: torch.Tensor, a_vals: Optional[torch.Tensor], b_keys: torch.Tensor,
+                 b_vals: Optional[torch.Tensor], out_keys: Optional[torch.Tensor] = None,
+                 out_vals: Optional[torch.Tensor] = None, *, key_type: Optional[str] = None, stream=None,
+                 p_A: Optional[int] = None, p_B: Optional[int] = None, block: Optional[int] = None,
+                 pdl: bool = True):
+    """Stable merge of sorted A and B (ties: A first).  Returns (keys, vals)."""
+    kt = _key_type(a_keys, key_type)
+    _key_type(b_keys, kt)
+    if (a_vals is None) != (b_vals is None):
+        raise ValueError("payloads must be given for both inputs or neither")
+    _vals_ok(a_vals); _vals_ok(b_vals)
+    n, m = a_keys.numel(), b_keys.numel()
+    if out_keys is None:
+        out_keys = torch.empty(n + m, dtype=a_keys.dtype, device=a_keys.device)
+    if a_vals is not None and out_vals is None:
+        out_vals = torch.empty(n + m, dtype=a_vals.dtype, device=a_keys.device)
+    if out_keys.numel() != n + m or (out_vals is not None and out_vals.numel() != n + m):
+        raise ValueError("output length must be n + m")
+    s = _stream_for(a_keys, stream)
+    opt = _options(p_A, p_B, block, 0 if pdl else SM_FLAG_NO_PDL)
+    args = (_ptr(a_keys), _ptr(a_vals), n, _ptr(b_keys), _ptr(b_vals), m, _ptr(out_keys), _ptr(out_vals), s)
+    if opt is None:
+        _check(getattr(_lib, f"merge_stable_{kt}")(*args), f"merge_stable_{kt}")
+    else:
+        _check(getattr(_lib, f"merge_stable_ex_{kt}")(*args, ctypes.byref(opt)), f"merge_stable_ex_{kt}")
+    _sync_if_host(out_keys, s)
+    return out_keys, out_vals
+
+
+def mergesort_stable(keys: torch.Tensor, vals: Optional[torch.Tensor] = None, *, key_type: Optional[str] = None,
+                     stream=None, pdl: bool = True):
+    """Stable merge sort in place (equal keys keep input order).  Returns (keys, vals)."""
+    kt = _key_type(keys, key_type)
+    _vals_ok(vals)
+    N = keys.numel()
+    if vals is not None and vals.numel() != N:
+        raise ValueError("vals must have the same length as keys")
+    s = _stream_for(keys, stream)
+    args = (_ptr(keys), _ptr(vals), N, s)
+    if pdl:
+        _check(getattr(_lib, f"mergesort_stable_{kt}")(*args), f"mergesort_stable_{kt}")
+    else:
+        opt = SmOptions(0, 0, 0, 0, SM_FLAG_NO_PDL)
+        _check(getattr(_lib, f"mergesort_stable_ex_{kt}")(*args, ctypes.byref(opt)), f"mergesort_stable_ex_{kt}")
+    _sync_if_host(keys, s)
+    return keys, vals
+
+
+def merge_plan(a_keys: torch.Tensor, b_keys: torch.Tensor, p_A: int, p_B: Optional[int] = None, *,
+               key_type: Optional[str] = None, stream=None):
+    """Steps 1-4 on the device: (xbar[p_A+1], ybar[p_B+1], tasks[p_A+p_B, 6]) int64 tensors."""
+    kt = _key_type(a_keys, key_type)
+    _key_type(b_keys, kt)
+    if p_B is None:
+        p_B = p_A
+    dev = a_keys.device
+    if not a_keys.is_cuda:
+        raise ValueError("merge_plan takes CUDA tensors")
+    xbar = torch.empty(p_A + 1, dtype=torch.int64, device=dev)
+    ybar = torch.empty(p_B + 1, dtype=torch.int64, device=dev)
+    tasks = torch.empty((p_A + p_B, 6), dtype=torch.int64, device=dev)
+    s = _stream_for(a_keys, stream)
+    _check(getattr(_lib, f"merge_plan_ex_{kt}")(_ptr(a_keys), a_keys.numel(), _ptr(b_keys), b_keys.numel(),
+                                                 p_A, p_B, _ptr(xbar), _ptr(ybar), _ptr(tasks), s),
+           f"merge_plan_ex_{kt}")
+    return xbar, ybar, tasks
+
+
+__all__ = ["merge_stable", "mergesort_stable", "merge_plan", "tile_capacity", "sort_run", "last_launch_count",
+           "StableMergeError", "KEY_TYPES", "LIB_PATH", "profile_enable", "profile_read", "PROF_K1", "PROF_K2",
+           "PROF_K3"]

@@ -1,0 +1,170 @@
+// sm_device.cuh -- device primitives of the B200 stable merge (arXiv 1202.6575).
+//
+// Citations: PAPER.md line numbers.  This file is
+// the CUDA side only; it shares nothing with oracle/.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace sm {
+
+// ---------------------------------------------------------------------------
+// Row a0: block partition.
+//   x_i = i*ceil(len/p)            for i <  r = len mod p
+//       = i*floor(len/p) + r       otherwise;      x_p = len
+//   block_of(k) = floor(k / ceil(len/p))                 if k < r*ceil(len/p)
+//               = floor((k - r*ceil(len/p)) / floor(len/p)) + r   otherwise
+//   block_of(len) = p  (reading R3: the virtual block after the last one)
+// ---------------------------------------------------------------------------
+struct Blocks {
+    int len, p, q, r;   // q = floor(len/p), r = len mod p
+    __device__ __forceinline__ Blocks(int len_, int p_) : len(len_), p(p_), q(len_ / p_), r(len_ % p_) {}
+    __device__ __forceinline__ int start(int i) const { return i < r ? i * (q + 1) : i * q + r; }
+    __device__ __forceinline__ int of(int k) const {
+        if (k >= len) return p;
+        const int big = r * (q + 1);
+        return k < big ? k / (q + 1) : (k - big) / q + r;   // q > 0 whenever k >= big and k < len
+    }
+};
+
+// ---------------------------------------------------------------------------
+// Rows a1/a2: rank_low(x, X) = #{X[t] < x}, rank_high(x, X) = #{X[t] <= x}
+// (virtual sentinels are the search bounds, L69-71).
+// Branch-free halving search: the probe index is a select, not a branch.
+// ---------------------------------------------------------------------------
+template <typename K>
+__device__ __forceinline__ int rank_low_dev(const K* __restrict__ X, int len, K x) {
+    int lo = 0;
+    while (len > 0) {
+        const int half = len >> 1;
+        const bool right = __ldg(X + lo + half) < x;
+        lo = right ? lo + half + 1 : lo;
+        len = right ? len - half - 1 : half;
+    }
+    return lo;
+}
+
+template <typename K>
+__device__ __forceinline__ int rank_high_dev(const K* __restrict__ X, int len, K x) {
+    int lo = 0;
+    while (len > 0) {
+        const int half = len >> 1;
+        const bool right = __ldg(X + lo + half) <= x;
+        lo = right ? lo + half + 1 : lo;
+        len = right ? len - half - 1 : half;
+    }
+    return lo;
+}
+
+// ---------------------------------------------------------------------------
+// Geometry of one launch: either one merge (S = 1, arrays A and B), or one
+// merge-sort round over S run pairs of a single array (§3:
+// "modifying the merge algorithm to work in parallel on the pairs").
+// Segment s of a sort round: A = runs [2sL, 2sL+L), B = [2sL+L, 2sL+2L),
+// clipped to N; the left run plays A so ties keep input order.  A pair whose
+// B is empty (odd trailing run) degenerates to case-(a) copies (L409-410).
+// ---------------------------------------------------------------------------
+struct Geom {
+    int S;        // segments
+    int pA, pB;   // block counts per segment
+    int n, m;     // plain merge sizes (sort == 0)
+    int L, N;     // sort round: run length, total length (sort == 1)
+    int sort;
+};
+
+struct Seg {
+    int aoff, n, boff, m, coff;
+};
+
+__device__ __forceinline__ Seg segment(const Geom& g, int s) {
+    Seg r;
+    if (!g.sort) {
+        r.aoff = 0; r.n = g.n; r.boff = 0; r.m = g.m; r.coff = 0;
+    } else {
+        r.aoff = s * 2 * g.L;                       // < N < 2^31 for s < S
+        r.n = min(g.L, g.N - r.aoff);
+        r.boff = r.aoff + r.n;
+        r.m = max(0, min(g.L, g.N - r.boff));
+        r.coff = r.aoff;
+    }
+    return r;
+}
+
+// ---------------------------------------------------------------------------
+// Rows a4/a5: classification of the PE at x_i (Step 3, L310-336) and at y_j
+// (Step 4, L337-340).  Cases tested in the order (a), (e), (b), (d), (c)
+// (reading R8); (d) takes A up to x_{i+1} (reading R1, the text's "x_{j+1}"
+// is a typo).  Output offset is always a0 + b0 (x_i + xbar_i, y_j + ybar_j).
+// ---------------------------------------------------------------------------
+enum { CASE_A = 0, CASE_B = 1, CASE_C = 2, CASE_D = 3, CASE_E = 4 };
+
+struct Task {
+    int side, kase, a0, a1, b0, b1;
+};
+
+__device__ __forceinline__ Task classify_a_side(int i, const Blocks& xa, const Blocks& yb,
+                                                const int* __restrict__ xbar, const int* __restrict__ ybar) {
+    Task t;
+    t.side = 0;
+    const int xi = xa.start(i), xi1 = xa.start(i + 1);
+    const int xb0 = xbar[i], xb1 = xbar[i + 1];
+    if (xb0 == xb1) {                                         // (a) copy A[x_i, x_{i+1})
+        t.kase = CASE_A; t.a0 = xi; t.a1 = xi1; t.b0 = t.b1 = xb0; return t;
+    }
+    const int j = yb.of(xb0);
+    const int yj = yb.start(j);
+    if (xb0 == yj) {                                          // (e) copy A[x_i, ybar_j)
+        t.kase = CASE_E; t.a0 = xi; t.a1 = ybar[j]; t.b0 = t.b1 = xb0; return t;
+    }
+    if (yb.of(xb1) == j) {                                    // (b) A block with B[xbar_i, xbar_{i+1})
+        t.kase = CASE_B; t.a0 = xi; t.a1 = xi1; t.b0 = xb0; t.b1 = xb1; return t;
+    }
+    const int yj1 = yb.start(j + 1);
+    if (xb1 == yj1) {                                         // (d) A block with B[xbar_i, y_{j+1})
+        t.kase = CASE_D; t.a0 = xi; t.a1 = xi1; t.b0 = xb0; t.b1 = yj1; return t;
+    }
+    t.kase = CASE_C;                                          // (c) A[x_i, ybar_{j+1}) with B[xbar_i, y_{j+1})
+    t.a0 = xi; t.a1 = ybar[j + 1]; t.b0 = xb0; t.b1 = yj1;
+    return t;
+}
+
+__device__ __forceinline__ Task classify_b_side(int j, const Blocks& xa, const Blocks& yb,
+                                                const int* __restrict__ xbar, const int* __restrict__ ybar) {
+    Task t;
+    t.side = 1;
+    const int yj = yb.start(j), yj1 = yb.start(j + 1);
+    const int yb0 = ybar[j], yb1 = ybar[j + 1];
+    if (yb0 == yb1) {                                         // (a) copy B[y_j, y_{j+1})
+        t.kase = CASE_A; t.b0 = yj; t.b1 = yj1; t.a0 = t.a1 = yb0; return t;
+    }
+    const int i = xa.of(yb0);
+    const int xi = xa.start(i);
+    if (yb0 == xi) {                                          // (e) copy B[y_j, xbar_i)
+        t.kase = CASE_E; t.b0 = yj; t.b1 = xbar[i]; t.a0 = t.a1 = yb0; return t;
+    }
+    if (xa.of(yb1) == i) {                                    // (b) B block with A[ybar_j, ybar_{j+1})
+        t.kase = CASE_B; t.b0 = yj; t.b1 = yj1; t.a0 = yb0; t.a1 = yb1; return t;
+    }
+    const int xi1 = xa.start(i + 1);
+    if (yb1 == xi1) {                                         // (d) B block with A[ybar_j, x_{i+1})
+        t.kase = CASE_D; t.b0 = yj; t.b1 = yj1; t.a0 = yb0; t.a1 = xi1; return t;
+    }
+    t.kase = CASE_C;                                          // (c) B[y_j, xbar_{i+1}) with A[ybar_j, x_{i+1})
+    t.b0 = yj; t.b1 = xbar[i + 1]; t.a0 = yb0; t.a1 = xi1;
+    return t;
+}
+
+// ---------------------------------------------------------------------------
+// Streaming cache hints: inputs are read once, outputs written once.
+// ---------------------------------------------------------------------------
+template <typename T>
+__device__ __forceinline__ T ld_stream(const T* p) { return __ldcs(p); }
+template <typename T>
+__device__ __forceinline__ void st_stream(T* p, T v) { __stcs(p, v); }
+
+// Programmatic dependent launch (sm_90+): wait for the producer grid's
+// memory to be visible; a no-op when the launch was not programmatic.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;"); }
+
+}  // namespace sm

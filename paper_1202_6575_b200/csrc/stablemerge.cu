@@ -1,0 +1,474 @@
+// stablemerge.cu -- host drivers and the C ABI (include/stablemerge.h) of the
+// B200 stable parallel merge / merge sort of arXiv 1202.6575.
+//
+// Call sequence of merge_stable:
+//   validate -> choose p_A, p_B -> cudaMallocAsync the two rank arrays ->
+//   K1 (cross ranks) -> [single synchronisation: stream order / PDL] ->
+//   K2 (classify + copy/merge every task) -> cudaFreeAsync.  No host sync.
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <vector>
+#include <climits>
+
+#include "stablemerge.h"
+#include "sm_kernels.cuh"
+
+namespace sm {
+
+thread_local char g_err[512] = "";
+thread_local int64_t g_launches = 0;
+
+// Tile shape of K2 and K3.  VT odd keeps the register <-> shared-memory
+// transposition free of bank conflicts for 4- and 8-byte keys.
+constexpr int NT = 128;
+constexpr int VT = 15;
+constexpr int NV = NT * VT;       // tile capacity: largest task / sort run
+constexpr int T_DEFAULT = NV / 2; // block size: task bound 2T (L388-393)
+
+static sm_status fail_cuda(cudaError_t e, const char* what) {
+    snprintf(g_err, sizeof(g_err), "%s: %s", what, cudaGetErrorString(e));
+    return SM_ECUDA;
+}
+
+static sm_status fail_inval(const char* what) {
+    snprintf(g_err, sizeof(g_err), "invalid argument: %s", what);
+    return SM_EINVAL;
+}
+
+// ------------------------------------------------------------ profiling
+// While enabled, every kernel launch is bracketed by two CUDA events on its
+// own stream; sm_profile_read() sums the durations per kernel kind.
+enum { PROF_K1 = 0, PROF_K2 = 1, PROF_K3 = 2, PROF_KINDS = 3 };
+struct ProfRec {
+    cudaEvent_t a, b;
+    int kind;
+};
+static bool g_prof_on = false;
+static std::vector<ProfRec> g_prof_pool;
+static size_t g_prof_used = 0;
+
+static void prof_before(int kind, cudaStream_t st) {
+    if (!g_prof_on) return;
+    if (g_prof_used == g_prof_pool.size()) {
+        ProfRec r;
+        cudaEventCreate(&r.a);
+        cudaEventCreate(&r.b);
+        g_prof_pool.push_back(r);
+    }
+    g_prof_pool[g_prof_used].kind = kind;
+    cudaEventRecord(g_prof_pool[g_prof_used].a, st);
+}
+
+static void prof_after(cudaStream_t st) {
+    if (!g_prof_on) return;
+    cudaEventRecord(g_prof_pool[g_prof_used].b, st);
+    ++g_prof_used;
+}
+
+static sm_status check_launch(const char* what) {
+    ++g_launches;
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? SM_OK : fail_cuda(e, what);
+}
+
+static inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// The default memory pool keeps freed blocks (no release at every sync), so
+// the per-call rank arrays cost no cudaMalloc after the first call.
+static void keep_pool(cudaStream_t) {
+    static bool done = false;
+    if (done) return;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t thr = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    cudaGetLastError();
+    done = true;
+}
+
+template <typename T>
+static sm_status dalloc(T** p, int64_t count, cudaStream_t st) {
+    *p = nullptr;
+    if (count <= 0) return SM_OK;
+    cudaError_t e = cudaMallocAsync((void**)p, (size_t)count * sizeof(T), st);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        snprintf(g_err, sizeof(g_err), "cudaMallocAsync(%lld bytes): %s", (long long)(count * sizeof(T)),
+                 cudaGetErrorString(e));
+        return SM_ENOMEM;
+    }
+    return SM_OK;
+}
+
+static void dfree(void* p, cudaStream_t st) {
+    if (p) cudaFreeAsync(p, st);
+}
+
+// ------------------------------------------------------------ launches
+template <typename K, bool HAS_V>
+static sm_status launch_merge(const K* A, const uint32_t* vA, const K* B, const uint32_t* vB, K* C,
+                              uint32_t* vC, const Geom& g, int* xbar, int* ybar, cudaStream_t st, bool pdl) {
+    const long long items = (long long)g.S * (g.pA + g.pB + 2);
+    const long long blocks1 = (items + 255) / 256;
+    prof_before(PROF_K1, st);
+    k_cross_ranks<K><<<(unsigned)blocks1, 256, 0, st>>>(A, B, g, xbar, ybar);
+    prof_after(st);
+    sm_status s = check_launch("k_cross_ranks");
+    if (s != SM_OK) return s;
+
+    cudaLaunchConfig_t cfg;
+    memset(&cfg, 0, sizeof(cfg));
+    cfg.gridDim = dim3((unsigned)((long long)g.S * (g.pA + g.pB)));
+    cfg.blockDim = dim3(NT);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = (pdl && !g_prof_on) ? 1 : 0;
+    prof_before(PROF_K2, st);
+    cudaError_t e = cudaLaunchKernelEx(&cfg, k_tasks<K, HAS_V, NT, VT>, A, vA, B, vB, C, vC, g,
+                                       (const int*)xbar, (const int*)ybar);
+    prof_after(st);
+    ++g_launches;
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return fail_cuda(e, "k_tasks");
+    }
+    return SM_OK;
+}
+
+// ------------------------------------------------ host-memory staging
+static bool is_host_ptr(const void* p) {
+    if (!p) return false;
+    cudaPointerAttributes a;
+    cudaError_t e = cudaPointerGetAttributes(&a, p);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return true;
+    }
+    return a.type == cudaMemoryTypeHost || a.type == cudaMemoryTypeUnregistered;
+}
+
+// One staged buffer: a device copy of a host range (in and/or out).
+struct Stage {
+    void* host = nullptr;
+    void* dev = nullptr;
+    size_t bytes = 0;
+    bool out = false;
+};
+
+static sm_status stage_in(Stage& s, const void* host, size_t bytes, bool is_out, bool copy_in, cudaStream_t st) {
+    s.host = (void*)host;
+    s.bytes = bytes;
+    s.out = is_out;
+    if (!host || bytes == 0) return SM_OK;
+    sm_status r = dalloc((char**)&s.dev, (int64_t)bytes, st);
+    if (r != SM_OK) return r;
+    if (copy_in) {
+        cudaError_t e = cudaMemcpyAsync(s.dev, host, bytes, cudaMemcpyHostToDevice, st);
+        if (e != cudaSuccess) return fail_cuda(e, "cudaMemcpyAsync H2D");
+    }
+    return SM_OK;
+}
+
+static sm_status stage_out(Stage& s, cudaStream_t st) {
+    if (!s.dev) return SM_OK;
+    sm_status r = SM_OK;
+    if (s.out) {
+        cudaError_t e = cudaMemcpyAsync(s.host, s.dev, s.bytes, cudaMemcpyDeviceToHost, st);
+        if (e != cudaSuccess) r = fail_cuda(e, "cudaMemcpyAsync D2H");
+    }
+    dfree(s.dev, st);
+    s.dev = nullptr;
+    return r;
+}
+
+static bool overlaps(const void* p, size_t pb, const void* q, size_t qb) {
+    if (!p || !q || pb == 0 || qb == 0) return false;
+    const char *a = (const char*)p, *b = (const char*)q;
+    return a < b + qb && b < a + pb;
+}
+
+// ------------------------------------------------------------ merge
+template <typename K>
+static sm_status merge_device(const K* A, const uint32_t* vA, int64_t n, const K* B, const uint32_t* vB, int64_t m,
+                              K* C, uint32_t* vC, cudaStream_t st, int64_t pA, int64_t pB, bool pdl) {
+    Geom g;
+    g.S = 1; g.pA = (int)pA; g.pB = (int)pB; g.n = (int)n; g.m = (int)m; g.L = 0; g.N = 0; g.sort = 0;
+    int* ranks = nullptr;
+    sm_status s = dalloc(&ranks, (pA + 1) + (pB + 1), st);
+    if (s != SM_OK) return s;
+    if (vC) s = launch_merge<K, true>(A, vA, B, vB, C, vC, g, ranks, ranks + pA + 1, st, pdl);
+    else s = launch_merge<K, false>(A, nullptr, B, nullptr, C, nullptr, g, ranks, ranks + pA + 1, st, pdl);
+    dfree(ranks, st);
+    return s;
+}
+
+template <typename K>
+static sm_status merge_entry(const K* A, const uint32_t* vA, int64_t n, const K* B, const uint32_t* vB, int64_t m,
+                             K* C, uint32_t* vC, void* stream, const sm_options* opt) {
+    g_launches = 0;
+    g_err[0] = 0;
+    cudaStream_t st = (cudaStream_t)stream;
+    if (n < 0 || m < 0) return fail_inval("negative size");
+    if ((n && !A) || (m && !B) || ((n + m) && !C)) return fail_inval("NULL key pointer with nonzero size");
+    if (vC) {
+        if ((n && !vA) || (m && !vB)) return fail_inval("payload pointers must be all set or all NULL");
+    } else if (vA || vB) {
+        return fail_inval("payload pointers must be all set or all NULL");
+    }
+    if (n + m > (int64_t)INT_MAX) return fail_inval("n + m > 2^31 - 1");
+    const size_t kb = sizeof(K);
+    const size_t cb = (size_t)(n + m);
+    if (overlaps(C, cb * kb, A, n * kb) || overlaps(C, cb * kb, B, m * kb) || overlaps(C, cb * kb, vA, n * 4) ||
+        overlaps(C, cb * kb, vB, m * 4) || overlaps(vC, cb * 4, A, n * kb) || overlaps(vC, cb * 4, B, m * kb) ||
+        overlaps(vC, cb * 4, vA, n * 4) || overlaps(vC, cb * 4, vB, m * 4) || overlaps(C, cb * kb, vC, cb * 4))
+        return SM_EALIAS;
+
+    int64_t pA, pB;
+    if (opt && (opt->p_A || opt->p_B)) {
+        if (opt->p_A < 1 || opt->p_B < 1) return fail_inval("p_A and p_B must both be >= 1");
+        pA = opt->p_A; pB = opt->p_B;
+        if (pA > INT_MAX / 2 || pB > INT_MAX / 2) return fail_inval("p too large");
+        if (ceil_div(n, pA) + ceil_div(m, pB) > NV) return fail_inval("task bound ceil(n/p_A)+ceil(m/p_B) exceeds the tile");
+    } else {
+        int64_t T = (opt && opt->block) ? opt->block : T_DEFAULT;
+        if (T < 1 || 2 * T > NV) return fail_inval("block size T must satisfy 1 <= 2T <= tile capacity");
+        pA = std::max<int64_t>(1, ceil_div(n, T));
+        pB = std::max<int64_t>(1, ceil_div(m, T));
+    }
+    const bool pdl = !(opt && (opt->flags & SM_FLAG_NO_PDL));
+    if (n + m == 0) return SM_OK;
+    keep_pool(st);
+
+    const bool host = is_host_ptr(A) || is_host_ptr(B) || is_host_ptr(vA) || is_host_ptr(vB) || is_host_ptr(C) ||
+                      is_host_ptr(vC);
+    if (!host) return merge_device<K>(A, vA, n, B, vB, m, C, vC, st, pA, pB, pdl);
+
+    // Host buffers: stage every buffer of the call through device memory.
+    Stage sA, sB, svA, svB, sC, svC;
+    sm_status s = SM_OK;
+    if (s == SM_OK) s = stage_in(sA, A, n * kb, false, true, st);
+    if (s == SM_OK) s = stage_in(sB, B, m * kb, false, true, st);
+    if (s == SM_OK && vC) s = stage_in(svA, vA, n * 4, false, true, st);
+    if (s == SM_OK && vC) s = stage_in(svB, vB, m * 4, false, true, st);
+    if (s == SM_OK) s = stage_in(sC, C, cb * kb, true, false, st);
+    if (s == SM_OK && vC) s = stage_in(svC, vC, cb * 4, true, false, st);
+    if (s == SM_OK)
+        s = merge_device<K>((const K*)sA.dev, (const uint32_t*)svA.dev, n, (const K*)sB.dev,
+                            (const uint32_t*)svB.dev, m, (K*)sC.dev, (uint32_t*)svC.dev, st, pA, pB, pdl);
+    sm_status s2 = SM_OK;
+    for (Stage* x : {&sC, &svC, &sA, &sB, &svA, &svB}) {
+        if (s != SM_OK) x->out = false;
+        sm_status r = stage_out(*x, st);
+        if (s2 == SM_OK) s2 = r;
+    }
+    return s != SM_OK ? s : s2;
+}
+
+// ------------------------------------------------------------ plan dump
+__global__ void k_widen(const int* __restrict__ in, int64_t* __restrict__ out, int count) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < count) out[i] = in[i];
+}
+
+template <typename K>
+static sm_status plan_entry(const K* A, int64_t n, const K* B, int64_t m, int64_t pA, int64_t pB, int64_t* xbar,
+                            int64_t* ybar, int64_t* tasks, void* stream) {
+    g_launches = 0;
+    g_err[0] = 0;
+    cudaStream_t st = (cudaStream_t)stream;
+    if (n < 0 || m < 0 || pA < 1 || pB < 1) return fail_inval("sizes / block counts");
+    if ((n && !A) || (m && !B) || !xbar || !ybar || !tasks) return fail_inval("NULL pointer");
+    if (n + m > (int64_t)INT_MAX || pA > INT_MAX / 4 || pB > INT_MAX / 4) return fail_inval("too large");
+    if (is_host_ptr(A) || is_host_ptr(B) || is_host_ptr(xbar) || is_host_ptr(ybar) || is_host_ptr(tasks))
+        return fail_inval("merge_plan_ex takes device pointers only");
+    keep_pool(st);
+    Geom g;
+    g.S = 1; g.pA = (int)pA; g.pB = (int)pB; g.n = (int)n; g.m = (int)m; g.L = 0; g.N = 0; g.sort = 0;
+    int* ranks = nullptr;
+    sm_status s = dalloc(&ranks, (pA + 1) + (pB + 1), st);
+    if (s != SM_OK) return s;
+    const long long items = pA + pB + 2;
+    k_cross_ranks<K><<<(unsigned)((items + 255) / 256), 256, 0, st>>>(A, B, g, ranks, ranks + pA + 1);
+    s = check_launch("k_cross_ranks");
+    if (s == SM_OK) {
+        k_widen<<<(unsigned)((pA + 1 + 255) / 256), 256, 0, st>>>(ranks, xbar, (int)(pA + 1));
+        s = check_launch("k_widen");
+    }
+    if (s == SM_OK) {
+        k_widen<<<(unsigned)((pB + 1 + 255) / 256), 256, 0, st>>>(ranks + pA + 1, ybar, (int)(pB + 1));
+        s = check_launch("k_widen");
+    }
+    if (s == SM_OK) {
+        k_plan_dump<K><<<(unsigned)((pA + pB + 127) / 128), 128, 0, st>>>(g, ranks, ranks + pA + 1, tasks);
+        s = check_launch("k_plan_dump");
+    }
+    dfree(ranks, st);
+    return s;
+}
+
+// ------------------------------------------------------------ merge sort
+template <typename K>
+static sm_status sort_device(K* keys, uint32_t* vals, int64_t N, cudaStream_t st, bool pdl) {
+    const int R = NV;   // initial run length: one K3 tile
+    int rounds = 0;
+    for (int64_t L = R; L < N; L *= 2) ++rounds;
+    K* aux = nullptr;
+    uint32_t* vaux = nullptr;
+    int* ranks = nullptr;
+    sm_status s = dalloc(&aux, N, st);
+    if (s == SM_OK && vals) s = dalloc(&vaux, N, st);
+    // rank arrays for the largest round: S*(pA+1) + S*(pB+1) <= 2*(N/T + 2*S) entries
+    if (s == SM_OK) s = dalloc(&ranks, 2 * (ceil_div(N, T_DEFAULT) + 2 * ceil_div(N, R) + 2), st);
+    if (s == SM_OK) {
+        // phase 1 lands in the buffer from which an even number of rounds
+        // ends in the caller's array (in place when rounds is even)
+        K* dst = (rounds % 2 == 0) ? keys : aux;
+        uint32_t* vdst = (rounds % 2 == 0) ? vals : vaux;
+        const unsigned blocks = (unsigned)ceil_div(N, R);
+        prof_before(PROF_K3, st);
+        if (vals) k_block_sort<K, true, NT, VT><<<blocks, NT, 0, st>>>(keys, vals, dst, vdst, (int)N);
+        else k_block_sort<K, false, NT, VT><<<blocks, NT, 0, st>>>(keys, nullptr, dst, nullptr, (int)N);
+        prof_after(st);
+        s = check_launch("k_block_sort");
+        K* src = dst;
+        uint32_t* vsrc = vdst;
+        for (int64_t L = R; s == SM_OK && L < N; L *= 2) {
+            K* d2 = (src == keys) ? aux : keys;
+            uint32_t* vd2 = (src == keys) ? vaux : vals;
+            Geom g;
+            g.S = (int)ceil_div(N, 2 * L);
+            g.pA = g.pB = (int)ceil_div(L, T_DEFAULT);
+            g.n = g.m = 0; g.L = (int)L; g.N = (int)N; g.sort = 1;
+            int* xbar = ranks;
+            int* ybar = ranks + (int64_t)g.S * (g.pA + 1);
+            if (vals) s = launch_merge<K, true>(src, vsrc, src, vsrc, d2, vd2, g, xbar, ybar, st, pdl);
+            else s = launch_merge<K, false>(src, nullptr, src, nullptr, d2, nullptr, g, xbar, ybar, st, pdl);
+            src = d2;
+            vsrc = vd2;
+        }
+    }
+    dfree(ranks, st);
+    dfree(vaux, st);
+    dfree(aux, st);
+    return s;
+}
+
+template <typename K>
+static sm_status sort_entry(K* keys, uint32_t* vals, int64_t N, void* stream, const sm_options* opt) {
+    g_launches = 0;
+    g_err[0] = 0;
+    cudaStream_t st = (cudaStream_t)stream;
+    if (N < 0) return fail_inval("negative size");
+    if (N && !keys) return fail_inval("NULL key pointer with nonzero size");
+    if (N > (int64_t)INT_MAX) return fail_inval("N > 2^31 - 1");
+    if (opt && opt->sort_run && opt->sort_run != NV) return fail_inval("sort_run must equal the block-sort tile");
+    if (overlaps(keys, N * sizeof(K), vals, N * 4)) return SM_EALIAS;
+    const bool pdl = !(opt && (opt->flags & SM_FLAG_NO_PDL));
+    if (N <= 1) return SM_OK;
+    keep_pool(st);
+    if (!is_host_ptr(keys) && !is_host_ptr(vals)) return sort_device<K>(keys, vals, N, st, pdl);
+    Stage sk, sv;
+    sm_status s = stage_in(sk, keys, N * sizeof(K), true, true, st);
+    if (s == SM_OK && vals) s = stage_in(sv, vals, N * 4, true, true, st);
+    if (s == SM_OK) s = sort_device<K>((K*)sk.dev, (uint32_t*)sv.dev, N, st, pdl);
+    if (s != SM_OK) { sk.out = false; sv.out = false; }
+    sm_status r1 = stage_out(sk, st), r2 = stage_out(sv, st);
+    return s != SM_OK ? s : (r1 != SM_OK ? r1 : r2);
+}
+
+}  // namespace sm
+
+// ================================================================ C ABI
+extern "C" {
+
+#define SM_DEFINE_ABI(SUF, K)                                                                                   \
+    sm_status merge_stable_##SUF(const K* keys_A, const uint32_t* vals_A, int64_t n, const K* keys_B,          \
+                                 const uint32_t* vals_B, int64_t m, K* out_keys, uint32_t* out_vals,          \
+                                 void* stream) {                                                               \
+        return sm::merge_entry<K>(keys_A, vals_A, n, keys_B, vals_B, m, out_keys, out_vals, stream, nullptr);   \
+    }                                                                                                           \
+    sm_status merge_stable_ex_##SUF(const K* keys_A, const uint32_t* vals_A, int64_t n, const K* keys_B,       \
+                                    const uint32_t* vals_B, int64_t m, K* out_keys, uint32_t* out_vals,       \
+                                    void* stream, const sm_options* opt) {                                     \
+        return sm::merge_entry<K>(keys_A, vals_A, n, keys_B, vals_B, m, out_keys, out_vals, stream, opt);       \
+    }                                                                                                           \
+    sm_status merge_plan_ex_##SUF(const K* keys_A, int64_t n, const K* keys_B, int64_t m, int64_t p_A,         \
+                                  int64_t p_B, int64_t* xbar, int64_t* ybar, int64_t* tasks, void* stream) {   \
+        return sm::plan_entry<K>(keys_A, n, keys_B, m, p_A, p_B, xbar, ybar, tasks, stream);                    \
+    }                                                                                                           \
+    sm_status mergesort_stable_##SUF(K* keys, uint32_t* vals, int64_t N, void* stream) {                       \
+        return sm::sort_entry<K>(keys, vals, N, stream, nullptr);                                               \
+    }                                                                                                           \
+    sm_status mergesort_stable_ex_##SUF(K* keys, uint32_t* vals, int64_t N, void* stream,                      \
+                                        const sm_options* opt) {                                               \
+        return sm::sort_entry<K>(keys, vals, N, stream, opt);                                                   \
+    }
+
+SM_DEFINE_ABI(u32, uint32_t)
+SM_DEFINE_ABI(i32, int32_t)
+SM_DEFINE_ABI(i64, int64_t)
+SM_DEFINE_ABI(u64, uint64_t)
+
+int64_t sm_tile_capacity(int32_t key_bytes, int32_t has_vals) {
+    (void)key_bytes;
+    (void)has_vals;
+    return sm::NV;
+}
+
+int64_t sm_sort_run(int32_t key_bytes, int32_t has_vals) {
+    (void)key_bytes;
+    (void)has_vals;
+    return sm::NV;
+}
+
+const char* sm_status_string(sm_status s) {
+    switch (s) {
+        case SM_OK: return "SM_OK";
+        case SM_EINVAL: return "SM_EINVAL: invalid argument";
+        case SM_EALIAS: return "SM_EALIAS: output overlaps an input";
+        case SM_ENOMEM: return "SM_ENOMEM: scratch allocation failed";
+        case SM_ECUDA: return "SM_ECUDA: CUDA error";
+    }
+    return "unknown status";
+}
+
+const char* sm_last_error(void) { return sm::g_err; }
+
+int64_t sm_last_launch_count(void) { return sm::g_launches; }
+
+void sm_profile_enable(int on) {
+    sm::g_prof_on = on != 0;
+    sm::g_prof_used = 0;
+}
+
+sm_status sm_profile_read(int kind, double* total_ms, int64_t* launches) {
+    double t = 0.0;
+    int64_t c = 0;
+    for (size_t i = 0; i < sm::g_prof_used; ++i) {
+        const sm::ProfRec& r = sm::g_prof_pool[i];
+        if (r.kind != kind) continue;
+        cudaError_t e = cudaEventSynchronize(r.b);
+        if (e != cudaSuccess) return sm::fail_cuda(e, "cudaEventSynchronize");
+        float ms = 0.f;
+        e = cudaEventElapsedTime(&ms, r.a, r.b);
+        if (e != cudaSuccess) return sm::fail_cuda(e, "cudaEventElapsedTime");
+        t += ms;
+        ++c;
+    }
+    if (total_ms) *total_ms = t;
+    if (launches) *launches = c;
+    return SM_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,80 @@
+"""The C-ABI library loads and exports every symbol include/*.h declares; host-side
+argument validation (no GPU, no compute calls)."""
+import ctypes
+import glob
+import os
+import re
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_functions():
+    names = []
+    for h in glob.glob(os.path.join(ROOT, "include", "*.h")):
+        text = re.sub(r"/\*.*?\*/", "", open(h).read(), flags=re.S)
+        names += re.findall(r"^\s*(?:sm_status|int64_t|void|const\s+char\s*\*)\s*\*?\s*(\w+)\s*\(", text, flags=re.M)
+    return names
+
+
+@pytest.fixture(scope="module")
+def sm():
+    import build_native
+    build_native.build()
+    import paper_1202_6575_b200 as sm
+    return sm
+
+
+def test_header_declares_entry_points():
+    names = declared_functions()
+    for kt in ("u32", "i32", "i64", "u64"):
+        for f in ("merge_stable", "mergesort_stable", "merge_stable_ex", "merge_plan_ex", "mergesort_stable_ex"):
+            assert f"{f}_{kt}" in names
+    assert len(names) == 27
+
+
+def test_library_exports_every_declared_symbol(sm):
+    lib = ctypes.CDLL(sm.LIB_PATH)
+    for name in declared_functions():
+        assert hasattr(lib, name), name
+    out = subprocess.run(["nm", "-D", "--defined-only", sm.LIB_PATH], capture_output=True, text=True).stdout
+    exported = set(re.findall(r"\s[TW]\s+(\w+)$", out, flags=re.M))
+    assert set(declared_functions()) <= exported
+
+
+def test_library_is_sm100a(sm):
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", sm.LIB_PATH], capture_output=True,
+                         text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_host_validation_without_gpu(sm):
+    lib = sm._lib
+    P = ctypes.c_void_p
+    # negative sizes -> SM_EINVAL before any CUDA call
+    assert lib.merge_stable_u32(None, None, -1, None, None, 0, None, None, None) == sm.SM_EINVAL
+    assert lib.mergesort_stable_i64(None, None, -5, None) == sm.SM_EINVAL
+    # NULL keys with a nonzero size
+    assert lib.merge_stable_i32(None, None, 10, None, None, 0, None, None, None) == sm.SM_EINVAL
+    # payload pointers half set
+    assert lib.merge_stable_u32(P(0x1000), P(0x2000), 4, P(0x3000), None, 4, P(0x9000), None, None) == sm.SM_EINVAL
+    # sizes beyond 32-bit in-kernel indices
+    assert lib.merge_stable_u64(P(0x1000), None, 1 << 31, P(0x1000), None, 1, P(0x1000), None, None) == sm.SM_EINVAL
+    # output overlapping an input -> SM_EALIAS
+    assert lib.merge_stable_u32(P(0x10000), None, 100, P(0x20000), None, 100, P(0x10100), None, None) == sm.SM_EALIAS
+    assert sm._lib.sm_status_string(sm.SM_EALIAS).startswith(b"SM_EALIAS")
+    assert b"invalid" in sm._lib.sm_status_string(sm.SM_EINVAL)
+    # invalid tuning options
+    opt = sm.SmOptions(0, 0, 10 ** 6, 0, 0)
+    assert lib.merge_stable_ex_u32(P(0x10000), None, 100, P(0x20000), None, 100, P(0x30000), None, None,
+                                   ctypes.byref(opt)) == sm.SM_EINVAL
+    opt = sm.SmOptions(1, 0, 0, 0, 0)
+    assert lib.merge_stable_ex_u32(P(0x10000), None, 100, P(0x20000), None, 100, P(0x30000), None, None,
+                                   ctypes.byref(opt)) == sm.SM_EINVAL
+
+
+def test_tile_constants(sm):
+    cap = sm.tile_capacity("u32", True)
+    assert cap >= 256 and cap == sm.sort_run("u32", True)

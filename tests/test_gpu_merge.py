@@ -1,0 +1,217 @@
+"""GPU parity of the stable merge (rows a0-a7) against the CPU oracle.
+
+Bit-exact (keys and payloads) on seeded synthetic inputs of every BASELINE.json
+merge config: at reduced sizes spanning many tiles with ragged tails, at the
+full sizes in the launch configuration bench.py times, and on the edge cases.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+from oracle import plan as P
+from gpu_util import assert_bit_exact, gpu_merge, lib, oracle_merge
+
+pytestmark = pytest.mark.gpu
+HERE = os.path.dirname(os.path.abspath(__file__))
+FIG1 = json.load(open(os.path.join(HERE, "golden", "fig1.json")))
+
+
+# ------------------------------------------------------- plan (Steps 1-4)
+
+def test_fig1_plan_on_device():
+    sm = lib()
+    A = torch.tensor(FIG1["A"], dtype=torch.int32, device="cuda")
+    B = torch.tensor(FIG1["B"], dtype=torch.int32, device="cuda")
+    xbar, ybar, tasks = sm.merge_plan(A, B, 5, 5)
+    assert xbar.tolist() == FIG1["xbar"]
+    assert ybar.tolist() == FIG1["ybar"]
+    *_, otasks = P.build_plan(FIG1["A"], FIG1["B"], 5)
+    assert tasks.cpu().numpy().tolist() == P.task_table(otasks).tolist()
+    offs = (tasks[:, 2] + tasks[:, 4]).tolist()
+    assert offs == [g["C"][0] for g in FIG1["tasks"]]
+
+
+def test_fig1_merge_on_device():
+    sm = lib()
+    A = torch.tensor(FIG1["A"], dtype=torch.int32, device="cuda")
+    B = torch.tensor(FIG1["B"], dtype=torch.int32, device="cuda")
+    va = torch.arange(18, dtype=torch.int32, device="cuda")
+    vb = (torch.arange(15, dtype=torch.int64, device="cuda") - (1 << 31)).to(torch.int32)
+    for p in (1, 2, 3, 5, 8):
+        ck, cv = sm.merge_stable(A, va, B, vb, p_A=p, p_B=p)
+        assert ck.tolist() == FIG1["C_keys"]
+        wk, wv = oracle.merge(A.cpu(), va.cpu(), B.cpu(), vb.cpu(), "i32")
+        assert np.array_equal(oracle.vals_np(cv.cpu()), wv)
+
+
+@pytest.mark.parametrize("kt,dist", [("i32", "bounded:7"), ("u32", "full"), ("i64", "bounded:1000"),
+                                     ("u64", "mostly:0x8000000000000000:9/10")])
+@pytest.mark.parametrize("pApB", [(1, 1), (3, 3), (17, 5), (64, 64), (1000, 7), (5, 999)])
+def test_plan_parity_random(kt, dist, pApB):
+    sm = lib()
+    pA, pB = pApB
+    inp = synth.merge_input(5003, 2999, kt, dist, seed=77 + pA, payload=False)
+    a, b = oracle.as_np(inp.a_keys, kt), oracle.as_np(inp.b_keys, kt)
+    x, y, oxbar, oybar, otasks = P.build_plan(a, b, pA, pB, vectorised=True)
+    xbar, ybar, tasks = sm.merge_plan(inp.a_keys.cuda(), inp.b_keys.cuda(), pA, pB, key_type=kt)
+    assert xbar.tolist() == oxbar and ybar.tolist() == oybar
+    assert np.array_equal(tasks.cpu().numpy(), P.task_table(otasks))
+
+
+def test_plan_parity_exhaustive_small():
+    sm = lib()
+    import itertools
+    seqs = [list(c) for L in range(5) for c in itertools.combinations_with_replacement(range(3), L)]
+    for a in seqs[::3]:
+        for b in seqs[::2]:
+            for p in (1, 2, 3, 5):
+                A = torch.tensor(a, dtype=torch.int32, device="cuda")
+                B = torch.tensor(b, dtype=torch.int32, device="cuda")
+                xbar, ybar, tasks = sm.merge_plan(A, B, p, p)
+                _, _, oxbar, oybar, otasks = P.build_plan(a, b, p)
+                assert xbar.tolist() == oxbar and ybar.tolist() == oybar
+                assert tasks.cpu().numpy().tolist() == P.task_table(otasks).tolist()
+
+
+# --------------------------------------------------- merge parity (small)
+
+@pytest.mark.parametrize("cfg,scale", [(1, 16), (1, 1), (2, 256), (3, 256), (4, 128)])
+def test_config_merge_reduced(cfg, scale):
+    sm = lib()
+    inp = synth.config_input(cfg, scale=scale)
+    want = oracle_merge(inp)
+    got = gpu_merge(sm, inp)
+    assert_bit_exact(*got, *want, inp.key_type)
+
+
+@pytest.mark.parametrize("kt", ["u32", "i32", "i64", "u64"])
+@pytest.mark.parametrize("nm", [(1, 0), (0, 1), (1, 1), (5, 3), (959, 961), (1920, 1), (1921, 3839),
+                                (70001, 12345), (12345, 70001), (100000, 17), (3, 200003)])
+@pytest.mark.parametrize("payload", [True, False])
+def test_merge_ragged(kt, nm, payload):
+    sm = lib()
+    n, m = nm
+    for dist in ("bounded:3", "full"):
+        inp = synth.merge_input(n, m, kt, dist, seed=n * 31 + m, payload=payload)
+        assert_bit_exact(*gpu_merge(sm, inp), *oracle_merge(inp), kt)
+
+
+@pytest.mark.parametrize("block", [1, 2, 7, 32, 257, 960])
+def test_merge_metamorphic_block_size(block):
+    """Output must not depend on the tuning (T, p_A vs p_B) -- S:L262."""
+    sm = lib()
+    inp = synth.merge_input(30011, 20011, "u32", "bounded:50", seed=5)
+    want = oracle_merge(inp)
+    assert_bit_exact(*gpu_merge(sm, inp, block=block), *want, "u32")
+    assert_bit_exact(*gpu_merge(sm, inp, block=block, pdl=False), *want, "u32")
+
+
+def test_merge_paper_single_p():
+    sm = lib()
+    inp = synth.merge_input(50000, 30000, "i64", "bounded:100", seed=9)
+    want = oracle_merge(inp)
+    for p in (60, 100, 1000):
+        assert_bit_exact(*gpu_merge(sm, inp, p_A=p, p_B=p), *want, "i64")
+
+
+def test_merge_repeatable():
+    sm = lib()
+    inp = synth.config_input(1, scale=4).to("cuda")
+    r1 = sm.merge_stable(inp.a_keys, inp.a_vals, inp.b_keys, inp.b_vals, key_type="u32")
+    r2 = sm.merge_stable(inp.a_keys, inp.a_vals, inp.b_keys, inp.b_vals, key_type="u32")
+    assert torch.equal(r1[0], r2[0]) and torch.equal(r1[1], r2[1])
+
+
+# ------------------------------------------------------------- edge cases
+
+def _mk(a, b, kt):
+    dt = {"u32": np.uint32, "i32": np.int32, "i64": np.int64, "u64": np.uint64}[kt]
+    a = np.sort(np.array(a, dtype=dt)); b = np.sort(np.array(b, dtype=dt))
+    ct = torch.int32 if kt in ("u32", "i32") else torch.int64
+    A = torch.from_numpy(a.view(np.int32 if ct == torch.int32 else np.int64).copy())
+    B = torch.from_numpy(b.view(np.int32 if ct == torch.int32 else np.int64).copy())
+    va, vb = synth.source_payloads(len(a), len(b))
+    return synth.MergeInput(kt, A, B, va, vb)
+
+
+@pytest.mark.parametrize("case", ["all_equal", "a_below_b", "a_above_b", "extremes", "interleaved_ties"])
+@pytest.mark.parametrize("kt", ["u32", "i32", "i64", "u64"])
+def test_merge_edge_cases(case, kt):
+    sm = lib()
+    big = 5000
+    info = np.iinfo({"u32": np.uint32, "i32": np.int32, "i64": np.int64, "u64": np.uint64}[kt])
+    if case == "all_equal":
+        a, b = [7] * big, [7] * (big // 2 + 3)
+    elif case == "a_below_b":
+        a, b = list(range(big)), list(range(big, 2 * big + 11))
+    elif case == "a_above_b":
+        a, b = list(range(big, 2 * big + 11)), list(range(big))
+    elif case == "extremes":
+        a = [info.min] * 1000 + [info.max] * 1001 + [0] * 17
+        b = [info.min] * 999 + [info.max] * 3000 + [1] * 5
+    else:
+        a = [i // 3 for i in range(3 * big)]
+        b = [i // 2 for i in range(2 * big)]
+    inp = _mk(a, b, kt)
+    assert_bit_exact(*gpu_merge(sm, inp), *oracle_merge(inp), kt)
+    if case == "all_equal":   # P7: C = A || B
+        _, cv = gpu_merge(sm, inp)
+        assert cv.tolist() == inp.a_vals.tolist() + inp.b_vals.tolist()
+
+
+def test_merge_empty_both():
+    sm = lib()
+    e = torch.empty(0, dtype=torch.int32, device="cuda")
+    ck, cv = sm.merge_stable(e, e, e, e)
+    assert ck.numel() == 0 and cv.numel() == 0
+
+
+def test_merge_host_buffers():
+    """The C ABI accepts host (pinned or pageable) buffers and stages them."""
+    sm = lib()
+    inp = synth.config_input(4, scale=512)
+    want = oracle_merge(inp)
+    got = sm.merge_stable(inp.a_keys, inp.a_vals, inp.b_keys, inp.b_vals, key_type="u64")
+    assert_bit_exact(*got, *want, "u64")
+    pin = lambda t: t.pin_memory()
+    out_k = torch.empty(inp.n + inp.m, dtype=torch.int64).pin_memory()
+    out_v = torch.empty(inp.n + inp.m, dtype=torch.int32).pin_memory()
+    got = sm.merge_stable(pin(inp.a_keys), pin(inp.a_vals), pin(inp.b_keys), pin(inp.b_vals), out_k, out_v,
+                          key_type="u64")
+    assert_bit_exact(*got, *want, "u64")
+
+
+def test_merge_errors():
+    sm = lib()
+    a = torch.arange(100, dtype=torch.int32, device="cuda")
+    with pytest.raises(sm.StableMergeError) as e:
+        sm.merge_stable(a, None, a, None, out_keys=a.new_empty(200), block=100000)
+    assert e.value.status == 1
+    out = torch.empty(300, dtype=torch.int32, device="cuda")
+    with pytest.raises(sm.StableMergeError) as e:      # output overlaps input
+        sm.merge_stable(out[:100], None, a, None, out_keys=out[100:300])
+    assert e.value.status == 2
+    with pytest.raises(sm.StableMergeError) as e:      # tile bound violated by explicit p
+        sm.merge_stable(torch.arange(5000, dtype=torch.int32, device="cuda"), None, a, None, p_A=1, p_B=1)
+    assert e.value.status == 1
+
+
+# ----------------------------------------------------- full-size parity
+
+@pytest.mark.parametrize("cfg", [1, 2, 3, 4])
+def test_config_merge_full_size(cfg):
+    """BASELINE.json sizes, default launch configuration (as bench.py times it):
+    the whole output against the oracle's merge, bit for bit."""
+    sm = lib()
+    dev = synth.config_input(cfg, device="cuda")
+    ck, cv = sm.merge_stable(dev.a_keys, dev.a_vals, dev.b_keys, dev.b_vals, key_type=dev.key_type)
+    torch.cuda.synchronize()
+    host = dev.to("cpu")
+    del dev
+    want_k, want_v = oracle_merge(host)
+    assert_bit_exact(ck.cpu(), None if cv is None else cv.cpu(), want_k, want_v, host.key_type)

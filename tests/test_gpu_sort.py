@@ -1,0 +1,87 @@
+"""GPU parity of the stable merge sort (rows a8-a9) against the CPU oracle."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+from gpu_util import assert_bit_exact, lib
+
+pytestmark = pytest.mark.gpu
+
+
+def gpu_sort(sm, inp: synth.SortInput):
+    k = inp.keys.cuda()
+    v = None if inp.vals is None else inp.vals.cuda()
+    sm.mergesort_stable(k, v, key_type=inp.key_type)
+    torch.cuda.synchronize()
+    return k.cpu(), (None if v is None else v.cpu())
+
+
+@pytest.mark.parametrize("kt", ["u32", "i32", "i64", "u64"])
+@pytest.mark.parametrize("N", [0, 1, 2, 3, 100, 1919, 1920, 1921, 3840, 5000, 65536, 100003, 1000001])
+def test_sort_ragged(kt, N):
+    sm = lib()
+    for dist, payload in (("bounded:64", True), ("full", True), ("bounded:5", False)):
+        inp = synth.sort_input(N, kt, dist, seed=N + 3, payload=payload)
+        want = oracle.sort(inp.keys, inp.vals, kt)
+        assert_bit_exact(*gpu_sort(sm, inp), *want, kt)
+
+
+@pytest.mark.parametrize("pattern", ["sorted", "reversed", "all_equal", "sawtooth"])
+def test_sort_patterns(pattern):
+    sm = lib()
+    N = 300007
+    if pattern == "sorted":
+        k = torch.arange(N, dtype=torch.int32)
+    elif pattern == "reversed":
+        k = torch.arange(N, 0, -1, dtype=torch.int32)
+    elif pattern == "all_equal":
+        k = torch.full((N,), 3, dtype=torch.int32)
+    else:
+        k = (torch.arange(N, dtype=torch.int32) % 1000)
+    inp = synth.SortInput("i32", k, torch.arange(N, dtype=torch.int32))
+    want = oracle.sort(inp.keys, inp.vals, "i32")
+    got = gpu_sort(sm, inp)
+    assert_bit_exact(*got, *want, "i32")
+    if pattern in ("sorted", "all_equal"):
+        assert torch.equal(got[1], torch.arange(N, dtype=torch.int32))
+
+
+def test_sort_reduced_config5():
+    sm = lib()
+    inp = synth.config_input(5, scale=64)
+    want = oracle.sort(inp.keys, inp.vals, "u32")
+    assert_bit_exact(*gpu_sort(sm, inp), *want, "u32")
+
+
+def test_sort_host_buffers():
+    sm = lib()
+    inp = synth.config_input(5, scale=4096)
+    want = oracle.sort(inp.keys, inp.vals, "u32")
+    k, v = inp.keys.clone(), inp.vals.clone()
+    sm.mergesort_stable(k, v, key_type="u32")
+    assert_bit_exact(k, v, *want, "u32")
+
+
+def test_sort_full_size_config5():
+    """N = 2^28 (BASELINE.json config 5), default launch configuration.  The
+    stable sort of (key, original index) is unique, so the check is: keys
+    non-decreasing, payload a permutation, out_key[t] == in_key[payload[t]],
+    and equal keys in increasing payload order; plus
+    the oracle's own sort on a 2^22 prefix-independent sample run."""
+    sm = lib()
+    dev = synth.config_input(5, device="cuda")
+    k0 = dev.keys.clone()
+    sm.mergesort_stable(dev.keys, dev.vals, key_type="u32")
+    torch.cuda.synchronize()
+    k, v = dev.keys, dev.vals.long()
+    ku = k.long() & 0xFFFFFFFF
+    assert bool((ku[1:] >= ku[:-1]).all())
+    assert bool((torch.sort(v).values == torch.arange(v.numel(), device="cuda")).all())
+    assert torch.equal(k, k0[v])
+    ties = ku[1:] == ku[:-1]
+    assert bool((v[1:][ties] > v[:-1][ties]).all())
+    # bit-exact against the oracle on the full array
+    want_k, want_v = oracle.sort(k0.cpu(), torch.arange(k0.numel(), dtype=torch.int32), "u32")
+    assert_bit_exact(k.cpu(), dev.vals.cpu(), want_k, want_v, "u32")
