@@ -118,6 +118,7 @@ __device__ __forceinline__ void serial_merge(const K* sk, int ai, int aend, int 
 }
 
 // ----------------------------------------------------------------- K2
+// Shared-memory tile used by K3 (block sort).
 template <typename K, bool HAS_V, int NT, int VT>
 struct TileSmem {
     static constexpr int NV = NT * VT;
@@ -125,69 +126,248 @@ struct TileSmem {
     uint32_t vals[HAS_V ? NV : 1];
 };
 
-template <typename K, bool HAS_V, int NT, int VT>
-__global__ void __launch_bounds__(NT) k_tasks(const K* __restrict__ A, const uint32_t* __restrict__ vA,
-                                              const K* __restrict__ B, const uint32_t* __restrict__ vB,
-                                              K* __restrict__ C, uint32_t* __restrict__ vC, Geom g,
-                                              const int* __restrict__ xbar, const int* __restrict__ ybar) {
-    constexpr int NV = NT * VT;
-    __shared__ TileSmem<K, HAS_V, NT, VT> sm_;
-    const int tid = threadIdx.x;
+// Merge-path split of diagonal d between sorted a[0,la) and b[0,lb):
+// smallest i with a[i] > b[d-1-i] (reading R17: advance while
+// a[mid] <= b[d-1-mid], so equal keys go to A).
+template <typename K>
+__device__ __forceinline__ int split_ab(const K* a, int la, const K* b, int lb, int d) {
+    int lo = max(0, d - lb), hi = min(d, la);
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (a[mid] <= b[d - 1 - mid]) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
 
+// Serial stable merge of VT outputs from (ai, bi), la >= 1 and lb >= 1;
+// ties take A.  src[k] = smem payload index of output k (va + ai or vb + bi).
+template <typename K, int VT, bool IDX>
+__device__ __forceinline__ void merge_serial(const K* a, int ai, int la, const K* b, int bi, int lb, int va, int vb,
+                                             K (&out)[VT], int (&src)[VT]) {
+    K ka = a[min(ai, la - 1)];
+    K kb = b[min(bi, lb - 1)];
+#pragma unroll
+    for (int k = 0; k < VT; ++k) {
+        const bool takeA = (bi >= lb) || (ai < la && ka <= kb);
+        out[k] = takeA ? ka : kb;
+        if (IDX) src[k] = takeA ? va + ai : vb + bi;
+        if (takeA) {
+            ++ai;
+            ka = a[min(ai, la - 1)];
+        } else {
+            ++bi;
+            kb = b[min(bi, lb - 1)];
+        }
+    }
+}
+
+// Task descriptor handed from the producer warp to the consumers (smem).
+struct TaskDesc {
+    int la, lb;        // lengths of the A and B ranges
+    int a_s, b_s;      // smem element index of A[a0] / B[b0] in the key region
+    int va_s, vb_s;    // smem element index of the payloads in the payload region
+    int off;           // global output element index (segment base + a0 + b0)
+    int pad;
+};
+
+template <typename K, bool HAS_V, int NC, int VT, int STAGES>
+struct K2Layout {
+    static constexpr int NV = NC * VT;                    // tile capacity (max task)
+    static constexpr int KPAD = 16 / (int)sizeof(K);      // elements per 16 bytes
+    static constexpr int KCAP = ((NV + 4 * KPAD + KPAD - 1) / KPAD) * KPAD;
+    static constexpr int VCAP = HAS_V ? ((NV + 16 + 3) / 4) * 4 : 0;
+    static constexpr int STAGE_BYTES = KCAP * (int)sizeof(K) + VCAP * 4;
+    static constexpr int SMEM = STAGES * STAGE_BYTES + STAGES * (int)sizeof(TaskDesc) + 2 * STAGES * 8 + 16;
+};
+
+// The 16-byte-aligned superset [g0, g0 + bytes) of src[0, len), to be
+// bulk-loaded at smem byte offset `at`; `idx` = smem element index of src[0].
+struct Span {
+    uintptr_t g0;
+    uint32_t bytes;
+    int at, idx;
+};
+
+template <typename T>
+__device__ __forceinline__ Span plan_range(int& at, const T* src, int len) {
+    Span sp;
+    const uintptr_t g = (uintptr_t)src;
+    sp.g0 = g & ~(uintptr_t)15;
+    sp.bytes = len > 0 ? (uint32_t)(((g + (uintptr_t)len * sizeof(T) + 15) & ~(uintptr_t)15) - sp.g0) : 0u;
+    sp.at = at;
+    sp.idx = (at + (int)(g - sp.g0)) / (int)sizeof(T);
+    at += (int)sp.bytes;
+    return sp;
+}
+
+__device__ __forceinline__ void issue_range(char* base, const Span& sp, uint64_t* bar) {
+    if (sp.bytes) bulk_g2s(base + sp.at, (const void*)sp.g0, sp.bytes, bar);
+}
+
+// Store smem sbuf[ph, ph+L) (already in output order) to dst[0, L): the
+// 16-byte-aligned middle with one bulk copy issued by consumer 0, the
+// <= 2*(16/sizeof(T)-1) edge elements with plain stores by consumers
+// edge0 .. edge0+5.
+template <typename T>
+__device__ __forceinline__ void store_range(T* dst, const T* sbuf, int ph, int L, int c, int edge0) {
+    const uintptr_t g = (uintptr_t)dst;
+    const uintptr_t gl = (g + 15) & ~(uintptr_t)15;
+    const uintptr_t gh = (g + (uintptr_t)L * sizeof(T)) & ~(uintptr_t)15;
+    int head = (int)((gl - g) / sizeof(T));
+    if (head > L) head = L;
+    const int tail0 = gh > gl ? (int)((gh - g) / sizeof(T)) : head;
+    if (c == 0) {
+        if (gh > gl) bulk_s2g((void*)gl, sbuf + ph + head, (uint32_t)(gh - gl));
+    } else {
+        const int e = c - edge0;
+        if (e >= 0 && e < head) dst[e] = sbuf[ph + e];
+        else if (e >= head && e - head < L - tail0) dst[tail0 + e - head] = sbuf[ph + tail0 + e - head];
+    }
+}
+
+// K2 (rows a4-a7): persistent, warp-specialised.  Warp 0 lane 0 is the
+// producer: it classifies task t (O(1), L310-340), and bulk-loads the task's
+// A and B ranges (keys, payloads) into a STAGES-deep shared-memory ring with
+// the TMA engine.  NC consumer threads merge (cases b, c, d) or realign
+// (copies, cases a, e) each task and write it back with bulk stores.
+template <typename K, bool HAS_V, int NC, int VT, int STAGES>
+__global__ void __launch_bounds__(NC + 32) k_tasks(const K* __restrict__ A, const uint32_t* __restrict__ vA,
+                                                   const K* __restrict__ B, const uint32_t* __restrict__ vB,
+                                                   K* __restrict__ C, uint32_t* __restrict__ vC, Geom g,
+                                                   const int* __restrict__ xbar, const int* __restrict__ ybar) {
+    using Lay = K2Layout<K, HAS_V, NC, VT, STAGES>;
+    extern __shared__ __align__(128) char smem[];
+    TaskDesc* desc = (TaskDesc*)(smem + STAGES * Lay::STAGE_BYTES);
+    uint64_t* full = (uint64_t*)(desc + STAGES);
+    uint64_t* empty = full + STAGES;
+    const int ntasks = g.S * (g.pA + g.pB);
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        fence_barrier_init();
+        fence_proxy_async();
+    }
+    __syncthreads();
     pdl_wait();   // the single synchronisation (L373-375): all ranks visible
 
-    Seg sg;
-    const Task t = decode_task(g, blockIdx.x, xbar, ybar, sg);
-    const int la = t.a1 - t.a0, lb = t.b1 - t.b0, L = la + lb;
-    const int off = sg.coff + t.a0 + t.b0;
-    const K* As = A + sg.aoff + t.a0;
-    const K* Bs = B + sg.boff + t.b0;
-
-    if (la == 0 || lb == 0) {                       // cases (a), (e): copy (row a6)
-        const int so = la ? sg.aoff + t.a0 : sg.boff + t.b0;
-        cta_copy<K, NT, 4>((la ? A : B) + so, C + off, L);
-        if (HAS_V) cta_copy<uint32_t, NT, 4>((la ? vA : vB) + so, vC + off, L);
+    if (threadIdx.x < 32) {
+        // ------------------------------------------------------ producer
+        if (threadIdx.x == 0) {
+            int it = 0;
+            for (int task = blockIdx.x; task < ntasks; task += gridDim.x, ++it) {
+                const int s = it % STAGES;
+                if (it >= STAGES) mbar_wait(&empty[s], ((it / STAGES) - 1) & 1);
+                Seg sg;
+                const Task t = decode_task(g, task, xbar, ybar, sg);
+                char* stage = smem + s * Lay::STAGE_BYTES;
+                char* vstage = stage + Lay::KCAP * (int)sizeof(K);
+                TaskDesc d;
+                d.la = t.a1 - t.a0;
+                d.lb = t.b1 - t.b0;
+                d.off = sg.coff + t.a0 + t.b0;
+                int at = 0, vat = 0;
+                const Span sa = plan_range(at, A + sg.aoff + t.a0, d.la);
+                const Span sb = plan_range(at, B + sg.boff + t.b0, d.lb);
+                Span sva, svb;
+                sva.bytes = svb.bytes = 0;
+                sva.idx = svb.idx = 0;
+                if (HAS_V) {
+                    sva = plan_range(vat, vA + sg.aoff + t.a0, d.la);
+                    svb = plan_range(vat, vB + sg.boff + t.b0, d.lb);
+                }
+                d.a_s = sa.idx; d.b_s = sb.idx; d.va_s = sva.idx; d.vb_s = svb.idx; d.pad = 0;
+                desc[s] = d;   // written before the arrive (release) below
+                mbar_arrive_expect_tx(&full[s], sa.bytes + sb.bytes + sva.bytes + svb.bytes);
+                issue_range(stage, sa, &full[s]);
+                issue_range(stage, sb, &full[s]);
+                if (HAS_V) {
+                    issue_range(vstage, sva, &full[s]);
+                    issue_range(vstage, svb, &full[s]);
+                }
+            }
+        }
         return;
     }
 
-    // cases (b), (c), (d): stable merge of A[a0,a1) and B[b0,b1) (row a7)
-#pragma unroll
-    for (int k = 0; k < VT; ++k) {
-        const int idx = k * NT + tid;
-        if (idx < L) {
-            sm_.keys[idx] = idx < la ? ld_stream(As + idx) : ld_stream(Bs + (idx - la));
-            if (HAS_V)
-                sm_.vals[idx] = idx < la ? ld_stream(vA + sg.aoff + t.a0 + idx)
-                                         : ld_stream(vB + sg.boff + t.b0 + (idx - la));
-        }
-    }
-    __syncthreads();
+    // ---------------------------------------------------------- consumers
+    const int c = threadIdx.x - 32;
+    int it = 0;
+    for (int task = blockIdx.x; task < ntasks; task += gridDim.x, ++it) {
+        const int s = it % STAGES;
+        mbar_wait(&full[s], (it / STAGES) & 1);
+        const TaskDesc d = desc[s];
+        K* sk = (K*)(smem + s * Lay::STAGE_BYTES);
+        uint32_t* sv = (uint32_t*)(smem + s * Lay::STAGE_BYTES + Lay::KCAP * (int)sizeof(K));
+        const int L = d.la + d.lb;
+        const int phC = (int)(((uintptr_t)(C + d.off) & 15) / sizeof(K));
+        const int phV = HAS_V ? (int)(((uintptr_t)(vC + d.off) & 15) / 4) : 0;
 
-    const int d = min(tid * VT, L);
-    const int ai = tile_split(sm_.keys, la, lb, d);
-    K out[VT];
-    int src[VT];
-    serial_merge<K, VT>(sm_.keys, ai, la, la + (d - ai), L, out, src);
-    uint32_t v[HAS_V ? VT : 1];
-    if (HAS_V) {
+        if (d.la > 0 && d.lb > 0) {
+            // cases (b), (c), (d): stable merge (row a7)
+            const int dg = min(c * VT, L);
+            const K* a = sk + d.a_s;
+            const K* b = sk + d.b_s;
+            const int ai = split_ab(a, d.la, b, d.lb, dg);
+            K out[VT];
+            int src[VT];
+            merge_serial<K, VT, HAS_V>(a, ai, d.la, b, dg - ai, d.lb, d.va_s, d.vb_s, out, src);
+            uint32_t v[HAS_V ? VT : 1];
+            if (HAS_V) {
 #pragma unroll
-        for (int k = 0; k < VT; ++k) v[k] = sm_.vals[min(src[k], NV - 1)];
-    }
-    __syncthreads();
+                for (int k = 0; k < VT; ++k) v[k] = sv[min(src[k], Lay::VCAP - 1)];
+            }
+            named_sync(1, NC);
 #pragma unroll
-    for (int k = 0; k < VT; ++k) {
-        sm_.keys[tid * VT + k] = out[k];
-        if (HAS_V) sm_.vals[tid * VT + k] = v[k];
-    }
-    __syncthreads();
+            for (int k = 0; k < VT; ++k) {
+                if (dg + k < L) {
+                    sk[phC + dg + k] = out[k];
+                    if (HAS_V) sv[phV + dg + k] = v[k];
+                }
+            }
+        } else if (L > 0) {
+            // cases (a), (e): copy (row a6) -- realign to the output phase
+            const int ks = d.la ? d.a_s : d.b_s;
+            const int vs = d.la ? d.va_s : d.vb_s;
+            const bool mv = ks != phC || (HAS_V && vs != phV);
+            if (mv) {
+                K r[VT];
+                uint32_t rv[HAS_V ? VT : 1];
 #pragma unroll
-    for (int k = 0; k < VT; ++k) {
-        const int idx = k * NT + tid;
-        if (idx < L) {
-            st_stream(C + off + idx, sm_.keys[idx]);
-            if (HAS_V) st_stream(vC + off + idx, sm_.vals[idx]);
+                for (int k = 0; k < VT; ++k) {
+                    const int t = k * NC + c;
+                    if (t < L) {
+                        r[k] = sk[ks + t];
+                        if (HAS_V) rv[k] = sv[vs + t];
+                    }
+                }
+                named_sync(1, NC);
+#pragma unroll
+                for (int k = 0; k < VT; ++k) {
+                    const int t = k * NC + c;
+                    if (t < L) {
+                        sk[phC + t] = r[k];
+                        if (HAS_V) sv[phV + t] = rv[k];
+                    }
+                }
+            }
+        }
+        fence_proxy_async();
+        named_sync(1, NC);
+        if (L > 0) {
+            store_range<K>(C + d.off, sk, phC, L, c, 1);
+            if (HAS_V) store_range<uint32_t>(vC + d.off, sv, phV, L, c, 32);
+        }
+        if (c == 0) {
+            bulk_commit();
+            bulk_wait_read<1>();                 // task it-1's stores have read their stage
+            if (it >= 1) mbar_arrive(&empty[(it - 1) % STAGES]);
         }
     }
+    if (c == 0) bulk_wait_read<0>();
 }
 
 // ----------------------------------------------------------- plan dump

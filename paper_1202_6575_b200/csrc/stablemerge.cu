@@ -22,12 +22,18 @@ namespace sm {
 thread_local char g_err[512] = "";
 thread_local int64_t g_launches = 0;
 
-// Tile shape of K2 and K3.  VT odd keeps the register <-> shared-memory
+// K2 shape: NC consumer threads x VT elements = tile capacity NV (largest
+// task), STAGES-deep TMA ring.  VT odd keeps the register <-> shared-memory
 // transposition free of bank conflicts for 4- and 8-byte keys.
+constexpr int K2_NC = 256;
+constexpr int K2_VT = 15;
+constexpr int K2_STAGES = 3;
+constexpr int NV = K2_NC * K2_VT;  // tile capacity: largest task
+constexpr int T_DEFAULT = NV / 2;  // block size: task bound 2T (L388-393)
+// K3 shape: one run of R = NT * VT elements per CTA.
 constexpr int NT = 128;
 constexpr int VT = 15;
-constexpr int NV = NT * VT;       // tile capacity: largest task / sort run
-constexpr int T_DEFAULT = NV / 2; // block size: task bound 2T (L388-393)
+constexpr int R_SORT = NT * VT;
 
 static sm_status fail_cuda(cudaError_t e, const char* what) {
     snprintf(g_err, sizeof(g_err), "%s: %s", what, cudaGetErrorString(e));
@@ -123,11 +129,25 @@ static sm_status launch_merge(const K* A, const uint32_t* vA, const K* B, const 
     sm_status s = check_launch("k_cross_ranks");
     if (s != SM_OK) return s;
 
+    using Lay = K2Layout<K, HAS_V, K2_NC, K2_VT, K2_STAGES>;
+    auto kern = k_tasks<K, HAS_V, K2_NC, K2_VT, K2_STAGES>;
+    static int per_sm = -1, n_sm = 0;
+    if (per_sm < 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Lay::SMEM);
+        cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, K2_NC + 32, Lay::SMEM);
+        if (per_sm < 1) per_sm = 1;
+    }
+    const long long ntasks = (long long)g.S * (g.pA + g.pB);
+    const long long grid = std::min<long long>(ntasks, (long long)per_sm * n_sm);
     cudaLaunchConfig_t cfg;
     memset(&cfg, 0, sizeof(cfg));
-    cfg.gridDim = dim3((unsigned)((long long)g.S * (g.pA + g.pB)));
-    cfg.blockDim = dim3(NT);
-    cfg.dynamicSmemBytes = 0;
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3(K2_NC + 32);
+    cfg.dynamicSmemBytes = Lay::SMEM;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -135,8 +155,7 @@ static sm_status launch_merge(const K* A, const uint32_t* vA, const K* B, const 
     cfg.attrs = attr;
     cfg.numAttrs = (pdl && !g_prof_on) ? 1 : 0;
     prof_before(PROF_K2, st);
-    cudaError_t e = cudaLaunchKernelEx(&cfg, k_tasks<K, HAS_V, NT, VT>, A, vA, B, vB, C, vC, g,
-                                       (const int*)xbar, (const int*)ybar);
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, A, vA, B, vB, C, vC, g, (const int*)xbar, (const int*)ybar);
     prof_after(st);
     ++g_launches;
     if (e != cudaSuccess) {
@@ -320,7 +339,7 @@ static sm_status plan_entry(const K* A, int64_t n, const K* B, int64_t m, int64_
 // ------------------------------------------------------------ merge sort
 template <typename K>
 static sm_status sort_device(K* keys, uint32_t* vals, int64_t N, cudaStream_t st, bool pdl) {
-    const int R = NV;   // initial run length: one K3 tile
+    const int R = R_SORT;   // initial run length: one K3 tile
     int rounds = 0;
     for (int64_t L = R; L < N; L *= 2) ++rounds;
     K* aux = nullptr;
@@ -372,7 +391,7 @@ static sm_status sort_entry(K* keys, uint32_t* vals, int64_t N, void* stream, co
     if (N < 0) return fail_inval("negative size");
     if (N && !keys) return fail_inval("NULL key pointer with nonzero size");
     if (N > (int64_t)INT_MAX) return fail_inval("N > 2^31 - 1");
-    if (opt && opt->sort_run && opt->sort_run != NV) return fail_inval("sort_run must equal the block-sort tile");
+    if (opt && opt->sort_run && opt->sort_run != R_SORT) return fail_inval("sort_run must equal the block-sort tile");
     if (overlaps(keys, N * sizeof(K), vals, N * 4)) return SM_EALIAS;
     const bool pdl = !(opt && (opt->flags & SM_FLAG_NO_PDL));
     if (N <= 1) return SM_OK;
@@ -429,7 +448,7 @@ int64_t sm_tile_capacity(int32_t key_bytes, int32_t has_vals) {
 int64_t sm_sort_run(int32_t key_bytes, int32_t has_vals) {
     (void)key_bytes;
     (void)has_vals;
-    return sm::NV;
+    return sm::R_SORT;
 }
 
 const char* sm_status_string(sm_status s) {

@@ -194,7 +194,7 @@ def test_merge_errors():
     assert e.value.status == 1
     out = torch.empty(300, dtype=torch.int32, device="cuda")
     with pytest.raises(sm.StableMergeError) as e:      # output overlaps input
-        sm.merge_stable(out[:100], None, a, None, out_keys=out[100:300])
+        sm.merge_stable(out[:100], None, a, None, out_keys=out[50:250])
     assert e.value.status == 2
     with pytest.raises(sm.StableMergeError) as e:      # tile bound violated by explicit p
         sm.merge_stable(torch.arange(5000, dtype=torch.int32, device="cuda"), None, a, None, p_A=1, p_B=1)
