@@ -19,33 +19,76 @@
 namespace sm {
 
 // ----------------------------------------------------------------- K1
-template <typename K>
+// Rows a1/a2.  A group of G lanes performs one rank search cooperatively:
+// each round the G lanes probe G evenly spaced keys of the remaining
+// interval and a group ballot picks the sub-interval holding the rank, so a
+// search over len keys takes ~log_{G+1}(len) dependent memory rounds instead
+// of log_2(len) (the latency chain is what bounds this kernel).
+//   HIGH = false: rank_low(x, X)  = #{X[t] <  x}   (L119-123)
+//   HIGH = true:  rank_high(x, X) = #{X[t] <= x}   (L124-128)
+template <typename K, int G>
+__device__ __forceinline__ int group_rank(const K* __restrict__ X, int len, K x, bool high, bool active) {
+    const int lane = threadIdx.x & 31;
+    const int sub = lane % G;
+    const int shift = lane - sub;
+    int lo = 0, hi = active ? len : 0;     // rank in [lo, hi]; X[lo, hi) undecided
+    while (__any_sync(0xffffffffu, hi > lo)) {
+        const int n = hi - lo;
+        int pos;
+        if (n <= G) pos = lo + sub;                                   // last round: probe all
+        else pos = lo + (int)(((long long)(sub + 1) * n) / (G + 1));  // G interior probes
+        bool pred = false;
+        if (hi > lo && (n > G || sub < n)) {
+            const K v = __ldg(X + pos);
+            pred = high ? (v <= x) : (v < x);
+        }
+        const unsigned bal = (__ballot_sync(0xffffffffu, pred) >> shift) & ((1u << G) - 1u);
+        const int t = __popc(bal);   // probes passed: a prefix of the group
+        if (hi > lo) {
+            if (n <= G) {
+                lo = lo + t;
+                hi = lo;
+            } else {
+                const int plast = t > 0 ? lo + (int)(((long long)t * n) / (G + 1)) : lo - 1;
+                const int pnext = t < G ? lo + (int)(((long long)(t + 1) * n) / (G + 1)) : hi;
+                lo = plast + 1;
+                hi = pnext;
+            }
+        }
+    }
+    return lo;
+}
+
+template <typename K, int G>
 __global__ void __launch_bounds__(256) k_cross_ranks(const K* __restrict__ A, const K* __restrict__ B, Geom g,
                                                      int* __restrict__ xbar, int* __restrict__ ybar) {
     const int per = g.pA + g.pB + 2;
-    const long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (gid < (long long)g.S * per) {
-        const int s = (int)(gid / per), t = (int)(gid % per);
-        const Seg sg = segment(g, s);
-        const K* As = A + sg.aoff;
-        const K* Bs = B + sg.boff;
-        if (t <= g.pA) {                                  // Step 1: xbar_i = rank_low(A[x_i], B)
-            const int i = t;
-            int v = sg.m;                                 // xbar_p = m; empty block start -> m (R4)
-            if (i < g.pA) {
-                const int xi = Blocks(sg.n, g.pA).start(i);
-                if (xi < sg.n) v = rank_low_dev(Bs, sg.m, __ldg(As + xi));
-            }
-            xbar[(size_t)s * (g.pA + 1) + i] = v;
-        } else {                                          // Step 2: ybar_j = rank_high(B[y_j], A)
-            const int j = t - g.pA - 1;
-            int v = sg.n;
-            if (j < g.pB) {
-                const int yj = Blocks(sg.m, g.pB).start(j);
-                if (yj < sg.m) v = rank_high_dev(As, sg.n, __ldg(Bs + yj));
-            }
-            ybar[(size_t)s * (g.pB + 1) + j] = v;
-        }
+    const long long item = ((long long)blockIdx.x * blockDim.x + threadIdx.x) / G;
+    const bool valid = item < (long long)g.S * per;
+    int s = 0, t = 0;
+    if (valid) {
+        s = (int)(item / per);
+        t = (int)(item % per);
+    }
+    const Seg sg = segment(g, s);
+    const K* As = A + sg.aoff;
+    const K* Bs = B + sg.boff;
+    // Step 1 (t <= pA): xbar_i = rank_low(A[x_i], B), xbar_pA = m, empty block start -> m (R4)
+    // Step 2 (t >  pA): ybar_j = rank_high(B[y_j], A), ybar_pB = n
+    const bool sideA = t <= g.pA;
+    const int idx = sideA ? t : t - g.pA - 1;
+    const int plen = sideA ? g.pA : g.pB;
+    const int own_len = sideA ? sg.n : sg.m;
+    int start = own_len;
+    if (valid && idx < plen) start = Blocks(own_len, plen).start(idx);
+    const bool search = valid && start < own_len;
+    K x = K(0);
+    if (search) x = __ldg((sideA ? As : Bs) + start);
+    const int r = group_rank<K, G>(sideA ? Bs : As, sideA ? sg.m : sg.n, x, !sideA, search);
+    if (valid && (threadIdx.x % G) == 0) {
+        const int v = search ? r : (sideA ? sg.m : sg.n);
+        if (sideA) xbar[(size_t)s * (g.pA + 1) + idx] = v;
+        else ybar[(size_t)s * (g.pB + 1) + idx] = v;
     }
     pdl_launch_dependents();
 }
@@ -307,25 +350,39 @@ __global__ void __launch_bounds__(NC + 32) k_tasks(const K* __restrict__ A, cons
         const int phV = HAS_V ? (int)(((uintptr_t)(vC + d.off) & 15) / 4) : 0;
 
         if (d.la > 0 && d.lb > 0) {
-            // cases (b), (c), (d): stable merge (row a7)
-            const int dg = min(c * VT, L);
-            const K* a = sk + d.a_s;
-            const K* b = sk + d.b_s;
-            const int ai = split_ab(a, d.la, b, d.lb, dg);
+            // cases (b), (c), (d): stable merge (row a7).  Only threads whose
+            // diagonal lies inside the task work (tasks average half a tile).
+            const int dg = c * VT;
+            const bool active = dg < L;
             K out[VT];
             int src[VT];
-            merge_serial<K, VT, HAS_V>(a, ai, d.la, b, dg - ai, d.lb, d.va_s, d.vb_s, out, src);
             uint32_t v[HAS_V ? VT : 1];
-            if (HAS_V) {
+            if (active) {
+                const K* a = sk + d.a_s;
+                const K* b = sk + d.b_s;
+                const int ai = split_ab(a, d.la, b, d.lb, dg);
+                merge_serial<K, VT, HAS_V>(a, ai, d.la, b, dg - ai, d.lb, d.va_s, d.vb_s, out, src);
+                if (HAS_V) {
 #pragma unroll
-                for (int k = 0; k < VT; ++k) v[k] = sv[min(src[k], Lay::VCAP - 1)];
+                    for (int k = 0; k < VT; ++k) v[k] = sv[min(src[k], Lay::VCAP - 1)];
+                }
             }
             named_sync(1, NC);
+            if (active) {
+                if (dg + VT <= L) {
 #pragma unroll
-            for (int k = 0; k < VT; ++k) {
-                if (dg + k < L) {
-                    sk[phC + dg + k] = out[k];
-                    if (HAS_V) sv[phV + dg + k] = v[k];
+                    for (int k = 0; k < VT; ++k) {
+                        sk[phC + dg + k] = out[k];
+                        if (HAS_V) sv[phV + dg + k] = v[k];
+                    }
+                } else {
+#pragma unroll
+                    for (int k = 0; k < VT; ++k) {
+                        if (dg + k < L) {
+                            sk[phC + dg + k] = out[k];
+                            if (HAS_V) sv[phV + dg + k] = v[k];
+                        }
+                    }
                 }
             }
         } else if (L > 0) {

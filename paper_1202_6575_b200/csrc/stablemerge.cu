@@ -34,6 +34,8 @@ constexpr int T_DEFAULT = NV / 2;  // block size: task bound 2T (L388-393)
 constexpr int NT = 128;
 constexpr int VT = 15;
 constexpr int R_SORT = NT * VT;
+// K1: lanes per cooperative rank search.
+constexpr int K1_G = 8;
 
 static sm_status fail_cuda(cudaError_t e, const char* what) {
     snprintf(g_err, sizeof(g_err), "%s: %s", what, cudaGetErrorString(e));
@@ -122,9 +124,9 @@ template <typename K, bool HAS_V>
 static sm_status launch_merge(const K* A, const uint32_t* vA, const K* B, const uint32_t* vB, K* C,
                               uint32_t* vC, const Geom& g, int* xbar, int* ybar, cudaStream_t st, bool pdl) {
     const long long items = (long long)g.S * (g.pA + g.pB + 2);
-    const long long blocks1 = (items + 255) / 256;
+    const long long blocks1 = (items * K1_G + 255) / 256;
     prof_before(PROF_K1, st);
-    k_cross_ranks<K><<<(unsigned)blocks1, 256, 0, st>>>(A, B, g, xbar, ybar);
+    k_cross_ranks<K, K1_G><<<(unsigned)blocks1, 256, 0, st>>>(A, B, g, xbar, ybar);
     prof_after(st);
     sm_status s = check_launch("k_cross_ranks");
     if (s != SM_OK) return s;
@@ -318,7 +320,7 @@ static sm_status plan_entry(const K* A, int64_t n, const K* B, int64_t m, int64_
     sm_status s = dalloc(&ranks, (pA + 1) + (pB + 1), st);
     if (s != SM_OK) return s;
     const long long items = pA + pB + 2;
-    k_cross_ranks<K><<<(unsigned)((items + 255) / 256), 256, 0, st>>>(A, B, g, ranks, ranks + pA + 1);
+    k_cross_ranks<K, K1_G><<<(unsigned)((items * K1_G + 255) / 256), 256, 0, st>>>(A, B, g, ranks, ranks + pA + 1);
     s = check_launch("k_cross_ranks");
     if (s == SM_OK) {
         k_widen<<<(unsigned)((pA + 1 + 255) / 256), 256, 0, st>>>(ranks, xbar, (int)(pA + 1));
