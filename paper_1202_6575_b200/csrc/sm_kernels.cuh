@@ -299,23 +299,25 @@ __global__ void __launch_bounds__(NC + 32) k_tasks(const K* __restrict__ A, cons
 
     if (threadIdx.x < 32) {
         // ------------------------------------------------------ producer
-        if (threadIdx.x == 0) {
-            int it = 0;
-            for (int task = blockIdx.x; task < ntasks; task += gridDim.x, ++it) {
-                const int s = it % STAGES;
-                if (it >= STAGES) mbar_wait(&empty[s], ((it / STAGES) - 1) & 1);
+        // The warp classifies the next 32 tasks of this CTA in parallel (one
+        // per lane: the dependent rank loads overlap), then hands them to the
+        // ring in order; the lane that owns a task issues its bulk loads.
+        const int lane = threadIdx.x;
+        for (int base = 0;; base += 32) {
+            const int my_task = blockIdx.x + (base + lane) * gridDim.x;
+            const bool have = my_task < ntasks;
+            if (!__any_sync(0xffffffffu, have)) break;
+            TaskDesc d;
+            Span sa, sb, sva, svb;
+            if (have) {
                 Seg sg;
-                const Task t = decode_task(g, task, xbar, ybar, sg);
-                char* stage = smem + s * Lay::STAGE_BYTES;
-                char* vstage = stage + Lay::KCAP * (int)sizeof(K);
-                TaskDesc d;
+                const Task t = decode_task(g, my_task, xbar, ybar, sg);
                 d.la = t.a1 - t.a0;
                 d.lb = t.b1 - t.b0;
                 d.off = sg.coff + t.a0 + t.b0;
                 int at = 0, vat = 0;
-                const Span sa = plan_range(at, A + sg.aoff + t.a0, d.la);
-                const Span sb = plan_range(at, B + sg.boff + t.b0, d.lb);
-                Span sva, svb;
+                sa = plan_range(at, A + sg.aoff + t.a0, d.la);
+                sb = plan_range(at, B + sg.boff + t.b0, d.lb);
                 sva.bytes = svb.bytes = 0;
                 sva.idx = svb.idx = 0;
                 if (HAS_V) {
@@ -323,14 +325,26 @@ __global__ void __launch_bounds__(NC + 32) k_tasks(const K* __restrict__ A, cons
                     svb = plan_range(vat, vB + sg.boff + t.b0, d.lb);
                 }
                 d.a_s = sa.idx; d.b_s = sb.idx; d.va_s = sva.idx; d.vb_s = svb.idx; d.pad = 0;
-                desc[s] = d;   // written before the arrive (release) below
-                mbar_arrive_expect_tx(&full[s], sa.bytes + sb.bytes + sva.bytes + svb.bytes);
-                issue_range(stage, sa, &full[s]);
-                issue_range(stage, sb, &full[s]);
-                if (HAS_V) {
-                    issue_range(vstage, sva, &full[s]);
-                    issue_range(vstage, svb, &full[s]);
+            }
+            const unsigned owners = __ballot_sync(0xffffffffu, have);
+            const int count = __popc(owners);        // tasks are a prefix of the lanes
+            for (int k = 0; k < count; ++k) {
+                const int it = base + k;
+                const int st = it % STAGES;
+                if (it >= STAGES) mbar_wait(&empty[st], ((it / STAGES) - 1) & 1);
+                if (lane == k) {
+                    char* stage = smem + st * Lay::STAGE_BYTES;
+                    char* vstage = stage + Lay::KCAP * (int)sizeof(K);
+                    desc[st] = d;   // written before the arrive (release) below
+                    mbar_arrive_expect_tx(&full[st], sa.bytes + sb.bytes + sva.bytes + svb.bytes);
+                    issue_range(stage, sa, &full[st]);
+                    issue_range(stage, sb, &full[st]);
+                    if (HAS_V) {
+                        issue_range(vstage, sva, &full[st]);
+                        issue_range(vstage, svb, &full[st]);
+                    }
                 }
+                __syncwarp();
             }
         }
         return;

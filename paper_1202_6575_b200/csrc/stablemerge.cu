@@ -27,7 +27,13 @@ thread_local int64_t g_launches = 0;
 // transposition free of bank conflicts for 4- and 8-byte keys.
 constexpr int K2_NC = 256;
 constexpr int K2_VT = 15;
-constexpr int K2_STAGES = 3;
+// Ring depth per element layout: enough bulk loads in flight per SM to cover
+// HBM latency within the shared-memory budget (228 KB per SM).
+template <typename K, bool HAS_V>
+struct K2Stages {
+    static constexpr int bytes = (int)sizeof(K) + (HAS_V ? 4 : 0);
+    static constexpr int value = bytes <= 4 ? 4 : (bytes <= 8 ? 3 : 4);
+};
 constexpr int NV = K2_NC * K2_VT;  // tile capacity: largest task
 constexpr int T_DEFAULT = NV / 2;  // block size: task bound 2T (L388-393)
 // K3 shape: one run of R = NT * VT elements per CTA.
@@ -131,8 +137,9 @@ static sm_status launch_merge(const K* A, const uint32_t* vA, const K* B, const 
     sm_status s = check_launch("k_cross_ranks");
     if (s != SM_OK) return s;
 
-    using Lay = K2Layout<K, HAS_V, K2_NC, K2_VT, K2_STAGES>;
-    auto kern = k_tasks<K, HAS_V, K2_NC, K2_VT, K2_STAGES>;
+    constexpr int STAGES = K2Stages<K, HAS_V>::value;
+    using Lay = K2Layout<K, HAS_V, K2_NC, K2_VT, STAGES>;
+    auto kern = k_tasks<K, HAS_V, K2_NC, K2_VT, STAGES>;
     static int per_sm = -1, n_sm = 0;
     if (per_sm < 0) {
         int dev = 0;
