@@ -237,3 +237,140 @@ __device__ __forceinline__ void named_sync(int id, int count) {
 }
 
 }  // namespace sm
+
+// ===========================================================================
+// Shared-memory merge primitives in inline PTX (rows a7, a8): branch-free,
+// predicated, on 32-bit shared-window addresses, one specialisation per key
+// type (signed compare for i32/i64, unsigned for u32/u64, reading R16).
+// ===========================================================================
+namespace sm {
+
+// One binary-lifting probe of the merge-path split (reading R17): with
+// sa = &a[i0], sb = &b[d-1-i0] and `rem` candidates left, if STEP <= rem and
+// a[i0+STEP-1] <= b[d-1-i0-STEP+1] then advance i0 by STEP.
+template <typename K, int STEP>
+__device__ __forceinline__ void lift_probe(uint32_t& sa, uint32_t& sb, int& rem);
+
+// One output of the serial stable merge: take A when A is not exhausted and
+// (B is exhausted or ka <= kb) -- ties to A.  Advances
+// the taken side and loads its next key (one past the end at most: the
+// stage holds slack there and the value is never selected).
+template <typename K>
+__device__ __forceinline__ void merge_step(uint32_t& pa, uint32_t& pb, K& ka, K& kb, uint32_t pae, uint32_t pbe,
+                                           K& out);
+// Same, also selecting the payload index (ia for A, ib for B).
+template <typename K>
+__device__ __forceinline__ void merge_step_idx(uint32_t& pa, uint32_t& pb, K& ka, K& kb, uint32_t pae,
+                                               uint32_t pbe, K& out, int& ia, int& ib, int& src);
+
+template <typename K>
+__device__ __forceinline__ K lds(uint32_t addr);
+
+#define SM_DEF_SMEM_OPS(K, CMP, BITS, RC, SZ)                                                                  \
+    template <int STEP>                                                                                        \
+    struct LiftProbe_##CMP {                                                                                   \
+        __device__ __forceinline__ static void run(uint32_t& sa, uint32_t& sb, int& rem) {                     \
+            asm volatile(                                                                                      \
+                "{\n\t.reg .pred p, q;\n\t.reg .b" BITS " x, y;\n\t"                                          \
+                "setp.le.s32 p, %3, %2;\n\t"                                                                   \
+                "@p ld.shared.b" BITS " x, [%0+%4];\n\t"                                                       \
+                "@p ld.shared.b" BITS " y, [%1+%5];\n\t"                                                       \
+                "setp.le.and." #CMP " q, x, y, p;\n\t"                                                          \
+                "@q add.u32 %0, %0, %6;\n\t"                                                                   \
+                "@q sub.u32 %1, %1, %6;\n\t"                                                                   \
+                "@q sub.s32 %2, %2, %3;\n\t}"                                                                  \
+                : "+r"(sa), "+r"(sb), "+r"(rem)                                                                \
+                : "n"(STEP), "n"((STEP - 1) * SZ), "n"(-(STEP - 1) * SZ), "n"(STEP * SZ)                     \
+                : "memory");                                                                                   \
+        }                                                                                                      \
+    };                                                                                                         \
+    template <>                                                                                                \
+    __device__ __forceinline__ K lds<K>(uint32_t addr) {                                                       \
+        K v;                                                                                                   \
+        asm volatile("ld.shared.b" BITS " %0, [%1];" : "=" RC(v) : "r"(addr) : "memory");                     \
+        return v;                                                                                              \
+    }                                                                                                          \
+    template <>                                                                                                \
+    __device__ __forceinline__ void merge_step<K>(uint32_t & pa, uint32_t & pb, K & ka, K & kb, uint32_t pae,  \
+                                                  uint32_t pbe, K & out) {                                     \
+        asm volatile(                                                                                          \
+            "{\n\t.reg .pred t;\n\t"                                                                           \
+            "setp.le." #CMP " t, %2, %3;\n\t"                                                                   \
+            "setp.lt.and.u32 t, %0, %5, t;\n\t"                                                                \
+            "setp.ge.or.u32 t, %1, %6, t;\n\t"                                                                 \
+            "selp.b" BITS " %4, %2, %3, t;\n\t"                                                                \
+            "@t add.u32 %0, %0, " #SZ ";\n\t"                                                                  \
+            "@!t add.u32 %1, %1, " #SZ ";\n\t"                                                                 \
+            "@t ld.shared.b" BITS " %2, [%0];\n\t"                                                             \
+            "@!t ld.shared.b" BITS " %3, [%1];\n\t}"                                                           \
+            : "+r"(pa), "+r"(pb), "+" RC(ka), "+" RC(kb), "=" RC(out)                                          \
+            : "r"(pae), "r"(pbe)                                                                               \
+            : "memory");                                                                                       \
+    }                                                                                                          \
+    template <>                                                                                                \
+    __device__ __forceinline__ void merge_step_idx<K>(uint32_t & pa, uint32_t & pb, K & ka, K & kb,            \
+                                                      uint32_t pae, uint32_t pbe, K & out, int& ia, int& ib,   \
+                                                      int& src) {                                              \
+        asm volatile(                                                                                          \
+            "{\n\t.reg .pred t;\n\t"                                                                           \
+            "setp.le." #CMP " t, %2, %3;\n\t"                                                                   \
+            "setp.lt.and.u32 t, %0, %8, t;\n\t"                                                                \
+            "setp.ge.or.u32 t, %1, %9, t;\n\t"                                                                 \
+            "selp.b" BITS " %4, %2, %3, t;\n\t"                                                                \
+            "selp.b32 %7, %5, %6, t;\n\t"                                                                      \
+            "@t add.u32 %0, %0, " #SZ ";\n\t"                                                                  \
+            "@!t add.u32 %1, %1, " #SZ ";\n\t"                                                                 \
+            "@t add.s32 %5, %5, 1;\n\t"                                                                        \
+            "@!t add.s32 %6, %6, 1;\n\t"                                                                       \
+            "@t ld.shared.b" BITS " %2, [%0];\n\t"                                                             \
+            "@!t ld.shared.b" BITS " %3, [%1];\n\t}"                                                           \
+            : "+r"(pa), "+r"(pb), "+" RC(ka), "+" RC(kb), "=" RC(out), "+r"(ia), "+r"(ib), "=r"(src)          \
+            : "r"(pae), "r"(pbe)                                                                               \
+            : "memory");                                                                                       \
+    }                                                                                                          \
+    template <int STEP>                                                                                        \
+    struct LiftSel<K, STEP> {                                                                                  \
+        using type = LiftProbe_##CMP<STEP>;                                                                    \
+    };
+
+template <typename K, int STEP>
+struct LiftSel;
+
+SM_DEF_SMEM_OPS(uint32_t, u32, "32", "r", 4)
+SM_DEF_SMEM_OPS(int32_t, s32, "32", "r", 4)
+SM_DEF_SMEM_OPS(uint64_t, u64, "64", "l", 8)
+SM_DEF_SMEM_OPS(int64_t, s64, "64", "l", 8)
+#undef SM_DEF_SMEM_OPS
+
+template <typename K, int STEP>
+__device__ __forceinline__ void lift_probe(uint32_t& sa, uint32_t& sb, int& rem) {
+    LiftSel<K, STEP>::type::run(sa, sb, rem);
+}
+
+// Merge-path split at diagonal d of sorted a[0, la) and b[0, lb) held in
+// shared memory at sa0 / sb0 (byte addresses): smallest i in
+// [max(0, d-lb), min(d, la)] with a[i] > b[d-1-i] (reading R17), by
+// LOG2+1 predicated probes (binary lifting; 2^(LOG2+1)-1 >= any range).
+template <typename K, int S>
+struct LiftAll {
+    __device__ __forceinline__ static void run(uint32_t& sa, uint32_t& sb, int& rem) {
+        lift_probe<K, (1 << S)>(sa, sb, rem);
+        LiftAll<K, S - 1>::run(sa, sb, rem);
+    }
+};
+template <typename K>
+struct LiftAll<K, -1> {
+    __device__ __forceinline__ static void run(uint32_t&, uint32_t&, int&) {}
+};
+
+template <typename K, int LOG2>
+__device__ __forceinline__ int split_smem(uint32_t sa0, int la, uint32_t sb0, int lb, int d) {
+    const int lo = max(0, d - lb);
+    int rem = min(d, la) - lo;
+    uint32_t sa = sa0 + (uint32_t)lo * sizeof(K);
+    uint32_t sb = sb0 + (uint32_t)(d - 1 - lo) * sizeof(K);
+    LiftAll<K, LOG2>::run(sa, sb, rem);
+    return (int)((sa - sa0) / sizeof(K));
+}
+
+}  // namespace sm

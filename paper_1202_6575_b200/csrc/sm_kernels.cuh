@@ -205,91 +205,173 @@ __device__ __forceinline__ void merge_serial(const K* a, int ai, int la, const K
     }
 }
 
-// Task descriptor handed from the producer warp to the consumers (smem).
+// Branch-free merge-path split (reading R17): smallest i in
+// [max(0, d-lb), min(d, la)] with a[i] > b[d-1-i], by binary lifting over
+// powers of two (LOG2 + 1 predicated probes, no data-dependent branch).
+// The predicate a[i] <= b[d-1-i] is monotone in i (true, then false).
+template <typename K, int LOG2>
+__device__ __forceinline__ int split_lift(const K* a, int la, const K* b, int lb, int d) {
+    const int lo = max(0, d - lb);
+    int rem = min(d, la) - lo;             // candidates left: a[lo .. lo+rem)
+    const K* pa = a + lo;                  // a[i]
+    const K* pb = b + (d - 1 - lo);        // b[d-1-i]
+#pragma unroll
+    for (int s = LOG2; s >= 0; --s) {
+        const int step = 1 << s;
+        if (step <= rem && pa[step - 1] <= pb[1 - step]) {
+            pa += step;
+            pb -= step;
+            rem -= step;
+        }
+    }
+    return (int)(pa - a);
+}
+
+// Serial stable merge of VT outputs starting at (ai, bi), la >= 1, lb >= 1:
+// take A when its key <= B's (ties to A).  Reads one element past the end
+// of a range at most (inside the stage, never selected).  With IDX, src[k]
+// is the stage payload index of output k (va + ai or vb + bi).
+template <typename K, int VT, bool IDX>
+__device__ __forceinline__ void merge_lean(const K* a, int ai, int la, const K* b, int bi, int lb, int va, int vb,
+                                           K (&out)[VT], int (&src)[VT]) {
+    const K* pa = a + ai;
+    const K* pb = b + bi;
+    const K* const pae = a + la;
+    const K* const pbe = b + lb;
+    int ia = va + ai, ib = vb + bi;
+    K ka = *pa, kb = *pb;
+#pragma unroll
+    for (int k = 0; k < VT; ++k) {
+        const bool takeA = pb >= pbe || (pa < pae && ka <= kb);
+        out[k] = takeA ? ka : kb;
+        if (IDX) src[k] = takeA ? ia : ib;
+        if (takeA) {
+            ++pa;
+            ka = *pa;
+            if (IDX) ++ia;
+        } else {
+            ++pb;
+            kb = *pb;
+            if (IDX) ++ib;
+        }
+    }
+}
+
+// ----------------------------------------------------------------- K2
+// A ring stage holds the input ranges of up to MAXT tasks ("packing"): the
+// paper's subproblems range from O(1) to ~2T elements (L388-393), so one task
+// per tile would leave half the consumer threads idle on average.  The
+// producer packs consecutive tasks of this CTA while their sizes, each
+// rounded up to VT, sum to at most NV = NC * VT; consumer thread c then owns
+// padded diagonal c * VT of the stage and finds its task by binary search.
 struct TaskDesc {
     int la, lb;        // lengths of the A and B ranges
-    int a_s, b_s;      // smem element index of A[a0] / B[b0] in the key region
-    int va_s, vb_s;    // smem element index of the payloads in the payload region
+    int a_s, b_s;      // stage key index of A[a0] / B[b0]
+    int va_s, vb_s;    // stage payload index of vA[a0] / vB[b0]
+    int ob, obv;       // stage index where output key / payload 0 of the task goes
     int off;           // global output element index (segment base + a0 + b0)
-    int pad;
+    int pst;           // first padded diagonal of the task in the stage
 };
 
-template <typename K, bool HAS_V, int NC, int VT, int STAGES>
+template <typename K, bool HAS_V, int NC, int VT, int STAGES, int MAXT>
 struct K2Layout {
-    static constexpr int NV = NC * VT;                    // tile capacity (max task)
-    static constexpr int KPAD = 16 / (int)sizeof(K);      // elements per 16 bytes
-    static constexpr int KCAP = ((NV + 4 * KPAD + KPAD - 1) / KPAD) * KPAD;
-    static constexpr int VCAP = HAS_V ? ((NV + 16 + 3) / 4) * 4 : 0;
-    static constexpr int STAGE_BYTES = KCAP * (int)sizeof(K) + VCAP * 4;
-    static constexpr int SMEM = STAGES * STAGE_BYTES + STAGES * (int)sizeof(TaskDesc) + 2 * STAGES * 8 + 16;
+    static constexpr int NV = NC * VT;                     // padded diagonals per stage
+    static constexpr int KB = (int)sizeof(K);
+    // Task k's key region: its A span and B span (16-byte aligned supersets,
+    // <= L*KB + 2*30 bytes) plus 16 bytes, so that its output, phase-aligned
+    // to the destination address, fits in the same region (written in place
+    // after every thread has read its inputs).
+    static constexpr int KREG = NV * KB + MAXT * 80;
+    static constexpr int VREG = HAS_V ? NV * 4 + MAXT * 80 : 0;
+    static constexpr int STAGE_BYTES = KREG + VREG;
+    static constexpr int OFF_DESC = STAGES * STAGE_BYTES;
+    static constexpr int OFF_PST = OFF_DESC + STAGES * MAXT * (int)sizeof(TaskDesc);
+    static constexpr int OFF_BAR = ((OFF_PST + STAGES * (MAXT + 2) * 4) + 15) & ~15;
+    static constexpr int SMEM = OFF_BAR + 3 * STAGES * 8;   // full, empty, written
 };
 
-// The 16-byte-aligned superset [g0, g0 + bytes) of src[0, len), to be
-// bulk-loaded at smem byte offset `at`; `idx` = smem element index of src[0].
-struct Span {
-    uintptr_t g0;
-    uint32_t bytes;
-    int at, idx;
-};
-
+// Bytes of the 16-byte-aligned superset of p[0, len).
 template <typename T>
-__device__ __forceinline__ Span plan_range(int& at, const T* src, int len) {
-    Span sp;
-    const uintptr_t g = (uintptr_t)src;
-    sp.g0 = g & ~(uintptr_t)15;
-    sp.bytes = len > 0 ? (uint32_t)(((g + (uintptr_t)len * sizeof(T) + 15) & ~(uintptr_t)15) - sp.g0) : 0u;
-    sp.at = at;
-    sp.idx = (at + (int)(g - sp.g0)) / (int)sizeof(T);
-    at += (int)sp.bytes;
-    return sp;
+__device__ __forceinline__ int span_bytes(const T* p, int len) {
+    if (len <= 0) return 0;
+    const uintptr_t g = (uintptr_t)p;
+    return (int)(((g + (uintptr_t)len * sizeof(T) + 15) & ~(uintptr_t)15) - (g & ~(uintptr_t)15));
 }
 
-__device__ __forceinline__ void issue_range(char* base, const Span& sp, uint64_t* bar) {
-    if (sp.bytes) bulk_g2s(base + sp.at, (const void*)sp.g0, sp.bytes, bar);
+// Bulk-load the aligned superset of p[0, len) to smem byte `at` of `base`;
+// returns the stage element index of p[0].
+template <typename T>
+__device__ __forceinline__ int issue_span(char* base, int at, const T* p, int len, uint64_t* bar) {
+    const uintptr_t g = (uintptr_t)p;
+    const uintptr_t g0 = g & ~(uintptr_t)15;
+    if (len > 0) bulk_g2s(base + at, (const void*)g0, (uint32_t)span_bytes(p, len), bar);
+    return (at + (int)(g - g0)) / (int)sizeof(T);
 }
 
-// Store smem sbuf[ph, ph+L) (already in output order) to dst[0, L): the
-// 16-byte-aligned middle with one bulk copy issued by consumer 0, the
-// <= 2*(16/sizeof(T)-1) edge elements with plain stores by consumers
-// edge0 .. edge0+5.
 template <typename T>
-__device__ __forceinline__ void store_range(T* dst, const T* sbuf, int ph, int L, int c, int edge0) {
+__device__ __forceinline__ int phase_of(const T* p) {
+    return (int)(((uintptr_t)p & 15) / sizeof(T));
+}
+
+// Store stage elements sbuf[o, o+L) to dst[0, L): the 16-byte-aligned middle
+// with one bulk copy (issued by the calling thread).
+template <typename T>
+__device__ __forceinline__ void store_middle(T* dst, const T* sbuf, int o, int L) {
+    const uintptr_t g = (uintptr_t)dst;
+    const uintptr_t gl = (g + 15) & ~(uintptr_t)15;
+    const uintptr_t gh = (g + (uintptr_t)L * sizeof(T)) & ~(uintptr_t)15;
+    if (gh > gl) bulk_s2g((void*)gl, sbuf + o + (int)((gl - g) / sizeof(T)), (uint32_t)(gh - gl));
+}
+
+// Edge element r (0 <= r < 2*(16/sizeof(T)-1)) of the store above: the
+// elements before the first and after the last 16-byte boundary.
+template <typename T>
+__device__ __forceinline__ void store_edge(T* dst, const T* sbuf, int o, int L, int r) {
     const uintptr_t g = (uintptr_t)dst;
     const uintptr_t gl = (g + 15) & ~(uintptr_t)15;
     const uintptr_t gh = (g + (uintptr_t)L * sizeof(T)) & ~(uintptr_t)15;
     int head = (int)((gl - g) / sizeof(T));
     if (head > L) head = L;
     const int tail0 = gh > gl ? (int)((gh - g) / sizeof(T)) : head;
-    if (c == 0) {
-        if (gh > gl) bulk_s2g((void*)gl, sbuf + ph + head, (uint32_t)(gh - gl));
-    } else {
-        const int e = c - edge0;
-        if (e >= 0 && e < head) dst[e] = sbuf[ph + e];
-        else if (e >= head && e - head < L - tail0) dst[tail0 + e - head] = sbuf[ph + tail0 + e - head];
-    }
+    const int e = r < head ? r : tail0 + (r - head);
+    if (e < L && (r < head || e >= tail0)) dst[e] = sbuf[o + e];
 }
 
-// K2 (rows a4-a7): persistent, warp-specialised.  Warp 0 lane 0 is the
-// producer: it classifies task t (O(1), L310-340), and bulk-loads the task's
-// A and B ranges (keys, payloads) into a STAGES-deep shared-memory ring with
-// the TMA engine.  NC consumer threads merge (cases b, c, d) or realign
-// (copies, cases a, e) each task and write it back with bulk stores.
-template <typename K, bool HAS_V, int NC, int VT, int STAGES>
-__global__ void __launch_bounds__(NC + 32) k_tasks(const K* __restrict__ A, const uint32_t* __restrict__ vA,
+// K2 (rows a4-a7): persistent, warp-specialised.
+//   warp 0 (producer): its lanes classify a window of up to 32 tasks of this
+//     CTA in parallel (O(1) each, L310-340), pack a prefix of the window into
+//     the next ring stage and bulk-load every packed task's A and B ranges
+//     (keys, payloads) with the TMA engine (full[s]).
+//   warps 2.. (NC consumers): merge (cases b, c, d) or realign (copies,
+//     cases a, e) their VT diagonals into registers and write them back in
+//     place, phase-aligned to the destination (written[s]).
+//   warp 1 (storer): bulk-stores each task's 16-byte-aligned middle, plain
+//     stores for the edge elements, and frees the stage as soon as the bulk
+//     stores have read it (empty[s]), so consumers never wait on the stores.
+template <typename K, bool HAS_V, int NC, int VT, int STAGES, int MAXT>
+__global__ void __launch_bounds__(NC + 64) k_tasks(const K* __restrict__ A, const uint32_t* __restrict__ vA,
                                                    const K* __restrict__ B, const uint32_t* __restrict__ vB,
                                                    K* __restrict__ C, uint32_t* __restrict__ vC, Geom g,
                                                    const int* __restrict__ xbar, const int* __restrict__ ybar) {
-    using Lay = K2Layout<K, HAS_V, NC, VT, STAGES>;
+    using Lay = K2Layout<K, HAS_V, NC, VT, STAGES, MAXT>;
+    static_assert(NC % 32 == 0 && MAXT <= 32, "warp-granular roles; one producer lane per packed task");
+    constexpr int NV = Lay::NV;
+    constexpr int LOG2NV = 31 - __builtin_clz(NV);   // 2^(LOG2NV+1) - 1 >= NV probes cover any range
+    constexpr int KB = Lay::KB;
+    constexpr int EPV = 16 / KB;
     extern __shared__ __align__(128) char smem[];
-    TaskDesc* desc = (TaskDesc*)(smem + STAGES * Lay::STAGE_BYTES);
-    uint64_t* full = (uint64_t*)(desc + STAGES);
+    TaskDesc* desc = (TaskDesc*)(smem + Lay::OFF_DESC);
+    int* pst = (int*)(smem + Lay::OFF_PST);              // [STAGES][MAXT + 2]: pst[0..nt], nt at MAXT+1
+    uint64_t* full = (uint64_t*)(smem + Lay::OFF_BAR);
     uint64_t* empty = full + STAGES;
+    uint64_t* written = empty + STAGES;
     const int ntasks = g.S * (g.pA + g.pB);
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
+            mbar_init(&written[s], NC / 32);
         }
         fence_barrier_init();
         fence_proxy_async();
@@ -299,146 +381,231 @@ __global__ void __launch_bounds__(NC + 32) k_tasks(const K* __restrict__ A, cons
 
     if (threadIdx.x < 32) {
         // ------------------------------------------------------ producer
-        // The warp classifies the next 32 tasks of this CTA in parallel (one
-        // per lane: the dependent rank loads overlap), then hands them to the
-        // ring in order; the lane that owns a task issues its bulk loads.
         const int lane = threadIdx.x;
-        for (int base = 0;; base += 32) {
-            const int my_task = blockIdx.x + (base + lane) * gridDim.x;
-            const bool have = my_task < ntasks;
-            if (!__any_sync(0xffffffffu, have)) break;
-            TaskDesc d;
-            Span sa, sb, sva, svb;
-            if (have) {
-                Seg sg;
-                const Task t = decode_task(g, my_task, xbar, ybar, sg);
-                d.la = t.a1 - t.a0;
-                d.lb = t.b1 - t.b0;
-                d.off = sg.coff + t.a0 + t.b0;
-                int at = 0, vat = 0;
-                sa = plan_range(at, A + sg.aoff + t.a0, d.la);
-                sb = plan_range(at, B + sg.boff + t.b0, d.lb);
-                sva.bytes = svb.bytes = 0;
-                sva.idx = svb.idx = 0;
+        int la = 0, lb = 0, off = 0, ag = 0, bg = 0;   // window slot `lane`
+        int cnt = 0;                                    // slots [0, cnt) hold tasks
+        int next = blockIdx.x;                          // next task of this CTA
+        int it = 0;
+        for (;;) {
+            if (cnt < MAXT && next < ntasks) {
+                const int my = next + (lane - cnt) * (int)gridDim.x;
+                const bool fill = lane >= cnt && my < ntasks;
+                if (fill) {
+                    Seg sg;
+                    const Task t = decode_task(g, my, xbar, ybar, sg);
+                    la = t.a1 - t.a0;
+                    lb = t.b1 - t.b0;
+                    off = sg.coff + t.a0 + t.b0;
+                    ag = sg.aoff + t.a0;
+                    bg = sg.boff + t.b0;
+                }
+                next += (32 - cnt) * (int)gridDim.x;
+                cnt += __popc(__ballot_sync(0xffffffffu, fill));
+            }
+            const int st = it % STAGES;
+            if (it >= STAGES) mbar_wait(&empty[st], ((it / STAGES) - 1) & 1);
+            int* ps = pst + st * (MAXT + 2);
+            if (cnt == 0) {                             // no task left: terminate the consumers
+                if (lane == 0) {
+                    ps[MAXT + 1] = -1;
+                    mbar_arrive(&full[st]);
+                }
+                break;
+            }
+            // pack the longest prefix of the window with sum of padded sizes <= NV
+            const int L = la + lb;
+            const int P = lane < cnt ? ((L + VT - 1) / VT) * VT : NV + 1;
+            int incl = P;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int t = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += t;
+            }
+            const bool take_me = lane < cnt && lane < MAXT && incl <= NV;
+            const int take = __popc(__ballot_sync(0xffffffffu, take_me));
+            // stage byte offsets of each packed task's key / payload region
+            const int kreg = take_me ? span_bytes(A + ag, la) + span_bytes(B + bg, lb) + 16 : 0;
+            const int vreg = (HAS_V && take_me) ? span_bytes(vA + ag, la) + span_bytes(vB + bg, lb) + 16 : 0;
+            int kat = kreg, vat = vreg;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int t1 = __shfl_up_sync(0xffffffffu, kat, o);
+                const int t2 = __shfl_up_sync(0xffffffffu, vat, o);
+                if (lane >= o) { kat += t1; vat += t2; }
+            }
+            kat -= kreg;                                 // exclusive
+            vat -= vreg;
+            const int ktot = __shfl_sync(0xffffffffu, kat + kreg, take - 1);
+            const int vtot = __shfl_sync(0xffffffffu, vat + vreg, take - 1);
+            char* stage = smem + st * Lay::STAGE_BYTES;
+            char* vstage = stage + Lay::KREG;
+            if (take_me) {
+                TaskDesc d;
+                d.la = la;
+                d.lb = lb;
+                d.off = off;
+                d.pst = incl - P;
+                d.a_s = issue_span(stage, kat, A + ag, la, &full[st]);
+                d.b_s = issue_span(stage, kat + span_bytes(A + ag, la), B + bg, lb, &full[st]);
+                // output position: in place for a copy whose source already has the
+                // destination's 16-byte phase, else phase-aligned at the region start
+                const int phC = phase_of(C + off);
+                if (lb == 0 && (d.a_s & (EPV - 1)) == phC) d.ob = d.a_s;
+                else if (la == 0 && (d.b_s & (EPV - 1)) == phC) d.ob = d.b_s;
+                else d.ob = kat / KB + phC;
+                d.va_s = d.vb_s = d.obv = 0;
                 if (HAS_V) {
-                    sva = plan_range(vat, vA + sg.aoff + t.a0, d.la);
-                    svb = plan_range(vat, vB + sg.boff + t.b0, d.lb);
+                    d.va_s = issue_span(vstage, vat, vA + ag, la, &full[st]);
+                    d.vb_s = issue_span(vstage, vat + span_bytes(vA + ag, la), vB + bg, lb, &full[st]);
+                    const int phV = phase_of(vC + off);
+                    if (lb == 0 && (d.va_s & 3) == phV) d.obv = d.va_s;
+                    else if (la == 0 && (d.vb_s & 3) == phV) d.obv = d.vb_s;
+                    else d.obv = vat / 4 + phV;
                 }
-                d.a_s = sa.idx; d.b_s = sb.idx; d.va_s = sva.idx; d.vb_s = svb.idx; d.pad = 0;
-            }
-            const unsigned owners = __ballot_sync(0xffffffffu, have);
-            const int count = __popc(owners);        // tasks are a prefix of the lanes
-            for (int k = 0; k < count; ++k) {
-                const int it = base + k;
-                const int st = it % STAGES;
-                if (it >= STAGES) mbar_wait(&empty[st], ((it / STAGES) - 1) & 1);
-                if (lane == k) {
-                    char* stage = smem + st * Lay::STAGE_BYTES;
-                    char* vstage = stage + Lay::KCAP * (int)sizeof(K);
-                    desc[st] = d;   // written before the arrive (release) below
-                    mbar_arrive_expect_tx(&full[st], sa.bytes + sb.bytes + sva.bytes + svb.bytes);
-                    issue_range(stage, sa, &full[st]);
-                    issue_range(stage, sb, &full[st]);
-                    if (HAS_V) {
-                        issue_range(vstage, sva, &full[st]);
-                        issue_range(vstage, svb, &full[st]);
-                    }
+                desc[st * MAXT + lane] = d;
+                if (lane == take - 1) {
+                    ps[take] = incl;
+                    ps[MAXT + 1] = take;
                 }
-                __syncwarp();
+                ps[lane] = incl - P;
             }
+            // the descriptors are released by the arrive; the bulk loads may
+            // complete_tx before the expect_tx (the phase needs both)
+            __syncwarp();
+            if (lane == 0)
+                mbar_arrive_expect_tx(&full[st], (uint32_t)(ktot - 16 * take + (HAS_V ? vtot - 16 * take : 0)));
+            // drop the packed prefix from the window
+            la = __shfl_down_sync(0xffffffffu, la, take);
+            lb = __shfl_down_sync(0xffffffffu, lb, take);
+            off = __shfl_down_sync(0xffffffffu, off, take);
+            ag = __shfl_down_sync(0xffffffffu, ag, take);
+            bg = __shfl_down_sync(0xffffffffu, bg, take);
+            cnt -= take;
+            ++it;
+        }
+        return;
+    }
+
+    if (threadIdx.x < 64) {
+        // -------------------------------------------------------- storer
+        const int lane = threadIdx.x - 32;
+        constexpr int EK = 2 * (EPV - 1);              // key edge elements per task
+        constexpr int EV = HAS_V ? 6 : 0;              // payload edge elements per task
+        for (int it = 0;; ++it) {
+            const int s = it % STAGES;
+            mbar_wait(&written[s], (it / STAGES) & 1);
+            const int nt = pst[s * (MAXT + 2) + MAXT + 1];
+            if (nt < 0) break;
+            const K* sk = (const K*)(smem + s * Lay::STAGE_BYTES);
+            const uint32_t* sv = (const uint32_t*)(smem + s * Lay::STAGE_BYTES + Lay::KREG);
+            if (lane < nt) {
+                const TaskDesc& t = desc[s * MAXT + lane];
+                const int L = t.la + t.lb;
+                if (L > 0) {
+                    store_middle<K>(C + t.off, sk, t.ob, L);
+                    if (HAS_V) store_middle<uint32_t>(vC + t.off, sv, t.obv, L);
+                }
+                bulk_commit();
+            }
+            for (int e = lane; e < nt * (EK + EV); e += 32) {
+                const int k = e / (EK + EV), r = e % (EK + EV);
+                const TaskDesc& t = desc[s * MAXT + k];
+                const int L = t.la + t.lb;
+                if (r < EK) store_edge<K>(C + t.off, sk, t.ob, L, r);
+                else if (HAS_V) store_edge<uint32_t>(vC + t.off, sv, t.obv, L, r - EK);
+            }
+            bulk_wait_read<0>();                       // this lane's bulk stores have read the stage
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[s]);
         }
         return;
     }
 
     // ---------------------------------------------------------- consumers
-    const int c = threadIdx.x - 32;
-    int it = 0;
-    for (int task = blockIdx.x; task < ntasks; task += gridDim.x, ++it) {
+    const int c = threadIdx.x - 64;
+    const int lane = threadIdx.x & 31;
+    for (int it = 0;; ++it) {
         const int s = it % STAGES;
         mbar_wait(&full[s], (it / STAGES) & 1);
-        const TaskDesc d = desc[s];
+        const int* ps = pst + s * (MAXT + 2);
+        const int nt = ps[MAXT + 1];
+        if (nt < 0) {
+            if (lane == 0) mbar_arrive(&written[s]);   // pass the termination on to the storer
+            break;
+        }
         K* sk = (K*)(smem + s * Lay::STAGE_BYTES);
-        uint32_t* sv = (uint32_t*)(smem + s * Lay::STAGE_BYTES + Lay::KCAP * (int)sizeof(K));
-        const int L = d.la + d.lb;
-        const int phC = (int)(((uintptr_t)(C + d.off) & 15) / sizeof(K));
-        const int phV = HAS_V ? (int)(((uintptr_t)(vC + d.off) & 15) / 4) : 0;
-
-        if (d.la > 0 && d.lb > 0) {
-            // cases (b), (c), (d): stable merge (row a7).  Only threads whose
-            // diagonal lies inside the task work (tasks average half a tile).
-            const int dg = c * VT;
-            const bool active = dg < L;
-            K out[VT];
-            int src[VT];
-            uint32_t v[HAS_V ? VT : 1];
-            if (active) {
-                const K* a = sk + d.a_s;
-                const K* b = sk + d.b_s;
-                const int ai = split_ab(a, d.la, b, d.lb, dg);
-                merge_serial<K, VT, HAS_V>(a, ai, d.la, b, dg - ai, d.lb, d.va_s, d.vb_s, out, src);
-                if (HAS_V) {
-#pragma unroll
-                    for (int k = 0; k < VT; ++k) v[k] = sv[min(src[k], Lay::VCAP - 1)];
-                }
+        uint32_t* sv = (uint32_t*)(smem + s * Lay::STAGE_BYTES + Lay::KREG);
+        const int D = c * VT;
+        TaskDesc td;
+        int d = 0, cntk = 0;
+        K out[VT];
+        uint32_t v[HAS_V ? VT : 1];
+        bool write = false;
+        if (D < ps[nt]) {
+            int lo = 0, hi = nt - 1;                   // task k: last with pst[k] <= D
+            while (lo < hi) {
+                const int mid = (lo + hi + 1) >> 1;
+                if (ps[mid] <= D) lo = mid;
+                else hi = mid - 1;
             }
-            named_sync(1, NC);
-            if (active) {
-                if (dg + VT <= L) {
+            td = desc[s * MAXT + lo];
+            d = D - td.pst;
+            const int L = td.la + td.lb;
+            cntk = min(VT, L - d);
+            if (cntk > 0) {
+                if (td.la > 0 && td.lb > 0) {
+                    // cases (b), (c), (d): stable merge (row a7), ties to A (R17)
+                    const uint32_t sa0 = smem_addr(sk + td.a_s);
+                    const uint32_t sb0 = smem_addr(sk + td.b_s);
+                    const int ai = split_smem<K, LOG2NV>(sa0, td.la, sb0, td.lb, d);
+                    const int bi = d - ai;
+                    uint32_t pa = sa0 + ai * KB, pb = sb0 + bi * KB;
+                    const uint32_t pae = sa0 + td.la * KB, pbe = sb0 + td.lb * KB;
+                    K ka = lds<K>(pa), kb = lds<K>(pb);
+                    int src[VT];
+                    int ia = td.va_s + ai, ib = td.vb_s + bi;
 #pragma unroll
                     for (int k = 0; k < VT; ++k) {
-                        sk[phC + dg + k] = out[k];
-                        if (HAS_V) sv[phV + dg + k] = v[k];
+                        if (HAS_V) merge_step_idx<K>(pa, pb, ka, kb, pae, pbe, out[k], ia, ib, src[k]);
+                        else merge_step<K>(pa, pb, ka, kb, pae, pbe, out[k]);
                     }
+                    if (HAS_V) {
+#pragma unroll
+                        for (int k = 0; k < VT; ++k)
+                            if (k < cntk) v[k] = sv[src[k]];
+                    }
+                    write = true;
                 } else {
+                    // cases (a), (e): copy (row a6); realign unless already in place
+                    const int ks = td.la ? td.a_s : td.b_s;
+                    const int vs = td.la ? td.va_s : td.vb_s;
+                    if (ks != td.ob || (HAS_V && vs != td.obv)) {
 #pragma unroll
-                    for (int k = 0; k < VT; ++k) {
-                        if (dg + k < L) {
-                            sk[phC + dg + k] = out[k];
-                            if (HAS_V) sv[phV + dg + k] = v[k];
+                        for (int k = 0; k < VT; ++k) {
+                            if (k < cntk) {
+                                out[k] = sk[ks + d + k];
+                                if (HAS_V) v[k] = sv[vs + d + k];
+                            }
                         }
-                    }
-                }
-            }
-        } else if (L > 0) {
-            // cases (a), (e): copy (row a6) -- realign to the output phase
-            const int ks = d.la ? d.a_s : d.b_s;
-            const int vs = d.la ? d.va_s : d.vb_s;
-            const bool mv = ks != phC || (HAS_V && vs != phV);
-            if (mv) {
-                K r[VT];
-                uint32_t rv[HAS_V ? VT : 1];
-#pragma unroll
-                for (int k = 0; k < VT; ++k) {
-                    const int t = k * NC + c;
-                    if (t < L) {
-                        r[k] = sk[ks + t];
-                        if (HAS_V) rv[k] = sv[vs + t];
-                    }
-                }
-                named_sync(1, NC);
-#pragma unroll
-                for (int k = 0; k < VT; ++k) {
-                    const int t = k * NC + c;
-                    if (t < L) {
-                        sk[phC + t] = r[k];
-                        if (HAS_V) sv[phV + t] = rv[k];
+                        write = true;
                     }
                 }
             }
         }
-        fence_proxy_async();
-        named_sync(1, NC);
-        if (L > 0) {
-            store_range<K>(C + d.off, sk, phC, L, c, 1);
-            if (HAS_V) store_range<uint32_t>(vC + d.off, sv, phV, L, c, 32);
+        named_sync(1, NC);                             // every input of the stage has been read
+        if (write) {
+#pragma unroll
+            for (int k = 0; k < VT; ++k) {
+                if (k < cntk) {
+                    sk[td.ob + d + k] = out[k];
+                    if (HAS_V) sv[td.obv + d + k] = v[k];
+                }
+            }
         }
-        if (c == 0) {
-            bulk_commit();
-            bulk_wait_read<1>();                 // task it-1's stores have read their stage
-            if (it >= 1) mbar_arrive(&empty[(it - 1) % STAGES]);
-        }
+        fence_proxy_async();                           // generic writes -> the storer's bulk reads
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&written[s]);
     }
-    if (c == 0) bulk_wait_read<0>();
 }
 
 // ----------------------------------------------------------- plan dump

@@ -28,12 +28,16 @@ thread_local int64_t g_launches = 0;
 constexpr int K2_NC = 256;
 constexpr int K2_VT = 15;
 // Ring depth per element layout: enough bulk loads in flight per SM to cover
-// HBM latency within the shared-memory budget (228 KB per SM).
+// HBM latency within the shared-memory budget (228 KB per SM): 4-byte
+// elements 4 x 16.6 KB (3 CTAs/SM), 8-byte 3 x 33 KB (2 CTAs/SM), 12-byte
+// 4 x 49 KB (1 CTA/SM).
 template <typename K, bool HAS_V>
 struct K2Stages {
     static constexpr int bytes = (int)sizeof(K) + (HAS_V ? 4 : 0);
     static constexpr int value = bytes <= 4 ? 4 : (bytes <= 8 ? 3 : 4);
 };
+// Tasks packed per ring stage at most.
+constexpr int K2_MAXT = 16;
 constexpr int NV = K2_NC * K2_VT;  // tile capacity: largest task
 constexpr int T_DEFAULT = NV / 2;  // block size: task bound 2T (L388-393)
 // K3 shape: one run of R = NT * VT elements per CTA.
@@ -138,8 +142,8 @@ static sm_status launch_merge(const K* A, const uint32_t* vA, const K* B, const 
     if (s != SM_OK) return s;
 
     constexpr int STAGES = K2Stages<K, HAS_V>::value;
-    using Lay = K2Layout<K, HAS_V, K2_NC, K2_VT, STAGES>;
-    auto kern = k_tasks<K, HAS_V, K2_NC, K2_VT, STAGES>;
+    using Lay = K2Layout<K, HAS_V, K2_NC, K2_VT, STAGES, K2_MAXT>;
+    auto kern = k_tasks<K, HAS_V, K2_NC, K2_VT, STAGES, K2_MAXT>;
     static int per_sm = -1, n_sm = 0;
     if (per_sm < 0) {
         int dev = 0;
@@ -147,7 +151,7 @@ static sm_status launch_merge(const K* A, const uint32_t* vA, const K* B, const 
         cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Lay::SMEM);
         cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, K2_NC + 32, Lay::SMEM);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, K2_NC + 64, Lay::SMEM);
         if (per_sm < 1) per_sm = 1;
     }
     const long long ntasks = (long long)g.S * (g.pA + g.pB);
@@ -155,7 +159,7 @@ static sm_status launch_merge(const K* A, const uint32_t* vA, const K* B, const 
     cudaLaunchConfig_t cfg;
     memset(&cfg, 0, sizeof(cfg));
     cfg.gridDim = dim3((unsigned)grid);
-    cfg.blockDim = dim3(K2_NC + 32);
+    cfg.blockDim = dim3(K2_NC + 64);
     cfg.dynamicSmemBytes = Lay::SMEM;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
