@@ -293,16 +293,20 @@ __device__ __forceinline__ K lds(uint32_t addr);
     template <>                                                                                                \
     __device__ __forceinline__ void merge_step<K>(uint32_t & pa, uint32_t & pb, K & ka, K & kb, uint32_t pae,  \
                                                   uint32_t pbe, K & out) {                                     \
+        /* one shared load per step (from the side just taken): half the */                                  \
+        /* shared-memory wavefronts of a load per side */                                                     \
         asm volatile(                                                                                          \
-            "{\n\t.reg .pred t;\n\t"                                                                           \
-            "setp.le." #CMP " t, %2, %3;\n\t"                                                                   \
+            "{\n\t.reg .pred t;\n\t.reg .b32 ad;\n\t.reg .b" BITS " k;\n\t"                                   \
+            "setp.le." #CMP " t, %2, %3;\n\t"                                                                  \
             "setp.lt.and.u32 t, %0, %5, t;\n\t"                                                                \
             "setp.ge.or.u32 t, %1, %6, t;\n\t"                                                                 \
             "selp.b" BITS " %4, %2, %3, t;\n\t"                                                                \
             "@t add.u32 %0, %0, " #SZ ";\n\t"                                                                  \
             "@!t add.u32 %1, %1, " #SZ ";\n\t"                                                                 \
-            "@t ld.shared.b" BITS " %2, [%0];\n\t"                                                             \
-            "@!t ld.shared.b" BITS " %3, [%1];\n\t}"                                                           \
+            "selp.b32 ad, %0, %1, t;\n\t"                                                                      \
+            "ld.shared.b" BITS " k, [ad];\n\t"                                                                 \
+            "selp.b" BITS " %2, k, %2, t;\n\t"                                                                 \
+            "selp.b" BITS " %3, %3, k, t;\n\t}"                                                                \
             : "+r"(pa), "+r"(pb), "+" RC(ka), "+" RC(kb), "=" RC(out)                                          \
             : "r"(pae), "r"(pbe)                                                                               \
             : "memory");                                                                                       \
@@ -312,8 +316,8 @@ __device__ __forceinline__ K lds(uint32_t addr);
                                                       uint32_t pae, uint32_t pbe, K & out, int& ia, int& ib,   \
                                                       int& src) {                                              \
         asm volatile(                                                                                          \
-            "{\n\t.reg .pred t;\n\t"                                                                           \
-            "setp.le." #CMP " t, %2, %3;\n\t"                                                                   \
+            "{\n\t.reg .pred t;\n\t.reg .b32 ad;\n\t.reg .b" BITS " k;\n\t"                                   \
+            "setp.le." #CMP " t, %2, %3;\n\t"                                                                  \
             "setp.lt.and.u32 t, %0, %8, t;\n\t"                                                                \
             "setp.ge.or.u32 t, %1, %9, t;\n\t"                                                                 \
             "selp.b" BITS " %4, %2, %3, t;\n\t"                                                                \
@@ -322,8 +326,10 @@ __device__ __forceinline__ K lds(uint32_t addr);
             "@!t add.u32 %1, %1, " #SZ ";\n\t"                                                                 \
             "@t add.s32 %5, %5, 1;\n\t"                                                                        \
             "@!t add.s32 %6, %6, 1;\n\t"                                                                       \
-            "@t ld.shared.b" BITS " %2, [%0];\n\t"                                                             \
-            "@!t ld.shared.b" BITS " %3, [%1];\n\t}"                                                           \
+            "selp.b32 ad, %0, %1, t;\n\t"                                                                      \
+            "ld.shared.b" BITS " k, [ad];\n\t"                                                                 \
+            "selp.b" BITS " %2, k, %2, t;\n\t"                                                                 \
+            "selp.b" BITS " %3, %3, k, t;\n\t}"                                                                \
             : "+r"(pa), "+r"(pb), "+" RC(ka), "+" RC(kb), "=" RC(out), "+r"(ia), "+r"(ib), "=r"(src)          \
             : "r"(pae), "r"(pbe)                                                                               \
             : "memory");                                                                                       \

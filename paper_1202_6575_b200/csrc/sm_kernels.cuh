@@ -20,37 +20,47 @@ namespace sm {
 
 // ----------------------------------------------------------------- K1
 // Rows a1/a2.  A group of G lanes performs one rank search cooperatively:
-// each round the G lanes probe G evenly spaced keys of the remaining
-// interval and a group ballot picks the sub-interval holding the rank, so a
-// search over len keys takes ~log_{G+1}(len) dependent memory rounds instead
-// of log_2(len) (the latency chain is what bounds this kernel).
+// each round the probing lanes read evenly spaced keys of the remaining
+// interval and a group ballot picks the sub-interval holding the rank.
+// While the interval is longer than `wide_above` all G lanes probe (log_{G+1}
+// rounds): those top levels are shared by many searches and hit L2.  Below
+// it every search's probes are private DRAM accesses, so only GT lanes probe
+// (GT = 1: plain binary search), trading a few dependent rounds for several
+// times less DRAM traffic (one 32-byte sector per probe).
 //   HIGH = false: rank_low(x, X)  = #{X[t] <  x}   (L119-123)
 //   HIGH = true:  rank_high(x, X) = #{X[t] <= x}   (L124-128)
-template <typename K, int G>
-__device__ __forceinline__ int group_rank(const K* __restrict__ X, int len, K x, bool high, bool active) {
+template <int GG>
+__device__ __forceinline__ int probe_pos(int lo, int n, int s) {
+    return lo + (int)(((long long)(s + 1) * n) / (GG + 1));
+}
+
+template <typename K, int G, int GT>
+__device__ __forceinline__ int group_rank(const K* __restrict__ X, int len, K x, bool high, bool active,
+                                          int wide_above) {
     const int lane = threadIdx.x & 31;
     const int sub = lane % G;
     const int shift = lane - sub;
     int lo = 0, hi = active ? len : 0;     // rank in [lo, hi]; X[lo, hi) undecided
     while (__any_sync(0xffffffffu, hi > lo)) {
         const int n = hi - lo;
-        int pos;
-        if (n <= G) pos = lo + sub;                                   // last round: probe all
-        else pos = lo + (int)(((long long)(sub + 1) * n) / (G + 1));  // G interior probes
+        const bool wide = n > wide_above;
+        const int gg = wide ? G : GT;       // probing lanes this round
+        int pos = lo + sub;                 // n <= gg: probe every remaining key
+        if (n > gg) pos = wide ? probe_pos<G>(lo, n, sub) : probe_pos<GT>(lo, n, sub);
         bool pred = false;
-        if (hi > lo && (n > G || sub < n)) {
+        if (hi > lo && sub < min(gg, n)) {
             const K v = __ldg(X + pos);
             pred = high ? (v <= x) : (v < x);
         }
         const unsigned bal = (__ballot_sync(0xffffffffu, pred) >> shift) & ((1u << G) - 1u);
-        const int t = __popc(bal);   // probes passed: a prefix of the group
+        const int t = __popc(bal);          // probes passed: a prefix of the probing lanes
         if (hi > lo) {
-            if (n <= G) {
+            if (n <= gg) {
                 lo = lo + t;
                 hi = lo;
             } else {
-                const int plast = t > 0 ? lo + (int)(((long long)t * n) / (G + 1)) : lo - 1;
-                const int pnext = t < G ? lo + (int)(((long long)(t + 1) * n) / (G + 1)) : hi;
+                const int plast = t > 0 ? (wide ? probe_pos<G>(lo, n, t - 1) : probe_pos<GT>(lo, n, t - 1)) : lo - 1;
+                const int pnext = t < gg ? (wide ? probe_pos<G>(lo, n, t) : probe_pos<GT>(lo, n, t)) : hi;
                 lo = plast + 1;
                 hi = pnext;
             }
@@ -59,9 +69,12 @@ __device__ __forceinline__ int group_rank(const K* __restrict__ X, int len, K x,
     return lo;
 }
 
-template <typename K, int G>
+// wide_A: interval length above which searches INTO B (Step 1) probe with
+// all G lanes; wide_B likewise for searches into A (Step 2).
+template <typename K, int G, int GT>
 __global__ void __launch_bounds__(256) k_cross_ranks(const K* __restrict__ A, const K* __restrict__ B, Geom g,
-                                                     int* __restrict__ xbar, int* __restrict__ ybar) {
+                                                     int* __restrict__ xbar, int* __restrict__ ybar, int wide_A,
+                                                     int wide_B) {
     const int per = g.pA + g.pB + 2;
     const long long item = ((long long)blockIdx.x * blockDim.x + threadIdx.x) / G;
     const bool valid = item < (long long)g.S * per;
@@ -84,7 +97,8 @@ __global__ void __launch_bounds__(256) k_cross_ranks(const K* __restrict__ A, co
     const bool search = valid && start < own_len;
     K x = K(0);
     if (search) x = __ldg((sideA ? As : Bs) + start);
-    const int r = group_rank<K, G>(sideA ? Bs : As, sideA ? sg.m : sg.n, x, !sideA, search);
+    const int r = group_rank<K, G, GT>(sideA ? Bs : As, sideA ? sg.m : sg.n, x, !sideA, search,
+                                       sideA ? wide_A : wide_B);
     if (valid && (threadIdx.x % G) == 0) {
         const int v = search ? r : (sideA ? sg.m : sg.n);
         if (sideA) xbar[(size_t)s * (g.pA + 1) + idx] = v;

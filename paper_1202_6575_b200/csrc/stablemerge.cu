@@ -9,6 +9,7 @@
 #include <stdint.h>
 #include <stdio.h>
 #include <string.h>
+#include <stdlib.h>
 
 #include <algorithm>
 #include <vector>
@@ -22,30 +23,62 @@ namespace sm {
 thread_local char g_err[512] = "";
 thread_local int64_t g_launches = 0;
 
-// K2 shape: NC consumer threads x VT elements = tile capacity NV (largest
-// task), STAGES-deep TMA ring.  VT odd keeps the register <-> shared-memory
-// transposition free of bank conflicts for 4- and 8-byte keys.
-constexpr int K2_NC = 256;
-constexpr int K2_VT = 15;
-// Ring depth per element layout: enough bulk loads in flight per SM to cover
-// HBM latency within the shared-memory budget (228 KB per SM): 4-byte
-// elements 4 x 16.6 KB (3 CTAs/SM), 8-byte 3 x 33 KB (2 CTAs/SM), 12-byte
+// K2 shape per element layout: NC consumer threads x VT diagonals per thread
+// = NV padded diagonals per ring stage, the largest task; block size
+// T = NV / 2 (task bound 2T); STAGES-deep TMA ring.
+// VT odd keeps the register -> shared-memory write-back free of bank
+// conflicts.  Keys-only 4-byte merges are bound by the consumers' shared-
+// memory traffic, so they take VT = 31 (half the merge-path splits per
+// element, T = 3968: half the cross-rank searches); wider elements are bound
+// by HBM and keep VT = 15 with a deeper ring.  Shared memory per CTA:
+// 4-byte 3 x 33 KB (2 CTAs/SM), 8-byte 3 x 33 KB (2 CTAs/SM), 12-byte
 // 4 x 49 KB (1 CTA/SM).
 template <typename K, bool HAS_V>
-struct K2Stages {
+struct K2Shape {
     static constexpr int bytes = (int)sizeof(K) + (HAS_V ? 4 : 0);
-    static constexpr int value = bytes <= 4 ? 4 : (bytes <= 8 ? 3 : 4);
+    static constexpr int NC = 256;
+    static constexpr int VT = bytes <= 4 ? 31 : 15;
+    static constexpr int STAGES = bytes <= 8 ? 3 : 4;
+    static constexpr int NV = NC * VT;
+    static constexpr int T = NV / 2;
 };
 // Tasks packed per ring stage at most.
 constexpr int K2_MAXT = 16;
-constexpr int NV = K2_NC * K2_VT;  // tile capacity: largest task
-constexpr int T_DEFAULT = NV / 2;  // block size: task bound 2T (L388-393)
+
+// Tile capacity NV (largest task) and default block size of a layout.
+static int64_t tile_nv(int key_bytes, bool has_v) {
+    if (key_bytes == 4) return has_v ? K2Shape<uint32_t, true>::NV : K2Shape<uint32_t, false>::NV;
+    return has_v ? K2Shape<uint64_t, true>::NV : K2Shape<uint64_t, false>::NV;
+}
+static int64_t tile_t(int key_bytes, bool has_v) { return tile_nv(key_bytes, has_v) / 2; }
 // K3 shape: one run of R = NT * VT elements per CTA.
 constexpr int NT = 128;
 constexpr int VT = 15;
 constexpr int R_SORT = NT * VT;
-// K1: lanes per cooperative rank search.
+// K1: lanes per cooperative rank search (top levels), lanes probing below
+// the L2-shared levels.
 constexpr int K1_G = 8;
+constexpr int K1_GT = 1;
+
+// Interval length below which a search into an array of `len` keys probes
+// with K1_GT lanes: searches are spaced ~len/searches apart, so intervals
+// shorter than a few spacings are private to one search (DRAM, not L2).
+// Arrays that fit comfortably in L2 (or few searches) stay wide throughout.
+template <typename K>
+static void k1_wide(const Geom& g, int& wide_A, int& wide_B) {
+    const long long n = g.sort ? g.L : g.n, m = g.sort ? g.L : g.m;
+    const long long S = g.sort ? g.S : 1;
+    const long long searchesA = S * g.pA, searchesB = S * g.pB;   // into B, into A
+    auto pick = [&](long long len, long long searches) -> int {
+        const long long bytes = len * S * (long long)sizeof(K);
+        if (bytes < (32ll << 20) || searches < 4096) return INT_MAX;
+        const long long spacing = (len + (searches / S) - 1) / (searches / S);
+        static const long long factor = getenv("SM_K1_FACTOR") ? atoll(getenv("SM_K1_FACTOR")) : 4;
+        return (int)std::min<long long>(INT_MAX, factor * spacing);
+    };
+    wide_A = pick(m, searchesA);
+    wide_B = pick(n, searchesB);
+}
 
 static sm_status fail_cuda(cudaError_t e, const char* what) {
     snprintf(g_err, sizeof(g_err), "%s: %s", what, cudaGetErrorString(e));
@@ -135,15 +168,25 @@ static sm_status launch_merge(const K* A, const uint32_t* vA, const K* B, const 
                               uint32_t* vC, const Geom& g, int* xbar, int* ybar, cudaStream_t st, bool pdl) {
     const long long items = (long long)g.S * (g.pA + g.pB + 2);
     const long long blocks1 = (items * K1_G + 255) / 256;
+    int wide_A, wide_B;
+    k1_wide<K>(g, wide_A, wide_B);
     prof_before(PROF_K1, st);
-    k_cross_ranks<K, K1_G><<<(unsigned)blocks1, 256, 0, st>>>(A, B, g, xbar, ybar);
+    static const int variant = getenv("SM_K1_VARIANT") ? atoi(getenv("SM_K1_VARIANT")) : 0;
+    if (variant == 1)
+        k_cross_ranks<K, 4, 1><<<(unsigned)((items * 4 + 255) / 256), 256, 0, st>>>(A, B, g, xbar, ybar, wide_A, wide_B);
+    else if (variant == 2)
+        k_cross_ranks<K, 8, 2><<<(unsigned)blocks1, 256, 0, st>>>(A, B, g, xbar, ybar, wide_A, wide_B);
+    else if (variant == 3)
+        k_cross_ranks<K, 4, 2><<<(unsigned)((items * 4 + 255) / 256), 256, 0, st>>>(A, B, g, xbar, ybar, wide_A, wide_B);
+    else
+    k_cross_ranks<K, K1_G, K1_GT><<<(unsigned)blocks1, 256, 0, st>>>(A, B, g, xbar, ybar, wide_A, wide_B);
     prof_after(st);
     sm_status s = check_launch("k_cross_ranks");
     if (s != SM_OK) return s;
 
-    constexpr int STAGES = K2Stages<K, HAS_V>::value;
-    using Lay = K2Layout<K, HAS_V, K2_NC, K2_VT, STAGES, K2_MAXT>;
-    auto kern = k_tasks<K, HAS_V, K2_NC, K2_VT, STAGES, K2_MAXT>;
+    using Sh = K2Shape<K, HAS_V>;
+    using Lay = K2Layout<K, HAS_V, Sh::NC, Sh::VT, Sh::STAGES, K2_MAXT>;
+    auto kern = k_tasks<K, HAS_V, Sh::NC, Sh::VT, Sh::STAGES, K2_MAXT>;
     static int per_sm = -1, n_sm = 0;
     if (per_sm < 0) {
         int dev = 0;
@@ -151,7 +194,7 @@ static sm_status launch_merge(const K* A, const uint32_t* vA, const K* B, const 
         cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Lay::SMEM);
         cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, K2_NC + 64, Lay::SMEM);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, Sh::NC + 64, Lay::SMEM);
         if (per_sm < 1) per_sm = 1;
     }
     const long long ntasks = (long long)g.S * (g.pA + g.pB);
@@ -159,7 +202,7 @@ static sm_status launch_merge(const K* A, const uint32_t* vA, const K* B, const 
     cudaLaunchConfig_t cfg;
     memset(&cfg, 0, sizeof(cfg));
     cfg.gridDim = dim3((unsigned)grid);
-    cfg.blockDim = dim3(K2_NC + 64);
+    cfg.blockDim = dim3(Sh::NC + 64);
     cfg.dynamicSmemBytes = Lay::SMEM;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
@@ -266,6 +309,7 @@ static sm_status merge_entry(const K* A, const uint32_t* vA, int64_t n, const K*
         overlaps(vC, cb * 4, vA, n * 4) || overlaps(vC, cb * 4, vB, m * 4) || overlaps(C, cb * kb, vC, cb * 4))
         return SM_EALIAS;
 
+    const int64_t NV = tile_nv((int)sizeof(K), vC != nullptr);
     int64_t pA, pB;
     if (opt && (opt->p_A || opt->p_B)) {
         if (opt->p_A < 1 || opt->p_B < 1) return fail_inval("p_A and p_B must both be >= 1");
@@ -273,7 +317,7 @@ static sm_status merge_entry(const K* A, const uint32_t* vA, int64_t n, const K*
         if (pA > INT_MAX / 2 || pB > INT_MAX / 2) return fail_inval("p too large");
         if (ceil_div(n, pA) + ceil_div(m, pB) > NV) return fail_inval("task bound ceil(n/p_A)+ceil(m/p_B) exceeds the tile");
     } else {
-        int64_t T = (opt && opt->block) ? opt->block : T_DEFAULT;
+        int64_t T = (opt && opt->block) ? opt->block : NV / 2;
         if (T < 1 || 2 * T > NV) return fail_inval("block size T must satisfy 1 <= 2T <= tile capacity");
         pA = std::max<int64_t>(1, ceil_div(n, T));
         pB = std::max<int64_t>(1, ceil_div(m, T));
@@ -331,7 +375,10 @@ static sm_status plan_entry(const K* A, int64_t n, const K* B, int64_t m, int64_
     sm_status s = dalloc(&ranks, (pA + 1) + (pB + 1), st);
     if (s != SM_OK) return s;
     const long long items = pA + pB + 2;
-    k_cross_ranks<K, K1_G><<<(unsigned)((items * K1_G + 255) / 256), 256, 0, st>>>(A, B, g, ranks, ranks + pA + 1);
+    int wide_A, wide_B;
+    k1_wide<K>(g, wide_A, wide_B);
+    k_cross_ranks<K, K1_G, K1_GT><<<(unsigned)((items * K1_G + 255) / 256), 256, 0, st>>>(A, B, g, ranks, ranks + pA + 1,
+                                                                                     wide_A, wide_B);
     s = check_launch("k_cross_ranks");
     if (s == SM_OK) {
         k_widen<<<(unsigned)((pA + 1 + 255) / 256), 256, 0, st>>>(ranks, xbar, (int)(pA + 1));
@@ -361,7 +408,8 @@ static sm_status sort_device(K* keys, uint32_t* vals, int64_t N, cudaStream_t st
     sm_status s = dalloc(&aux, N, st);
     if (s == SM_OK && vals) s = dalloc(&vaux, N, st);
     // rank arrays for the largest round: S*(pA+1) + S*(pB+1) <= 2*(N/T + 2*S) entries
-    if (s == SM_OK) s = dalloc(&ranks, 2 * (ceil_div(N, T_DEFAULT) + 2 * ceil_div(N, R) + 2), st);
+    const int64_t T = tile_t((int)sizeof(K), vals != nullptr);
+    if (s == SM_OK) s = dalloc(&ranks, 2 * (ceil_div(N, T) + 2 * ceil_div(N, R) + 2), st);
     if (s == SM_OK) {
         // phase 1 lands in the buffer from which an even number of rounds
         // ends in the caller's array (in place when rounds is even)
@@ -380,7 +428,7 @@ static sm_status sort_device(K* keys, uint32_t* vals, int64_t N, cudaStream_t st
             uint32_t* vd2 = (src == keys) ? vaux : vals;
             Geom g;
             g.S = (int)ceil_div(N, 2 * L);
-            g.pA = g.pB = (int)ceil_div(L, T_DEFAULT);
+            g.pA = g.pB = (int)ceil_div(L, T);
             g.n = g.m = 0; g.L = (int)L; g.N = (int)N; g.sort = 1;
             int* xbar = ranks;
             int* ybar = ranks + (int64_t)g.S * (g.pA + 1);
@@ -453,9 +501,7 @@ SM_DEFINE_ABI(i64, int64_t)
 SM_DEFINE_ABI(u64, uint64_t)
 
 int64_t sm_tile_capacity(int32_t key_bytes, int32_t has_vals) {
-    (void)key_bytes;
-    (void)has_vals;
-    return sm::NV;
+    return sm::tile_nv(key_bytes, has_vals != 0);
 }
 
 int64_t sm_sort_run(int32_t key_bytes, int32_t has_vals) {

@@ -101,6 +101,21 @@ def test_merge_ragged(kt, nm, payload):
         assert_bit_exact(*gpu_merge(sm, inp), *oracle_merge(inp), kt)
 
 
+@pytest.mark.parametrize("kt,payload", [("u32", True), ("i32", False)])
+def test_merge_tile_boundaries(kt, payload):
+    """Sizes around the block size T and the tile capacity NV = 2T of the
+    layout actually used (they differ per key width / payload mode)."""
+    sm = lib()
+    nv = sm.tile_capacity(kt, payload)
+    T = nv // 2
+    for n, m in ((T, T), (T + 1, T - 1), (2 * T, 1), (nv - 1, nv + 1), (3 * T + 7, 5 * T - 3), (nv * 4, 3)):
+        inp = synth.merge_input(n, m, kt, "bounded:40", seed=n + 7 * m, payload=payload)
+        assert_bit_exact(*gpu_merge(sm, inp), *oracle_merge(inp), kt)
+        inp = synth.merge_input(n, m, kt, "full", seed=n + 11 * m, payload=payload)
+        assert_bit_exact(*gpu_merge(sm, inp, p_A=max(1, -(-n // T)), p_B=max(1, -(-m // T))),
+                         *oracle_merge(inp), kt)
+
+
 @pytest.mark.parametrize("block", [1, 2, 7, 32, 257, 960])
 def test_merge_metamorphic_block_size(block):
     """Output must not depend on the tuning (T, p_A vs p_B) -- S:L262."""
@@ -197,7 +212,7 @@ def test_merge_errors():
         sm.merge_stable(out[:100], None, a, None, out_keys=out[50:250])
     assert e.value.status == 2
     with pytest.raises(sm.StableMergeError) as e:      # tile bound violated by explicit p
-        sm.merge_stable(torch.arange(5000, dtype=torch.int32, device="cuda"), None, a, None, p_A=1, p_B=1)
+        sm.merge_stable(torch.arange(20000, dtype=torch.int32, device="cuda"), None, a, None, p_A=1, p_B=1)
     assert e.value.status == 1
 
 
