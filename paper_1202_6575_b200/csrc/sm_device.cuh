@@ -253,14 +253,14 @@ __device__ __forceinline__ void lift_probe(uint32_t& sa, uint32_t& sb, int& rem)
 
 // One output of the serial stable merge: take A when A is not exhausted and
 // (B is exhausted or ka <= kb) -- ties to A.  Advances
-// the taken side and loads its next key (one past the end at most: the
-// stage holds slack there and the value is never selected).
+// the taken side and loads the key after its new head (two past the end at
+// most: the stage holds slack there and the value is never selected).
 template <typename K>
-__device__ __forceinline__ void merge_step(uint32_t& pa, uint32_t& pb, K& ka, K& kb, uint32_t pae, uint32_t pbe,
-                                           K& out);
+__device__ __forceinline__ void merge_step(uint32_t& pa, uint32_t& pb, K& ka, K& kb, K& na, K& nb, uint32_t pae,
+                                           uint32_t pbe, K& out);
 // Same, also selecting the payload index (ia for A, ib for B).
 template <typename K>
-__device__ __forceinline__ void merge_step_idx(uint32_t& pa, uint32_t& pb, K& ka, K& kb, uint32_t pae,
+__device__ __forceinline__ void merge_step_idx(uint32_t& pa, uint32_t& pb, K& ka, K& kb, K& na, K& nb, uint32_t pae,
                                                uint32_t pbe, K& out, int& ia, int& ib, int& src);
 
 template <typename K>
@@ -291,46 +291,54 @@ __device__ __forceinline__ K lds(uint32_t addr);
         return v;                                                                                              \
     }                                                                                                          \
     template <>                                                                                                \
-    __device__ __forceinline__ void merge_step<K>(uint32_t & pa, uint32_t & pb, K & ka, K & kb, uint32_t pae,  \
-                                                  uint32_t pbe, K & out) {                                     \
-        /* one shared load per step (from the side just taken): half the */                                  \
-        /* shared-memory wavefronts of a load per side */                                                     \
+    __device__ __forceinline__ void merge_step<K>(uint32_t & pa, uint32_t & pb, K & ka, K & kb, K & na, K & nb,\
+                                                  uint32_t pae, uint32_t pbe, K & out) {                       \
+        /* ka/kb: current heads, na/nb: the elements after them (loaded a */                                  \
+        /* step ahead, so the load latency is off the compare chain); one */                                 \
+        /* shared load per step, from the side just taken */                                                  \
         asm volatile(                                                                                          \
-            "{\n\t.reg .pred t;\n\t.reg .b32 ad;\n\t.reg .b" BITS " k;\n\t"                                   \
-            "setp.le." #CMP " t, %2, %3;\n\t"                                                                  \
-            "setp.lt.and.u32 t, %0, %5, t;\n\t"                                                                \
-            "setp.ge.or.u32 t, %1, %6, t;\n\t"                                                                 \
-            "selp.b" BITS " %4, %2, %3, t;\n\t"                                                                \
+            "{\n\t.reg .pred t, u, w;\n\t.reg .b32 ad;\n\t.reg .b" BITS " k;\n\t"                             \
+            "setp.lt.u32 u, %0, %7;\n\t"                                                                       \
+            "setp.ge.u32 w, %1, %8;\n\t"                                                                       \
+            "setp.le.and." #CMP " t, %2, %3, u;\n\t"                                                           \
+            "or.pred t, t, w;\n\t"                                                                             \
+            "selp.b" BITS " %6, %2, %3, t;\n\t"                                                                \
+            "selp.b" BITS " %2, %4, %2, t;\n\t"                                                                \
+            "selp.b" BITS " %3, %3, %5, t;\n\t"                                                                \
             "@t add.u32 %0, %0, " #SZ ";\n\t"                                                                  \
             "@!t add.u32 %1, %1, " #SZ ";\n\t"                                                                 \
             "selp.b32 ad, %0, %1, t;\n\t"                                                                      \
-            "ld.shared.b" BITS " k, [ad];\n\t"                                                                 \
-            "selp.b" BITS " %2, k, %2, t;\n\t"                                                                 \
-            "selp.b" BITS " %3, %3, k, t;\n\t}"                                                                \
-            : "+r"(pa), "+r"(pb), "+" RC(ka), "+" RC(kb), "=" RC(out)                                          \
+            "ld.shared.b" BITS " k, [ad+" #SZ "];\n\t"                                                         \
+            "selp.b" BITS " %4, k, %4, t;\n\t"                                                                 \
+            "selp.b" BITS " %5, %5, k, t;\n\t}"                                                                \
+            : "+r"(pa), "+r"(pb), "+" RC(ka), "+" RC(kb), "+" RC(na), "+" RC(nb), "=" RC(out)                  \
             : "r"(pae), "r"(pbe)                                                                               \
             : "memory");                                                                                       \
     }                                                                                                          \
     template <>                                                                                                \
-    __device__ __forceinline__ void merge_step_idx<K>(uint32_t & pa, uint32_t & pb, K & ka, K & kb,            \
-                                                      uint32_t pae, uint32_t pbe, K & out, int& ia, int& ib,   \
-                                                      int& src) {                                              \
+    __device__ __forceinline__ void merge_step_idx<K>(uint32_t & pa, uint32_t & pb, K & ka, K & kb, K & na,    \
+                                                      K & nb, uint32_t pae, uint32_t pbe, K & out, int& ia,    \
+                                                      int& ib, int& src) {                                     \
         asm volatile(                                                                                          \
-            "{\n\t.reg .pred t;\n\t.reg .b32 ad;\n\t.reg .b" BITS " k;\n\t"                                   \
-            "setp.le." #CMP " t, %2, %3;\n\t"                                                                  \
-            "setp.lt.and.u32 t, %0, %8, t;\n\t"                                                                \
-            "setp.ge.or.u32 t, %1, %9, t;\n\t"                                                                 \
-            "selp.b" BITS " %4, %2, %3, t;\n\t"                                                                \
-            "selp.b32 %7, %5, %6, t;\n\t"                                                                      \
+            "{\n\t.reg .pred t, u, w;\n\t.reg .b32 ad;\n\t.reg .b" BITS " k;\n\t"                             \
+            "setp.lt.u32 u, %0, %10;\n\t"                                                                      \
+            "setp.ge.u32 w, %1, %11;\n\t"                                                                      \
+            "setp.le.and." #CMP " t, %2, %3, u;\n\t"                                                           \
+            "or.pred t, t, w;\n\t"                                                                             \
+            "selp.b" BITS " %6, %2, %3, t;\n\t"                                                                \
+            "selp.b32 %9, %7, %8, t;\n\t"                                                                      \
+            "selp.b" BITS " %2, %4, %2, t;\n\t"                                                                \
+            "selp.b" BITS " %3, %3, %5, t;\n\t"                                                                \
             "@t add.u32 %0, %0, " #SZ ";\n\t"                                                                  \
             "@!t add.u32 %1, %1, " #SZ ";\n\t"                                                                 \
-            "@t add.s32 %5, %5, 1;\n\t"                                                                        \
-            "@!t add.s32 %6, %6, 1;\n\t"                                                                       \
+            "@t add.s32 %7, %7, 1;\n\t"                                                                        \
+            "@!t add.s32 %8, %8, 1;\n\t"                                                                       \
             "selp.b32 ad, %0, %1, t;\n\t"                                                                      \
-            "ld.shared.b" BITS " k, [ad];\n\t"                                                                 \
-            "selp.b" BITS " %2, k, %2, t;\n\t"                                                                 \
-            "selp.b" BITS " %3, %3, k, t;\n\t}"                                                                \
-            : "+r"(pa), "+r"(pb), "+" RC(ka), "+" RC(kb), "=" RC(out), "+r"(ia), "+r"(ib), "=r"(src)          \
+            "ld.shared.b" BITS " k, [ad+" #SZ "];\n\t"                                                         \
+            "selp.b" BITS " %4, k, %4, t;\n\t"                                                                 \
+            "selp.b" BITS " %5, %5, k, t;\n\t}"                                                                \
+            : "+r"(pa), "+r"(pb), "+" RC(ka), "+" RC(kb), "+" RC(na), "+" RC(nb), "=" RC(out), "+r"(ia),      \
+              "+r"(ib), "=r"(src)                                                                              \
             : "r"(pae), "r"(pbe)                                                                               \
             : "memory");                                                                                       \
     }                                                                                                          \

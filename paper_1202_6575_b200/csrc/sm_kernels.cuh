@@ -575,13 +575,13 @@ __global__ void __launch_bounds__(NC + 64) k_tasks(const K* __restrict__ A, cons
                     const int bi = d - ai;
                     uint32_t pa = sa0 + ai * KB, pb = sb0 + bi * KB;
                     const uint32_t pae = sa0 + td.la * KB, pbe = sb0 + td.lb * KB;
-                    K ka = lds<K>(pa), kb = lds<K>(pb);
+                    K ka = lds<K>(pa), kb = lds<K>(pb), na = lds<K>(pa + KB), nb = lds<K>(pb + KB);
                     int src[VT];
                     int ia = td.va_s + ai, ib = td.vb_s + bi;
 #pragma unroll
                     for (int k = 0; k < VT; ++k) {
-                        if (HAS_V) merge_step_idx<K>(pa, pb, ka, kb, pae, pbe, out[k], ia, ib, src[k]);
-                        else merge_step<K>(pa, pb, ka, kb, pae, pbe, out[k]);
+                        if (HAS_V) merge_step_idx<K>(pa, pb, ka, kb, na, nb, pae, pbe, out[k], ia, ib, src[k]);
+                        else merge_step<K>(pa, pb, ka, kb, na, nb, pae, pbe, out[k]);
                     }
                     if (HAS_V) {
 #pragma unroll

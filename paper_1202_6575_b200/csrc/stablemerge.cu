@@ -57,7 +57,7 @@ constexpr int VT = 15;
 constexpr int R_SORT = NT * VT;
 // K1: lanes per cooperative rank search (top levels), lanes probing below
 // the L2-shared levels.
-constexpr int K1_G = 8;
+constexpr int K1_G = 4;
 constexpr int K1_GT = 1;
 
 // Interval length below which a search into an array of `len` keys probes
@@ -73,7 +73,7 @@ static void k1_wide(const Geom& g, int& wide_A, int& wide_B) {
         const long long bytes = len * S * (long long)sizeof(K);
         if (bytes < (32ll << 20) || searches < 4096) return INT_MAX;
         const long long spacing = (len + (searches / S) - 1) / (searches / S);
-        static const long long factor = getenv("SM_K1_FACTOR") ? atoll(getenv("SM_K1_FACTOR")) : 4;
+        static const long long factor = getenv("SM_K1_FACTOR") ? atoll(getenv("SM_K1_FACTOR")) : 2;
         return (int)std::min<long long>(INT_MAX, factor * spacing);
     };
     wide_A = pick(m, searchesA);
