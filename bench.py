@@ -479,6 +479,8 @@ def main():
                             "avg_launch_ms": k2_avg,
                             "share_of_step": k2_ms / max(1e-9, k1_ms + k2_ms + k3_ms),
                             "k_cross_ranks_avg_ms": k1_ms / max(1, k1_n),
+                            "k_cross_ranks_ms_per_step": k1_ms / r["kernels"]["steps"],
+                            "k_tasks_ms_per_step": k2_ms / r["kernels"]["steps"],
                             "k_block_sort_avg_ms": (k3_ms / k3_n) if k3_n else None}
     if "e2e" in r:
         line["e2e"] = r["e2e"]

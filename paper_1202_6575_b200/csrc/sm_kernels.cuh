@@ -52,7 +52,7 @@ __device__ __forceinline__ int group_rank(const K* __restrict__ X, int len, K x,
             const K v = __ldg(X + pos);
             pred = high ? (v <= x) : (v < x);
         }
-        const unsigned bal = (__ballot_sync(0xffffffffu, pred) >> shift) & ((1u << G) - 1u);
+        const unsigned bal = (__ballot_sync(0xffffffffu, pred) >> shift) & (G == 32 ? 0xffffffffu : ((1u << (G & 31)) - 1u));
         const int t = __popc(bal);          // probes passed: a prefix of the probing lanes
         if (hi > lo) {
             if (n <= gg) {
@@ -69,12 +69,15 @@ __device__ __forceinline__ int group_rank(const K* __restrict__ X, int len, K x,
     return lo;
 }
 
-// wide_A: interval length above which searches INTO B (Step 1) probe with
-// all G lanes; wide_B likewise for searches into A (Step 2).
-template <typename K, int G, int GT>
+// K1 (rows a1/a2): one group of G lanes per cross rank, searching the whole
+// other array (G = 1: a plain binary search per thread, measured fastest on
+// B200 for every config: the top levels are shared by all searches and hit
+// L1/L2, the bottom levels are private DRAM probes, one sector each).
+//   Step 1: xbar_i = rank_low(A[x_i], B) (L304-306), xbar_pA = m, empty block start -> m (R4)
+//   Step 2: ybar_j = rank_high(B[y_j], A) (L307-309), ybar_pB = n
+template <typename K, int G>
 __global__ void __launch_bounds__(256) k_cross_ranks(const K* __restrict__ A, const K* __restrict__ B, Geom g,
-                                                     int* __restrict__ xbar, int* __restrict__ ybar, int wide_A,
-                                                     int wide_B) {
+                                                     int* __restrict__ xbar, int* __restrict__ ybar) {
     const int per = g.pA + g.pB + 2;
     const long long item = ((long long)blockIdx.x * blockDim.x + threadIdx.x) / G;
     const bool valid = item < (long long)g.S * per;
@@ -84,23 +87,17 @@ __global__ void __launch_bounds__(256) k_cross_ranks(const K* __restrict__ A, co
         t = (int)(item % per);
     }
     const Seg sg = segment(g, s);
-    const K* As = A + sg.aoff;
-    const K* Bs = B + sg.boff;
-    // Step 1 (t <= pA): xbar_i = rank_low(A[x_i], B), xbar_pA = m, empty block start -> m (R4)
-    // Step 2 (t >  pA): ybar_j = rank_high(B[y_j], A), ybar_pB = n
     const bool sideA = t <= g.pA;
     const int idx = sideA ? t : t - g.pA - 1;
-    const int plen = sideA ? g.pA : g.pB;
+    const int plen = sideA ? g.pA : g.pB;            // own blocks
     const int own_len = sideA ? sg.n : sg.m;
-    int start = own_len;
-    if (valid && idx < plen) start = Blocks(own_len, plen).start(idx);
-    const bool search = valid && start < own_len;
+    const int oth_len = sideA ? sg.m : sg.n;         // searched array
+    const bool search = valid && idx < plen && idx < own_len;   // x_idx < own_len  <=>  idx < own_len
     K x = K(0);
-    if (search) x = __ldg((sideA ? As : Bs) + start);
-    const int r = group_rank<K, G, GT>(sideA ? Bs : As, sideA ? sg.m : sg.n, x, !sideA, search,
-                                       sideA ? wide_A : wide_B);
+    if (search) x = __ldg((sideA ? A + sg.aoff : B + sg.boff) + Blocks(own_len, plen).start(idx));
+    const int r = group_rank<K, G, G>(sideA ? B + sg.boff : A + sg.aoff, oth_len, x, !sideA, search, 0);
     if (valid && (threadIdx.x % G) == 0) {
-        const int v = search ? r : (sideA ? sg.m : sg.n);
+        const int v = search ? r : oth_len;
         if (sideA) xbar[(size_t)s * (g.pA + 1) + idx] = v;
         else ybar[(size_t)s * (g.pB + 1) + idx] = v;
     }

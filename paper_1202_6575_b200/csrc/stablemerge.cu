@@ -55,30 +55,10 @@ static int64_t tile_t(int key_bytes, bool has_v) { return tile_nv(key_bytes, has
 constexpr int NT = 128;
 constexpr int VT = 15;
 constexpr int R_SORT = NT * VT;
-// K1: lanes per cooperative rank search (top levels), lanes probing below
-// the L2-shared levels.
-constexpr int K1_G = 4;
-constexpr int K1_GT = 1;
-
-// Interval length below which a search into an array of `len` keys probes
-// with K1_GT lanes: searches are spaced ~len/searches apart, so intervals
-// shorter than a few spacings are private to one search (DRAM, not L2).
-// Arrays that fit comfortably in L2 (or few searches) stay wide throughout.
-template <typename K>
-static void k1_wide(const Geom& g, int& wide_A, int& wide_B) {
-    const long long n = g.sort ? g.L : g.n, m = g.sort ? g.L : g.m;
-    const long long S = g.sort ? g.S : 1;
-    const long long searchesA = S * g.pA, searchesB = S * g.pB;   // into B, into A
-    auto pick = [&](long long len, long long searches) -> int {
-        const long long bytes = len * S * (long long)sizeof(K);
-        if (bytes < (32ll << 20) || searches < 4096) return INT_MAX;
-        const long long spacing = (len + (searches / S) - 1) / (searches / S);
-        static const long long factor = getenv("SM_K1_FACTOR") ? atoll(getenv("SM_K1_FACTOR")) : 2;
-        return (int)std::min<long long>(INT_MAX, factor * spacing);
-    };
-    wide_A = pick(m, searchesA);
-    wide_B = pick(n, searchesB);
-}
+// K1: lanes per rank search (see k_cross_ranks).  Many searches: one lane
+// each (the DRAM-probe traffic of wider groups costs more than it saves).
+// Few searches (< K1_FEW): a whole warp each, ~log_33 dependent rounds.
+constexpr int K1_FEW = 4096;
 
 static sm_status fail_cuda(cudaError_t e, const char* what) {
     snprintf(g_err, sizeof(g_err), "%s: %s", what, cudaGetErrorString(e));
@@ -163,25 +143,21 @@ static void dfree(void* p, cudaStream_t st) {
 }
 
 // ------------------------------------------------------------ launches
+// K1: the cross ranks of every block start of every segment.
+template <typename K>
+static sm_status launch_cross_ranks(const K* A, const K* B, const Geom& g, int* xbar, int* ybar, cudaStream_t st) {
+    const long long items = (long long)g.S * (g.pA + g.pB + 2);
+    prof_before(PROF_K1, st);
+    if (items < K1_FEW) k_cross_ranks<K, 32><<<(unsigned)((items * 32 + 255) / 256), 256, 0, st>>>(A, B, g, xbar, ybar);
+    else k_cross_ranks<K, 1><<<(unsigned)((items + 255) / 256), 256, 0, st>>>(A, B, g, xbar, ybar);
+    prof_after(st);
+    return check_launch("k_cross_ranks");
+}
+
 template <typename K, bool HAS_V>
 static sm_status launch_merge(const K* A, const uint32_t* vA, const K* B, const uint32_t* vB, K* C,
                               uint32_t* vC, const Geom& g, int* xbar, int* ybar, cudaStream_t st, bool pdl) {
-    const long long items = (long long)g.S * (g.pA + g.pB + 2);
-    const long long blocks1 = (items * K1_G + 255) / 256;
-    int wide_A, wide_B;
-    k1_wide<K>(g, wide_A, wide_B);
-    prof_before(PROF_K1, st);
-    static const int variant = getenv("SM_K1_VARIANT") ? atoi(getenv("SM_K1_VARIANT")) : 0;
-    if (variant == 1)
-        k_cross_ranks<K, 4, 1><<<(unsigned)((items * 4 + 255) / 256), 256, 0, st>>>(A, B, g, xbar, ybar, wide_A, wide_B);
-    else if (variant == 2)
-        k_cross_ranks<K, 8, 2><<<(unsigned)blocks1, 256, 0, st>>>(A, B, g, xbar, ybar, wide_A, wide_B);
-    else if (variant == 3)
-        k_cross_ranks<K, 4, 2><<<(unsigned)((items * 4 + 255) / 256), 256, 0, st>>>(A, B, g, xbar, ybar, wide_A, wide_B);
-    else
-    k_cross_ranks<K, K1_G, K1_GT><<<(unsigned)blocks1, 256, 0, st>>>(A, B, g, xbar, ybar, wide_A, wide_B);
-    prof_after(st);
-    sm_status s = check_launch("k_cross_ranks");
+    sm_status s = launch_cross_ranks<K>(A, B, g, xbar, ybar, st);
     if (s != SM_OK) return s;
 
     using Sh = K2Shape<K, HAS_V>;
@@ -374,12 +350,7 @@ static sm_status plan_entry(const K* A, int64_t n, const K* B, int64_t m, int64_
     int* ranks = nullptr;
     sm_status s = dalloc(&ranks, (pA + 1) + (pB + 1), st);
     if (s != SM_OK) return s;
-    const long long items = pA + pB + 2;
-    int wide_A, wide_B;
-    k1_wide<K>(g, wide_A, wide_B);
-    k_cross_ranks<K, K1_G, K1_GT><<<(unsigned)((items * K1_G + 255) / 256), 256, 0, st>>>(A, B, g, ranks, ranks + pA + 1,
-                                                                                     wide_A, wide_B);
-    s = check_launch("k_cross_ranks");
+    s = launch_cross_ranks<K>(A, B, g, ranks, ranks + pA + 1, st);
     if (s == SM_OK) {
         k_widen<<<(unsigned)((pA + 1 + 255) / 256), 256, 0, st>>>(ranks, xbar, (int)(pA + 1));
         s = check_launch("k_widen");

@@ -10,7 +10,7 @@ for c in ${CONFIGS:-2 5 3}; do
 import json,sys
 try:
   d=json.loads(sys.stdin.read()); r=d.get('roofline',{})
-  print($c, 'ms %.4f'%d['ms_per_step'], 'GB/s %.0f'%d['achieved_hbm_gbs'], 'frac %.3f'%d['achieved_hbm_frac'], 'K2 %.0f frac %.3f k1ms %.4f k2ms %.4f k3 %s'%(r['achieved'],r['frac'],r['k_cross_ranks_avg_ms'],r['avg_launch_ms'],r['k_block_sort_avg_ms']), d['clocks']['sm_mhz'], d['clocks']['reasons'])
+  print($c, 'ms %.4f'%d['ms_per_step'], 'GB/s %.0f'%d['achieved_hbm_gbs'], 'frac %.3f'%d['achieved_hbm_frac'], 'K2 %.0f frac %.3f k1ms %.4f k2ms %.4f k3 %s'%(r['achieved'],r['frac'],r['k_cross_ranks_ms_per_step'],r['avg_launch_ms'],r['k_block_sort_avg_ms']), d['clocks']['sm_mhz'], d['clocks']['reasons'])
 except Exception as e: print('parse fail', e)
 "
 done
