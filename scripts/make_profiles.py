@@ -1,0 +1,116 @@
+#!/usr/bin/env python
+"""Turn a gpu_evidence.sh run (gpurun_out/ev/) into the committed profiles/:
+bench JSON lines, launch-list summaries, ncu --set full summaries of K2 per
+config, and profiles/traffic.json (DRAM bytes per K2 launch, read by bench.py).
+
+    python scripts/make_profiles.py r01
+"""
+import csv
+import json
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+EV = os.path.join(ROOT, "gpurun_out", "ev")
+OUT = os.path.join(ROOT, "profiles")
+KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+        "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
+        "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed",
+        "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "smsp__issue_active.avg.pct_of_peak_sustained_active",
+        "sm__warps_active.avg.pct_of_peak_sustained_active", "launch__registers_per_thread",
+        "launch__occupancy_limit_shared_mem", "launch__grid_size", "launch__block_size", "smsp__inst_executed.sum",
+        "sm__cycles_elapsed.avg.per_second"]
+UNIT = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+
+
+def ncu_raw(rep):
+    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    r = list(csv.reader(out.splitlines()))
+    return r[0], r[1], r[2]
+
+
+def summarize_ncu(rep, cfg, tag):
+    h, u, v = ncu_raw(rep)
+    get = lambda k: (v[h.index(k)], u[h.index(k)]) if k in h else (None, None)
+    lines = [f"# ncu --set full: K2 (k_tasks), config C{cfg} ({tag})", "",
+             f"kernel: `{v[h.index('Kernel Name')][:140]}`", "",
+             "command: `ncu --set full --clock-control none --import-source on -k regex:k_tasks -s 3 -c 1 "
+             f"python bench.py --config {cfg} --steps 3 --warmup 3 --no-extras`", "",
+             "| metric | value | unit |", "|---|---|---|"]
+    for k in KEYS:
+        val, un = get(k)
+        if val is not None:
+            lines.append(f"| {k} | {val} | {un} |")
+    st = []
+    for i, k in enumerate(h):
+        if k.startswith("smsp__pcsamp_warps_issue_stalled_") and not k.endswith("not_issued"):
+            try:
+                st.append((float(v[i]), k[len("smsp__pcsamp_warps_issue_stalled_"):]))
+            except ValueError:
+                pass
+    tot = sum(s for s, _ in st) or 1
+    lines += ["", "warp-stall samples: " + ", ".join(f"{n} {s / tot * 100:.0f}%" for s, n in sorted(st, reverse=True)[:8])]
+    rd, ur = get("dram__bytes_read.sum")
+    wr, uw = get("dram__bytes_write.sum")
+    traffic = float(rd) * UNIT.get(ur, 1) + float(wr) * UNIT.get(uw, 1)
+    dur, ud = get("gpu__time_duration.sum")
+    return "\n".join(lines) + "\n", traffic, float(dur) * (1e-3 if ud == "us" else (1.0 if ud == "ms" else 1e-6))
+
+
+def summarize_launches(path):
+    rows = [r for r in csv.reader(open(path)) if len(r) > 10 and r[0] != "ID"]
+    agg = {}
+    for r in rows:
+        name = r[4].split("(")[0].replace("void ", "")[:70]
+        a = agg.setdefault(name, [0, 0.0])
+        a[0] += 1
+        a[1] += float(r[-1])
+    ours = sum(v[1] for k, v in agg.items() if k.startswith("sm::"))
+    lines = ["| kernel | launches | total us | avg us | share of library time |", "|---|---|---|---|---|"]
+    for k, v in agg.items():
+        share = f"{v[1] / ours:.3f}" if k.startswith("sm::") and ours else "-"
+        lines.append(f"| `{k}` | {v[0]} | {v[1] / 1e3:.1f} | {v[1] / v[0] / 1e3:.2f} | {share} |")
+    return "\n".join(lines) + "\n"
+
+
+def main(tag):
+    os.makedirs(OUT, exist_ok=True)
+    traffic = {}
+    rows = []
+    for cfg in (2, 1, 3, 4, 5):
+        blog = os.path.join(EV, "bench_default.log" if cfg == 2 else f"bench_c{cfg}.log")
+        line = None
+        if os.path.exists(blog):
+            for ln in open(blog):
+                if ln.startswith("{"):
+                    line = json.loads(ln)
+        if line:
+            json.dump(line, open(os.path.join(OUT, f"{tag}_bench_c{cfg}.json"), "w"))
+        rep = os.path.join(EV, f"{tag}_c{cfg}_k_tasks.ncu-rep")
+        tr = None
+        if os.path.exists(rep):
+            text, tr, dur = summarize_ncu(rep, cfg, tag)
+            open(os.path.join(OUT, f"{tag}_ncu_k_tasks_c{cfg}.md"), "w").write(text)
+            traffic[str(cfg)] = {"dram_bytes_per_launch": tr, "ncu_duration_ms": dur,
+                                 "source": f"profiles/{tag}_ncu_k_tasks_c{cfg}.md (dram__bytes_read.sum + "
+                                           "dram__bytes_write.sum, one ncu --set full capture)"}
+        lpath = os.path.join(EV, f"{tag}_launches_c{cfg}.csv")
+        if os.path.exists(lpath):
+            open(os.path.join(OUT, f"{tag}_launches_c{cfg}.md"), "w").write(
+                f"# ncu launch list, config C{cfg} ({tag})\n\n`ncu --metrics gpu__time_duration.sum --clock-control "
+                f"none python bench.py --config {cfg} --steps 3 --warmup 3 --no-extras` -- cold-cache, serialised "
+                f"per-launch times: compare shares, not absolutes\n\n" + summarize_launches(lpath))
+        if line:
+            rf = line.get("roofline", {})
+            rows.append((cfg, line, rf, tr))
+    json.dump(traffic, open(os.path.join(OUT, "traffic.json"), "w"), indent=1)
+    print(json.dumps(traffic, indent=1))
+    for cfg, line, rf, tr in rows:
+        print(cfg, f"{line['value']:.4g} elem/s", f"{line['ms_per_step']:.4f} ms", f"{line.get('achieved_hbm_gbs', 0):.0f} GB/s",
+              f"K2 {rf.get('achieved', 0):.0f} GB/s frac {rf.get('frac', 0):.3f}", "traffic", tr,
+              "alg", rf.get("algorithmic_bytes_per_launch"))
+
+
+if __name__ == "__main__":
+    main(sys.argv[1] if len(sys.argv) > 1 else "r01")

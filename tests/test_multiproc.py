@@ -1,0 +1,73 @@
+"""N>1 host logic of bench.py on CPU with the gloo backend (world size 2).
+
+The metric is quoted at one GPU; N>1 runs are replicas only:
+each rank merges its own seeded replica, there is no collective on the data
+path, and the reported value is all ranks' elements over the max-over-ranks
+device time.  These tests cover that logic without a GPU.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import bench
+import oracle
+import synth
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _worker(rank, world, port, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        # per-rank device time: the job value must use the slowest rank
+        t_ms = 10.0 * (rank + 1)
+        t_max = bench.max_over_ranks(t_ms, world, device="cpu")
+        # replicas: distinct seeded inputs, each merged independently
+        seed = bench.rank_seed(2, rank)
+        inp = synth.merge_input(3000, 2000, "i32", "full", seed, payload=True)
+        ck, cv = oracle.merge(inp.a_keys, inp.a_vals, inp.b_keys, inp.b_vals, "i32")
+        digest = torch.tensor([int(np.int64(ck.astype(np.int64).sum()))], dtype=torch.int64)
+        gathered = [torch.zeros_like(digest) for _ in range(world)]
+        dist.all_gather(gathered, digest)
+        dist.barrier()
+        out.put((rank, t_max, seed, [int(g.item()) for g in gathered],
+                 bool(np.all(ck[1:] >= ck[:-1])), int(cv.size)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.timeout(180)
+def test_gloo_world2_replicas_and_max_over_ranks():
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=150) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert [r[1] for r in res] == [20.0, 20.0]                 # max over ranks, seen by every rank
+    assert res[0][2] != res[1][2]                              # distinct replica seeds
+    assert res[0][3] == res[1][3] and res[0][3][0] != res[0][3][1]   # distinct replicas, same view
+    assert all(r[4] and r[5] == 5000 for r in res)
+
+
+def test_aggregate_value_is_whole_job():
+    # 2 ranks x 1000 elements x 10 steps in 20 ms (max over ranks) = 1e6 elements/s
+    assert bench.aggregate_value(1000, 2, 10, 20.0) == pytest.approx(1e6)
+    assert bench.max_over_ranks(3.5, 1) == 3.5
