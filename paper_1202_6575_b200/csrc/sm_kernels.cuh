@@ -180,94 +180,6 @@ struct TileSmem {
     uint32_t vals[HAS_V ? NV : 1];
 };
 
-// Merge-path split of diagonal d between sorted a[0,la) and b[0,lb):
-// smallest i with a[i] > b[d-1-i] (reading R17: advance while
-// a[mid] <= b[d-1-mid], so equal keys go to A).
-template <typename K>
-__device__ __forceinline__ int split_ab(const K* a, int la, const K* b, int lb, int d) {
-    int lo = max(0, d - lb), hi = min(d, la);
-    while (lo < hi) {
-        const int mid = (lo + hi) >> 1;
-        if (a[mid] <= b[d - 1 - mid]) lo = mid + 1;
-        else hi = mid;
-    }
-    return lo;
-}
-
-// Serial stable merge of VT outputs from (ai, bi), la >= 1 and lb >= 1;
-// ties take A.  src[k] = smem payload index of output k (va + ai or vb + bi).
-template <typename K, int VT, bool IDX>
-__device__ __forceinline__ void merge_serial(const K* a, int ai, int la, const K* b, int bi, int lb, int va, int vb,
-                                             K (&out)[VT], int (&src)[VT]) {
-    K ka = a[min(ai, la - 1)];
-    K kb = b[min(bi, lb - 1)];
-#pragma unroll
-    for (int k = 0; k < VT; ++k) {
-        const bool takeA = (bi >= lb) || (ai < la && ka <= kb);
-        out[k] = takeA ? ka : kb;
-        if (IDX) src[k] = takeA ? va + ai : vb + bi;
-        if (takeA) {
-            ++ai;
-            ka = a[min(ai, la - 1)];
-        } else {
-            ++bi;
-            kb = b[min(bi, lb - 1)];
-        }
-    }
-}
-
-// Branch-free merge-path split (reading R17): smallest i in
-// [max(0, d-lb), min(d, la)] with a[i] > b[d-1-i], by binary lifting over
-// powers of two (LOG2 + 1 predicated probes, no data-dependent branch).
-// The predicate a[i] <= b[d-1-i] is monotone in i (true, then false).
-template <typename K, int LOG2>
-__device__ __forceinline__ int split_lift(const K* a, int la, const K* b, int lb, int d) {
-    const int lo = max(0, d - lb);
-    int rem = min(d, la) - lo;             // candidates left: a[lo .. lo+rem)
-    const K* pa = a + lo;                  // a[i]
-    const K* pb = b + (d - 1 - lo);        // b[d-1-i]
-#pragma unroll
-    for (int s = LOG2; s >= 0; --s) {
-        const int step = 1 << s;
-        if (step <= rem && pa[step - 1] <= pb[1 - step]) {
-            pa += step;
-            pb -= step;
-            rem -= step;
-        }
-    }
-    return (int)(pa - a);
-}
-
-// Serial stable merge of VT outputs starting at (ai, bi), la >= 1, lb >= 1:
-// take A when its key <= B's (ties to A).  Reads one element past the end
-// of a range at most (inside the stage, never selected).  With IDX, src[k]
-// is the stage payload index of output k (va + ai or vb + bi).
-template <typename K, int VT, bool IDX>
-__device__ __forceinline__ void merge_lean(const K* a, int ai, int la, const K* b, int bi, int lb, int va, int vb,
-                                           K (&out)[VT], int (&src)[VT]) {
-    const K* pa = a + ai;
-    const K* pb = b + bi;
-    const K* const pae = a + la;
-    const K* const pbe = b + lb;
-    int ia = va + ai, ib = vb + bi;
-    K ka = *pa, kb = *pb;
-#pragma unroll
-    for (int k = 0; k < VT; ++k) {
-        const bool takeA = pb >= pbe || (pa < pae && ka <= kb);
-        out[k] = takeA ? ka : kb;
-        if (IDX) src[k] = takeA ? ia : ib;
-        if (takeA) {
-            ++pa;
-            ka = *pa;
-            if (IDX) ++ia;
-        } else {
-            ++pb;
-            kb = *pb;
-            if (IDX) ++ib;
-        }
-    }
-}
-
 // ----------------------------------------------------------------- K2
 // A ring stage holds the input ranges of up to MAXT tasks ("packing"): the
 // paper's subproblems range from O(1) to ~2T elements (L388-393), so one task
@@ -279,26 +191,39 @@ struct TaskDesc {
     int la, lb;        // lengths of the A and B ranges
     int a_s, b_s;      // stage key index of A[a0] / B[b0]
     int va_s, vb_s;    // stage payload index of vA[a0] / vB[b0]
-    int ob, obv;       // stage index where output key / payload 0 of the task goes
+    int ob, obv;       // (in-place store) stage index of output key / payload 0 of the task
     int off;           // global output element index (segment base + a0 + b0)
     int pst;           // first padded diagonal of the task in the stage
 };
 
-template <typename K, bool HAS_V, int NC, int VT, int STAGES, int MAXT>
+// WB = false: outputs are written back in place into the stage and a storer
+// warp bulk-stores them (the stage is held until its bulk reads complete).
+// WB = true: every consumer warp writes its outputs into a private buffer and
+// bulk-stores them itself; the stage is freed as soon as all consumer warps
+// have read it, and no CTA-wide barrier is needed.
+template <typename K, bool HAS_V, int NC, int VT, int STAGES, int MAXT, bool WB>
 struct K2Layout {
     static constexpr int NV = NC * VT;                     // padded diagonals per stage
     static constexpr int KB = (int)sizeof(K);
+    static constexpr int EPV = 16 / KB;                    // keys per 16 bytes
     // Task k's key region: its A span and B span (16-byte aligned supersets,
-    // <= L*KB + 2*30 bytes) plus 16 bytes, so that its output, phase-aligned
-    // to the destination address, fits in the same region (written in place
-    // after every thread has read its inputs).
+    // <= L*KB + 2*30 bytes) plus 16 bytes: room for the in-place output
+    // phase-aligned to the destination, and for the merge's look-ahead reads
+    // past the end of a range.
     static constexpr int KREG = NV * KB + MAXT * 80;
     static constexpr int VREG = HAS_V ? NV * 4 + MAXT * 80 : 0;
     static constexpr int STAGE_BYTES = KREG + VREG;
-    static constexpr int OFF_DESC = STAGES * STAGE_BYTES;
+    // per-warp output buffer (WB): 32 lanes x VT outputs + a 16-byte phase
+    // slack per segment (at most 32 segments)
+    static constexpr int WBK = WB ? 32 * VT + 32 * EPV : 0;
+    static constexpr int WBV = (WB && HAS_V) ? 32 * VT + 32 * 4 : 0;
+    static constexpr int WB_BYTES = ((WBK * KB + WBV * 4) + 15) & ~15;
+    static constexpr int OFF_WB = STAGES * STAGE_BYTES;
+    static constexpr int OFF_DESC = OFF_WB + (NC / 32) * WB_BYTES;
     static constexpr int OFF_PST = OFF_DESC + STAGES * MAXT * (int)sizeof(TaskDesc);
     static constexpr int OFF_BAR = ((OFF_PST + STAGES * (MAXT + 2) * 4) + 15) & ~15;
     static constexpr int SMEM = OFF_BAR + 3 * STAGES * 8;   // full, empty, written
+    static constexpr int THREADS = NC + (WB ? 32 : 64);    // producer (+ storer) + consumers
 };
 
 // Bytes of the 16-byte-aligned superset of p[0, len).
@@ -324,7 +249,7 @@ __device__ __forceinline__ int phase_of(const T* p) {
     return (int)(((uintptr_t)p & 15) / sizeof(T));
 }
 
-// Store stage elements sbuf[o, o+L) to dst[0, L): the 16-byte-aligned middle
+// Store smem elements sbuf[o, o+L) to dst[0, L): the 16-byte-aligned middle
 // with one bulk copy (issued by the calling thread).
 template <typename T>
 __device__ __forceinline__ void store_middle(T* dst, const T* sbuf, int o, int L) {
@@ -348,40 +273,224 @@ __device__ __forceinline__ void store_edge(T* dst, const T* sbuf, int o, int L, 
     if (e < L && (r < head || e >= tail0)) dst[e] = sbuf[o + e];
 }
 
+// ---- producer (warp 0): classify, pack, bulk-load (rows a4/a5) ----------
+// Its lanes classify a window of up to 32 tasks of this CTA in parallel
+// (O(1) each, L310-340); a prefix of the window whose padded sizes fit NV
+// goes into the next ring stage; every packed task's lane issues the TMA bulk
+// loads of its A and B ranges (keys, payloads).  A stage with task count -1
+// terminates the consumers.
+template <typename K, bool HAS_V, int VT, int STAGES, int MAXT, typename Lay>
+__device__ __forceinline__ void k2_producer(const K* __restrict__ A, const uint32_t* __restrict__ vA,
+                                            const K* __restrict__ B, const uint32_t* __restrict__ vB,
+                                            const K* C, const uint32_t* vC, const Geom& g,
+                                            const int* __restrict__ xbar, const int* __restrict__ ybar, char* smem,
+                                            TaskDesc* desc, int* pst, uint64_t* full, uint64_t* empty) {
+    constexpr int NV = Lay::NV;
+    constexpr int KB = Lay::KB;
+    constexpr int EPV = Lay::EPV;
+    const int ntasks = g.S * (g.pA + g.pB);
+    const int lane = threadIdx.x;
+    int la = 0, lb = 0, off = 0, ag = 0, bg = 0;   // window slot `lane`
+    int cnt = 0;                                    // slots [0, cnt) hold tasks
+    int next = blockIdx.x;                          // next task of this CTA
+    for (int it = 0;; ++it) {
+        if (cnt < MAXT && next < ntasks) {
+            const int my = next + (lane - cnt) * (int)gridDim.x;
+            const bool fill = lane >= cnt && my < ntasks;
+            if (fill) {
+                Seg sg;
+                const Task t = decode_task(g, my, xbar, ybar, sg);
+                la = t.a1 - t.a0;
+                lb = t.b1 - t.b0;
+                off = sg.coff + t.a0 + t.b0;
+                ag = sg.aoff + t.a0;
+                bg = sg.boff + t.b0;
+            }
+            next += (32 - cnt) * (int)gridDim.x;
+            cnt += __popc(__ballot_sync(0xffffffffu, fill));
+        }
+        const int st = it % STAGES;
+        if (it >= STAGES) mbar_wait(&empty[st], ((it / STAGES) - 1) & 1);
+        int* ps = pst + st * (MAXT + 2);
+        if (cnt == 0) {                             // no task left: terminate the consumers
+            if (lane == 0) {
+                ps[MAXT + 1] = -1;
+                mbar_arrive(&full[st]);
+            }
+            return;
+        }
+        // pack the longest prefix of the window with sum of padded sizes <= NV
+        const int L = la + lb;
+        const int P = lane < cnt ? ((L + VT - 1) / VT) * VT : NV + 1;
+        int incl = P;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int t = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += t;
+        }
+        const bool take_me = lane < cnt && lane < MAXT && incl <= NV;
+        const int take = __popc(__ballot_sync(0xffffffffu, take_me));
+        // stage byte offsets of each packed task's key / payload region
+        const int kreg = take_me ? span_bytes(A + ag, la) + span_bytes(B + bg, lb) + 16 : 0;
+        const int vreg = (HAS_V && take_me) ? span_bytes(vA + ag, la) + span_bytes(vB + bg, lb) + 16 : 0;
+        int kat = kreg, vat = vreg;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int t1 = __shfl_up_sync(0xffffffffu, kat, o);
+            const int t2 = __shfl_up_sync(0xffffffffu, vat, o);
+            if (lane >= o) { kat += t1; vat += t2; }
+        }
+        kat -= kreg;                                 // exclusive
+        vat -= vreg;
+        const int ktot = __shfl_sync(0xffffffffu, kat + kreg, take - 1);
+        const int vtot = __shfl_sync(0xffffffffu, vat + vreg, take - 1);
+        char* stage = smem + st * Lay::STAGE_BYTES;
+        char* vstage = stage + Lay::KREG;
+        if (take_me) {
+            TaskDesc d;
+            d.la = la;
+            d.lb = lb;
+            d.off = off;
+            d.pst = incl - P;
+            d.a_s = issue_span(stage, kat, A + ag, la, &full[st]);
+            d.b_s = issue_span(stage, kat + span_bytes(A + ag, la), B + bg, lb, &full[st]);
+            // in-place output position: where a copy's source already has the
+            // destination's 16-byte phase, else phase-aligned at the region start
+            const int phC = phase_of(C + off);
+            if (lb == 0 && (d.a_s & (EPV - 1)) == phC) d.ob = d.a_s;
+            else if (la == 0 && (d.b_s & (EPV - 1)) == phC) d.ob = d.b_s;
+            else d.ob = kat / KB + phC;
+            d.va_s = d.vb_s = d.obv = 0;
+            if (HAS_V) {
+                d.va_s = issue_span(vstage, vat, vA + ag, la, &full[st]);
+                d.vb_s = issue_span(vstage, vat + span_bytes(vA + ag, la), vB + bg, lb, &full[st]);
+                const int phV = phase_of(vC + off);
+                if (lb == 0 && (d.va_s & 3) == phV) d.obv = d.va_s;
+                else if (la == 0 && (d.vb_s & 3) == phV) d.obv = d.vb_s;
+                else d.obv = vat / 4 + phV;
+            }
+            desc[st * MAXT + lane] = d;
+            if (lane == take - 1) {
+                ps[take] = incl;
+                ps[MAXT + 1] = take;
+            }
+            ps[lane] = incl - P;
+        }
+        // the descriptors are released by the arrive; the bulk loads may
+        // complete_tx before the expect_tx (the phase needs both)
+        __syncwarp();
+        if (lane == 0)
+            mbar_arrive_expect_tx(&full[st], (uint32_t)(ktot - 16 * take + (HAS_V ? vtot - 16 * take : 0)));
+        // drop the packed prefix from the window
+        la = __shfl_down_sync(0xffffffffu, la, take);
+        lb = __shfl_down_sync(0xffffffffu, lb, take);
+        off = __shfl_down_sync(0xffffffffu, off, take);
+        ag = __shfl_down_sync(0xffffffffu, ag, take);
+        bg = __shfl_down_sync(0xffffffffu, bg, take);
+        cnt -= take;
+    }
+}
+
+// ---- consumer compute (rows a6/a7) ----------------------------------------
+// Thread with padded diagonal D of stage s: its task (binary search over the
+// packed tasks' first diagonals), its diagonal d inside the task, and its
+// cnt <= VT outputs in registers.  Returns false when D lies in no task.
+//   copy = the task is a copy (cases a, e) and out/v were not filled because
+//          the in-place store needs no movement (INPLACE only).
+template <typename K, bool HAS_V, int VT, int MAXT, int LOG2NV, bool INPLACE>
+__device__ __forceinline__ bool k2_compute(const K* sk, const uint32_t* sv, const TaskDesc* desc_s, const int* ps,
+                                           int nt, int D, TaskDesc& td, int& d, int& cnt, bool& write, K (&out)[VT],
+                                           uint32_t (&v)[HAS_V ? VT : 1]) {
+    constexpr int KB = (int)sizeof(K);
+    write = false;
+    cnt = 0;
+    if (D >= ps[nt]) return false;
+    int lo = 0, hi = nt - 1;                       // task k: last with pst[k] <= D
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (ps[mid] <= D) lo = mid;
+        else hi = mid - 1;
+    }
+    td = desc_s[lo];
+    d = D - td.pst;
+    cnt = min(VT, td.la + td.lb - d);
+    if (cnt <= 0) return true;
+    if (td.la > 0 && td.lb > 0) {
+        // cases (b), (c), (d): stable merge (row a7), ties to A (R17)
+        const uint32_t sa0 = smem_addr(sk + td.a_s);
+        const uint32_t sb0 = smem_addr(sk + td.b_s);
+        const int ai = split_smem<K, LOG2NV>(sa0, td.la, sb0, td.lb, d);
+        const int bi = d - ai;
+        uint32_t pa = sa0 + ai * KB, pb = sb0 + bi * KB;
+        const uint32_t pae = sa0 + td.la * KB, pbe = sb0 + td.lb * KB;
+        K ka = lds<K>(pa), kb = lds<K>(pb), na = lds<K>(pa + KB), nb = lds<K>(pb + KB);
+        int src[VT];
+        int ia = td.va_s + ai, ib = td.vb_s + bi;
+#pragma unroll
+        for (int k = 0; k < VT; ++k) {
+            if (HAS_V) merge_step_idx<K>(pa, pb, ka, kb, na, nb, pae, pbe, out[k], ia, ib, src[k]);
+            else merge_step<K>(pa, pb, ka, kb, na, nb, pae, pbe, out[k]);
+        }
+        if (HAS_V) {
+#pragma unroll
+            for (int k = 0; k < VT; ++k)
+                if (k < cnt) v[k] = sv[src[k]];
+        }
+        write = true;
+    } else {
+        // cases (a), (e): copy (row a6); in place: no movement when the source
+        // already has the destination's phase
+        const int ks = td.la ? td.a_s : td.b_s;
+        const int vs = td.la ? td.va_s : td.vb_s;
+        if (!INPLACE || ks != td.ob || (HAS_V && vs != td.obv)) {
+#pragma unroll
+            for (int k = 0; k < VT; ++k) {
+                if (k < cnt) {
+                    out[k] = sk[ks + d + k];
+                    if (HAS_V) v[k] = sv[vs + d + k];
+                }
+            }
+            write = true;
+        }
+    }
+    return true;
+}
+
 // K2 (rows a4-a7): persistent, warp-specialised.
-//   warp 0 (producer): its lanes classify a window of up to 32 tasks of this
-//     CTA in parallel (O(1) each, L310-340), pack a prefix of the window into
-//     the next ring stage and bulk-load every packed task's A and B ranges
-//     (keys, payloads) with the TMA engine (full[s]).
-//   warps 2.. (NC consumers): merge (cases b, c, d) or realign (copies,
-//     cases a, e) their VT diagonals into registers and write them back in
-//     place, phase-aligned to the destination (written[s]).
-//   warp 1 (storer): bulk-stores each task's 16-byte-aligned middle, plain
-//     stores for the edge elements, and frees the stage as soon as the bulk
-//     stores have read it (empty[s]), so consumers never wait on the stores.
-template <typename K, bool HAS_V, int NC, int VT, int STAGES, int MAXT>
-__global__ void __launch_bounds__(NC + 64) k_tasks(const K* __restrict__ A, const uint32_t* __restrict__ vA,
-                                                   const K* __restrict__ B, const uint32_t* __restrict__ vB,
-                                                   K* __restrict__ C, uint32_t* __restrict__ vC, Geom g,
-                                                   const int* __restrict__ xbar, const int* __restrict__ ybar) {
-    using Lay = K2Layout<K, HAS_V, NC, VT, STAGES, MAXT>;
-    static_assert(NC % 32 == 0 && MAXT <= 32, "warp-granular roles; one producer lane per packed task");
+//   warp 0 (producer): k2_producer above (full[s]).
+//   consumers (NC threads): k2_compute, then
+//     WB = false: write back in place (phase-aligned to the destination) and
+//       hand the stage to warp 1 (storer), which bulk-stores each task's
+//       16-byte-aligned middle, plain-stores the edge elements and frees the
+//       stage once the bulk reads complete (written[s] -> empty[s]);
+//     WB = true: free the stage at once (empty[s], one arrival per warp),
+//       write the outputs into the warp's private buffer, each segment of
+//       consecutive lanes of one task placed at the destination's 16-byte
+//       phase, and bulk-store the segments from there (segment leader lane).
+template <typename K, bool HAS_V, int NC, int VT, int STAGES, int MAXT, bool WB>
+__global__ void __launch_bounds__(K2Layout<K, HAS_V, NC, VT, STAGES, MAXT, WB>::THREADS)
+    k_tasks(const K* __restrict__ A, const uint32_t* __restrict__ vA, const K* __restrict__ B,
+            const uint32_t* __restrict__ vB, K* __restrict__ C, uint32_t* __restrict__ vC, Geom g,
+            const int* __restrict__ xbar, const int* __restrict__ ybar) {
+    using Lay = K2Layout<K, HAS_V, NC, VT, STAGES, MAXT, WB>;
+    static_assert(NC % 32 == 0 && MAXT <= 32 && STAGES >= 2, "warp-granular roles; one producer lane per task");
     constexpr int NV = Lay::NV;
     constexpr int LOG2NV = 31 - __builtin_clz(NV);   // 2^(LOG2NV+1) - 1 >= NV probes cover any range
-    constexpr int KB = Lay::KB;
-    constexpr int EPV = 16 / KB;
+    constexpr int EPV = Lay::EPV;
+    constexpr int EK = 2 * (EPV - 1);                // key edge elements per store
+    constexpr int EV = HAS_V ? 6 : 0;                // payload edge elements per store
+    constexpr int FIRST = WB ? 32 : 64;              // first consumer thread
     extern __shared__ __align__(128) char smem[];
     TaskDesc* desc = (TaskDesc*)(smem + Lay::OFF_DESC);
-    int* pst = (int*)(smem + Lay::OFF_PST);              // [STAGES][MAXT + 2]: pst[0..nt], nt at MAXT+1
+    int* pst = (int*)(smem + Lay::OFF_PST);          // [STAGES][MAXT + 2]: pst[0..nt], nt at MAXT+1
     uint64_t* full = (uint64_t*)(smem + Lay::OFF_BAR);
     uint64_t* empty = full + STAGES;
     uint64_t* written = empty + STAGES;
-    const int ntasks = g.S * (g.pA + g.pB);
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], 1);
+            mbar_init(&empty[s], WB ? NC / 32 : 1);
             mbar_init(&written[s], NC / 32);
         }
         fence_barrier_init();
@@ -391,117 +500,14 @@ __global__ void __launch_bounds__(NC + 64) k_tasks(const K* __restrict__ A, cons
     pdl_wait();   // the single synchronisation (L373-375): all ranks visible
 
     if (threadIdx.x < 32) {
-        // ------------------------------------------------------ producer
-        const int lane = threadIdx.x;
-        int la = 0, lb = 0, off = 0, ag = 0, bg = 0;   // window slot `lane`
-        int cnt = 0;                                    // slots [0, cnt) hold tasks
-        int next = blockIdx.x;                          // next task of this CTA
-        int it = 0;
-        for (;;) {
-            if (cnt < MAXT && next < ntasks) {
-                const int my = next + (lane - cnt) * (int)gridDim.x;
-                const bool fill = lane >= cnt && my < ntasks;
-                if (fill) {
-                    Seg sg;
-                    const Task t = decode_task(g, my, xbar, ybar, sg);
-                    la = t.a1 - t.a0;
-                    lb = t.b1 - t.b0;
-                    off = sg.coff + t.a0 + t.b0;
-                    ag = sg.aoff + t.a0;
-                    bg = sg.boff + t.b0;
-                }
-                next += (32 - cnt) * (int)gridDim.x;
-                cnt += __popc(__ballot_sync(0xffffffffu, fill));
-            }
-            const int st = it % STAGES;
-            if (it >= STAGES) mbar_wait(&empty[st], ((it / STAGES) - 1) & 1);
-            int* ps = pst + st * (MAXT + 2);
-            if (cnt == 0) {                             // no task left: terminate the consumers
-                if (lane == 0) {
-                    ps[MAXT + 1] = -1;
-                    mbar_arrive(&full[st]);
-                }
-                break;
-            }
-            // pack the longest prefix of the window with sum of padded sizes <= NV
-            const int L = la + lb;
-            const int P = lane < cnt ? ((L + VT - 1) / VT) * VT : NV + 1;
-            int incl = P;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const int t = __shfl_up_sync(0xffffffffu, incl, o);
-                if (lane >= o) incl += t;
-            }
-            const bool take_me = lane < cnt && lane < MAXT && incl <= NV;
-            const int take = __popc(__ballot_sync(0xffffffffu, take_me));
-            // stage byte offsets of each packed task's key / payload region
-            const int kreg = take_me ? span_bytes(A + ag, la) + span_bytes(B + bg, lb) + 16 : 0;
-            const int vreg = (HAS_V && take_me) ? span_bytes(vA + ag, la) + span_bytes(vB + bg, lb) + 16 : 0;
-            int kat = kreg, vat = vreg;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const int t1 = __shfl_up_sync(0xffffffffu, kat, o);
-                const int t2 = __shfl_up_sync(0xffffffffu, vat, o);
-                if (lane >= o) { kat += t1; vat += t2; }
-            }
-            kat -= kreg;                                 // exclusive
-            vat -= vreg;
-            const int ktot = __shfl_sync(0xffffffffu, kat + kreg, take - 1);
-            const int vtot = __shfl_sync(0xffffffffu, vat + vreg, take - 1);
-            char* stage = smem + st * Lay::STAGE_BYTES;
-            char* vstage = stage + Lay::KREG;
-            if (take_me) {
-                TaskDesc d;
-                d.la = la;
-                d.lb = lb;
-                d.off = off;
-                d.pst = incl - P;
-                d.a_s = issue_span(stage, kat, A + ag, la, &full[st]);
-                d.b_s = issue_span(stage, kat + span_bytes(A + ag, la), B + bg, lb, &full[st]);
-                // output position: in place for a copy whose source already has the
-                // destination's 16-byte phase, else phase-aligned at the region start
-                const int phC = phase_of(C + off);
-                if (lb == 0 && (d.a_s & (EPV - 1)) == phC) d.ob = d.a_s;
-                else if (la == 0 && (d.b_s & (EPV - 1)) == phC) d.ob = d.b_s;
-                else d.ob = kat / KB + phC;
-                d.va_s = d.vb_s = d.obv = 0;
-                if (HAS_V) {
-                    d.va_s = issue_span(vstage, vat, vA + ag, la, &full[st]);
-                    d.vb_s = issue_span(vstage, vat + span_bytes(vA + ag, la), vB + bg, lb, &full[st]);
-                    const int phV = phase_of(vC + off);
-                    if (lb == 0 && (d.va_s & 3) == phV) d.obv = d.va_s;
-                    else if (la == 0 && (d.vb_s & 3) == phV) d.obv = d.vb_s;
-                    else d.obv = vat / 4 + phV;
-                }
-                desc[st * MAXT + lane] = d;
-                if (lane == take - 1) {
-                    ps[take] = incl;
-                    ps[MAXT + 1] = take;
-                }
-                ps[lane] = incl - P;
-            }
-            // the descriptors are released by the arrive; the bulk loads may
-            // complete_tx before the expect_tx (the phase needs both)
-            __syncwarp();
-            if (lane == 0)
-                mbar_arrive_expect_tx(&full[st], (uint32_t)(ktot - 16 * take + (HAS_V ? vtot - 16 * take : 0)));
-            // drop the packed prefix from the window
-            la = __shfl_down_sync(0xffffffffu, la, take);
-            lb = __shfl_down_sync(0xffffffffu, lb, take);
-            off = __shfl_down_sync(0xffffffffu, off, take);
-            ag = __shfl_down_sync(0xffffffffu, ag, take);
-            bg = __shfl_down_sync(0xffffffffu, bg, take);
-            cnt -= take;
-            ++it;
-        }
+        k2_producer<K, HAS_V, VT, STAGES, MAXT, Lay>(A, vA, B, vB, C, vC, g, xbar, ybar, smem, desc, pst, full,
+                                                    empty);
         return;
     }
 
-    if (threadIdx.x < 64) {
+    if (!WB && threadIdx.x < 64) {
         // -------------------------------------------------------- storer
         const int lane = threadIdx.x - 32;
-        constexpr int EK = 2 * (EPV - 1);              // key edge elements per task
-        constexpr int EV = HAS_V ? 6 : 0;              // payload edge elements per task
         for (int it = 0;; ++it) {
             const int s = it % STAGES;
             mbar_wait(&written[s], (it / STAGES) & 1);
@@ -533,90 +539,96 @@ __global__ void __launch_bounds__(NC + 64) k_tasks(const K* __restrict__ A, cons
     }
 
     // ---------------------------------------------------------- consumers
-    const int c = threadIdx.x - 64;
+    const int c = threadIdx.x - FIRST;
     const int lane = threadIdx.x & 31;
+    K* wk = (K*)(smem + Lay::OFF_WB + (c >> 5) * Lay::WB_BYTES);   // WB: this warp's buffer
+    uint32_t* wv = (uint32_t*)(wk + Lay::WBK);
     for (int it = 0;; ++it) {
         const int s = it % STAGES;
         mbar_wait(&full[s], (it / STAGES) & 1);
         const int* ps = pst + s * (MAXT + 2);
         const int nt = ps[MAXT + 1];
         if (nt < 0) {
-            if (lane == 0) mbar_arrive(&written[s]);   // pass the termination on to the storer
+            if (!WB && lane == 0) mbar_arrive(&written[s]);   // pass the termination on to the storer
             break;
         }
         K* sk = (K*)(smem + s * Lay::STAGE_BYTES);
         uint32_t* sv = (uint32_t*)(smem + s * Lay::STAGE_BYTES + Lay::KREG);
-        const int D = c * VT;
         TaskDesc td;
-        int d = 0, cntk = 0;
+        int d = 0, cnt = 0;
+        bool write = false;
         K out[VT];
         uint32_t v[HAS_V ? VT : 1];
-        bool write = false;
-        if (D < ps[nt]) {
-            int lo = 0, hi = nt - 1;                   // task k: last with pst[k] <= D
-            while (lo < hi) {
-                const int mid = (lo + hi + 1) >> 1;
-                if (ps[mid] <= D) lo = mid;
-                else hi = mid - 1;
-            }
-            td = desc[s * MAXT + lo];
-            d = D - td.pst;
-            const int L = td.la + td.lb;
-            cntk = min(VT, L - d);
-            if (cntk > 0) {
-                if (td.la > 0 && td.lb > 0) {
-                    // cases (b), (c), (d): stable merge (row a7), ties to A (R17)
-                    const uint32_t sa0 = smem_addr(sk + td.a_s);
-                    const uint32_t sb0 = smem_addr(sk + td.b_s);
-                    const int ai = split_smem<K, LOG2NV>(sa0, td.la, sb0, td.lb, d);
-                    const int bi = d - ai;
-                    uint32_t pa = sa0 + ai * KB, pb = sb0 + bi * KB;
-                    const uint32_t pae = sa0 + td.la * KB, pbe = sb0 + td.lb * KB;
-                    K ka = lds<K>(pa), kb = lds<K>(pb), na = lds<K>(pa + KB), nb = lds<K>(pb + KB);
-                    int src[VT];
-                    int ia = td.va_s + ai, ib = td.vb_s + bi;
+        const bool mine = k2_compute<K, HAS_V, VT, MAXT, LOG2NV, !WB>(sk, sv, desc + s * MAXT, ps, nt, c * VT, td, d,
+                                                                       cnt, write, out, v);
+        if (!WB) {
+            named_sync(1, NC);                         // every input of the stage has been read
+            if (write) {
 #pragma unroll
-                    for (int k = 0; k < VT; ++k) {
-                        if (HAS_V) merge_step_idx<K>(pa, pb, ka, kb, na, nb, pae, pbe, out[k], ia, ib, src[k]);
-                        else merge_step<K>(pa, pb, ka, kb, na, nb, pae, pbe, out[k]);
-                    }
-                    if (HAS_V) {
-#pragma unroll
-                        for (int k = 0; k < VT; ++k)
-                            if (k < cntk) v[k] = sv[src[k]];
-                    }
-                    write = true;
-                } else {
-                    // cases (a), (e): copy (row a6); realign unless already in place
-                    const int ks = td.la ? td.a_s : td.b_s;
-                    const int vs = td.la ? td.va_s : td.vb_s;
-                    if (ks != td.ob || (HAS_V && vs != td.obv)) {
-#pragma unroll
-                        for (int k = 0; k < VT; ++k) {
-                            if (k < cntk) {
-                                out[k] = sk[ks + d + k];
-                                if (HAS_V) v[k] = sv[vs + d + k];
-                            }
-                        }
-                        write = true;
+                for (int k = 0; k < VT; ++k) {
+                    if (k < cnt) {
+                        sk[td.ob + d + k] = out[k];
+                        if (HAS_V) sv[td.obv + d + k] = v[k];
                     }
                 }
             }
+            fence_proxy_async();                       // generic writes -> the storer's bulk reads
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&written[s]);
+            continue;
         }
-        named_sync(1, NC);                             // every input of the stage has been read
-        if (write) {
+        // WB: this warp is done with the stage
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+        // segments: maximal runs of lanes of one task with outputs
+        const bool has = mine && cnt > 0;
+        const int task_id = has ? td.pst : -1;           // unique per task within the stage
+        const int prev_id = __shfl_up_sync(0xffffffffu, task_id, 1);
+        const bool lead = has && (lane == 0 || prev_id != task_id);
+        const unsigned leads = __ballot_sync(0xffffffffu, lead);
+        const unsigned le_mask = 0xffffffffu >> (31 - lane);
+        const int l0 = 31 - __clz(leads & le_mask);       // this lane's segment leader (valid if has)
+        const int seg = __popc(leads & le_mask) - 1;
+        const int d0 = __shfl_sync(0xffffffffu, d, has ? l0 : lane);
+        const int g0 = td.off + d0;                        // global index of the segment's first output
+        int pk = 0, pv = 0;                                // buffer index of this lane's first output
+        if (has) {
+            const int phk = phase_of(C + g0);
+            const int bk = l0 * VT + seg * EPV;
+            pk = lane * VT + seg * EPV + (((phk - bk) % EPV) + EPV) % EPV;
+            if (HAS_V) {
+                const int phv = phase_of(vC + g0);
+                const int bv = l0 * VT + seg * 4;
+                pv = lane * VT + seg * 4 + (((phv - bv) % 4) + 4) % 4;
+            }
+        }
+        bulk_wait_read<0>();                               // this lane's previous stores have read the buffer
+        __syncwarp();
+        if (has) {
 #pragma unroll
             for (int k = 0; k < VT; ++k) {
-                if (k < cntk) {
-                    sk[td.ob + d + k] = out[k];
-                    if (HAS_V) sv[td.obv + d + k] = v[k];
+                if (k < cnt) {
+                    wk[pk + k] = out[k];
+                    if (HAS_V) wv[pv + k] = v[k];
                 }
             }
         }
-        fence_proxy_async();                           // generic writes -> the storer's bulk reads
+        fence_proxy_async();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&written[s]);
+        if (lead) {
+            const int n = min(td.la + td.lb - d0, (32 - l0) * VT);   // the segment's outputs
+            store_middle<K>(C + g0, wk, pk, n);
+            if (HAS_V) store_middle<uint32_t>(vC + g0, wv, pv, n);
+            bulk_commit();
+#pragma unroll
+            for (int r = 0; r < EK; ++r) store_edge<K>(C + g0, wk, pk, n, r);
+            if (HAS_V) {
+#pragma unroll
+                for (int r = 0; r < EV; ++r) store_edge<uint32_t>(vC + g0, wv, pv, n, r);
+            }
+        }
     }
+    if (WB) bulk_wait_read<0>();
 }
 
 // ----------------------------------------------------------- plan dump

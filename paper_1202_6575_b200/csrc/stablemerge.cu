@@ -38,6 +38,7 @@ struct K2Shape {
     static constexpr int bytes = (int)sizeof(K) + (HAS_V ? 4 : 0);
     static constexpr int NC = 256;
     static constexpr int VT = bytes <= 4 ? 31 : 15;
+    static constexpr bool WB = false;                 // per-warp output buffers (see k_tasks): measured slower
     static constexpr int STAGES = bytes <= 8 ? 3 : 4;
     static constexpr int NV = NC * VT;
     static constexpr int T = NV / 2;
@@ -161,8 +162,8 @@ static sm_status launch_merge(const K* A, const uint32_t* vA, const K* B, const 
     if (s != SM_OK) return s;
 
     using Sh = K2Shape<K, HAS_V>;
-    using Lay = K2Layout<K, HAS_V, Sh::NC, Sh::VT, Sh::STAGES, K2_MAXT>;
-    auto kern = k_tasks<K, HAS_V, Sh::NC, Sh::VT, Sh::STAGES, K2_MAXT>;
+    using Lay = K2Layout<K, HAS_V, Sh::NC, Sh::VT, Sh::STAGES, K2_MAXT, Sh::WB>;
+    auto kern = k_tasks<K, HAS_V, Sh::NC, Sh::VT, Sh::STAGES, K2_MAXT, Sh::WB>;
     static int per_sm = -1, n_sm = 0;
     if (per_sm < 0) {
         int dev = 0;
@@ -170,7 +171,7 @@ static sm_status launch_merge(const K* A, const uint32_t* vA, const K* B, const 
         cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Lay::SMEM);
         cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, Sh::NC + 64, Lay::SMEM);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, Lay::THREADS, Lay::SMEM);
         if (per_sm < 1) per_sm = 1;
     }
     const long long ntasks = (long long)g.S * (g.pA + g.pB);
@@ -178,7 +179,7 @@ static sm_status launch_merge(const K* A, const uint32_t* vA, const K* B, const 
     cudaLaunchConfig_t cfg;
     memset(&cfg, 0, sizeof(cfg));
     cfg.gridDim = dim3((unsigned)grid);
-    cfg.blockDim = dim3(Sh::NC + 64);
+    cfg.blockDim = dim3(Lay::THREADS);
     cfg.dynamicSmemBytes = Lay::SMEM;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
