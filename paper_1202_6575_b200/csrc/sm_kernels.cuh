@@ -134,52 +134,6 @@ __device__ __forceinline__ void cta_copy(const T* __restrict__ src, T* __restric
     }
 }
 
-// Merge-path split of diagonal d inside a shared-memory tile holding A at
-// [0, la) and B at [la, la+lb): smallest i with A[i] > B[d-1-i] (reading R17:
-// advance while A[mid] <= B[d-1-mid], so equal keys go to A).
-template <typename K>
-__device__ __forceinline__ int tile_split(const K* sk, int la, int lb, int d) {
-    int lo = max(0, d - lb), hi = min(d, la);
-    while (lo < hi) {
-        const int mid = (lo + hi) >> 1;
-        if (sk[mid] <= sk[la + d - 1 - mid]) lo = mid + 1;
-        else hi = mid;
-    }
-    return lo;
-}
-
-// Serial stable merge of VT outputs from the tile, starting at (ai, bi);
-// A occupies [.., aend), B [.., bend) of the same tile; ties take A.
-template <typename K, int VT>
-__device__ __forceinline__ void serial_merge(const K* sk, int ai, int aend, int bi, int bend, K (&out)[VT],
-                                             int (&src)[VT]) {
-    K ka = sk[0], kb = sk[0];
-    if (ai < aend) ka = sk[ai];
-    if (bi < bend) kb = sk[bi];
-#pragma unroll
-    for (int k = 0; k < VT; ++k) {
-        const bool takeA = (bi >= bend) || (ai < aend && ka <= kb);
-        out[k] = takeA ? ka : kb;
-        src[k] = takeA ? ai : bi;
-        if (takeA) {
-            ++ai;
-            if (ai < aend) ka = sk[ai];
-        } else {
-            ++bi;
-            if (bi < bend) kb = sk[bi];
-        }
-    }
-}
-
-// ----------------------------------------------------------------- K2
-// Shared-memory tile used by K3 (block sort).
-template <typename K, bool HAS_V, int NT, int VT>
-struct TileSmem {
-    static constexpr int NV = NT * VT;
-    K keys[NV];
-    uint32_t vals[HAS_V ? NV : 1];
-};
-
 // ----------------------------------------------------------------- K2
 // A ring stage holds the input ranges of up to MAXT tasks ("packing"): the
 // paper's subproblems range from O(1) to ~2T elements (L388-393), so one task
@@ -644,86 +598,191 @@ __global__ void k_plan_dump(Geom g, const int* __restrict__ xbar, const int* __r
 }
 
 // ----------------------------------------------------------------- K3
-// Stable block sort of runs of NT*VT elements (row a8).  A partial last run
-// is padded with the maximum key AFTER the real elements: the sort is stable,
-// so padding stays behind every real element and is never stored.
+// Row a8 (§3: "sorting sequentially in parallel p
+// consecutive blocks"): a stable sort of each run of R = NT * IPT consecutive
+// elements, one CTA per run, in shared memory.  The paper leaves the block
+// sort open; a least-significant-digit radix sort is stable by construction
+// and costs a fixed number of passes whatever R, so the runs can be long
+// (fewer merge rounds, row a9).
+//   - keys are ranked through their unsigned view (sign bit flipped for
+//     signed keys, reading R16); 4-bit digits;
+//   - digits on which every key of the run agrees are skipped (the pass
+//     would be the identity);
+//   - blocked arrangement: thread t owns run positions [t*IPT, t*IPT+IPT)
+//     (IPT odd: conflict-free strided shared loads), counts its digits in two
+//     registers of packed 8-bit counters (its in-thread ranks), and one
+//     block-wide exclusive scan in (digit, thread) order gives every
+//     thread's base offset per digit -- equal digits keep sequence order;
+//   - a partial last run is padded with the maximum unsigned view AFTER the
+//     real elements: stability keeps the padding last, and it is never stored.
 template <typename K>
-__device__ __forceinline__ K key_max();
-template <> __device__ __forceinline__ uint32_t key_max<uint32_t>() { return 0xFFFFFFFFu; }
-template <> __device__ __forceinline__ int32_t key_max<int32_t>() { return 0x7FFFFFFF; }
-template <> __device__ __forceinline__ uint64_t key_max<uint64_t>() { return 0xFFFFFFFFFFFFFFFFull; }
-template <> __device__ __forceinline__ int64_t key_max<int64_t>() { return 0x7FFFFFFFFFFFFFFFll; }
+struct RadixView;
+template <> struct RadixView<uint32_t> { using U = uint32_t; static constexpr U flip = 0u; };
+template <> struct RadixView<int32_t> { using U = uint32_t; static constexpr U flip = 0x80000000u; };
+template <> struct RadixView<uint64_t> { using U = uint64_t; static constexpr U flip = 0ull; };
+template <> struct RadixView<int64_t> { using U = uint64_t; static constexpr U flip = 0x8000000000000000ull; };
 
-template <typename K, bool HAS_V, int NT, int VT>
+template <typename K, bool HAS_V, int NT, int IPT>
+struct K3Layout {
+    using U = typename RadixView<K>::U;
+    static constexpr int R = NT * IPT;
+    static constexpr int NW = NT / 32;
+    static constexpr int ND = 16;                        // 4-bit digits
+    static constexpr int ROW = ND + 1;                   // padded per-thread base row
+    static constexpr int OFF_V = 2 * R * (int)sizeof(U);
+    static constexpr int OFF_ROW = OFF_V + (HAS_V ? 2 * R * 4 : 0);
+    static constexpr int OFF_W = OFF_ROW + NT * ROW * 4; // warp totals [NW][ND]
+    static constexpr int OFF_RED = OFF_W + NW * ND * 4;
+    static constexpr int SMEM = OFF_RED + NW * 8 + 16;
+};
+
+// 16 packed 8-bit counters in two 64-bit words: field d of (lo, hi).
+__device__ __forceinline__ uint32_t cnt_get(uint64_t lo, uint64_t hi, int d) {
+    const uint64_t w = d < 8 ? lo : hi;
+    return (uint32_t)(w >> ((d & 7) * 8)) & 0xFFu;
+}
+
+template <typename K, bool HAS_V, int NT, int IPT>
 __global__ void __launch_bounds__(NT) k_block_sort(const K* __restrict__ in, const uint32_t* __restrict__ vin,
                                                    K* __restrict__ out, uint32_t* __restrict__ vout, int N) {
-    constexpr int NV = NT * VT;
-    __shared__ TileSmem<K, HAS_V, NT, VT> sm_;
-    const int tid = threadIdx.x;
-    const int base = blockIdx.x * NV;
-    const int len = min(NV, N - base);
+    using Lay = K3Layout<K, HAS_V, NT, IPT>;
+    using U = typename Lay::U;
+    constexpr int R = Lay::R, NW = Lay::NW, ND = Lay::ND, ROW = Lay::ROW;
+    constexpr int NDIG = (int)sizeof(U) * 2;             // 4-bit digits per key
+    constexpr U FLIP = RadixView<K>::flip;
+    static_assert(IPT % 2 == 1 && IPT < 256 && NT % 32 == 0 && NT >= 32, "odd IPT; 8-bit counters");
+    extern __shared__ __align__(16) char smem[];
+    U* ku0 = (U*)smem;
+    uint32_t* vv0 = (uint32_t*)(smem + Lay::OFF_V);
+    uint32_t* rowb = (uint32_t*)(smem + Lay::OFF_ROW);  // [NT][ROW] per-thread digit bases
+    uint32_t* wtot = (uint32_t*)(smem + Lay::OFF_W);    // [NW][ND] warp digit totals
+    U* red = (U*)(smem + Lay::OFF_RED);                  // [NW]
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const int base = blockIdx.x * R;
+    const int len = min(R, N - base);
 
+    {   // coalesced load, all loads in flight before the shared stores
+        U u[IPT];
+        uint32_t vl[HAS_V ? IPT : 1];
 #pragma unroll
-    for (int k = 0; k < VT; ++k) {
-        const int idx = k * NT + tid;
-        sm_.keys[idx] = idx < len ? ld_stream(in + base + idx) : key_max<K>();
-        if (HAS_V) sm_.vals[idx] = idx < len ? ld_stream(vin + base + idx) : 0u;
+        for (int k = 0; k < IPT; ++k) {
+            const int e = k * NT + tid;
+            u[k] = e < len ? ((U)ld_stream(in + base + e) ^ FLIP) : ~(U)0;
+            if (HAS_V) vl[k] = e < len ? ld_stream(vin + base + e) : 0u;
+        }
+#pragma unroll
+        for (int k = 0; k < IPT; ++k) {
+            ku0[k * NT + tid] = u[k];
+            if (HAS_V) vv0[k * NT + tid] = vl[k];
+        }
     }
     __syncthreads();
-
-    K k_[VT];
-    uint32_t v_[HAS_V ? VT : 1];
+    // digits on which the run's keys differ
+    U diff = 0;
+    {
+        const U first = ku0[0];
+        for (int e = tid; e < len; e += NT) diff |= ku0[e] ^ first;
 #pragma unroll
-    for (int k = 0; k < VT; ++k) {
-        k_[k] = sm_.keys[tid * VT + k];
-        if (HAS_V) v_[k] = sm_.vals[tid * VT + k];
+        for (int o = 16; o > 0; o >>= 1) diff |= __shfl_xor_sync(0xffffffffu, diff, o);
+        if (lane == 0) red[w] = diff;
+        __syncthreads();
+        diff = 0;
+#pragma unroll
+        for (int i = 0; i < NW; ++i) diff |= red[i];
     }
-    // odd-even transposition sort; swapping only on strict '>' keeps it stable
+
+    int cur = 0;
+    for (int dg = 0; dg < NDIG; ++dg) {
+        const int sh = dg * 4;
+        if (((diff >> sh) & 0xF) == 0) continue;       // every key of the run has this digit
+        const U* ks = ku0 + cur * R;
+        U* kd = ku0 + (cur ^ 1) * R;
+        const uint32_t* vs = vv0 + cur * R;
+        uint32_t* vd = vv0 + (cur ^ 1) * R;
+        // 1. this thread's items (blocked) and in-thread ranks
+        U key[IPT];
+        uint32_t val[HAS_V ? IPT : 1];
+        uint32_t rank[IPT];
+        uint64_t clo = 0, chi = 0;
 #pragma unroll
-    for (int pass = 0; pass < VT; ++pass) {
+        for (int k = 0; k < IPT; ++k) {
+            key[k] = ks[tid * IPT + k];
+            if (HAS_V) val[k] = vs[tid * IPT + k];
+            const int d = (int)(key[k] >> sh) & 0xF;
+            rank[k] = cnt_get(clo, chi, d);
+            const uint64_t inc = 1ull << ((d & 7) * 8);
+            if (d < 8) clo += inc;
+            else chi += inc;
+        }
+        // 2. warp-inclusive scan of the 16 counts, packed two 16-bit fields per word
+        uint32_t c[ND / 2], x[ND / 2];
 #pragma unroll
-        for (int i = pass & 1; i + 1 < VT; i += 2) {
-            if (k_[i + 1] < k_[i]) {
-                K tk = k_[i]; k_[i] = k_[i + 1]; k_[i + 1] = tk;
-                if (HAS_V) { uint32_t tv = v_[i]; v_[i] = v_[i + 1]; v_[i + 1] = tv; }
+        for (int i = 0; i < ND / 2; ++i) {
+            const uint32_t a0 = cnt_get(clo, chi, 2 * i), a1 = cnt_get(clo, chi, 2 * i + 1);
+            c[i] = a0 | (a1 << 16);
+            x[i] = c[i];
+        }
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+#pragma unroll
+            for (int i = 0; i < ND / 2; ++i) {
+                const uint32_t t = __shfl_up_sync(0xffffffffu, x[i], o);
+                if (lane >= o) x[i] += t;
             }
         }
-    }
-    // in-CTA merge passes: groups of `coop` threads merge two sorted runs
-#pragma unroll 1
-    for (int coop = 2; coop <= NT; coop *= 2) {
-        __syncthreads();
+        if (lane == 31) {
 #pragma unroll
-        for (int k = 0; k < VT; ++k) {
-            sm_.keys[tid * VT + k] = k_[k];
-            if (HAS_V) sm_.vals[tid * VT + k] = v_[k];
+            for (int i = 0; i < ND / 2; ++i) {
+                wtot[w * ND + 2 * i] = x[i] & 0xFFFFu;
+                wtot[w * ND + 2 * i + 1] = x[i] >> 16;
+            }
         }
         __syncthreads();
-        const int run = (coop / 2) * VT;
-        const int start = (tid & ~(coop - 1)) * VT;
-        const int d = (tid & (coop - 1)) * VT;
-        const K* sk = sm_.keys + start;
-        const int ai = tile_split(sk, run, run, d);
-        int src[VT];
-        serial_merge<K, VT>(sk, ai, run, run + (d - ai), 2 * run, k_, src);
-        if (HAS_V) {
+        // 3. digit-major, warp-minor bases: lanes d < ND of warp 0
+        if (tid < ND) {
+            uint32_t tot = 0;
+            for (int i = 0; i < NW; ++i) tot += wtot[i * ND + tid];
+            uint32_t ex = tot;                           // exclusive scan over the 16 digits
 #pragma unroll
-            for (int k = 0; k < VT; ++k) v_[k] = sm_.vals[start + src[k]];
+            for (int o = 1; o < ND; o <<= 1) {
+                const uint32_t t = __shfl_up_sync(0xFFFFu, ex, o);
+                if (tid >= o) ex += t;
+            }
+            uint32_t b = ex - tot;
+            for (int i = 0; i < NW; ++i) {
+                const uint32_t t = wtot[i * ND + tid];
+                wtot[i * ND + tid] = b;
+                b += t;
+            }
         }
-    }
-    __syncthreads();
+        __syncthreads();
+        // 4. this thread's base per digit: warp base + exclusive lane prefix
 #pragma unroll
-    for (int k = 0; k < VT; ++k) {
-        sm_.keys[tid * VT + k] = k_[k];
-        if (HAS_V) sm_.vals[tid * VT + k] = v_[k];
-    }
-    __syncthreads();
+        for (int i = 0; i < ND / 2; ++i) {
+            const uint32_t ex = x[i] - c[i];
+            rowb[tid * ROW + 2 * i] = wtot[w * ND + 2 * i] + (ex & 0xFFFFu);
+            rowb[tid * ROW + 2 * i + 1] = wtot[w * ND + 2 * i + 1] + (ex >> 16);
+        }
+        __syncwarp();
+        // 5. scatter
 #pragma unroll
-    for (int k = 0; k < VT; ++k) {
-        const int idx = k * NT + tid;
-        if (idx < len) {
-            st_stream(out + base + idx, sm_.keys[idx]);
-            if (HAS_V) st_stream(vout + base + idx, sm_.vals[idx]);
+        for (int k = 0; k < IPT; ++k) {
+            const int d = (int)(key[k] >> sh) & 0xF;
+            const int pos = (int)(rowb[tid * ROW + d] + rank[k]);
+            kd[pos] = key[k];
+            if (HAS_V) vd[pos] = val[k];
+        }
+        __syncthreads();
+        cur ^= 1;
+    }
+    const U* kf = ku0 + cur * R;
+    const uint32_t* vf = vv0 + cur * R;
+#pragma unroll
+    for (int k = 0; k < IPT; ++k) {
+        const int e = k * NT + tid;
+        if (e < len) {
+            st_stream(out + base + e, (K)(kf[e] ^ FLIP));
+            if (HAS_V) st_stream(vout + base + e, vf[e]);
         }
     }
 }

@@ -52,10 +52,10 @@ static int64_t tile_nv(int key_bytes, bool has_v) {
     return has_v ? K2Shape<uint64_t, true>::NV : K2Shape<uint64_t, false>::NV;
 }
 static int64_t tile_t(int key_bytes, bool has_v) { return tile_nv(key_bytes, has_v) / 2; }
-// K3 shape: one run of R = NT * VT elements per CTA.
-constexpr int NT = 128;
-constexpr int VT = 15;
-constexpr int R_SORT = NT * VT;
+// K3 shape: one run of R = K3_NT * K3_IPT elements per CTA (radix block sort).
+constexpr int K3_NT = 256;
+constexpr int K3_IPT = 17;
+constexpr int R_SORT = K3_NT * K3_IPT;
 // K1: lanes per rank search (see k_cross_ranks).  Many searches: one lane
 // each (the DRAM-probe traffic of wider groups costs more than it saves).
 // Few searches (< K1_FEW): a whole warp each, ~log_33 dependent rounds.
@@ -369,6 +369,20 @@ static sm_status plan_entry(const K* A, int64_t n, const K* B, int64_t m, int64_
 }
 
 // ------------------------------------------------------------ merge sort
+template <typename K, bool HAS_V>
+static sm_status launch_block_sort(const K* in, const uint32_t* vin, K* out, uint32_t* vout, int64_t N,
+                                   unsigned blocks, cudaStream_t st) {
+    using Lay = K3Layout<K, HAS_V, K3_NT, K3_IPT>;
+    auto kern = k_block_sort<K, HAS_V, K3_NT, K3_IPT>;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Lay::SMEM);
+        attr = true;
+    }
+    kern<<<blocks, K3_NT, Lay::SMEM, st>>>(in, vin, out, vout, (int)N);
+    return SM_OK;
+}
+
 template <typename K>
 static sm_status sort_device(K* keys, uint32_t* vals, int64_t N, cudaStream_t st, bool pdl) {
     const int R = R_SORT;   // initial run length: one K3 tile
@@ -389,8 +403,8 @@ static sm_status sort_device(K* keys, uint32_t* vals, int64_t N, cudaStream_t st
         uint32_t* vdst = (rounds % 2 == 0) ? vals : vaux;
         const unsigned blocks = (unsigned)ceil_div(N, R);
         prof_before(PROF_K3, st);
-        if (vals) k_block_sort<K, true, NT, VT><<<blocks, NT, 0, st>>>(keys, vals, dst, vdst, (int)N);
-        else k_block_sort<K, false, NT, VT><<<blocks, NT, 0, st>>>(keys, nullptr, dst, nullptr, (int)N);
+        if (vals) s = launch_block_sort<K, true>(keys, vals, dst, vdst, N, blocks, st);
+        else s = launch_block_sort<K, false>(keys, nullptr, dst, nullptr, N, blocks, st);
         prof_after(st);
         s = check_launch("k_block_sort");
         K* src = dst;

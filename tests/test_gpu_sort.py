@@ -28,6 +28,36 @@ def test_sort_ragged(kt, N):
         assert_bit_exact(*gpu_sort(sm, inp), *want, kt)
 
 
+@pytest.mark.parametrize("kt", ["u32", "i32", "i64", "u64"])
+def test_sort_run_boundaries(kt):
+    """Sizes around the block-sort run length R and its powers of two
+    (the number of merge rounds changes there), full-range and narrow keys
+    (the block sort skips digits all keys of a run share)."""
+    sm = lib()
+    R = sm.sort_run(kt, True)
+    for N in (R - 1, R, R + 1, 2 * R - 1, 2 * R + 3, 4 * R, 5 * R + 7):
+        for dist in ("full", "bounded:3", "equal"):
+            inp = synth.sort_input(N, kt, dist, seed=N, payload=True)
+            want = oracle.sort(inp.keys, inp.vals, kt)
+            assert_bit_exact(*gpu_sort(sm, inp), *want, kt)
+
+
+def test_sort_signed_extremes():
+    """Signed keys across zero and at both extremes (the block sort ranks the
+    unsigned view with the sign bit flipped)."""
+    sm = lib()
+    for kt, dt in (("i32", np.int32), ("i64", np.int64)):
+        info = np.iinfo(dt)
+        rng = np.random.default_rng(7)
+        vals = np.array([info.min, info.max, -1, 0, 1, info.min + 1, info.max - 1], dtype=dt)
+        k = rng.choice(vals, size=20011).astype(dt)
+        ct = torch.int32 if dt == np.int32 else torch.int64
+        inp = synth.SortInput(kt, torch.from_numpy(k.view(np.int32 if dt == np.int32 else np.int64).copy()),
+                              torch.arange(k.size, dtype=torch.int32))
+        want = oracle.sort(inp.keys, inp.vals, kt)
+        assert_bit_exact(*gpu_sort(sm, inp), *want, kt)
+
+
 @pytest.mark.parametrize("pattern", ["sorted", "reversed", "all_equal", "sawtooth"])
 def test_sort_patterns(pattern):
     sm = lib()
