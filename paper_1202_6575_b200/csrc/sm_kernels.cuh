@@ -421,8 +421,8 @@ __device__ __forceinline__ bool k2_compute(const K* sk, const uint32_t* sv, cons
 //       write the outputs into the warp's private buffer, each segment of
 //       consecutive lanes of one task placed at the destination's 16-byte
 //       phase, and bulk-store the segments from there (segment leader lane).
-template <typename K, bool HAS_V, int NC, int VT, int STAGES, int MAXT, bool WB>
-__global__ void __launch_bounds__(K2Layout<K, HAS_V, NC, VT, STAGES, MAXT, WB>::THREADS)
+template <typename K, bool HAS_V, int NC, int VT, int STAGES, int MAXT, bool WB, int MINB>
+__global__ void __launch_bounds__(K2Layout<K, HAS_V, NC, VT, STAGES, MAXT, WB>::THREADS, MINB)
     k_tasks(const K* __restrict__ A, const uint32_t* __restrict__ vA, const K* __restrict__ B,
             const uint32_t* __restrict__ vB, K* __restrict__ C, uint32_t* __restrict__ vC, Geom g,
             const int* __restrict__ xbar, const int* __restrict__ ybar) {

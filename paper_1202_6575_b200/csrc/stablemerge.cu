@@ -12,6 +12,7 @@
 #include <stdlib.h>
 
 #include <algorithm>
+#include <type_traits>
 #include <vector>
 #include <climits>
 
@@ -25,31 +26,33 @@ thread_local int64_t g_launches = 0;
 
 // K2 shape per element layout: NC consumer threads x VT diagonals per thread
 // = NV padded diagonals per ring stage, the largest task; block size
-// T = NV / 2 (task bound 2T); STAGES-deep TMA ring.
-// VT odd keeps the register -> shared-memory write-back free of bank
-// conflicts.  Keys-only 4-byte merges are bound by the consumers' shared-
-// memory traffic, so they take VT = 31 (half the merge-path splits per
-// element, T = 3968: half the cross-rank searches); wider elements are bound
-// by HBM and keep VT = 15 with a deeper ring.  Shared memory per CTA:
-// 4-byte 3 x 33 KB (2 CTAs/SM), 8-byte 3 x 33 KB (2 CTAs/SM), 12-byte
-// 4 x 49 KB (1 CTA/SM).
+// T = NV / 2 (task bound 2T); STAGES-deep TMA ring; MINB
+// CTAs per SM requested from ptxas.  VT odd keeps the register -> shared
+// write-back free of bank conflicts.  Measured on B200 (profiles/): 4-byte
+// keys-only merges are bound by the consumers' shared-memory merge, and the
+// best of the shapes tried is 352 x 23 (2 CTAs/SM: T = 4048, half the
+// cross-rank searches of VT = 15); 8-byte elements 256 x 15 (2 CTAs/SM);
+// 12-byte elements 256 x 15 with a 4-deep ring (1 CTA/SM).
+template <int NC_, int VT_, int STAGES_, int MINB_ = 1>
+struct K2Geo {
+    static constexpr int NC = NC_, VT = VT_, STAGES = STAGES_, MINB = MINB_;
+    static constexpr bool WB = false;                 // per-warp output buffers (see k_tasks): measured slower
+    static constexpr int NV = NC * VT;
+    static constexpr int T = NV / 2;
+};
 template <typename K, bool HAS_V>
 struct K2Shape {
     static constexpr int bytes = (int)sizeof(K) + (HAS_V ? 4 : 0);
-    static constexpr int NC = 256;
-    static constexpr int VT = bytes <= 4 ? 31 : 15;
-    static constexpr bool WB = false;                 // per-warp output buffers (see k_tasks): measured slower
-    static constexpr int STAGES = bytes <= 8 ? 3 : 4;
-    static constexpr int NV = NC * VT;
-    static constexpr int T = NV / 2;
+    using type = typename std::conditional<bytes <= 4, K2Geo<352, 23, 3, 2>,
+                 typename std::conditional<bytes <= 8, K2Geo<256, 15, 3>, K2Geo<256, 15, 4>>::type>::type;
 };
 // Tasks packed per ring stage at most.
 constexpr int K2_MAXT = 16;
 
 // Tile capacity NV (largest task) and default block size of a layout.
 static int64_t tile_nv(int key_bytes, bool has_v) {
-    if (key_bytes == 4) return has_v ? K2Shape<uint32_t, true>::NV : K2Shape<uint32_t, false>::NV;
-    return has_v ? K2Shape<uint64_t, true>::NV : K2Shape<uint64_t, false>::NV;
+    if (key_bytes == 4) return has_v ? K2Shape<uint32_t, true>::type::NV : K2Shape<uint32_t, false>::type::NV;
+    return has_v ? K2Shape<uint64_t, true>::type::NV : K2Shape<uint64_t, false>::type::NV;
 }
 static int64_t tile_t(int key_bytes, bool has_v) { return tile_nv(key_bytes, has_v) / 2; }
 // K3 shape: one run of R = K3_NT * K3_IPT elements per CTA (radix block sort).
@@ -155,15 +158,11 @@ static sm_status launch_cross_ranks(const K* A, const K* B, const Geom& g, int* 
     return check_launch("k_cross_ranks");
 }
 
-template <typename K, bool HAS_V>
-static sm_status launch_merge(const K* A, const uint32_t* vA, const K* B, const uint32_t* vB, K* C,
-                              uint32_t* vC, const Geom& g, int* xbar, int* ybar, cudaStream_t st, bool pdl) {
-    sm_status s = launch_cross_ranks<K>(A, B, g, xbar, ybar, st);
-    if (s != SM_OK) return s;
-
-    using Sh = K2Shape<K, HAS_V>;
+template <typename K, bool HAS_V, typename Sh>
+static sm_status launch_tasks(const K* A, const uint32_t* vA, const K* B, const uint32_t* vB, K* C, uint32_t* vC,
+                              const Geom& g, const int* xbar, const int* ybar, cudaStream_t st, bool pdl) {
     using Lay = K2Layout<K, HAS_V, Sh::NC, Sh::VT, Sh::STAGES, K2_MAXT, Sh::WB>;
-    auto kern = k_tasks<K, HAS_V, Sh::NC, Sh::VT, Sh::STAGES, K2_MAXT, Sh::WB>;
+    auto kern = k_tasks<K, HAS_V, Sh::NC, Sh::VT, Sh::STAGES, K2_MAXT, Sh::WB, Sh::MINB>;
     static int per_sm = -1, n_sm = 0;
     if (per_sm < 0) {
         int dev = 0;
@@ -188,7 +187,7 @@ static sm_status launch_merge(const K* A, const uint32_t* vA, const K* B, const 
     cfg.attrs = attr;
     cfg.numAttrs = (pdl && !g_prof_on) ? 1 : 0;
     prof_before(PROF_K2, st);
-    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, A, vA, B, vB, C, vC, g, (const int*)xbar, (const int*)ybar);
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, A, vA, B, vB, C, vC, g, xbar, ybar);
     prof_after(st);
     ++g_launches;
     if (e != cudaSuccess) {
@@ -196,6 +195,14 @@ static sm_status launch_merge(const K* A, const uint32_t* vA, const K* B, const 
         return fail_cuda(e, "k_tasks");
     }
     return SM_OK;
+}
+
+template <typename K, bool HAS_V>
+static sm_status launch_merge(const K* A, const uint32_t* vA, const K* B, const uint32_t* vB, K* C,
+                              uint32_t* vC, const Geom& g, int* xbar, int* ybar, cudaStream_t st, bool pdl) {
+    sm_status s = launch_cross_ranks<K>(A, B, g, xbar, ybar, st);
+    if (s != SM_OK) return s;
+    return launch_tasks<K, HAS_V, typename K2Shape<K, HAS_V>::type>(A, vA, B, vB, C, vC, g, xbar, ybar, st, pdl);
 }
 
 // ------------------------------------------------ host-memory staging
