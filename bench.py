@@ -43,6 +43,8 @@ CONFIG_NAMES = {
     3: "C3 unbalanced stable merge n=2^28 m=2^16 int64 keys in [0,1000) + u32 payload (BASELINE.json configs[2])",
     4: "C4 adversarial stable merge n=2^27 m=2^25 u64 90% one value + u32 payload (BASELINE.json configs[3])",
     5: "C5 stable merge sort N=2^28 u32 keys in [0,2^20) + u32 original-index payload (BASELINE.json configs[4])",
+    6: "B1 batched stable merges: 2^16 pairs, lengths uniform in [0,2^11) per side, u32 keys in [0,2^16) + u32 "
+       "payload (SURVEY.md §8(f) row 1; not a BASELINE.json config)",
 }
 L2_BYTES = 126 * 1024 * 1024
 FALLBACK_HBM_GBS = 6650.0
@@ -66,7 +68,8 @@ def args_():
     ap.add_argument("--steps", type=int, default=2000)
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", type=int, choices=[1, 2, 3, 4, 5], default=2)
+    ap.add_argument("--config", type=int, choices=sorted(synth.CONFIGS), default=2,
+                    help="1-5: BASELINE.json configs[0..4] (2 = the metric's workload); 6: batched merges (NEXT row)")
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--cpu-seconds", type=float, default=10.0, help="bounded CPU-oracle sample budget")
     ap.add_argument("--no-extras", action="store_true", help="timed loop only (for ncu launch lists)")
@@ -175,36 +178,6 @@ def aggregate_value(elems_per_rank, world, steps, t_ms_max):
     return world * elems_per_rank * steps / (t_ms_max / 1e3)
 
 
-def elements_of(cfg):
-    c = synth.CONFIGS[cfg]
-    return c["N"] if c["kind"] == "sort" else c["n"] + c["m"]
-
-
-def step_bytes(cfg):
-    """Algorithmic HBM bytes of one launch of the dominant kernel (K2) per
-    SURVEY.md §8(d): read A+B + write C, keys + payload."""
-    c = synth.CONFIGS[cfg]
-    eb = synth.elem_bytes(c["key_type"], c["payload"])
-    return 2 * elements_of(cfg) * eb
-
-
-def sort_passes(cfg):
-    """Passes of the merge sort over HBM: the block sort (row a8) plus
-    ceil(log2(N / R)) merge rounds (row a9), R = the library's run length."""
-    import math
-    import paper_1202_6575_b200 as sm
-    c = synth.CONFIGS[cfg]
-    R = sm.sort_run(c["key_type"], c["payload"])
-    return 1 + max(0, math.ceil(math.log2(c["N"] / R)))
-
-
-def step_alg_bytes(cfg):
-    """Algorithmic HBM bytes of one whole step: a merge reads A+B and writes C
-    once; the sort reads and writes the array once per pass."""
-    c = synth.CONFIGS[cfg]
-    return step_bytes(cfg) * (sort_passes(cfg) if c["kind"] == "sort" else 1)
-
-
 def traffic_from_profiles(cfg):
     p = os.path.join(ROOT, "profiles", "traffic.json")
     if not os.path.exists(p):
@@ -215,6 +188,190 @@ def traffic_from_profiles(cfg):
     return d.get("dram_bytes_per_launch"), d.get("source")
 
 
+# -------------------------------------------------------------- workloads
+class Workload:
+    """One bench workload: its inputs resident in HBM, the timed call, the
+    algorithmic bytes, the end-to-end (host-buffer) call and the bounded CPU
+    oracle sample."""
+
+    def __init__(self, cfg, seed, dev):
+        self.cfg, self.c, self.dev = cfg, synth.CONFIGS[cfg], dev
+        self.kt = self.c["key_type"]
+        self.eb = synth.elem_bytes(self.kt, self.c["payload"])
+
+    passes = 1                                  # HBM passes of the algorithmic bytes
+
+    def k2_launch_bytes(self):
+        """Algorithmic bytes of one launch of the dominant kernel K2 (SURVEY
+        §8(d): read A+B + write C, keys + payload)."""
+        return 2 * self.elems * self.eb
+
+    def step_bytes(self):
+        return self.k2_launch_bytes() * self.passes
+
+    def prep(self):
+        pass
+
+
+class MergeWork(Workload):
+    def __init__(self, cfg, seed, dev, sm):
+        super().__init__(cfg, seed, dev)
+        c, kt = self.c, self.kt
+        self.inp = synth.merge_input(c["n"], c["m"], kt, c["dist"], seed, c["payload"], device=dev)
+        n, m = self.inp.n, self.inp.m
+        self.elems = n + m
+        self.out_k = torch.empty(n + m, dtype=self.inp.a_keys.dtype, device=dev)
+        self.out_v = torch.empty(n + m, dtype=torch.int32, device=dev) if c["payload"] else None
+        self.sm = sm
+
+    def call(self):
+        i = self.inp
+        self.sm.merge_stable(i.a_keys, i.a_vals, i.b_keys, i.b_vals, self.out_k, self.out_v, key_type=self.kt)
+
+    def e2e_setup(self, stream):
+        h = self.host = self.inp.to("cpu")
+        pin = lambda t: None if t is None else t.pin_memory()
+        self.h_args = (pin(h.a_keys), pin(h.a_vals), pin(h.b_keys), pin(h.b_vals),
+                       torch.empty(self.elems, dtype=h.a_keys.dtype).pin_memory(),
+                       torch.empty(self.elems, dtype=torch.int32).pin_memory() if self.c["payload"] else None)
+        self.stream = stream
+        return self.elems * self.eb, self.elems * self.eb       # H2D, D2H bytes
+
+    def e2e_call(self):
+        self.sm.merge_stable(*self.h_args, key_type=self.kt, stream=self.stream)
+
+    def oracle_sample(self, budget_s):
+        import oracle
+        h, kt = self.host, self.kt
+        t0 = time.perf_counter()
+        oracle.merge(h.a_keys[:1 << 16], None if h.a_vals is None else h.a_vals[:1 << 16],
+                     h.b_keys[:1 << 16], None if h.b_vals is None else h.b_vals[:1 << 16], kt)
+        est = (time.perf_counter() - t0) / (1 << 17) * (h.n + h.m)
+        frac = min(1.0, budget_s / est) if est > 0 else 1.0
+        na, nb = max(1, int(h.n * frac)), max(1, int(h.m * frac))
+        args = (h.a_keys[:na], None if h.a_vals is None else h.a_vals[:na],
+                h.b_keys[:nb], None if h.b_vals is None else h.b_vals[:nb], kt)
+        what = "the full workload" if frac == 1.0 else f"prefixes A[:{na}], B[:{nb}] of the workload"
+        return lambda: oracle.merge(*args), na + nb, f"oracle_merge (two-pointer, 1 thread) on {what}"
+
+
+class SortWork(Workload):
+    def __init__(self, cfg, seed, dev, sm):
+        super().__init__(cfg, seed, dev)
+        c, kt = self.c, self.kt
+        self.src = synth.sort_input(c["N"], kt, c["dist"], seed, c["payload"], device=dev)
+        self.elems = c["N"]
+        self.work_k = self.src.keys.clone()
+        self.work_v = self.src.vals.clone() if self.src.vals is not None else None
+        self.sm = sm
+        import math
+        R = sm.sort_run(kt, c["payload"])
+        self.passes = 1 + max(0, math.ceil(math.log2(c["N"] / R)))   # block sort + merge rounds
+
+    def prep(self):                              # restore the unsorted input (untimed)
+        self.work_k.copy_(self.src.keys)
+        if self.work_v is not None:
+            self.work_v.copy_(self.src.vals)
+
+    def call(self):
+        self.sm.mergesort_stable(self.work_k, self.work_v, key_type=self.kt)
+
+    def e2e_setup(self, stream):
+        self.hk = self.src.keys.cpu().pin_memory()
+        self.hv = self.src.vals.cpu().pin_memory() if self.src.vals is not None else None
+        self.hwk = self.hk.clone().pin_memory()
+        self.hwv = self.hv.clone().pin_memory() if self.hv is not None else None
+        self.stream = stream
+        return self.elems * self.eb, self.elems * self.eb
+
+    def e2e_prep(self):
+        self.hwk.copy_(self.hk)
+        if self.hwv is not None:
+            self.hwv.copy_(self.hv)
+
+    def e2e_call(self):
+        self.sm.mergesort_stable(self.hwk, self.hwv, key_type=self.kt, stream=self.stream)
+
+    def oracle_sample(self, budget_s):
+        import oracle
+        N = self.hk.numel()
+        Ns = min(N, 1 << 22)
+        args = (self.hk[:Ns], None if self.hv is None else self.hv[:Ns], self.kt)
+        return (lambda: oracle.sort(*args), Ns,
+                f"oracle_sort (bottom-up stable merge sort, 1 thread) on the first {Ns} of {N} input elements "
+                f"(sort cost grows as N log N: this per-element rate over-states the full-size CPU rate)")
+
+
+class BatchWork(Workload):
+    def __init__(self, cfg, seed, dev, sm):
+        super().__init__(cfg, seed, dev)
+        c, kt = self.c, self.kt
+        self.inp = synth.batch_input(c["S"], c["mean"], kt, c["dist"], seed, c["payload"], device=dev)
+        self.elems = self.inp.n + self.inp.m
+        self.out_k = torch.empty(self.elems, dtype=self.inp.a_keys.dtype, device=dev)
+        self.out_v = torch.empty(self.elems, dtype=torch.int32, device=dev) if c["payload"] else None
+        self.sm = sm
+
+    def call(self):
+        i = self.inp
+        self.sm.merge_stable_batched(i.a_keys, i.a_vals, i.a_offsets, i.b_keys, i.b_vals, i.b_offsets,
+                                     self.out_k, self.out_v, key_type=self.kt)
+
+    def e2e_setup(self, stream):
+        # the batched entry takes device buffers: e2e = pinned H2D copies of
+        # the inputs and offsets, the call, and the D2H copy of the output
+        self.host = self.inp.to("cpu")
+        h = self.host
+        pin = lambda t: None if t is None else t.pin_memory()
+        self.h_in = [pin(t) for t in (h.a_keys, h.a_vals, h.a_offsets, h.b_keys, h.b_vals, h.b_offsets)]
+        self.d_in = [None if t is None else torch.empty_like(t, device=self.dev) for t in self.h_in]
+        self.h_out = [torch.empty(self.elems, dtype=h.a_keys.dtype).pin_memory(),
+                      torch.empty(self.elems, dtype=torch.int32).pin_memory() if self.c["payload"] else None]
+        self.stream = stream
+        h2d = sum(t.numel() * t.element_size() for t in self.h_in if t is not None)
+        d2h = sum(t.numel() * t.element_size() for t in self.h_out if t is not None)
+        return h2d, d2h
+
+    def e2e_call(self):
+        with torch.cuda.stream(self.stream):
+            for d, h in zip(self.d_in, self.h_in):
+                if d is not None:
+                    d.copy_(h, non_blocking=True)
+            ak, av, ao, bk, bv, bo = self.d_in
+            self.sm.merge_stable_batched(ak, av, ao, bk, bv, bo, self.out_k, self.out_v, key_type=self.kt)
+            self.h_out[0].copy_(self.out_k, non_blocking=True)
+            if self.out_v is not None:
+                self.h_out[1].copy_(self.out_v, non_blocking=True)
+        self.stream.synchronize()
+
+    def oracle_sample(self, budget_s):
+        import oracle
+        h, kt = self.host, self.kt
+        ao, bo = h.a_offsets.numpy(), h.b_offsets.numpy()
+        S = len(ao) - 1
+        # a prefix of the segments, ~budget_s of per-segment oracle merges
+        t0 = time.perf_counter()
+        k = min(S, 64)
+        for s in range(k):
+            oracle.merge(h.a_keys[ao[s]:ao[s + 1]], None if h.a_vals is None else h.a_vals[ao[s]:ao[s + 1]],
+                         h.b_keys[bo[s]:bo[s + 1]], None if h.b_vals is None else h.b_vals[bo[s]:bo[s + 1]], kt)
+        est = (time.perf_counter() - t0) / k * S
+        ks = max(1, min(S, int(S * budget_s / max(est, 1e-9))))
+
+        def fn():
+            for s in range(ks):
+                oracle.merge(h.a_keys[ao[s]:ao[s + 1]], None if h.a_vals is None else h.a_vals[ao[s]:ao[s + 1]],
+                             h.b_keys[bo[s]:bo[s + 1]], None if h.b_vals is None else h.b_vals[bo[s]:bo[s + 1]],
+                             kt)
+        elems = int(ao[ks] + bo[ks])
+        return fn, elems, f"oracle_merge per segment (1 thread) on the first {ks} of {S} segments"
+
+
+def make_workload(cfg, seed, dev, sm):
+    kind = synth.CONFIGS[cfg]["kind"]
+    return {"merge": MergeWork, "sort": SortWork, "batch": BatchWork}[kind](cfg, seed, dev, sm)
+
+
 # ------------------------------------------------------------------ ours
 def run_ours(a, world, rank, local):
     import paper_1202_6575_b200 as sm
@@ -222,46 +379,21 @@ def run_ours(a, world, rank, local):
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
     cfg = a.config
-    c = synth.CONFIGS[cfg]
-    kt = c["key_type"]
-    seed = rank_seed(cfg, rank)
     clocks = ClockSampler(local).start()
-
-    # ---- inputs resident in HBM
-    if c["kind"] == "merge":
-        inp = synth.merge_input(c["n"], c["m"], kt, c["dist"], seed, c["payload"], device=dev)
-        n, m = inp.n, inp.m
-        out_k = torch.empty(n + m, dtype=inp.a_keys.dtype, device=dev)
-        out_v = torch.empty(n + m, dtype=torch.int32, device=dev) if c["payload"] else None
-
-        def call():
-            sm.merge_stable(inp.a_keys, inp.a_vals, inp.b_keys, inp.b_vals, out_k, out_v, key_type=kt)
-        in_bytes = step_bytes(cfg) // 2
-    else:
-        src = synth.sort_input(c["N"], kt, c["dist"], seed, c["payload"], device=dev)
-        work_k = src.keys.clone()
-        work_v = src.vals.clone() if src.vals is not None else None
-
-        def call():
-            sm.mergesort_stable(work_k, work_v, key_type=kt)
-        in_bytes = step_bytes(cfg) // 2
-    elems = elements_of(cfg)
-    per_step_events = c["kind"] == "sort" or in_bytes * 2 < 4 * L2_BYTES
+    wl = make_workload(cfg, rank_seed(cfg, rank), dev, sm)     # inputs resident in HBM
+    per_step_events = wl.c["kind"] == "sort" or wl.step_bytes() < 4 * L2_BYTES
     flush = torch.empty(2 * L2_BYTES // 4, dtype=torch.int32, device=dev) if per_step_events else None
 
     def prep():
-        if c["kind"] == "sort":                       # restore the unsorted input (untimed)
-            work_k.copy_(src.keys)
-            if work_v is not None:
-                work_v.copy_(src.vals)
+        wl.prep()
         if flush is not None:
             flush.add_(1)                             # write > L2 between timed steps
 
     stream = torch.cuda.current_stream(dev)
     for _ in range(a.warmup):
         prep()
-        call()
-    call()
+        wl.call()
+    wl.call()
     launches_per_step = sm.last_launch_count()
     torch.cuda.synchronize(dev)
     barrier(world)
@@ -272,7 +404,7 @@ def run_ours(a, world, rank, local):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         for _ in range(a.steps):
-            call()
+            wl.call()
         e1.record(stream)
         torch.cuda.synchronize(dev)
         t_ms = e0.elapsed_time(e1)
@@ -282,7 +414,7 @@ def run_ours(a, world, rank, local):
             prep()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            call()
+            wl.call()
             e1.record(stream)
             evs.append((e0, e1))
         torch.cuda.synchronize(dev)
@@ -292,116 +424,65 @@ def run_ours(a, world, rank, local):
     t_ms = max_over_ranks(t_ms, world)
     clk = clocks.summary(t_wall0, t_wall1)
 
-    value = aggregate_value(elems, world, a.steps, t_ms)
-    ms_per_step = t_ms / a.steps
-    res = dict(value=value, ms_per_step=ms_per_step, launches=launches_per_step * a.steps, clocks=clk,
-               per_step_events=per_step_events)
+    res = dict(value=aggregate_value(wl.elems, world, a.steps, t_ms), ms_per_step=t_ms / a.steps,
+               launches=launches_per_step * a.steps, clocks=clk, per_step_events=per_step_events, wl=wl)
     if a.no_extras:
         clocks.stop()
         return res
 
     # ---- per-kernel durations (CUDA events on the launch stream)
-    prof_steps = max(3, min(a.steps, 50 if c["kind"] == "sort" else 200))
+    prof_steps = max(3, min(a.steps, 50 if wl.c["kind"] == "sort" else 200))
     sm.profile_enable(True)
     for _ in range(prof_steps):
         prep()
-        call()
+        wl.call()
     torch.cuda.synchronize(dev)
-    k1 = sm.profile_read(sm.PROF_K1)
-    k2 = sm.profile_read(sm.PROF_K2)
-    k3 = sm.profile_read(sm.PROF_K3)
+    res["kernels"] = {"k_cross_ranks": sm.profile_read(sm.PROF_K1), "k_tasks": sm.profile_read(sm.PROF_K2),
+                      "k_block_sort": sm.profile_read(sm.PROF_K3), "steps": prof_steps}
     sm.profile_enable(False)
-    res["kernels"] = {"k_cross_ranks": k1, "k_tasks": k2, "k_block_sort": k3, "steps": prof_steps}
 
-    # ---- end to end through the C ABI with pinned host buffers
-    if c["kind"] == "merge":
-        h = inp.to("cpu")
-        pin = lambda t: None if t is None else t.pin_memory()
-        ha, hav, hb, hbv = pin(h.a_keys), pin(h.a_vals), pin(h.b_keys), pin(h.b_vals)
-        hok = torch.empty(n + m, dtype=h.a_keys.dtype).pin_memory()
-        hov = torch.empty(n + m, dtype=torch.int32).pin_memory() if c["payload"] else None
-
-        def e2e_call():
-            sm.merge_stable(ha, hav, hb, hbv, hok, hov, key_type=kt, stream=stream)
-        h2d = in_bytes
-        d2h = in_bytes
-    else:
-        hk = src.keys.cpu().pin_memory()
-        hv = src.vals.cpu().pin_memory() if src.vals is not None else None
-        hwk, hwv = hk.clone().pin_memory(), (hv.clone().pin_memory() if hv is not None else None)
-
-        def e2e_call():
-            sm.mergesort_stable(hwk, hwv, key_type=kt, stream=stream)
-        h2d = d2h = in_bytes
-    e2e_call()
+    # ---- end to end through the public API with pinned host buffers
+    h2d, d2h = wl.e2e_setup(stream)
+    wl.e2e_call()
     torch.cuda.synchronize(dev)
     e2e_ms = 0.0
     for _ in range(a.e2e_steps):
-        if c["kind"] == "sort":
-            hwk.copy_(hk)
-            if hwv is not None:
-                hwv.copy_(hv)
+        if hasattr(wl, "e2e_prep"):
+            wl.e2e_prep()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        e2e_call()     # binding synchronises the stream for host outputs
+        wl.e2e_call()     # host outputs are ready when the call returns
         e1.record(stream)
         torch.cuda.synchronize(dev)
         e2e_ms += e0.elapsed_time(e1)
     e2e_ms = max_over_ranks(e2e_ms, world)
-    res["e2e"] = {"value": world * elems * a.e2e_steps / (e2e_ms / 1e3), "unit": "elements/s",
+    res["e2e"] = {"value": aggregate_value(wl.elems, world, a.e2e_steps, e2e_ms), "unit": "elements/s",
                   "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": a.e2e_steps,
-                  "path": "C ABI with pinned host buffers (library stages H2D, kernels, D2H)"}
-    res["host_input"] = (h if c["kind"] == "merge" else (hk, hv))
+                  "path": "public API with pinned host buffers (H2D, kernels, D2H inside the timed region)"}
     clocks.stop()
     return res
 
 
-def cpu_oracle_sample(cfg, host_input, budget_s):
+def cpu_oracle_sample(wl, budget_s):
     """The oracle as it stands, single thread, on a bounded sample of the
-    workload: whole-workload calls repeated for ~budget_s, or a prefix sample
-    if one call would exceed it."""
-    import oracle
-    c = synth.CONFIGS[cfg]
-    kt = c["key_type"]
-    reps, elems, t = 0, 0, 0.0
-    if c["kind"] == "merge":
-        h = host_input
-        frac = 1.0
+    workload (whole-workload calls, or a prefix if one call exceeds the
+    budget), repeated for ~budget_s."""
+    fn, elems, what = wl.oracle_sample(budget_s)
+    reps, t = 0, 0.0
+    while t < budget_s or reps == 0:
         t0 = time.perf_counter()
-        oracle.merge(h.a_keys[:1 << 16], None if h.a_vals is None else h.a_vals[:1 << 16],
-                     h.b_keys[:1 << 16], None if h.b_vals is None else h.b_vals[:1 << 16], kt)
-        est = (time.perf_counter() - t0) / (1 << 17) * (h.n + h.m)
-        if est > budget_s:
-            frac = budget_s / est
-        na, nb = max(1, int(h.n * frac)), max(1, int(h.m * frac))
-        A, AV = h.a_keys[:na], None if h.a_vals is None else h.a_vals[:na]
-        B, BV = h.b_keys[:nb], None if h.b_vals is None else h.b_vals[:nb]
-        while t < budget_s or reps == 0:
-            t0 = time.perf_counter()
-            oracle.merge(A, AV, B, BV, kt)
-            t += time.perf_counter() - t0
-            reps += 1
-            elems += na + nb
-        sample = (f"oracle_merge (two-pointer, 1 thread) on {'the full workload' if frac == 1.0 else f'prefixes A[:{na}], B[:{nb}] of the workload'}"
-                  f", {reps} repetition(s), {t:.1f} s")
-    else:
-        hk, hv = host_input
-        N = hk.numel()
-        Ns = min(N, 1 << 22)
-        while t < budget_s or reps == 0:
-            t0 = time.perf_counter()
-            oracle.sort(hk[:Ns], None if hv is None else hv[:Ns], kt)
-            t += time.perf_counter() - t0
-            reps += 1
-            elems += Ns
-        sample = (f"oracle_sort (bottom-up stable merge sort, 1 thread) on the first {Ns} of {N} input elements, "
-                  f"{reps} repetition(s), {t:.1f} s (sort cost grows as N log N: this per-element rate "
-                  f"over-states the full-size CPU rate)")
-    return {"value": elems / t, "unit": "elements/s", "cores": 1, "kind": "oracle", "sample": sample,
-            "host_cores_available": os.cpu_count()}
+        fn()
+        t += time.perf_counter() - t0
+        reps += 1
+    return {"value": elems * reps / t, "unit": "elements/s", "cores": 1, "kind": "oracle",
+            "sample": f"{what}, {reps} repetition(s), {t:.1f} s", "host_cores_available": os.cpu_count()}
 
 
 # ------------------------------------------------------------- reference
+class _HostOnly:
+    """Workload inputs on the host only (the reference arm has no GPU path)."""
+
+
 def run_reference(a):
     """Reference arm of this tier: the CPU oracle, as it stands, each step a
     bounded sample of the workload sized so the whole run takes ~1-2 min."""
@@ -410,32 +491,24 @@ def run_reference(a):
     cfg = a.config
     c = synth.CONFIGS[cfg]
     kt = c["key_type"]
-    total_budget = 90.0
-    per_step = total_budget / max(1, a.steps + a.warmup)
+    per_step = 90.0 / max(1, a.steps + a.warmup)
+    wl = _HostOnly()
+    wl.kt, wl.c = kt, c
     if c["kind"] == "merge":
-        h = synth.merge_input(c["n"], c["m"], kt, c["dist"], synth.BASE_SEED + cfg, c["payload"])
-        t0 = time.perf_counter()
-        oracle.merge(h.a_keys[:1 << 16], None if h.a_vals is None else h.a_vals[:1 << 16], h.b_keys[:1 << 16],
-                     None if h.b_vals is None else h.b_vals[:1 << 16], kt)
-        ns = (time.perf_counter() - t0) / (1 << 17)
-        frac = min(1.0, per_step / (ns * (h.n + h.m)))
-        na, nb = max(1, int(h.n * frac)), max(1, int(h.m * frac))
-        args = (h.a_keys[:na], None if h.a_vals is None else h.a_vals[:na], h.b_keys[:nb],
-                None if h.b_vals is None else h.b_vals[:nb], kt)
-        fn = lambda: oracle.merge(*args)
-        elems = na + nb
-        sample = f"oracle_merge on prefixes A[:{na}], B[:{nb}] of the workload per step"
+        wl.host = synth.merge_input(c["n"], c["m"], kt, c["dist"], synth.BASE_SEED + cfg, c["payload"])
+        fn, elems, what = MergeWork.oracle_sample(wl, per_step)
+    elif c["kind"] == "batch":
+        wl.host = synth.batch_input(c["S"], c["mean"], kt, c["dist"], synth.BASE_SEED + cfg, c["payload"])
+        fn, elems, what = BatchWork.oracle_sample(wl, per_step)
     else:
-        s = synth.sort_input(c["N"], kt, c["dist"], synth.BASE_SEED + cfg, c["payload"])
+        src = synth.sort_input(c["N"], kt, c["dist"], synth.BASE_SEED + cfg, c["payload"])
         Ns = 1 << 16
         t0 = time.perf_counter()
-        oracle.sort(s.keys[:Ns], None if s.vals is None else s.vals[:Ns], kt)
+        oracle.sort(src.keys[:Ns], None if src.vals is None else src.vals[:Ns], kt)
         ns = (time.perf_counter() - t0) / Ns
         Ns = int(max(1 << 12, min(c["N"], per_step / ns)))
-        args = (s.keys[:Ns], None if s.vals is None else s.vals[:Ns], kt)
-        fn = lambda: oracle.sort(*args)
-        elems = Ns
-        sample = f"oracle_sort on the first {Ns} of {c['N']} input elements per step"
+        args = (src.keys[:Ns], None if src.vals is None else src.vals[:Ns], kt)
+        fn, elems, what = (lambda: oracle.sort(*args)), Ns, f"oracle_sort on the first {Ns} of {c['N']} elements"
     for _ in range(a.warmup):
         fn()
     t = 0.0
@@ -451,7 +524,8 @@ def run_reference(a):
         "ms_per_step": 1e3 * t / a.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": kt, "data": "synthetic",
         "config": {"workload": CONFIG_NAMES[cfg], "elements_per_step_sampled": elems},
-        "cpu_baseline": {"value": value, "unit": "elements/s", "cores": 1, "kind": "oracle", "sample": sample},
+        "cpu_baseline": {"value": value, "unit": "elements/s", "cores": 1, "kind": "oracle",
+                         "sample": f"{what} per step"},
         "e2e": {"value": value, "unit": "elements/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
 
@@ -472,23 +546,22 @@ def main():
             dist.destroy_process_group()
         return
     cfg = a.config
-    c = synth.CONFIGS[cfg]
+    wl = r["wl"]
+    c = wl.c
     peak, peak_src = hbm_peak()
-    elems = elements_of(cfg)
-    alg = step_bytes(cfg)
     line = {
         "metric": load_json("BASELINE.json")["metric"],
         "value": r["value"], "unit": "elements/s", "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
         "ms_per_step": r["ms_per_step"], "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": c["key_type"] + ("+u32" if c["payload"] else ""), "data": "synthetic",
-        "config": {"workload": CONFIG_NAMES[cfg], "elements_per_gpu_step": elems, "key_type": c["key_type"],
+        "config": {"workload": CONFIG_NAMES[cfg], "elements_per_gpu_step": wl.elems, "key_type": c["key_type"],
                    "payload": c["payload"], "dist": c["dist"], "seed": f"{synth.BASE_SEED + cfg:#x} + 1000*rank",
                    "l2": ("per-step events, L2 flushed (2x L2 write) and sort input restored between timed steps"
                           if r["per_step_events"] else
-                          f"inputs+output {alg / 1e9:.2f} GB > 126 MB L2: no flush, back-to-back steps"),
+                          f"inputs+output {wl.step_bytes() / 1e9:.2f} GB > 126 MB L2: no flush, back-to-back steps"),
                    "parallelism": f"replicas x{world}" if world > 1 else "1 GPU"},
-        "achieved_hbm_gbs": step_alg_bytes(cfg) / (r["ms_per_step"] * 1e-3) / 1e9,
-        "algorithmic_bytes_per_step": step_alg_bytes(cfg),
+        "achieved_hbm_gbs": wl.step_bytes() / (r["ms_per_step"] * 1e-3) / 1e9,
+        "algorithmic_bytes_per_step": wl.step_bytes(),
         "gpu_launches": r["launches"],
         "clocks": r["clocks"],
     }
@@ -497,10 +570,8 @@ def main():
         k2_ms, k2_n = r["kernels"]["k_tasks"]
         k1_ms, k1_n = r["kernels"]["k_cross_ranks"]
         k3_ms, k3_n = r["kernels"]["k_block_sort"]
-        if c["kind"] == "sort":
-            per_launch_bytes = 2 * elems * synth.elem_bytes(c["key_type"], c["payload"])
-        else:
-            per_launch_bytes = alg
+        steps = r["kernels"]["steps"]
+        per_launch_bytes = wl.k2_launch_bytes()
         k2_avg = k2_ms / max(1, k2_n)
         achieved = per_launch_bytes / (k2_avg * 1e-3) / 1e9
         traffic, tsrc = traffic_from_profiles(cfg)
@@ -511,13 +582,13 @@ def main():
                             "avg_launch_ms": k2_avg,
                             "share_of_step": k2_ms / max(1e-9, k1_ms + k2_ms + k3_ms),
                             "k_cross_ranks_avg_ms": k1_ms / max(1, k1_n),
-                            "k_cross_ranks_ms_per_step": k1_ms / r["kernels"]["steps"],
-                            "k_tasks_ms_per_step": k2_ms / r["kernels"]["steps"],
+                            "k_cross_ranks_ms_per_step": k1_ms / steps,
+                            "k_tasks_ms_per_step": k2_ms / steps,
                             "k_block_sort_avg_ms": (k3_ms / k3_n) if k3_n else None}
     if "e2e" in r:
         line["e2e"] = r["e2e"]
     if world == 1 and not a.no_extras:
-        line["cpu_baseline"] = cpu_oracle_sample(cfg, r["host_input"], a.cpu_seconds)
+        line["cpu_baseline"] = cpu_oracle_sample(wl, a.cpu_seconds)
     print(json.dumps(line), flush=True)
     if world > 1:
         import torch.distributed as dist

@@ -94,13 +94,53 @@ sm_status merge_stable_u64(const uint64_t *keys_A, const uint32_t *vals_A, int64
                            uint64_t *out_keys, uint32_t *out_vals, void *stream);
 
 /* ---------------------------------------------------------------------
+ * merge_stable_batched_<K>  -- SURVEY.md §8(f) row 1: S independent stable
+ * merges in one call (variable lengths), through the segmented machinery of
+ * the merge-sort rounds (§3, "modifying the merge
+ * algorithm to work in parallel on the pairs").
+ *
+ *   keys_A[n], vals_A[n]     the A segments, concatenated
+ *   a_offsets[S+1]  int64    segment s of A is keys_A[a_offsets[s], a_offsets[s+1])
+ *   keys_B[m], vals_B[m], b_offsets[S+1]   likewise for B
+ *   out_keys[n+m], out_vals[n+m]   segment s of C starts at
+ *                            a_offsets[s] + b_offsets[s] and holds the stable
+ *                            merge (ties: A first) of the two segments
+ *   vals_*: all three set or all NULL; stream as above.
+ *
+ * DEVICE pointers only (keys, payloads and both offset arrays; a host
+ * pointer gives SM_EINVAL).  Precondition: a_offsets[0] = 0,
+ * a_offsets[S] = n, non-decreasing (same for b_offsets with m), and every
+ * segment sorted.  The offsets are read on the device only; a violated
+ * precondition gives unspecified output but no write outside C (offsets
+ * are clamped into [0, n] / [0, m] and each segment to a non-negative
+ * length).  Errors and scratch as merge_stable_<K>.
+ * ------------------------------------------------------------------- */
+sm_status merge_stable_batched_u32(const uint32_t *keys_A, const uint32_t *vals_A, int64_t n,
+                                   const int64_t *a_offsets, const uint32_t *keys_B, const uint32_t *vals_B,
+                                   int64_t m, const int64_t *b_offsets, int64_t S, uint32_t *out_keys,
+                                   uint32_t *out_vals, void *stream);
+sm_status merge_stable_batched_i32(const int32_t *keys_A, const uint32_t *vals_A, int64_t n,
+                                   const int64_t *a_offsets, const int32_t *keys_B, const uint32_t *vals_B,
+                                   int64_t m, const int64_t *b_offsets, int64_t S, int32_t *out_keys,
+                                   uint32_t *out_vals, void *stream);
+sm_status merge_stable_batched_i64(const int64_t *keys_A, const uint32_t *vals_A, int64_t n,
+                                   const int64_t *a_offsets, const int64_t *keys_B, const uint32_t *vals_B,
+                                   int64_t m, const int64_t *b_offsets, int64_t S, int64_t *out_keys,
+                                   uint32_t *out_vals, void *stream);
+sm_status merge_stable_batched_u64(const uint64_t *keys_A, const uint32_t *vals_A, int64_t n,
+                                   const int64_t *a_offsets, const uint64_t *keys_B, const uint32_t *vals_B,
+                                   int64_t m, const int64_t *b_offsets, int64_t S, uint64_t *out_keys,
+                                   uint32_t *out_vals, void *stream);
+
+/* ---------------------------------------------------------------------
  * mergesort_stable_<K>  -- SURVEY.md §8 rows a8-a9 (§3).
  *
  *   keys[N], vals[N] (vals may be NULL: keys only), sorted IN PLACE from the
  *   caller's view; stable: equal keys keep their input order.
  *
  * Device path: runs of R consecutive elements are sorted stably inside one
- * CTA each ("sorting sequentially in parallel p consecutive blocks", L406-407),
+ * CTA each ("sorting sequentially in parallel p consecutive blocks", L406-407;
+ * a shared-memory LSD radix sort, stable by construction),
  * then ceil(log2(N/R)) rounds merge run pairs (2k, 2k+1) with the left run
  * playing A, every pair of a round in one segmented launch of the merge
  * above ("modifying the merge algorithm to work in parallel on the

@@ -7,6 +7,7 @@ merge rounds) runs in the library's CUDA kernels.  There is no CPU fallback:
 importing this package fails loudly if the library is missing.
 
     merge_stable(a_keys, a_vals, b_keys, b_vals, out_keys=None, out_vals=None)
+    merge_stable_batched(a_keys, a_vals, a_offsets, b_keys, b_vals, b_offsets)
     mergesort_stable(keys, vals=None)
     merge_plan(a_keys, b_keys, p_A, p_B)          # Steps 1-4 only (tests)
 
@@ -54,6 +55,7 @@ for _kt in KEY_TYPES:
     for _name, _args in ((f"merge_stable_{_kt}", [_P, _P, _I, _P, _P, _I, _P, _P, _P]),
                          (f"merge_stable_ex_{_kt}", [_P, _P, _I, _P, _P, _I, _P, _P, _P, ctypes.POINTER(SmOptions)]),
                          (f"merge_plan_ex_{_kt}", [_P, _I, _P, _I, _I, _I, _P, _P, _P, _P]),
+                         (f"merge_stable_batched_{_kt}", [_P, _P, _I, _P, _P, _P, _I, _P, _I, _P, _P, _P]),
                          (f"mergesort_stable_{_kt}", [_P, _P, _I, _P]),
                          (f"mergesort_stable_ex_{_kt}", [_P, _P, _I, _P, ctypes.POINTER(SmOptions)])):
         _f = getattr(_lib, _name)
@@ -190,6 +192,36 @@ def merge_stable(a_keys: torch.Tensor, a_vals: Optional[torch.Tensor], b_keys: t
     return out_keys, out_vals
 
 
+def merge_stable_batched(a_keys: torch.Tensor, a_vals: Optional[torch.Tensor], a_offsets: torch.Tensor,
+                         b_keys: torch.Tensor, b_vals: Optional[torch.Tensor], b_offsets: torch.Tensor,
+                         out_keys: Optional[torch.Tensor] = None, out_vals: Optional[torch.Tensor] = None, *,
+                         key_type: Optional[str] = None, stream=None):
+    """S = len(a_offsets) - 1 independent stable merges (ties: A first):
+    segment s of A (a_keys[a_offsets[s]:a_offsets[s+1]]) with segment s of B
+    into out[a_offsets[s] + b_offsets[s] : ...].  CUDA tensors only; offsets
+    int64.  Returns (keys, vals)."""
+    kt = _key_type(a_keys, key_type)
+    _key_type(b_keys, kt)
+    if (a_vals is None) != (b_vals is None):
+        raise ValueError("payloads must be given for both inputs or neither")
+    _vals_ok(a_vals); _vals_ok(b_vals)
+    if a_offsets.dtype != torch.int64 or b_offsets.dtype != torch.int64:
+        raise TypeError("offsets must be int64")
+    if a_offsets.numel() != b_offsets.numel() or a_offsets.numel() < 1:
+        raise ValueError("a_offsets and b_offsets must both hold S + 1 entries")
+    S = a_offsets.numel() - 1
+    n, m = a_keys.numel(), b_keys.numel()
+    if out_keys is None:
+        out_keys = torch.empty(n + m, dtype=a_keys.dtype, device=a_keys.device)
+    if a_vals is not None and out_vals is None:
+        out_vals = torch.empty(n + m, dtype=a_vals.dtype, device=a_keys.device)
+    s = _stream_for(a_keys, stream)
+    _check(getattr(_lib, f"merge_stable_batched_{kt}")(_ptr(a_keys), _ptr(a_vals), n, _ptr(a_offsets), _ptr(b_keys),
+                                                         _ptr(b_vals), m, _ptr(b_offsets), S, _ptr(out_keys),
+                                                         _ptr(out_vals), s), f"merge_stable_batched_{kt}")
+    return out_keys, out_vals
+
+
 def mergesort_stable(keys: torch.Tensor, vals: Optional[torch.Tensor] = None, *, key_type: Optional[str] = None,
                      stream=None, pdl: bool = True):
     """Stable merge sort in place (equal keys keep input order).  Returns (keys, vals)."""
@@ -229,6 +261,6 @@ def merge_plan(a_keys: torch.Tensor, b_keys: torch.Tensor, p_A: int, p_B: Option
     return xbar, ybar, tasks
 
 
-__all__ = ["merge_stable", "mergesort_stable", "merge_plan", "tile_capacity", "sort_run", "last_launch_count",
+__all__ = ["merge_stable", "merge_stable_batched", "mergesort_stable", "merge_plan", "tile_capacity", "sort_run", "last_launch_count",
            "StableMergeError", "KEY_TYPES", "LIB_PATH", "profile_enable", "profile_read", "PROF_K1", "PROF_K2",
            "PROF_K3"]

@@ -57,28 +57,57 @@ __device__ __forceinline__ int rank_high_dev(const K* __restrict__ X, int len, K
 }
 
 // ---------------------------------------------------------------------------
-// Geometry of one launch: either one merge (S = 1, arrays A and B), or one
-// merge-sort round over S run pairs of a single array (§3:
-// "modifying the merge algorithm to work in parallel on the pairs").
+// Geometry of one launch: one merge (mode 0, S = 1), one merge-sort round
+// over S equal run pairs of a single array (mode 1; §3:
+// "modifying the merge algorithm to work in parallel on the pairs"), or a
+// batch of S independent merges of any lengths (mode 2, SURVEY §8(f) row 1:
+// the same machinery exposed to callers, one segment table entry each).
 // Segment s of a sort round: A = runs [2sL, 2sL+L), B = [2sL+L, 2sL+2L),
 // clipped to N; the left run plays A so ties keep input order.  A pair whose
 // B is empty (odd trailing run) degenerates to case-(a) copies (L409-410).
+// Ranks: modes 0/1 keep xbar[s*(pA+1)..] and ybar[s*(pB+1)..]; mode 2 keeps
+// one array, segment s at rbase: xbar (pA+1 entries) then ybar (pB+1).
 // ---------------------------------------------------------------------------
-struct Geom {
-    int S;        // segments
-    int pA, pB;   // block counts per segment
-    int n, m;     // plain merge sizes (sort == 0)
-    int L, N;     // sort round: run length, total length (sort == 1)
-    int sort;
+struct SegInfo {          // mode-2 segment table entry (built by k_batch_*)
+    int aoff, n, boff, m, coff;
+    int pA, pB;           // block counts of this segment
+    int tbase, rbase;     // first task / first rank entry of this segment
 };
 
+struct Geom {
+    int S;                // segments
+    int pA, pB;           // block counts per segment (modes 0, 1)
+    int n, m;             // plain merge sizes (mode 0)
+    int L, N;             // sort round: run length, total length (mode 1)
+    int sort;             // mode: 0 merge, 1 sort round, 2 batch
+    int T;                // mode 2: block size
+    const SegInfo* segs;  // mode 2: segment table [S]
+    const int* totals;    // mode 2: [0] = tasks, [1] = rank entries
+    const int* task_seg;  // mode 2: segment of every task
+    const int* rank_seg;  // mode 2: segment of every rank entry
+};
+
+// One segment, located: its ranges, block counts and rank arrays.
 struct Seg {
     int aoff, n, boff, m, coff;
+    int pA, pB;
+    int* xs;              // xbar of the segment (pA+1 entries)
+    int* ys;              // ybar of the segment (pB+1 entries)
 };
 
-__device__ __forceinline__ Seg segment(const Geom& g, int s) {
+__device__ __forceinline__ Seg segment(const Geom& g, int s, int* xbar, int* ybar) {
     Seg r;
-    if (!g.sort) {
+    if (g.sort == 2) {
+        const SegInfo e = g.segs[s];
+        r.aoff = e.aoff; r.n = e.n; r.boff = e.boff; r.m = e.m; r.coff = e.coff; r.pA = e.pA; r.pB = e.pB;
+        r.xs = xbar + e.rbase;
+        r.ys = xbar + e.rbase + e.pA + 1;
+        return r;
+    }
+    r.pA = g.pA; r.pB = g.pB;
+    r.xs = xbar + (size_t)s * (g.pA + 1);
+    r.ys = ybar + (size_t)s * (g.pB + 1);
+    if (g.sort == 0) {
         r.aoff = 0; r.n = g.n; r.boff = 0; r.m = g.m; r.coff = 0;
     } else {
         r.aoff = s * 2 * g.L;                       // < N < 2^31 for s < S
@@ -88,6 +117,27 @@ __device__ __forceinline__ Seg segment(const Geom& g, int s) {
         r.coff = r.aoff;
     }
     return r;
+}
+
+// Number of tasks / rank entries of the launch (mode 2: from the device).
+__device__ __forceinline__ int total_tasks(const Geom& g) {
+    return g.sort == 2 ? g.totals[0] : g.S * (g.pA + g.pB);
+}
+__device__ __forceinline__ int total_rank_items(const Geom& g) {
+    return g.sort == 2 ? g.totals[1] : g.S * (g.pA + g.pB + 2);
+}
+
+// Segment of global task (ranks = false) or rank entry (ranks = true) idx,
+// and the index local to that segment (mode 2: O(1) through the maps).
+__device__ __forceinline__ int locate(const Geom& g, int idx, bool ranks, int& local) {
+    if (g.sort != 2) {
+        const int per = g.pA + g.pB + (ranks ? 2 : 0);
+        local = idx % per;
+        return idx / per;
+    }
+    const int sg = ranks ? __ldg(&g.rank_seg[idx]) : __ldg(&g.task_seg[idx]);
+    local = idx - (ranks ? __ldg(&g.segs[sg].rbase) : __ldg(&g.segs[sg].tbase));
+    return sg;
 }
 
 // ---------------------------------------------------------------------------

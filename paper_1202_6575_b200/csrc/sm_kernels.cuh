@@ -1,15 +1,15 @@
 // sm_kernels.cuh -- the kernels of the B200 stable merge / merge sort.
 //
-//   K1  k_cross_ranks   rows a1/a2: one thread per block start, rank_low of
+//   K1  k_cross_ranks   rows a1/a2: one search per block start, rank_low of
 //                       A[x_i] in B / rank_high of B[y_j] in A  (L304-309)
 //   --  stream order (or PDL griddepcontrol.wait) = the single
 //       synchronisation of L373-375 (row a3)
-//   K2  k_tasks         rows a4-a7: one CTA per block start (task), O(1)
-//                       classification, then copy (a, e) or stable merge
-//                       (b, c, d) of the task through a shared-memory tile
-//   K3  k_block_sort    row a8: stable sort of one run of NT*VT elements per
-//                       CTA (odd-even transposition in registers, then
-//                       in-CTA merge-path merges, left run = A)
+//   K2  k_tasks         rows a4-a7: persistent, warp-specialised; O(1)
+//                       classification of every block start's task, then
+//                       copy (a, e) or stable merge (b, c, d) through a TMA
+//                       shared-memory ring, several tasks packed per stage
+//   K3  k_block_sort    row a8: stable LSD radix sort of one run per CTA
+//   --  k_batch_*       batched merges: segment table
 //   --  k_plan_dump     Steps 1-4 only: the task table for parity tests
 //
 // All in-kernel indices are 32-bit (the ABI rejects n+m or N > 2^31-1).
@@ -78,18 +78,15 @@ __device__ __forceinline__ int group_rank(const K* __restrict__ X, int len, K x,
 template <typename K, int G>
 __global__ void __launch_bounds__(256) k_cross_ranks(const K* __restrict__ A, const K* __restrict__ B, Geom g,
                                                      int* __restrict__ xbar, int* __restrict__ ybar) {
-    const int per = g.pA + g.pB + 2;
+    pdl_wait();   // a batch's segment table (no-op for plain launches)
     const long long item = ((long long)blockIdx.x * blockDim.x + threadIdx.x) / G;
-    const bool valid = item < (long long)g.S * per;
+    const bool valid = item < (long long)total_rank_items(g);
     int s = 0, t = 0;
-    if (valid) {
-        s = (int)(item / per);
-        t = (int)(item % per);
-    }
-    const Seg sg = segment(g, s);
-    const bool sideA = t <= g.pA;
-    const int idx = sideA ? t : t - g.pA - 1;
-    const int plen = sideA ? g.pA : g.pB;            // own blocks
+    if (valid) s = locate(g, (int)item, true, t);
+    const Seg sg = segment(g, s, xbar, ybar);
+    const bool sideA = t <= sg.pA;
+    const int idx = sideA ? t : t - sg.pA - 1;
+    const int plen = sideA ? sg.pA : sg.pB;          // own blocks
     const int own_len = sideA ? sg.n : sg.m;
     const int oth_len = sideA ? sg.m : sg.n;         // searched array
     const bool search = valid && idx < plen && idx < own_len;   // x_idx < own_len  <=>  idx < own_len
@@ -98,40 +95,20 @@ __global__ void __launch_bounds__(256) k_cross_ranks(const K* __restrict__ A, co
     const int r = group_rank<K, G, G>(sideA ? B + sg.boff : A + sg.aoff, oth_len, x, !sideA, search, 0);
     if (valid && (threadIdx.x % G) == 0) {
         const int v = search ? r : oth_len;
-        if (sideA) xbar[(size_t)s * (g.pA + 1) + idx] = v;
-        else ybar[(size_t)s * (g.pB + 1) + idx] = v;
+        if (sideA) sg.xs[idx] = v;
+        else sg.ys[idx] = v;
     }
     pdl_launch_dependents();
 }
 
-// Decode the task of this CTA (rows a4/a5).
+// Decode a task (rows a4/a5).
 __device__ __forceinline__ Task decode_task(const Geom& g, int task, const int* __restrict__ xbar,
                                             const int* __restrict__ ybar, Seg& sg) {
-    const int per = g.pA + g.pB;
-    const int s = task / per, t = task % per;
-    sg = segment(g, s);
-    const Blocks xa(sg.n, g.pA), yb(sg.m, g.pB);
-    const int* xs = xbar + (size_t)s * (g.pA + 1);
-    const int* ys = ybar + (size_t)s * (g.pB + 1);
-    return t < g.pA ? classify_a_side(t, xa, yb, xs, ys) : classify_b_side(t - g.pA, xa, yb, xs, ys);
-}
-
-// CTA-wide copy of len elements, U loads in flight per thread (row a6).
-template <typename T, int NT, int U>
-__device__ __forceinline__ void cta_copy(const T* __restrict__ src, T* __restrict__ dst, int len) {
-    for (int base = 0; base < len; base += NT * U) {
-        T r[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const int idx = base + u * NT + (int)threadIdx.x;
-            if (idx < len) r[u] = ld_stream(src + idx);
-        }
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const int idx = base + u * NT + (int)threadIdx.x;
-            if (idx < len) st_stream(dst + idx, r[u]);
-        }
-    }
+    int t;
+    const int s = locate(g, task, false, t);
+    sg = segment(g, s, (int*)xbar, (int*)ybar);
+    const Blocks xa(sg.n, sg.pA), yb(sg.m, sg.pB);
+    return t < sg.pA ? classify_a_side(t, xa, yb, sg.xs, sg.ys) : classify_b_side(t - sg.pA, xa, yb, sg.xs, sg.ys);
 }
 
 // ----------------------------------------------------------------- K2
@@ -242,7 +219,7 @@ __device__ __forceinline__ void k2_producer(const K* __restrict__ A, const uint3
     constexpr int NV = Lay::NV;
     constexpr int KB = Lay::KB;
     constexpr int EPV = Lay::EPV;
-    const int ntasks = g.S * (g.pA + g.pB);
+    const int ntasks = total_tasks(g);
     const int lane = threadIdx.x;
     int la = 0, lb = 0, off = 0, ag = 0, bg = 0;   // window slot `lane`
     int cnt = 0;                                    // slots [0, cnt) hold tasks
@@ -585,12 +562,108 @@ __global__ void __launch_bounds__(K2Layout<K, HAS_V, NC, VT, STAGES, MAXT, WB>::
     if (WB) bulk_wait_read<0>();
 }
 
+// ------------------------------------------------------- batch setup
+// Batched merges (mode 2): segment s merges A[a_off[s], a_off[s+1]) with
+// B[b_off[s], b_off[s+1]) into C[a_off[s] + b_off[s], ...).  Offsets are
+// clamped into [0, n] / [0, m] and made non-decreasing per segment, so a
+// malformed table can give a wrong result but never a write outside C.
+// Block counts per segment: p_A = max(1, ceil(n_s / T)) (same for B), the
+// single-merge rule (reading R7).  Three passes: per-block counts and local
+// exclusive scans (tasks p_A + p_B, rank entries p_A + p_B + 2), a scan of the
+// block sums, and the block offsets added.
+constexpr int BATCH_NT = 256;
+
+__global__ void __launch_bounds__(BATCH_NT) k_batch_count(const int64_t* __restrict__ a_off,
+                                                          const int64_t* __restrict__ b_off, int S, int64_t n,
+                                                          int64_t m, int T, SegInfo* __restrict__ segs,
+                                                          int2* __restrict__ blk) {
+    __shared__ int2 wsum[BATCH_NT / 32];
+    const int s = blockIdx.x * BATCH_NT + threadIdx.x;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    int tasks = 0, ranks = 0;
+    SegInfo e;
+    if (s < S) {
+        const int64_t a0 = min(max(a_off[s], (int64_t)0), n), a1 = min(max(a_off[s + 1], a0), n);
+        const int64_t b0 = min(max(b_off[s], (int64_t)0), m), b1 = min(max(b_off[s + 1], b0), m);
+        e.aoff = (int)a0; e.n = (int)(a1 - a0); e.boff = (int)b0; e.m = (int)(b1 - b0); e.coff = (int)(a0 + b0);
+        e.pA = max(1, (e.n + T - 1) / T);
+        e.pB = max(1, (e.m + T - 1) / T);
+        tasks = e.pA + e.pB;
+        ranks = tasks + 2;
+    }
+    int ti = tasks, ri = ranks;                         // block-inclusive scan
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int t1 = __shfl_up_sync(0xffffffffu, ti, o), t2 = __shfl_up_sync(0xffffffffu, ri, o);
+        if (lane >= o) { ti += t1; ri += t2; }
+    }
+    if (lane == 31) wsum[w] = make_int2(ti, ri);
+    __syncthreads();
+    int bt = 0, br = 0;
+    for (int i = 0; i < w; ++i) { bt += wsum[i].x; br += wsum[i].y; }
+    if (s < S) {
+        e.tbase = bt + ti - tasks;
+        e.rbase = br + ri - ranks;
+        segs[s] = e;
+    }
+    if (threadIdx.x == BATCH_NT - 1) blk[blockIdx.x] = make_int2(bt + ti, br + ri);
+}
+
+// One CTA: exclusive scan of the nblk block sums in place; totals[0..1].
+__global__ void __launch_bounds__(BATCH_NT) k_batch_scan(int2* __restrict__ blk, int nblk, int* __restrict__ totals) {
+    __shared__ int2 wsum[BATCH_NT / 32];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    int ct = 0, cr = 0;                                 // carry across chunks
+    for (int c0 = 0; c0 < nblk; c0 += BATCH_NT) {
+        const int i = c0 + threadIdx.x;
+        const int2 v = i < nblk ? blk[i] : make_int2(0, 0);
+        int ti = v.x, ri = v.y;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int t1 = __shfl_up_sync(0xffffffffu, ti, o), t2 = __shfl_up_sync(0xffffffffu, ri, o);
+            if (lane >= o) { ti += t1; ri += t2; }
+        }
+        if (lane == 31) wsum[w] = make_int2(ti, ri);
+        __syncthreads();
+        int bt = 0, br = 0, at = 0, ar = 0;
+        for (int k = 0; k < BATCH_NT / 32; ++k) {
+            if (k < w) { bt += wsum[k].x; br += wsum[k].y; }
+            at += wsum[k].x; ar += wsum[k].y;
+        }
+        if (i < nblk) blk[i] = make_int2(ct + bt + ti - v.x, cr + br + ri - v.y);
+        ct += at;
+        cr += ar;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        totals[0] = ct;
+        totals[1] = cr;
+    }
+}
+
+__global__ void __launch_bounds__(BATCH_NT) k_batch_apply(const int2* __restrict__ blk, int S,
+                                                          SegInfo* __restrict__ segs, int* __restrict__ task_seg,
+                                                          int* __restrict__ rank_seg) {
+    const int s = blockIdx.x * BATCH_NT + threadIdx.x;
+    if (s < S) {
+        const int2 b = blk[blockIdx.x];
+        SegInfo e = segs[s];
+        e.tbase += b.x;
+        e.rbase += b.y;
+        segs[s] = e;
+        // task -> segment and rank entry -> segment maps (K1/K2 locate in O(1))
+        for (int t = 0; t < e.pA + e.pB; ++t) task_seg[e.tbase + t] = s;
+        for (int t = 0; t < e.pA + e.pB + 2; ++t) rank_seg[e.rbase + t] = s;
+    }
+    pdl_launch_dependents();
+}
+
 // ----------------------------------------------------------- plan dump
 template <typename K>
 __global__ void k_plan_dump(Geom g, const int* __restrict__ xbar, const int* __restrict__ ybar,
                             int64_t* __restrict__ tasks) {
     const int task = blockIdx.x * blockDim.x + threadIdx.x;
-    if (task >= g.S * (g.pA + g.pB)) return;
+    if (task >= total_tasks(g)) return;
     Seg sg;
     const Task t = decode_task(g, task, xbar, ybar, sg);
     int64_t* row = tasks + (size_t)task * 6;
@@ -651,7 +724,7 @@ __global__ void __launch_bounds__(NT) k_block_sort(const K* __restrict__ in, con
     constexpr int NDIG = (int)sizeof(U) * 2;             // 4-bit digits per key
     constexpr U FLIP = RadixView<K>::flip;
     static_assert(IPT % 2 == 1 && IPT < 256 && NT % 32 == 0 && NT >= 32, "odd IPT; 8-bit counters");
-    extern __shared__ __align__(16) char smem[];
+    extern __shared__ __align__(128) char smem[];
     U* ku0 = (U*)smem;
     uint32_t* vv0 = (uint32_t*)(smem + Lay::OFF_V);
     uint32_t* rowb = (uint32_t*)(smem + Lay::OFF_ROW);  // [NT][ROW] per-thread digit bases

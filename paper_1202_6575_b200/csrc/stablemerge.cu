@@ -148,9 +148,19 @@ static void dfree(void* p, cudaStream_t st) {
 
 // ------------------------------------------------------------ launches
 // K1: the cross ranks of every block start of every segment.
+// Upper bounds of the launch's rank entries and tasks (exact for modes 0/1;
+// mode 2 counts them on the device, the host sizes the grids by the bound).
+struct GeomCounts {
+    long long items, tasks;
+};
+static GeomCounts geom_counts(const Geom& g) {
+    return {(long long)g.S * (g.pA + g.pB + 2), (long long)g.S * (g.pA + g.pB)};
+}
+
 template <typename K>
-static sm_status launch_cross_ranks(const K* A, const K* B, const Geom& g, int* xbar, int* ybar, cudaStream_t st) {
-    const long long items = (long long)g.S * (g.pA + g.pB + 2);
+static sm_status launch_cross_ranks(const K* A, const K* B, const Geom& g, const GeomCounts& gc, int* xbar, int* ybar,
+                                    cudaStream_t st) {
+    const long long items = gc.items;
     prof_before(PROF_K1, st);
     if (items < K1_FEW) k_cross_ranks<K, 32><<<(unsigned)((items * 32 + 255) / 256), 256, 0, st>>>(A, B, g, xbar, ybar);
     else k_cross_ranks<K, 1><<<(unsigned)((items + 255) / 256), 256, 0, st>>>(A, B, g, xbar, ybar);
@@ -160,7 +170,8 @@ static sm_status launch_cross_ranks(const K* A, const K* B, const Geom& g, int* 
 
 template <typename K, bool HAS_V, typename Sh>
 static sm_status launch_tasks(const K* A, const uint32_t* vA, const K* B, const uint32_t* vB, K* C, uint32_t* vC,
-                              const Geom& g, const int* xbar, const int* ybar, cudaStream_t st, bool pdl) {
+                              const Geom& g, const GeomCounts& gc, const int* xbar, const int* ybar, cudaStream_t st,
+                              bool pdl) {
     using Lay = K2Layout<K, HAS_V, Sh::NC, Sh::VT, Sh::STAGES, K2_MAXT, Sh::WB>;
     auto kern = k_tasks<K, HAS_V, Sh::NC, Sh::VT, Sh::STAGES, K2_MAXT, Sh::WB, Sh::MINB>;
     static int per_sm = -1, n_sm = 0;
@@ -173,8 +184,7 @@ static sm_status launch_tasks(const K* A, const uint32_t* vA, const K* B, const 
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, Lay::THREADS, Lay::SMEM);
         if (per_sm < 1) per_sm = 1;
     }
-    const long long ntasks = (long long)g.S * (g.pA + g.pB);
-    const long long grid = std::min<long long>(ntasks, (long long)per_sm * n_sm);
+    const long long grid = std::max(1ll, std::min<long long>(gc.tasks, (long long)per_sm * n_sm));
     cudaLaunchConfig_t cfg;
     memset(&cfg, 0, sizeof(cfg));
     cfg.gridDim = dim3((unsigned)grid);
@@ -199,10 +209,12 @@ static sm_status launch_tasks(const K* A, const uint32_t* vA, const K* B, const 
 
 template <typename K, bool HAS_V>
 static sm_status launch_merge(const K* A, const uint32_t* vA, const K* B, const uint32_t* vB, K* C,
-                              uint32_t* vC, const Geom& g, int* xbar, int* ybar, cudaStream_t st, bool pdl) {
-    sm_status s = launch_cross_ranks<K>(A, B, g, xbar, ybar, st);
+                              uint32_t* vC, const Geom& g, int* xbar, int* ybar, cudaStream_t st, bool pdl,
+                              const GeomCounts* counts = nullptr) {
+    const GeomCounts gc = counts ? *counts : geom_counts(g);
+    sm_status s = launch_cross_ranks<K>(A, B, g, gc, xbar, ybar, st);
     if (s != SM_OK) return s;
-    return launch_tasks<K, HAS_V, typename K2Shape<K, HAS_V>::type>(A, vA, B, vB, C, vC, g, xbar, ybar, st, pdl);
+    return launch_tasks<K, HAS_V, typename K2Shape<K, HAS_V>::type>(A, vA, B, vB, C, vC, g, gc, xbar, ybar, st, pdl);
 }
 
 // ------------------------------------------------ host-memory staging
@@ -261,7 +273,7 @@ static bool overlaps(const void* p, size_t pb, const void* q, size_t qb) {
 template <typename K>
 static sm_status merge_device(const K* A, const uint32_t* vA, int64_t n, const K* B, const uint32_t* vB, int64_t m,
                               K* C, uint32_t* vC, cudaStream_t st, int64_t pA, int64_t pB, bool pdl) {
-    Geom g;
+    Geom g{};
     g.S = 1; g.pA = (int)pA; g.pB = (int)pB; g.n = (int)n; g.m = (int)m; g.L = 0; g.N = 0; g.sort = 0;
     int* ranks = nullptr;
     sm_status s = dalloc(&ranks, (pA + 1) + (pB + 1), st);
@@ -335,6 +347,74 @@ static sm_status merge_entry(const K* A, const uint32_t* vA, int64_t n, const K*
     return s != SM_OK ? s : s2;
 }
 
+// ------------------------------------------------------------ batched merge
+// S independent stable merges in one call, through the
+// sort rounds' segmented machinery (§3) with a segment
+// table instead of equal runs.  Device pointers only.
+template <typename K>
+static sm_status batch_entry(const K* A, const uint32_t* vA, int64_t n, const int64_t* a_off, const K* B,
+                             const uint32_t* vB, int64_t m, const int64_t* b_off, int64_t S, K* C, uint32_t* vC,
+                             void* stream) {
+    g_launches = 0;
+    g_err[0] = 0;
+    cudaStream_t st = (cudaStream_t)stream;
+    if (n < 0 || m < 0 || S < 0) return fail_inval("negative size");
+    if (S > (int64_t)(INT_MAX / 8)) return fail_inval("too many segments");
+    if (n + m > (int64_t)INT_MAX) return fail_inval("n + m > 2^31 - 1");
+    if ((n && !A) || (m && !B) || ((n + m) && !C)) return fail_inval("NULL key pointer with nonzero size");
+    if (S && (!a_off || !b_off)) return fail_inval("NULL segment offsets");
+    if (vC) {
+        if ((n && !vA) || (m && !vB)) return fail_inval("payload pointers must be all set or all NULL");
+    } else if (vA || vB) {
+        return fail_inval("payload pointers must be all set or all NULL");
+    }
+    const size_t kb = sizeof(K), cb = (size_t)(n + m);
+    if (overlaps(C, cb * kb, A, n * kb) || overlaps(C, cb * kb, B, m * kb) || overlaps(C, cb * kb, vA, n * 4) ||
+        overlaps(C, cb * kb, vB, m * 4) || overlaps(vC, cb * 4, A, n * kb) || overlaps(vC, cb * 4, B, m * kb) ||
+        overlaps(vC, cb * 4, vA, n * 4) || overlaps(vC, cb * 4, vB, m * 4) || overlaps(C, cb * kb, vC, cb * 4))
+        return SM_EALIAS;
+    if (S == 0 || n + m == 0) return SM_OK;
+    if (is_host_ptr(A) || is_host_ptr(B) || is_host_ptr(vA) || is_host_ptr(vB) || is_host_ptr(C) || is_host_ptr(vC) ||
+        is_host_ptr(a_off) || is_host_ptr(b_off))
+        return fail_inval("merge_stable_batched takes device pointers only");
+    keep_pool(st);
+    const int64_t T = tile_t((int)sizeof(K), vC != nullptr);
+    const int nblk = (int)ceil_div(S, BATCH_NT);
+    GeomCounts gc;
+    gc.tasks = ceil_div(n, T) + ceil_div(m, T) + 2 * S;      // sum over segments of p_A + p_B
+    gc.items = gc.tasks + 2 * S;
+    const size_t seg_bytes = ((size_t)S * sizeof(SegInfo) + 15) & ~(size_t)15;
+    const size_t blk_bytes = ((size_t)nblk * sizeof(int2) + 15) & ~(size_t)15;
+    char* scratch = nullptr;
+    sm_status s = dalloc(&scratch, (int64_t)(seg_bytes + blk_bytes + 16 + (size_t)(2 * gc.items + gc.tasks) * 4), st);
+    if (s != SM_OK) return s;
+    SegInfo* segs = (SegInfo*)scratch;
+    int2* blk = (int2*)(scratch + seg_bytes);
+    int* totals = (int*)(scratch + seg_bytes + blk_bytes);
+    int* ranks = totals + 4;
+    int* rank_seg = ranks + gc.items;
+    int* task_seg = rank_seg + gc.items;
+    k_batch_count<<<nblk, BATCH_NT, 0, st>>>(a_off, b_off, (int)S, n, m, (int)T, segs, blk);
+    s = check_launch("k_batch_count");
+    if (s == SM_OK) {
+        k_batch_scan<<<1, BATCH_NT, 0, st>>>(blk, nblk, totals);
+        s = check_launch("k_batch_scan");
+    }
+    if (s == SM_OK) {
+        k_batch_apply<<<nblk, BATCH_NT, 0, st>>>(blk, (int)S, segs, task_seg, rank_seg);
+        s = check_launch("k_batch_apply");
+    }
+    if (s == SM_OK) {
+        Geom g{};
+        g.S = (int)S; g.sort = 2; g.T = (int)T; g.segs = segs; g.totals = totals;
+        g.task_seg = task_seg; g.rank_seg = rank_seg;
+        if (vC) s = launch_merge<K, true>(A, vA, B, vB, C, vC, g, ranks, ranks, st, true, &gc);
+        else s = launch_merge<K, false>(A, nullptr, B, nullptr, C, nullptr, g, ranks, ranks, st, true, &gc);
+    }
+    dfree(scratch, st);
+    return s;
+}
+
 // ------------------------------------------------------------ plan dump
 __global__ void k_widen(const int* __restrict__ in, int64_t* __restrict__ out, int count) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -353,12 +433,12 @@ static sm_status plan_entry(const K* A, int64_t n, const K* B, int64_t m, int64_
     if (is_host_ptr(A) || is_host_ptr(B) || is_host_ptr(xbar) || is_host_ptr(ybar) || is_host_ptr(tasks))
         return fail_inval("merge_plan_ex takes device pointers only");
     keep_pool(st);
-    Geom g;
+    Geom g{};
     g.S = 1; g.pA = (int)pA; g.pB = (int)pB; g.n = (int)n; g.m = (int)m; g.L = 0; g.N = 0; g.sort = 0;
     int* ranks = nullptr;
     sm_status s = dalloc(&ranks, (pA + 1) + (pB + 1), st);
     if (s != SM_OK) return s;
-    s = launch_cross_ranks<K>(A, B, g, ranks, ranks + pA + 1, st);
+    s = launch_cross_ranks<K>(A, B, g, geom_counts(g), ranks, ranks + pA + 1, st);
     if (s == SM_OK) {
         k_widen<<<(unsigned)((pA + 1 + 255) / 256), 256, 0, st>>>(ranks, xbar, (int)(pA + 1));
         s = check_launch("k_widen");
@@ -419,7 +499,7 @@ static sm_status sort_device(K* keys, uint32_t* vals, int64_t N, cudaStream_t st
         for (int64_t L = R; s == SM_OK && L < N; L *= 2) {
             K* d2 = (src == keys) ? aux : keys;
             uint32_t* vd2 = (src == keys) ? vaux : vals;
-            Geom g;
+            Geom g{};
             g.S = (int)ceil_div(N, 2 * L);
             g.pA = g.pB = (int)ceil_div(L, T);
             g.n = g.m = 0; g.L = (int)L; g.N = (int)N; g.sort = 1;
@@ -479,6 +559,13 @@ extern "C" {
     sm_status merge_plan_ex_##SUF(const K* keys_A, int64_t n, const K* keys_B, int64_t m, int64_t p_A,         \
                                   int64_t p_B, int64_t* xbar, int64_t* ybar, int64_t* tasks, void* stream) {   \
         return sm::plan_entry<K>(keys_A, n, keys_B, m, p_A, p_B, xbar, ybar, tasks, stream);                    \
+    }                                                                                                           \
+    sm_status merge_stable_batched_##SUF(const K* keys_A, const uint32_t* vals_A, int64_t n,                   \
+                                         const int64_t* a_offsets, const K* keys_B, const uint32_t* vals_B,    \
+                                         int64_t m, const int64_t* b_offsets, int64_t S, K* out_keys,          \
+                                         uint32_t* out_vals, void* stream) {                                   \
+        return sm::batch_entry<K>(keys_A, vals_A, n, a_offsets, keys_B, vals_B, m, b_offsets, S, out_keys,    \
+                                  out_vals, stream);                                                           \
     }                                                                                                           \
     sm_status mergesort_stable_##SUF(K* keys, uint32_t* vals, int64_t N, void* stream) {                       \
         return sm::sort_entry<K>(keys, vals, N, stream, nullptr);                                               \

@@ -181,6 +181,64 @@ def sort_input(N: int, key_type: str, dist: str, seed: int, payload: bool = True
     return SortInput(key_type, keys, vals)
 
 
+@dataclasses.dataclass
+class BatchInput:
+    key_type: str
+    a_keys: torch.Tensor
+    b_keys: torch.Tensor
+    a_vals: Optional[torch.Tensor]
+    b_vals: Optional[torch.Tensor]
+    a_offsets: torch.Tensor      # int64 [S+1]
+    b_offsets: torch.Tensor
+
+    @property
+    def S(self) -> int:
+        return self.a_offsets.numel() - 1
+
+    @property
+    def n(self) -> int:
+        return self.a_keys.numel()
+
+    @property
+    def m(self) -> int:
+        return self.b_keys.numel()
+
+    def to(self, device) -> "BatchInput":
+        f = lambda t: None if t is None else t.to(device)
+        return BatchInput(self.key_type, f(self.a_keys), f(self.b_keys), f(self.a_vals), f(self.b_vals),
+                          f(self.a_offsets), f(self.b_offsets))
+
+
+def _segmented(S: int, mean: int, key_type: str, dist: str, seed: int, stream: int, device):
+    """S segments of lengths uniform in [0, 2*mean), each sorted (library
+    sort on (segment, key)); returns (keys, offsets)."""
+    _, unsigned, _ = KEY_TYPES[key_type]
+    lens = bounded(splitmix_stream(seed, 16 * STREAM_BERN + 8 + stream, S, device), 2 * mean)
+    off = torch.zeros(S + 1, dtype=torch.int64, device=device)
+    off[1:] = torch.cumsum(lens, 0)
+    total = int(off[-1].item())
+    keys = _keys(dist, key_type, seed, stream, total, device)
+    seg = torch.repeat_interleave(torch.arange(S, device=device), lens)
+    # order by (segment, key): a stable sort by key, then a stable sort by segment
+    flip = torch.iinfo(keys.dtype).min if unsigned else 0
+    order = torch.sort(keys ^ flip if unsigned else keys, stable=True).indices
+    order = order[torch.sort(seg[order], stable=True).indices]
+    return keys[order], off
+
+
+def batch_input(S: int, mean: int, key_type: str, dist: str, seed: int, payload: bool = True,
+                device="cpu") -> BatchInput:
+    """S independent merge pairs, segment lengths
+    uniform in [0, 2*mean) on each side, keys of `dist` sorted per segment;
+    payloads as R13 over the concatenated arrays."""
+    a, aoff = _segmented(S, mean, key_type, dist, seed, STREAM_A, device)
+    b, boff = _segmented(S, mean, key_type, dist, seed, STREAM_B, device)
+    av = bv = None
+    if payload:
+        av, bv = source_payloads(a.numel(), b.numel(), device)
+    return BatchInput(key_type, a, b, av, bv, aoff, boff)
+
+
 # BASELINE.json configs (index 1..5 as in SURVEY.md §8).  `scale` divides the
 # sizes (power of two) for small parity cases of the same distribution.
 CONFIGS = {
@@ -190,6 +248,9 @@ CONFIGS = {
     4: dict(kind="merge", n=1 << 27, m=1 << 25, key_type="u64", dist="mostly:0x8000000000000000:9/10",
             payload=True),
     5: dict(kind="sort", N=1 << 28, key_type="u32", dist="bounded:1048576", payload=True),
+    # not a BASELINE.json config: the batched-merge NEXT row,
+    # 2^16 pairs of mean 2^10 + 2^10 elements (~1.3e8 elements), C1's key mix
+    6: dict(kind="batch", S=1 << 16, mean=1 << 10, key_type="u32", dist="bounded:65536", payload=True),
 }
 
 
@@ -199,6 +260,8 @@ def config_input(cfg: int, scale: int = 1, device="cpu"):
     if c["kind"] == "merge":
         return merge_input(max(c["n"] // scale, 1), max(c["m"] // scale, 1), c["key_type"], c["dist"], seed,
                            c["payload"], device)
+    if c["kind"] == "batch":
+        return batch_input(max(c["S"] // scale, 1), c["mean"], c["key_type"], c["dist"], seed, c["payload"], device)
     return sort_input(max(c["N"] // scale, 1), c["key_type"], c["dist"], seed, c["payload"], device)
 
 
