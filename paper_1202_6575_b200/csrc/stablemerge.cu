@@ -272,15 +272,172 @@ static bool overlaps(const void* p, size_t pb, const void* q, size_t qb) {
 // ------------------------------------------------------------ merge
 template <typename K>
 static sm_status merge_device(const K* A, const uint32_t* vA, int64_t n, const K* B, const uint32_t* vB, int64_t m,
-                              K* C, uint32_t* vC, cudaStream_t st, int64_t pA, int64_t pB, bool pdl) {
+                              K* C, uint32_t* vC, cudaStream_t st, int64_t pA, int64_t pB, bool pdl,
+                              int* ranks_given = nullptr) {
     Geom g{};
     g.S = 1; g.pA = (int)pA; g.pB = (int)pB; g.n = (int)n; g.m = (int)m; g.L = 0; g.N = 0; g.sort = 0;
-    int* ranks = nullptr;
-    sm_status s = dalloc(&ranks, (pA + 1) + (pB + 1), st);
+    int* ranks = ranks_given;
+    sm_status s = SM_OK;
+    if (!ranks) s = dalloc(&ranks, (pA + 1) + (pB + 1), st);
     if (s != SM_OK) return s;
     if (vC) s = launch_merge<K, true>(A, vA, B, vB, C, vC, g, ranks, ranks + pA + 1, st, pdl);
     else s = launch_merge<K, false>(A, nullptr, B, nullptr, C, nullptr, g, ranks, ranks + pA + 1, st, pdl);
-    dfree(ranks, st);
+    if (!ranks_given) dfree(ranks, st);
+    return s;
+}
+
+// ----------------------------------------------- pipelined host staging
+// A call with HOST inputs is cut into independent sub-merges with the paper's
+// own Steps 1-4 at coarse granularity (p_h blocks per array, PAPER.md
+// L168-340): 2 p_h binary searches over the host arrays give the cross ranks,
+// the five cases give 2 p_h disjoint tasks with their input ranges and output
+// offsets.  Each task then runs the full device path (K1 + K2) on its own
+// sub-ranges, and the tasks alternate between two streams so that one task's
+// device->host copy overlaps the next one's host->device copy (the copy
+// engines are independent); the merge itself is ~1% of the staged call.
+struct SubMerge {
+    int64_t a0, a1, b0, b1;
+};
+
+template <typename K>
+static int64_t host_pipeline_blocks(int64_t n, int64_t m, bool has_v) {
+    const int64_t bytes = (n + m) * (int64_t)(sizeof(K) + (has_v ? 4 : 0));
+    return std::max<int64_t>(1, std::min<int64_t>(32, bytes / (16ll << 20)));
+}
+
+static inline int64_t hblock_start(int64_t len, int64_t p, int64_t i) {    // x_i, L168-182; x_p = len
+    const int64_t q = len / p, r = len % p;
+    return i < r ? i * (q + 1) : i * q + r;
+}
+
+static inline int64_t hblock_of(int64_t len, int64_t p, int64_t k) {       // L294-300; block_of(len) = p (R3)
+    if (k >= len) return p;
+    const int64_t q = len / p, r = len % p, big = r * (q + 1);
+    return k < big ? k / (q + 1) : (k - big) / q + r;
+}
+
+template <typename K>
+static void host_plan(const K* A, int64_t n, const K* B, int64_t m, int64_t p, std::vector<SubMerge>& tasks) {
+    std::vector<int64_t> x(p + 1), y(p + 1), xb(p + 1), yb(p + 1);
+    for (int64_t i = 0; i <= p; ++i) {
+        x[i] = hblock_start(n, p, i);
+        y[i] = hblock_start(m, p, i);
+    }
+    for (int64_t i = 0; i < p; ++i) {      // Step 1: xbar_i = rank_low(A[x_i], B); empty block start -> m (R4)
+        xb[i] = x[i] < n ? std::lower_bound(B, B + m, A[x[i]]) - B : m;
+        yb[i] = y[i] < m ? std::upper_bound(A, A + n, B[y[i]]) - A : n;   // Step 2: rank_high
+    }
+    xb[p] = m;
+    yb[p] = n;
+    for (int64_t i = 0; i < p; ++i) {      // Step 3, cases tested (a), (e), (b), (d), (c) (R8, R1)
+        SubMerge t;
+        if (xb[i] == xb[i + 1]) {
+            t = {x[i], x[i + 1], xb[i], xb[i]};
+        } else {
+            const int64_t j = hblock_of(m, p, xb[i]);
+            if (xb[i] == y[j]) t = {x[i], yb[j], xb[i], xb[i]};
+            else if (hblock_of(m, p, xb[i + 1]) == j) t = {x[i], x[i + 1], xb[i], xb[i + 1]};
+            else if (xb[i + 1] == y[j + 1]) t = {x[i], x[i + 1], xb[i], y[j + 1]};
+            else t = {x[i], yb[j + 1], xb[i], y[j + 1]};
+        }
+        tasks.push_back(t);
+    }
+    for (int64_t j = 0; j < p; ++j) {      // Step 4: the mirror (ties still to A, R2)
+        SubMerge t;
+        if (yb[j] == yb[j + 1]) {
+            t = {yb[j], yb[j], y[j], y[j + 1]};
+        } else {
+            const int64_t i = hblock_of(n, p, yb[j]);
+            if (yb[j] == x[i]) t = {yb[j], yb[j], y[j], xb[i]};
+            else if (hblock_of(n, p, yb[j + 1]) == i) t = {yb[j], yb[j + 1], y[j], y[j + 1]};
+            else if (yb[j + 1] == x[i + 1]) t = {yb[j], x[i + 1], y[j], y[j + 1]};
+            else t = {yb[j], x[i + 1], y[j], xb[i + 1]};
+        }
+        tasks.push_back(t);
+    }
+    std::sort(tasks.begin(), tasks.end(),
+              [](const SubMerge& u, const SubMerge& v) { return u.a0 + u.b0 < v.a0 + v.b0; });
+}
+
+
+template <typename K>
+static sm_status merge_host_pipelined(const K* A, const uint32_t* vA, int64_t n, const K* B, const uint32_t* vB,
+                                      int64_t m, K* C, uint32_t* vC, cudaStream_t st, bool pdl) {
+    // two-stage pipeline: stream sH uploads task after task without a break,
+    // stream sD merges each task once its upload event fires, then downloads
+    // it -- so the two copy engines stay busy concurrently
+    thread_local cudaStream_t sH = nullptr, sD = nullptr;
+    thread_local cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    thread_local std::vector<cudaEvent_t> ev_up;
+    if (!sH) {
+        if (cudaStreamCreateWithFlags(&sH, cudaStreamNonBlocking) != cudaSuccess ||
+            cudaStreamCreateWithFlags(&sD, cudaStreamNonBlocking) != cudaSuccess ||
+            cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming) != cudaSuccess)
+            return fail_cuda(cudaGetLastError(), "stream/event create");
+    }
+    std::vector<SubMerge> tasks;
+    host_plan<K>(A, n, B, m, host_pipeline_blocks<K>(n, m, vC != nullptr), tasks);
+    while (ev_up.size() < tasks.size()) {
+        cudaEvent_t e;
+        if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess)
+            return fail_cuda(cudaGetLastError(), "event create");
+        ev_up.push_back(e);
+    }
+    const size_t kb = sizeof(K);
+    const int64_t T = tile_t((int)kb, vC != nullptr);
+    // every device buffer comes from `st` before the fork (stream-ordered pool)
+    int64_t rank_ints = 0;
+    for (const SubMerge& t : tasks)
+        rank_ints += std::max<int64_t>(1, ceil_div(t.a1 - t.a0, T)) + std::max<int64_t>(1, ceil_div(t.b1 - t.b0, T)) + 2;
+    K *dA = nullptr, *dB = nullptr, *dC = nullptr;
+    uint32_t *dvA = nullptr, *dvB = nullptr, *dvC = nullptr;
+    int* dranks = nullptr;
+    sm_status s = dalloc(&dranks, rank_ints, st);
+    if (s == SM_OK) s = dalloc(&dA, n, st);
+    if (s == SM_OK) s = dalloc(&dB, m, st);
+    if (s == SM_OK) s = dalloc(&dC, n + m, st);
+    if (s == SM_OK && vC) s = dalloc(&dvA, n, st);
+    if (s == SM_OK && vC) s = dalloc(&dvB, m, st);
+    if (s == SM_OK && vC) s = dalloc(&dvC, n + m, st);
+    if (s == SM_OK) {
+        cudaEventRecord(ev_fork, st);
+        cudaStreamWaitEvent(sH, ev_fork, 0);
+        cudaStreamWaitEvent(sD, ev_fork, 0);
+    }
+    // uploads
+    for (size_t k = 0; s == SM_OK && k < tasks.size(); ++k) {
+        const SubMerge& t = tasks[k];
+        const int64_t la = t.a1 - t.a0, lb = t.b1 - t.b0;
+        cudaError_t e = cudaSuccess;
+        if (la) e = cudaMemcpyAsync(dA + t.a0, A + t.a0, la * kb, cudaMemcpyDefault, sH);
+        if (e == cudaSuccess && lb) e = cudaMemcpyAsync(dB + t.b0, B + t.b0, lb * kb, cudaMemcpyDefault, sH);
+        if (e == cudaSuccess && vC && la) e = cudaMemcpyAsync(dvA + t.a0, vA + t.a0, la * 4, cudaMemcpyDefault, sH);
+        if (e == cudaSuccess && vC && lb) e = cudaMemcpyAsync(dvB + t.b0, vB + t.b0, lb * 4, cudaMemcpyDefault, sH);
+        if (e == cudaSuccess) e = cudaEventRecord(ev_up[k], sH);
+        if (e != cudaSuccess) s = fail_cuda(e, "cudaMemcpyAsync H2D");
+    }
+    // merges and downloads
+    int64_t rank_at = 0;
+    for (size_t k = 0; s == SM_OK && k < tasks.size(); ++k) {
+        const SubMerge& t = tasks[k];
+        const int64_t la = t.a1 - t.a0, lb = t.b1 - t.b0, L = la + lb, off = t.a0 + t.b0;
+        if (L == 0) continue;
+        cudaStreamWaitEvent(sD, ev_up[k], 0);
+        const int64_t pa = std::max<int64_t>(1, ceil_div(la, T)), pb = std::max<int64_t>(1, ceil_div(lb, T));
+        s = merge_device<K>(dA + t.a0, vC ? dvA + t.a0 : nullptr, la, dB + t.b0, vC ? dvB + t.b0 : nullptr, lb,
+                            dC + off, vC ? dvC + off : nullptr, sD, pa, pb, pdl, dranks + rank_at);
+        rank_at += pa + pb + 2;
+        if (s != SM_OK) break;
+        cudaError_t e = cudaMemcpyAsync(C + off, dC + off, L * kb, cudaMemcpyDefault, sD);
+        if (e == cudaSuccess && vC) e = cudaMemcpyAsync(vC + off, dvC + off, L * 4, cudaMemcpyDefault, sD);
+        if (e != cudaSuccess) s = fail_cuda(e, "cudaMemcpyAsync D2H");
+    }
+    cudaEventRecord(ev_join, sH);                  // join: st waits for both streams
+    cudaStreamWaitEvent(st, ev_join, 0);
+    cudaEventRecord(ev_join, sD);
+    cudaStreamWaitEvent(st, ev_join, 0);
+    for (void* q : {(void*)dA, (void*)dB, (void*)dC, (void*)dvA, (void*)dvB, (void*)dvC, (void*)dranks}) dfree(q, st);
     return s;
 }
 
@@ -325,6 +482,11 @@ static sm_status merge_entry(const K* A, const uint32_t* vA, int64_t n, const K*
     const bool host = is_host_ptr(A) || is_host_ptr(B) || is_host_ptr(vA) || is_host_ptr(vB) || is_host_ptr(C) ||
                       is_host_ptr(vC);
     if (!host) return merge_device<K>(A, vA, n, B, vB, m, C, vC, st, pA, pB, pdl);
+
+    // Host inputs large enough to pipeline: sub-merges over two streams.
+    const bool host_inputs = is_host_ptr(A) && is_host_ptr(B) && (!vC || (is_host_ptr(vA) && is_host_ptr(vB)));
+    if (host_inputs && host_pipeline_blocks<K>(n, m, vC != nullptr) > 1)
+        return merge_host_pipelined<K>(A, vA, n, B, vB, m, C, vC, st, pdl);
 
     // Host buffers: stage every buffer of the call through device memory.
     Stage sA, sB, svA, svB, sC, svC;

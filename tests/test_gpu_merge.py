@@ -201,6 +201,25 @@ def test_merge_host_buffers():
     assert_bit_exact(*got, *want, "u64")
 
 
+@pytest.mark.parametrize("kt,payload,dist", [("i32", False, "full"), ("u32", True, "bounded:65536"),
+                                             ("u64", True, "mostly:0x8000000000000000:9/10"),
+                                             ("i64", True, "equal")])
+@pytest.mark.parametrize("pinned", [True, False])
+def test_merge_host_pipelined(kt, payload, dist, pinned):
+    """Host inputs above the pipelining threshold (>= 64 MB): the library
+    cuts the call into sub-merges with the paper's Steps 1-4 on the host and
+    streams them over two CUDA streams -- same bytes as the oracle."""
+    sm = lib()
+    eb = synth.elem_bytes(kt, payload)
+    n = (100 << 20) // eb // 2 + 12345
+    m = (100 << 20) // eb // 2 - 999
+    inp = synth.merge_input(n, m, kt, dist, seed=4242, payload=payload)
+    want = oracle_merge(inp)
+    f = (lambda t: None if t is None else t.pin_memory()) if pinned else (lambda t: t)
+    got = sm.merge_stable(f(inp.a_keys), f(inp.a_vals), f(inp.b_keys), f(inp.b_vals), key_type=kt)
+    assert_bit_exact(*got, *want, kt)
+
+
 def test_merge_errors():
     sm = lib()
     a = torch.arange(100, dtype=torch.int32, device="cuda")
