@@ -27,8 +27,13 @@
  * pointers the call is fully asynchronous on `stream`.  If any key/payload
  * pointer of a call is host memory, the library stages all of that call's
  * buffers through device memory (cudaMemcpyAsync host->device, the kernels,
- * device->host) on `stream`; host outputs are valid once `stream` has been
- * synchronised (for pageable outputs the final copy is synchronous).
+ * device->host) ordered after `stream`; host outputs are valid once `stream`
+ * has been synchronised (for pageable outputs the final copy is
+ * synchronous).  merge_stable with host inputs above 32 MB is cut on the
+ * host into 2 p_h independent sub-merges (Steps 1-4 at p_h <= 32 blocks per
+ * array) pipelined over two internal streams (uploads || merges+downloads),
+ * joined back into `stream`; the library reads the host keys for that
+ * partition (2 p_h binary searches).
  * Ownership: the caller owns every buffer; the library never frees or
  * retains them past the stream point of the call.  Scratch (the two
  * cross-rank arrays of p+1 entries, L373-375; the merge sort's auxiliary
