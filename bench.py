@@ -73,6 +73,8 @@ def args_():
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--cpu-seconds", type=float, default=10.0, help="bounded CPU-oracle sample budget")
     ap.add_argument("--no-extras", action="store_true", help="timed loop only (for ncu launch lists)")
+    ap.add_argument("--merge-path", action="store_true",
+                    help="merges only: time the equal-output merge-path COMPARISON instead of the paper's method")
     return ap.parse_args()
 
 
@@ -224,9 +226,12 @@ class MergeWork(Workload):
         self.out_v = torch.empty(n + m, dtype=torch.int32, device=dev) if c["payload"] else None
         self.sm = sm
 
+    merge_path = False
+
     def call(self):
         i = self.inp
-        self.sm.merge_stable(i.a_keys, i.a_vals, i.b_keys, i.b_vals, self.out_k, self.out_v, key_type=self.kt)
+        self.sm.merge_stable(i.a_keys, i.a_vals, i.b_keys, i.b_vals, self.out_k, self.out_v, key_type=self.kt,
+                             merge_path=self.merge_path)
 
     def e2e_setup(self, stream):
         h = self.host = self.inp.to("cpu")
@@ -381,6 +386,7 @@ def run_ours(a, world, rank, local):
     cfg = a.config
     clocks = ClockSampler(local).start()
     wl = make_workload(cfg, rank_seed(cfg, rank), dev, sm)     # inputs resident in HBM
+    wl.merge_path = a.merge_path
     per_step_events = wl.c["kind"] == "sort" or wl.step_bytes() < 4 * L2_BYTES
     flush = torch.empty(2 * L2_BYTES // 4, dtype=torch.int32, device=dev) if per_step_events else None
 
@@ -559,7 +565,9 @@ def main():
                    "l2": ("per-step events, L2 flushed (2x L2 write) and sort input restored between timed steps"
                           if r["per_step_events"] else
                           f"inputs+output {wl.step_bytes() / 1e9:.2f} GB > 126 MB L2: no flush, back-to-back steps"),
-                   "parallelism": f"replicas x{world}" if world > 1 else "1 GPU"},
+                   "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
+                   "method": ("merge-path comparison (equal output tiles; NOT the paper's method)" if a.merge_path
+                              else "paper: cross ranks + cases (a)-(e)")},
         "achieved_hbm_gbs": wl.step_bytes() / (r["ms_per_step"] * 1e-3) / 1e9,
         "algorithmic_bytes_per_step": wl.step_bytes(),
         "gpu_launches": r["launches"],

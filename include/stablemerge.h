@@ -169,8 +169,9 @@ sm_status mergesort_stable_u64(uint64_t *keys, uint32_t *vals, int64_t N, void *
  *              p_A = ceil(n/T), p_B = ceil(m/T); 2T <= tile capacity.
  *   sort_run   merge sort initial run length R (0 = default; must equal
  *              the block-sort tile of the key type, or be rejected)
- *   flags      bit 0: disable programmatic dependent launch between the
- *              cross-rank and task kernels.
+ *   flags      bit 0 (SM_FLAG_NO_PDL): disable programmatic dependent launch
+ *              between the cross-rank and task kernels; bit 1
+ *              (SM_FLAG_MERGE_PATH): the merge-path comparison below.
  * ------------------------------------------------------------------- */
 typedef struct {
     int64_t p_A;
@@ -181,6 +182,12 @@ typedef struct {
 } sm_options;
 
 #define SM_FLAG_NO_PDL 1
+/* merge_stable_ex only, device pointers only: the merge-path COMPARISON
+ * ([AklSantoro87]) -- C cut into
+ * tiles of exactly tile-capacity outputs by one binary search per diagonal,
+ * instead of the paper's cross ranks and cases.  Same output; exists to
+ * measure what the paper's factor-two task imbalance costs.  Not the method. */
+#define SM_FLAG_MERGE_PATH 2
 
 sm_status merge_stable_ex_u32(const uint32_t *keys_A, const uint32_t *vals_A, int64_t n,
                               const uint32_t *keys_B, const uint32_t *vals_B, int64_t m,

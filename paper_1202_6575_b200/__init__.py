@@ -43,6 +43,7 @@ _CARRIER = {"u32": (torch.int32, torch.uint32), "i32": (torch.int32,), "i64": (t
 
 SM_OK, SM_EINVAL, SM_EALIAS, SM_ENOMEM, SM_ECUDA = range(5)
 SM_FLAG_NO_PDL = 1
+SM_FLAG_MERGE_PATH = 2
 
 
 class SmOptions(ctypes.Structure):
@@ -167,8 +168,10 @@ def merge_stable(a_keys: torch.Tensor, a_vals: Optional[torch.Tensor], b_keys: t
                  b_vals: Optional[torch.Tensor], out_keys: Optional[torch.Tensor] = None,
                  out_vals: Optional[torch.Tensor] = None, *, key_type: Optional[str] = None, stream=None,
                  p_A: Optional[int] = None, p_B: Optional[int] = None, block: Optional[int] = None,
-                 pdl: bool = True):
-    """Stable merge of sorted A and B (ties: A first).  Returns (keys, vals)."""
+                 pdl: bool = True, merge_path: bool = False):
+    """Stable merge of sorted A and B (ties: A first).  Returns (keys, vals).
+    merge_path=True runs the equal-output merge-path COMPARISON instead of the
+    paper's method (same result; CUDA tensors only)."""
     kt = _key_type(a_keys, key_type)
     _key_type(b_keys, kt)
     if (a_vals is None) != (b_vals is None):
@@ -182,7 +185,7 @@ def merge_stable(a_keys: torch.Tensor, a_vals: Optional[torch.Tensor], b_keys: t
     if out_keys.numel() != n + m or (out_vals is not None and out_vals.numel() != n + m):
         raise ValueError("output length must be n + m")
     s = _stream_for(a_keys, stream)
-    opt = _options(p_A, p_B, block, 0 if pdl else SM_FLAG_NO_PDL)
+    opt = _options(p_A, p_B, block, (0 if pdl else SM_FLAG_NO_PDL) | (SM_FLAG_MERGE_PATH if merge_path else 0))
     args = (_ptr(a_keys), _ptr(a_vals), n, _ptr(b_keys), _ptr(b_vals), m, _ptr(out_keys), _ptr(out_vals), s)
     if opt is None:
         _check(getattr(_lib, f"merge_stable_{kt}")(*args), f"merge_stable_{kt}")

@@ -79,7 +79,7 @@ struct Geom {
     int pA, pB;           // block counts per segment (modes 0, 1)
     int n, m;             // plain merge sizes (mode 0)
     int L, N;             // sort round: run length, total length (mode 1)
-    int sort;             // mode: 0 merge, 1 sort round, 2 batch
+    int sort;             // mode: 0 merge, 1 sort round, 2 batch, 3 merge-path comparison
     int T;                // mode 2: block size
     const SegInfo* segs;  // mode 2: segment table [S]
     const int* totals;    // mode 2: [0] = tasks, [1] = rank entries
@@ -107,7 +107,7 @@ __device__ __forceinline__ Seg segment(const Geom& g, int s, int* xbar, int* yba
     r.pA = g.pA; r.pB = g.pB;
     r.xs = xbar + (size_t)s * (g.pA + 1);
     r.ys = ybar + (size_t)s * (g.pB + 1);
-    if (g.sort == 0) {
+    if (g.sort == 0 || g.sort == 3) {
         r.aoff = 0; r.n = g.n; r.boff = 0; r.m = g.m; r.coff = 0;
     } else {
         r.aoff = s * 2 * g.L;                       // < N < 2^31 for s < S
@@ -121,6 +121,7 @@ __device__ __forceinline__ Seg segment(const Geom& g, int s, int* xbar, int* yba
 
 // Number of tasks / rank entries of the launch (mode 2: from the device).
 __device__ __forceinline__ int total_tasks(const Geom& g) {
+    if (g.sort == 3) return (g.n + g.m + g.T - 1) / g.T;   // equal output tiles of T
     return g.sort == 2 ? g.totals[0] : g.S * (g.pA + g.pB);
 }
 __device__ __forceinline__ int total_rank_items(const Geom& g) {

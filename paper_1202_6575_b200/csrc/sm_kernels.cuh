@@ -101,9 +101,20 @@ __global__ void __launch_bounds__(256) k_cross_ranks(const K* __restrict__ A, co
     pdl_launch_dependents();
 }
 
-// Decode a task (rows a4/a5).
+// Decode a task (rows a4/a5).  Mode 3 (the merge-path comparison, not the
+// paper's method): task k is output tile [kT, (k+1)T) with the diagonal
+// splits of K1mp in xbar.
 __device__ __forceinline__ Task decode_task(const Geom& g, int task, const int* __restrict__ xbar,
                                             const int* __restrict__ ybar, Seg& sg) {
+    if (g.sort == 3) {
+        sg = segment(g, 0, (int*)xbar, (int*)ybar);
+        const int d0 = task * g.T, d1 = min(g.n + g.m, d0 + g.T);
+        Task t;
+        t.side = 0; t.kase = CASE_B;
+        t.a0 = xbar[task]; t.a1 = xbar[task + 1];
+        t.b0 = d0 - t.a0; t.b1 = d1 - t.a1;
+        return t;
+    }
     int t;
     const int s = locate(g, task, false, t);
     sg = segment(g, s, (int*)xbar, (int*)ybar);
@@ -560,6 +571,31 @@ __global__ void __launch_bounds__(K2Layout<K, HAS_V, NC, VT, STAGES, MAXT, WB>::
         }
     }
     if (WB) bulk_wait_read<0>();
+}
+
+// ------------------------------------------------ merge-path comparison
+// SURVEY.md §8(f) row 4, an A/B comparison only (the equal-output
+// partitioning of [AklSantoro87], the class the paper contrasts itself with,
+// P:L49-59): split C into tiles of exactly T outputs; the split of diagonal
+// D is the smallest i in [max(0, D-m), min(D, n)] with A[i] > B[D-1-i]
+// (ties to A, reading R17), one binary search per diagonal over global
+// memory.  Same output bytes as the method; no factor-two imbalance.
+template <typename K>
+__global__ void __launch_bounds__(256) k_diag_splits(const K* __restrict__ A, const K* __restrict__ B, int n, int m,
+                                                     int T, int* __restrict__ split) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    const int tiles = (n + m + T - 1) / T;
+    if (k <= tiles) {
+        const int D = min(n + m, k * T);
+        int lo = max(0, D - m), hi = min(D, n);
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (__ldg(A + mid) <= __ldg(B + (D - 1 - mid))) lo = mid + 1;
+            else hi = mid;
+        }
+        split[k] = lo;
+    }
+    pdl_launch_dependents();
 }
 
 // ------------------------------------------------------- batch setup

@@ -286,6 +286,34 @@ static sm_status merge_device(const K* A, const uint32_t* vA, int64_t n, const K
     return s;
 }
 
+// ------------------------------------------- merge-path comparison (f4)
+// Equal-output tiles of NV (one tile per ring stage), diagonal splits by
+// K1mp, the same K2 -- to measure what the paper's factor-two task
+// imbalance costs against perfectly balanced tiles.
+template <typename K>
+static sm_status merge_path_device(const K* A, const uint32_t* vA, int64_t n, const K* B, const uint32_t* vB,
+                                   int64_t m, K* C, uint32_t* vC, cudaStream_t st, bool pdl) {
+    const int64_t W = tile_nv((int)sizeof(K), vC != nullptr);
+    const int64_t tiles = ceil_div(n + m, W);
+    int* split = nullptr;
+    sm_status s = dalloc(&split, tiles + 1, st);
+    if (s != SM_OK) return s;
+    prof_before(PROF_K1, st);
+    k_diag_splits<K><<<(unsigned)((tiles + 1 + 255) / 256), 256, 0, st>>>(A, B, (int)n, (int)m, (int)W, split);
+    prof_after(st);
+    s = check_launch("k_diag_splits");
+    if (s == SM_OK) {
+        Geom g{};
+        g.S = 1; g.n = (int)n; g.m = (int)m; g.sort = 3; g.T = (int)W; g.pA = g.pB = 1;
+        GeomCounts gc{tiles + 2, tiles};
+        if (vC) s = launch_tasks<K, true, typename K2Shape<K, true>::type>(A, vA, B, vB, C, vC, g, gc, split, split, st, pdl);
+        else s = launch_tasks<K, false, typename K2Shape<K, false>::type>(A, nullptr, B, nullptr, C, nullptr, g, gc, split,
+                                                                         split, st, pdl);
+    }
+    dfree(split, st);
+    return s;
+}
+
 // ----------------------------------------------- pipelined host staging
 // A call with HOST inputs is cut into independent sub-merges with the paper's
 // own Steps 1-4 at coarse granularity (p_h blocks per array, PAPER.md
@@ -478,6 +506,12 @@ static sm_status merge_entry(const K* A, const uint32_t* vA, int64_t n, const K*
     const bool pdl = !(opt && (opt->flags & SM_FLAG_NO_PDL));
     if (n + m == 0) return SM_OK;
     keep_pool(st);
+    if (opt && (opt->flags & SM_FLAG_MERGE_PATH)) {
+        if (is_host_ptr(A) || is_host_ptr(B) || is_host_ptr(vA) || is_host_ptr(vB) || is_host_ptr(C) ||
+            is_host_ptr(vC))
+            return fail_inval("the merge-path comparison takes device pointers only");
+        return merge_path_device<K>(A, vA, n, B, vB, m, C, vC, st, pdl);
+    }
 
     const bool host = is_host_ptr(A) || is_host_ptr(B) || is_host_ptr(vA) || is_host_ptr(vB) || is_host_ptr(C) ||
                       is_host_ptr(vC);

@@ -220,6 +220,23 @@ def test_merge_host_pipelined(kt, payload, dist, pinned):
     assert_bit_exact(*got, *want, kt)
 
 
+@pytest.mark.parametrize("cfg,scale", [(1, 4), (2, 64), (3, 64), (4, 32)])
+def test_merge_path_comparison_same_bytes(cfg, scale):
+    """The merge-path comparison variant produces the
+    same unique stable merge."""
+    sm = lib()
+    inp = synth.config_input(cfg, scale=scale)
+    assert_bit_exact(*gpu_merge(sm, inp, merge_path=True), *oracle_merge(inp), inp.key_type)
+
+
+@pytest.mark.parametrize("nm", [(1, 0), (0, 1), (5, 3), (8095, 8097), (20000, 1), (3, 70001)])
+def test_merge_path_comparison_ragged(nm):
+    sm = lib()
+    for kt in ("i32", "u64"):
+        inp = synth.merge_input(*nm, kt, "bounded:3", seed=sum(nm), payload=kt == "u64")
+        assert_bit_exact(*gpu_merge(sm, inp, merge_path=True), *oracle_merge(inp), kt)
+
+
 def test_merge_errors():
     sm = lib()
     a = torch.arange(100, dtype=torch.int32, device="cuda")
