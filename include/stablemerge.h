@@ -19,8 +19,12 @@
  * (swapping would flip the tie rule).  Sentinels A[-1] = -inf, A[n] = +inf are
  * virtual and never stored (L69-71).
  *
- * Key order: _u32 / _u64 compare unsigned, _i32 / _i64 compare signed
- * (two's complement).  Payloads are uint32 and travel with their key.
+ * Key order ("<=" of PAPER.md L63): _u32 / _u64 compare unsigned, _i32 /
+ * _i64 signed (two's complement), _f32 / _f64 by IEEE 754 totalOrder
+ * (-NaN < -inf < ... < -0.0 < +0.0 < ... < +inf < +NaN; SURVEY.md §8(f)
+ * row 2) -- a total order, so the stable merge is unique.  Inputs must be
+ * non-decreasing in that order (e.g. sorted by mergesort_stable_f32).
+ * Payloads are uint32 and travel with their key.
  *
  * Memory: every pointer may be DEVICE memory (cudaMalloc / torch CUDA
  * tensors / managed) or HOST memory (pinned or pageable).  With device
@@ -97,6 +101,12 @@ sm_status merge_stable_i64(const int64_t *keys_A, const uint32_t *vals_A, int64_
 sm_status merge_stable_u64(const uint64_t *keys_A, const uint32_t *vals_A, int64_t n,
                            const uint64_t *keys_B, const uint32_t *vals_B, int64_t m,
                            uint64_t *out_keys, uint32_t *out_vals, void *stream);
+sm_status merge_stable_f32(const float *keys_A, const uint32_t *vals_A, int64_t n,
+                           const float *keys_B, const uint32_t *vals_B, int64_t m,
+                           float *out_keys, uint32_t *out_vals, void *stream);
+sm_status merge_stable_f64(const double *keys_A, const uint32_t *vals_A, int64_t n,
+                           const double *keys_B, const uint32_t *vals_B, int64_t m,
+                           double *out_keys, uint32_t *out_vals, void *stream);
 
 /* ---------------------------------------------------------------------
  * merge_stable_batched_<K>  -- SURVEY.md §8(f) row 1: S independent stable
@@ -136,6 +146,14 @@ sm_status merge_stable_batched_u64(const uint64_t *keys_A, const uint32_t *vals_
                                    const int64_t *a_offsets, const uint64_t *keys_B, const uint32_t *vals_B,
                                    int64_t m, const int64_t *b_offsets, int64_t S, uint64_t *out_keys,
                                    uint32_t *out_vals, void *stream);
+sm_status merge_stable_batched_f32(const float *keys_A, const uint32_t *vals_A, int64_t n,
+                                   const int64_t *a_offsets, const float *keys_B, const uint32_t *vals_B,
+                                   int64_t m, const int64_t *b_offsets, int64_t S, float *out_keys,
+                                   uint32_t *out_vals, void *stream);
+sm_status merge_stable_batched_f64(const double *keys_A, const uint32_t *vals_A, int64_t n,
+                                   const int64_t *a_offsets, const double *keys_B, const uint32_t *vals_B,
+                                   int64_t m, const int64_t *b_offsets, int64_t S, double *out_keys,
+                                   uint32_t *out_vals, void *stream);
 
 /* ---------------------------------------------------------------------
  * mergesort_stable_<K>  -- SURVEY.md §8 rows a8-a9 (§3).
@@ -156,6 +174,8 @@ sm_status mergesort_stable_u32(uint32_t *keys, uint32_t *vals, int64_t N, void *
 sm_status mergesort_stable_i32(int32_t *keys, uint32_t *vals, int64_t N, void *stream);
 sm_status mergesort_stable_i64(int64_t *keys, uint32_t *vals, int64_t N, void *stream);
 sm_status mergesort_stable_u64(uint64_t *keys, uint32_t *vals, int64_t N, void *stream);
+sm_status mergesort_stable_f32(float *keys, uint32_t *vals, int64_t N, void *stream);
+sm_status mergesort_stable_f64(double *keys, uint32_t *vals, int64_t N, void *stream);
 
 /* ---------------------------------------------------------------------
  * Test / tuning variants (not the contract).
@@ -205,6 +225,14 @@ sm_status merge_stable_ex_u64(const uint64_t *keys_A, const uint32_t *vals_A, in
                               const uint64_t *keys_B, const uint32_t *vals_B, int64_t m,
                               uint64_t *out_keys, uint32_t *out_vals, void *stream,
                               const sm_options *opt);
+sm_status merge_stable_ex_f32(const float *keys_A, const uint32_t *vals_A, int64_t n,
+                              const float *keys_B, const uint32_t *vals_B, int64_t m,
+                              float *out_keys, uint32_t *out_vals, void *stream,
+                              const sm_options *opt);
+sm_status merge_stable_ex_f64(const double *keys_A, const uint32_t *vals_A, int64_t n,
+                              const double *keys_B, const uint32_t *vals_B, int64_t m,
+                              double *out_keys, uint32_t *out_vals, void *stream,
+                              const sm_options *opt);
 
 /* merge_plan_ex_<K>: Steps 1-4 only, dumped for parity with the oracle's plan
  * (Fig. 1, L73-117).  DEVICE pointers only (host -> SM_EINVAL).
@@ -226,6 +254,12 @@ sm_status merge_plan_ex_i64(const int64_t *keys_A, int64_t n, const int64_t *key
 sm_status merge_plan_ex_u64(const uint64_t *keys_A, int64_t n, const uint64_t *keys_B, int64_t m,
                             int64_t p_A, int64_t p_B, int64_t *xbar, int64_t *ybar, int64_t *tasks,
                             void *stream);
+sm_status merge_plan_ex_f32(const float *keys_A, int64_t n, const float *keys_B, int64_t m,
+                            int64_t p_A, int64_t p_B, int64_t *xbar, int64_t *ybar, int64_t *tasks,
+                            void *stream);
+sm_status merge_plan_ex_f64(const double *keys_A, int64_t n, const double *keys_B, int64_t m,
+                            int64_t p_A, int64_t p_B, int64_t *xbar, int64_t *ybar, int64_t *tasks,
+                            void *stream);
 
 sm_status mergesort_stable_ex_u32(uint32_t *keys, uint32_t *vals, int64_t N, void *stream,
                                   const sm_options *opt);
@@ -234,6 +268,10 @@ sm_status mergesort_stable_ex_i32(int32_t *keys, uint32_t *vals, int64_t N, void
 sm_status mergesort_stable_ex_i64(int64_t *keys, uint32_t *vals, int64_t N, void *stream,
                                   const sm_options *opt);
 sm_status mergesort_stable_ex_u64(uint64_t *keys, uint32_t *vals, int64_t N, void *stream,
+                                  const sm_options *opt);
+sm_status mergesort_stable_ex_f32(float *keys, uint32_t *vals, int64_t N, void *stream,
+                                  const sm_options *opt);
+sm_status mergesort_stable_ex_f64(double *keys, uint32_t *vals, int64_t N, void *stream,
                                   const sm_options *opt);
 
 /* Largest task (elements) one CTA tile holds for this key width / payload

@@ -29,8 +29,10 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "oracle.c")
 _LIB = os.path.join(_HERE, "liboracle.so")
 
-NP_DTYPES = {"u32": np.uint32, "i32": np.int32, "i64": np.int64, "u64": np.uint64}
-_C_KEY = {"u32": ctypes.c_uint32, "i32": ctypes.c_int32, "i64": ctypes.c_int64, "u64": ctypes.c_uint64}
+NP_DTYPES = {"u32": np.uint32, "i32": np.int32, "i64": np.int64, "u64": np.uint64, "f32": np.float32,
+             "f64": np.float64}
+_C_KEY = {"u32": ctypes.c_uint32, "i32": ctypes.c_int32, "i64": ctypes.c_int64, "u64": ctypes.c_uint64,
+          "f32": ctypes.c_float, "f64": ctypes.c_double}
 
 _lib = None
 

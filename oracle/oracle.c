@@ -24,7 +24,8 @@
  *   oracle_positions_*  the closed form of PAPER.md L158-166: A[i] goes to
  *                    C[i + rank_low(A[i],B)], B[j] to C[j + rank_high(B[j],A)].
  *
- * Keys: u32 / i32 / i64 / u64 with the natural (unsigned or signed) order.
+ * Keys: u32 / i32 / i64 / u64 with the natural (unsigned or signed) order;
+ * f32 / f64 with IEEE 754 totalOrder.
  * Payloads: uint32, travelling with their key; NULL payload pointers mean
  * keys only.  Sizes are int64.  No error paths: callers pass valid sizes.
  */
@@ -32,7 +33,20 @@
 #include <stdlib.h>
 #include <string.h>
 
-#define DEFINE_ORACLE(SUF, K)                                                         \
+/* The key order "<=": natural for integer keys; IEEE 754
+ * totalOrder for floating-point keys, through an integer key: the bit
+ * pattern read as a signed integer, with the magnitude bits of negative
+ * values inverted (so -NaN < -inf < ... < -0.0 < +0.0 < ... < +inf < +NaN). */
+static int32_t tot_f32(float x) { int32_t i; memcpy(&i, &x, 4); return i < 0 ? i ^ 0x7fffffff : i; }
+static int64_t tot_f64(double x) { int64_t i; memcpy(&i, &x, 8); return i < 0 ? i ^ 0x7fffffffffffffffLL : i; }
+#define LE_INT(a, b) ((a) <= (b))
+#define LT_INT(a, b) ((a) < (b))
+#define LE_F32(a, b) (tot_f32(a) <= tot_f32(b))
+#define LT_F32(a, b) (tot_f32(a) < tot_f32(b))
+#define LE_F64(a, b) (tot_f64(a) <= tot_f64(b))
+#define LT_F64(a, b) (tot_f64(a) < tot_f64(b))
+
+#define DEFINE_ORACLE(SUF, K, LE, LT)                                                 \
                                                                                       \
 /* Stable two-way merge, ties to A.  vc may be NULL (keys only). */                  \
 void oracle_merge_##SUF(const K *a, const uint32_t *va, int64_t n,                   \
@@ -41,7 +55,7 @@ void oracle_merge_##SUF(const K *a, const uint32_t *va, int64_t n,              
 {                                                                                     \
     int64_t i = 0, j = 0, k = 0;                                                     \
     while (i < n && j < m) {                                                         \
-        if (a[i] <= b[j]) {               /* tie -> A first */                       \
+        if (LE(a[i], b[j])) {             /* tie -> A first */                       \
             c[k] = a[i];                                                             \
             if (vc) vc[k] = va[i];                                                   \
             i++;                                                                     \
@@ -98,7 +112,7 @@ int64_t oracle_rank_low_##SUF(K x, const K *X, int64_t len)                     
     int64_t lo = 0, hi = len;       /* answer in [lo, hi] */                        \
     while (lo < hi) {                                                                \
         int64_t mid = lo + (hi - lo) / 2;                                            \
-        if (X[mid] < x) lo = mid + 1; else hi = mid;                                 \
+        if (LT(X[mid], x)) lo = mid + 1; else hi = mid;                              \
     }                                                                                \
     return lo;                                                                       \
 }                                                                                     \
@@ -109,7 +123,7 @@ int64_t oracle_rank_high_##SUF(K x, const K *X, int64_t len)                    
     int64_t lo = 0, hi = len;                                                        \
     while (lo < hi) {                                                                \
         int64_t mid = lo + (hi - lo) / 2;                                            \
-        if (X[mid] <= x) lo = mid + 1; else hi = mid;                                \
+        if (LE(X[mid], x)) lo = mid + 1; else hi = mid;                              \
     }                                                                                \
     return lo;                                                                       \
 }                                                                                     \
@@ -133,7 +147,9 @@ void oracle_positions_sample_##SUF(const K *a, int64_t n, const K *b, int64_t m,
     for (t = 0; t < nb; t++) pos_b[t] = jb[t] + oracle_rank_high_##SUF(b[jb[t]], a, n);\
 }
 
-DEFINE_ORACLE(u32, uint32_t)
-DEFINE_ORACLE(i32, int32_t)
-DEFINE_ORACLE(i64, int64_t)
-DEFINE_ORACLE(u64, uint64_t)
+DEFINE_ORACLE(u32, uint32_t, LE_INT, LT_INT)
+DEFINE_ORACLE(i32, int32_t, LE_INT, LT_INT)
+DEFINE_ORACLE(i64, int64_t, LE_INT, LT_INT)
+DEFINE_ORACLE(u64, uint64_t, LE_INT, LT_INT)
+DEFINE_ORACLE(f32, float, LE_F32, LT_F32)
+DEFINE_ORACLE(f64, double, LE_F64, LT_F64)

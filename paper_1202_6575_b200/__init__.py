@@ -15,6 +15,8 @@ Tensors may live on a CUDA device (asynchronous on the current stream) or on
 the host (the library stages them; the binding then synchronises the stream
 so host results are ready on return).  Unsigned keys: pass torch.uint32 /
 torch.uint64 tensors, or int32/int64 carriers with key_type="u32"/"u64".
+Floating-point keys (float32 / float64, or int32/int64 bit carriers with
+key_type="f32"/"f64") are ordered by IEEE 754 totalOrder.
 Payloads are 32-bit (int32 or uint32 tensors, same bits).
 """
 from __future__ import annotations
@@ -34,12 +36,13 @@ if not os.path.exists(LIB_PATH):
 
 _lib = ctypes.CDLL(LIB_PATH)
 
-KEY_TYPES = ("u32", "i32", "i64", "u64")
-_CT = {"u32": ctypes.c_uint32, "i32": ctypes.c_int32, "i64": ctypes.c_int64, "u64": ctypes.c_uint64}
-_BYTES = {"u32": 4, "i32": 4, "i64": 8, "u64": 8}
-_DTYPE_KT = {torch.int32: "i32", torch.int64: "i64", torch.uint32: "u32", torch.uint64: "u64"}
+KEY_TYPES = ("u32", "i32", "i64", "u64", "f32", "f64")
+_BYTES = {"u32": 4, "i32": 4, "i64": 8, "u64": 8, "f32": 4, "f64": 8}
+_DTYPE_KT = {torch.int32: "i32", torch.int64: "i64", torch.uint32: "u32", torch.uint64: "u64",
+             torch.float32: "f32", torch.float64: "f64"}
 _CARRIER = {"u32": (torch.int32, torch.uint32), "i32": (torch.int32,), "i64": (torch.int64,),
-            "u64": (torch.int64, torch.uint64)}
+            "u64": (torch.int64, torch.uint64), "f32": (torch.float32, torch.int32),
+            "f64": (torch.float64, torch.int64)}
 
 SM_OK, SM_EINVAL, SM_EALIAS, SM_ENOMEM, SM_ECUDA = range(5)
 SM_FLAG_NO_PDL = 1

@@ -5,6 +5,7 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <string.h>
 
 namespace sm {
 
@@ -28,32 +29,82 @@ struct Blocks {
 };
 
 // ---------------------------------------------------------------------------
-// Rows a1/a2: rank_low(x, X) = #{X[t] < x}, rank_high(x, X) = #{X[t] <= x}
-// (virtual sentinels are the search bounds, L69-71).
-// Branch-free halving search: the probe index is a select, not a branch.
+// The key order "<=" of PAPER.md L63 ("ordered by a relation <="): natural
+// order for integer keys (signed for i32/i64, unsigned for u32/u64, reading
+// R16) and IEEE 754 totalOrder for floating-point keys (SURVEY §8(f) row 2:
+// -NaN < -inf < ... < -0.0 < +0.0 < ... < +inf < +NaN).  Every key maps
+// bijectively and monotonically to an unsigned "order view" U (used by the
+// radix block sort and by the floating-point compares): identity for unsigned,
+// sign bit flipped for signed, sign bit flipped for non-negative floats and
+// all bits flipped for negative ones.
 // ---------------------------------------------------------------------------
 template <typename K>
-__device__ __forceinline__ int rank_low_dev(const K* __restrict__ X, int len, K x) {
-    int lo = 0;
-    while (len > 0) {
-        const int half = len >> 1;
-        const bool right = __ldg(X + lo + half) < x;
-        lo = right ? lo + half + 1 : lo;
-        len = right ? len - half - 1 : half;
+struct KeyOrd;
+template <> struct KeyOrd<uint32_t> {
+    using U = uint32_t;
+    static constexpr bool FLOAT = false;
+    __device__ __host__ __forceinline__ static U to(uint32_t x) { return x; }
+    __device__ __host__ __forceinline__ static uint32_t from(U u) { return u; }
+};
+template <> struct KeyOrd<int32_t> {
+    using U = uint32_t;
+    static constexpr bool FLOAT = false;
+    __device__ __host__ __forceinline__ static U to(int32_t x) { return (U)x ^ 0x80000000u; }
+    __device__ __host__ __forceinline__ static int32_t from(U u) { return (int32_t)(u ^ 0x80000000u); }
+};
+template <> struct KeyOrd<uint64_t> {
+    using U = uint64_t;
+    static constexpr bool FLOAT = false;
+    __device__ __host__ __forceinline__ static U to(uint64_t x) { return x; }
+    __device__ __host__ __forceinline__ static uint64_t from(U u) { return u; }
+};
+template <> struct KeyOrd<int64_t> {
+    using U = uint64_t;
+    static constexpr bool FLOAT = false;
+    __device__ __host__ __forceinline__ static U to(int64_t x) { return (U)x ^ 0x8000000000000000ull; }
+    __device__ __host__ __forceinline__ static int64_t from(U u) { return (int64_t)(u ^ 0x8000000000000000ull); }
+};
+template <> struct KeyOrd<float> {
+    using U = uint32_t;
+    static constexpr bool FLOAT = true;
+    __device__ __host__ __forceinline__ static U to(float x) {
+        U b;
+        memcpy(&b, &x, 4);
+        return b ^ ((U)((int32_t)b >> 31) | 0x80000000u);
     }
-    return lo;
-}
+    __device__ __host__ __forceinline__ static float from(U u) {
+        const U b = u ^ ((U)((int32_t)~u >> 31) | 0x80000000u);
+        float x;
+        memcpy(&x, &b, 4);
+        return x;
+    }
+};
+template <> struct KeyOrd<double> {
+    using U = uint64_t;
+    static constexpr bool FLOAT = true;
+    __device__ __host__ __forceinline__ static U to(double x) {
+        U b;
+        memcpy(&b, &x, 8);
+        return b ^ ((U)((int64_t)b >> 63) | 0x8000000000000000ull);
+    }
+    __device__ __host__ __forceinline__ static double from(U u) {
+        const U b = u ^ ((U)((int64_t)~u >> 63) | 0x8000000000000000ull);
+        double x;
+        memcpy(&x, &b, 8);
+        return x;
+    }
+};
 
+// a <= b and a < b in the key order (native compares for integer keys)
 template <typename K>
-__device__ __forceinline__ int rank_high_dev(const K* __restrict__ X, int len, K x) {
-    int lo = 0;
-    while (len > 0) {
-        const int half = len >> 1;
-        const bool right = __ldg(X + lo + half) <= x;
-        lo = right ? lo + half + 1 : lo;
-        len = right ? len - half - 1 : half;
-    }
-    return lo;
+__device__ __host__ __forceinline__ bool key_le(K a, K b) {
+    if constexpr (KeyOrd<K>::FLOAT) return KeyOrd<K>::to(a) <= KeyOrd<K>::to(b);
+    else return a <= b;
+}
+template <typename K>
+__device__ __host__ __forceinline__ bool key_lt(K a, K b) {
+    if constexpr (KeyOrd<K>::FLOAT) return KeyOrd<K>::to(a) < KeyOrd<K>::to(b);
+    else return a < b;
 }
 
 // ---------------------------------------------------------------------------

@@ -50,7 +50,7 @@ __device__ __forceinline__ int group_rank(const K* __restrict__ X, int len, K x,
         bool pred = false;
         if (hi > lo && sub < min(gg, n)) {
             const K v = __ldg(X + pos);
-            pred = high ? (v <= x) : (v < x);
+            pred = high ? key_le(v, x) : key_lt(v, x);
         }
         const unsigned bal = (__ballot_sync(0xffffffffu, pred) >> shift) & (G == 32 ? 0xffffffffu : ((1u << (G & 31)) - 1u));
         const int t = __popc(bal);          // probes passed: a prefix of the probing lanes
@@ -390,24 +390,52 @@ __device__ __forceinline__ bool k2_compute(const K* sk, const uint32_t* sv, cons
     if (cnt <= 0) return true;
     if (td.la > 0 && td.lb > 0) {
         // cases (b), (c), (d): stable merge (row a7), ties to A (R17)
-        const uint32_t sa0 = smem_addr(sk + td.a_s);
-        const uint32_t sb0 = smem_addr(sk + td.b_s);
-        const int ai = split_smem<K, LOG2NV>(sa0, td.la, sb0, td.lb, d);
-        const int bi = d - ai;
-        uint32_t pa = sa0 + ai * KB, pb = sb0 + bi * KB;
-        const uint32_t pae = sa0 + td.la * KB, pbe = sb0 + td.lb * KB;
-        K ka = lds<K>(pa), kb = lds<K>(pb), na = lds<K>(pa + KB), nb = lds<K>(pb + KB);
-        int src[VT];
-        int ia = td.va_s + ai, ib = td.vb_s + bi;
+        if constexpr (KeyOrd<K>::FLOAT) {
+            // floating-point keys: the same merge on the order view (C++ path)
+            using U = typename KeyOrd<K>::U;
+            const K* a = sk + td.a_s;
+            const K* b = sk + td.b_s;
+            int lo = max(0, d - td.lb), hi = min(d, td.la);
+            while (lo < hi) {
+                const int mid = (lo + hi) >> 1;
+                if (KeyOrd<K>::to(a[mid]) <= KeyOrd<K>::to(b[d - 1 - mid])) lo = mid + 1;
+                else hi = mid;
+            }
+            int ai = lo, bi = d - lo;
+            U ka = KeyOrd<K>::to(a[min(ai, td.la - 1)]), kb = KeyOrd<K>::to(b[min(bi, td.lb - 1)]);
 #pragma unroll
-        for (int k = 0; k < VT; ++k) {
-            if (HAS_V) merge_step_idx<K>(pa, pb, ka, kb, na, nb, pae, pbe, out[k], ia, ib, src[k]);
-            else merge_step<K>(pa, pb, ka, kb, na, nb, pae, pbe, out[k]);
-        }
-        if (HAS_V) {
+            for (int k = 0; k < VT; ++k) {
+                const bool t = bi >= td.lb || (ai < td.la && ka <= kb);
+                out[k] = t ? a[min(ai, td.la - 1)] : b[min(bi, td.lb - 1)];
+                if (HAS_V) v[k] = t ? sv[td.va_s + min(ai, td.la - 1)] : sv[td.vb_s + min(bi, td.lb - 1)];
+                if (t) {
+                    ++ai;
+                    ka = KeyOrd<K>::to(a[min(ai, td.la - 1)]);
+                } else {
+                    ++bi;
+                    kb = KeyOrd<K>::to(b[min(bi, td.lb - 1)]);
+                }
+            }
+        } else {
+            const uint32_t sa0 = smem_addr(sk + td.a_s);
+            const uint32_t sb0 = smem_addr(sk + td.b_s);
+            const int ai = split_smem<K, LOG2NV>(sa0, td.la, sb0, td.lb, d);
+            const int bi = d - ai;
+            uint32_t pa = sa0 + ai * KB, pb = sb0 + bi * KB;
+            const uint32_t pae = sa0 + td.la * KB, pbe = sb0 + td.lb * KB;
+            K ka = lds<K>(pa), kb = lds<K>(pb), na = lds<K>(pa + KB), nb = lds<K>(pb + KB);
+            int src[VT];
+            int ia = td.va_s + ai, ib = td.vb_s + bi;
 #pragma unroll
-            for (int k = 0; k < VT; ++k)
-                if (k < cnt) v[k] = sv[src[k]];
+            for (int k = 0; k < VT; ++k) {
+                if (HAS_V) merge_step_idx<K>(pa, pb, ka, kb, na, nb, pae, pbe, out[k], ia, ib, src[k]);
+                else merge_step<K>(pa, pb, ka, kb, na, nb, pae, pbe, out[k]);
+            }
+            if (HAS_V) {
+#pragma unroll
+                for (int k = 0; k < VT; ++k)
+                    if (k < cnt) v[k] = sv[src[k]];
+            }
         }
         write = true;
     } else {
@@ -621,7 +649,7 @@ __global__ void __launch_bounds__(256) k_diag_splits(const K* __restrict__ A, co
         int lo = max(0, D - m), hi = min(D, n);
         while (lo < hi) {
             const int mid = (lo + hi) >> 1;
-            if (__ldg(A + mid) <= __ldg(B + (D - 1 - mid))) lo = mid + 1;
+            if (key_le(__ldg(A + mid), __ldg(B + (D - 1 - mid)))) lo = mid + 1;
             else hi = mid;
         }
         split[k] = lo;
@@ -744,8 +772,8 @@ __global__ void k_plan_dump(Geom g, const int* __restrict__ xbar, const int* __r
 // sort open; a least-significant-digit radix sort is stable by construction
 // and costs a fixed number of passes whatever R, so the runs can be long
 // (fewer merge rounds, row a9).
-//   - keys are ranked through their unsigned view (sign bit flipped for
-//     signed keys, reading R16); 4-bit digits;
+//   - keys are ranked through their unsigned order view (KeyOrd: sign bit
+//     flipped for signed keys, IEEE totalOrder for floats); 4-bit digits;
 //   - digits on which every key of the run agrees are skipped (the pass
 //     would be the identity);
 //   - blocked arrangement: thread t owns run positions [t*IPT, t*IPT+IPT)
@@ -755,16 +783,9 @@ __global__ void k_plan_dump(Geom g, const int* __restrict__ xbar, const int* __r
 //     thread's base offset per digit -- equal digits keep sequence order;
 //   - a partial last run is padded with the maximum unsigned view AFTER the
 //     real elements: stability keeps the padding last, and it is never stored.
-template <typename K>
-struct RadixView;
-template <> struct RadixView<uint32_t> { using U = uint32_t; static constexpr U flip = 0u; };
-template <> struct RadixView<int32_t> { using U = uint32_t; static constexpr U flip = 0x80000000u; };
-template <> struct RadixView<uint64_t> { using U = uint64_t; static constexpr U flip = 0ull; };
-template <> struct RadixView<int64_t> { using U = uint64_t; static constexpr U flip = 0x8000000000000000ull; };
-
 template <typename K, bool HAS_V, int NT, int IPT>
 struct K3Layout {
-    using U = typename RadixView<K>::U;
+    using U = typename KeyOrd<K>::U;
     static constexpr int R = NT * IPT;
     static constexpr int NW = NT / 32;
     static constexpr int ND = 16;                        // 4-bit digits
@@ -789,7 +810,6 @@ __global__ void __launch_bounds__(NT) k_block_sort(const K* __restrict__ in, con
     using U = typename Lay::U;
     constexpr int R = Lay::R, NW = Lay::NW, ND = Lay::ND, ROW = Lay::ROW;
     constexpr int NDIG = (int)sizeof(U) * 2;             // 4-bit digits per key
-    constexpr U FLIP = RadixView<K>::flip;
     static_assert(IPT % 2 == 1 && IPT < 256 && NT % 32 == 0 && NT >= 32, "odd IPT; 8-bit counters");
     extern __shared__ __align__(128) char smem[];
     U* ku0 = (U*)smem;
@@ -807,7 +827,7 @@ __global__ void __launch_bounds__(NT) k_block_sort(const K* __restrict__ in, con
 #pragma unroll
         for (int k = 0; k < IPT; ++k) {
             const int e = k * NT + tid;
-            u[k] = e < len ? ((U)ld_stream(in + base + e) ^ FLIP) : ~(U)0;
+            u[k] = e < len ? KeyOrd<K>::to(ld_stream(in + base + e)) : ~(U)0;
             if (HAS_V) vl[k] = e < len ? ld_stream(vin + base + e) : 0u;
         }
 #pragma unroll
@@ -921,7 +941,7 @@ __global__ void __launch_bounds__(NT) k_block_sort(const K* __restrict__ in, con
     for (int k = 0; k < IPT; ++k) {
         const int e = k * NT + tid;
         if (e < len) {
-            st_stream(out + base + e, (K)(kf[e] ^ FLIP));
+            st_stream(out + base + e, KeyOrd<K>::from(kf[e]));
             if (HAS_V) st_stream(vout + base + e, vf[e]);
         }
     }

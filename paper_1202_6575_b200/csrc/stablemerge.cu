@@ -352,8 +352,9 @@ static void host_plan(const K* A, int64_t n, const K* B, int64_t m, int64_t p, s
         y[i] = hblock_start(m, p, i);
     }
     for (int64_t i = 0; i < p; ++i) {      // Step 1: xbar_i = rank_low(A[x_i], B); empty block start -> m (R4)
-        xb[i] = x[i] < n ? std::lower_bound(B, B + m, A[x[i]]) - B : m;
-        yb[i] = y[i] < m ? std::upper_bound(A, A + n, B[y[i]]) - A : n;   // Step 2: rank_high
+        auto lt = [](K u, K v) { return key_lt<K>(u, v); };
+        xb[i] = x[i] < n ? std::lower_bound(B, B + m, A[x[i]], lt) - B : m;
+        yb[i] = y[i] < m ? std::upper_bound(A, A + n, B[y[i]], lt) - A : n;   // Step 2: rank_high
     }
     xb[p] = m;
     yb[p] = n;
@@ -775,6 +776,8 @@ SM_DEFINE_ABI(u32, uint32_t)
 SM_DEFINE_ABI(i32, int32_t)
 SM_DEFINE_ABI(i64, int64_t)
 SM_DEFINE_ABI(u64, uint64_t)
+SM_DEFINE_ABI(f32, float)
+SM_DEFINE_ABI(f64, double)
 
 int64_t sm_tile_capacity(int32_t key_bytes, int32_t has_vals) {
     return sm::tile_nv(key_bytes, has_vals != 0);

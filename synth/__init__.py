@@ -80,21 +80,41 @@ def bounded(r: torch.Tensor, k: int) -> torch.Tensor:
     return _lsr(_lsr(r, 32) * k, 32)
 
 
-def sort_bits(x: torch.Tensor, unsigned: bool) -> torch.Tensor:
-    """Library sort of keys carried as int32/int64 bit patterns (ascending in
-    the signed or unsigned order)."""
-    if not unsigned:
-        return torch.sort(x, stable=True).values
-    flip = torch.tensor(torch.iinfo(x.dtype).min, dtype=x.dtype, device=x.device)
-    return torch.sort(x ^ flip, stable=True).values ^ flip
+def _order_key(x: torch.Tensor, order: str) -> torch.Tensor:
+    """An integer with the key order, for a library sort: identity for signed,
+    sign bit flipped for unsigned, and for IEEE 754 totalOrder the magnitude
+    bits of negative values inverted (an involution)."""
+    if order == "s":
+        return x
+    if order == "u":
+        return x ^ torch.iinfo(x.dtype).min
+    return torch.where(x < 0, x ^ torch.iinfo(x.dtype).max, x)
+
+
+def sort_bits(x: torch.Tensor, order: str) -> torch.Tensor:
+    """Library sort of keys carried as int32/int64 bit patterns, ascending in
+    the key type's order ("s" signed, "u" unsigned, "f" IEEE totalOrder)."""
+    return _order_key(torch.sort(_order_key(x, order), stable=True).values, order)
 
 
 KEY_TYPES = {
-    # name: (torch carrier dtype, unsigned, key bytes)
-    "u32": (torch.int32, True, 4),
-    "i32": (torch.int32, False, 4),
-    "i64": (torch.int64, False, 8),
-    "u64": (torch.int64, True, 8),
+    # name: (torch carrier dtype, order: s signed / u unsigned / f IEEE totalOrder, key bytes)
+    "u32": (torch.int32, "u", 4),
+    "i32": (torch.int32, "s", 4),
+    "i64": (torch.int64, "s", 8),
+    "u64": (torch.int64, "u", 8),
+    "f32": (torch.int32, "f", 4),
+    "f64": (torch.int64, "f", 8),
+}
+
+# float bit patterns of the "special" distribution: +-0, +-inf, +-NaN (quiet,
+# with payloads), the smallest subnormals, +-1, +-max
+_SPECIAL = {
+    "f32": [0x00000000, 0x80000000, 0x7F800000, 0xFF800000, 0x7FC00000, 0xFFC00000, 0x7FC00001, 0x00000001,
+            0x80000001, 0x3F800000, 0xBF800000, 0x7F7FFFFF, 0xFF7FFFFF],
+    "f64": [0x0, 0x8000000000000000, 0x7FF0000000000000, 0xFFF0000000000000, 0x7FF8000000000000,
+            0xFFF8000000000000, 0x7FF8000000000001, 0x1, 0x8000000000000001, 0x3FF0000000000000,
+            0xBFF0000000000000, 0x7FEFFFFFFFFFFFFF, 0xFFEFFFFFFFFFFFFF],
 }
 
 
@@ -140,8 +160,22 @@ def source_payloads(n: int, m: int, device="cpu"):
 
 
 def _keys(dist: str, key_type: str, seed: int, stream: int, count: int, device) -> torch.Tensor:
-    dtype, unsigned, _ = KEY_TYPES[key_type]
+    dtype, order, _ = KEY_TYPES[key_type]
     r = splitmix_stream(seed, stream, count, device)
+    if order == "f":
+        ftype = torch.float32 if dtype == torch.int32 else torch.float64
+        if dist.startswith("bounded:"):             # small integers, negatives too, many ties
+            k = int(dist.split(":", 1)[1])
+            return (bounded(r, k) - k // 2).to(ftype).view(dtype)
+        if dist == "full":                          # every bit pattern: NaNs, infinities, subnormals
+            return r.to(dtype)
+        if dist == "special":
+            table = torch.tensor([_s64(v) if dtype == torch.int64 else (v - (1 << 32) if v >= (1 << 31) else v)
+                                  for v in _SPECIAL[key_type]], dtype=dtype, device=device)
+            return table[bounded(r, table.numel())]
+        if dist == "equal":
+            return torch.zeros(count, dtype=dtype, device=device)
+        raise ValueError(dist)
     if dist.startswith("bounded:"):
         k = int(dist.split(":", 1)[1])
         v = bounded(r, k)
@@ -166,9 +200,9 @@ def _keys(dist: str, key_type: str, seed: int, stream: int, count: int, device) 
 def merge_input(n: int, m: int, key_type: str, dist: str, seed: int, payload: bool = True,
                 device="cpu") -> MergeInput:
     """Two independently sorted arrays A (n) and B (m) of `dist` keys."""
-    _, unsigned, _ = KEY_TYPES[key_type]
-    a = sort_bits(_keys(dist, key_type, seed, STREAM_A, n, device), unsigned)
-    b = sort_bits(_keys(dist, key_type, seed, STREAM_B, m, device), unsigned)
+    _, order, _ = KEY_TYPES[key_type]
+    a = sort_bits(_keys(dist, key_type, seed, STREAM_A, n, device), order)
+    b = sort_bits(_keys(dist, key_type, seed, STREAM_B, m, device), order)
     av = bv = None
     if payload:
         av, bv = source_payloads(n, m, device)
@@ -212,7 +246,7 @@ class BatchInput:
 def _segmented(S: int, mean: int, key_type: str, dist: str, seed: int, stream: int, device):
     """S segments of lengths uniform in [0, 2*mean), each sorted (library
     sort on (segment, key)); returns (keys, offsets)."""
-    _, unsigned, _ = KEY_TYPES[key_type]
+    _, order, _ = KEY_TYPES[key_type]
     lens = bounded(splitmix_stream(seed, 16 * STREAM_BERN + 8 + stream, S, device), 2 * mean)
     off = torch.zeros(S + 1, dtype=torch.int64, device=device)
     off[1:] = torch.cumsum(lens, 0)
@@ -220,10 +254,9 @@ def _segmented(S: int, mean: int, key_type: str, dist: str, seed: int, stream: i
     keys = _keys(dist, key_type, seed, stream, total, device)
     seg = torch.repeat_interleave(torch.arange(S, device=device), lens)
     # order by (segment, key): a stable sort by key, then a stable sort by segment
-    flip = torch.iinfo(keys.dtype).min if unsigned else 0
-    order = torch.sort(keys ^ flip if unsigned else keys, stable=True).indices
-    order = order[torch.sort(seg[order], stable=True).indices]
-    return keys[order], off
+    idx = torch.sort(_order_key(keys, order), stable=True).indices
+    idx = idx[torch.sort(seg[idx], stable=True).indices]
+    return keys[idx], off
 
 
 def batch_input(S: int, mean: int, key_type: str, dist: str, seed: int, payload: bool = True,

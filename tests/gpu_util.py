@@ -32,6 +32,9 @@ def oracle_merge(inp: synth.MergeInput):
 def assert_bit_exact(got_k, got_v, want_k, want_v, key_type):
     gk = oracle.as_np(got_k, key_type)
     assert gk.shape == want_k.shape
+    if gk.dtype.kind == "f":           # bit patterns: NaN payloads, signed zeros
+        ui = np.uint32 if gk.dtype.itemsize == 4 else np.uint64
+        gk, want_k = gk.view(ui), np.ascontiguousarray(want_k).view(ui)
     if not np.array_equal(gk, want_k):
         bad = np.flatnonzero(gk != want_k)
         raise AssertionError(f"{bad.size} key mismatches, first at {bad[:8].tolist()}: "

@@ -29,11 +29,11 @@ def sm():
 
 def test_header_declares_entry_points():
     names = declared_functions()
-    for kt in ("u32", "i32", "i64", "u64"):
+    for kt in ("u32", "i32", "i64", "u64", "f32", "f64"):
         for f in ("merge_stable", "mergesort_stable", "merge_stable_ex", "merge_plan_ex", "mergesort_stable_ex",
                   "merge_stable_batched"):
             assert f"{f}_{kt}" in names
-    assert len(names) == 31
+    assert len(names) == 43
 
 
 def test_library_exports_every_declared_symbol(sm):

@@ -11,20 +11,21 @@ from gpu_util import assert_bit_exact, lib
 
 pytestmark = pytest.mark.gpu
 
-NP = {"u32": np.uint32, "i32": np.int32, "i64": np.int64, "u64": np.uint64}
-CARRIER = {"u32": np.int32, "i32": np.int32, "i64": np.int64, "u64": np.int64}
+NP = {"u32": np.uint32, "i32": np.int32, "i64": np.int64, "u64": np.uint64, "f32": np.float32, "f64": np.float64}
+CARRIER = {"u32": np.int32, "i32": np.int32, "i64": np.int64, "u64": np.int64, "f32": np.int32, "f64": np.int64}
 
 
 def _segments(lengths, kt, dist, seed, stream):
     """Concatenated, per-segment sorted keys drawn from synth's generator."""
     total = int(sum(lengths))
-    raw = synth._keys(dist, kt, seed, stream, total, "cpu")
-    raw = oracle.as_np(raw, kt).copy()
+    bits = synth._keys(dist, kt, seed, stream, total, "cpu")
     off = np.zeros(len(lengths) + 1, dtype=np.int64)
     off[1:] = np.cumsum(lengths)
-    for s in range(len(lengths)):
-        raw[off[s]:off[s + 1]].sort(kind="stable")
-    return raw, off
+    order = synth.KEY_TYPES[kt][1]
+    seg = torch.repeat_interleave(torch.arange(len(lengths)), torch.as_tensor(np.asarray(lengths, dtype=np.int64)))
+    idx = torch.sort(synth._order_key(bits, order), stable=True).indices       # library sort by key,
+    idx = idx[torch.sort(seg[idx], stable=True).indices]                        # then by segment
+    return oracle.as_np(bits[idx], kt).copy(), off
 
 
 def _case(S, la, lb, kt, dist, payload, seed):
@@ -53,7 +54,7 @@ def _run(sm, case, kt):
     assert_bit_exact(ck.cpu(), None if cv is None else cv.cpu(), want_k, want_v, kt)
 
 
-@pytest.mark.parametrize("kt", ["u32", "i32", "i64", "u64"])
+@pytest.mark.parametrize("kt", ["u32", "i32", "i64", "u64", "f32", "f64"])
 @pytest.mark.parametrize("payload", [True, False])
 def test_batched_random_lengths(kt, payload):
     sm = lib()

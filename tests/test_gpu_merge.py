@@ -89,7 +89,7 @@ def test_config_merge_reduced(cfg, scale):
     assert_bit_exact(*got, *want, inp.key_type)
 
 
-@pytest.mark.parametrize("kt", ["u32", "i32", "i64", "u64"])
+@pytest.mark.parametrize("kt", ["u32", "i32", "i64", "u64", "f32", "f64"])
 @pytest.mark.parametrize("nm", [(1, 0), (0, 1), (1, 1), (5, 3), (959, 961), (1920, 1), (1921, 3839),
                                 (70001, 12345), (12345, 70001), (100000, 17), (3, 200003)])
 @pytest.mark.parametrize("payload", [True, False])
@@ -235,6 +235,23 @@ def test_merge_path_comparison_ragged(nm):
     for kt in ("i32", "u64"):
         inp = synth.merge_input(*nm, kt, "bounded:3", seed=sum(nm), payload=kt == "u64")
         assert_bit_exact(*gpu_merge(sm, inp, merge_path=True), *oracle_merge(inp), kt)
+
+
+@pytest.mark.parametrize("kt", ["f32", "f64"])
+@pytest.mark.parametrize("dist", ["special", "full", "bounded:9"])
+def test_merge_float_total_order(kt, dist):
+    """Floating-point keys: IEEE totalOrder, NaNs, signed
+    zeros, infinities and subnormals -- bit-exact against the oracle, on the
+    device path, the merge-path comparison and the pipelined host path."""
+    sm = lib()
+    inp = synth.merge_input(70001, 50003, kt, dist, seed=23, payload=True)
+    want = oracle_merge(inp)
+    assert_bit_exact(*gpu_merge(sm, inp), *want, kt)
+    assert_bit_exact(*gpu_merge(sm, inp, merge_path=True), *want, kt)
+    big = synth.merge_input((40 << 20) // 12, (30 << 20) // 12, kt, dist, seed=24, payload=True)
+    got = sm.merge_stable(big.a_keys.pin_memory(), big.a_vals.pin_memory(), big.b_keys.pin_memory(),
+                          big.b_vals.pin_memory(), key_type=kt)
+    assert_bit_exact(*got, *oracle_merge(big), kt)
 
 
 def test_merge_errors():

@@ -18,7 +18,7 @@ def gpu_sort(sm, inp: synth.SortInput):
     return k.cpu(), (None if v is None else v.cpu())
 
 
-@pytest.mark.parametrize("kt", ["u32", "i32", "i64", "u64"])
+@pytest.mark.parametrize("kt", ["u32", "i32", "i64", "u64", "f32", "f64"])
 @pytest.mark.parametrize("N", [0, 1, 2, 3, 100, 1919, 1920, 1921, 3840, 5000, 65536, 100003, 1000001])
 def test_sort_ragged(kt, N):
     sm = lib()
@@ -28,7 +28,7 @@ def test_sort_ragged(kt, N):
         assert_bit_exact(*gpu_sort(sm, inp), *want, kt)
 
 
-@pytest.mark.parametrize("kt", ["u32", "i32", "i64", "u64"])
+@pytest.mark.parametrize("kt", ["u32", "i32", "i64", "u64", "f32", "f64"])
 def test_sort_run_boundaries(kt):
     """Sizes around the block-sort run length R and its powers of two
     (the number of merge rounds changes there), full-range and narrow keys
@@ -36,7 +36,7 @@ def test_sort_run_boundaries(kt):
     sm = lib()
     R = sm.sort_run(kt, True)
     for N in (R - 1, R, R + 1, 2 * R - 1, 2 * R + 3, 4 * R, 5 * R + 7):
-        for dist in ("full", "bounded:3", "equal"):
+        for dist in ("full", "bounded:3", "equal") + (("special",) if kt.startswith("f") else ()):
             inp = synth.sort_input(N, kt, dist, seed=N, payload=True)
             want = oracle.sort(inp.keys, inp.vals, kt)
             assert_bit_exact(*gpu_sort(sm, inp), *want, kt)

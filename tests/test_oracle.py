@@ -354,3 +354,69 @@ def test_special_cases(orc):
     *_, tasks = P.build_plan([5] * 4, [5] * 3, 2)
     assert all(t.case in "ae" for t in tasks if t.side == "A")
     assert all(t.case == "a" for t in tasks if t.side == "B")
+
+
+# ------------------------------------------------- floating-point keys (f2)
+# IEEE 754 totalOrder written from its definition (sign, then magnitude as
+# exponent-and-significand fields, reversed for negatives) -- a formulation
+# independent of oracle.c's integer-key trick.
+
+import functools  # noqa: E402
+
+
+def _fields(bits, width):
+    sign = bits >> (width - 1)
+    mag = bits & ((1 << (width - 1)) - 1)        # exponent and significand, as one field
+    return sign, mag
+
+
+def _total_order_cmp(width):
+    def cmp(x, y):
+        sx, mx = _fields(x, width)
+        sy, my = _fields(y, width)
+        if sx != sy:
+            return -1 if sx else 1                 # every negative (incl. -0, -NaN) before every positive
+        if sx == 0:
+            return (mx > my) - (mx < my)
+        return (my > mx) - (my < mx)               # both negative: larger magnitude first
+    return cmp
+
+
+@pytest.mark.parametrize("kt,width,np_u,np_f", [("f32", 32, np.uint32, np.float32), ("f64", 64, np.uint64, np.float64)])
+def test_float_merge_and_sort_vs_total_order_definition(orc, kt, width, np_u, np_f):
+    import synth
+    cmp = _total_order_cmp(width)
+    for dist in ("special", "full", "bounded:5"):
+        inp = synth.merge_input(300, 211, kt, dist, seed=31)
+        a = orc.as_np(inp.a_keys, kt)
+        b = orc.as_np(inp.b_keys, kt)
+        ab, bb = a.view(np_u).tolist(), b.view(np_u).tolist()
+        # inputs sorted under the definition
+        assert all(cmp(ab[i], ab[i + 1]) <= 0 for i in range(len(ab) - 1))
+        tagged = [(k, 0, i) for i, k in enumerate(ab)] + [(k, 1, j) for j, k in enumerate(bb)]
+        want = sorted(tagged, key=functools.cmp_to_key(lambda u, v: cmp(u[0], v[0])))   # stable: A first
+        va = np.arange(a.size, dtype=np.uint32)
+        vb = np.arange(b.size, dtype=np.uint32) | np.uint32(1 << 31)
+        ck, cv = orc.merge(a, va, b, vb, kt)
+        assert ck.view(np_u).tolist() == [t[0] for t in want]
+        assert cv.tolist() == [t[2] | (t[1] << 31) for t in want]
+        # sort: stable sort of the concatenation under the definition
+        keys = np.concatenate([b, a])
+        sk, sv = orc.sort(keys, np.arange(keys.size, dtype=np.uint32), kt)
+        kb = keys.view(np_u).tolist()
+        order = sorted(range(len(kb)), key=functools.cmp_to_key(lambda i, j: cmp(kb[i], kb[j])))
+        assert sv.tolist() == order
+        assert sk.view(np_u).tolist() == [kb[i] for i in order]
+
+
+def test_float_total_order_special_values(orc):
+    """-NaN < -inf < -1 < -0 < +0 < subnormal < 1 < inf < +NaN, and -0/+0 are
+    different keys (totalOrder), so A's +0 follows B's -0."""
+    f = np.float32
+    neg_nan = np.array([0xFFC00000], dtype=np.uint32).view(f)[0]
+    a = np.array([-np.inf, -1.0, 0.0, 1.0, np.inf], dtype=f)
+    b = np.array([neg_nan, -0.0, np.float32(1e-45), np.nan], dtype=f)
+    ck, _ = orc.merge(a, None, b, None, "f32")
+    bits = ck.view(np.uint32).tolist()
+    assert bits == [0xFFC00000, 0xFF800000, 0xBF800000, 0x80000000, 0x00000000, 0x00000001, 0x3F800000,
+                    0x7F800000, 0x7FC00000]
