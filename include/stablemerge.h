@@ -156,6 +156,28 @@ sm_status merge_stable_batched_f64(const double *keys_A, const uint32_t *vals_A,
                                    uint32_t *out_vals, void *stream);
 
 /* ---------------------------------------------------------------------
+ * ranks_stable_<K>  -- rank queries, the primitive of rows a1/a2 on its own
+ * (PAPER.md L119-128): out[i] = rank_low(keys[i], X) = #{X[t] < keys[i]}
+ * when high = 0, rank_high(keys[i], X) = #{X[t] <= keys[i]} when high != 0,
+ * for X[len] non-decreasing in the key order.  One binary search per key.
+ * DEVICE pointers only; out is int64[nkeys].  Used by the sharded
+ * multi-GPU merge (paper_1202_6575_b200.distributed): the
+ * global cross rank of a block start is the sum of its ranks in the shards.
+ * ------------------------------------------------------------------- */
+sm_status ranks_stable_u32(const uint32_t *X, int64_t len, const uint32_t *keys, int64_t nkeys, int32_t high,
+                             int64_t *out, void *stream);
+sm_status ranks_stable_i32(const int32_t *X, int64_t len, const int32_t *keys, int64_t nkeys, int32_t high,
+                             int64_t *out, void *stream);
+sm_status ranks_stable_i64(const int64_t *X, int64_t len, const int64_t *keys, int64_t nkeys, int32_t high,
+                             int64_t *out, void *stream);
+sm_status ranks_stable_u64(const uint64_t *X, int64_t len, const uint64_t *keys, int64_t nkeys, int32_t high,
+                             int64_t *out, void *stream);
+sm_status ranks_stable_f32(const float *X, int64_t len, const float *keys, int64_t nkeys, int32_t high,
+                             int64_t *out, void *stream);
+sm_status ranks_stable_f64(const double *X, int64_t len, const double *keys, int64_t nkeys, int32_t high,
+                             int64_t *out, void *stream);
+
+/* ---------------------------------------------------------------------
  * mergesort_stable_<K>  -- SURVEY.md §8 rows a8-a9 (§3).
  *
  *   keys[N], vals[N] (vals may be NULL: keys only), sorted IN PLACE from the

@@ -60,6 +60,7 @@ for _kt in KEY_TYPES:
                          (f"merge_stable_ex_{_kt}", [_P, _P, _I, _P, _P, _I, _P, _P, _P, ctypes.POINTER(SmOptions)]),
                          (f"merge_plan_ex_{_kt}", [_P, _I, _P, _I, _I, _I, _P, _P, _P, _P]),
                          (f"merge_stable_batched_{_kt}", [_P, _P, _I, _P, _P, _P, _I, _P, _I, _P, _P, _P]),
+                         (f"ranks_stable_{_kt}", [_P, _I, _P, _I, ctypes.c_int32, _P, _P]),
                          (f"mergesort_stable_{_kt}", [_P, _P, _I, _P]),
                          (f"mergesort_stable_ex_{_kt}", [_P, _P, _I, _P, ctypes.POINTER(SmOptions)])):
         _f = getattr(_lib, _name)
@@ -228,6 +229,19 @@ def merge_stable_batched(a_keys: torch.Tensor, a_vals: Optional[torch.Tensor], a
     return out_keys, out_vals
 
 
+def ranks_stable(X: torch.Tensor, keys: torch.Tensor, high: bool = False, *, key_type: Optional[str] = None,
+                 stream=None) -> torch.Tensor:
+    """rank_low (high=False) or rank_high (high=True) of every key in sorted
+    X.  CUDA tensors; returns int64 ranks."""
+    kt = _key_type(X, key_type)
+    _key_type(keys, kt)
+    out = torch.empty(keys.numel(), dtype=torch.int64, device=keys.device)
+    s = _stream_for(X, stream)
+    _check(getattr(_lib, f"ranks_stable_{kt}")(_ptr(X), X.numel(), _ptr(keys), keys.numel(), int(bool(high)),
+                                                _ptr(out), s), f"ranks_stable_{kt}")
+    return out
+
+
 def mergesort_stable(keys: torch.Tensor, vals: Optional[torch.Tensor] = None, *, key_type: Optional[str] = None,
                      stream=None, pdl: bool = True):
     """Stable merge sort in place (equal keys keep input order).  Returns (keys, vals)."""
@@ -267,6 +281,6 @@ def merge_plan(a_keys: torch.Tensor, b_keys: torch.Tensor, p_A: int, p_B: Option
     return xbar, ybar, tasks
 
 
-__all__ = ["merge_stable", "merge_stable_batched", "mergesort_stable", "merge_plan", "tile_capacity", "sort_run", "last_launch_count",
+__all__ = ["merge_stable", "merge_stable_batched", "mergesort_stable", "ranks_stable", "merge_plan", "tile_capacity", "sort_run", "last_launch_count",
            "StableMergeError", "KEY_TYPES", "LIB_PATH", "profile_enable", "profile_read", "PROF_K1", "PROF_K2",
            "PROF_K3"]

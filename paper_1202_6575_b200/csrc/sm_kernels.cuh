@@ -632,6 +632,27 @@ __global__ void __launch_bounds__(K2Layout<K, HAS_V, NC, VT, STAGES, MAXT, WB>::
     if (WB) bulk_wait_read<0>();
 }
 
+// ------------------------------------------------------- rank queries
+// rank_low (high = 0) or rank_high (high = 1) of a batch of keys in one
+// sorted array: the primitive of rows a1/a2 on its own,
+// used by the sharded multi-GPU merge (each rank ranks every block-start key
+// in its local shard; the sums over ranks are the global cross ranks).
+template <typename K>
+__global__ void __launch_bounds__(256) k_rank_keys(const K* __restrict__ X, int64_t len, const K* __restrict__ keys,
+                                                   int64_t nkeys, int high, int64_t* __restrict__ out) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nkeys) return;
+    const K x = keys[i];
+    int64_t lo = 0, hi = len;
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        const K v = __ldg(X + mid);
+        if (high ? key_le(v, x) : key_lt(v, x)) lo = mid + 1;
+        else hi = mid;
+    }
+    out[i] = lo;
+}
+
 // ------------------------------------------------ merge-path comparison
 // SURVEY.md §8(f) row 4, an A/B comparison only (the equal-output
 // partitioning of [AklSantoro87], the class the paper contrasts itself with,

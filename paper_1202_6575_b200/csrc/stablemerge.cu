@@ -612,6 +612,21 @@ static sm_status batch_entry(const K* A, const uint32_t* vA, int64_t n, const in
     return s;
 }
 
+// ------------------------------------------------------------ rank queries
+template <typename K>
+static sm_status ranks_entry(const K* X, int64_t len, const K* keys, int64_t nkeys, int32_t high, int64_t* out,
+                             void* stream) {
+    g_launches = 0;
+    g_err[0] = 0;
+    cudaStream_t st = (cudaStream_t)stream;
+    if (len < 0 || nkeys < 0) return fail_inval("negative size");
+    if ((len && !X) || (nkeys && (!keys || !out))) return fail_inval("NULL pointer with nonzero size");
+    if (nkeys == 0) return SM_OK;
+    if (is_host_ptr(X) || is_host_ptr(keys) || is_host_ptr(out)) return fail_inval("device pointers only");
+    k_rank_keys<K><<<(unsigned)ceil_div(nkeys, 256), 256, 0, st>>>(X, len, keys, nkeys, high ? 1 : 0, out);
+    return check_launch("k_rank_keys");
+}
+
 // ------------------------------------------------------------ plan dump
 __global__ void k_widen(const int* __restrict__ in, int64_t* __restrict__ out, int count) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -763,6 +778,10 @@ extern "C" {
                                          uint32_t* out_vals, void* stream) {                                   \
         return sm::batch_entry<K>(keys_A, vals_A, n, a_offsets, keys_B, vals_B, m, b_offsets, S, out_keys,    \
                                   out_vals, stream);                                                           \
+    }                                                                                                           \
+    sm_status ranks_stable_##SUF(const K* X, int64_t len, const K* keys, int64_t nkeys, int32_t high,        \
+                                 int64_t* out, void* stream) {                                                 \
+        return sm::ranks_entry<K>(X, len, keys, nkeys, high, out, stream);                                      \
     }                                                                                                           \
     sm_status mergesort_stable_##SUF(K* keys, uint32_t* vals, int64_t N, void* stream) {                       \
         return sm::sort_entry<K>(keys, vals, N, stream, nullptr);                                               \

@@ -31,9 +31,9 @@ def test_header_declares_entry_points():
     names = declared_functions()
     for kt in ("u32", "i32", "i64", "u64", "f32", "f64"):
         for f in ("merge_stable", "mergesort_stable", "merge_stable_ex", "merge_plan_ex", "mergesort_stable_ex",
-                  "merge_stable_batched"):
+                  "merge_stable_batched", "ranks_stable"):
             assert f"{f}_{kt}" in names
-    assert len(names) == 43
+    assert len(names) == 49
 
 
 def test_library_exports_every_declared_symbol(sm):

@@ -1,0 +1,59 @@
+"""The sharded merge on the GPU with the library's kernels (world size 1 over
+NCCL: the collectives and the CUDA rank/merge primitives; the multi-rank
+exchange is covered on CPU by tests/test_distributed.py -- one GPU here)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+
+import oracle
+import synth
+from gpu_util import assert_bit_exact, lib
+
+pytestmark = pytest.mark.gpu
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+@pytest.fixture(scope="module")
+def nccl1():
+    lib()
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(_port()), RANK="0", WORLD_SIZE="1")
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    yield
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("kt,dist_name", [("i32", "full"), ("u64", "mostly:0x8000000000000000:9/10"),
+                                          ("f32", "special")])
+def test_sharded_merge_world1_cuda(nccl1, kt, dist_name):
+    from paper_1202_6575_b200 import distributed as D
+    inp = synth.merge_input(300001, 200003, kt, dist_name, seed=5, payload=True)
+    d = inp.to("cuda")
+    pieces = D.merge_stable_sharded(d.a_keys, d.a_vals, d.b_keys, d.b_vals, inp.n, inp.m, key_type=kt)
+    pieces.sort(key=lambda p: p.offset)
+    keys = torch.cat([p.keys for p in pieces]).cpu()
+    vals = torch.cat([p.vals for p in pieces]).cpu()
+    assert_bit_exact(keys, vals, *oracle.merge(inp.a_keys, inp.a_vals, inp.b_keys, inp.b_vals, kt), kt)
+
+
+def test_ranks_stable_matches_oracle():
+    sm = lib()
+    for kt, dist_name in (("i32", "bounded:50"), ("u64", "full"), ("f64", "special")):
+        inp = synth.merge_input(100003, 5000, kt, dist_name, seed=8, payload=False)
+        X, keys = inp.a_keys.cuda(), inp.b_keys.cuda()
+        lo = sm.ranks_stable(X, keys, False, key_type=kt).cpu().numpy()
+        hi = sm.ranks_stable(X, keys, True, key_type=kt).cpu().numpy()
+        xs, ks = oracle.as_np(inp.a_keys, kt), oracle.as_np(inp.b_keys, kt)
+        sample = range(0, ks.size, 97)
+        assert [lo[i] for i in sample] == [oracle.rank_low(ks[i], xs, kt) for i in sample]
+        assert [hi[i] for i in sample] == [oracle.rank_high(ks[i], xs, kt) for i in sample]
