@@ -78,7 +78,7 @@ def main(tag):
     os.makedirs(OUT, exist_ok=True)
     traffic = {}
     rows = []
-    for cfg in (2, 1, 3, 4, 5):
+    for cfg in (2, 1, 3, 4, 5, 6):
         blog = os.path.join(EV, "bench_default.log" if cfg == 2 else f"bench_c{cfg}.log")
         line = None
         if os.path.exists(blog):
@@ -104,12 +104,66 @@ def main(tag):
         if line:
             rf = line.get("roofline", {})
             rows.append((cfg, line, rf, tr))
+    # extra captures: K1 on C2, K3 on C5; the merge-path comparison line
+    for name, rep in (("k_cross_ranks_c2", f"{tag}_c2_k_cross_ranks"), ("k_block_sort_c5", f"{tag}_c5_k_block_sort")):
+        path = os.path.join(EV, rep + ".ncu-rep")
+        if os.path.exists(path):
+            text, tr, dur = summarize_ncu(path, 2 if "c2" in name else 5, tag)
+            text = text.replace("K2 (k_tasks)", name.split("_c")[0])
+            open(os.path.join(OUT, f"{tag}_ncu_{name}.md"), "w").write(text)
+    mp = os.path.join(EV, "bench_c2_mergepath.log")
+    if os.path.exists(mp):
+        for ln in open(mp):
+            if ln.startswith("{"):
+                json.dump(json.loads(ln), open(os.path.join(OUT, f"{tag}_bench_c2_mergepath.json"), "w"))
     json.dump(traffic, open(os.path.join(OUT, "traffic.json"), "w"), indent=1)
     print(json.dumps(traffic, indent=1))
+    write_readme(tag, rows, traffic)
     for cfg, line, rf, tr in rows:
         print(cfg, f"{line['value']:.4g} elem/s", f"{line['ms_per_step']:.4f} ms", f"{line.get('achieved_hbm_gbs', 0):.0f} GB/s",
               f"K2 {rf.get('achieved', 0):.0f} GB/s frac {rf.get('frac', 0):.3f}", "traffic", tr,
               "alg", rf.get("algorithmic_bytes_per_launch"))
+
+
+NAMES = {1: "C1 merge 2^20+2^20 u32+u32", 2: "C2 merge 2^26+2^26 i32 keys-only (default)",
+         3: "C3 merge 2^28+2^16 i64+u32", 4: "C4 merge 2^27+2^25 u64+u32", 5: "C5 sort 2^28 u32+u32",
+         6: "B1 batched 2^16 pairs u32+u32 (NEXT row)"}
+
+
+def write_readme(tag, rows, traffic):
+    out = [f"# Profiles and measurements -- {tag}", "",
+           "One B200 (gpurun, `scripts/gpu_evidence.sh`, then `scripts/make_profiles.py`).  Peak = "
+           "MEASURED_PEAKS.json `hbm_gbs` (measured copy, read+write); every `frac` is of that measured peak.  "
+           "Clocks: NVML samples inside each timed region (in each bench line); no throttle reason other than "
+           "`sw_power_cap` is accepted.", "",
+           "| Config | ms/step | elements/s | step GB/s (frac) | K2 GB/s (frac) | K2 share | K2 DRAM traffic / algorithmic "
+           "| e2e elements/s (host buffers) | CPU oracle elements/s (1 core) | clocks |",
+           "|---|---|---|---|---|---|---|---|---|---|"]
+    for cfg, line, rf, tr in rows:
+        clk = line.get("clocks", {})
+        out.append(f"| {NAMES.get(cfg, cfg)} | {line['ms_per_step']:.4f} | {line['value']:.3e} | "
+                   f"{line['achieved_hbm_gbs']:.0f} ({line['achieved_hbm_frac']:.3f}) | {rf.get('achieved', 0):.0f} "
+                   f"({rf.get('frac', 0):.3f}) | {rf.get('share_of_step', 0):.3f} | "
+                   f"{(tr / rf['algorithmic_bytes_per_launch']) if tr else float('nan'):.3f} | "
+                   f"{line.get('e2e', {}).get('value', float('nan')):.3e} | "
+                   f"{line.get('cpu_baseline', {}).get('value', float('nan')):.3e} | "
+                   f"{clk.get('sm_mhz')} MHz {clk.get('reasons')} |")
+    mp = os.path.join(OUT, f"{tag}_bench_c2_mergepath.json")
+    if os.path.exists(mp):
+        d = json.load(open(mp))
+        out += ["", f"Merge-path comparison (not the method; `bench.py --merge-path`, C2): {d['ms_per_step']:.4f} "
+                    f"ms/step, {d['value']:.3e} elements/s, {d['achieved_hbm_gbs']:.0f} GB/s "
+                    f"({d['achieved_hbm_frac']:.3f}) -- see DESIGN.md for what it measures."]
+    out += ["", "Files:",
+            f"- `{tag}_bench_cN.json` -- the bench.py JSON line of config N (default N=2).",
+            f"- `{tag}_launches_cN.md` -- ncu launch list of `bench.py --config N --steps 3 --warmup 3 --no-extras` "
+            "(`--metrics gpu__time_duration.sum --clock-control none`): per-kernel share of the library's time.",
+            f"- `{tag}_ncu_k_tasks_cN.md` -- one `ncu --set full` capture of K2 per config (DRAM bytes, throughput, "
+            "shared-memory pipe, bank conflicts, occupancy, issue, warp stalls); "
+            f"`{tag}_ncu_k_cross_ranks_c2.md` (K1) and `{tag}_ncu_k_block_sort_c5.md` (K3).",
+            "- `traffic.json` -- DRAM read+write bytes per K2 launch from those captures (bench.py `roofline.traffic`).",
+            f"- `{tag}_pytest_gpu.log` -- the full `pytest -m gpu` run on the B200."]
+    open(os.path.join(OUT, "README.md"), "w").write("\n".join(out) + "\n")
 
 
 if __name__ == "__main__":
