@@ -19,6 +19,9 @@
 namespace sm {
 
 // ----------------------------------------------------------------- K1
+#ifndef K1_WAYS
+#define K1_WAYS 4
+#endif
 // Rows a1/a2.  A group of G lanes performs one rank search cooperatively:
 // each round the probing lanes read evenly spaced keys of the remaining
 // interval and a group ballot picks the sub-interval holding the rank.
@@ -69,6 +72,35 @@ __device__ __forceinline__ int group_rank(const K* __restrict__ X, int len, K x,
     return lo;
 }
 
+// One-thread rank search with WAYS-1 independent probes per round (the
+// quantile points of the remaining interval): log_WAYS(len) dependent
+// memory rounds instead of log_2(len), (WAYS-1)/log2(WAYS) loads per level.
+//   high = false: rank_low(x, X) = #{X[t] < x};  high = true: rank_high = #{X[t] <= x}
+template <typename K, int WAYS>
+__device__ __forceinline__ int rank_kary(const K* __restrict__ X, int len, K x, bool high) {
+    int lo = 0, n = len;                     // rank in [lo, lo + n]; X[lo, lo+n) undecided
+    while (n >= WAYS) {
+        const int q = n / WAYS;
+        K v[WAYS - 1];
+#pragma unroll
+        for (int k = 0; k < WAYS - 1; ++k) v[k] = __ldg(X + lo + (k + 1) * q - 1);   // independent loads
+        int t = 0;                           // probes passed: a prefix
+#pragma unroll
+        for (int k = 0; k < WAYS - 1; ++k) t += (high ? key_le(v[k], x) : key_lt(v[k], x)) ? 1 : 0;
+        // probes at lo + (k+1)q - 1: passing t of them leaves [lo + t*q, lo + (t+1)q - 1)
+        // (the last sub-interval runs to the end of the interval)
+        lo += t * q;
+        n = (t == WAYS - 1) ? n - t * q : q - 1;
+    }
+    while (n > 0) {                          // binary tail
+        const int half = n >> 1;
+        const bool right = high ? key_le(__ldg(X + lo + half), x) : key_lt(__ldg(X + lo + half), x);
+        lo = right ? lo + half + 1 : lo;
+        n = right ? n - half - 1 : half;
+    }
+    return lo;
+}
+
 // K1 (rows a1/a2): one group of G lanes per cross rank, searching the whole
 // other array (G = 1: a plain binary search per thread, measured fastest on
 // B200 for every config: the top levels are shared by all searches and hit
@@ -92,7 +124,12 @@ __global__ void __launch_bounds__(256) k_cross_ranks(const K* __restrict__ A, co
     const bool search = valid && idx < plen && idx < own_len;   // x_idx < own_len  <=>  idx < own_len
     K x = K(0);
     if (search) x = __ldg((sideA ? A + sg.aoff : B + sg.boff) + Blocks(own_len, plen).start(idx));
-    const int r = group_rank<K, G, G>(sideA ? B + sg.boff : A + sg.aoff, oth_len, x, !sideA, search, 0);
+    int r;
+    if constexpr (G == 1) {
+        r = search ? rank_kary<K, K1_WAYS>(sideA ? B + sg.boff : A + sg.aoff, oth_len, x, !sideA) : 0;
+    } else {
+        r = group_rank<K, G, G>(sideA ? B + sg.boff : A + sg.aoff, oth_len, x, !sideA, search, 0);
+    }
     if (valid && (threadIdx.x % G) == 0) {
         const int v = search ? r : oth_len;
         if (sideA) sg.xs[idx] = v;
