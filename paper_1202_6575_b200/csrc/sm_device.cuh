@@ -310,6 +310,21 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         : "memory");
 }
 
+// The same for warps that are often idle (storer, producer): the suspend-time
+// hint lets the hardware park the warp until the phase completes instead of
+// re-polling every few hundred cycles (the polls took ~6% of issue slots).
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n"
+        "LAB_WAIT:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
+        "@P1 bra DONE;\n\t"
+        "bra LAB_WAIT;\n"
+        "DONE:\n\t}" ::"r"(smem_addr(bar)),
+        "r"(parity), "r"(1000000u)
+        : "memory");
+}
+
 // global -> shared bulk copy; completion counted on `bar` (bytes % 16 == 0,
 // both addresses 16-byte aligned)
 __device__ __forceinline__ void bulk_g2s(void* dst_smem, const void* src_gmem, uint32_t bytes, uint64_t* bar) {

@@ -279,8 +279,11 @@ __device__ __forceinline__ void k2_producer(const K* __restrict__ A, const uint3
             if (fill) {
                 Seg sg;
                 const Task t = decode_task(g, my, xbar, ybar, sg);
-                la = t.a1 - t.a0;
-                lb = t.b1 - t.b0;
+                // sorted inputs give 0 <= la + lb <= NV (the task bound of
+                // L388-393); unsorted ones (a precondition violation) may not:
+                // clamp so the kernel still terminates inside its buffers
+                la = max(0, min(t.a1 - t.a0, NV));
+                lb = max(0, min(t.b1 - t.b0, NV - la));
                 off = sg.coff + t.a0 + t.b0;
                 ag = sg.aoff + t.a0;
                 bg = sg.boff + t.b0;
@@ -289,7 +292,7 @@ __device__ __forceinline__ void k2_producer(const K* __restrict__ A, const uint3
             cnt += __popc(__ballot_sync(0xffffffffu, fill));
         }
         const int st = it % STAGES;
-        if (it >= STAGES) mbar_wait(&empty[st], ((it / STAGES) - 1) & 1);
+        if (it >= STAGES) mbar_wait_sleep(&empty[st], ((it / STAGES) - 1) & 1);
         int* ps = pst + st * (MAXT + 2);
         if (cnt == 0) {                             // no task left: terminate the consumers
             if (lane == 0) {
@@ -548,7 +551,7 @@ __global__ void __launch_bounds__(K2Layout<K, HAS_V, NC, VT, STAGES, MAXT, WB>::
         const int lane = threadIdx.x - 32;
         for (int it = 0;; ++it) {
             const int s = it % STAGES;
-            mbar_wait(&written[s], (it / STAGES) & 1);
+            mbar_wait_sleep(&written[s], (it / STAGES) & 1);
             const int nt = pst[s * (MAXT + 2) + MAXT + 1];
             if (nt < 0) break;
             const K* sk = (const K*)(smem + s * Lay::STAGE_BYTES);

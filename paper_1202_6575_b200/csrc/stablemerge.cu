@@ -384,6 +384,10 @@ static void host_plan(const K* A, int64_t n, const K* B, int64_t m, int64_t p, s
         }
         tasks.push_back(t);
     }
+    for (SubMerge& t : tasks) {            // unsorted inputs (a precondition violation): never negative
+        t.a1 = std::max(t.a0, std::min(t.a1, n));
+        t.b1 = std::max(t.b0, std::min(t.b1, m));
+    }
     std::sort(tasks.begin(), tasks.end(),
               [](const SubMerge& u, const SubMerge& v) { return u.a0 + u.b0 < v.a0 + v.b0; });
 }

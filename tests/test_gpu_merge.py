@@ -254,6 +254,43 @@ def test_merge_float_total_order(kt, dist):
     assert_bit_exact(*got, *oracle_merge(big), kt)
 
 
+@pytest.mark.parametrize("kt,payload", [("u32", True), ("i32", False), ("u64", True), ("f32", True)])
+@pytest.mark.parametrize("merge_path", [False, True])
+def test_unsorted_inputs_never_write_outside_output(kt, payload, merge_path):
+    """The header's promise for a violated precondition (unsorted A or B):
+    unspecified output, but no write outside C (guard zones on both sides;
+    compute-sanitizer is closed on this pool, so the guard is the check)."""
+    sm = lib()
+    n, m = 70001, 50003
+    ct = synth.KEY_TYPES[kt][0]
+    a = synth._keys("full" if kt != "f32" else "special", kt, 91, 1, n, "cpu").cuda()   # NOT sorted
+    b = synth._keys("full" if kt != "f32" else "special", kt, 91, 2, m, "cpu").cuda()
+    va = torch.arange(n, dtype=torch.int32, device="cuda") if payload else None
+    vb = torch.arange(m, dtype=torch.int32, device="cuda") if payload else None
+    G = 4096
+    kbuf = torch.full((n + m + 2 * G,), 77, dtype=ct, device="cuda")
+    vbuf = torch.full((n + m + 2 * G,), 77, dtype=torch.int32, device="cuda") if payload else None
+    sm.merge_stable(a, va, b, vb, kbuf[G:G + n + m], None if vbuf is None else vbuf[G:G + n + m], key_type=kt,
+                    merge_path=merge_path)
+    torch.cuda.synchronize()
+    assert bool((kbuf[:G] == 77).all()) and bool((kbuf[G + n + m:] == 77).all())
+    if payload:
+        assert bool((vbuf[:G] == 77).all()) and bool((vbuf[G + n + m:] == 77).all())
+
+
+def test_unsorted_host_inputs_pipelined_path_terminates_in_bounds():
+    """Unsorted host inputs above the pipelining threshold: the host plan's
+    tasks are clamped, the call terminates, nothing outside C is written."""
+    sm = lib()
+    n, m = (24 << 20) // 4, (20 << 20) // 4
+    a = synth._keys("full", "i32", 5, 1, n, "cpu").pin_memory()
+    b = synth._keys("full", "i32", 5, 2, m, "cpu").pin_memory()
+    G = 4096
+    buf = torch.full((n + m + 2 * G,), 77, dtype=torch.int32).pin_memory()
+    sm.merge_stable(a, None, b, None, buf[G:G + n + m], key_type="i32")
+    assert bool((buf[:G] == 77).all()) and bool((buf[G + n + m:] == 77).all())
+
+
 def test_merge_errors():
     sm = lib()
     a = torch.arange(100, dtype=torch.int32, device="cuda")
