@@ -23,47 +23,40 @@ namespace sm {
 #define K1_WAYS 4
 #endif
 // Rows a1/a2.  A group of G lanes performs one rank search cooperatively:
-// each round the probing lanes read evenly spaced keys of the remaining
-// interval and a group ballot picks the sub-interval holding the rank.
-// While the interval is longer than `wide_above` all G lanes probe (log_{G+1}
-// rounds): those top levels are shared by many searches and hit L2.  Below
-// it every search's probes are private DRAM accesses, so only GT lanes probe
-// (GT = 1: plain binary search), trading a few dependent rounds for several
-// times less DRAM traffic (one 32-byte sector per probe).
-//   HIGH = false: rank_low(x, X)  = #{X[t] <  x}   (L119-123)
-//   HIGH = true:  rank_high(x, X) = #{X[t] <= x}   (L124-128)
+// each round the G lanes probe G evenly spaced keys of the remaining
+// interval and a group ballot picks the sub-interval holding the rank:
+// ~log_{G+1}(len) dependent rounds.  Used (G = 32) when there are few
+// searches, so latency, not probe traffic, is what counts.
+//   high = false: rank_low(x, X)  = #{X[t] <  x}   (L119-123)
+//   high = true:  rank_high(x, X) = #{X[t] <= x}   (L124-128)
 template <int GG>
 __device__ __forceinline__ int probe_pos(int lo, int n, int s) {
     return lo + (int)(((long long)(s + 1) * n) / (GG + 1));
 }
 
-template <typename K, int G, int GT>
-__device__ __forceinline__ int group_rank(const K* __restrict__ X, int len, K x, bool high, bool active,
-                                          int wide_above) {
+template <typename K, int G>
+__device__ __forceinline__ int group_rank(const K* __restrict__ X, int len, K x, bool high, bool active) {
     const int lane = threadIdx.x & 31;
     const int sub = lane % G;
     const int shift = lane - sub;
     int lo = 0, hi = active ? len : 0;     // rank in [lo, hi]; X[lo, hi) undecided
     while (__any_sync(0xffffffffu, hi > lo)) {
         const int n = hi - lo;
-        const bool wide = n > wide_above;
-        const int gg = wide ? G : GT;       // probing lanes this round
-        int pos = lo + sub;                 // n <= gg: probe every remaining key
-        if (n > gg) pos = wide ? probe_pos<G>(lo, n, sub) : probe_pos<GT>(lo, n, sub);
+        const int pos = n > G ? probe_pos<G>(lo, n, sub) : lo + sub;   // n <= G: probe every key left
         bool pred = false;
-        if (hi > lo && sub < min(gg, n)) {
+        if (hi > lo && sub < min(G, n)) {
             const K v = __ldg(X + pos);
             pred = high ? key_le(v, x) : key_lt(v, x);
         }
         const unsigned bal = (__ballot_sync(0xffffffffu, pred) >> shift) & (G == 32 ? 0xffffffffu : ((1u << (G & 31)) - 1u));
         const int t = __popc(bal);          // probes passed: a prefix of the probing lanes
         if (hi > lo) {
-            if (n <= gg) {
+            if (n <= G) {
                 lo = lo + t;
                 hi = lo;
             } else {
-                const int plast = t > 0 ? (wide ? probe_pos<G>(lo, n, t - 1) : probe_pos<GT>(lo, n, t - 1)) : lo - 1;
-                const int pnext = t < gg ? (wide ? probe_pos<G>(lo, n, t) : probe_pos<GT>(lo, n, t)) : hi;
+                const int plast = t > 0 ? probe_pos<G>(lo, n, t - 1) : lo - 1;
+                const int pnext = t < G ? probe_pos<G>(lo, n, t) : hi;
                 lo = plast + 1;
                 hi = pnext;
             }
@@ -128,7 +121,7 @@ __global__ void __launch_bounds__(256) k_cross_ranks(const K* __restrict__ A, co
     if constexpr (G == 1) {
         r = search ? rank_kary<K, K1_WAYS>(sideA ? B + sg.boff : A + sg.aoff, oth_len, x, !sideA) : 0;
     } else {
-        r = group_rank<K, G, G>(sideA ? B + sg.boff : A + sg.aoff, oth_len, x, !sideA, search, 0);
+        r = group_rank<K, G>(sideA ? B + sg.boff : A + sg.aoff, oth_len, x, !sideA, search);
     }
     if (valid && (threadIdx.x % G) == 0) {
         const int v = search ? r : oth_len;
@@ -175,12 +168,12 @@ struct TaskDesc {
     int pst;           // first padded diagonal of the task in the stage
 };
 
-// WB = false: outputs are written back in place into the stage and a storer
-// warp bulk-stores them (the stage is held until its bulk reads complete).
-// WB = true: every consumer warp writes its outputs into a private buffer and
-// bulk-stores them itself; the stage is freed as soon as all consumer warps
-// have read it, and no CTA-wide barrier is needed.
-template <typename K, bool HAS_V, int NC, int VT, int STAGES, int MAXT, bool WB>
+// Outputs are written back in place into the stage (phase-aligned to the
+// destination) and a storer warp bulk-stores them; the stage is held until
+// its bulk reads complete.  (A variant with per-warp output buffers, freeing
+// the stage as soon as it was read, measured 2-4% slower on C2: fewer stages
+// fit in shared memory.)
+template <typename K, bool HAS_V, int NC, int VT, int STAGES, int MAXT>
 struct K2Layout {
     static constexpr int NV = NC * VT;                     // padded diagonals per stage
     static constexpr int KB = (int)sizeof(K);
@@ -192,17 +185,11 @@ struct K2Layout {
     static constexpr int KREG = NV * KB + MAXT * 80;
     static constexpr int VREG = HAS_V ? NV * 4 + MAXT * 80 : 0;
     static constexpr int STAGE_BYTES = KREG + VREG;
-    // per-warp output buffer (WB): 32 lanes x VT outputs + a 16-byte phase
-    // slack per segment (at most 32 segments)
-    static constexpr int WBK = WB ? 32 * VT + 32 * EPV : 0;
-    static constexpr int WBV = (WB && HAS_V) ? 32 * VT + 32 * 4 : 0;
-    static constexpr int WB_BYTES = ((WBK * KB + WBV * 4) + 15) & ~15;
-    static constexpr int OFF_WB = STAGES * STAGE_BYTES;
-    static constexpr int OFF_DESC = OFF_WB + (NC / 32) * WB_BYTES;
+    static constexpr int OFF_DESC = STAGES * STAGE_BYTES;
     static constexpr int OFF_PST = OFF_DESC + STAGES * MAXT * (int)sizeof(TaskDesc);
     static constexpr int OFF_BAR = ((OFF_PST + STAGES * (MAXT + 2) * 4) + 15) & ~15;
     static constexpr int SMEM = OFF_BAR + 3 * STAGES * 8;   // full, empty, written
-    static constexpr int THREADS = NC + (WB ? 32 : 64);    // producer (+ storer) + consumers
+    static constexpr int THREADS = NC + 64;                 // producer + storer + consumers
 };
 
 // Bytes of the 16-byte-aligned superset of p[0, len).
@@ -499,28 +486,24 @@ __device__ __forceinline__ bool k2_compute(const K* sk, const uint32_t* sv, cons
 
 // K2 (rows a4-a7): persistent, warp-specialised.
 //   warp 0 (producer): k2_producer above (full[s]).
-//   consumers (NC threads): k2_compute, then
-//     WB = false: write back in place (phase-aligned to the destination) and
-//       hand the stage to warp 1 (storer), which bulk-stores each task's
-//       16-byte-aligned middle, plain-stores the edge elements and frees the
-//       stage once the bulk reads complete (written[s] -> empty[s]);
-//     WB = true: free the stage at once (empty[s], one arrival per warp),
-//       write the outputs into the warp's private buffer, each segment of
-//       consecutive lanes of one task placed at the destination's 16-byte
-//       phase, and bulk-store the segments from there (segment leader lane).
-template <typename K, bool HAS_V, int NC, int VT, int STAGES, int MAXT, bool WB, int MINB>
-__global__ void __launch_bounds__(K2Layout<K, HAS_V, NC, VT, STAGES, MAXT, WB>::THREADS, MINB)
+//   warps 2.. (NC consumers): k2_compute, then write back in place,
+//     phase-aligned to the destination, and hand the stage to the storer
+//     (written[s]).
+//   warp 1 (storer): bulk-stores each task's 16-byte-aligned middle,
+//     plain-stores the edge elements, and frees the stage once the bulk reads
+//     complete (empty[s]), so the consumers never wait on the stores.
+template <typename K, bool HAS_V, int NC, int VT, int STAGES, int MAXT, int MINB>
+__global__ void __launch_bounds__(K2Layout<K, HAS_V, NC, VT, STAGES, MAXT>::THREADS, MINB)
     k_tasks(const K* __restrict__ A, const uint32_t* __restrict__ vA, const K* __restrict__ B,
             const uint32_t* __restrict__ vB, K* __restrict__ C, uint32_t* __restrict__ vC, Geom g,
             const int* __restrict__ xbar, const int* __restrict__ ybar) {
-    using Lay = K2Layout<K, HAS_V, NC, VT, STAGES, MAXT, WB>;
+    using Lay = K2Layout<K, HAS_V, NC, VT, STAGES, MAXT>;
     static_assert(NC % 32 == 0 && MAXT <= 32 && STAGES >= 2, "warp-granular roles; one producer lane per task");
     constexpr int NV = Lay::NV;
     constexpr int LOG2NV = 31 - __builtin_clz(NV);   // 2^(LOG2NV+1) - 1 >= NV probes cover any range
     constexpr int EPV = Lay::EPV;
     constexpr int EK = 2 * (EPV - 1);                // key edge elements per store
     constexpr int EV = HAS_V ? 6 : 0;                // payload edge elements per store
-    constexpr int FIRST = WB ? 32 : 64;              // first consumer thread
     extern __shared__ __align__(128) char smem[];
     TaskDesc* desc = (TaskDesc*)(smem + Lay::OFF_DESC);
     int* pst = (int*)(smem + Lay::OFF_PST);          // [STAGES][MAXT + 2]: pst[0..nt], nt at MAXT+1
@@ -531,7 +514,7 @@ __global__ void __launch_bounds__(K2Layout<K, HAS_V, NC, VT, STAGES, MAXT, WB>::
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], WB ? NC / 32 : 1);
+            mbar_init(&empty[s], 1);
             mbar_init(&written[s], NC / 32);
         }
         fence_barrier_init();
@@ -546,7 +529,7 @@ __global__ void __launch_bounds__(K2Layout<K, HAS_V, NC, VT, STAGES, MAXT, WB>::
         return;
     }
 
-    if (!WB && threadIdx.x < 64) {
+    if (threadIdx.x < 64) {
         // -------------------------------------------------------- storer
         const int lane = threadIdx.x - 32;
         for (int it = 0;; ++it) {
@@ -580,17 +563,15 @@ __global__ void __launch_bounds__(K2Layout<K, HAS_V, NC, VT, STAGES, MAXT, WB>::
     }
 
     // ---------------------------------------------------------- consumers
-    const int c = threadIdx.x - FIRST;
+    const int c = threadIdx.x - 64;
     const int lane = threadIdx.x & 31;
-    K* wk = (K*)(smem + Lay::OFF_WB + (c >> 5) * Lay::WB_BYTES);   // WB: this warp's buffer
-    uint32_t* wv = (uint32_t*)(wk + Lay::WBK);
     for (int it = 0;; ++it) {
         const int s = it % STAGES;
         mbar_wait(&full[s], (it / STAGES) & 1);
         const int* ps = pst + s * (MAXT + 2);
         const int nt = ps[MAXT + 1];
         if (nt < 0) {
-            if (!WB && lane == 0) mbar_arrive(&written[s]);   // pass the termination on to the storer
+            if (lane == 0) mbar_arrive(&written[s]);   // pass the termination on to the storer
             break;
         }
         K* sk = (K*)(smem + s * Lay::STAGE_BYTES);
@@ -600,76 +581,22 @@ __global__ void __launch_bounds__(K2Layout<K, HAS_V, NC, VT, STAGES, MAXT, WB>::
         bool write = false;
         K out[VT];
         uint32_t v[HAS_V ? VT : 1];
-        const bool mine = k2_compute<K, HAS_V, VT, MAXT, LOG2NV, !WB>(sk, sv, desc + s * MAXT, ps, nt, c * VT, td, d,
-                                                                       cnt, write, out, v);
-        if (!WB) {
-            named_sync(1, NC);                         // every input of the stage has been read
-            if (write) {
-#pragma unroll
-                for (int k = 0; k < VT; ++k) {
-                    if (k < cnt) {
-                        sk[td.ob + d + k] = out[k];
-                        if (HAS_V) sv[td.obv + d + k] = v[k];
-                    }
-                }
-            }
-            fence_proxy_async();                       // generic writes -> the storer's bulk reads
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&written[s]);
-            continue;
-        }
-        // WB: this warp is done with the stage
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[s]);
-        // segments: maximal runs of lanes of one task with outputs
-        const bool has = mine && cnt > 0;
-        const int task_id = has ? td.pst : -1;           // unique per task within the stage
-        const int prev_id = __shfl_up_sync(0xffffffffu, task_id, 1);
-        const bool lead = has && (lane == 0 || prev_id != task_id);
-        const unsigned leads = __ballot_sync(0xffffffffu, lead);
-        const unsigned le_mask = 0xffffffffu >> (31 - lane);
-        const int l0 = 31 - __clz(leads & le_mask);       // this lane's segment leader (valid if has)
-        const int seg = __popc(leads & le_mask) - 1;
-        const int d0 = __shfl_sync(0xffffffffu, d, has ? l0 : lane);
-        const int g0 = td.off + d0;                        // global index of the segment's first output
-        int pk = 0, pv = 0;                                // buffer index of this lane's first output
-        if (has) {
-            const int phk = phase_of(C + g0);
-            const int bk = l0 * VT + seg * EPV;
-            pk = lane * VT + seg * EPV + (((phk - bk) % EPV) + EPV) % EPV;
-            if (HAS_V) {
-                const int phv = phase_of(vC + g0);
-                const int bv = l0 * VT + seg * 4;
-                pv = lane * VT + seg * 4 + (((phv - bv) % 4) + 4) % 4;
-            }
-        }
-        bulk_wait_read<0>();                               // this lane's previous stores have read the buffer
-        __syncwarp();
-        if (has) {
+        k2_compute<K, HAS_V, VT, MAXT, LOG2NV, true>(sk, sv, desc + s * MAXT, ps, nt, c * VT, td, d, cnt, write, out,
+                                                    v);
+        named_sync(1, NC);                             // every input of the stage has been read
+        if (write) {
 #pragma unroll
             for (int k = 0; k < VT; ++k) {
                 if (k < cnt) {
-                    wk[pk + k] = out[k];
-                    if (HAS_V) wv[pv + k] = v[k];
+                    sk[td.ob + d + k] = out[k];
+                    if (HAS_V) sv[td.obv + d + k] = v[k];
                 }
             }
         }
-        fence_proxy_async();
+        fence_proxy_async();                           // generic writes -> the storer's bulk reads
         __syncwarp();
-        if (lead) {
-            const int n = min(td.la + td.lb - d0, (32 - l0) * VT);   // the segment's outputs
-            store_middle<K>(C + g0, wk, pk, n);
-            if (HAS_V) store_middle<uint32_t>(vC + g0, wv, pv, n);
-            bulk_commit();
-#pragma unroll
-            for (int r = 0; r < EK; ++r) store_edge<K>(C + g0, wk, pk, n, r);
-            if (HAS_V) {
-#pragma unroll
-                for (int r = 0; r < EV; ++r) store_edge<uint32_t>(vC + g0, wv, pv, n, r);
-            }
-        }
+        if (lane == 0) mbar_arrive(&written[s]);
     }
-    if (WB) bulk_wait_read<0>();
 }
 
 // ------------------------------------------------------- rank queries

@@ -36,7 +36,6 @@ thread_local int64_t g_launches = 0;
 template <int NC_, int VT_, int STAGES_, int MINB_ = 1>
 struct K2Geo {
     static constexpr int NC = NC_, VT = VT_, STAGES = STAGES_, MINB = MINB_;
-    static constexpr bool WB = false;                 // per-warp output buffers (see k_tasks): measured slower
     static constexpr int NV = NC * VT;
     static constexpr int T = NV / 2;
 };
@@ -172,8 +171,8 @@ template <typename K, bool HAS_V, typename Sh>
 static sm_status launch_tasks(const K* A, const uint32_t* vA, const K* B, const uint32_t* vB, K* C, uint32_t* vC,
                               const Geom& g, const GeomCounts& gc, const int* xbar, const int* ybar, cudaStream_t st,
                               bool pdl) {
-    using Lay = K2Layout<K, HAS_V, Sh::NC, Sh::VT, Sh::STAGES, K2_MAXT, Sh::WB>;
-    auto kern = k_tasks<K, HAS_V, Sh::NC, Sh::VT, Sh::STAGES, K2_MAXT, Sh::WB, Sh::MINB>;
+    using Lay = K2Layout<K, HAS_V, Sh::NC, Sh::VT, Sh::STAGES, K2_MAXT>;
+    auto kern = k_tasks<K, HAS_V, Sh::NC, Sh::VT, Sh::STAGES, K2_MAXT, Sh::MINB>;
     static int per_sm = -1, n_sm = 0;
     if (per_sm < 0) {
         int dev = 0;
