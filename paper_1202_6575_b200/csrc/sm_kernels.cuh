@@ -245,6 +245,12 @@ __device__ __forceinline__ void store_edge(T* dst, const T* sbuf, int o, int L, 
 // goes into the next ring stage; every packed task's lane issues the TMA bulk
 // loads of its A and B ranges (keys, payloads).  A stage with task count -1
 // terminates the consumers.
+// The window is refilled (up to 32 tasks classified in parallel, one per
+// lane) whenever fewer than `refill` tasks are left in it: after every stage
+// (32) for plain merges of wide elements (mode 0, > 8 bytes: measured -10%
+// on C3/C4), else only when it runs low (8): the batched and sort-round
+// classifications take more dependent loads (mode 2/1: +46%/+19% when
+// refilled every stage).
 template <typename K, bool HAS_V, int VT, int STAGES, int MAXT, bool FIRSTFIT, typename Lay>
 __device__ __forceinline__ void k2_producer(const K* __restrict__ A, const uint32_t* __restrict__ vA,
                                             const K* __restrict__ B, const uint32_t* __restrict__ vB,
@@ -259,8 +265,9 @@ __device__ __forceinline__ void k2_producer(const K* __restrict__ A, const uint3
     int la = 0, lb = 0, off = 0, ag = 0, bg = 0;   // window slot `lane`
     int cnt = 0;                                    // slots [0, cnt) hold tasks
     int next = blockIdx.x;                          // next task of this CTA
+    const int refill = (g.sort == 0 && KB + (HAS_V ? 4 : 0) > 8) ? 32 : 8;
     for (int it = 0;; ++it) {
-        if (cnt < MAXT && next < ntasks) {
+        if (cnt < refill && next < ntasks) {
             const int my = next + (lane - cnt) * (int)gridDim.x;
             const bool fill = lane >= cnt && my < ntasks;
             if (fill) {
