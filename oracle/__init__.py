@@ -51,14 +51,14 @@ def lib():
         _lib = ctypes.CDLL(_LIB)
         P = ctypes.c_void_p
         I = ctypes.c_int64
-        for kt in NP_DTYPES:
+        for kt in list(NP_DTYPES) + [f"desc_{k}" for k in NP_DTYPES]:
             getattr(_lib, f"oracle_merge_{kt}").argtypes = [P, P, I, P, P, I, P, P]
             getattr(_lib, f"oracle_merge_{kt}").restype = None
             getattr(_lib, f"oracle_sort_{kt}").argtypes = [P, P, I]
             getattr(_lib, f"oracle_sort_{kt}").restype = ctypes.c_int
-            getattr(_lib, f"oracle_rank_low_{kt}").argtypes = [_C_KEY[kt], P, I]
+            getattr(_lib, f"oracle_rank_low_{kt}").argtypes = [_C_KEY[kt.replace("desc_", "")], P, I]
             getattr(_lib, f"oracle_rank_low_{kt}").restype = I
-            getattr(_lib, f"oracle_rank_high_{kt}").argtypes = [_C_KEY[kt], P, I]
+            getattr(_lib, f"oracle_rank_high_{kt}").argtypes = [_C_KEY[kt.replace("desc_", "")], P, I]
             getattr(_lib, f"oracle_rank_high_{kt}").restype = I
             getattr(_lib, f"oracle_positions_{kt}").argtypes = [P, I, P, I, P, P]
             getattr(_lib, f"oracle_positions_{kt}").restype = None
@@ -91,55 +91,60 @@ def vals_np(x):
     return as_np(x).view(np.uint32)
 
 
-def merge(a_keys, a_vals, b_keys, b_vals, key_type: str):
+def _fn(name: str, key_type: str, descending: bool):
+    return getattr(lib(), f"oracle_{name}_{'desc_' if descending else ''}{key_type}")
+
+
+def merge(a_keys, a_vals, b_keys, b_vals, key_type: str, descending: bool = False):
     """O1: the stable merge of A and B, ties to A.  Returns (c_keys, c_vals)
-    as numpy arrays (c_vals None when the inputs carry no payload)."""
+    as numpy arrays (c_vals None when the inputs carry no payload).
+    descending=True: the same under the reversed key order."""
     a, b = as_np(a_keys, key_type), as_np(b_keys, key_type)
     va, vb = vals_np(a_vals), vals_np(b_vals)
     assert (va is None) == (vb is None)
     n, m = a.size, b.size
     c = np.empty(n + m, dtype=NP_DTYPES[key_type])
     vc = None if va is None else np.empty(n + m, dtype=np.uint32)
-    getattr(lib(), f"oracle_merge_{key_type}")(_ptr(a), _ptr(va), n, _ptr(b), _ptr(vb), m, _ptr(c), _ptr(vc))
+    _fn("merge", key_type, descending)(_ptr(a), _ptr(va), n, _ptr(b), _ptr(vb), m, _ptr(c), _ptr(vc))
     return c, vc
 
 
-def sort(keys, vals, key_type: str):
+def sort(keys, vals, key_type: str, descending: bool = False):
     """O2: stable bottom-up merge sort.  Returns sorted copies."""
     k = as_np(keys, key_type).copy()
     v = None if vals is None else vals_np(vals).copy()
-    rc = getattr(lib(), f"oracle_sort_{key_type}")(_ptr(k), _ptr(v), k.size)
+    rc = _fn("sort", key_type, descending)(_ptr(k), _ptr(v), k.size)
     if rc != 0:
         raise MemoryError("oracle_sort: allocation failed")
     return k, v
 
 
-def rank_low(x, X, key_type: str) -> int:
+def rank_low(x, X, key_type: str, descending: bool = False) -> int:
     X = as_np(X, key_type)
-    return int(getattr(lib(), f"oracle_rank_low_{key_type}")(NP_DTYPES[key_type](x).item(), _ptr(X), X.size))
+    return int(_fn("rank_low", key_type, descending)(NP_DTYPES[key_type](x).item(), _ptr(X), X.size))
 
 
-def rank_high(x, X, key_type: str) -> int:
+def rank_high(x, X, key_type: str, descending: bool = False) -> int:
     X = as_np(X, key_type)
-    return int(getattr(lib(), f"oracle_rank_high_{key_type}")(NP_DTYPES[key_type](x).item(), _ptr(X), X.size))
+    return int(_fn("rank_high", key_type, descending)(NP_DTYPES[key_type](x).item(), _ptr(X), X.size))
 
 
-def positions(a_keys, b_keys, key_type: str):
+def positions(a_keys, b_keys, key_type: str, descending: bool = False):
     """O4: closed-form output positions."""
     a, b = as_np(a_keys, key_type), as_np(b_keys, key_type)
     pa = np.empty(a.size, dtype=np.int64)
     pb = np.empty(b.size, dtype=np.int64)
-    getattr(lib(), f"oracle_positions_{key_type}")(_ptr(a), a.size, _ptr(b), b.size, _ptr(pa), _ptr(pb))
+    _fn("positions", key_type, descending)(_ptr(a), a.size, _ptr(b), b.size, _ptr(pa), _ptr(pb))
     return pa, pb
 
 
-def positions_sample(a_keys, b_keys, key_type: str, ia, jb):
+def positions_sample(a_keys, b_keys, key_type: str, ia, jb, descending: bool = False):
     """O4 for sampled indices ia (into A) and jb (into B)."""
     a, b = as_np(a_keys, key_type), as_np(b_keys, key_type)
     ia = np.ascontiguousarray(ia, dtype=np.int64)
     jb = np.ascontiguousarray(jb, dtype=np.int64)
     pa = np.empty(ia.size, dtype=np.int64)
     pb = np.empty(jb.size, dtype=np.int64)
-    getattr(lib(), f"oracle_positions_sample_{key_type}")(_ptr(a), a.size, _ptr(b), b.size, _ptr(ia), ia.size,
-                                                          _ptr(pa), _ptr(jb), jb.size, _ptr(pb))
+    _fn("positions_sample", key_type, descending)(_ptr(a), a.size, _ptr(b), b.size, _ptr(ia), ia.size,
+                                                  _ptr(pa), _ptr(jb), jb.size, _ptr(pb))
     return pa, pb

@@ -25,7 +25,8 @@
  *                    C[i + rank_low(A[i],B)], B[j] to C[j + rank_high(B[j],A)].
  *
  * Keys: u32 / i32 / i64 / u64 with the natural (unsigned or signed) order;
- * f32 / f64 with IEEE 754 totalOrder.
+ * f32 / f64 with IEEE 754 totalOrder; the desc_*
+ * functions use the reversed order (descending keys, still ties to A).
  * Payloads: uint32, travelling with their key; NULL payload pointers mean
  * keys only.  Sizes are int64.  No error paths: callers pass valid sizes.
  */
@@ -147,9 +148,27 @@ void oracle_positions_sample_##SUF(const K *a, int64_t n, const K *b, int64_t m,
     for (t = 0; t < nb; t++) pos_b[t] = jb[t] + oracle_rank_high_##SUF(b[jb[t]], a, n);\
 }
 
+/* Descending order: the paper's method for an
+ * arbitrary total order "<=", instantiated with the reversed
+ * order a <=' b  <=>  b <= a.  Everything above is unchanged: stability is
+ * still "A before B on ties" (L160-163) under the reversed order. */
+#define LE_REV(LE, a, b) LE(b, a)
+#define LE_D_INT(a, b) LE_REV(LE_INT, a, b)
+#define LT_D_INT(a, b) LE_REV(LT_INT, a, b)
+#define LE_D_F32(a, b) LE_REV(LE_F32, a, b)
+#define LT_D_F32(a, b) LE_REV(LT_F32, a, b)
+#define LE_D_F64(a, b) LE_REV(LE_F64, a, b)
+#define LT_D_F64(a, b) LE_REV(LT_F64, a, b)
+
 DEFINE_ORACLE(u32, uint32_t, LE_INT, LT_INT)
 DEFINE_ORACLE(i32, int32_t, LE_INT, LT_INT)
 DEFINE_ORACLE(i64, int64_t, LE_INT, LT_INT)
 DEFINE_ORACLE(u64, uint64_t, LE_INT, LT_INT)
 DEFINE_ORACLE(f32, float, LE_F32, LT_F32)
 DEFINE_ORACLE(f64, double, LE_F64, LT_F64)
+DEFINE_ORACLE(desc_u32, uint32_t, LE_D_INT, LT_D_INT)
+DEFINE_ORACLE(desc_i32, int32_t, LE_D_INT, LT_D_INT)
+DEFINE_ORACLE(desc_i64, int64_t, LE_D_INT, LT_D_INT)
+DEFINE_ORACLE(desc_u64, uint64_t, LE_D_INT, LT_D_INT)
+DEFINE_ORACLE(desc_f32, float, LE_D_F32, LT_D_F32)
+DEFINE_ORACLE(desc_f64, double, LE_D_F64, LT_D_F64)

@@ -420,3 +420,74 @@ def test_float_total_order_special_values(orc):
     bits = ck.view(np.uint32).tolist()
     assert bits == [0xFFC00000, 0xFF800000, 0xBF800000, 0x80000000, 0x00000000, 0x00000001, 0x3F800000,
                     0x7F800000, 0x7FC00000]
+
+
+# ------------------------------------------------ descending order (f row 2)
+# The paper's method holds for any total order "<="; the
+# desc_* oracle functions instantiate it with the reversed order.  Pinned by
+# Python's stable sort under the reversed comparison (reverse=True keeps
+# stability), by the reversal identity with the ascending oracle, and by
+# linear counts for the ranks.
+
+def _desc_sorted_input(rng, dt, kt, n, few):
+    if kt in ("f32", "f64"):
+        v = rng.choice(np.array([-np.inf, -2.5, -0.0, 0.0, 1.0, 3.0, np.inf, np.nan], dtype=dt), n) if few \
+            else rng.standard_normal(n).astype(dt)
+    elif few:
+        v = rng.integers(0, 4, n).astype(dt)
+    else:
+        info = np.iinfo(dt)
+        v = rng.integers(info.min, info.max, n, dtype=dt, endpoint=True)
+    return v
+
+
+def _order_int(x, kt):
+    """An integer with the key order (floats: totalOrder, test-side)."""
+    if kt == "f32":
+        u = int(np.array([x], dtype=np.float32).view(np.uint32)[0])
+        return (u ^ 0xFFFFFFFF) if u >> 31 else (u | (1 << 31))
+    if kt == "f64":
+        u = int(np.array([x], dtype=np.float64).view(np.uint64)[0])
+        return (u ^ 0xFFFFFFFFFFFFFFFF) if u >> 63 else (u | (1 << 63))
+    return int(x)
+
+
+@pytest.mark.parametrize("kt", ["u32", "i32", "i64", "u64", "f32", "f64"])
+def test_desc_merge_and_sort_vs_python_reverse_sorted(orc, kt):
+    rng = np.random.default_rng(11)
+    dt = orc.NP_DTYPES[kt]
+    for trial in range(30):
+        n, m = int(rng.integers(0, 200)), int(rng.integers(0, 200))
+        a = _desc_sorted_input(rng, dt, kt, n, trial % 2 == 0)
+        b = _desc_sorted_input(rng, dt, kt, m, trial % 2 == 0)
+        a = np.array(sorted(a, key=lambda x: _order_int(x, kt), reverse=True), dtype=dt)
+        b = np.array(sorted(b, key=lambda x: _order_int(x, kt), reverse=True), dtype=dt)
+        va = np.arange(n, dtype=np.uint32)
+        vb = (np.arange(m) | (1 << 31)).astype(np.uint32)
+        c, vc = orc.merge(a, va, b, vb, kt, descending=True)
+        tagged = [(_order_int(k, kt), int(v)) for k, v in zip(a, va)] + \
+                 [(_order_int(k, kt), int(v)) for k, v in zip(b, vb)]
+        want = sorted(tagged, key=lambda e: e[0], reverse=True)     # stable: A (first in the list) first
+        assert vc.tolist() == [v for _, v in want]
+        assert [_order_int(k, kt) for k in c] == [k for k, _ in want]
+        # reversal identity: desc(A, B) = reverse(asc(reverse(B), reverse(A)))
+        c2, vc2 = orc.merge(b[::-1].copy(), vb[::-1].copy(), a[::-1].copy(), va[::-1].copy(), kt)
+        assert vc2[::-1].tolist() == vc.tolist()
+        # stable descending sort of the unsorted concatenation
+        keys = np.concatenate([b, a])
+        rng.shuffle(keys)
+        sk, sv = orc.sort(keys, np.arange(keys.size, dtype=np.uint32), kt, descending=True)
+        order = sorted(range(keys.size), key=lambda i: _order_int(keys[i], kt), reverse=True)
+        assert sv.tolist() == order
+
+
+@pytest.mark.parametrize("kt", ["u32", "i32", "i64", "u64", "f32", "f64"])
+def test_desc_ranks_vs_linear_count(orc, kt):
+    rng = np.random.default_rng(13)
+    dt = orc.NP_DTYPES[kt]
+    X = _desc_sorted_input(rng, dt, kt, 150, True)
+    X = np.array(sorted(X, key=lambda x: _order_int(x, kt), reverse=True), dtype=dt)
+    for x in list(X[::7]) + list(_desc_sorted_input(rng, dt, kt, 10, False)):
+        ox = _order_int(x, kt)
+        assert orc.rank_low(x, X, kt, descending=True) == sum(_order_int(t, kt) > ox for t in X)
+        assert orc.rank_high(x, X, kt, descending=True) == sum(_order_int(t, kt) >= ox for t in X)
