@@ -322,6 +322,134 @@ int64_t sm_last_launch_count(void);
 void sm_profile_enable(int on);
 sm_status sm_profile_read(int kind, double *total_ms, int64_t *launches);
 
+
+/* ---------------------------------------------------------------------
+ * Descending order -- SURVEY.md §8(f) row 2: the method for an arbitrary
+ * total order "<=", instantiated with the REVERSED key order
+ * (u32/u64 unsigned, i32/i64 signed, f32/f64 IEEE totalOrder, each
+ * reversed).  <op>_desc_<K> has exactly the signature and contract of
+ * <op>_<K> above, with "non-decreasing" read as "non-increasing":
+ *   inputs sorted non-increasingly; C non-increasing; stability unchanged --
+ *   every element of A precedes every equal-keyed element of B, and
+ *   mergesort_stable_desc keeps equal keys in input order;
+ *   ranks_stable_desc: rank_low(x, X) = #{X[t] > x}, rank_high = #{X[t] >= x}.
+ * Same kernels (one template instantiation per key type), same bytes moved.
+ * ------------------------------------------------------------------- */
+sm_status merge_stable_desc_u32(const uint32_t *keys_A, const uint32_t *vals_A, int64_t n,
+                                const uint32_t *keys_B, const uint32_t *vals_B, int64_t m,
+                                uint32_t *out_keys, uint32_t *out_vals, void *stream);
+sm_status merge_stable_desc_i32(const int32_t *keys_A, const uint32_t *vals_A, int64_t n,
+                                const int32_t *keys_B, const uint32_t *vals_B, int64_t m,
+                                int32_t *out_keys, uint32_t *out_vals, void *stream);
+sm_status merge_stable_desc_i64(const int64_t *keys_A, const uint32_t *vals_A, int64_t n,
+                                const int64_t *keys_B, const uint32_t *vals_B, int64_t m,
+                                int64_t *out_keys, uint32_t *out_vals, void *stream);
+sm_status merge_stable_desc_u64(const uint64_t *keys_A, const uint32_t *vals_A, int64_t n,
+                                const uint64_t *keys_B, const uint32_t *vals_B, int64_t m,
+                                uint64_t *out_keys, uint32_t *out_vals, void *stream);
+sm_status merge_stable_desc_f32(const float *keys_A, const uint32_t *vals_A, int64_t n,
+                                const float *keys_B, const uint32_t *vals_B, int64_t m,
+                                float *out_keys, uint32_t *out_vals, void *stream);
+sm_status merge_stable_desc_f64(const double *keys_A, const uint32_t *vals_A, int64_t n,
+                                const double *keys_B, const uint32_t *vals_B, int64_t m,
+                                double *out_keys, uint32_t *out_vals, void *stream);
+sm_status merge_stable_ex_desc_u32(const uint32_t *keys_A, const uint32_t *vals_A, int64_t n,
+                                   const uint32_t *keys_B, const uint32_t *vals_B, int64_t m,
+                                   uint32_t *out_keys, uint32_t *out_vals, void *stream,
+                                   const sm_options *opt);
+sm_status merge_stable_ex_desc_i32(const int32_t *keys_A, const uint32_t *vals_A, int64_t n,
+                                   const int32_t *keys_B, const uint32_t *vals_B, int64_t m,
+                                   int32_t *out_keys, uint32_t *out_vals, void *stream,
+                                   const sm_options *opt);
+sm_status merge_stable_ex_desc_i64(const int64_t *keys_A, const uint32_t *vals_A, int64_t n,
+                                   const int64_t *keys_B, const uint32_t *vals_B, int64_t m,
+                                   int64_t *out_keys, uint32_t *out_vals, void *stream,
+                                   const sm_options *opt);
+sm_status merge_stable_ex_desc_u64(const uint64_t *keys_A, const uint32_t *vals_A, int64_t n,
+                                   const uint64_t *keys_B, const uint32_t *vals_B, int64_t m,
+                                   uint64_t *out_keys, uint32_t *out_vals, void *stream,
+                                   const sm_options *opt);
+sm_status merge_stable_ex_desc_f32(const float *keys_A, const uint32_t *vals_A, int64_t n,
+                                   const float *keys_B, const uint32_t *vals_B, int64_t m,
+                                   float *out_keys, uint32_t *out_vals, void *stream,
+                                   const sm_options *opt);
+sm_status merge_stable_ex_desc_f64(const double *keys_A, const uint32_t *vals_A, int64_t n,
+                                   const double *keys_B, const uint32_t *vals_B, int64_t m,
+                                   double *out_keys, uint32_t *out_vals, void *stream,
+                                   const sm_options *opt);
+sm_status merge_plan_ex_desc_u32(const uint32_t *keys_A, int64_t n, const uint32_t *keys_B, int64_t m,
+                                 int64_t p_A, int64_t p_B, int64_t *xbar, int64_t *ybar, int64_t *tasks,
+                                 void *stream);
+sm_status merge_plan_ex_desc_i32(const int32_t *keys_A, int64_t n, const int32_t *keys_B, int64_t m,
+                                 int64_t p_A, int64_t p_B, int64_t *xbar, int64_t *ybar, int64_t *tasks,
+                                 void *stream);
+sm_status merge_plan_ex_desc_i64(const int64_t *keys_A, int64_t n, const int64_t *keys_B, int64_t m,
+                                 int64_t p_A, int64_t p_B, int64_t *xbar, int64_t *ybar, int64_t *tasks,
+                                 void *stream);
+sm_status merge_plan_ex_desc_u64(const uint64_t *keys_A, int64_t n, const uint64_t *keys_B, int64_t m,
+                                 int64_t p_A, int64_t p_B, int64_t *xbar, int64_t *ybar, int64_t *tasks,
+                                 void *stream);
+sm_status merge_plan_ex_desc_f32(const float *keys_A, int64_t n, const float *keys_B, int64_t m,
+                                 int64_t p_A, int64_t p_B, int64_t *xbar, int64_t *ybar, int64_t *tasks,
+                                 void *stream);
+sm_status merge_plan_ex_desc_f64(const double *keys_A, int64_t n, const double *keys_B, int64_t m,
+                                 int64_t p_A, int64_t p_B, int64_t *xbar, int64_t *ybar, int64_t *tasks,
+                                 void *stream);
+sm_status merge_stable_batched_desc_u32(const uint32_t *keys_A, const uint32_t *vals_A, int64_t n,
+                                        const int64_t *a_offsets, const uint32_t *keys_B, const uint32_t *vals_B,
+                                        int64_t m, const int64_t *b_offsets, int64_t S, uint32_t *out_keys,
+                                        uint32_t *out_vals, void *stream);
+sm_status merge_stable_batched_desc_i32(const int32_t *keys_A, const uint32_t *vals_A, int64_t n,
+                                        const int64_t *a_offsets, const int32_t *keys_B, const uint32_t *vals_B,
+                                        int64_t m, const int64_t *b_offsets, int64_t S, int32_t *out_keys,
+                                        uint32_t *out_vals, void *stream);
+sm_status merge_stable_batched_desc_i64(const int64_t *keys_A, const uint32_t *vals_A, int64_t n,
+                                        const int64_t *a_offsets, const int64_t *keys_B, const uint32_t *vals_B,
+                                        int64_t m, const int64_t *b_offsets, int64_t S, int64_t *out_keys,
+                                        uint32_t *out_vals, void *stream);
+sm_status merge_stable_batched_desc_u64(const uint64_t *keys_A, const uint32_t *vals_A, int64_t n,
+                                        const int64_t *a_offsets, const uint64_t *keys_B, const uint32_t *vals_B,
+                                        int64_t m, const int64_t *b_offsets, int64_t S, uint64_t *out_keys,
+                                        uint32_t *out_vals, void *stream);
+sm_status merge_stable_batched_desc_f32(const float *keys_A, const uint32_t *vals_A, int64_t n,
+                                        const int64_t *a_offsets, const float *keys_B, const uint32_t *vals_B,
+                                        int64_t m, const int64_t *b_offsets, int64_t S, float *out_keys,
+                                        uint32_t *out_vals, void *stream);
+sm_status merge_stable_batched_desc_f64(const double *keys_A, const uint32_t *vals_A, int64_t n,
+                                        const int64_t *a_offsets, const double *keys_B, const uint32_t *vals_B,
+                                        int64_t m, const int64_t *b_offsets, int64_t S, double *out_keys,
+                                        uint32_t *out_vals, void *stream);
+sm_status ranks_stable_desc_u32(const uint32_t *X, int64_t len, const uint32_t *keys, int64_t nkeys, int32_t high,
+                                  int64_t *out, void *stream);
+sm_status ranks_stable_desc_i32(const int32_t *X, int64_t len, const int32_t *keys, int64_t nkeys, int32_t high,
+                                  int64_t *out, void *stream);
+sm_status ranks_stable_desc_i64(const int64_t *X, int64_t len, const int64_t *keys, int64_t nkeys, int32_t high,
+                                  int64_t *out, void *stream);
+sm_status ranks_stable_desc_u64(const uint64_t *X, int64_t len, const uint64_t *keys, int64_t nkeys, int32_t high,
+                                  int64_t *out, void *stream);
+sm_status ranks_stable_desc_f32(const float *X, int64_t len, const float *keys, int64_t nkeys, int32_t high,
+                                  int64_t *out, void *stream);
+sm_status ranks_stable_desc_f64(const double *X, int64_t len, const double *keys, int64_t nkeys, int32_t high,
+                                  int64_t *out, void *stream);
+sm_status mergesort_stable_desc_u32(uint32_t *keys, uint32_t *vals, int64_t N, void *stream);
+sm_status mergesort_stable_desc_i32(int32_t *keys, uint32_t *vals, int64_t N, void *stream);
+sm_status mergesort_stable_desc_i64(int64_t *keys, uint32_t *vals, int64_t N, void *stream);
+sm_status mergesort_stable_desc_u64(uint64_t *keys, uint32_t *vals, int64_t N, void *stream);
+sm_status mergesort_stable_desc_f32(float *keys, uint32_t *vals, int64_t N, void *stream);
+sm_status mergesort_stable_desc_f64(double *keys, uint32_t *vals, int64_t N, void *stream);
+sm_status mergesort_stable_ex_desc_u32(uint32_t *keys, uint32_t *vals, int64_t N, void *stream,
+                                       const sm_options *opt);
+sm_status mergesort_stable_ex_desc_i32(int32_t *keys, uint32_t *vals, int64_t N, void *stream,
+                                       const sm_options *opt);
+sm_status mergesort_stable_ex_desc_i64(int64_t *keys, uint32_t *vals, int64_t N, void *stream,
+                                       const sm_options *opt);
+sm_status mergesort_stable_ex_desc_u64(uint64_t *keys, uint32_t *vals, int64_t N, void *stream,
+                                       const sm_options *opt);
+sm_status mergesort_stable_ex_desc_f32(float *keys, uint32_t *vals, int64_t N, void *stream,
+                                       const sm_options *opt);
+sm_status mergesort_stable_ex_desc_f64(double *keys, uint32_t *vals, int64_t N, void *stream,
+                                       const sm_options *opt);
+
 #ifdef __cplusplus
 }
 #endif

@@ -16,7 +16,9 @@ the host (the library stages them; the binding then synchronises the stream
 so host results are ready on return).  Unsigned keys: pass torch.uint32 /
 torch.uint64 tensors, or int32/int64 carriers with key_type="u32"/"u64".
 Floating-point keys (float32 / float64, or int32/int64 bit carriers with
-key_type="f32"/"f64") are ordered by IEEE 754 totalOrder.
+key_type="f32"/"f64") are ordered by IEEE 754 totalOrder.  descending=True
+uses the reversed key order (inputs and outputs non-increasing; ties still
+keep A first / input order).
 Payloads are 32-bit (int32 or uint32 tensors, same bits).
 """
 from __future__ import annotations
@@ -55,7 +57,7 @@ class SmOptions(ctypes.Structure):
 
 
 _P, _I = ctypes.c_void_p, ctypes.c_int64
-for _kt in KEY_TYPES:
+for _kt in KEY_TYPES + tuple(f"desc_{k}" for k in KEY_TYPES):
     for _name, _args in ((f"merge_stable_{_kt}", [_P, _P, _I, _P, _P, _I, _P, _P, _P]),
                          (f"merge_stable_ex_{_kt}", [_P, _P, _I, _P, _P, _I, _P, _P, _P, ctypes.POINTER(SmOptions)]),
                          (f"merge_plan_ex_{_kt}", [_P, _I, _P, _I, _I, _I, _P, _P, _P, _P]),
@@ -122,6 +124,10 @@ def _vals_ok(t: Optional[torch.Tensor]):
         raise TypeError("payloads must be 32-bit (int32 / uint32)")
 
 
+def _sym(op: str, kt: str, descending: bool) -> str:
+    return f"{op}_desc_{kt}" if descending else f"{op}_{kt}"
+
+
 def _stream_for(t: torch.Tensor, stream):
     if stream is not None:
         return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
@@ -172,7 +178,7 @@ def merge_stable(a_keys: torch.Tensor, a_vals: Optional[torch.Tensor], b_keys: t
                  b_vals: Optional[torch.Tensor], out_keys: Optional[torch.Tensor] = None,
                  out_vals: Optional[torch.Tensor] = None, *, key_type: Optional[str] = None, stream=None,
                  p_A: Optional[int] = None, p_B: Optional[int] = None, block: Optional[int] = None,
-                 pdl: bool = True, merge_path: bool = False):
+                 pdl: bool = True, merge_path: bool = False, descending: bool = False):
     """Stable merge of sorted A and B (ties: A first).  Returns (keys, vals).
     merge_path=True runs the equal-output merge-path COMPARISON instead of the
     paper's method (same result; CUDA tensors only)."""
@@ -192,9 +198,11 @@ def merge_stable(a_keys: torch.Tensor, a_vals: Optional[torch.Tensor], b_keys: t
     opt = _options(p_A, p_B, block, (0 if pdl else SM_FLAG_NO_PDL) | (SM_FLAG_MERGE_PATH if merge_path else 0))
     args = (_ptr(a_keys), _ptr(a_vals), n, _ptr(b_keys), _ptr(b_vals), m, _ptr(out_keys), _ptr(out_vals), s)
     if opt is None:
-        _check(getattr(_lib, f"merge_stable_{kt}")(*args), f"merge_stable_{kt}")
+        fn = _sym("merge_stable", kt, descending)
+        _check(getattr(_lib, fn)(*args), fn)
     else:
-        _check(getattr(_lib, f"merge_stable_ex_{kt}")(*args, ctypes.byref(opt)), f"merge_stable_ex_{kt}")
+        fn = _sym("merge_stable_ex", kt, descending)
+        _check(getattr(_lib, fn)(*args, ctypes.byref(opt)), fn)
     _sync_if_host(out_keys, s)
     return out_keys, out_vals
 
@@ -202,7 +210,7 @@ def merge_stable(a_keys: torch.Tensor, a_vals: Optional[torch.Tensor], b_keys: t
 def merge_stable_batched(a_keys: torch.Tensor, a_vals: Optional[torch.Tensor], a_offsets: torch.Tensor,
                          b_keys: torch.Tensor, b_vals: Optional[torch.Tensor], b_offsets: torch.Tensor,
                          out_keys: Optional[torch.Tensor] = None, out_vals: Optional[torch.Tensor] = None, *,
-                         key_type: Optional[str] = None, stream=None):
+                         key_type: Optional[str] = None, stream=None, descending: bool = False):
     """S = len(a_offsets) - 1 independent stable merges (ties: A first):
     segment s of A (a_keys[a_offsets[s]:a_offsets[s+1]]) with segment s of B
     into out[a_offsets[s] + b_offsets[s] : ...].  CUDA tensors only; offsets
@@ -223,27 +231,27 @@ def merge_stable_batched(a_keys: torch.Tensor, a_vals: Optional[torch.Tensor], a
     if a_vals is not None and out_vals is None:
         out_vals = torch.empty(n + m, dtype=a_vals.dtype, device=a_keys.device)
     s = _stream_for(a_keys, stream)
-    _check(getattr(_lib, f"merge_stable_batched_{kt}")(_ptr(a_keys), _ptr(a_vals), n, _ptr(a_offsets), _ptr(b_keys),
-                                                         _ptr(b_vals), m, _ptr(b_offsets), S, _ptr(out_keys),
-                                                         _ptr(out_vals), s), f"merge_stable_batched_{kt}")
+    fn = _sym("merge_stable_batched", kt, descending)
+    _check(getattr(_lib, fn)(_ptr(a_keys), _ptr(a_vals), n, _ptr(a_offsets), _ptr(b_keys), _ptr(b_vals), m,
+                             _ptr(b_offsets), S, _ptr(out_keys), _ptr(out_vals), s), fn)
     return out_keys, out_vals
 
 
 def ranks_stable(X: torch.Tensor, keys: torch.Tensor, high: bool = False, *, key_type: Optional[str] = None,
-                 stream=None) -> torch.Tensor:
+                 stream=None, descending: bool = False) -> torch.Tensor:
     """rank_low (high=False) or rank_high (high=True) of every key in sorted
     X.  CUDA tensors; returns int64 ranks."""
     kt = _key_type(X, key_type)
     _key_type(keys, kt)
     out = torch.empty(keys.numel(), dtype=torch.int64, device=keys.device)
     s = _stream_for(X, stream)
-    _check(getattr(_lib, f"ranks_stable_{kt}")(_ptr(X), X.numel(), _ptr(keys), keys.numel(), int(bool(high)),
-                                                _ptr(out), s), f"ranks_stable_{kt}")
+    fn = _sym("ranks_stable", kt, descending)
+    _check(getattr(_lib, fn)(_ptr(X), X.numel(), _ptr(keys), keys.numel(), int(bool(high)), _ptr(out), s), fn)
     return out
 
 
 def mergesort_stable(keys: torch.Tensor, vals: Optional[torch.Tensor] = None, *, key_type: Optional[str] = None,
-                     stream=None, pdl: bool = True):
+                     stream=None, pdl: bool = True, descending: bool = False):
     """Stable merge sort in place (equal keys keep input order).  Returns (keys, vals)."""
     kt = _key_type(keys, key_type)
     _vals_ok(vals)
@@ -253,16 +261,18 @@ def mergesort_stable(keys: torch.Tensor, vals: Optional[torch.Tensor] = None, *,
     s = _stream_for(keys, stream)
     args = (_ptr(keys), _ptr(vals), N, s)
     if pdl:
-        _check(getattr(_lib, f"mergesort_stable_{kt}")(*args), f"mergesort_stable_{kt}")
+        fn = _sym("mergesort_stable", kt, descending)
+        _check(getattr(_lib, fn)(*args), fn)
     else:
         opt = SmOptions(0, 0, 0, 0, SM_FLAG_NO_PDL)
-        _check(getattr(_lib, f"mergesort_stable_ex_{kt}")(*args, ctypes.byref(opt)), f"mergesort_stable_ex_{kt}")
+        fn = _sym("mergesort_stable_ex", kt, descending)
+        _check(getattr(_lib, fn)(*args, ctypes.byref(opt)), fn)
     _sync_if_host(keys, s)
     return keys, vals
 
 
 def merge_plan(a_keys: torch.Tensor, b_keys: torch.Tensor, p_A: int, p_B: Optional[int] = None, *,
-               key_type: Optional[str] = None, stream=None):
+               key_type: Optional[str] = None, stream=None, descending: bool = False):
     """Steps 1-4 on the device: (xbar[p_A+1], ybar[p_B+1], tasks[p_A+p_B, 6]) int64 tensors."""
     kt = _key_type(a_keys, key_type)
     _key_type(b_keys, kt)
@@ -275,9 +285,9 @@ def merge_plan(a_keys: torch.Tensor, b_keys: torch.Tensor, p_A: int, p_B: Option
     ybar = torch.empty(p_B + 1, dtype=torch.int64, device=dev)
     tasks = torch.empty((p_A + p_B, 6), dtype=torch.int64, device=dev)
     s = _stream_for(a_keys, stream)
-    _check(getattr(_lib, f"merge_plan_ex_{kt}")(_ptr(a_keys), a_keys.numel(), _ptr(b_keys), b_keys.numel(),
-                                                 p_A, p_B, _ptr(xbar), _ptr(ybar), _ptr(tasks), s),
-           f"merge_plan_ex_{kt}")
+    fn = _sym("merge_plan_ex", kt, descending)
+    _check(getattr(_lib, fn)(_ptr(a_keys), a_keys.numel(), _ptr(b_keys), b_keys.numel(), p_A, p_B, _ptr(xbar),
+                             _ptr(ybar), _ptr(tasks), s), fn)
     return xbar, ybar, tasks
 
 

@@ -95,17 +95,48 @@ template <> struct KeyOrd<double> {
     }
 };
 
+// Descending order: the method for an arbitrary
+// total order "<=" instantiated with the reversed one.  Desc<B>
+// is a distinct key type with B's bits and the complemented order view, so
+// every kernel template runs unchanged on it (ties still go to A).
+template <typename B>
+struct Desc {
+    B v;
+    Desc() = default;
+    __device__ __host__ __forceinline__ constexpr explicit Desc(B x) : v(x) {}
+};
+template <typename B> struct KeyOrd<Desc<B>> {
+    using U = typename KeyOrd<B>::U;
+    static constexpr bool FLOAT = KeyOrd<B>::FLOAT;
+    __device__ __host__ __forceinline__ static U to(Desc<B> x) { return (U)~KeyOrd<B>::to(x.v); }
+    __device__ __host__ __forceinline__ static Desc<B> from(U u) { return Desc<B>(KeyOrd<B>::from((U)~u)); }
+};
+template <typename K> struct IsDesc { static constexpr bool value = false; };
+template <typename B> struct IsDesc<Desc<B>> { static constexpr bool value = true; };
+
 // a <= b and a < b in the key order (native compares for integer keys)
 template <typename K>
 __device__ __host__ __forceinline__ bool key_le(K a, K b) {
-    if constexpr (KeyOrd<K>::FLOAT) return KeyOrd<K>::to(a) <= KeyOrd<K>::to(b);
+    if constexpr (KeyOrd<K>::FLOAT || IsDesc<K>::value) return KeyOrd<K>::to(a) <= KeyOrd<K>::to(b);
     else return a <= b;
 }
 template <typename K>
 __device__ __host__ __forceinline__ bool key_lt(K a, K b) {
-    if constexpr (KeyOrd<K>::FLOAT) return KeyOrd<K>::to(a) < KeyOrd<K>::to(b);
+    if constexpr (KeyOrd<K>::FLOAT || IsDesc<K>::value) return KeyOrd<K>::to(a) < KeyOrd<K>::to(b);
     else return a < b;
 }
+
+// The bits of a key as its base type (for inline PTX operands).
+template <typename K>
+__device__ __forceinline__ K& raw_ref(K& k) { return k; }
+template <typename B>
+__device__ __forceinline__ B& raw_ref(Desc<B>& k) { return k.v; }
+
+// Read-only global load of a key.
+template <typename K>
+__device__ __forceinline__ K ldg_key(const K* p) { return __ldg(p); }
+template <typename B>
+__device__ __forceinline__ Desc<B> ldg_key(const Desc<B>* p) { return Desc<B>(__ldg((const B*)p)); }
 
 // ---------------------------------------------------------------------------
 // Geometry of one launch: one merge (mode 0, S = 1), one merge-sort round
@@ -263,6 +294,10 @@ template <typename T>
 __device__ __forceinline__ T ld_stream(const T* p) { return __ldcs(p); }
 template <typename T>
 __device__ __forceinline__ void st_stream(T* p, T v) { __stcs(p, v); }
+template <typename B>
+__device__ __forceinline__ Desc<B> ld_stream(const Desc<B>* p) { return Desc<B>(__ldcs((const B*)p)); }
+template <typename B>
+__device__ __forceinline__ void st_stream(Desc<B>* p, Desc<B> v) { __stcs((B*)p, v.v); }
 
 // Programmatic dependent launch (sm_90+): wait for the producer grid's
 // memory to be visible; a no-op when the launch was not programmatic.
@@ -383,16 +418,18 @@ __device__ __forceinline__ void merge_step_idx(uint32_t& pa, uint32_t& pb, K& ka
 template <typename K>
 __device__ __forceinline__ K lds(uint32_t addr);
 
-#define SM_DEF_SMEM_OPS(K, CMP, BITS, RC, SZ)                                                                  \
+// NAME: specialisation tag; X_LE_Y / KA_LE_KB: the operand order of the key
+// compare ("x, y" / "%2, %3" ascending; reversed for the Desc<> types).
+#define SM_DEF_SMEM_OPS(K, NAME, CMP, BITS, RC, SZ, X_LE_Y, KA_LE_KB)                                          \
     template <int STEP>                                                                                        \
-    struct LiftProbe_##CMP {                                                                                   \
+    struct LiftProbe_##NAME {                                                                                  \
         __device__ __forceinline__ static void run(uint32_t& sa, uint32_t& sb, int& rem) {                     \
             asm volatile(                                                                                      \
                 "{\n\t.reg .pred p, q;\n\t.reg .b" BITS " x, y;\n\t"                                          \
                 "setp.le.s32 p, %3, %2;\n\t"                                                                   \
                 "@p ld.shared.b" BITS " x, [%0+%4];\n\t"                                                       \
                 "@p ld.shared.b" BITS " y, [%1+%5];\n\t"                                                       \
-                "setp.le.and." #CMP " q, x, y, p;\n\t"                                                          \
+                "setp.le.and." #CMP " q, " X_LE_Y ", p;\n\t"                                                   \
                 "@q add.u32 %0, %0, %6;\n\t"                                                                   \
                 "@q sub.u32 %1, %1, %6;\n\t"                                                                   \
                 "@q sub.s32 %2, %2, %3;\n\t}"                                                                  \
@@ -404,7 +441,7 @@ __device__ __forceinline__ K lds(uint32_t addr);
     template <>                                                                                                \
     __device__ __forceinline__ K lds<K>(uint32_t addr) {                                                       \
         K v;                                                                                                   \
-        asm volatile("ld.shared.b" BITS " %0, [%1];" : "=" RC(v) : "r"(addr) : "memory");                     \
+        asm volatile("ld.shared.b" BITS " %0, [%1];" : "=" RC(raw_ref(v)) : "r"(addr) : "memory");            \
         return v;                                                                                              \
     }                                                                                                          \
     template <>                                                                                                \
@@ -417,7 +454,7 @@ __device__ __forceinline__ K lds(uint32_t addr);
             "{\n\t.reg .pred t, u, w;\n\t.reg .b32 ad;\n\t.reg .b" BITS " k;\n\t"                             \
             "setp.lt.u32 u, %0, %7;\n\t"                                                                       \
             "setp.ge.u32 w, %1, %8;\n\t"                                                                       \
-            "setp.le.and." #CMP " t, %2, %3, u;\n\t"                                                           \
+            "setp.le.and." #CMP " t, " KA_LE_KB ", u;\n\t"                                                    \
             "or.pred t, t, w;\n\t"                                                                             \
             "selp.b" BITS " %6, %2, %3, t;\n\t"                                                                \
             "selp.b" BITS " %2, %4, %2, t;\n\t"                                                                \
@@ -428,7 +465,8 @@ __device__ __forceinline__ K lds(uint32_t addr);
             "ld.shared.b" BITS " k, [ad+" #SZ "];\n\t"                                                         \
             "selp.b" BITS " %4, k, %4, t;\n\t"                                                                 \
             "selp.b" BITS " %5, %5, k, t;\n\t}"                                                                \
-            : "+r"(pa), "+r"(pb), "+" RC(ka), "+" RC(kb), "+" RC(na), "+" RC(nb), "=" RC(out)                  \
+            : "+r"(pa), "+r"(pb), "+" RC(raw_ref(ka)), "+" RC(raw_ref(kb)), "+" RC(raw_ref(na)),              \
+              "+" RC(raw_ref(nb)), "=" RC(raw_ref(out))                                                        \
             : "r"(pae), "r"(pbe)                                                                               \
             : "memory");                                                                                       \
     }                                                                                                          \
@@ -440,7 +478,7 @@ __device__ __forceinline__ K lds(uint32_t addr);
             "{\n\t.reg .pred t, u, w;\n\t.reg .b32 ad;\n\t.reg .b" BITS " k;\n\t"                             \
             "setp.lt.u32 u, %0, %10;\n\t"                                                                      \
             "setp.ge.u32 w, %1, %11;\n\t"                                                                      \
-            "setp.le.and." #CMP " t, %2, %3, u;\n\t"                                                           \
+            "setp.le.and." #CMP " t, " KA_LE_KB ", u;\n\t"                                                    \
             "or.pred t, t, w;\n\t"                                                                             \
             "selp.b" BITS " %6, %2, %3, t;\n\t"                                                                \
             "selp.b32 %9, %7, %8, t;\n\t"                                                                      \
@@ -454,23 +492,27 @@ __device__ __forceinline__ K lds(uint32_t addr);
             "ld.shared.b" BITS " k, [ad+" #SZ "];\n\t"                                                         \
             "selp.b" BITS " %4, k, %4, t;\n\t"                                                                 \
             "selp.b" BITS " %5, %5, k, t;\n\t}"                                                                \
-            : "+r"(pa), "+r"(pb), "+" RC(ka), "+" RC(kb), "+" RC(na), "+" RC(nb), "=" RC(out), "+r"(ia),      \
-              "+r"(ib), "=r"(src)                                                                              \
+            : "+r"(pa), "+r"(pb), "+" RC(raw_ref(ka)), "+" RC(raw_ref(kb)), "+" RC(raw_ref(na)),              \
+              "+" RC(raw_ref(nb)), "=" RC(raw_ref(out)), "+r"(ia), "+r"(ib), "=r"(src)                         \
             : "r"(pae), "r"(pbe)                                                                               \
             : "memory");                                                                                       \
     }                                                                                                          \
     template <int STEP>                                                                                        \
     struct LiftSel<K, STEP> {                                                                                  \
-        using type = LiftProbe_##CMP<STEP>;                                                                    \
+        using type = LiftProbe_##NAME<STEP>;                                                                   \
     };
 
 template <typename K, int STEP>
 struct LiftSel;
 
-SM_DEF_SMEM_OPS(uint32_t, u32, "32", "r", 4)
-SM_DEF_SMEM_OPS(int32_t, s32, "32", "r", 4)
-SM_DEF_SMEM_OPS(uint64_t, u64, "64", "l", 8)
-SM_DEF_SMEM_OPS(int64_t, s64, "64", "l", 8)
+SM_DEF_SMEM_OPS(uint32_t, u32, u32, "32", "r", 4, "x, y", "%2, %3")
+SM_DEF_SMEM_OPS(int32_t, s32, s32, "32", "r", 4, "x, y", "%2, %3")
+SM_DEF_SMEM_OPS(uint64_t, u64, u64, "64", "l", 8, "x, y", "%2, %3")
+SM_DEF_SMEM_OPS(int64_t, s64, s64, "64", "l", 8, "x, y", "%2, %3")
+SM_DEF_SMEM_OPS(Desc<uint32_t>, du32, u32, "32", "r", 4, "y, x", "%3, %2")
+SM_DEF_SMEM_OPS(Desc<int32_t>, ds32, s32, "32", "r", 4, "y, x", "%3, %2")
+SM_DEF_SMEM_OPS(Desc<uint64_t>, du64, u64, "64", "l", 8, "y, x", "%3, %2")
+SM_DEF_SMEM_OPS(Desc<int64_t>, ds64, s64, "64", "l", 8, "y, x", "%3, %2")
 #undef SM_DEF_SMEM_OPS
 
 template <typename K, int STEP>

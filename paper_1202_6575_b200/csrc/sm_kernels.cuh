@@ -45,7 +45,7 @@ __device__ __forceinline__ int group_rank(const K* __restrict__ X, int len, K x,
         const int pos = n > G ? probe_pos<G>(lo, n, sub) : lo + sub;   // n <= G: probe every key left
         bool pred = false;
         if (hi > lo && sub < min(G, n)) {
-            const K v = __ldg(X + pos);
+            const K v = ldg_key(X + pos);
             pred = high ? key_le(v, x) : key_lt(v, x);
         }
         const unsigned bal = (__ballot_sync(0xffffffffu, pred) >> shift) & (G == 32 ? 0xffffffffu : ((1u << (G & 31)) - 1u));
@@ -76,7 +76,7 @@ __device__ __forceinline__ int rank_kary(const K* __restrict__ X, int len, K x, 
         const int q = n / WAYS;
         K v[WAYS - 1];
 #pragma unroll
-        for (int k = 0; k < WAYS - 1; ++k) v[k] = __ldg(X + lo + (k + 1) * q - 1);   // independent loads
+        for (int k = 0; k < WAYS - 1; ++k) v[k] = ldg_key(X + lo + (k + 1) * q - 1);   // independent loads
         int t = 0;                           // probes passed: a prefix
 #pragma unroll
         for (int k = 0; k < WAYS - 1; ++k) t += (high ? key_le(v[k], x) : key_lt(v[k], x)) ? 1 : 0;
@@ -87,7 +87,7 @@ __device__ __forceinline__ int rank_kary(const K* __restrict__ X, int len, K x, 
     }
     while (n > 0) {                          // binary tail
         const int half = n >> 1;
-        const bool right = high ? key_le(__ldg(X + lo + half), x) : key_lt(__ldg(X + lo + half), x);
+        const bool right = high ? key_le(ldg_key(X + lo + half), x) : key_lt(ldg_key(X + lo + half), x);
         lo = right ? lo + half + 1 : lo;
         n = right ? n - half - 1 : half;
     }
@@ -116,7 +116,7 @@ __global__ void __launch_bounds__(256) k_cross_ranks(const K* __restrict__ A, co
     const int oth_len = sideA ? sg.m : sg.n;         // searched array
     const bool search = valid && idx < plen && idx < own_len;   // x_idx < own_len  <=>  idx < own_len
     K x = K(0);
-    if (search) x = __ldg((sideA ? A + sg.aoff : B + sg.boff) + Blocks(own_len, plen).start(idx));
+    if (search) x = ldg_key((sideA ? A + sg.aoff : B + sg.boff) + Blocks(own_len, plen).start(idx));
     int r;
     if constexpr (G == 1) {
         r = search ? rank_kary<K, K1_WAYS>(sideA ? B + sg.boff : A + sg.aoff, oth_len, x, !sideA) : 0;
@@ -620,7 +620,7 @@ __global__ void __launch_bounds__(256) k_rank_keys(const K* __restrict__ X, int6
     int64_t lo = 0, hi = len;
     while (lo < hi) {
         const int64_t mid = (lo + hi) >> 1;
-        const K v = __ldg(X + mid);
+        const K v = ldg_key(X + mid);
         if (high ? key_le(v, x) : key_lt(v, x)) lo = mid + 1;
         else hi = mid;
     }
@@ -644,7 +644,7 @@ __global__ void __launch_bounds__(256) k_diag_splits(const K* __restrict__ A, co
         int lo = max(0, D - m), hi = min(D, n);
         while (lo < hi) {
             const int mid = (lo + hi) >> 1;
-            if (key_le(__ldg(A + mid), __ldg(B + (D - 1 - mid)))) lo = mid + 1;
+            if (key_le(ldg_key(A + mid), ldg_key(B + (D - 1 - mid)))) lo = mid + 1;
             else hi = mid;
         }
         split[k] = lo;

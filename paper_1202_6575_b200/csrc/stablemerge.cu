@@ -760,46 +760,57 @@ static sm_status sort_entry(K* keys, uint32_t* vals, int64_t N, void* stream, co
 // ================================================================ C ABI
 extern "C" {
 
-#define SM_DEFINE_ABI(SUF, K)                                                                                   \
-    sm_status merge_stable_##SUF(const K* keys_A, const uint32_t* vals_A, int64_t n, const K* keys_B,          \
-                                 const uint32_t* vals_B, int64_t m, K* out_keys, uint32_t* out_vals,          \
+// K: the key type the kernels see; C: its bits as the ABI type (C = K, or
+// the base type of Desc<C> for the descending-order entries).
+#define SM_DEFINE_ABI(SUF, K, C)                                                                                \
+    sm_status merge_stable_##SUF(const C* keys_A, const uint32_t* vals_A, int64_t n, const C* keys_B,          \
+                                 const uint32_t* vals_B, int64_t m, C* out_keys, uint32_t* out_vals,          \
                                  void* stream) {                                                               \
-        return sm::merge_entry<K>(keys_A, vals_A, n, keys_B, vals_B, m, out_keys, out_vals, stream, nullptr);   \
+        return sm::merge_entry<K>((const K*)keys_A, vals_A, n, (const K*)keys_B, vals_B, m, (K*)out_keys,      \
+                                  out_vals, stream, nullptr);                                                  \
     }                                                                                                           \
-    sm_status merge_stable_ex_##SUF(const K* keys_A, const uint32_t* vals_A, int64_t n, const K* keys_B,       \
-                                    const uint32_t* vals_B, int64_t m, K* out_keys, uint32_t* out_vals,       \
+    sm_status merge_stable_ex_##SUF(const C* keys_A, const uint32_t* vals_A, int64_t n, const C* keys_B,       \
+                                    const uint32_t* vals_B, int64_t m, C* out_keys, uint32_t* out_vals,       \
                                     void* stream, const sm_options* opt) {                                     \
-        return sm::merge_entry<K>(keys_A, vals_A, n, keys_B, vals_B, m, out_keys, out_vals, stream, opt);       \
+        return sm::merge_entry<K>((const K*)keys_A, vals_A, n, (const K*)keys_B, vals_B, m, (K*)out_keys,      \
+                                  out_vals, stream, opt);                                                      \
     }                                                                                                           \
-    sm_status merge_plan_ex_##SUF(const K* keys_A, int64_t n, const K* keys_B, int64_t m, int64_t p_A,         \
+    sm_status merge_plan_ex_##SUF(const C* keys_A, int64_t n, const C* keys_B, int64_t m, int64_t p_A,         \
                                   int64_t p_B, int64_t* xbar, int64_t* ybar, int64_t* tasks, void* stream) {   \
-        return sm::plan_entry<K>(keys_A, n, keys_B, m, p_A, p_B, xbar, ybar, tasks, stream);                    \
+        return sm::plan_entry<K>((const K*)keys_A, n, (const K*)keys_B, m, p_A, p_B, xbar, ybar, tasks,        \
+                                 stream);                                                                      \
     }                                                                                                           \
-    sm_status merge_stable_batched_##SUF(const K* keys_A, const uint32_t* vals_A, int64_t n,                   \
-                                         const int64_t* a_offsets, const K* keys_B, const uint32_t* vals_B,    \
-                                         int64_t m, const int64_t* b_offsets, int64_t S, K* out_keys,          \
+    sm_status merge_stable_batched_##SUF(const C* keys_A, const uint32_t* vals_A, int64_t n,                   \
+                                         const int64_t* a_offsets, const C* keys_B, const uint32_t* vals_B,    \
+                                         int64_t m, const int64_t* b_offsets, int64_t S, C* out_keys,          \
                                          uint32_t* out_vals, void* stream) {                                   \
-        return sm::batch_entry<K>(keys_A, vals_A, n, a_offsets, keys_B, vals_B, m, b_offsets, S, out_keys,    \
-                                  out_vals, stream);                                                           \
+        return sm::batch_entry<K>((const K*)keys_A, vals_A, n, a_offsets, (const K*)keys_B, vals_B, m,        \
+                                  b_offsets, S, (K*)out_keys, out_vals, stream);                               \
     }                                                                                                           \
-    sm_status ranks_stable_##SUF(const K* X, int64_t len, const K* keys, int64_t nkeys, int32_t high,        \
+    sm_status ranks_stable_##SUF(const C* X, int64_t len, const C* keys, int64_t nkeys, int32_t high,        \
                                  int64_t* out, void* stream) {                                                 \
-        return sm::ranks_entry<K>(X, len, keys, nkeys, high, out, stream);                                      \
+        return sm::ranks_entry<K>((const K*)X, len, (const K*)keys, nkeys, high, out, stream);                  \
     }                                                                                                           \
-    sm_status mergesort_stable_##SUF(K* keys, uint32_t* vals, int64_t N, void* stream) {                       \
-        return sm::sort_entry<K>(keys, vals, N, stream, nullptr);                                               \
+    sm_status mergesort_stable_##SUF(C* keys, uint32_t* vals, int64_t N, void* stream) {                       \
+        return sm::sort_entry<K>((K*)keys, vals, N, stream, nullptr);                                           \
     }                                                                                                           \
-    sm_status mergesort_stable_ex_##SUF(K* keys, uint32_t* vals, int64_t N, void* stream,                      \
+    sm_status mergesort_stable_ex_##SUF(C* keys, uint32_t* vals, int64_t N, void* stream,                      \
                                         const sm_options* opt) {                                               \
-        return sm::sort_entry<K>(keys, vals, N, stream, opt);                                                   \
+        return sm::sort_entry<K>((K*)keys, vals, N, stream, opt);                                               \
     }
 
-SM_DEFINE_ABI(u32, uint32_t)
-SM_DEFINE_ABI(i32, int32_t)
-SM_DEFINE_ABI(i64, int64_t)
-SM_DEFINE_ABI(u64, uint64_t)
-SM_DEFINE_ABI(f32, float)
-SM_DEFINE_ABI(f64, double)
+SM_DEFINE_ABI(u32, uint32_t, uint32_t)
+SM_DEFINE_ABI(i32, int32_t, int32_t)
+SM_DEFINE_ABI(i64, int64_t, int64_t)
+SM_DEFINE_ABI(u64, uint64_t, uint64_t)
+SM_DEFINE_ABI(f32, float, float)
+SM_DEFINE_ABI(f64, double, double)
+SM_DEFINE_ABI(desc_u32, sm::Desc<uint32_t>, uint32_t)
+SM_DEFINE_ABI(desc_i32, sm::Desc<int32_t>, int32_t)
+SM_DEFINE_ABI(desc_i64, sm::Desc<int64_t>, int64_t)
+SM_DEFINE_ABI(desc_u64, sm::Desc<uint64_t>, uint64_t)
+SM_DEFINE_ABI(desc_f32, sm::Desc<float>, float)
+SM_DEFINE_ABI(desc_f64, sm::Desc<double>, double)
 
 int64_t sm_tile_capacity(int32_t key_bytes, int32_t has_vals) {
     return sm::tile_nv(key_bytes, has_vals != 0);

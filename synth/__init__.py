@@ -198,11 +198,14 @@ def _keys(dist: str, key_type: str, seed: int, stream: int, count: int, device) 
 
 
 def merge_input(n: int, m: int, key_type: str, dist: str, seed: int, payload: bool = True,
-                device="cpu") -> MergeInput:
-    """Two independently sorted arrays A (n) and B (m) of `dist` keys."""
+                device="cpu", descending: bool = False) -> MergeInput:
+    """Two independently sorted arrays A (n) and B (m) of `dist` keys
+    (non-increasing when `descending`)."""
     _, order, _ = KEY_TYPES[key_type]
     a = sort_bits(_keys(dist, key_type, seed, STREAM_A, n, device), order)
     b = sort_bits(_keys(dist, key_type, seed, STREAM_B, m, device), order)
+    if descending:
+        a, b = a.flip(0), b.flip(0)
     av = bv = None
     if payload:
         av, bv = source_payloads(n, m, device)
@@ -243,7 +246,8 @@ class BatchInput:
                           f(self.a_offsets), f(self.b_offsets))
 
 
-def _segmented(S: int, mean: int, key_type: str, dist: str, seed: int, stream: int, device):
+def _segmented(S: int, mean: int, key_type: str, dist: str, seed: int, stream: int, device,
+               descending: bool = False):
     """S segments of lengths uniform in [0, 2*mean), each sorted (library
     sort on (segment, key)); returns (keys, offsets)."""
     _, order, _ = KEY_TYPES[key_type]
@@ -254,18 +258,18 @@ def _segmented(S: int, mean: int, key_type: str, dist: str, seed: int, stream: i
     keys = _keys(dist, key_type, seed, stream, total, device)
     seg = torch.repeat_interleave(torch.arange(S, device=device), lens)
     # order by (segment, key): a stable sort by key, then a stable sort by segment
-    idx = torch.sort(_order_key(keys, order), stable=True).indices
+    idx = torch.sort(_order_key(keys, order), stable=True, descending=descending).indices
     idx = idx[torch.sort(seg[idx], stable=True).indices]
     return keys[idx], off
 
 
 def batch_input(S: int, mean: int, key_type: str, dist: str, seed: int, payload: bool = True,
-                device="cpu") -> BatchInput:
+                device="cpu", descending: bool = False) -> BatchInput:
     """S independent merge pairs, segment lengths
     uniform in [0, 2*mean) on each side, keys of `dist` sorted per segment;
     payloads as R13 over the concatenated arrays."""
-    a, aoff = _segmented(S, mean, key_type, dist, seed, STREAM_A, device)
-    b, boff = _segmented(S, mean, key_type, dist, seed, STREAM_B, device)
+    a, aoff = _segmented(S, mean, key_type, dist, seed, STREAM_A, device, descending)
+    b, boff = _segmented(S, mean, key_type, dist, seed, STREAM_B, device, descending)
     av = bv = None
     if payload:
         av, bv = source_payloads(a.numel(), b.numel(), device)

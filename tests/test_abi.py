@@ -33,7 +33,8 @@ def test_header_declares_entry_points():
         for f in ("merge_stable", "mergesort_stable", "merge_stable_ex", "merge_plan_ex", "mergesort_stable_ex",
                   "merge_stable_batched", "ranks_stable"):
             assert f"{f}_{kt}" in names
-    assert len(names) == 49
+            assert f"{f}_desc_{kt}" in names          # descending order
+    assert len(names) == 91
 
 
 def test_library_exports_every_declared_symbol(sm):
