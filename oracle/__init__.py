@@ -60,6 +60,10 @@ def lib():
             getattr(_lib, f"oracle_rank_low_{kt}").restype = I
             getattr(_lib, f"oracle_rank_high_{kt}").argtypes = [_C_KEY[kt.replace("desc_", "")], P, I]
             getattr(_lib, f"oracle_rank_high_{kt}").restype = I
+            getattr(_lib, f"oracle_merge_wide_{kt}").argtypes = [P, P, I, P, P, I, P, P, I]
+            getattr(_lib, f"oracle_merge_wide_{kt}").restype = None
+            getattr(_lib, f"oracle_sort_wide_{kt}").argtypes = [P, P, I, I]
+            getattr(_lib, f"oracle_sort_wide_{kt}").restype = ctypes.c_int
             getattr(_lib, f"oracle_positions_{kt}").argtypes = [P, I, P, I, P, P]
             getattr(_lib, f"oracle_positions_{kt}").restype = None
             getattr(_lib, f"oracle_positions_sample_{kt}").argtypes = [P, I, P, I, P, I, P, P, I, P]
@@ -117,6 +121,41 @@ def sort(keys, vals, key_type: str, descending: bool = False):
     if rc != 0:
         raise MemoryError("oracle_sort: allocation failed")
     return k, v
+
+
+def _rows(v, count: int):
+    """Payload tensor/array with `count` rows -> contiguous numpy bytes (count, w)."""
+    v = np.ascontiguousarray(as_np(v))
+    assert v.shape[0] == count
+    w = v.dtype.itemsize * int(np.prod(v.shape[1:], dtype=np.int64))
+    return np.frombuffer(v.tobytes(), dtype=np.uint8).reshape(count, w), v
+
+
+def merge_wide(a_keys, a_vals, b_keys, b_vals, key_type: str, descending: bool = False):
+    """O1 with payloads of any width: row i of a_vals (any dtype and trailing
+    shape) travels with A[i].  Returns (c_keys, c_vals) with c_vals shaped
+    and typed like the inputs' rows."""
+    a, b = as_np(a_keys, key_type), as_np(b_keys, key_type)
+    ra, va = _rows(a_vals, a.size)
+    rb, vb = _rows(b_vals, b.size)
+    w = ra.shape[1]
+    assert rb.shape[1] == w
+    c = np.empty(a.size + b.size, dtype=NP_DTYPES[key_type])
+    rc = np.empty((a.size + b.size, w), dtype=np.uint8)
+    _fn("merge_wide", key_type, descending)(_ptr(a), _ptr(ra), a.size, _ptr(b), _ptr(rb), b.size, _ptr(c),
+                                             _ptr(rc), w)
+    return c, rc.view(va.dtype).reshape((a.size + b.size,) + va.shape[1:])
+
+
+def sort_wide(keys, vals, key_type: str, descending: bool = False):
+    """O2 with payloads of any width (rows of `vals`).  Returns sorted copies."""
+    k = as_np(keys, key_type).copy()
+    rv, v = _rows(vals, k.size)
+    rv = rv.copy()
+    rc = _fn("sort_wide", key_type, descending)(_ptr(k), _ptr(rv), k.size, rv.shape[1])
+    if rc != 0:
+        raise MemoryError("oracle_sort_wide: allocation failed")
+    return k, rv.view(v.dtype).reshape(v.shape)
 
 
 def rank_low(x, X, key_type: str, descending: bool = False) -> int:

@@ -28,7 +28,7 @@
  * f32 / f64 with IEEE 754 totalOrder; the desc_*
  * functions use the reversed order (descending keys, still ties to A).
  * Payloads: uint32, travelling with their key; NULL payload pointers mean
- * keys only.  Sizes are int64.  No error paths: callers pass valid sizes.
+ * keys only.  *_wide_*: payloads of any w bytes (structs), same definition.  Sizes are int64.  No error paths: callers pass valid sizes.
  */
 #include <stdint.h>
 #include <stdlib.h>
@@ -136,6 +136,62 @@ void oracle_positions_##SUF(const K *a, int64_t n, const K *b, int64_t m,       
     int64_t i, j;                                                                    \
     for (i = 0; i < n; i++) pos_a[i] = i + oracle_rank_low_##SUF(a[i], b, m);        \
     for (j = 0; j < m; j++) pos_b[j] = j + oracle_rank_high_##SUF(b[j], a, n);       \
+}                                                                                     \
+                                                                                      \
+/* Stable merge with payloads of w bytes each (wide   \
+ * and struct payloads): the same two-pointer definition, the w payload       \
+ * bytes travelling with their key. */                                        \
+void oracle_merge_wide_##SUF(const K *a, const void *va, int64_t n,              \
+                             const K *b, const void *vb, int64_t m,              \
+                             K *c, void *vc, int64_t w)                          \
+{                                                                                     \
+    int64_t i = 0, j = 0, k = 0;                                                     \
+    const char *pa = (const char *)va, *pb = (const char *)vb;                       \
+    char *pc = (char *)vc;                                                           \
+    while (i < n || j < m) {                                                         \
+        if (j >= m || (i < n && LE(a[i], b[j]))) {    /* tie -> A first */           \
+            c[k] = a[i];                                                             \
+            memcpy(pc + k * w, pa + i * w, (size_t)w);                               \
+            i++;                                                                     \
+        } else {                                                                     \
+            c[k] = b[j];                                                             \
+            memcpy(pc + k * w, pb + j * w, (size_t)w);                               \
+            j++;                                                                     \
+        }                                                                            \
+        k++;                                                                         \
+    }                                                                                \
+}                                                                                     \
+                                                                                      \
+/* Bottom-up stable merge sort in place with w-byte payloads. */                    \
+int oracle_sort_wide_##SUF(K *keys, void *vals, int64_t N, int64_t w)              \
+{                                                                                     \
+    K *src = keys, *dst;                                                             \
+    char *vsrc = (char *)vals, *vdst;                                                \
+    int64_t width;                                                                   \
+    if (N <= 1) return 0;                                                            \
+    dst = (K *)malloc((size_t)N * sizeof(K));                                        \
+    vdst = (char *)malloc((size_t)(N * w));                                          \
+    if (!dst || !vdst) { free(dst); free(vdst); return -1; }                         \
+    K *kbuf = dst; char *vbuf = vdst;                                                \
+    for (width = 1; width < N; width *= 2) {                                         \
+        int64_t lo;                                                                  \
+        for (lo = 0; lo < N; lo += 2 * width) {                                      \
+            int64_t mid = lo + width < N ? lo + width : N;                           \
+            int64_t hi = lo + 2 * width < N ? lo + 2 * width : N;                    \
+            oracle_merge_wide_##SUF(src + lo, vsrc + lo * w, mid - lo,               \
+                                    src + mid, vsrc + mid * w, hi - mid,             \
+                                    dst + lo, vdst + lo * w, w);                     \
+        }                                                                            \
+        { K *t = src; src = dst; dst = t; }                                          \
+        { char *t = vsrc; vsrc = vdst; vdst = t; }                                   \
+    }                                                                                \
+    if (src != keys) {                                                               \
+        memcpy(keys, src, (size_t)N * sizeof(K));                                    \
+        memcpy(vals, vsrc, (size_t)(N * w));                                         \
+    }                                                                                \
+    free(kbuf);                                                                      \
+    free(vbuf);                                                                      \
+    return 0;                                                                        \
 }                                                                                     \
                                                                                       \
 /* Positions for a sample of indices only (full-size parity checks). */             \

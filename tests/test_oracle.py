@@ -491,3 +491,43 @@ def test_desc_ranks_vs_linear_count(orc, kt):
         ox = _order_int(x, kt)
         assert orc.rank_low(x, X, kt, descending=True) == sum(_order_int(t, kt) > ox for t in X)
         assert orc.rank_high(x, X, kt, descending=True) == sum(_order_int(t, kt) >= ox for t in X)
+
+
+# --------------------------------------------- wide / struct payloads (f row 2)
+# Pinned by brute force (Python's stable sort of the tagged concatenation,
+# rows gathered by the tags) and by agreement with the uint32-payload oracle
+# when the wide payload is four copies of the uint32 one.
+
+@pytest.mark.parametrize("kt", ["u32", "i64", "f32"])
+@pytest.mark.parametrize("desc", [False, True])
+def test_wide_merge_and_sort_vs_brute_force(orc, kt, desc):
+    rng = np.random.default_rng(17)
+    dt = orc.NP_DTYPES[kt]
+    rdt = np.dtype([("x", "<f8"), ("tag", "<u2"), ("pad", "u1", (5,))])     # a 15-byte struct
+    for trial in range(20):
+        n, m = int(rng.integers(0, 120)), int(rng.integers(0, 120))
+        a = _desc_sorted_input(rng, dt, kt, n, trial % 2 == 0)
+        b = _desc_sorted_input(rng, dt, kt, m, trial % 2 == 0)
+        a = np.array(sorted(a, key=lambda x: _order_int(x, kt), reverse=desc), dtype=dt)
+        b = np.array(sorted(b, key=lambda x: _order_int(x, kt), reverse=desc), dtype=dt)
+        va = np.zeros(n, dtype=rdt); va["x"] = rng.standard_normal(n); va["tag"] = np.arange(n)
+        vb = np.zeros(m, dtype=rdt); vb["x"] = rng.standard_normal(m); vb["tag"] = 1000 + np.arange(m)
+        va["pad"] = rng.integers(0, 256, (n, 5)); vb["pad"] = rng.integers(0, 256, (m, 5))
+        c, vc = orc.merge_wide(a, va, b, vb, kt, descending=desc)
+        rows = list(va) + list(vb)
+        tagged = [(_order_int(k, kt), r) for k, r in zip(list(a) + list(b), range(n + m))]
+        want = sorted(tagged, key=lambda e: e[0], reverse=desc)
+        assert [_order_int(k, kt) for k in c] == [k for k, _ in want]
+        assert vc.tobytes() == b"".join(rows[r].tobytes() for _, r in want)
+        # four copies of a uint32 payload == the uint32 oracle's payload
+        ua, ub = np.arange(n, dtype=np.uint32), np.arange(m, dtype=np.uint32) | np.uint32(1 << 31)
+        _, vc4 = orc.merge_wide(a, np.repeat(ua[:, None], 4, 1), b, np.repeat(ub[:, None], 4, 1), kt,
+                                descending=desc)
+        _, vc1 = orc.merge(a, ua, b, ub, kt, descending=desc)
+        assert vc4.shape == (n + m, 4) and all(np.array_equal(vc4[:, q], vc1) for q in range(4))
+        # sort: stable (tags keep input order among equal keys)
+        keys = np.concatenate([b, a]); rng.shuffle(keys)
+        vals = np.zeros(keys.size, dtype=rdt); vals["tag"] = np.arange(keys.size)
+        sk, sv = orc.sort_wide(keys, vals, kt, descending=desc)
+        order = sorted(range(keys.size), key=lambda i: _order_int(keys[i], kt), reverse=desc)
+        assert sv["tag"].tolist() == order
