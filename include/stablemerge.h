@@ -450,6 +450,122 @@ sm_status mergesort_stable_ex_desc_f32(float *keys, uint32_t *vals, int64_t N, v
 sm_status mergesort_stable_ex_desc_f64(double *keys, uint32_t *vals, int64_t N, void *stream,
                                        const sm_options *opt);
 
+
+/* ---------------------------------------------------------------------
+ * Wide / struct payloads -- SURVEY.md §8(f) row 2.  Each element carries a
+ * payload ROW of val_bytes bytes (1 <= val_bytes <= 4096: 64-bit values,
+ * structs, fixed-size records), moved with its key:
+ *   merge_stable_wide_<K>          as merge_stable_<K>, vals_* = rows
+ *   merge_stable_batched_wide_<K>  as merge_stable_batched_<K>
+ *   mergesort_stable_wide_<K>      as mergesort_stable_<K> (rows sorted in
+ *                                  place with their keys, stable)
+ * and the same for the descending order (_wide_desc_<K>).  Payload
+ * pointers are required (use the uint32 / keys-only calls otherwise).
+ * DEVICE pointers only (host -> SM_EINVAL).  Rows are copied in the widest
+ * word (16/8/4/2/1 bytes) that divides val_bytes and the three payload
+ * pointers' alignment.
+ * Device path: the method runs unchanged with a uint32 INDEX payload (the
+ * position of each element in A||B, or in the sort input), then one gather
+ * kernel moves row idx[k] to output row k.  Scratch: 2 (n+m) uint32
+ * (merge), N uint32 + N rows (sort), stream-ordered as above.
+ * ------------------------------------------------------------------- */
+sm_status merge_stable_wide_u32(const uint32_t *keys_A, const void *vals_A, int64_t n,
+                                const uint32_t *keys_B, const void *vals_B, int64_t m,
+                                uint32_t *out_keys, void *out_vals, int64_t val_bytes, void *stream);
+sm_status merge_stable_wide_i32(const int32_t *keys_A, const void *vals_A, int64_t n,
+                                const int32_t *keys_B, const void *vals_B, int64_t m,
+                                int32_t *out_keys, void *out_vals, int64_t val_bytes, void *stream);
+sm_status merge_stable_wide_i64(const int64_t *keys_A, const void *vals_A, int64_t n,
+                                const int64_t *keys_B, const void *vals_B, int64_t m,
+                                int64_t *out_keys, void *out_vals, int64_t val_bytes, void *stream);
+sm_status merge_stable_wide_u64(const uint64_t *keys_A, const void *vals_A, int64_t n,
+                                const uint64_t *keys_B, const void *vals_B, int64_t m,
+                                uint64_t *out_keys, void *out_vals, int64_t val_bytes, void *stream);
+sm_status merge_stable_wide_f32(const float *keys_A, const void *vals_A, int64_t n,
+                                const float *keys_B, const void *vals_B, int64_t m,
+                                float *out_keys, void *out_vals, int64_t val_bytes, void *stream);
+sm_status merge_stable_wide_f64(const double *keys_A, const void *vals_A, int64_t n,
+                                const double *keys_B, const void *vals_B, int64_t m,
+                                double *out_keys, void *out_vals, int64_t val_bytes, void *stream);
+sm_status merge_stable_wide_desc_u32(const uint32_t *keys_A, const void *vals_A, int64_t n,
+                                     const uint32_t *keys_B, const void *vals_B, int64_t m,
+                                     uint32_t *out_keys, void *out_vals, int64_t val_bytes, void *stream);
+sm_status merge_stable_wide_desc_i32(const int32_t *keys_A, const void *vals_A, int64_t n,
+                                     const int32_t *keys_B, const void *vals_B, int64_t m,
+                                     int32_t *out_keys, void *out_vals, int64_t val_bytes, void *stream);
+sm_status merge_stable_wide_desc_i64(const int64_t *keys_A, const void *vals_A, int64_t n,
+                                     const int64_t *keys_B, const void *vals_B, int64_t m,
+                                     int64_t *out_keys, void *out_vals, int64_t val_bytes, void *stream);
+sm_status merge_stable_wide_desc_u64(const uint64_t *keys_A, const void *vals_A, int64_t n,
+                                     const uint64_t *keys_B, const void *vals_B, int64_t m,
+                                     uint64_t *out_keys, void *out_vals, int64_t val_bytes, void *stream);
+sm_status merge_stable_wide_desc_f32(const float *keys_A, const void *vals_A, int64_t n,
+                                     const float *keys_B, const void *vals_B, int64_t m,
+                                     float *out_keys, void *out_vals, int64_t val_bytes, void *stream);
+sm_status merge_stable_wide_desc_f64(const double *keys_A, const void *vals_A, int64_t n,
+                                     const double *keys_B, const void *vals_B, int64_t m,
+                                     double *out_keys, void *out_vals, int64_t val_bytes, void *stream);
+sm_status merge_stable_batched_wide_u32(const uint32_t *keys_A, const void *vals_A, int64_t n,
+                                        const int64_t *a_offsets, const uint32_t *keys_B, const void *vals_B,
+                                        int64_t m, const int64_t *b_offsets, int64_t S, uint32_t *out_keys,
+                                        void *out_vals, int64_t val_bytes, void *stream);
+sm_status merge_stable_batched_wide_i32(const int32_t *keys_A, const void *vals_A, int64_t n,
+                                        const int64_t *a_offsets, const int32_t *keys_B, const void *vals_B,
+                                        int64_t m, const int64_t *b_offsets, int64_t S, int32_t *out_keys,
+                                        void *out_vals, int64_t val_bytes, void *stream);
+sm_status merge_stable_batched_wide_i64(const int64_t *keys_A, const void *vals_A, int64_t n,
+                                        const int64_t *a_offsets, const int64_t *keys_B, const void *vals_B,
+                                        int64_t m, const int64_t *b_offsets, int64_t S, int64_t *out_keys,
+                                        void *out_vals, int64_t val_bytes, void *stream);
+sm_status merge_stable_batched_wide_u64(const uint64_t *keys_A, const void *vals_A, int64_t n,
+                                        const int64_t *a_offsets, const uint64_t *keys_B, const void *vals_B,
+                                        int64_t m, const int64_t *b_offsets, int64_t S, uint64_t *out_keys,
+                                        void *out_vals, int64_t val_bytes, void *stream);
+sm_status merge_stable_batched_wide_f32(const float *keys_A, const void *vals_A, int64_t n,
+                                        const int64_t *a_offsets, const float *keys_B, const void *vals_B,
+                                        int64_t m, const int64_t *b_offsets, int64_t S, float *out_keys,
+                                        void *out_vals, int64_t val_bytes, void *stream);
+sm_status merge_stable_batched_wide_f64(const double *keys_A, const void *vals_A, int64_t n,
+                                        const int64_t *a_offsets, const double *keys_B, const void *vals_B,
+                                        int64_t m, const int64_t *b_offsets, int64_t S, double *out_keys,
+                                        void *out_vals, int64_t val_bytes, void *stream);
+sm_status merge_stable_batched_wide_desc_u32(const uint32_t *keys_A, const void *vals_A, int64_t n,
+                                             const int64_t *a_offsets, const uint32_t *keys_B, const void *vals_B,
+                                             int64_t m, const int64_t *b_offsets, int64_t S, uint32_t *out_keys,
+                                             void *out_vals, int64_t val_bytes, void *stream);
+sm_status merge_stable_batched_wide_desc_i32(const int32_t *keys_A, const void *vals_A, int64_t n,
+                                             const int64_t *a_offsets, const int32_t *keys_B, const void *vals_B,
+                                             int64_t m, const int64_t *b_offsets, int64_t S, int32_t *out_keys,
+                                             void *out_vals, int64_t val_bytes, void *stream);
+sm_status merge_stable_batched_wide_desc_i64(const int64_t *keys_A, const void *vals_A, int64_t n,
+                                             const int64_t *a_offsets, const int64_t *keys_B, const void *vals_B,
+                                             int64_t m, const int64_t *b_offsets, int64_t S, int64_t *out_keys,
+                                             void *out_vals, int64_t val_bytes, void *stream);
+sm_status merge_stable_batched_wide_desc_u64(const uint64_t *keys_A, const void *vals_A, int64_t n,
+                                             const int64_t *a_offsets, const uint64_t *keys_B, const void *vals_B,
+                                             int64_t m, const int64_t *b_offsets, int64_t S, uint64_t *out_keys,
+                                             void *out_vals, int64_t val_bytes, void *stream);
+sm_status merge_stable_batched_wide_desc_f32(const float *keys_A, const void *vals_A, int64_t n,
+                                             const int64_t *a_offsets, const float *keys_B, const void *vals_B,
+                                             int64_t m, const int64_t *b_offsets, int64_t S, float *out_keys,
+                                             void *out_vals, int64_t val_bytes, void *stream);
+sm_status merge_stable_batched_wide_desc_f64(const double *keys_A, const void *vals_A, int64_t n,
+                                             const int64_t *a_offsets, const double *keys_B, const void *vals_B,
+                                             int64_t m, const int64_t *b_offsets, int64_t S, double *out_keys,
+                                             void *out_vals, int64_t val_bytes, void *stream);
+sm_status mergesort_stable_wide_u32(uint32_t *keys, void *vals, int64_t N, int64_t val_bytes, void *stream);
+sm_status mergesort_stable_wide_i32(int32_t *keys, void *vals, int64_t N, int64_t val_bytes, void *stream);
+sm_status mergesort_stable_wide_i64(int64_t *keys, void *vals, int64_t N, int64_t val_bytes, void *stream);
+sm_status mergesort_stable_wide_u64(uint64_t *keys, void *vals, int64_t N, int64_t val_bytes, void *stream);
+sm_status mergesort_stable_wide_f32(float *keys, void *vals, int64_t N, int64_t val_bytes, void *stream);
+sm_status mergesort_stable_wide_f64(double *keys, void *vals, int64_t N, int64_t val_bytes, void *stream);
+sm_status mergesort_stable_wide_desc_u32(uint32_t *keys, void *vals, int64_t N, int64_t val_bytes, void *stream);
+sm_status mergesort_stable_wide_desc_i32(int32_t *keys, void *vals, int64_t N, int64_t val_bytes, void *stream);
+sm_status mergesort_stable_wide_desc_i64(int64_t *keys, void *vals, int64_t N, int64_t val_bytes, void *stream);
+sm_status mergesort_stable_wide_desc_u64(uint64_t *keys, void *vals, int64_t N, int64_t val_bytes, void *stream);
+sm_status mergesort_stable_wide_desc_f32(float *keys, void *vals, int64_t N, int64_t val_bytes, void *stream);
+sm_status mergesort_stable_wide_desc_f64(double *keys, void *vals, int64_t N, int64_t val_bytes, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

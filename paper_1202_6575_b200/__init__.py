@@ -19,7 +19,11 @@ Floating-point keys (float32 / float64, or int32/int64 bit carriers with
 key_type="f32"/"f64") are ordered by IEEE 754 totalOrder.  descending=True
 uses the reversed key order (inputs and outputs non-increasing; ties still
 keep A first / input order).
-Payloads are 32-bit (int32 or uint32 tensors, same bits).
+Payloads: 1-D 32-bit tensors (int32 / uint32) take the fused path; any
+other payload (64-bit, or rows of any dtype and trailing shape, e.g. a
+(n, 3) float64 tensor or a structured record as uint8 (n, 24)) takes the
+wide-payload path (CUDA tensors only): the same method with an index payload
+and one row gather.
 """
 from __future__ import annotations
 
@@ -64,7 +68,10 @@ for _kt in KEY_TYPES + tuple(f"desc_{k}" for k in KEY_TYPES):
                          (f"merge_stable_batched_{_kt}", [_P, _P, _I, _P, _P, _P, _I, _P, _I, _P, _P, _P]),
                          (f"ranks_stable_{_kt}", [_P, _I, _P, _I, ctypes.c_int32, _P, _P]),
                          (f"mergesort_stable_{_kt}", [_P, _P, _I, _P]),
-                         (f"mergesort_stable_ex_{_kt}", [_P, _P, _I, _P, ctypes.POINTER(SmOptions)])):
+                         (f"mergesort_stable_ex_{_kt}", [_P, _P, _I, _P, ctypes.POINTER(SmOptions)]),
+                         (f"merge_stable_wide_{_kt}", [_P, _P, _I, _P, _P, _I, _P, _P, _I, _P]),
+                         (f"merge_stable_batched_wide_{_kt}", [_P, _P, _I, _P, _P, _P, _I, _P, _I, _P, _P, _I, _P]),
+                         (f"mergesort_stable_wide_{_kt}", [_P, _P, _I, _I, _P])):
         _f = getattr(_lib, _name)
         _f.argtypes = _args
         _f.restype = ctypes.c_int
@@ -122,6 +129,31 @@ def _ptr(t: Optional[torch.Tensor]):
 def _vals_ok(t: Optional[torch.Tensor]):
     if t is not None and t.dtype not in (torch.int32, torch.uint32):
         raise TypeError("payloads must be 32-bit (int32 / uint32)")
+
+
+def _is_wide(*vals) -> bool:
+    """Payload rows other than one 32-bit word: the wide-payload path."""
+    return any(v is not None and (v.dim() != 1 or v.element_size() != 4) for v in vals)
+
+
+def _row_bytes(v: torch.Tensor) -> int:
+    b = v.element_size()
+    for d in v.shape[1:]:
+        b *= d
+    return b
+
+
+def _wide_args(a_vals, b_vals):
+    if a_vals is None or b_vals is None:
+        raise ValueError("payloads must be given for both inputs or neither")
+    if a_vals.dtype != b_vals.dtype or a_vals.shape[1:] != b_vals.shape[1:]:
+        raise ValueError("A and B payload rows must have the same dtype and shape")
+    if not (a_vals.is_cuda and b_vals.is_cuda):
+        raise ValueError("wide payloads take CUDA tensors")
+    vb = _row_bytes(a_vals)
+    if vb < 1 or vb > 4096:
+        raise ValueError("payload rows must be 1..4096 bytes")
+    return vb
 
 
 def _sym(op: str, kt: str, descending: bool) -> str:
@@ -186,8 +218,19 @@ def merge_stable(a_keys: torch.Tensor, a_vals: Optional[torch.Tensor], b_keys: t
     _key_type(b_keys, kt)
     if (a_vals is None) != (b_vals is None):
         raise ValueError("payloads must be given for both inputs or neither")
-    _vals_ok(a_vals); _vals_ok(b_vals)
     n, m = a_keys.numel(), b_keys.numel()
+    if _is_wide(a_vals, b_vals):
+        vb = _wide_args(a_vals, b_vals)
+        if out_keys is None:
+            out_keys = torch.empty(n + m, dtype=a_keys.dtype, device=a_keys.device)
+        if out_vals is None:
+            out_vals = torch.empty((n + m,) + tuple(a_vals.shape[1:]), dtype=a_vals.dtype, device=a_keys.device)
+        s = _stream_for(a_keys, stream)
+        fn = _sym("merge_stable_wide", kt, descending)
+        _check(getattr(_lib, fn)(_ptr(a_keys), _ptr(a_vals), n, _ptr(b_keys), _ptr(b_vals), m, _ptr(out_keys),
+                                 _ptr(out_vals), vb, s), fn)
+        return out_keys, out_vals
+    _vals_ok(a_vals); _vals_ok(b_vals)
     if out_keys is None:
         out_keys = torch.empty(n + m, dtype=a_keys.dtype, device=a_keys.device)
     if a_vals is not None and out_vals is None:
@@ -219,7 +262,9 @@ def merge_stable_batched(a_keys: torch.Tensor, a_vals: Optional[torch.Tensor], a
     _key_type(b_keys, kt)
     if (a_vals is None) != (b_vals is None):
         raise ValueError("payloads must be given for both inputs or neither")
-    _vals_ok(a_vals); _vals_ok(b_vals)
+    wide = _is_wide(a_vals, b_vals)
+    if not wide:
+        _vals_ok(a_vals); _vals_ok(b_vals)
     if a_offsets.dtype != torch.int64 or b_offsets.dtype != torch.int64:
         raise TypeError("offsets must be int64")
     if a_offsets.numel() != b_offsets.numel() or a_offsets.numel() < 1:
@@ -228,9 +273,17 @@ def merge_stable_batched(a_keys: torch.Tensor, a_vals: Optional[torch.Tensor], a
     n, m = a_keys.numel(), b_keys.numel()
     if out_keys is None:
         out_keys = torch.empty(n + m, dtype=a_keys.dtype, device=a_keys.device)
+    s = _stream_for(a_keys, stream)
+    if wide:
+        vb = _wide_args(a_vals, b_vals)
+        if out_vals is None:
+            out_vals = torch.empty((n + m,) + tuple(a_vals.shape[1:]), dtype=a_vals.dtype, device=a_keys.device)
+        fn = _sym("merge_stable_batched_wide", kt, descending)
+        _check(getattr(_lib, fn)(_ptr(a_keys), _ptr(a_vals), n, _ptr(a_offsets), _ptr(b_keys), _ptr(b_vals), m,
+                                 _ptr(b_offsets), S, _ptr(out_keys), _ptr(out_vals), vb, s), fn)
+        return out_keys, out_vals
     if a_vals is not None and out_vals is None:
         out_vals = torch.empty(n + m, dtype=a_vals.dtype, device=a_keys.device)
-    s = _stream_for(a_keys, stream)
     fn = _sym("merge_stable_batched", kt, descending)
     _check(getattr(_lib, fn)(_ptr(a_keys), _ptr(a_vals), n, _ptr(a_offsets), _ptr(b_keys), _ptr(b_vals), m,
                              _ptr(b_offsets), S, _ptr(out_keys), _ptr(out_vals), s), fn)
@@ -254,11 +307,18 @@ def mergesort_stable(keys: torch.Tensor, vals: Optional[torch.Tensor] = None, *,
                      stream=None, pdl: bool = True, descending: bool = False):
     """Stable merge sort in place (equal keys keep input order).  Returns (keys, vals)."""
     kt = _key_type(keys, key_type)
-    _vals_ok(vals)
     N = keys.numel()
+    s = _stream_for(keys, stream)
+    if _is_wide(vals):
+        if vals.shape[0] != N:
+            raise ValueError("vals must have one row per key")
+        vb = _wide_args(vals, vals)
+        fn = _sym("mergesort_stable_wide", kt, descending)
+        _check(getattr(_lib, fn)(_ptr(keys), _ptr(vals), N, vb, s), fn)
+        return keys, vals
+    _vals_ok(vals)
     if vals is not None and vals.numel() != N:
         raise ValueError("vals must have the same length as keys")
-    s = _stream_for(keys, stream)
     args = (_ptr(keys), _ptr(vals), N, s)
     if pdl:
         fn = _sym("mergesort_stable", kt, descending)

@@ -606,6 +606,33 @@ __global__ void __launch_bounds__(K2Layout<K, HAS_V, NC, VT, STAGES, MAXT>::THRE
     }
 }
 
+// ------------------------------------------------------- wide payloads
+// SURVEY.md §8(f) row 2 (wide and struct payloads): the merge / sort runs
+// with a uint32 INDEX payload (each element's position in A||B, or in the
+// sort input), then k_gather_rows moves payload row idx[k] to output row k
+// in W-byte words (consecutive outputs mostly come from consecutive rows of
+// one input, so both sides stay coalesced).
+__global__ void __launch_bounds__(256) k_iota(uint32_t* __restrict__ out, int64_t count) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = (uint32_t)i;
+}
+
+template <typename W>
+__global__ void __launch_bounds__(256) k_gather_rows(const uint32_t* __restrict__ idx, const W* __restrict__ PA,
+                                                     int64_t n, const W* __restrict__ PB, W* __restrict__ out,
+                                                     int64_t rows, int wpr) {
+    const uint64_t total = (uint64_t)rows * (uint64_t)wpr;
+    const bool small = total < (1ull << 32);
+    for (uint64_t w = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; w < total;
+         w += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t r = small ? (uint64_t)((uint32_t)w / (uint32_t)wpr) : w / (uint64_t)wpr;
+        const int c = (int)(w - r * (uint64_t)wpr);
+        const int64_t src = (int64_t)__ldg(idx + r);
+        const W* row = src < n ? PA + src * wpr : PB + (src - n) * wpr;
+        st_stream(out + w, __ldg(row + c));
+    }
+}
+
 // ------------------------------------------------------- rank queries
 // rank_low (high = 0) or rank_high (high = 1) of a batch of keys in one
 // sorted array: the primitive of rows a1/a2 on its own,

@@ -755,6 +755,137 @@ static sm_status sort_entry(K* keys, uint32_t* vals, int64_t N, void* stream, co
     return s != SM_OK ? s : (r1 != SM_OK ? r1 : r2);
 }
 
+// ------------------------------------------------------------ wide payloads
+// payload rows of vbytes bytes (any width: structs,
+// 64-bit, ...).  The method runs unchanged with a uint32 index payload (the
+// position of each element in A||B), then one gather moves the rows.
+// Device pointers only.
+static const int64_t WIDE_MAX_BYTES = 4096;
+
+static sm_status gather_rows(const uint32_t* idx, const void* PA, int64_t n, const void* PB, void* out, int64_t rows,
+                             int64_t vbytes, cudaStream_t st) {
+    if (rows == 0) return SM_OK;
+    const uintptr_t al = (uintptr_t)PA | (uintptr_t)PB | (uintptr_t)out | (uintptr_t)vbytes;
+    const int64_t blocks = std::min<int64_t>(ceil_div(rows * vbytes / 4 + 1, 256), 148 * 16);
+    const unsigned grid = (unsigned)std::max<int64_t>(1, blocks);
+#define SM_GATHER(W)                                                                                            \
+    k_gather_rows<W><<<grid, 256, 0, st>>>(idx, (const W*)PA, n, (const W*)PB, (W*)out, rows,                 \
+                                           (int)(vbytes / (int64_t)sizeof(W)))
+    if ((al & 15) == 0) SM_GATHER(uint4);
+    else if ((al & 7) == 0) SM_GATHER(uint2);
+    else if ((al & 3) == 0) SM_GATHER(uint32_t);
+    else if ((al & 1) == 0) SM_GATHER(uint16_t);
+    else SM_GATHER(uint8_t);
+#undef SM_GATHER
+    return check_launch("k_gather_rows");
+}
+
+static sm_status iota(uint32_t* out, int64_t count, cudaStream_t st) {
+    if (count == 0) return SM_OK;
+    k_iota<<<(unsigned)std::min<int64_t>(ceil_div(count, 256), 148 * 16), 256, 0, st>>>(out, count);
+    return check_launch("k_iota");
+}
+
+static sm_status wide_check(int64_t vbytes, std::initializer_list<const void*> ptrs) {
+    if (vbytes < 1 || vbytes > WIDE_MAX_BYTES) return fail_inval("payload row bytes must be in [1, 4096]");
+    for (const void* p : ptrs)
+        if (is_host_ptr(p)) return fail_inval("the wide-payload calls take device pointers only");
+    return SM_OK;
+}
+
+template <typename K>
+static sm_status merge_wide_entry(const K* A, const void* vA, int64_t n, const K* B, const void* vB, int64_t m, K* C,
+                                  void* vC, int64_t vbytes, void* stream) {
+    g_launches = 0;
+    g_err[0] = 0;
+    cudaStream_t st = (cudaStream_t)stream;
+    if (n < 0 || m < 0) return fail_inval("negative size");
+    if ((n && (!A || !vA)) || (m && (!B || !vB)) || ((n + m) && (!C || !vC)))
+        return fail_inval("NULL pointer with nonzero size");
+    if (n + m > (int64_t)INT_MAX) return fail_inval("n + m > 2^31 - 1");
+    sm_status s = wide_check(vbytes, {A, B, C, vA, vB, vC});
+    if (s != SM_OK) return s;
+    const size_t kb = sizeof(K), cb = (size_t)(n + m), vb = (size_t)vbytes;
+    if (overlaps(C, cb * kb, A, n * kb) || overlaps(C, cb * kb, B, m * kb) || overlaps(C, cb * kb, vA, n * vb) ||
+        overlaps(C, cb * kb, vB, m * vb) || overlaps(vC, cb * vb, A, n * kb) || overlaps(vC, cb * vb, B, m * kb) ||
+        overlaps(vC, cb * vb, vA, n * vb) || overlaps(vC, cb * vb, vB, m * vb) || overlaps(C, cb * kb, vC, cb * vb))
+        return SM_EALIAS;
+    if (n + m == 0) return SM_OK;
+    keep_pool(st);
+    uint32_t* idx = nullptr;
+    s = dalloc(&idx, 2 * (n + m), st);
+    if (s != SM_OK) return s;
+    const int64_t NV = tile_nv((int)sizeof(K), true);
+    s = iota(idx, n + m, st);
+    if (s == SM_OK)
+        s = merge_device<K>(A, idx, n, B, idx + n, m, C, idx + n + m, st, std::max<int64_t>(1, ceil_div(n, NV / 2)),
+                            std::max<int64_t>(1, ceil_div(m, NV / 2)), true);
+    if (s == SM_OK) s = gather_rows(idx + n + m, vA, n, vB, vC, n + m, vbytes, st);
+    dfree(idx, st);
+    return s;
+}
+
+template <typename K>
+static sm_status batch_wide_entry(const K* A, const void* vA, int64_t n, const int64_t* a_off, const K* B,
+                                  const void* vB, int64_t m, const int64_t* b_off, int64_t S, K* C, void* vC,
+                                  int64_t vbytes, void* stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    g_launches = 0;
+    g_err[0] = 0;
+    if (n < 0 || m < 0 || S < 0) return fail_inval("negative size");
+    if ((n && !vA) || (m && !vB) || ((n + m) && !vC)) return fail_inval("NULL payload pointer with nonzero size");
+    if (n + m > (int64_t)INT_MAX) return fail_inval("n + m > 2^31 - 1");
+    sm_status s = wide_check(vbytes, {vA, vB, vC});
+    if (s != SM_OK) return s;
+    const size_t kb = sizeof(K), cb = (size_t)(n + m), vb = (size_t)vbytes;
+    if (overlaps(vC, cb * vb, A, n * kb) || overlaps(vC, cb * vb, B, m * kb) || overlaps(vC, cb * vb, vA, n * vb) ||
+        overlaps(vC, cb * vb, vB, m * vb) || overlaps(C, cb * kb, vC, cb * vb) || overlaps(C, cb * kb, vA, n * vb) ||
+        overlaps(C, cb * kb, vB, m * vb))
+        return SM_EALIAS;
+    if (S == 0 || n + m == 0)
+        return batch_entry<K>(A, nullptr, n, a_off, B, nullptr, m, b_off, S, C, nullptr, stream);
+    keep_pool(st);
+    uint32_t* idx = nullptr;
+    s = dalloc(&idx, 2 * (n + m), st);
+    if (s != SM_OK) return s;
+    s = iota(idx, n + m, st);
+    const int64_t l0 = g_launches;
+    if (s == SM_OK) s = batch_entry<K>(A, idx, n, a_off, B, idx + n, m, b_off, S, C, idx + n + m, stream);
+    g_launches += l0;
+    if (s == SM_OK) s = gather_rows(idx + n + m, vA, n, vB, vC, n + m, vbytes, st);
+    dfree(idx, st);
+    return s;
+}
+
+template <typename K>
+static sm_status sort_wide_entry(K* keys, void* vals, int64_t N, int64_t vbytes, void* stream) {
+    g_launches = 0;
+    g_err[0] = 0;
+    cudaStream_t st = (cudaStream_t)stream;
+    if (N < 0) return fail_inval("negative size");
+    if (N && (!keys || !vals)) return fail_inval("NULL pointer with nonzero size");
+    if (N > (int64_t)INT_MAX) return fail_inval("N > 2^31 - 1");
+    sm_status s = wide_check(vbytes, {keys, vals});
+    if (s != SM_OK) return s;
+    if (overlaps(keys, N * sizeof(K), vals, (size_t)(N * vbytes))) return SM_EALIAS;
+    if (N <= 1) return SM_OK;
+    keep_pool(st);
+    uint32_t* idx = nullptr;
+    char* tmp = nullptr;
+    s = dalloc(&idx, N, st);
+    if (s == SM_OK) s = dalloc(&tmp, N * vbytes, st);
+    if (s == SM_OK) s = iota(idx, N, st);
+    if (s == SM_OK) s = sort_device<K>(keys, idx, N, st, true);
+    if (s == SM_OK) s = gather_rows(idx, vals, N, nullptr, tmp, N, vbytes, st);
+    if (s == SM_OK) {
+        cudaError_t e = cudaMemcpyAsync(vals, tmp, (size_t)(N * vbytes), cudaMemcpyDeviceToDevice, st);
+        if (e != cudaSuccess) s = fail_cuda(e, "cudaMemcpyAsync");
+    }
+    dfree(tmp, st);
+    dfree(idx, st);
+    return s;
+}
+
 }  // namespace sm
 
 // ================================================================ C ABI
@@ -797,6 +928,22 @@ extern "C" {
     sm_status mergesort_stable_ex_##SUF(C* keys, uint32_t* vals, int64_t N, void* stream,                      \
                                         const sm_options* opt) {                                               \
         return sm::sort_entry<K>((K*)keys, vals, N, stream, opt);                                               \
+    }                                                                                                           \
+    sm_status merge_stable_wide_##SUF(const C* keys_A, const void* vals_A, int64_t n, const C* keys_B,         \
+                                      const void* vals_B, int64_t m, C* out_keys, void* out_vals,             \
+                                      int64_t val_bytes, void* stream) {                                       \
+        return sm::merge_wide_entry<K>((const K*)keys_A, vals_A, n, (const K*)keys_B, vals_B, m, (K*)out_keys, \
+                                       out_vals, val_bytes, stream);                                           \
+    }                                                                                                           \
+    sm_status merge_stable_batched_wide_##SUF(const C* keys_A, const void* vals_A, int64_t n,                  \
+                                              const int64_t* a_offsets, const C* keys_B, const void* vals_B,   \
+                                              int64_t m, const int64_t* b_offsets, int64_t S, C* out_keys,     \
+                                              void* out_vals, int64_t val_bytes, void* stream) {               \
+        return sm::batch_wide_entry<K>((const K*)keys_A, vals_A, n, a_offsets, (const K*)keys_B, vals_B, m,   \
+                                       b_offsets, S, (K*)out_keys, out_vals, val_bytes, stream);               \
+    }                                                                                                           \
+    sm_status mergesort_stable_wide_##SUF(C* keys, void* vals, int64_t N, int64_t val_bytes, void* stream) {   \
+        return sm::sort_wide_entry<K>((K*)keys, vals, N, val_bytes, stream);                                    \
     }
 
 SM_DEFINE_ABI(u32, uint32_t, uint32_t)

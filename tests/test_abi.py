@@ -34,7 +34,9 @@ def test_header_declares_entry_points():
                   "merge_stable_batched", "ranks_stable"):
             assert f"{f}_{kt}" in names
             assert f"{f}_desc_{kt}" in names          # descending order
-    assert len(names) == 91
+        for f in ("merge_stable_wide", "merge_stable_batched_wide", "mergesort_stable_wide"):
+            assert f"{f}_{kt}" in names and f"{f}_desc_{kt}" in names   # wide payloads (row 2)
+    assert len(names) == 127
 
 
 def test_library_exports_every_declared_symbol(sm):
