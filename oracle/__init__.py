@@ -29,8 +29,11 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "oracle.c")
 _LIB = os.path.join(_HERE, "liboracle.so")
 
+# u128: unsigned 128-bit keys as (lo, hi) little-endian uint64 pairs (the
+# bytes of a C unsigned __int128); torch carrier: int64 tensors of shape (N, 2)
+U128 = np.dtype([("lo", "<u8"), ("hi", "<u8")])
 NP_DTYPES = {"u32": np.uint32, "i32": np.int32, "i64": np.int64, "u64": np.uint64, "f32": np.float32,
-             "f64": np.float64}
+             "f64": np.float64, "u128": U128}
 _C_KEY = {"u32": ctypes.c_uint32, "i32": ctypes.c_int32, "i64": ctypes.c_int64, "u64": ctypes.c_uint64,
           "f32": ctypes.c_float, "f64": ctypes.c_double}
 
@@ -56,10 +59,15 @@ def lib():
             getattr(_lib, f"oracle_merge_{kt}").restype = None
             getattr(_lib, f"oracle_sort_{kt}").argtypes = [P, P, I]
             getattr(_lib, f"oracle_sort_{kt}").restype = ctypes.c_int
-            getattr(_lib, f"oracle_rank_low_{kt}").argtypes = [_C_KEY[kt.replace("desc_", "")], P, I]
-            getattr(_lib, f"oracle_rank_low_{kt}").restype = I
-            getattr(_lib, f"oracle_rank_high_{kt}").argtypes = [_C_KEY[kt.replace("desc_", "")], P, I]
-            getattr(_lib, f"oracle_rank_high_{kt}").restype = I
+            if not kt.endswith("u128"):
+                getattr(_lib, f"oracle_rank_low_{kt}").argtypes = [_C_KEY[kt.replace("desc_", "")], P, I]
+                getattr(_lib, f"oracle_rank_low_{kt}").restype = I
+                getattr(_lib, f"oracle_rank_high_{kt}").argtypes = [_C_KEY[kt.replace("desc_", "")], P, I]
+                getattr(_lib, f"oracle_rank_high_{kt}").restype = I
+            else:
+                for f in ("low", "high"):
+                    getattr(_lib, f"oracle_rank_{f}_ptr_{kt}").argtypes = [P, P, I]
+                    getattr(_lib, f"oracle_rank_{f}_ptr_{kt}").restype = I
             getattr(_lib, f"oracle_merge_wide_{kt}").argtypes = [P, P, I, P, P, I, P, P, I]
             getattr(_lib, f"oracle_merge_wide_{kt}").restype = None
             getattr(_lib, f"oracle_sort_wide_{kt}").argtypes = [P, P, I, I]
@@ -83,9 +91,17 @@ def as_np(x, key_type: str = None):
     if hasattr(x, "detach"):
         x = x.detach().cpu().contiguous().numpy()
     x = np.ascontiguousarray(x)
+    if key_type == "u128":
+        return np.ascontiguousarray(x).view(np.uint64).reshape(-1, 2).view(U128).reshape(-1)
     if key_type is not None:
         x = x.view(NP_DTYPES[key_type])
     return x
+
+
+def u128_ints(x):
+    """u128 keys -> Python ints (high << 64 | low)."""
+    a = as_np(x, "u128")
+    return [(int(h) << 64) | int(lo) for lo, h in zip(a["lo"], a["hi"])]
 
 
 def vals_np(x):
@@ -158,12 +174,24 @@ def sort_wide(keys, vals, key_type: str, descending: bool = False):
     return k, rv.view(v.dtype).reshape(v.shape)
 
 
+def _rank_u128(which, x, X, descending):
+    X = as_np(X, "u128")
+    xa = np.array([(int(x) & ((1 << 64) - 1), int(x) >> 64)], dtype=U128)
+    return int(getattr(lib(), f"oracle_rank_{which}_ptr_{'desc_' if descending else ''}u128")(_ptr(xa), _ptr(X),
+                                                                                              X.size))
+
+
 def rank_low(x, X, key_type: str, descending: bool = False) -> int:
+    """rank_low(x, X); u128 keys x as a Python int."""
+    if key_type == "u128":
+        return _rank_u128("low", x, X, descending)
     X = as_np(X, key_type)
     return int(_fn("rank_low", key_type, descending)(NP_DTYPES[key_type](x).item(), _ptr(X), X.size))
 
 
 def rank_high(x, X, key_type: str, descending: bool = False) -> int:
+    if key_type == "u128":
+        return _rank_u128("high", x, X, descending)
     X = as_np(X, key_type)
     return int(_fn("rank_high", key_type, descending)(NP_DTYPES[key_type](x).item(), _ptr(X), X.size))
 

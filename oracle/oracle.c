@@ -25,7 +25,8 @@
  *                    C[i + rank_low(A[i],B)], B[j] to C[j + rank_high(B[j],A)].
  *
  * Keys: u32 / i32 / i64 / u64 with the natural (unsigned or signed) order;
- * f32 / f64 with IEEE 754 totalOrder; the desc_*
+ * f32 / f64 with IEEE 754 totalOrder; u128 unsigned
+ * 128-bit (= (high, low) 64-bit tuples, lexicographic); the desc_*
  * functions use the reversed order (descending keys, still ties to A).
  * Payloads: uint32, travelling with their key; NULL payload pointers mean
  * keys only.  *_wide_*: payloads of any w bytes (structs), same definition.  Sizes are int64.  No error paths: callers pass valid sizes.
@@ -222,6 +223,17 @@ DEFINE_ORACLE(i64, int64_t, LE_INT, LT_INT)
 DEFINE_ORACLE(u64, uint64_t, LE_INT, LT_INT)
 DEFINE_ORACLE(f32, float, LE_F32, LT_F32)
 DEFINE_ORACLE(f64, double, LE_F64, LT_F64)
+/* 128-bit keys (128-bit keys and (key, tie) tuples):
+ * unsigned, i.e. the lexicographic order of (high 64 bits, low 64 bits). */
+typedef unsigned __int128 u128_t;
+DEFINE_ORACLE(u128, u128_t, LE_INT, LT_INT)
+DEFINE_ORACLE(desc_u128, u128_t, LE_D_INT, LT_D_INT)
+/* the rank functions with the key passed by pointer (no 128-bit scalars in ctypes) */
+int64_t oracle_rank_low_ptr_u128(const u128_t *x, const u128_t *X, int64_t len) { return oracle_rank_low_u128(*x, X, len); }
+int64_t oracle_rank_high_ptr_u128(const u128_t *x, const u128_t *X, int64_t len) { return oracle_rank_high_u128(*x, X, len); }
+int64_t oracle_rank_low_ptr_desc_u128(const u128_t *x, const u128_t *X, int64_t len) { return oracle_rank_low_desc_u128(*x, X, len); }
+int64_t oracle_rank_high_ptr_desc_u128(const u128_t *x, const u128_t *X, int64_t len) { return oracle_rank_high_desc_u128(*x, X, len); }
+
 DEFINE_ORACLE(desc_u32, uint32_t, LE_D_INT, LT_D_INT)
 DEFINE_ORACLE(desc_i32, int32_t, LE_D_INT, LT_D_INT)
 DEFINE_ORACLE(desc_i64, int64_t, LE_D_INT, LT_D_INT)

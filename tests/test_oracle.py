@@ -531,3 +531,50 @@ def test_wide_merge_and_sort_vs_brute_force(orc, kt, desc):
         sk, sv = orc.sort_wide(keys, vals, kt, descending=desc)
         order = sorted(range(keys.size), key=lambda i: _order_int(keys[i], kt), reverse=desc)
         assert sv["tag"].tolist() == order
+
+
+# ------------------------------------------------- 128-bit keys (f row 2)
+# u128 keys = (high, low) 64-bit tuples in lexicographic order; pinned by
+# Python's stable sort of the tagged concatenation on Python ints / tuples.
+
+def _u128_input(rng, n, few):
+    hi = rng.integers(0, 3, n, dtype=np.uint64) if few else rng.integers(0, 2**64 - 1, n, dtype=np.uint64,
+                                                                           endpoint=True)
+    lo = rng.integers(0, 4, n, dtype=np.uint64) if few else rng.integers(0, 2**64 - 1, n, dtype=np.uint64,
+                                                                           endpoint=True)
+    return [(int(h) << 64) | int(l) for h, l in zip(hi, lo)]
+
+
+def _u128_arr(ints):
+    from oracle import U128
+    a = np.empty(len(ints), dtype=U128)
+    a["lo"] = [x & (2**64 - 1) for x in ints]
+    a["hi"] = [x >> 64 for x in ints]
+    return a
+
+
+@pytest.mark.parametrize("desc", [False, True])
+def test_u128_merge_sort_ranks_vs_python(orc, desc):
+    rng = np.random.default_rng(19)
+    for trial in range(30):
+        n, m = int(rng.integers(0, 150)), int(rng.integers(0, 150))
+        a = sorted(_u128_input(rng, n, trial % 2 == 0), reverse=desc)
+        b = sorted(_u128_input(rng, m, trial % 2 == 0), reverse=desc)
+        va = np.arange(n, dtype=np.uint32)
+        vb = (np.arange(m) | (1 << 31)).astype(np.uint32)
+        c, vc = orc.merge(_u128_arr(a), va, _u128_arr(b), vb, "u128", descending=desc)
+        want = sorted([(k, int(v)) for k, v in zip(a, va)] + [(k, int(v)) for k, v in zip(b, vb)],
+                      key=lambda e: e[0], reverse=desc)
+        assert orc.u128_ints(c) == [k for k, _ in want]
+        assert vc.tolist() == [v for _, v in want]
+        # tuples: the same order as Python's lexicographic tuple order
+        assert sorted([(k >> 64, k & (2**64 - 1)) for k in a], reverse=desc) == [(k >> 64, k & (2**64 - 1)) for k in a]
+        keys = a + b
+        rng.shuffle(keys)
+        sk, sv = orc.sort(_u128_arr(keys), np.arange(len(keys), dtype=np.uint32), "u128", descending=desc)
+        assert sv.tolist() == sorted(range(len(keys)), key=lambda i: keys[i], reverse=desc)
+        for x in (a[::9] + _u128_input(rng, 3, True)):
+            lt = sum((t > x) if desc else (t < x) for t in b)
+            le = sum((t >= x) if desc else (t <= x) for t in b)
+            assert orc.rank_low(x, _u128_arr(b), "u128", descending=desc) == lt
+            assert orc.rank_high(x, _u128_arr(b), "u128", descending=desc) == le
