@@ -64,6 +64,15 @@
 extern "C" {
 #endif
 
+/* An unsigned 128-bit key (the _u128 entry points): value = hi * 2^64 + lo,
+ * i.e. (hi, lo) tuples in lexicographic order -- "(key, tie)" pairs.  Same
+ * bytes as a little-endian unsigned __int128.  Arrays of sm_u128 keys must be
+ * 16-byte aligned (SM_EINVAL otherwise). */
+typedef struct {
+    uint64_t lo;
+    uint64_t hi;
+} sm_u128;
+
 typedef enum {
     SM_OK = 0,
     SM_EINVAL = 1,
@@ -565,6 +574,70 @@ sm_status mergesort_stable_wide_desc_i64(int64_t *keys, void *vals, int64_t N, i
 sm_status mergesort_stable_wide_desc_u64(uint64_t *keys, void *vals, int64_t N, int64_t val_bytes, void *stream);
 sm_status mergesort_stable_wide_desc_f32(float *keys, void *vals, int64_t N, int64_t val_bytes, void *stream);
 sm_status mergesort_stable_wide_desc_f64(double *keys, void *vals, int64_t N, int64_t val_bytes, void *stream);
+
+
+/* ---------------------------------------------------------------------
+ * 128-bit keys -- SURVEY.md §8(f) row 2 (128-bit keys, (key, tie) tuples):
+ * every call above for sm_u128 keys (unsigned, = lexicographic (hi, lo)),
+ * ascending and descending, uint32 / wide payloads.  Same contracts; the
+ * key arrays must be 16-byte aligned.  Device path: the same kernels with
+ * 16-byte keys (the C++ merge over the order view; 32 radix digits in the
+ * block sort).
+ * ------------------------------------------------------------------- */
+sm_status merge_stable_u128(const sm_u128 *keys_A, const uint32_t *vals_A, int64_t n,
+                            const sm_u128 *keys_B, const uint32_t *vals_B, int64_t m,
+                            sm_u128 *out_keys, uint32_t *out_vals, void *stream);
+sm_status merge_stable_batched_u128(const sm_u128 *keys_A, const uint32_t *vals_A, int64_t n,
+                                    const int64_t *a_offsets, const sm_u128 *keys_B, const uint32_t *vals_B,
+                                    int64_t m, const int64_t *b_offsets, int64_t S, sm_u128 *out_keys,
+                                    uint32_t *out_vals, void *stream);
+sm_status ranks_stable_u128(const sm_u128 *X, int64_t len, const sm_u128 *keys, int64_t nkeys, int32_t high,
+                              int64_t *out, void *stream);
+sm_status mergesort_stable_u128(sm_u128 *keys, uint32_t *vals, int64_t N, void *stream);
+sm_status merge_stable_ex_u128(const sm_u128 *keys_A, const uint32_t *vals_A, int64_t n,
+                               const sm_u128 *keys_B, const uint32_t *vals_B, int64_t m,
+                               sm_u128 *out_keys, uint32_t *out_vals, void *stream,
+                               const sm_options *opt);
+sm_status merge_plan_ex_u128(const sm_u128 *keys_A, int64_t n, const sm_u128 *keys_B, int64_t m,
+                             int64_t p_A, int64_t p_B, int64_t *xbar, int64_t *ybar, int64_t *tasks,
+                             void *stream);
+sm_status mergesort_stable_ex_u128(sm_u128 *keys, uint32_t *vals, int64_t N, void *stream,
+                                   const sm_options *opt);
+sm_status merge_stable_desc_u128(const sm_u128 *keys_A, const uint32_t *vals_A, int64_t n,
+                                 const sm_u128 *keys_B, const uint32_t *vals_B, int64_t m,
+                                 sm_u128 *out_keys, uint32_t *out_vals, void *stream);
+sm_status merge_stable_ex_desc_u128(const sm_u128 *keys_A, const uint32_t *vals_A, int64_t n,
+                                    const sm_u128 *keys_B, const uint32_t *vals_B, int64_t m,
+                                    sm_u128 *out_keys, uint32_t *out_vals, void *stream,
+                                    const sm_options *opt);
+sm_status merge_plan_ex_desc_u128(const sm_u128 *keys_A, int64_t n, const sm_u128 *keys_B, int64_t m,
+                                  int64_t p_A, int64_t p_B, int64_t *xbar, int64_t *ybar, int64_t *tasks,
+                                  void *stream);
+sm_status merge_stable_batched_desc_u128(const sm_u128 *keys_A, const uint32_t *vals_A, int64_t n,
+                                         const int64_t *a_offsets, const sm_u128 *keys_B, const uint32_t *vals_B,
+                                         int64_t m, const int64_t *b_offsets, int64_t S, sm_u128 *out_keys,
+                                         uint32_t *out_vals, void *stream);
+sm_status ranks_stable_desc_u128(const sm_u128 *X, int64_t len, const sm_u128 *keys, int64_t nkeys, int32_t high,
+                                   int64_t *out, void *stream);
+sm_status mergesort_stable_desc_u128(sm_u128 *keys, uint32_t *vals, int64_t N, void *stream);
+sm_status mergesort_stable_ex_desc_u128(sm_u128 *keys, uint32_t *vals, int64_t N, void *stream,
+                                        const sm_options *opt);
+sm_status merge_stable_wide_u128(const sm_u128 *keys_A, const void *vals_A, int64_t n,
+                                 const sm_u128 *keys_B, const void *vals_B, int64_t m,
+                                 sm_u128 *out_keys, void *out_vals, int64_t val_bytes, void *stream);
+sm_status merge_stable_wide_desc_u128(const sm_u128 *keys_A, const void *vals_A, int64_t n,
+                                      const sm_u128 *keys_B, const void *vals_B, int64_t m,
+                                      sm_u128 *out_keys, void *out_vals, int64_t val_bytes, void *stream);
+sm_status merge_stable_batched_wide_u128(const sm_u128 *keys_A, const void *vals_A, int64_t n,
+                                         const int64_t *a_offsets, const sm_u128 *keys_B, const void *vals_B,
+                                         int64_t m, const int64_t *b_offsets, int64_t S, sm_u128 *out_keys,
+                                         void *out_vals, int64_t val_bytes, void *stream);
+sm_status merge_stable_batched_wide_desc_u128(const sm_u128 *keys_A, const void *vals_A, int64_t n,
+                                              const int64_t *a_offsets, const sm_u128 *keys_B, const void *vals_B,
+                                              int64_t m, const int64_t *b_offsets, int64_t S, sm_u128 *out_keys,
+                                              void *out_vals, int64_t val_bytes, void *stream);
+sm_status mergesort_stable_wide_u128(sm_u128 *keys, void *vals, int64_t N, int64_t val_bytes, void *stream);
+sm_status mergesort_stable_wide_desc_u128(sm_u128 *keys, void *vals, int64_t N, int64_t val_bytes, void *stream);
 
 #ifdef __cplusplus
 }

@@ -16,7 +16,10 @@ the host (the library stages them; the binding then synchronises the stream
 so host results are ready on return).  Unsigned keys: pass torch.uint32 /
 torch.uint64 tensors, or int32/int64 carriers with key_type="u32"/"u64".
 Floating-point keys (float32 / float64, or int32/int64 bit carriers with
-key_type="f32"/"f64") are ordered by IEEE 754 totalOrder.  descending=True
+key_type="f32"/"f64") are ordered by IEEE 754 totalOrder.  128-bit keys
+(key_type="u128", always explicit): int64 tensors of shape (N, 2) holding
+(lo, hi) words of the unsigned value hi * 2^64 + lo, i.e. (hi, lo) tuples
+in lexicographic order -- "(key, tie)" pairs.  descending=True
 uses the reversed key order (inputs and outputs non-increasing; ties still
 keep A first / input order).
 Payloads: 1-D 32-bit tensors (int32 / uint32) take the fused path; any
@@ -42,13 +45,13 @@ if not os.path.exists(LIB_PATH):
 
 _lib = ctypes.CDLL(LIB_PATH)
 
-KEY_TYPES = ("u32", "i32", "i64", "u64", "f32", "f64")
-_BYTES = {"u32": 4, "i32": 4, "i64": 8, "u64": 8, "f32": 4, "f64": 8}
+KEY_TYPES = ("u32", "i32", "i64", "u64", "f32", "f64", "u128")
+_BYTES = {"u32": 4, "i32": 4, "i64": 8, "u64": 8, "f32": 4, "f64": 8, "u128": 16}
 _DTYPE_KT = {torch.int32: "i32", torch.int64: "i64", torch.uint32: "u32", torch.uint64: "u64",
              torch.float32: "f32", torch.float64: "f64"}
 _CARRIER = {"u32": (torch.int32, torch.uint32), "i32": (torch.int32,), "i64": (torch.int64,),
             "u64": (torch.int64, torch.uint64), "f32": (torch.float32, torch.int32),
-            "f64": (torch.float64, torch.int64)}
+            "f64": (torch.float64, torch.int64), "u128": (torch.int64,)}
 
 SM_OK, SM_EINVAL, SM_EALIAS, SM_ENOMEM, SM_ECUDA = range(5)
 SM_FLAG_NO_PDL = 1
@@ -110,12 +113,28 @@ def _key_type(t: torch.Tensor, key_type: Optional[str]) -> str:
     if key_type is None:
         if t.dtype not in _DTYPE_KT:
             raise TypeError(f"unsupported key dtype {t.dtype}")
+        if t.dim() != 1:
+            raise ValueError("multi-dimensional key tensor: pass key_type='u128' for 128-bit keys")
         return _DTYPE_KT[t.dtype]
     if key_type not in KEY_TYPES:
         raise ValueError(f"key_type must be one of {KEY_TYPES}")
     if t.dtype not in _CARRIER[key_type]:
         raise TypeError(f"key_type {key_type} cannot be carried in {t.dtype}")
     return key_type
+
+
+def _count(t: torch.Tensor, kt: str) -> int:
+    """Number of keys in a key tensor (u128: rows of an (N, 2) int64 tensor)."""
+    if kt == "u128":
+        if t.dim() != 2 or t.shape[1] != 2:
+            raise ValueError("u128 keys are int64 tensors of shape (N, 2) = (lo, hi) words")
+        return t.shape[0]
+    return t.numel()
+
+
+def _empty_keys(count: int, like: torch.Tensor, kt: str) -> torch.Tensor:
+    shape = (count, 2) if kt == "u128" else (count,)
+    return torch.empty(shape, dtype=like.dtype, device=like.device)
 
 
 def _ptr(t: Optional[torch.Tensor]):
@@ -218,11 +237,11 @@ def merge_stable(a_keys: torch.Tensor, a_vals: Optional[torch.Tensor], b_keys: t
     _key_type(b_keys, kt)
     if (a_vals is None) != (b_vals is None):
         raise ValueError("payloads must be given for both inputs or neither")
-    n, m = a_keys.numel(), b_keys.numel()
+    n, m = _count(a_keys, kt), _count(b_keys, kt)
     if _is_wide(a_vals, b_vals):
         vb = _wide_args(a_vals, b_vals)
         if out_keys is None:
-            out_keys = torch.empty(n + m, dtype=a_keys.dtype, device=a_keys.device)
+            out_keys = _empty_keys(n + m, a_keys, kt)
         if out_vals is None:
             out_vals = torch.empty((n + m,) + tuple(a_vals.shape[1:]), dtype=a_vals.dtype, device=a_keys.device)
         s = _stream_for(a_keys, stream)
@@ -232,10 +251,10 @@ def merge_stable(a_keys: torch.Tensor, a_vals: Optional[torch.Tensor], b_keys: t
         return out_keys, out_vals
     _vals_ok(a_vals); _vals_ok(b_vals)
     if out_keys is None:
-        out_keys = torch.empty(n + m, dtype=a_keys.dtype, device=a_keys.device)
+        out_keys = _empty_keys(n + m, a_keys, kt)
     if a_vals is not None and out_vals is None:
         out_vals = torch.empty(n + m, dtype=a_vals.dtype, device=a_keys.device)
-    if out_keys.numel() != n + m or (out_vals is not None and out_vals.numel() != n + m):
+    if _count(out_keys, kt) != n + m or (out_vals is not None and out_vals.numel() != n + m):
         raise ValueError("output length must be n + m")
     s = _stream_for(a_keys, stream)
     opt = _options(p_A, p_B, block, (0 if pdl else SM_FLAG_NO_PDL) | (SM_FLAG_MERGE_PATH if merge_path else 0))
@@ -270,9 +289,9 @@ def merge_stable_batched(a_keys: torch.Tensor, a_vals: Optional[torch.Tensor], a
     if a_offsets.numel() != b_offsets.numel() or a_offsets.numel() < 1:
         raise ValueError("a_offsets and b_offsets must both hold S + 1 entries")
     S = a_offsets.numel() - 1
-    n, m = a_keys.numel(), b_keys.numel()
+    n, m = _count(a_keys, kt), _count(b_keys, kt)
     if out_keys is None:
-        out_keys = torch.empty(n + m, dtype=a_keys.dtype, device=a_keys.device)
+        out_keys = _empty_keys(n + m, a_keys, kt)
     s = _stream_for(a_keys, stream)
     if wide:
         vb = _wide_args(a_vals, b_vals)
@@ -296,10 +315,11 @@ def ranks_stable(X: torch.Tensor, keys: torch.Tensor, high: bool = False, *, key
     X.  CUDA tensors; returns int64 ranks."""
     kt = _key_type(X, key_type)
     _key_type(keys, kt)
-    out = torch.empty(keys.numel(), dtype=torch.int64, device=keys.device)
+    nk = _count(keys, kt)
+    out = torch.empty(nk, dtype=torch.int64, device=keys.device)
     s = _stream_for(X, stream)
     fn = _sym("ranks_stable", kt, descending)
-    _check(getattr(_lib, fn)(_ptr(X), X.numel(), _ptr(keys), keys.numel(), int(bool(high)), _ptr(out), s), fn)
+    _check(getattr(_lib, fn)(_ptr(X), _count(X, kt), _ptr(keys), nk, int(bool(high)), _ptr(out), s), fn)
     return out
 
 
@@ -307,7 +327,7 @@ def mergesort_stable(keys: torch.Tensor, vals: Optional[torch.Tensor] = None, *,
                      stream=None, pdl: bool = True, descending: bool = False):
     """Stable merge sort in place (equal keys keep input order).  Returns (keys, vals)."""
     kt = _key_type(keys, key_type)
-    N = keys.numel()
+    N = _count(keys, kt)
     s = _stream_for(keys, stream)
     if _is_wide(vals):
         if vals.shape[0] != N:
@@ -346,7 +366,7 @@ def merge_plan(a_keys: torch.Tensor, b_keys: torch.Tensor, p_A: int, p_B: Option
     tasks = torch.empty((p_A + p_B, 6), dtype=torch.int64, device=dev)
     s = _stream_for(a_keys, stream)
     fn = _sym("merge_plan_ex", kt, descending)
-    _check(getattr(_lib, fn)(_ptr(a_keys), a_keys.numel(), _ptr(b_keys), b_keys.numel(), p_A, p_B, _ptr(xbar),
+    _check(getattr(_lib, fn)(_ptr(a_keys), _count(a_keys, kt), _ptr(b_keys), _count(b_keys, kt), p_A, p_B, _ptr(xbar),
                              _ptr(ybar), _ptr(tasks), s), fn)
     return xbar, ybar, tasks
 

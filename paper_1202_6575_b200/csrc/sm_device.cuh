@@ -43,30 +43,35 @@ struct KeyOrd;
 template <> struct KeyOrd<uint32_t> {
     using U = uint32_t;
     static constexpr bool FLOAT = false;
+    static constexpr bool PTX = true;    // inline-PTX merge/split steps exist
     __device__ __host__ __forceinline__ static U to(uint32_t x) { return x; }
     __device__ __host__ __forceinline__ static uint32_t from(U u) { return u; }
 };
 template <> struct KeyOrd<int32_t> {
     using U = uint32_t;
     static constexpr bool FLOAT = false;
+    static constexpr bool PTX = true;    // inline-PTX merge/split steps exist
     __device__ __host__ __forceinline__ static U to(int32_t x) { return (U)x ^ 0x80000000u; }
     __device__ __host__ __forceinline__ static int32_t from(U u) { return (int32_t)(u ^ 0x80000000u); }
 };
 template <> struct KeyOrd<uint64_t> {
     using U = uint64_t;
     static constexpr bool FLOAT = false;
+    static constexpr bool PTX = true;    // inline-PTX merge/split steps exist
     __device__ __host__ __forceinline__ static U to(uint64_t x) { return x; }
     __device__ __host__ __forceinline__ static uint64_t from(U u) { return u; }
 };
 template <> struct KeyOrd<int64_t> {
     using U = uint64_t;
     static constexpr bool FLOAT = false;
+    static constexpr bool PTX = true;    // inline-PTX merge/split steps exist
     __device__ __host__ __forceinline__ static U to(int64_t x) { return (U)x ^ 0x8000000000000000ull; }
     __device__ __host__ __forceinline__ static int64_t from(U u) { return (int64_t)(u ^ 0x8000000000000000ull); }
 };
 template <> struct KeyOrd<float> {
     using U = uint32_t;
     static constexpr bool FLOAT = true;
+    static constexpr bool PTX = false;
     __device__ __host__ __forceinline__ static U to(float x) {
         U b;
         memcpy(&b, &x, 4);
@@ -82,6 +87,7 @@ template <> struct KeyOrd<float> {
 template <> struct KeyOrd<double> {
     using U = uint64_t;
     static constexpr bool FLOAT = true;
+    static constexpr bool PTX = false;
     __device__ __host__ __forceinline__ static U to(double x) {
         U b;
         memcpy(&b, &x, 8);
@@ -93,6 +99,17 @@ template <> struct KeyOrd<double> {
         memcpy(&x, &b, 8);
         return x;
     }
+};
+// Unsigned 128-bit keys (128-bit keys, (key, tie)
+// tuples = (high, low) words in lexicographic order): native compares, no
+// PTX fast path (the C++ merge over the order view, which is the identity).
+typedef unsigned __int128 u128;
+template <> struct KeyOrd<u128> {
+    using U = u128;
+    static constexpr bool FLOAT = false;
+    static constexpr bool PTX = false;
+    __device__ __host__ __forceinline__ static U to(u128 x) { return x; }
+    __device__ __host__ __forceinline__ static u128 from(U u) { return u; }
 };
 
 // Descending order: the method for an arbitrary
@@ -108,6 +125,7 @@ struct Desc {
 template <typename B> struct KeyOrd<Desc<B>> {
     using U = typename KeyOrd<B>::U;
     static constexpr bool FLOAT = KeyOrd<B>::FLOAT;
+    static constexpr bool PTX = KeyOrd<B>::PTX;
     __device__ __host__ __forceinline__ static U to(Desc<B> x) { return (U)~KeyOrd<B>::to(x.v); }
     __device__ __host__ __forceinline__ static Desc<B> from(U u) { return Desc<B>(KeyOrd<B>::from((U)~u)); }
 };
@@ -132,11 +150,15 @@ __device__ __forceinline__ K& raw_ref(K& k) { return k; }
 template <typename B>
 __device__ __forceinline__ B& raw_ref(Desc<B>& k) { return k.v; }
 
-// Read-only global load of a key.
+// Read-only global load of a key (u128: one 16-byte load; 16-byte aligned).
 template <typename K>
 __device__ __forceinline__ K ldg_key(const K* p) { return __ldg(p); }
+__device__ __forceinline__ u128 ldg_key(const u128* p) {
+    const ulonglong2 v = __ldg((const ulonglong2*)p);
+    return ((u128)v.y << 64) | (u128)v.x;
+}
 template <typename B>
-__device__ __forceinline__ Desc<B> ldg_key(const Desc<B>* p) { return Desc<B>(__ldg((const B*)p)); }
+__device__ __forceinline__ Desc<B> ldg_key(const Desc<B>* p) { return Desc<B>(ldg_key((const B*)p)); }
 
 // ---------------------------------------------------------------------------
 // Geometry of one launch: one merge (mode 0, S = 1), one merge-sort round
@@ -294,10 +316,17 @@ template <typename T>
 __device__ __forceinline__ T ld_stream(const T* p) { return __ldcs(p); }
 template <typename T>
 __device__ __forceinline__ void st_stream(T* p, T v) { __stcs(p, v); }
+__device__ __forceinline__ u128 ld_stream(const u128* p) {
+    const ulonglong2 v = __ldcs((const ulonglong2*)p);
+    return ((u128)v.y << 64) | (u128)v.x;
+}
+__device__ __forceinline__ void st_stream(u128* p, u128 v) {
+    __stcs((ulonglong2*)p, make_ulonglong2((unsigned long long)v, (unsigned long long)(v >> 64)));
+}
 template <typename B>
-__device__ __forceinline__ Desc<B> ld_stream(const Desc<B>* p) { return Desc<B>(__ldcs((const B*)p)); }
+__device__ __forceinline__ Desc<B> ld_stream(const Desc<B>* p) { return Desc<B>(ld_stream((const B*)p)); }
 template <typename B>
-__device__ __forceinline__ void st_stream(Desc<B>* p, Desc<B> v) { __stcs((B*)p, v.v); }
+__device__ __forceinline__ void st_stream(Desc<B>* p, Desc<B> v) { st_stream((B*)p, v.v); }
 
 // Programmatic dependent launch (sm_90+): wait for the producer grid's
 // memory to be visible; a no-op when the launch was not programmatic.

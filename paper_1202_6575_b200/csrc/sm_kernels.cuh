@@ -424,8 +424,8 @@ __device__ __forceinline__ bool k2_compute(const K* sk, const uint32_t* sv, cons
     if (cnt <= 0) return true;
     if (td.la > 0 && td.lb > 0) {
         // cases (b), (c), (d): stable merge (row a7), ties to A (R17)
-        if constexpr (KeyOrd<K>::FLOAT) {
-            // floating-point keys: the same merge on the order view (C++ path)
+        if constexpr (!KeyOrd<K>::PTX) {
+            // floating-point and 128-bit keys: the same merge on the order view (C++ path)
             using U = typename KeyOrd<K>::U;
             const K* a = sk + td.a_s;
             const K* b = sk + td.b_s;
@@ -555,12 +555,14 @@ __global__ void __launch_bounds__(K2Layout<K, HAS_V, NC, VT, STAGES, MAXT>::THRE
                 }
                 bulk_commit();
             }
-            for (int e = lane; e < nt * (EK + EV); e += 32) {
-                const int k = e / (EK + EV), r = e % (EK + EV);
-                const TaskDesc& t = desc[s * MAXT + k];
-                const int L = t.la + t.lb;
-                if (r < EK) store_edge<K>(C + t.off, sk, t.ob, L, r);
-                else if (HAS_V) store_edge<uint32_t>(vC + t.off, sv, t.obv, L, r - EK);
+            if constexpr (EK + EV > 0) {                 // (16-byte keys alone have no edges)
+                for (int e = lane; e < nt * (EK + EV); e += 32) {
+                    const int k = e / (EK + EV), r = e % (EK + EV);
+                    const TaskDesc& t = desc[s * MAXT + k];
+                    const int L = t.la + t.lb;
+                    if (r < EK) store_edge<K>(C + t.off, sk, t.ob, L, r);
+                    else if (HAS_V) store_edge<uint32_t>(vC + t.off, sv, t.obv, L, r - EK);
+                }
             }
             bulk_wait_read<0>();                       // this lane's bulk stores have read the stage
             __syncwarp();
@@ -816,7 +818,7 @@ struct K3Layout {
     static constexpr int OFF_ROW = OFF_V + (HAS_V ? 2 * R * 4 : 0);
     static constexpr int OFF_W = OFF_ROW + NT * ROW * 4; // warp totals [NW][ND]
     static constexpr int OFF_RED = OFF_W + NW * ND * 4;
-    static constexpr int SMEM = OFF_RED + NW * 8 + 16;
+    static constexpr int SMEM = OFF_RED + NW * (int)sizeof(U) + 16;
 };
 
 // 16 packed 8-bit counters in two 64-bit words: field d of (lo, hi).
@@ -865,7 +867,15 @@ __global__ void __launch_bounds__(NT) k_block_sort(const K* __restrict__ in, con
         const U first = ku0[0];
         for (int e = tid; e < len; e += NT) diff |= ku0[e] ^ first;
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) diff |= __shfl_xor_sync(0xffffffffu, diff, o);
+        for (int o = 16; o > 0; o >>= 1) {
+            if constexpr (sizeof(U) == 16) {
+                const uint64_t lo = __shfl_xor_sync(0xffffffffu, (uint64_t)diff, o);
+                const uint64_t hi = __shfl_xor_sync(0xffffffffu, (uint64_t)(diff >> 64), o);
+                diff |= ((U)hi << 64) | (U)lo;
+            } else {
+                diff |= __shfl_xor_sync(0xffffffffu, diff, o);
+            }
+        }
         if (lane == 0) red[w] = diff;
         __syncthreads();
         diff = 0;

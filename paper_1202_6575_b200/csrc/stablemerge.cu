@@ -15,6 +15,7 @@
 #include <type_traits>
 #include <vector>
 #include <climits>
+#include <initializer_list>
 
 #include "stablemerge.h"
 #include "sm_kernels.cuh"
@@ -42,8 +43,11 @@ struct K2Geo {
 template <typename K, bool HAS_V>
 struct K2Shape {
     static constexpr int bytes = (int)sizeof(K) + (HAS_V ? 4 : 0);
-    using type = typename std::conditional<bytes <= 4, K2Geo<352, 23, 3, 2>,
-                 typename std::conditional<bytes <= 8, K2Geo<256, 15, 3>, K2Geo<256, 15, 4>>::type>::type;
+    using type = typename std::conditional<
+        bytes <= 4, K2Geo<352, 23, 3, 2>,
+        typename std::conditional<bytes <= 8, K2Geo<256, 15, 3>,
+                                  typename std::conditional<bytes <= 12, K2Geo<256, 15, 4>,
+                                                            K2Geo<256, 11, 3>>::type>::type>::type;
 };
 // Tasks packed per ring stage at most.
 constexpr int K2_MAXT = 16;
@@ -51,7 +55,19 @@ constexpr int K2_MAXT = 16;
 // Tile capacity NV (largest task) and default block size of a layout.
 static int64_t tile_nv(int key_bytes, bool has_v) {
     if (key_bytes == 4) return has_v ? K2Shape<uint32_t, true>::type::NV : K2Shape<uint32_t, false>::type::NV;
+    if (key_bytes == 16) return has_v ? K2Shape<u128, true>::type::NV : K2Shape<u128, false>::type::NV;
     return has_v ? K2Shape<uint64_t, true>::type::NV : K2Shape<uint64_t, false>::type::NV;
+}
+
+// 128-bit keys are loaded as one 16-byte word: their arrays must be aligned.
+template <typename K>
+static bool keys_aligned(std::initializer_list<const void*> ptrs) {
+    if constexpr (sizeof(K) >= 16) {
+        for (const void* p : ptrs)
+            if ((uintptr_t)p & 15) return false;
+    }
+    (void)ptrs;
+    return true;
 }
 static int64_t tile_t(int key_bytes, bool has_v) { return tile_nv(key_bytes, has_v) / 2; }
 // K3 shape: one run of R = K3_NT * K3_IPT elements per CTA (radix block sort).
@@ -481,6 +497,7 @@ static sm_status merge_entry(const K* A, const uint32_t* vA, int64_t n, const K*
     cudaStream_t st = (cudaStream_t)stream;
     if (n < 0 || m < 0) return fail_inval("negative size");
     if ((n && !A) || (m && !B) || ((n + m) && !C)) return fail_inval("NULL key pointer with nonzero size");
+    if (!keys_aligned<K>({A, B, C})) return fail_inval("128-bit keys must be 16-byte aligned");
     if (vC) {
         if ((n && !vA) || (m && !vB)) return fail_inval("payload pointers must be all set or all NULL");
     } else if (vA || vB) {
@@ -562,6 +579,7 @@ static sm_status batch_entry(const K* A, const uint32_t* vA, int64_t n, const in
     if (S > (int64_t)(INT_MAX / 8)) return fail_inval("too many segments");
     if (n + m > (int64_t)INT_MAX) return fail_inval("n + m > 2^31 - 1");
     if ((n && !A) || (m && !B) || ((n + m) && !C)) return fail_inval("NULL key pointer with nonzero size");
+    if (!keys_aligned<K>({A, B, C})) return fail_inval("128-bit keys must be 16-byte aligned");
     if (S && (!a_off || !b_off)) return fail_inval("NULL segment offsets");
     if (vC) {
         if ((n && !vA) || (m && !vB)) return fail_inval("payload pointers must be all set or all NULL");
@@ -624,6 +642,7 @@ static sm_status ranks_entry(const K* X, int64_t len, const K* keys, int64_t nke
     cudaStream_t st = (cudaStream_t)stream;
     if (len < 0 || nkeys < 0) return fail_inval("negative size");
     if ((len && !X) || (nkeys && (!keys || !out))) return fail_inval("NULL pointer with nonzero size");
+    if (!keys_aligned<K>({X, keys})) return fail_inval("128-bit keys must be 16-byte aligned");
     if (nkeys == 0) return SM_OK;
     if (is_host_ptr(X) || is_host_ptr(keys) || is_host_ptr(out)) return fail_inval("device pointers only");
     k_rank_keys<K><<<(unsigned)ceil_div(nkeys, 256), 256, 0, st>>>(X, len, keys, nkeys, high ? 1 : 0, out);
@@ -644,6 +663,7 @@ static sm_status plan_entry(const K* A, int64_t n, const K* B, int64_t m, int64_
     cudaStream_t st = (cudaStream_t)stream;
     if (n < 0 || m < 0 || pA < 1 || pB < 1) return fail_inval("sizes / block counts");
     if ((n && !A) || (m && !B) || !xbar || !ybar || !tasks) return fail_inval("NULL pointer");
+    if (!keys_aligned<K>({A, B})) return fail_inval("128-bit keys must be 16-byte aligned");
     if (n + m > (int64_t)INT_MAX || pA > INT_MAX / 4 || pB > INT_MAX / 4) return fail_inval("too large");
     if (is_host_ptr(A) || is_host_ptr(B) || is_host_ptr(xbar) || is_host_ptr(ybar) || is_host_ptr(tasks))
         return fail_inval("merge_plan_ex takes device pointers only");
@@ -739,6 +759,7 @@ static sm_status sort_entry(K* keys, uint32_t* vals, int64_t N, void* stream, co
     cudaStream_t st = (cudaStream_t)stream;
     if (N < 0) return fail_inval("negative size");
     if (N && !keys) return fail_inval("NULL key pointer with nonzero size");
+    if (!keys_aligned<K>({keys})) return fail_inval("128-bit keys must be 16-byte aligned");
     if (N > (int64_t)INT_MAX) return fail_inval("N > 2^31 - 1");
     if (opt && opt->sort_run && opt->sort_run != R_SORT) return fail_inval("sort_run must equal the block-sort tile");
     if (overlaps(keys, N * sizeof(K), vals, N * 4)) return SM_EALIAS;
@@ -802,6 +823,7 @@ static sm_status merge_wide_entry(const K* A, const void* vA, int64_t n, const K
     if (n < 0 || m < 0) return fail_inval("negative size");
     if ((n && (!A || !vA)) || (m && (!B || !vB)) || ((n + m) && (!C || !vC)))
         return fail_inval("NULL pointer with nonzero size");
+    if (!keys_aligned<K>({A, B, C})) return fail_inval("128-bit keys must be 16-byte aligned");
     if (n + m > (int64_t)INT_MAX) return fail_inval("n + m > 2^31 - 1");
     sm_status s = wide_check(vbytes, {A, B, C, vA, vB, vC});
     if (s != SM_OK) return s;
@@ -864,6 +886,7 @@ static sm_status sort_wide_entry(K* keys, void* vals, int64_t N, int64_t vbytes,
     cudaStream_t st = (cudaStream_t)stream;
     if (N < 0) return fail_inval("negative size");
     if (N && (!keys || !vals)) return fail_inval("NULL pointer with nonzero size");
+    if (!keys_aligned<K>({keys})) return fail_inval("128-bit keys must be 16-byte aligned");
     if (N > (int64_t)INT_MAX) return fail_inval("N > 2^31 - 1");
     sm_status s = wide_check(vbytes, {keys, vals});
     if (s != SM_OK) return s;
@@ -958,6 +981,8 @@ SM_DEFINE_ABI(desc_i64, sm::Desc<int64_t>, int64_t)
 SM_DEFINE_ABI(desc_u64, sm::Desc<uint64_t>, uint64_t)
 SM_DEFINE_ABI(desc_f32, sm::Desc<float>, float)
 SM_DEFINE_ABI(desc_f64, sm::Desc<double>, double)
+SM_DEFINE_ABI(u128, sm::u128, sm_u128)
+SM_DEFINE_ABI(desc_u128, sm::Desc<sm::u128>, sm_u128)
 
 int64_t sm_tile_capacity(int32_t key_bytes, int32_t has_vals) {
     return sm::tile_nv(key_bytes, has_vals != 0);

@@ -105,6 +105,8 @@ KEY_TYPES = {
     "u64": (torch.int64, "u", 8),
     "f32": (torch.int32, "f", 4),
     "f64": (torch.int64, "f", 8),
+    # unsigned 128-bit: int64 carrier of shape (N, 2) = (lo, hi) words
+    "u128": (torch.int64, "u128", 16),
 }
 
 # float bit patterns of the "special" distribution: +-0, +-inf, +-NaN (quiet,
@@ -128,11 +130,11 @@ class MergeInput:
 
     @property
     def n(self) -> int:
-        return self.a_keys.numel()
+        return self.a_keys.shape[0]
 
     @property
     def m(self) -> int:
-        return self.b_keys.numel()
+        return self.b_keys.shape[0]
 
     def to(self, device) -> "MergeInput":
         f = lambda t: None if t is None else t.to(device)
@@ -147,7 +149,7 @@ class SortInput:
 
     @property
     def N(self) -> int:
-        return self.keys.numel()
+        return self.keys.shape[0]
 
 
 def source_payloads(n: int, m: int, device="cpu"):
@@ -197,10 +199,45 @@ def _keys(dist: str, key_type: str, seed: int, stream: int, count: int, device) 
     return v.to(dtype)
 
 
+def u128_keys(dist: str, seed: int, stream: int, count: int, device="cpu") -> torch.Tensor:
+    """(count, 2) int64 = (lo, hi) words of unsigned 128-bit keys:
+    "full" both words uniform; "tuple:K" hi uniform in [0, K) and lo in
+    [0, 4) -- (key, tie) pairs with many equal keys and equal ties;
+    "equal" all zero."""
+    if dist == "equal":
+        return torch.zeros(count, 2, dtype=torch.int64, device=device)
+    r_lo = splitmix_stream(seed, stream, count, device)
+    r_hi = splitmix_stream(seed, 16 * STREAM_BERN + 12 + stream, count, device)
+    if dist == "full":
+        lo, hi = r_lo, r_hi
+    elif dist.startswith("tuple:"):
+        lo, hi = bounded(r_lo, 4), bounded(r_hi, int(dist.split(":", 1)[1]))
+    else:
+        raise ValueError(dist)
+    return torch.stack([lo, hi], 1).contiguous()
+
+
+def u128_order(keys: torch.Tensor, descending: bool = False, seg: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """Permutation sorting (segment, hi, lo) unsigned, stably (library sorts)."""
+    idx = torch.sort(_order_key(keys[:, 0], "u"), stable=True, descending=descending).indices
+    idx = idx[torch.sort(_order_key(keys[idx, 1], "u"), stable=True, descending=descending).indices]
+    if seg is not None:
+        idx = idx[torch.sort(seg[idx], stable=True).indices]
+    return idx
+
+
 def merge_input(n: int, m: int, key_type: str, dist: str, seed: int, payload: bool = True,
                 device="cpu", descending: bool = False) -> MergeInput:
     """Two independently sorted arrays A (n) and B (m) of `dist` keys
     (non-increasing when `descending`)."""
+    if key_type == "u128":
+        a = u128_keys(dist, seed, STREAM_A, n, device)
+        b = u128_keys(dist, seed, STREAM_B, m, device)
+        a, b = a[u128_order(a, descending)], b[u128_order(b, descending)]
+        av = bv = None
+        if payload:
+            av, bv = source_payloads(n, m, device)
+        return MergeInput(key_type, a, b, av, bv)
     _, order, _ = KEY_TYPES[key_type]
     a = sort_bits(_keys(dist, key_type, seed, STREAM_A, n, device), order)
     b = sort_bits(_keys(dist, key_type, seed, STREAM_B, m, device), order)
@@ -213,7 +250,8 @@ def merge_input(n: int, m: int, key_type: str, dist: str, seed: int, payload: bo
 
 
 def sort_input(N: int, key_type: str, dist: str, seed: int, payload: bool = True, device="cpu") -> SortInput:
-    keys = _keys(dist, key_type, seed, STREAM_SORT, N, device)
+    keys = u128_keys(dist, seed, STREAM_SORT, N, device) if key_type == "u128" else \
+        _keys(dist, key_type, seed, STREAM_SORT, N, device)
     vals = torch.arange(N, dtype=torch.int32, device=device) if payload else None
     return SortInput(key_type, keys, vals)
 
@@ -234,11 +272,11 @@ class BatchInput:
 
     @property
     def n(self) -> int:
-        return self.a_keys.numel()
+        return self.a_keys.shape[0]
 
     @property
     def m(self) -> int:
-        return self.b_keys.numel()
+        return self.b_keys.shape[0]
 
     def to(self, device) -> "BatchInput":
         f = lambda t: None if t is None else t.to(device)
@@ -255,8 +293,11 @@ def _segmented(S: int, mean: int, key_type: str, dist: str, seed: int, stream: i
     off = torch.zeros(S + 1, dtype=torch.int64, device=device)
     off[1:] = torch.cumsum(lens, 0)
     total = int(off[-1].item())
-    keys = _keys(dist, key_type, seed, stream, total, device)
     seg = torch.repeat_interleave(torch.arange(S, device=device), lens)
+    if key_type == "u128":
+        keys = u128_keys(dist, seed, stream, total, device)
+        return keys[u128_order(keys, descending, seg)], off
+    keys = _keys(dist, key_type, seed, stream, total, device)
     # order by (segment, key): a stable sort by key, then a stable sort by segment
     idx = torch.sort(_order_key(keys, order), stable=True, descending=descending).indices
     idx = idx[torch.sort(seg[idx], stable=True).indices]

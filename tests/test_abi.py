@@ -29,14 +29,14 @@ def sm():
 
 def test_header_declares_entry_points():
     names = declared_functions()
-    for kt in ("u32", "i32", "i64", "u64", "f32", "f64"):
+    for kt in ("u32", "i32", "i64", "u64", "f32", "f64", "u128"):
         for f in ("merge_stable", "mergesort_stable", "merge_stable_ex", "merge_plan_ex", "mergesort_stable_ex",
                   "merge_stable_batched", "ranks_stable"):
             assert f"{f}_{kt}" in names
             assert f"{f}_desc_{kt}" in names          # descending order
         for f in ("merge_stable_wide", "merge_stable_batched_wide", "mergesort_stable_wide"):
             assert f"{f}_{kt}" in names and f"{f}_desc_{kt}" in names   # wide payloads (row 2)
-    assert len(names) == 127
+    assert len(names) == 147
 
 
 def test_library_exports_every_declared_symbol(sm):
