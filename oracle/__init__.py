@@ -92,6 +92,8 @@ def as_np(x, key_type: str = None):
         x = x.detach().cpu().contiguous().numpy()
     x = np.ascontiguousarray(x)
     if key_type == "u128":
+        if x.dtype == U128:
+            return x
         return np.ascontiguousarray(x).view(np.uint64).reshape(-1, 2).view(U128).reshape(-1)
     if key_type is not None:
         x = x.view(NP_DTYPES[key_type])

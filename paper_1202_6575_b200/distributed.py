@@ -45,19 +45,25 @@ class Piece(NamedTuple):
 
 
 class CudaOps:
-    """The two local primitives on this rank's GPU (the library's kernels)."""
+    """The local primitives on this rank's GPU (the library's kernels)."""
 
-    def __init__(self, key_type: Optional[str] = None):
-        from . import merge_stable, ranks_stable
-        self._merge, self._ranks, self.key_type = merge_stable, ranks_stable, key_type
+    def __init__(self, key_type: Optional[str] = None, descending: bool = False):
+        from . import merge_stable, mergesort_stable, ranks_stable
+        self._merge, self._ranks, self._sort = merge_stable, ranks_stable, mergesort_stable
+        self.key_type, self.descending = key_type, descending
 
     def ranks(self, X: torch.Tensor, keys: torch.Tensor, high: bool) -> torch.Tensor:
         if X.numel() == 0 or keys.numel() == 0:
             return torch.zeros(keys.numel(), dtype=torch.int64, device=keys.device)
-        return self._ranks(X, keys, high, key_type=self.key_type)
+        return self._ranks(X, keys, high, key_type=self.key_type, descending=self.descending)
 
     def merge(self, ak, av, bk, bv):
-        return self._merge(ak, av, bk, bv, key_type=self.key_type)
+        return self._merge(ak, av, bk, bv, key_type=self.key_type, descending=self.descending)
+
+    def sort(self, keys, vals):
+        keys = keys.clone()
+        vals = None if vals is None else vals.clone()
+        return self._sort(keys, vals, key_type=self.key_type, descending=self.descending)
 
 
 def block_starts(length: int, p: int) -> List[int]:
@@ -75,33 +81,35 @@ def block_of(k: int, length: int, p: int) -> int:
     return k // (q + 1) if k < big else (k - big) // q + r
 
 
-def plan_tasks(n: int, m: int, p: int, xbar: Sequence[int], ybar: Sequence[int]):
-    """Steps 3-4 (L310-340; readings R1, R8): the 2p tasks as
-    (owner, a0, a1, b0, b1), A-side task q then B-side task q for every q."""
-    x, y = block_starts(n, p), block_starts(m, p)
+def plan_tasks(n: int, m: int, p: int, xbar: Sequence[int], ybar: Sequence[int], pB: Optional[int] = None):
+    """Steps 3-4 (L310-340; readings R1, R8): the p_A + p_B tasks as
+    (owner, a0, a1, b0, b1), A-side task q then B-side task q for every q
+    (p_A = p, p_B = pB or p: reading R7)."""
+    pA, pB = p, (p if pB is None else pB)
+    x, y = block_starts(n, pA), block_starts(m, pB)
     tasks = []
-    for i in range(p):
+    for i in range(pA):
         if xbar[i] == xbar[i + 1]:
             t = (x[i], x[i + 1], xbar[i], xbar[i])
         else:
-            j = block_of(xbar[i], m, p)
+            j = block_of(xbar[i], m, pB)
             if xbar[i] == y[j]:
                 t = (x[i], ybar[j], xbar[i], xbar[i])
-            elif block_of(xbar[i + 1], m, p) == j:
+            elif block_of(xbar[i + 1], m, pB) == j:
                 t = (x[i], x[i + 1], xbar[i], xbar[i + 1])
             elif xbar[i + 1] == y[j + 1]:
                 t = (x[i], x[i + 1], xbar[i], y[j + 1])
             else:
                 t = (x[i], ybar[j + 1], xbar[i], y[j + 1])
         tasks.append((i,) + t)
-    for j in range(p):
+    for j in range(pB):
         if ybar[j] == ybar[j + 1]:
             t = (ybar[j], ybar[j], y[j], y[j + 1])
         else:
-            i = block_of(ybar[j], n, p)
+            i = block_of(ybar[j], n, pA)
             if ybar[j] == x[i]:
                 t = (ybar[j], ybar[j], y[j], xbar[i])
-            elif block_of(ybar[j + 1], n, p) == i:
+            elif block_of(ybar[j + 1], n, pA) == i:
                 t = (ybar[j], ybar[j + 1], y[j], y[j + 1])
             elif ybar[j + 1] == x[i + 1]:
                 t = (ybar[j], x[i + 1], y[j], y[j + 1])
@@ -199,3 +207,175 @@ def merge_stable_sharded(a_keys: torch.Tensor, a_vals: Optional[torch.Tensor], b
                            None if bv is None else bv.contiguous())
         pieces.append(Piece(a0 + b0, ck, cv))
     return pieces
+
+
+# ------------------------------------------------------------ sharded sort
+# SURVEY.md §8(f) row 3 (merge SORT over the GPUs), the paper's merge sort
+# (§3) with the ranks as processing elements:
+#   phase 1  each rank sorts its block of the input (the library's sort:
+#            "sorting sequentially in parallel p consecutive blocks", L406-407)
+#   phase 2  ceil(log2 p) rounds; round i merges run pairs (2k, 2k+1), a run
+#            being the sorted union of 2^i consecutive ranks' blocks, held
+#            block-partitioned over those ranks (rank j of the run holds its
+#            block j, PAPER.md L168-182 with p = the run's rank count).  One
+#            pair is one sharded merge with p_A, p_B = the two runs' rank
+#            counts (reading R7): one all-gather of block-start keys, local
+#            ranks summed by ONE all-reduce (the single synchronisation,
+#            L373-375), the p_A + p_B task plan (Steps 3-4), one round of
+#            point-to-point sends of each task's foreign range (one block,
+#            L343-361), local merges, and one round of sends that re-blocks
+#            the merged run over its ranks.  All pairs of a round share the
+#            same collectives; an odd trailing run waits (L409-410).
+# Result: rank r holds block r of the stably sorted whole (equal keys keep
+# their global input order: left runs play A).
+
+def _cat(parts, like):
+    parts = [t for t in parts if t is not None and t.shape[0] > 0]
+    if not parts:
+        return like[:0]
+    return torch.cat(parts) if len(parts) > 1 else parts[0]
+
+
+def mergesort_stable_sharded(keys: torch.Tensor, vals: Optional[torch.Tensor], N: int, *, group=None,
+                             key_type: Optional[str] = None, descending: bool = False, ops=None):
+    """Stable sort of an array of N keys (+ uint32 payloads) sharded over the
+    ranks of `group`: this rank passes block r of the input (PAPER.md block
+    partition, p = world size) and gets back block r of the sorted array.
+    Returns (keys, vals)."""
+    p = dist.get_world_size(group)
+    r = dist.get_rank(group)
+    ops = ops or CudaOps(key_type, descending)
+    xs = block_starts(N, p)
+    if keys.shape[0] != xs[r + 1] - xs[r]:
+        raise ValueError("the shard must be the paper's block r of the input: [x_r, x_r+1)")
+    if vals is not None and vals.shape[0] != keys.shape[0]:
+        raise ValueError("vals must have one entry per key")
+    dev = keys.device
+    sizes = [xs[q + 1] - xs[q] for q in range(p)]      # run length = sum of its ranks' input blocks
+    if keys.shape[0] > 1:
+        keys, vals = ops.sort(keys, vals)                # phase 1
+    h = 1
+    while h < p:                                         # phase 2: round with runs of h ranks
+        # block-start key of every rank's current block (one all-gather)
+        mine = torch.zeros((1,) + tuple(keys.shape[1:]), dtype=keys.dtype, device=dev)
+        if keys.shape[0]:
+            mine[0] = keys[0]
+        starts = torch.empty((p,) + tuple(keys.shape[1:]), dtype=keys.dtype, device=dev)
+        dist.all_gather_into_tensor(starts, mine, group=group)
+        part = torch.zeros(2 * p, dtype=torch.int64, device=dev)
+        pairs = []
+        for a0 in range(0, p, 2 * h):
+            b0, b1 = a0 + h, min(a0 + 2 * h, p)
+            if b0 >= p:
+                continue                                 # odd trailing run: unchanged this round
+            pA, pB = h, b1 - b0
+            n, m = sum(sizes[a0:b0]), sum(sizes[b0:b1])
+            pairs.append((a0, b0, b1, n, m))
+            x, y = block_starts(n, pA), block_starts(m, pB)
+            if b0 <= r < b1:                             # B rank: rank_low(A[x_q], my B block)
+                loc = ops.ranks(keys, starts[a0:b0].contiguous(), False)
+                loc = torch.where(torch.tensor([x[q] >= n for q in range(pA)], device=dev),
+                                  torch.full_like(loc, keys.shape[0]), loc)    # empty block start: m (R4)
+                part[a0:b0] = loc
+            elif a0 <= r < b0:                           # A rank: rank_high(B[y_q], my A block)
+                loc = ops.ranks(keys, starts[b0:b1].contiguous(), True)
+                loc = torch.where(torch.tensor([y[q] >= m for q in range(pB)], device=dev),
+                                  torch.full_like(loc, keys.shape[0]), loc)
+                part[p + b0:p + b1] = loc
+        dist.all_reduce(part, op=dist.ReduceOp.SUM, group=group)   # the single synchronisation
+        ranks = part.cpu().tolist()
+        ops_list, recv, mypair = [], {}, None
+        plans = []
+        for (a0, b0, b1, n, m) in pairs:
+            pA, pB = b0 - a0, b1 - b0
+            xbar = ranks[a0:b0] + [m]
+            ybar = ranks[p + b0:p + b1] + [n]
+            tasks = plan_tasks(n, m, pA, xbar, ybar, pB)
+            x, y = block_starts(n, pA), block_starts(m, pB)
+            # owners: A-side task q on A rank a0+q, B-side task q on B rank b0+q
+            owned = [(a0 + q if k < pA else b0 + (k - pA), t) for k, (q, *t) in enumerate(tasks)]
+            plans.append((a0, b0, b1, n, m, x, y, owned))
+            if a0 <= r < b1:
+                mypair = plans[-1]
+            for k, (owner, (ta0, ta1, tb0, tb1)) in enumerate(owned):
+                for side, lo, hi, length, st, base in (("A", ta0, ta1, n, x, a0), ("B", tb0, tb1, m, y, b0)):
+                    if hi <= lo:
+                        continue
+                    holder = base + block_of(lo, length, len(st) - 1)
+                    if holder == owner:
+                        continue
+                    if owner == r:
+                        kt_ = torch.empty((hi - lo,) + tuple(keys.shape[1:]), dtype=keys.dtype, device=dev)
+                        ops_list.append(dist.P2POp(dist.irecv, kt_, holder, group=group))
+                        vt_ = None
+                        if vals is not None:
+                            vt_ = torch.empty(hi - lo, dtype=vals.dtype, device=dev)
+                            ops_list.append(dist.P2POp(dist.irecv, vt_, holder, group=group))
+                        recv[(a0, k, side)] = (kt_, vt_)
+                    elif holder == r:
+                        s0, s1 = lo - st[r - base], hi - st[r - base]
+                        ops_list.append(dist.P2POp(dist.isend, keys[s0:s1].contiguous(), owner, group=group))
+                        if vals is not None:
+                            ops_list.append(dist.P2POp(dist.isend, vals[s0:s1].contiguous(), owner, group=group))
+        if ops_list:
+            for w in dist.batch_isend_irecv(ops_list):
+                w.wait()
+        # local merges of this rank's tasks -> pieces (offset in the merged run)
+        pieces = []
+        if mypair is not None:
+            a0, b0, b1, n, m, x, y, owned = mypair
+            for k, (owner, (ta0, ta1, tb0, tb1)) in enumerate(owned):
+                if owner != r or ta1 - ta0 + tb1 - tb0 == 0:
+                    continue
+
+                def local(side, lo, hi, st, base):
+                    if (a0, k, side) in recv:
+                        return recv[(a0, k, side)]
+                    if hi <= lo:
+                        return keys[:0], (None if vals is None else vals[:0])
+                    s0, s1 = lo - st[r - base], hi - st[r - base]
+                    return keys[s0:s1], (None if vals is None else vals[s0:s1])
+
+                ak, av = local("A", ta0, ta1, x, a0)
+                bk, bv = local("B", tb0, tb1, y, b0)
+                ck, cv = ops.merge(ak.contiguous(), None if av is None else av.contiguous(), bk.contiguous(),
+                                   None if bv is None else bv.contiguous())
+                pieces.append((ta0 + tb0, ck, cv))
+        # re-block every merged run over its ranks (one round of sends)
+        ops_list, incoming = [], []
+        for (a0, b0, b1, n, m, x, y, owned) in plans:
+            z = block_starts(n + m, b1 - a0)
+            for k, (owner, (ta0, ta1, tb0, tb1)) in enumerate(owned):
+                off, L = ta0 + tb0, ta1 - ta0 + tb1 - tb0
+                for blk in range(b1 - a0):
+                    lo, hi = max(off, z[blk]), min(off + L, z[blk + 1])
+                    if hi <= lo:
+                        continue
+                    dest = a0 + blk
+                    if owner == r:
+                        ck, cv = next((pk, pv) for (po, pk, pv) in pieces if po == off)
+                        seg_k, seg_v = ck[lo - off:hi - off], None if cv is None else cv[lo - off:hi - off]
+                        if dest == r:
+                            incoming.append((lo, seg_k, seg_v))
+                        else:
+                            ops_list.append(dist.P2POp(dist.isend, seg_k.contiguous(), dest, group=group))
+                            if vals is not None:
+                                ops_list.append(dist.P2POp(dist.isend, seg_v.contiguous(), dest, group=group))
+                    elif dest == r:
+                        kt_ = torch.empty((hi - lo,) + tuple(keys.shape[1:]), dtype=keys.dtype, device=dev)
+                        ops_list.append(dist.P2POp(dist.irecv, kt_, owner, group=group))
+                        vt_ = None
+                        if vals is not None:
+                            vt_ = torch.empty(hi - lo, dtype=vals.dtype, device=dev)
+                            ops_list.append(dist.P2POp(dist.irecv, vt_, owner, group=group))
+                        incoming.append((lo, kt_, vt_))
+        if ops_list:
+            for w in dist.batch_isend_irecv(ops_list):
+                w.wait()
+        if mypair is not None:
+            incoming.sort(key=lambda t: t[0])
+            keys = _cat([t[1] for t in incoming], keys)
+            vals = None if vals is None else _cat([t[2] for t in incoming], vals)
+        # the merged runs' ranks now hold blocks of runs of 2h ranks
+        h *= 2
+    return keys, vals

@@ -57,3 +57,16 @@ def test_ranks_stable_matches_oracle():
         sample = range(0, ks.size, 97)
         assert [lo[i] for i in sample] == [oracle.rank_low(ks[i], xs, kt) for i in sample]
         assert [hi[i] for i in sample] == [oracle.rank_high(ks[i], xs, kt) for i in sample]
+
+
+@pytest.mark.parametrize("kt,dist_name,desc", [("u32", "bounded:1048576", False), ("i64", "bounded:1000", True),
+                                               ("u128", "tuple:50", False)])
+def test_sharded_sort_world1_cuda(nccl1, kt, dist_name, desc):
+    """World size 1: phase 1 only (the library's sort through CudaOps); the
+    multi-rank rounds are covered on CPU by tests/test_distributed_sort.py."""
+    from paper_1202_6575_b200 import distributed as D
+    inp = synth.sort_input(200003, kt, dist_name, seed=3)
+    k, v = D.mergesort_stable_sharded(inp.keys.cuda(), inp.vals.cuda(), inp.N, key_type=kt, descending=desc)
+    wk, wv = oracle.sort(inp.keys, inp.vals, kt, descending=desc)
+    assert np.array_equal(oracle.as_np(k.cpu(), kt).view(np.uint8), wk.view(np.uint8))
+    assert np.array_equal(oracle.vals_np(v.cpu()), wv)
