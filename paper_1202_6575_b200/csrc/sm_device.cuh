@@ -444,6 +444,14 @@ template <typename K>
 __device__ __forceinline__ void merge_step_idx(uint32_t& pa, uint32_t& pb, K& ka, K& kb, K& na, K& nb, uint32_t pae,
                                                uint32_t pbe, K& out, int& ia, int& ib, int& src);
 
+// The same without the exhaustion checks: valid while neither input can run
+// out within the thread's outputs (ai + VT <= la and bi + VT <= lb).
+template <typename K>
+__device__ __forceinline__ void merge_step_fast(uint32_t& pa, uint32_t& pb, K& ka, K& kb, K& na, K& nb, K& out);
+template <typename K>
+__device__ __forceinline__ void merge_step_idx_fast(uint32_t& pa, uint32_t& pb, K& ka, K& kb, K& na, K& nb, K& out,
+                                                    int& ia, int& ib, int& src);
+
 template <typename K>
 __device__ __forceinline__ K lds(uint32_t addr);
 
@@ -524,6 +532,50 @@ __device__ __forceinline__ K lds(uint32_t addr);
             : "+r"(pa), "+r"(pb), "+" RC(raw_ref(ka)), "+" RC(raw_ref(kb)), "+" RC(raw_ref(na)),              \
               "+" RC(raw_ref(nb)), "=" RC(raw_ref(out)), "+r"(ia), "+r"(ib), "=r"(src)                         \
             : "r"(pae), "r"(pbe)                                                                               \
+            : "memory");                                                                                       \
+    }                                                                                                          \
+    template <>                                                                                                \
+    __device__ __forceinline__ void merge_step_fast<K>(uint32_t & pa, uint32_t & pb, K & ka, K & kb, K & na,   \
+                                                       K & nb, K & out) {                                      \
+        asm volatile(                                                                                          \
+            "{\n\t.reg .pred t;\n\t.reg .b32 ad;\n\t.reg .b" BITS " k;\n\t"                                  \
+            "setp.le." #CMP " t, " KA_LE_KB ";\n\t"                                                            \
+            "selp.b" BITS " %6, %2, %3, t;\n\t"                                                                \
+            "selp.b" BITS " %2, %4, %2, t;\n\t"                                                                \
+            "selp.b" BITS " %3, %3, %5, t;\n\t"                                                                \
+            "@t add.u32 %0, %0, " #SZ ";\n\t"                                                                  \
+            "@!t add.u32 %1, %1, " #SZ ";\n\t"                                                                 \
+            "selp.b32 ad, %0, %1, t;\n\t"                                                                      \
+            "ld.shared.b" BITS " k, [ad+" #SZ "];\n\t"                                                         \
+            "selp.b" BITS " %4, k, %4, t;\n\t"                                                                 \
+            "selp.b" BITS " %5, %5, k, t;\n\t}"                                                                \
+            : "+r"(pa), "+r"(pb), "+" RC(raw_ref(ka)), "+" RC(raw_ref(kb)), "+" RC(raw_ref(na)),              \
+              "+" RC(raw_ref(nb)), "=" RC(raw_ref(out))                                                        \
+            :                                                                                                  \
+            : "memory");                                                                                       \
+    }                                                                                                          \
+    template <>                                                                                                \
+    __device__ __forceinline__ void merge_step_idx_fast<K>(uint32_t & pa, uint32_t & pb, K & ka, K & kb,       \
+                                                           K & na, K & nb, K & out, int& ia, int& ib,          \
+                                                           int& src) {                                         \
+        asm volatile(                                                                                          \
+            "{\n\t.reg .pred t;\n\t.reg .b32 ad;\n\t.reg .b" BITS " k;\n\t"                                  \
+            "setp.le." #CMP " t, " KA_LE_KB ";\n\t"                                                            \
+            "selp.b" BITS " %6, %2, %3, t;\n\t"                                                                \
+            "selp.b32 %9, %7, %8, t;\n\t"                                                                      \
+            "selp.b" BITS " %2, %4, %2, t;\n\t"                                                                \
+            "selp.b" BITS " %3, %3, %5, t;\n\t"                                                                \
+            "@t add.u32 %0, %0, " #SZ ";\n\t"                                                                  \
+            "@!t add.u32 %1, %1, " #SZ ";\n\t"                                                                 \
+            "@t add.s32 %7, %7, 1;\n\t"                                                                        \
+            "@!t add.s32 %8, %8, 1;\n\t"                                                                       \
+            "selp.b32 ad, %0, %1, t;\n\t"                                                                      \
+            "ld.shared.b" BITS " k, [ad+" #SZ "];\n\t"                                                         \
+            "selp.b" BITS " %4, k, %4, t;\n\t"                                                                 \
+            "selp.b" BITS " %5, %5, k, t;\n\t}"                                                                \
+            : "+r"(pa), "+r"(pb), "+" RC(raw_ref(ka)), "+" RC(raw_ref(kb)), "+" RC(raw_ref(na)),              \
+              "+" RC(raw_ref(nb)), "=" RC(raw_ref(out)), "+r"(ia), "+r"(ib), "=r"(src)                         \
+            :                                                                                                  \
             : "memory");                                                                                       \
     }                                                                                                          \
     template <int STEP>                                                                                        \

@@ -460,10 +460,21 @@ __device__ __forceinline__ bool k2_compute(const K* sk, const uint32_t* sv, cons
             K ka = lds<K>(pa), kb = lds<K>(pb), na = lds<K>(pa + KB), nb = lds<K>(pb + KB);
             int src[VT];
             int ia = td.va_s + ai, ib = td.vb_s + bi;
+            // warp-uniform choice: no exhaustion checks when no lane can run
+            // out of A or B within its VT outputs (all but the last warps of
+            // a task)
+            if (__all_sync(__activemask(), ai + VT <= td.la && bi + VT <= td.lb)) {
 #pragma unroll
-            for (int k = 0; k < VT; ++k) {
-                if (HAS_V) merge_step_idx<K>(pa, pb, ka, kb, na, nb, pae, pbe, out[k], ia, ib, src[k]);
-                else merge_step<K>(pa, pb, ka, kb, na, nb, pae, pbe, out[k]);
+                for (int k = 0; k < VT; ++k) {
+                    if (HAS_V) merge_step_idx_fast<K>(pa, pb, ka, kb, na, nb, out[k], ia, ib, src[k]);
+                    else merge_step_fast<K>(pa, pb, ka, kb, na, nb, out[k]);
+                }
+            } else {
+#pragma unroll
+                for (int k = 0; k < VT; ++k) {
+                    if (HAS_V) merge_step_idx<K>(pa, pb, ka, kb, na, nb, pae, pbe, out[k], ia, ib, src[k]);
+                    else merge_step<K>(pa, pb, ka, kb, na, nb, pae, pbe, out[k]);
+                }
             }
             if (HAS_V) {
 #pragma unroll

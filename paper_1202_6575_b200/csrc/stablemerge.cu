@@ -32,8 +32,10 @@ thread_local int64_t g_launches = 0;
 // write-back free of bank conflicts.  Measured on B200 (profiles/): 4-byte
 // keys-only merges are bound by the consumers' shared-memory merge, and the
 // best of the shapes tried is 352 x 23 (2 CTAs/SM: T = 4048, half the
-// cross-rank searches of VT = 15); 8-byte elements 256 x 15 (2 CTAs/SM);
-// 12-byte elements 256 x 15 with a 4-deep ring (1 CTA/SM).
+// cross-rank searches of VT = 15); 8-byte elements 256 x 15 (2 CTAs/SM,
+// requested: 8-byte keys-only merges of random keys +25% over 1 CTA/SM);
+// 12-byte elements 256 x 15 with a 4-deep ring (1 CTA/SM); 16-20-byte
+// elements (128-bit keys) 256 x 11 (three stages fit).
 template <int NC_, int VT_, int STAGES_, int MINB_ = 1>
 struct K2Geo {
     static constexpr int NC = NC_, VT = VT_, STAGES = STAGES_, MINB = MINB_;
@@ -45,7 +47,7 @@ struct K2Shape {
     static constexpr int bytes = (int)sizeof(K) + (HAS_V ? 4 : 0);
     using type = typename std::conditional<
         bytes <= 4, K2Geo<352, 23, 3, 2>,
-        typename std::conditional<bytes <= 8, K2Geo<256, 15, 3>,
+        typename std::conditional<bytes <= 8, K2Geo<256, 15, 3, 2>,
                                   typename std::conditional<bytes <= 12, K2Geo<256, 15, 4>,
                                                             K2Geo<256, 11, 3>>::type>::type>::type;
 };
