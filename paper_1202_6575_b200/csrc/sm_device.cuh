@@ -3,6 +3,7 @@
 // Citations: PAPER.md line numbers.  This file is
 // the CUDA side only; it shares nothing with oracle/.
 #pragma once
+#include <limits>
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <string.h>
@@ -144,11 +145,41 @@ __device__ __host__ __forceinline__ bool key_lt(K a, K b) {
     else return a < b;
 }
 
-// The bits of a key as its base type (for inline PTX operands).
+// A floating-point key held in registers as its totalOrder integer view I
+// (int32_t / int64_t) by the PTX merge path; FViewOf maps float / double
+// (and their Desc) to it.
+template <typename I>
+struct FView {
+    I v;
+};
+template <typename K> struct FViewOf { using type = K; };
+template <> struct FViewOf<float> { using type = FView<int32_t>; };
+template <> struct FViewOf<double> { using type = FView<int64_t>; };
+template <typename B> struct FViewOf<Desc<B>> { using type = Desc<typename FViewOf<B>::type>; };
+
+// The bits of a key as an integer (for inline PTX operands).
 template <typename K>
 __device__ __forceinline__ K& raw_ref(K& k) { return k; }
+template <typename I>
+__device__ __forceinline__ I& raw_ref(FView<I>& k) { return k.v; }
 template <typename B>
-__device__ __forceinline__ B& raw_ref(Desc<B>& k) { return k.v; }
+__device__ __forceinline__ auto& raw_ref(Desc<B>& k) { return raw_ref(k.v); }
+
+// A merged key back from the PTX path's register form (floats: the view's
+// involution, then the float bits).
+template <typename K, typename V>
+__device__ __forceinline__ K from_reg(V x) {
+    if constexpr (sizeof(K) == sizeof(V) && !KeyOrd<K>::FLOAT) {
+        return *reinterpret_cast<K*>(&x);
+    } else {
+        auto b = raw_ref(x);
+        using I = decltype(b);
+        b ^= (b >> (8 * sizeof(I) - 1)) & std::numeric_limits<I>::max();
+        K k;
+        memcpy(&k, &b, sizeof(K));
+        return k;
+    }
+}
 
 // Read-only global load of a key (u128: one 16-byte load; 16-byte aligned).
 template <typename K>
@@ -457,15 +488,15 @@ __device__ __forceinline__ K lds(uint32_t addr);
 
 // NAME: specialisation tag; X_LE_Y / KA_LE_KB: the operand order of the key
 // compare ("x, y" / "%2, %3" ascending; reversed for the Desc<> types).
-#define SM_DEF_SMEM_OPS(K, NAME, CMP, BITS, RC, SZ, X_LE_Y, KA_LE_KB)                                          \
+#define SM_DEF_SMEM_OPS(K, NAME, CMP, BITS, RC, SZ, X_LE_Y, KA_LE_KB, XF_XY, XF_K, XF_0)                                \
     template <int STEP>                                                                                        \
     struct LiftProbe_##NAME {                                                                                  \
         __device__ __forceinline__ static void run(uint32_t& sa, uint32_t& sb, int& rem) {                     \
             asm volatile(                                                                                      \
-                "{\n\t.reg .pred p, q;\n\t.reg .b" BITS " x, y;\n\t"                                          \
+                "{\n\t.reg .pred p, q;\n\t.reg .b" BITS " x, y, xt;\n\t"                                          \
                 "setp.le.s32 p, %3, %2;\n\t"                                                                   \
                 "@p ld.shared.b" BITS " x, [%0+%4];\n\t"                                                       \
-                "@p ld.shared.b" BITS " y, [%1+%5];\n\t"                                                       \
+                "@p ld.shared.b" BITS " y, [%1+%5];\n\t" XF_XY                                                 \
                 "setp.le.and." #CMP " q, " X_LE_Y ", p;\n\t"                                                   \
                 "@q add.u32 %0, %0, %6;\n\t"                                                                   \
                 "@q sub.u32 %1, %1, %6;\n\t"                                                                   \
@@ -478,7 +509,8 @@ __device__ __forceinline__ K lds(uint32_t addr);
     template <>                                                                                                \
     __device__ __forceinline__ K lds<K>(uint32_t addr) {                                                       \
         K v;                                                                                                   \
-        asm volatile("ld.shared.b" BITS " %0, [%1];" : "=" RC(raw_ref(v)) : "r"(addr) : "memory");            \
+        asm volatile("{\n\t.reg .b" BITS " xt;\n\tld.shared.b" BITS " %0, [%1];\n\t" XF_0 "}"                \
+                     : "=" RC(raw_ref(v)) : "r"(addr) : "memory");                                             \
         return v;                                                                                              \
     }                                                                                                          \
     template <>                                                                                                \
@@ -488,7 +520,7 @@ __device__ __forceinline__ K lds(uint32_t addr);
         /* step ahead, so the load latency is off the compare chain); one */                                 \
         /* shared load per step, from the side just taken */                                                  \
         asm volatile(                                                                                          \
-            "{\n\t.reg .pred t, u, w;\n\t.reg .b32 ad;\n\t.reg .b" BITS " k;\n\t"                             \
+            "{\n\t.reg .pred t, u, w;\n\t.reg .b32 ad;\n\t.reg .b" BITS " k, xt;\n\t"                             \
             "setp.lt.u32 u, %0, %7;\n\t"                                                                       \
             "setp.ge.u32 w, %1, %8;\n\t"                                                                       \
             "setp.le.and." #CMP " t, " KA_LE_KB ", u;\n\t"                                                    \
@@ -499,7 +531,7 @@ __device__ __forceinline__ K lds(uint32_t addr);
             "@t add.u32 %0, %0, " #SZ ";\n\t"                                                                  \
             "@!t add.u32 %1, %1, " #SZ ";\n\t"                                                                 \
             "selp.b32 ad, %0, %1, t;\n\t"                                                                      \
-            "ld.shared.b" BITS " k, [ad+" #SZ "];\n\t"                                                         \
+            "ld.shared.b" BITS " k, [ad+" #SZ "];\n\t" XF_K                                                         \
             "selp.b" BITS " %4, k, %4, t;\n\t"                                                                 \
             "selp.b" BITS " %5, %5, k, t;\n\t}"                                                                \
             : "+r"(pa), "+r"(pb), "+" RC(raw_ref(ka)), "+" RC(raw_ref(kb)), "+" RC(raw_ref(na)),              \
@@ -512,7 +544,7 @@ __device__ __forceinline__ K lds(uint32_t addr);
                                                       K & nb, uint32_t pae, uint32_t pbe, K & out, int& ia,    \
                                                       int& ib, int& src) {                                     \
         asm volatile(                                                                                          \
-            "{\n\t.reg .pred t, u, w;\n\t.reg .b32 ad;\n\t.reg .b" BITS " k;\n\t"                             \
+            "{\n\t.reg .pred t, u, w;\n\t.reg .b32 ad;\n\t.reg .b" BITS " k, xt;\n\t"                             \
             "setp.lt.u32 u, %0, %10;\n\t"                                                                      \
             "setp.ge.u32 w, %1, %11;\n\t"                                                                      \
             "setp.le.and." #CMP " t, " KA_LE_KB ", u;\n\t"                                                    \
@@ -526,7 +558,7 @@ __device__ __forceinline__ K lds(uint32_t addr);
             "@t add.s32 %7, %7, 1;\n\t"                                                                        \
             "@!t add.s32 %8, %8, 1;\n\t"                                                                       \
             "selp.b32 ad, %0, %1, t;\n\t"                                                                      \
-            "ld.shared.b" BITS " k, [ad+" #SZ "];\n\t"                                                         \
+            "ld.shared.b" BITS " k, [ad+" #SZ "];\n\t" XF_K                                                         \
             "selp.b" BITS " %4, k, %4, t;\n\t"                                                                 \
             "selp.b" BITS " %5, %5, k, t;\n\t}"                                                                \
             : "+r"(pa), "+r"(pb), "+" RC(raw_ref(ka)), "+" RC(raw_ref(kb)), "+" RC(raw_ref(na)),              \
@@ -538,7 +570,7 @@ __device__ __forceinline__ K lds(uint32_t addr);
     __device__ __forceinline__ void merge_step_fast<K>(uint32_t & pa, uint32_t & pb, K & ka, K & kb, K & na,   \
                                                        K & nb, K & out) {                                      \
         asm volatile(                                                                                          \
-            "{\n\t.reg .pred t;\n\t.reg .b32 ad;\n\t.reg .b" BITS " k;\n\t"                                  \
+            "{\n\t.reg .pred t;\n\t.reg .b32 ad;\n\t.reg .b" BITS " k, xt;\n\t"                                  \
             "setp.le." #CMP " t, " KA_LE_KB ";\n\t"                                                            \
             "selp.b" BITS " %6, %2, %3, t;\n\t"                                                                \
             "selp.b" BITS " %2, %4, %2, t;\n\t"                                                                \
@@ -546,7 +578,7 @@ __device__ __forceinline__ K lds(uint32_t addr);
             "@t add.u32 %0, %0, " #SZ ";\n\t"                                                                  \
             "@!t add.u32 %1, %1, " #SZ ";\n\t"                                                                 \
             "selp.b32 ad, %0, %1, t;\n\t"                                                                      \
-            "ld.shared.b" BITS " k, [ad+" #SZ "];\n\t"                                                         \
+            "ld.shared.b" BITS " k, [ad+" #SZ "];\n\t" XF_K                                                         \
             "selp.b" BITS " %4, k, %4, t;\n\t"                                                                 \
             "selp.b" BITS " %5, %5, k, t;\n\t}"                                                                \
             : "+r"(pa), "+r"(pb), "+" RC(raw_ref(ka)), "+" RC(raw_ref(kb)), "+" RC(raw_ref(na)),              \
@@ -559,7 +591,7 @@ __device__ __forceinline__ K lds(uint32_t addr);
                                                            K & na, K & nb, K & out, int& ia, int& ib,          \
                                                            int& src) {                                         \
         asm volatile(                                                                                          \
-            "{\n\t.reg .pred t;\n\t.reg .b32 ad;\n\t.reg .b" BITS " k;\n\t"                                  \
+            "{\n\t.reg .pred t;\n\t.reg .b32 ad;\n\t.reg .b" BITS " k, xt;\n\t"                                  \
             "setp.le." #CMP " t, " KA_LE_KB ";\n\t"                                                            \
             "selp.b" BITS " %6, %2, %3, t;\n\t"                                                                \
             "selp.b32 %9, %7, %8, t;\n\t"                                                                      \
@@ -570,7 +602,7 @@ __device__ __forceinline__ K lds(uint32_t addr);
             "@t add.s32 %7, %7, 1;\n\t"                                                                        \
             "@!t add.s32 %8, %8, 1;\n\t"                                                                       \
             "selp.b32 ad, %0, %1, t;\n\t"                                                                      \
-            "ld.shared.b" BITS " k, [ad+" #SZ "];\n\t"                                                         \
+            "ld.shared.b" BITS " k, [ad+" #SZ "];\n\t" XF_K                                                         \
             "selp.b" BITS " %4, k, %4, t;\n\t"                                                                 \
             "selp.b" BITS " %5, %5, k, t;\n\t}"                                                                \
             : "+r"(pa), "+r"(pb), "+" RC(raw_ref(ka)), "+" RC(raw_ref(kb)), "+" RC(raw_ref(na)),              \
@@ -586,14 +618,30 @@ __device__ __forceinline__ K lds(uint32_t addr);
 template <typename K, int STEP>
 struct LiftSel;
 
-SM_DEF_SMEM_OPS(uint32_t, u32, u32, "32", "r", 4, "x, y", "%2, %3")
-SM_DEF_SMEM_OPS(int32_t, s32, s32, "32", "r", 4, "x, y", "%2, %3")
-SM_DEF_SMEM_OPS(uint64_t, u64, u64, "64", "l", 8, "x, y", "%2, %3")
-SM_DEF_SMEM_OPS(int64_t, s64, s64, "64", "l", 8, "x, y", "%2, %3")
-SM_DEF_SMEM_OPS(Desc<uint32_t>, du32, u32, "32", "r", 4, "y, x", "%3, %2")
-SM_DEF_SMEM_OPS(Desc<int32_t>, ds32, s32, "32", "r", 4, "y, x", "%3, %2")
-SM_DEF_SMEM_OPS(Desc<uint64_t>, du64, u64, "64", "l", 8, "y, x", "%3, %2")
-SM_DEF_SMEM_OPS(Desc<int64_t>, ds64, s64, "64", "l", 8, "y, x", "%3, %2")
+SM_DEF_SMEM_OPS(uint32_t, u32, u32, "32", "r", 4, "x, y", "%2, %3", "", "", "")
+SM_DEF_SMEM_OPS(int32_t, s32, s32, "32", "r", 4, "x, y", "%2, %3", "", "", "")
+SM_DEF_SMEM_OPS(uint64_t, u64, u64, "64", "l", 8, "x, y", "%2, %3", "", "", "")
+SM_DEF_SMEM_OPS(int64_t, s64, s64, "64", "l", 8, "x, y", "%2, %3", "", "", "")
+SM_DEF_SMEM_OPS(Desc<uint32_t>, du32, u32, "32", "r", 4, "y, x", "%3, %2", "", "", "")
+SM_DEF_SMEM_OPS(Desc<int32_t>, ds32, s32, "32", "r", 4, "y, x", "%3, %2", "", "", "")
+SM_DEF_SMEM_OPS(Desc<uint64_t>, du64, u64, "64", "l", 8, "y, x", "%3, %2", "", "", "")
+SM_DEF_SMEM_OPS(Desc<int64_t>, ds64, s64, "64", "l", 8, "y, x", "%3, %2", "", "", "")
+// Floating-point keys: every shared load is followed by the totalOrder view
+// (sign-magnitude -> two's complement: flip the magnitude bits of negative
+// values, an involution), compared as signed integers; the merged outputs
+// are mapped back by the same involution (FView below).
+#define SM_XF32(R) "shr.s32 xt, " R ", 31;\n\tand.b32 xt, xt, 0x7fffffff;\n\txor.b32 " R ", " R ", xt;\n\t"
+#define SM_XF64(R) "shr.s64 xt, " R ", 63;\n\tand.b64 xt, xt, 0x7fffffffffffffff;\n\txor.b64 " R ", " R ", xt;\n\t"
+SM_DEF_SMEM_OPS(FView<int32_t>, fs32, s32, "32", "r", 4, "x, y", "%2, %3", SM_XF32("x") SM_XF32("y"), SM_XF32("k"),
+                SM_XF32("%0"))
+SM_DEF_SMEM_OPS(FView<int64_t>, fs64, s64, "64", "l", 8, "x, y", "%2, %3", SM_XF64("x") SM_XF64("y"), SM_XF64("k"),
+                SM_XF64("%0"))
+SM_DEF_SMEM_OPS(Desc<FView<int32_t>>, dfs32, s32, "32", "r", 4, "y, x", "%3, %2", SM_XF32("x") SM_XF32("y"),
+                SM_XF32("k"), SM_XF32("%0"))
+SM_DEF_SMEM_OPS(Desc<FView<int64_t>>, dfs64, s64, "64", "l", 8, "y, x", "%3, %2", SM_XF64("x") SM_XF64("y"),
+                SM_XF64("k"), SM_XF64("%0"))
+#undef SM_XF32
+#undef SM_XF64
 #undef SM_DEF_SMEM_OPS
 
 template <typename K, int STEP>

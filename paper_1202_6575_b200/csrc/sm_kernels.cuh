@@ -424,8 +424,8 @@ __device__ __forceinline__ bool k2_compute(const K* sk, const uint32_t* sv, cons
     if (cnt <= 0) return true;
     if (td.la > 0 && td.lb > 0) {
         // cases (b), (c), (d): stable merge (row a7), ties to A (R17)
-        if constexpr (!KeyOrd<K>::PTX) {
-            // floating-point and 128-bit keys: the same merge on the order view (C++ path)
+        if constexpr (!KeyOrd<K>::PTX && !KeyOrd<K>::FLOAT) {
+            // 128-bit keys: the same merge on the order view (C++ path)
             using U = typename KeyOrd<K>::U;
             const K* a = sk + td.a_s;
             const K* b = sk + td.b_s;
@@ -451,13 +451,17 @@ __device__ __forceinline__ bool k2_compute(const K* sk, const uint32_t* sv, cons
                 }
             }
         } else {
+            // PTX path: integer keys as they are, floating-point keys as
+            // their totalOrder integer view (V), mapped back at the end
+            using V = typename FViewOf<K>::type;
             const uint32_t sa0 = smem_addr(sk + td.a_s);
             const uint32_t sb0 = smem_addr(sk + td.b_s);
-            const int ai = split_smem<K, LOG2NV>(sa0, td.la, sb0, td.lb, d);
+            const int ai = split_smem<V, LOG2NV>(sa0, td.la, sb0, td.lb, d);
             const int bi = d - ai;
             uint32_t pa = sa0 + ai * KB, pb = sb0 + bi * KB;
             const uint32_t pae = sa0 + td.la * KB, pbe = sb0 + td.lb * KB;
-            K ka = lds<K>(pa), kb = lds<K>(pb), na = lds<K>(pa + KB), nb = lds<K>(pb + KB);
+            V ka = lds<V>(pa), kb = lds<V>(pb), na = lds<V>(pa + KB), nb = lds<V>(pb + KB);
+            V ov[VT];
             int src[VT];
             int ia = td.va_s + ai, ib = td.vb_s + bi;
             // warp-uniform choice: no exhaustion checks when no lane can run
@@ -466,16 +470,18 @@ __device__ __forceinline__ bool k2_compute(const K* sk, const uint32_t* sv, cons
             if (__all_sync(__activemask(), ai + VT <= td.la && bi + VT <= td.lb)) {
 #pragma unroll
                 for (int k = 0; k < VT; ++k) {
-                    if (HAS_V) merge_step_idx_fast<K>(pa, pb, ka, kb, na, nb, out[k], ia, ib, src[k]);
-                    else merge_step_fast<K>(pa, pb, ka, kb, na, nb, out[k]);
+                    if (HAS_V) merge_step_idx_fast<V>(pa, pb, ka, kb, na, nb, ov[k], ia, ib, src[k]);
+                    else merge_step_fast<V>(pa, pb, ka, kb, na, nb, ov[k]);
                 }
             } else {
 #pragma unroll
                 for (int k = 0; k < VT; ++k) {
-                    if (HAS_V) merge_step_idx<K>(pa, pb, ka, kb, na, nb, pae, pbe, out[k], ia, ib, src[k]);
-                    else merge_step<K>(pa, pb, ka, kb, na, nb, pae, pbe, out[k]);
+                    if (HAS_V) merge_step_idx<V>(pa, pb, ka, kb, na, nb, pae, pbe, ov[k], ia, ib, src[k]);
+                    else merge_step<V>(pa, pb, ka, kb, na, nb, pae, pbe, ov[k]);
                 }
             }
+#pragma unroll
+            for (int k = 0; k < VT; ++k) out[k] = from_reg<K>(ov[k]);
             if (HAS_V) {
 #pragma unroll
                 for (int k = 0; k < VT; ++k)
