@@ -33,9 +33,9 @@
  * buffers through device memory (cudaMemcpyAsync host->device, the kernels,
  * device->host) ordered after `stream`; host outputs are valid once `stream`
  * has been synchronised (for pageable outputs the final copy is
- * synchronous).  merge_stable with host inputs above 32 MB is cut on the
- * host into 2 p_h independent sub-merges (Steps 1-4 at p_h <= 32 blocks per
- * array) pipelined over two internal streams (uploads || merges+downloads),
+ * synchronous).  merge_stable with host inputs of 64 MB or more is cut on the
+ * host into 2 p_h independent sub-merges (Steps 1-4 at p_h <= 16 blocks per
+ * array) pipelined over three internal streams (uploads || merges || downloads),
  * joined back into `stream`; the library reads the host keys for that
  * partition (2 p_h binary searches).
  * Ownership: the caller owns every buffer; the library never frees or

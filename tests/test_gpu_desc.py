@@ -51,7 +51,7 @@ def test_desc_merge_ties_only(kt):
 
 @pytest.mark.parametrize("kt,nm", [("u32", (300001, 200003)), ("i64", (3 << 20, 3 << 20))])
 def test_desc_merge_host_buffers(kt, nm):
-    """Host inputs and outputs: small ones staged, large ones (> 32 MB) cut
+    """Host inputs and outputs: small ones staged, large ones (>= 64 MB) cut
     on the host into pipelined sub-merges under the descending order."""
     sm = lib()
     inp = synth.merge_input(nm[0], nm[1], kt, DIST[kt], seed=9, descending=True)

@@ -282,7 +282,7 @@ def test_unsorted_host_inputs_pipelined_path_terminates_in_bounds():
     """Unsorted host inputs above the pipelining threshold: the host plan's
     tasks are clamped, the call terminates, nothing outside C is written."""
     sm = lib()
-    n, m = (24 << 20) // 4, (20 << 20) // 4
+    n, m = (40 << 20) // 4, (36 << 20) // 4
     a = synth._keys("full", "i32", 5, 1, n, "cpu").pin_memory()
     b = synth._keys("full", "i32", 5, 2, m, "cpu").pin_memory()
     G = 4096
