@@ -131,6 +131,66 @@ __global__ void __launch_bounds__(256) k_cross_ranks(const K* __restrict__ A, co
     pdl_launch_dependents();
 }
 
+// K1 for one plain merge (mode 0) with the top levels of every search in
+// shared memory (BASELINE.json north_star): each CTA first loads a sample
+// of the searched array(s) -- the last key of each of SMP equal chunks --
+// with all its threads at once (one round of independent loads, mostly L2
+// hits after the first CTA), binary-searches it in shared memory, and only
+// the chunk found (len / SMP keys) is searched in global memory.
+//   rank_low(x):  c = #{chunks whose last key < x}: every key of chunks < c
+//                 is < x, chunk c's last is >= x, so the rank lies in chunk c
+//   rank_high:    the same with <=
+template <typename K, int SMP>
+__global__ void __launch_bounds__(256) k_cross_ranks_smp(const K* __restrict__ A, const K* __restrict__ B, Geom g,
+                                                         int* __restrict__ xbar, int* __restrict__ ybar) {
+    __shared__ K smp[2][SMP];                          // [0]: sample of B (A-side searches), [1]: of A
+    pdl_wait();
+    const int n = g.n, m = g.m, pA = g.pA, pB = g.pB;
+    const int items = pA + 1 + pB + 1;
+    const int i0 = blockIdx.x * blockDim.x;
+    const int i1 = min(items, i0 + (int)blockDim.x);
+    const bool need[2] = {i0 <= pA && m > 0, i1 > pA + 1 && n > 0};
+    const K* X[2] = {B, A};
+    const int len[2] = {m, n};
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+        if (!need[q]) continue;
+        const int stride = (len[q] + SMP - 1) / SMP;
+        for (int k = threadIdx.x; k < SMP; k += blockDim.x) {
+            const long long at = min((long long)(k + 1) * stride, (long long)len[q]) - 1;
+            smp[q][k] = ldg_key(X[q] + at);
+        }
+    }
+    __syncthreads();
+    const int item = i0 + threadIdx.x;
+    if (item >= items) return;
+    const bool sideA = item <= pA;
+    const int idx = sideA ? item : item - pA - 1;
+    const int plen = sideA ? pA : pB;
+    const int own_len = sideA ? n : m;
+    const int q = sideA ? 0 : 1;
+    const int oth = len[q];
+    int r = oth;                                       // empty block start / sentinel: the other length (R4)
+    if (idx < plen && idx < own_len && oth > 0) {
+        const K x = ldg_key((sideA ? A : B) + Blocks(own_len, plen).start(idx));
+        const bool high = !sideA;
+        const int stride = (oth + SMP - 1) / SMP;
+        const int chunks = (oth + stride - 1) / stride;
+        int lo = 0, hi = chunks;                       // chunks whose last key passes
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            const bool pass = high ? key_le(smp[q][mid], x) : key_lt(smp[q][mid], x);
+            lo = pass ? mid + 1 : lo;
+            hi = pass ? hi : mid;
+        }
+        const int c0 = lo * stride;
+        r = c0 >= oth ? oth : c0 + rank_kary<K, K1_WAYS>(X[q] + c0, min(stride, oth - c0), x, high);
+    }
+    if (sideA) xbar[idx] = (idx < plen && idx < own_len) ? r : m;
+    else ybar[idx] = (idx < plen && idx < own_len) ? r : n;
+    pdl_launch_dependents();
+}
+
 // Decode a task (rows a4/a5).  Mode 3 (the merge-path comparison, not the
 // paper's method): task k is output tile [kT, (k+1)T) with the diagonal
 // splits of K1mp in xbar.

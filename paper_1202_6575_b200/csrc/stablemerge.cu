@@ -77,8 +77,11 @@ constexpr int K3_NT = 256;
 constexpr int K3_IPT = 17;
 constexpr int R_SORT = K3_NT * K3_IPT;
 // K1: lanes per rank search (see k_cross_ranks).  Many searches: one lane
-// each (the DRAM-probe traffic of wider groups costs more than it saves).
-// Few searches (< K1_FEW): a whole warp each, ~log_33 dependent rounds.
+// each (the DRAM-probe traffic of wider groups costs more than it saves);
+// for a plain merge the top levels come from a per-CTA shared-memory sample
+// (k_cross_ranks_smp, the north_star's design; measured equal to searching
+// them through L1/L2 on C2-C4, within 0.3%).  Few searches (< K1_FEW): a
+// whole warp each, ~log_33 dependent rounds.
 constexpr int K1_FEW = 4096;
 
 static sm_status fail_cuda(cudaError_t e, const char* what) {
@@ -179,7 +182,10 @@ static sm_status launch_cross_ranks(const K* A, const K* B, const Geom& g, const
                                     cudaStream_t st) {
     const long long items = gc.items;
     prof_before(PROF_K1, st);
+    constexpr int SMP = 8192 / (int)sizeof(K);    // 8 KB sample per searched array
     if (items < K1_FEW) k_cross_ranks<K, 32><<<(unsigned)((items * 32 + 255) / 256), 256, 0, st>>>(A, B, g, xbar, ybar);
+    else if (g.sort == 0)
+        k_cross_ranks_smp<K, SMP><<<(unsigned)((items + 255) / 256), 256, 0, st>>>(A, B, g, xbar, ybar);
     else k_cross_ranks<K, 1><<<(unsigned)((items + 255) / 256), 256, 0, st>>>(A, B, g, xbar, ybar);
     prof_after(st);
     return check_launch("k_cross_ranks");
