@@ -220,6 +220,7 @@ struct Geom {
     const int* totals;    // mode 2: [0] = tasks, [1] = rank entries
     const int* task_seg;  // mode 2: segment of every task
     const int* rank_seg;  // mode 2: segment of every rank entry
+    const int4* tdesc;    // modes 1, 2: tasks classified ahead by k_classify (or null)
 };
 
 // One segment, located: its ranges, block counts and rank arrays.

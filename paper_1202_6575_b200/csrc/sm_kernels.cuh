@@ -331,16 +331,25 @@ __device__ __forceinline__ void k2_producer(const K* __restrict__ A, const uint3
             const int my = next + (lane - cnt) * (int)gridDim.x;
             const bool fill = lane >= cnt && my < ntasks;
             if (fill) {
-                Seg sg;
-                const Task t = decode_task(g, my, xbar, ybar, sg);
-                // sorted inputs give 0 <= la + lb <= NV (the task bound of
-                // L388-393); unsorted ones (a precondition violation) may not:
-                // clamp so the kernel still terminates inside its buffers
-                la = max(0, min(t.a1 - t.a0, NV));
-                lb = max(0, min(t.b1 - t.b0, NV - la));
-                off = sg.coff + t.a0 + t.b0;
-                ag = sg.aoff + t.a0;
-                bg = sg.boff + t.b0;
+                if (g.tdesc) {                      // classified ahead (k_classify): one load
+                    const int4 q = __ldg(g.tdesc + my);
+                    ag = q.x;
+                    bg = q.y;
+                    off = q.z;
+                    la = q.w >> 16;
+                    lb = q.w & 0xFFFF;
+                } else {
+                    Seg sg;
+                    const Task t = decode_task(g, my, xbar, ybar, sg);
+                    // sorted inputs give 0 <= la + lb <= NV (the task bound of
+                    // L388-393); unsorted ones (a precondition violation) may
+                    // not: clamp so the kernel still terminates in its buffers
+                    la = max(0, min(t.a1 - t.a0, NV));
+                    lb = max(0, min(t.b1 - t.b0, NV - la));
+                    off = sg.coff + t.a0 + t.b0;
+                    ag = sg.aoff + t.a0;
+                    bg = sg.boff + t.b0;
+                }
             }
             next += (32 - cnt) * (int)gridDim.x;
             cnt += __popc(__ballot_sync(0xffffffffu, fill));
@@ -456,6 +465,26 @@ __device__ __forceinline__ void k2_producer(const K* __restrict__ A, const uint3
         bg = __shfl_sync(0xffffffffu, bg, sl);
         cnt -= take;
     }
+}
+
+// ---- k_classify: Steps 3-4 of every task ahead of K2 (modes 1, 2) --------
+// The segmented classifications take three dependent loads (segment table,
+// then ranks); done here once per task, in parallel, so K2's producer reads
+// one 16-byte descriptor per task: (A start, B start, C start, la<<16 | lb),
+// global element indices, lengths clamped as in the producer.
+template <int NV>
+__global__ void __launch_bounds__(256) k_classify(Geom g, const int* __restrict__ xbar, const int* __restrict__ ybar,
+                                                  int4* __restrict__ tdesc) {
+    pdl_wait();
+    const int task = blockIdx.x * blockDim.x + threadIdx.x;
+    if (task < total_tasks(g)) {
+        Seg sg;
+        const Task t = decode_task(g, task, xbar, ybar, sg);
+        const int la = max(0, min(t.a1 - t.a0, NV));
+        const int lb = max(0, min(t.b1 - t.b0, NV - la));
+        tdesc[task] = make_int4(sg.aoff + t.a0, sg.boff + t.b0, sg.coff + t.a0 + t.b0, (la << 16) | lb);
+    }
+    pdl_launch_dependents();
 }
 
 // ---- consumer compute (rows a6/a7) ----------------------------------------

@@ -232,11 +232,31 @@ static sm_status launch_tasks(const K* A, const uint32_t* vA, const K* B, const 
 
 template <typename K, bool HAS_V>
 static sm_status launch_merge(const K* A, const uint32_t* vA, const K* B, const uint32_t* vB, K* C,
-                              uint32_t* vC, const Geom& g, int* xbar, int* ybar, cudaStream_t st, bool pdl,
-                              const GeomCounts* counts = nullptr) {
-    const GeomCounts gc = counts ? *counts : geom_counts(g);
-    sm_status s = launch_cross_ranks<K>(A, B, g, gc, xbar, ybar, st);
+                              uint32_t* vC, const Geom& g0, int* xbar, int* ybar, cudaStream_t st, bool pdl,
+                              const GeomCounts* counts = nullptr, int4* tdesc = nullptr) {
+    const GeomCounts gc = counts ? *counts : geom_counts(g0);
+    sm_status s = launch_cross_ranks<K>(A, B, g0, gc, xbar, ybar, st);
     if (s != SM_OK) return s;
+    Geom g = g0;
+    if (tdesc && gc.tasks > 0) {
+        // segmented modes: classify every task once, ahead of K2 (k_classify)
+        using Sh = typename K2Shape<K, HAS_V>::type;
+        cudaLaunchConfig_t cfg;
+        memset(&cfg, 0, sizeof(cfg));
+        cfg.gridDim = dim3((unsigned)((gc.tasks + 255) / 256));
+        cfg.blockDim = dim3(256);
+        cfg.stream = st;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = (pdl && !g_prof_on) ? 1 : 0;
+        cudaError_t e = cudaLaunchKernelEx(&cfg, k_classify<Sh::NV>, g0, (const int*)xbar, (const int*)ybar, tdesc);
+        if (e != cudaSuccess) return fail_cuda(e, "k_classify");
+        s = check_launch("k_classify");
+        if (s != SM_OK) return s;
+        g.tdesc = tdesc;
+    }
     return launch_tasks<K, HAS_V, typename K2Shape<K, HAS_V>::type>(A, vA, B, vB, C, vC, g, gc, xbar, ybar, st, pdl);
 }
 
@@ -621,8 +641,10 @@ static sm_status batch_entry(const K* A, const uint32_t* vA, int64_t n, const in
     const size_t seg_bytes = ((size_t)S * sizeof(SegInfo) + 15) & ~(size_t)15;
     const size_t blk_bytes = ((size_t)nblk * sizeof(int2) + 15) & ~(size_t)15;
     char* scratch = nullptr;
-    sm_status s = dalloc(&scratch, (int64_t)(seg_bytes + blk_bytes + 16 + (size_t)(2 * gc.items + gc.tasks) * 4), st);
+    const size_t td_at = (seg_bytes + blk_bytes + 16 + (size_t)(2 * gc.items + gc.tasks) * 4 + 15) & ~(size_t)15;
+    sm_status s = dalloc(&scratch, (int64_t)(td_at + (size_t)gc.tasks * sizeof(int4)), st);
     if (s != SM_OK) return s;
+    int4* tdesc = (int4*)(scratch + td_at);
     SegInfo* segs = (SegInfo*)scratch;
     int2* blk = (int2*)(scratch + seg_bytes);
     int* totals = (int*)(scratch + seg_bytes + blk_bytes);
@@ -643,8 +665,8 @@ static sm_status batch_entry(const K* A, const uint32_t* vA, int64_t n, const in
         Geom g{};
         g.S = (int)S; g.sort = 2; g.T = (int)T; g.segs = segs; g.totals = totals;
         g.task_seg = task_seg; g.rank_seg = rank_seg;
-        if (vC) s = launch_merge<K, true>(A, vA, B, vB, C, vC, g, ranks, ranks, st, true, &gc);
-        else s = launch_merge<K, false>(A, nullptr, B, nullptr, C, nullptr, g, ranks, ranks, st, true, &gc);
+        if (vC) s = launch_merge<K, true>(A, vA, B, vB, C, vC, g, ranks, ranks, st, true, &gc, tdesc);
+        else s = launch_merge<K, false>(A, nullptr, B, nullptr, C, nullptr, g, ranks, ranks, st, true, &gc, tdesc);
     }
     dfree(scratch, st);
     return s;
@@ -730,11 +752,13 @@ static sm_status sort_device(K* keys, uint32_t* vals, int64_t N, cudaStream_t st
     K* aux = nullptr;
     uint32_t* vaux = nullptr;
     int* ranks = nullptr;
+    int4* tdesc = nullptr;
     sm_status s = dalloc(&aux, N, st);
     if (s == SM_OK && vals) s = dalloc(&vaux, N, st);
     // rank arrays for the largest round: S*(pA+1) + S*(pB+1) <= 2*(N/T + 2*S) entries
     const int64_t T = tile_t((int)sizeof(K), vals != nullptr);
     if (s == SM_OK) s = dalloc(&ranks, 2 * (ceil_div(N, T) + 2 * ceil_div(N, R) + 2), st);
+    if (s == SM_OK) s = dalloc(&tdesc, ceil_div(N, T) + 2 * ceil_div(N, R) + 2, st);   // tasks of a round
     if (s == SM_OK) {
         // phase 1 lands in the buffer from which an even number of rounds
         // ends in the caller's array (in place when rounds is even)
@@ -757,12 +781,14 @@ static sm_status sort_device(K* keys, uint32_t* vals, int64_t N, cudaStream_t st
             g.n = g.m = 0; g.L = (int)L; g.N = (int)N; g.sort = 1;
             int* xbar = ranks;
             int* ybar = ranks + (int64_t)g.S * (g.pA + 1);
-            if (vals) s = launch_merge<K, true>(src, vsrc, src, vsrc, d2, vd2, g, xbar, ybar, st, pdl);
-            else s = launch_merge<K, false>(src, nullptr, src, nullptr, d2, nullptr, g, xbar, ybar, st, pdl);
+            if (vals) s = launch_merge<K, true>(src, vsrc, src, vsrc, d2, vd2, g, xbar, ybar, st, pdl, nullptr, tdesc);
+            else s = launch_merge<K, false>(src, nullptr, src, nullptr, d2, nullptr, g, xbar, ybar, st, pdl, nullptr,
+                                            tdesc);
             src = d2;
             vsrc = vd2;
         }
     }
+    dfree(tdesc, st);
     dfree(ranks, st);
     dfree(vaux, st);
     dfree(aux, st);
