@@ -30,12 +30,12 @@ def ncu_raw(rep):
     return r[0], r[1], r[2]
 
 
-def summarize_ncu(rep, cfg, tag):
+def summarize_ncu(rep, cfg, tag, kern="k_tasks", skip=3):
     h, u, v = ncu_raw(rep)
     get = lambda k: (v[h.index(k)], u[h.index(k)]) if k in h else (None, None)
     lines = [f"# ncu --set full: K2 (k_tasks), config C{cfg} ({tag})", "",
              f"kernel: `{v[h.index('Kernel Name')][:140]}`", "",
-             "command: `ncu --set full --clock-control none --import-source on -k regex:k_tasks -s 3 -c 1 "
+             f"command: `ncu --set full --clock-control none --import-source on -k regex:{kern} -s {skip} -c 1 "
              f"python bench.py --config {cfg} --steps 3 --warmup 3 --no-extras`", "",
              "| metric | value | unit |", "|---|---|---|"]
     for k in KEYS:
@@ -108,7 +108,8 @@ def main(tag):
     for name, rep in (("k_cross_ranks_c2", f"{tag}_c2_k_cross_ranks"), ("k_block_sort_c5", f"{tag}_c5_k_block_sort")):
         path = os.path.join(EV, rep + ".ncu-rep")
         if os.path.exists(path):
-            text, tr, dur = summarize_ncu(path, 2 if "c2" in name else 5, tag)
+            kern = name.split("_c")[0]
+            text, tr, dur = summarize_ncu(path, 2 if "c2" in name else 5, tag, kern, 3 if "c2" in name else 2)
             text = text.replace("K2 (k_tasks)", name.split("_c")[0])
             open(os.path.join(OUT, f"{tag}_ncu_{name}.md"), "w").write(text)
     mp = os.path.join(EV, "bench_c2_mergepath.log")
@@ -116,6 +117,14 @@ def main(tag):
         for ln in open(mp):
             if ln.startswith("{"):
                 json.dump(json.loads(ln), open(os.path.join(OUT, f"{tag}_bench_c2_mergepath.json"), "w"))
+    ref = os.path.join(EV, "bench_reference.log")
+    if os.path.exists(ref):
+        for ln in open(ref):
+            if ln.startswith("{"):
+                json.dump(json.loads(ln), open(os.path.join(OUT, f"{tag}_bench_reference.json"), "w"))
+    pt = os.path.join(EV, "pytest_gpu.log")
+    if os.path.exists(pt):
+        open(os.path.join(OUT, f"{tag}_pytest_gpu.log"), "w").write(open(pt).read())
     json.dump(traffic, open(os.path.join(OUT, "traffic.json"), "w"), indent=1)
     print(json.dumps(traffic, indent=1))
     write_readme(tag, rows, traffic)
@@ -162,6 +171,7 @@ def write_readme(tag, rows, traffic):
             "shared-memory pipe, bank conflicts, occupancy, issue, warp stalls); "
             f"`{tag}_ncu_k_cross_ranks_c2.md` (K1) and `{tag}_ncu_k_block_sort_c5.md` (K3).",
             "- `traffic.json` -- DRAM read+write bytes per K2 launch from those captures (bench.py `roofline.traffic`).",
+            f"- `{tag}_bench_reference.json` -- `bench.py --impl reference`: the CPU oracle as the reference arm.",
             f"- `{tag}_pytest_gpu.log` -- the full `pytest -m gpu` run on the B200."]
     open(os.path.join(OUT, "README.md"), "w").write("\n".join(out) + "\n")
 
