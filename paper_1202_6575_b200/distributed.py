@@ -124,15 +124,46 @@ def _holder(lo: int, hi: int, length: int, p: int) -> int:
     return block_of(lo, length, p) if hi > lo else -1
 
 
+def _coll_device(t: torch.Tensor, group) -> torch.device:
+    """Where the small collectives run: the tensors' device, or the host for
+    a gloo group (CPU tests; several ranks sharing one GPU)."""
+    return torch.device("cpu") if dist.get_backend(group) == "gloo" else t.device
+
+
+def _share(t: Optional[torch.Tensor]):
+    """A picklable CUDA IPC handle of t (torch's own IPC reduction)."""
+    if t is None:
+        return None
+    from torch.multiprocessing.reductions import reduce_tensor
+    return reduce_tensor(t.contiguous())
+
+
+def _open(shared) -> Optional[torch.Tensor]:
+    if shared is None:
+        return None
+    fn, args = shared
+    return fn(*args)
+
+
 def merge_stable_sharded(a_keys: torch.Tensor, a_vals: Optional[torch.Tensor], b_keys: torch.Tensor,
                          b_vals: Optional[torch.Tensor], n: int, m: int, *, group=None,
-                         key_type: Optional[str] = None, ops=None) -> List[Piece]:
+                         key_type: Optional[str] = None, ops=None,
+                         peer_access: Optional[bool] = None) -> List[Piece]:
     """Stable merge (ties: A first) of A (n) and B (m) sharded over the ranks
     of `group`: this rank passes its blocks A[x_r, x_{r+1}) and B[y_r, y_{r+1})
     (PAPER.md block partition, p = world size).  Returns this rank's output
-    pieces."""
+    pieces.
+
+    peer_access (default: on for CUDA shards in an NCCL group -- the GPUs of
+    one NVLink/NVSwitch node, reachable by CUDA IPC): no exchange step at all -- every rank maps the
+    other ranks' shards (CUDA IPC handles, one all-gather) and the merge
+    kernel's TMA loads read each task's foreign range straight from the
+    holder's memory over NVLink, so the transfer overlaps the merge stage by
+    stage inside ONE kernel; a barrier before the merges (inputs complete)
+    and after them (no rank frees its shard while peers read it)."""
     p = dist.get_world_size(group)
     r = dist.get_rank(group)
+    custom_ops = ops is not None
     ops = ops or CudaOps(key_type)
     x, y = block_starts(n, p), block_starts(m, p)
     if a_keys.numel() != x[r + 1] - x[r] or b_keys.numel() != y[r + 1] - y[r]:
@@ -140,14 +171,16 @@ def merge_stable_sharded(a_keys: torch.Tensor, a_vals: Optional[torch.Tensor], b
     if (a_vals is None) != (b_vals is None):
         raise ValueError("payloads must be given for both inputs or neither")
     dev = a_keys.device
+    cdev = _coll_device(a_keys, group)
     # block-start keys of every rank: one all-gather of (A[x_r], B[y_r])
     mine = torch.zeros(2, dtype=a_keys.dtype, device=dev)
     if a_keys.numel():
         mine[0] = a_keys[0]
     if b_keys.numel():
         mine[1] = b_keys[0]
-    starts = torch.empty(2 * p, dtype=a_keys.dtype, device=dev)
-    dist.all_gather_into_tensor(starts, mine, group=group)
+    starts = torch.empty(2 * p, dtype=a_keys.dtype, device=cdev)
+    dist.all_gather_into_tensor(starts, mine.to(cdev), group=group)
+    starts = starts.to(dev)
     sa, sb = starts[0::2].contiguous(), starts[1::2].contiguous()
     # Steps 1-2: ranks in the local shards; empty block starts rank as the
     # sentinel (their sum is the full length, reading R4)
@@ -158,11 +191,17 @@ def merge_stable_sharded(a_keys: torch.Tensor, a_vals: Optional[torch.Tensor], b
     empty_b = torch.tensor([y[q] >= m for q in range(p)], device=dev)
     part[:p] = torch.where(empty_a, torch.full_like(part[:p], b_keys.numel()), part[:p])
     part[p:] = torch.where(empty_b, torch.full_like(part[p:], a_keys.numel()), part[p:])
+    part = part.to(cdev)
     dist.all_reduce(part, op=dist.ReduceOp.SUM, group=group)  # the single synchronisation (L373-375)
     ranks = part.cpu().tolist()
     xbar = ranks[:p] + [m]
     ybar = ranks[p:] + [n]
     tasks = plan_tasks(n, m, p, xbar, ybar)
+
+    if peer_access is None:
+        peer_access = a_keys.is_cuda and b_keys.is_cuda and dist.get_backend(group) == "nccl" and not custom_ops
+    if peer_access:
+        return _merge_tasks_peer(tasks, r, p, n, m, x, y, a_keys, a_vals, b_keys, b_vals, ops, group)
 
     # exchange: every task's foreign range from its single holder
     ops_list, recv = [], {}
@@ -206,6 +245,37 @@ def merge_stable_sharded(a_keys: torch.Tensor, a_vals: Optional[torch.Tensor], b
         ck, cv = ops.merge(ak.contiguous(), None if av is None else av.contiguous(), bk.contiguous(),
                            None if bv is None else bv.contiguous())
         pieces.append(Piece(a0 + b0, ck, cv))
+    return pieces
+
+
+def _merge_tasks_peer(tasks, r, p, n, m, x, y, a_keys, a_vals, b_keys, b_vals, ops, group) -> List[Piece]:
+    """The merges of merge_stable_sharded(peer_access=True): foreign ranges
+    are read in place from the peers' shards (CUDA IPC mappings)."""
+    torch.cuda.synchronize(a_keys.device)               # this rank's shards are complete ...
+    handles = [None] * p
+    dist.all_gather_object(handles, [_share(a_keys), _share(a_vals), _share(b_keys), _share(b_vals)], group=group)
+    mapped = {}                                          # ... and every rank's, after the all-gather
+
+    def shard(q):
+        if q == r:
+            return a_keys, a_vals, b_keys, b_vals
+        if q not in mapped:
+            mapped[q] = [_open(h) for h in handles[q]]
+        return mapped[q]
+
+    pieces = []
+    for k, (owner, a0, a1, b0, b1) in enumerate(tasks):
+        if owner != r or a1 - a0 + b1 - b0 == 0:
+            continue
+        ha, hb = _holder(a0, a1, n, p), _holder(b0, b1, m, p)
+        ak = a_keys[:0] if ha < 0 else shard(ha)[0][a0 - x[ha]:a1 - x[ha]]
+        av = None if a_vals is None else (a_vals[:0] if ha < 0 else shard(ha)[1][a0 - x[ha]:a1 - x[ha]])
+        bk = b_keys[:0] if hb < 0 else shard(hb)[2][b0 - y[hb]:b1 - y[hb]]
+        bv = None if b_vals is None else (b_vals[:0] if hb < 0 else shard(hb)[3][b0 - y[hb]:b1 - y[hb]])
+        ck, cv = ops.merge(ak, av, bk, bv)           # the kernel reads peer memory directly
+        pieces.append(Piece(a0 + b0, ck, cv))
+    torch.cuda.synchronize(a_keys.device)               # done reading the peers' shards
+    dist.barrier(group=group)
     return pieces
 
 
@@ -260,8 +330,10 @@ def mergesort_stable_sharded(keys: torch.Tensor, vals: Optional[torch.Tensor], N
         mine = torch.zeros((1,) + tuple(keys.shape[1:]), dtype=keys.dtype, device=dev)
         if keys.shape[0]:
             mine[0] = keys[0]
-        starts = torch.empty((p,) + tuple(keys.shape[1:]), dtype=keys.dtype, device=dev)
-        dist.all_gather_into_tensor(starts, mine, group=group)
+        cdev = _coll_device(keys, group)
+        starts = torch.empty((p,) + tuple(keys.shape[1:]), dtype=keys.dtype, device=cdev)
+        dist.all_gather_into_tensor(starts, mine.to(cdev), group=group)
+        starts = starts.to(dev)
         part = torch.zeros(2 * p, dtype=torch.int64, device=dev)
         pairs = []
         for a0 in range(0, p, 2 * h):
@@ -282,6 +354,7 @@ def mergesort_stable_sharded(keys: torch.Tensor, vals: Optional[torch.Tensor], N
                 loc = torch.where(torch.tensor([y[q] >= m for q in range(pB)], device=dev),
                                   torch.full_like(loc, keys.shape[0]), loc)
                 part[p + b0:p + b1] = loc
+        part = part.to(cdev)
         dist.all_reduce(part, op=dist.ReduceOp.SUM, group=group)   # the single synchronisation
         ranks = part.cpu().tolist()
         ops_list, recv, mypair = [], {}, None

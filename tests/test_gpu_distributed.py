@@ -70,3 +70,49 @@ def test_sharded_sort_world1_cuda(nccl1, kt, dist_name, desc):
     wk, wv = oracle.sort(inp.keys, inp.vals, kt, descending=desc)
     assert np.array_equal(oracle.as_np(k.cpu(), kt).view(np.uint8), wk.view(np.uint8))
     assert np.array_equal(oracle.vals_np(v.cpu()), wv)
+
+
+def _peer_worker(rank, world, port, cases, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1202_6575_b200 import distributed as D
+        for case in cases:
+            n, m, kt, dist_name = case
+            inp = synth.merge_input(n, m, kt, dist_name, seed=n + m, payload=True)
+            x, y = D.block_starts(n, world), D.block_starts(m, world)
+            ak = inp.a_keys[x[rank]:x[rank + 1]].cuda()
+            av = inp.a_vals[x[rank]:x[rank + 1]].cuda()
+            bk = inp.b_keys[y[rank]:y[rank + 1]].cuda()
+            bv = inp.b_vals[y[rank]:y[rank + 1]].cuda()
+            pieces = D.merge_stable_sharded(ak, av, bk, bv, n, m, key_type=kt, peer_access=True)
+            got = [None] * world
+            dist.all_gather_object(got, [(pc.offset, pc.keys.cpu(), pc.vals.cpu()) for pc in pieces])
+            if rank == 0:
+                allp = sorted((t for g in got for t in g), key=lambda t: t[0])
+                keys = torch.cat([t[1] for t in allp])
+                vals = torch.cat([t[2] for t in allp])
+                wk, wv = oracle.merge(inp.a_keys, inp.a_vals, inp.b_keys, inp.b_vals, kt)
+                ok = np.array_equal(oracle.as_np(keys, kt).view(np.uint8), wk.view(np.uint8)) and \
+                    np.array_equal(oracle.vals_np(vals), wv)
+                out.put((case, ok))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_merge_peer_access_ipc(world):
+    """peer_access=True: the merge kernel reads each task's foreign range
+    straight from the holder rank's shard through CUDA IPC (no exchange
+    step).  Functional check with `world` processes sharing cuda:0 (gloo for
+    the small collectives); on a node every rank has its own GPU and the
+    reads go over NVLink."""
+    lib()
+    import torch.multiprocessing as mp
+    cases = [(300001, 200003, "i32", "full"), (100000, 7, "u64", "mostly:0x8000000000000000:9/10"),
+             (5, 90001, "f32", "special")]
+    ctx = mp.get_context("spawn")
+    out = ctx.Queue()
+    mp.spawn(_peer_worker, args=(world, _port(), cases, out), nprocs=world, join=True)
+    res = [out.get(timeout=5) for _ in cases]
+    assert all(ok for _, ok in res), res
