@@ -177,17 +177,43 @@ static GeomCounts geom_counts(const Geom& g) {
     return {(long long)g.S * (g.pA + g.pB + 2), (long long)g.S * (g.pA + g.pB)};
 }
 
+// Launch with programmatic dependent launch (PDL) when `pdl`: the grid may
+// start while the previous kernel in the stream drains; the kernel's first
+// action is griddepcontrol.wait, so it reads nothing that kernel writes
+// before it completes.
+template <typename... KA, typename... Args>
+static cudaError_t launch_maybe_pdl(void (*kern)(KA...), unsigned grid, unsigned block, cudaStream_t st, bool pdl,
+                                    Args... args) {
+    cudaLaunchConfig_t cfg;
+    memset(&cfg, 0, sizeof(cfg));
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = (pdl && !g_prof_on) ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
 template <typename K>
 static sm_status launch_cross_ranks(const K* A, const K* B, const Geom& g, const GeomCounts& gc, int* xbar, int* ybar,
-                                    cudaStream_t st) {
+                                    cudaStream_t st, bool pdl = false) {
     const long long items = gc.items;
     prof_before(PROF_K1, st);
     constexpr int SMP = 8192 / (int)sizeof(K);    // 8 KB sample per searched array
-    if (items < K1_FEW) k_cross_ranks<K, 32><<<(unsigned)((items * 32 + 255) / 256), 256, 0, st>>>(A, B, g, xbar, ybar);
+    cudaError_t e;
+    if (items < K1_FEW)
+        e = launch_maybe_pdl(k_cross_ranks<K, 32>, (unsigned)((items * 32 + 255) / 256), 256, st, pdl, A, B, g, xbar,
+                             ybar);
     else if (g.sort == 0)
-        k_cross_ranks_smp<K, SMP><<<(unsigned)((items + 255) / 256), 256, 0, st>>>(A, B, g, xbar, ybar);
-    else k_cross_ranks<K, 1><<<(unsigned)((items + 255) / 256), 256, 0, st>>>(A, B, g, xbar, ybar);
+        e = launch_maybe_pdl(k_cross_ranks_smp<K, SMP>, (unsigned)((items + 255) / 256), 256, st, pdl, A, B, g, xbar,
+                             ybar);
+    else
+        e = launch_maybe_pdl(k_cross_ranks<K, 1>, (unsigned)((items + 255) / 256), 256, st, pdl, A, B, g, xbar, ybar);
     prof_after(st);
+    if (e != cudaSuccess) return fail_cuda(e, "k_cross_ranks");
     return check_launch("k_cross_ranks");
 }
 
@@ -235,7 +261,7 @@ static sm_status launch_merge(const K* A, const uint32_t* vA, const K* B, const 
                               uint32_t* vC, const Geom& g0, int* xbar, int* ybar, cudaStream_t st, bool pdl,
                               const GeomCounts* counts = nullptr, int4* tdesc = nullptr) {
     const GeomCounts gc = counts ? *counts : geom_counts(g0);
-    sm_status s = launch_cross_ranks<K>(A, B, g0, gc, xbar, ybar, st);
+    sm_status s = launch_cross_ranks<K>(A, B, g0, gc, xbar, ybar, st, pdl);
     if (s != SM_OK) return s;
     Geom g = g0;
     if (tdesc && gc.tasks > 0) {
