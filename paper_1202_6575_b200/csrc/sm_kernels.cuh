@@ -741,6 +741,19 @@ __global__ void __launch_bounds__(256) k_gather_rows(const uint32_t* __restrict_
     }
 }
 
+// ------------------------------------------------ coarse partition (>= 2^31)
+// The keys at the block starts of the paper's partition of X[0, len) into p
+// blocks, 64-bit indices; empty blocks are skipped.
+template <typename K>
+__global__ void __launch_bounds__(256) k_block_start_keys(const K* __restrict__ X, int64_t len, int64_t p,
+                                                          K* __restrict__ out) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= p) return;
+    const int64_t q = len / p, r = len % p;
+    const int64_t xi = i < r ? i * (q + 1) : i * q + r;
+    if (xi < len) out[i] = ldg_key(X + xi);
+}
+
 // ------------------------------------------------------- rank queries
 // rank_low (high = 0) or rank_high (high = 1) of a batch of keys in one
 // sorted array: the primitive of rows a1/a2 on its own,

@@ -395,13 +395,17 @@ static sm_status merge_path_device(const K* A, const uint32_t* vA, int64_t n, co
 struct SubMerge {
     int64_t a0, a1, b0, b1;
 };
+static void plan_from_ranks(int64_t n, int64_t m, int64_t p, const std::vector<int64_t>& xb,
+                            const std::vector<int64_t>& yb, std::vector<SubMerge>& tasks);
 
 template <typename K>
 static int64_t host_pipeline_blocks(int64_t n, int64_t m, bool has_v) {
     const int64_t bytes = (n + m) * (int64_t)(sizeof(K) + (has_v ? 4 : 0));
     // p_h <= 16 blocks of >= 32 MB: fewer, larger copies (measured C2 e2e
     // +5% over p_h <= 32 of 16 MB; p_h <= 8 equal on C2, -4% on C4)
-    return std::max<int64_t>(1, std::min<int64_t>(16, bytes / (32ll << 20)));
+    // (and blocks of <= 2^29 elements: every sub-merge stays below 2^31)
+    return std::max(std::max<int64_t>(1, std::min<int64_t>(16, bytes / (32ll << 20))),
+                    ceil_div(std::max(n, m), 1ll << 29));
 }
 
 static inline int64_t hblock_start(int64_t len, int64_t p, int64_t i) {    // x_i, L168-182; x_p = len
@@ -417,18 +421,26 @@ static inline int64_t hblock_of(int64_t len, int64_t p, int64_t k) {       // L2
 
 template <typename K>
 static void host_plan(const K* A, int64_t n, const K* B, int64_t m, int64_t p, std::vector<SubMerge>& tasks) {
-    std::vector<int64_t> x(p + 1), y(p + 1), xb(p + 1), yb(p + 1);
+    std::vector<int64_t> xb(p + 1), yb(p + 1);
+    for (int64_t i = 0; i < p; ++i) {      // Step 1: xbar_i = rank_low(A[x_i], B); empty block start -> m (R4)
+        auto lt = [](K u, K v) { return key_lt<K>(u, v); };
+        const int64_t xi = hblock_start(n, p, i), yi = hblock_start(m, p, i);
+        xb[i] = xi < n ? std::lower_bound(B, B + m, A[xi], lt) - B : m;
+        yb[i] = yi < m ? std::upper_bound(A, A + n, B[yi], lt) - A : n;   // Step 2: rank_high
+    }
+    xb[p] = m;
+    yb[p] = n;
+    plan_from_ranks(n, m, p, xb, yb, tasks);
+}
+
+// Steps 3-4 at coarse granularity from the cross ranks xb[0..p], yb[0..p].
+static void plan_from_ranks(int64_t n, int64_t m, int64_t p, const std::vector<int64_t>& xb,
+                            const std::vector<int64_t>& yb, std::vector<SubMerge>& tasks) {
+    std::vector<int64_t> x(p + 1), y(p + 1);
     for (int64_t i = 0; i <= p; ++i) {
         x[i] = hblock_start(n, p, i);
         y[i] = hblock_start(m, p, i);
     }
-    for (int64_t i = 0; i < p; ++i) {      // Step 1: xbar_i = rank_low(A[x_i], B); empty block start -> m (R4)
-        auto lt = [](K u, K v) { return key_lt<K>(u, v); };
-        xb[i] = x[i] < n ? std::lower_bound(B, B + m, A[x[i]], lt) - B : m;
-        yb[i] = y[i] < m ? std::upper_bound(A, A + n, B[y[i]], lt) - A : n;   // Step 2: rank_high
-    }
-    xb[p] = m;
-    yb[p] = n;
     for (int64_t i = 0; i < p; ++i) {      // Step 3, cases tested (a), (e), (b), (d), (c) (R8, R1)
         SubMerge t;
         if (xb[i] == xb[i + 1]) {
@@ -552,6 +564,66 @@ static sm_status merge_host_pipelined(const K* A, const uint32_t* vA, int64_t n,
     return s;
 }
 
+// Device merges of n + m >= 2^31 elements (the kernels index 32-bit): the
+// paper's Steps 1-4 once more at coarse granularity -- p blocks of <= 2^29
+// elements per array, their block-start keys ranked by the rank kernel
+// (64-bit), the cases on the host -- give 2p independent sub-merges of
+// < 2^31 elements, each run by the whole device path.  One host
+// synchronisation (the 2p ranks).
+template <typename K>
+static sm_status merge_large_device(const K* A, const uint32_t* vA, int64_t n, const K* B, const uint32_t* vB,
+                                    int64_t m, K* C, uint32_t* vC, cudaStream_t st, bool pdl) {
+    const int64_t p = std::max<int64_t>(1, ceil_div(std::max(n, m), 1ll << 29));
+    K* keys = nullptr;
+    int64_t* rk = nullptr;
+    sm_status s = dalloc(&keys, 2 * p, st);
+    if (s == SM_OK) s = dalloc(&rk, 2 * p, st);
+    const unsigned g = (unsigned)ceil_div(p, 256);
+    if (s == SM_OK) {
+        k_block_start_keys<K><<<g, 256, 0, st>>>(A, n, p, keys);
+        k_block_start_keys<K><<<g, 256, 0, st>>>(B, m, p, keys + p);
+        k_rank_keys<K><<<g, 256, 0, st>>>(B, m, keys, p, 0, rk);          // Step 1: rank_low(A[x_i], B)
+        k_rank_keys<K><<<g, 256, 0, st>>>(A, n, keys + p, p, 1, rk + p);  // Step 2: rank_high(B[y_j], A)
+        s = check_launch("k_rank_keys (coarse)");
+    }
+    std::vector<int64_t> hr(2 * p);
+    if (s == SM_OK) {
+        cudaError_t e = cudaMemcpyAsync(hr.data(), rk, 2 * p * sizeof(int64_t), cudaMemcpyDeviceToHost, st);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+        if (e != cudaSuccess) s = fail_cuda(e, "coarse ranks D2H");
+    }
+    dfree(keys, st);
+    dfree(rk, st);
+    if (s != SM_OK) return s;
+    std::vector<int64_t> xb(p + 1), yb(p + 1);
+    for (int64_t i = 0; i < p; ++i) {              // empty block starts: the other length (R4)
+        xb[i] = hblock_start(n, p, i) < n ? hr[i] : m;
+        yb[i] = hblock_start(m, p, i) < m ? hr[p + i] : n;
+    }
+    xb[p] = m;
+    yb[p] = n;
+    std::vector<SubMerge> tasks;
+    plan_from_ranks(n, m, p, xb, yb, tasks);
+    const int64_t T = tile_t((int)sizeof(K), vC != nullptr);
+    for (const SubMerge& t : tasks) {
+        const int64_t la = t.a1 - t.a0, lb = t.b1 - t.b0, off = t.a0 + t.b0;
+        if (la + lb == 0) continue;
+        s = merge_device<K>(A + t.a0, vC ? vA + t.a0 : nullptr, la, B + t.b0, vC ? vB + t.b0 : nullptr, lb, C + off,
+                            vC ? vC + off : nullptr, st, std::max<int64_t>(1, ceil_div(la, T)),
+                            std::max<int64_t>(1, ceil_div(lb, T)), pdl);
+        if (s != SM_OK) break;
+    }
+    return s;
+}
+
+// Any size, device buffers.
+template <typename K>
+static sm_status merge_any_device(const K* A, const uint32_t* vA, int64_t n, const K* B, const uint32_t* vB, int64_t m,
+                                  K* C, uint32_t* vC, cudaStream_t st, int64_t pA, int64_t pB, bool pdl) {
+    if (n + m > (int64_t)INT_MAX) return merge_large_device<K>(A, vA, n, B, vB, m, C, vC, st, pdl);
+    return merge_device<K>(A, vA, n, B, vB, m, C, vC, st, pA, pB, pdl);
+}
+
 template <typename K>
 static sm_status merge_entry(const K* A, const uint32_t* vA, int64_t n, const K* B, const uint32_t* vB, int64_t m,
                              K* C, uint32_t* vC, void* stream, const sm_options* opt) {
@@ -566,7 +638,9 @@ static sm_status merge_entry(const K* A, const uint32_t* vA, int64_t n, const K*
     } else if (vA || vB) {
         return fail_inval("payload pointers must be all set or all NULL");
     }
-    if (n + m > (int64_t)INT_MAX) return fail_inval("n + m > 2^31 - 1");
+    const bool large = n + m > (int64_t)INT_MAX;   // sub-merges below 2^31 (merge_large_device)
+    if (large && opt && (opt->p_A || opt->p_B || opt->block || (opt->flags & SM_FLAG_MERGE_PATH)))
+        return fail_inval("n + m > 2^31 - 1 takes no p_A / p_B / block / merge-path options");
     const size_t kb = sizeof(K);
     const size_t cb = (size_t)(n + m);
     if (overlaps(C, cb * kb, A, n * kb) || overlaps(C, cb * kb, B, m * kb) || overlaps(C, cb * kb, vA, n * 4) ||
@@ -587,6 +661,7 @@ static sm_status merge_entry(const K* A, const uint32_t* vA, int64_t n, const K*
         pA = std::max<int64_t>(1, ceil_div(n, T));
         pB = std::max<int64_t>(1, ceil_div(m, T));
     }
+    if (large) pA = pB = 1;                         // (chosen per sub-merge)
     const bool pdl = !(opt && (opt->flags & SM_FLAG_NO_PDL));
     if (n + m == 0) return SM_OK;
     keep_pool(st);
@@ -599,7 +674,7 @@ static sm_status merge_entry(const K* A, const uint32_t* vA, int64_t n, const K*
 
     const bool host = is_host_ptr(A) || is_host_ptr(B) || is_host_ptr(vA) || is_host_ptr(vB) || is_host_ptr(C) ||
                       is_host_ptr(vC);
-    if (!host) return merge_device<K>(A, vA, n, B, vB, m, C, vC, st, pA, pB, pdl);
+    if (!host) return merge_any_device<K>(A, vA, n, B, vB, m, C, vC, st, pA, pB, pdl);
 
     // Host inputs large enough to pipeline: sub-merges over two streams.
     const bool host_inputs = is_host_ptr(A) && is_host_ptr(B) && (!vC || (is_host_ptr(vA) && is_host_ptr(vB)));
@@ -616,8 +691,8 @@ static sm_status merge_entry(const K* A, const uint32_t* vA, int64_t n, const K*
     if (s == SM_OK) s = stage_in(sC, C, cb * kb, true, false, st);
     if (s == SM_OK && vC) s = stage_in(svC, vC, cb * 4, true, false, st);
     if (s == SM_OK)
-        s = merge_device<K>((const K*)sA.dev, (const uint32_t*)svA.dev, n, (const K*)sB.dev,
-                            (const uint32_t*)svB.dev, m, (K*)sC.dev, (uint32_t*)svC.dev, st, pA, pB, pdl);
+        s = merge_any_device<K>((const K*)sA.dev, (const uint32_t*)svA.dev, n, (const K*)sB.dev,
+                                (const uint32_t*)svB.dev, m, (K*)sC.dev, (uint32_t*)svC.dev, st, pA, pB, pdl);
     sm_status s2 = SM_OK;
     for (Stage* x : {&sC, &svC, &sA, &sB, &svA, &svB}) {
         if (s != SM_OK) x->out = false;
@@ -821,6 +896,56 @@ static sm_status sort_device(K* keys, uint32_t* vals, int64_t N, cudaStream_t st
     return s;
 }
 
+// Sorts of N >= 2^31 elements: chunks of 2^30 sorted by the device path,
+// then pairwise rounds of (large) merges, ping-ponged through one auxiliary
+// array -- the paper's phase 2 at chunk granularity (L407-416).
+template <typename K>
+static sm_status sort_large_device(K* keys, uint32_t* vals, int64_t N, cudaStream_t st, bool pdl) {
+    const int64_t CH = 1ll << 30;
+    sm_status s = SM_OK;
+    for (int64_t c0 = 0; s == SM_OK && c0 < N; c0 += CH)
+        s = sort_device<K>(keys + c0, vals ? vals + c0 : nullptr, std::min(CH, N - c0), st, pdl);
+    K* aux = nullptr;
+    uint32_t* vaux = nullptr;
+    if (s == SM_OK) s = dalloc(&aux, N, st);
+    if (s == SM_OK && vals) s = dalloc(&vaux, N, st);
+    K* src = keys;
+    uint32_t* vsrc = vals;
+    K* dst = aux;
+    uint32_t* vdst = vaux;
+    for (int64_t L = CH; s == SM_OK && L < N; L *= 2) {
+        for (int64_t s0 = 0; s == SM_OK && s0 < N; s0 += 2 * L) {
+            const int64_t la = std::min(L, N - s0), lb = std::max<int64_t>(0, std::min(L, N - s0 - L));
+            if (lb == 0) {                         // odd trailing run: copied (L409-410)
+                cudaError_t e = cudaMemcpyAsync(dst + s0, src + s0, la * sizeof(K), cudaMemcpyDeviceToDevice, st);
+                if (e == cudaSuccess && vals)
+                    e = cudaMemcpyAsync(vdst + s0, vsrc + s0, la * 4, cudaMemcpyDeviceToDevice, st);
+                if (e != cudaSuccess) s = fail_cuda(e, "cudaMemcpyAsync D2D");
+                continue;
+            }
+            const int64_t T = tile_t((int)sizeof(K), vals != nullptr);
+            s = merge_any_device<K>(src + s0, vals ? vsrc + s0 : nullptr, la, src + s0 + la,
+                                    vals ? vsrc + s0 + la : nullptr, lb, dst + s0, vals ? vdst + s0 : nullptr, st,
+                                    std::max<int64_t>(1, ceil_div(la, T)), std::max<int64_t>(1, ceil_div(lb, T)), pdl);
+        }
+        std::swap(src, dst);
+        std::swap(vsrc, vdst);
+    }
+    if (s == SM_OK && src != keys) {
+        cudaError_t e = cudaMemcpyAsync(keys, src, N * sizeof(K), cudaMemcpyDeviceToDevice, st);
+        if (e == cudaSuccess && vals) e = cudaMemcpyAsync(vals, vsrc, N * 4, cudaMemcpyDeviceToDevice, st);
+        if (e != cudaSuccess) s = fail_cuda(e, "cudaMemcpyAsync D2D");
+    }
+    dfree(vaux, st);
+    dfree(aux, st);
+    return s;
+}
+
+template <typename K>
+static sm_status sort_any_device(K* keys, uint32_t* vals, int64_t N, cudaStream_t st, bool pdl) {
+    return N > (int64_t)INT_MAX ? sort_large_device<K>(keys, vals, N, st, pdl) : sort_device<K>(keys, vals, N, st, pdl);
+}
+
 template <typename K>
 static sm_status sort_entry(K* keys, uint32_t* vals, int64_t N, void* stream, const sm_options* opt) {
     g_launches = 0;
@@ -829,17 +954,16 @@ static sm_status sort_entry(K* keys, uint32_t* vals, int64_t N, void* stream, co
     if (N < 0) return fail_inval("negative size");
     if (N && !keys) return fail_inval("NULL key pointer with nonzero size");
     if (!keys_aligned<K>({keys})) return fail_inval("128-bit keys must be 16-byte aligned");
-    if (N > (int64_t)INT_MAX) return fail_inval("N > 2^31 - 1");
     if (opt && opt->sort_run && opt->sort_run != R_SORT) return fail_inval("sort_run must equal the block-sort tile");
     if (overlaps(keys, N * sizeof(K), vals, N * 4)) return SM_EALIAS;
     const bool pdl = !(opt && (opt->flags & SM_FLAG_NO_PDL));
     if (N <= 1) return SM_OK;
     keep_pool(st);
-    if (!is_host_ptr(keys) && !is_host_ptr(vals)) return sort_device<K>(keys, vals, N, st, pdl);
+    if (!is_host_ptr(keys) && !is_host_ptr(vals)) return sort_any_device<K>(keys, vals, N, st, pdl);
     Stage sk, sv;
     sm_status s = stage_in(sk, keys, N * sizeof(K), true, true, st);
     if (s == SM_OK && vals) s = stage_in(sv, vals, N * 4, true, true, st);
-    if (s == SM_OK) s = sort_device<K>((K*)sk.dev, (uint32_t*)sv.dev, N, st, pdl);
+    if (s == SM_OK) s = sort_any_device<K>((K*)sk.dev, (uint32_t*)sv.dev, N, st, pdl);
     if (s != SM_OK) { sk.out = false; sv.out = false; }
     sm_status r1 = stage_out(sk, st), r2 = stage_out(sv, st);
     return s != SM_OK ? s : (r1 != SM_OK ? r1 : r2);

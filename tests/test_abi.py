@@ -64,8 +64,12 @@ def test_host_validation_without_gpu(sm):
     assert lib.merge_stable_i32(None, None, 10, None, None, 0, None, None, None) == sm.SM_EINVAL
     # payload pointers half set
     assert lib.merge_stable_u32(P(0x1000), P(0x2000), 4, P(0x3000), None, 4, P(0x9000), None, None) == sm.SM_EINVAL
-    # sizes beyond 32-bit in-kernel indices
-    assert lib.merge_stable_u64(P(0x1000), None, 1 << 31, P(0x1000), None, 1, P(0x1000), None, None) == sm.SM_EINVAL
+    # sizes beyond 32-bit in-kernel indices: accepted by merge_stable (coarse
+    # partition; here the aliasing check answers first), rejected with options
+    assert lib.merge_stable_u64(P(0x1000), None, 1 << 31, P(0x1000), None, 1, P(0x1000), None, None) == sm.SM_EALIAS
+    opt = sm.SmOptions(0, 0, 1024, 0, 0)
+    assert lib.merge_stable_ex_u64(P(1 << 40), None, 1 << 31, P(1 << 41), None, 1, P(1 << 42), None, None,
+                                   ctypes.byref(opt)) == sm.SM_EINVAL
     # output overlapping an input -> SM_EALIAS
     assert lib.merge_stable_u32(P(0x10000), None, 100, P(0x20000), None, 100, P(0x10100), None, None) == sm.SM_EALIAS
     assert sm._lib.sm_status_string(sm.SM_EALIAS).startswith(b"SM_EALIAS")
