@@ -275,6 +275,7 @@ def _merge_tasks_peer(tasks, r, p, n, m, x, y, a_keys, a_vals, b_keys, b_vals, o
         ck, cv = ops.merge(ak, av, bk, bv)           # the kernel reads peer memory directly
         pieces.append(Piece(a0 + b0, ck, cv))
     torch.cuda.synchronize(a_keys.device)               # done reading the peers' shards
+    mapped.clear()                                      # release the IPC mappings before the owners may free
     dist.barrier(group=group)
     return pieces
 
