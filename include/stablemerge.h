@@ -37,7 +37,10 @@
  * host into 2 p_h independent sub-merges (Steps 1-4 at p_h <= 16 blocks per
  * array) pipelined over three internal streams (uploads || merges || downloads),
  * joined back into `stream`; the library reads the host keys for that
- * partition (2 p_h binary searches).
+ * partition (2 p_h binary searches).  mergesort_stable with host keys (and
+ * payloads) of 64 MB or more uploads in chunks sorted as they arrive and
+ * downloads the last merge round in sub-merges as they finish (one host
+ * synchronisation for that round's coarse partition).
  * Ownership: the caller owns every buffer; the library never frees or
  * retains them past the stream point of the call.  Scratch (the two
  * cross-rank arrays of p+1 entries, L373-375; the merge sort's auxiliary

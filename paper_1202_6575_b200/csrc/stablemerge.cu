@@ -946,6 +946,161 @@ static sm_status sort_any_device(K* keys, uint32_t* vals, int64_t N, cudaStream_
     return N > (int64_t)INT_MAX ? sort_large_device<K>(keys, vals, N, st, pdl) : sort_device<K>(keys, vals, N, st, pdl);
 }
 
+// Sort of host buffers (both keys and payloads on the host, N <= 2^31 - 1,
+// >= 64 MB): a pipeline instead of upload -> sort -> download.
+//   stream sH  uploads Q chunks (multiples of the block-sort run)
+//   stream sM  sorts each chunk when its upload event fires (the device sort
+//              on the chunk: block sort + the merge rounds inside it), then
+//              the merge rounds across chunks but the last
+//   last round the paper's Steps 1-4 at coarse granularity on the two
+//              sorted halves (merge_large_device's partition, one host
+//              synchronisation) give independent sub-merges; sD downloads
+//              each as soon as it is merged
+// so the uploads overlap the chunk sorts and the downloads the last round.
+template <typename K>
+static sm_status sort_host_pipelined(K* keys, uint32_t* vals, int64_t N, cudaStream_t st, bool pdl) {
+    thread_local cudaStream_t sH = nullptr, sM = nullptr, sD = nullptr;
+    thread_local cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    thread_local std::vector<cudaEvent_t> evs;
+    if (!sH) {
+        if (cudaStreamCreateWithFlags(&sH, cudaStreamNonBlocking) != cudaSuccess ||
+            cudaStreamCreateWithFlags(&sM, cudaStreamNonBlocking) != cudaSuccess ||
+            cudaStreamCreateWithFlags(&sD, cudaStreamNonBlocking) != cudaSuccess ||
+            cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming) != cudaSuccess)
+            return fail_cuda(cudaGetLastError(), "stream/event create");
+    }
+    auto event = [&](size_t k) -> cudaEvent_t {
+        while (evs.size() <= k) {
+            cudaEvent_t e;
+            if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return nullptr;
+            evs.push_back(e);
+        }
+        return evs[k];
+    };
+    const int64_t Q = 8;                                    // chunks
+    const int64_t Cs = ceil_div(ceil_div(N, Q), (int64_t)R_SORT) * R_SORT;
+    const size_t kb = sizeof(K);
+    K *dk = nullptr, *dk2 = nullptr;
+    uint32_t *dv = nullptr, *dv2 = nullptr;
+    sm_status s = dalloc(&dk, N, st);
+    if (s == SM_OK) s = dalloc(&dk2, N, st);
+    if (s == SM_OK && vals) s = dalloc(&dv, N, st);
+    if (s == SM_OK && vals) s = dalloc(&dv2, N, st);
+    if (s != SM_OK) {
+        for (void* q : {(void*)dk, (void*)dk2, (void*)dv, (void*)dv2}) dfree(q, st);
+        return s;
+    }
+    cudaEventRecord(ev_fork, st);
+    for (cudaStream_t x : {sH, sM, sD}) cudaStreamWaitEvent(x, ev_fork, 0);
+    // uploads and chunk sorts
+    int64_t nch = 0;
+    for (int64_t c0 = 0; s == SM_OK && c0 < N; c0 += Cs, ++nch) {
+        const int64_t len = std::min(Cs, N - c0);
+        cudaEvent_t e_up = event(2 * nch);
+        if (!e_up) { s = fail_cuda(cudaGetLastError(), "event create"); break; }
+        cudaError_t e = cudaMemcpyAsync(dk + c0, keys + c0, len * kb, cudaMemcpyHostToDevice, sH);
+        if (e == cudaSuccess && vals) e = cudaMemcpyAsync(dv + c0, vals + c0, len * 4, cudaMemcpyHostToDevice, sH);
+        if (e == cudaSuccess) e = cudaEventRecord(e_up, sH);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(sM, e_up, 0);
+        if (e != cudaSuccess) { s = fail_cuda(e, "cudaMemcpyAsync H2D"); break; }
+        s = sort_device<K>(dk + c0, vals ? dv + c0 : nullptr, len, sM, pdl);
+    }
+    // merge rounds across chunks, all but the last (ping-pong dk <-> dk2)
+    K* src = dk;
+    uint32_t* vsrc = dv;
+    K* dst = dk2;
+    uint32_t* vdst = dv2;
+    const int64_t T = tile_t((int)kb, vals != nullptr);
+    int64_t L = Cs;
+    for (; s == SM_OK && 2 * L < N; L *= 2) {
+        for (int64_t s0 = 0; s == SM_OK && s0 < N; s0 += 2 * L) {
+            const int64_t la = std::min(L, N - s0), lb = std::max<int64_t>(0, std::min(L, N - s0 - L));
+            if (lb == 0) {
+                cudaError_t e = cudaMemcpyAsync(dst + s0, src + s0, la * kb, cudaMemcpyDeviceToDevice, sM);
+                if (e == cudaSuccess && vals) e = cudaMemcpyAsync(vdst + s0, vsrc + s0, la * 4, cudaMemcpyDeviceToDevice, sM);
+                if (e != cudaSuccess) s = fail_cuda(e, "cudaMemcpyAsync D2D");
+                continue;
+            }
+            s = merge_device<K>(src + s0, vals ? vsrc + s0 : nullptr, la, src + s0 + la, vals ? vsrc + s0 + la : nullptr,
+                                lb, dst + s0, vals ? vdst + s0 : nullptr, sM, std::max<int64_t>(1, ceil_div(la, T)),
+                                std::max<int64_t>(1, ceil_div(lb, T)), pdl);
+        }
+        std::swap(src, dst);
+        std::swap(vsrc, vdst);
+    }
+    // the last round: halves [0, L) and [L, N) (or a single chunk: download it)
+    std::vector<SubMerge> tasks;
+    const int64_t n = std::min(L, N), m = N - n;
+    if (s == SM_OK && m > 0) {
+        const int64_t p = std::max<int64_t>(4, std::min<int64_t>(16, ceil_div(N * (int64_t)kb, 64ll << 20)));
+        K* bk = nullptr;
+        int64_t* rk = nullptr;
+        s = dalloc(&bk, 2 * p, sM);
+        if (s == SM_OK) s = dalloc(&rk, 2 * p, sM);
+        if (s == SM_OK) {
+            const unsigned g = (unsigned)ceil_div(p, 256);
+            k_block_start_keys<K><<<g, 256, 0, sM>>>(src, n, p, bk);
+            k_block_start_keys<K><<<g, 256, 0, sM>>>(src + n, m, p, bk + p);
+            k_rank_keys<K><<<g, 256, 0, sM>>>(src + n, m, bk, p, 0, rk);
+            k_rank_keys<K><<<g, 256, 0, sM>>>(src, n, bk + p, p, 1, rk + p);
+            s = check_launch("k_rank_keys (coarse)");
+        }
+        std::vector<int64_t> hr(2 * p);
+        if (s == SM_OK) {
+            cudaError_t e = cudaMemcpyAsync(hr.data(), rk, 2 * p * sizeof(int64_t), cudaMemcpyDeviceToHost, sM);
+            if (e == cudaSuccess) e = cudaStreamSynchronize(sM);
+            if (e != cudaSuccess) s = fail_cuda(e, "coarse ranks D2H");
+        }
+        dfree(bk, sM);
+        dfree(rk, sM);
+        if (s == SM_OK) {
+            std::vector<int64_t> xb(p + 1), yb(p + 1);
+            for (int64_t i = 0; i < p; ++i) {
+                xb[i] = hblock_start(n, p, i) < n ? hr[i] : m;
+                yb[i] = hblock_start(m, p, i) < m ? hr[p + i] : n;
+            }
+            xb[p] = m;
+            yb[p] = n;
+            plan_from_ranks(n, m, p, xb, yb, tasks);
+        }
+    } else if (s == SM_OK) {
+        tasks.push_back({0, N, 0, 0});                      // one chunk: sorted in place already
+    }
+    for (size_t k = 0; s == SM_OK && k < tasks.size(); ++k) {
+        const SubMerge& t = tasks[k];
+        const int64_t la = t.a1 - t.a0, lb = t.b1 - t.b0, off = t.a0 + t.b0;
+        if (la + lb == 0) continue;
+        if (lb == 0 && m == 0) {                            // single chunk: src holds the result
+            cudaError_t e = cudaStreamWaitEvent(sD, ev_fork, 0);
+            cudaEvent_t e_m = event(2 * nch + 2 * k + 1);
+            if (e == cudaSuccess) e = cudaEventRecord(e_m, sM);
+            if (e == cudaSuccess) e = cudaStreamWaitEvent(sD, e_m, 0);
+            if (e == cudaSuccess) e = cudaMemcpyAsync(keys, src, N * kb, cudaMemcpyDeviceToHost, sD);
+            if (e == cudaSuccess && vals) e = cudaMemcpyAsync(vals, vsrc, N * 4, cudaMemcpyDeviceToHost, sD);
+            if (e != cudaSuccess) s = fail_cuda(e, "cudaMemcpyAsync D2H");
+            continue;
+        }
+        s = merge_device<K>(src + t.a0, vals ? vsrc + t.a0 : nullptr, la, src + n + t.b0,
+                            vals ? vsrc + n + t.b0 : nullptr, lb, dst + off, vals ? vdst + off : nullptr, sM,
+                            std::max<int64_t>(1, ceil_div(la, T)), std::max<int64_t>(1, ceil_div(lb, T)), pdl);
+        if (s != SM_OK) break;
+        cudaEvent_t e_m = event(2 * nch + 2 * k + 1);
+        cudaError_t e = e_m ? cudaEventRecord(e_m, sM) : cudaErrorUnknown;
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(sD, e_m, 0);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(keys + off, dst + off, (la + lb) * kb, cudaMemcpyDeviceToHost, sD);
+        if (e == cudaSuccess && vals)
+            e = cudaMemcpyAsync(vals + off, vdst + off, (la + lb) * 4, cudaMemcpyDeviceToHost, sD);
+        if (e != cudaSuccess) s = fail_cuda(e, "cudaMemcpyAsync D2H");
+    }
+    for (cudaStream_t x : {sH, sM, sD}) {
+        cudaEventRecord(ev_join, x);
+        cudaStreamWaitEvent(st, ev_join, 0);
+    }
+    for (void* q : {(void*)dk, (void*)dk2, (void*)dv, (void*)dv2}) dfree(q, st);
+    return s;
+}
+
 template <typename K>
 static sm_status sort_entry(K* keys, uint32_t* vals, int64_t N, void* stream, const sm_options* opt) {
     g_launches = 0;
@@ -960,6 +1115,9 @@ static sm_status sort_entry(K* keys, uint32_t* vals, int64_t N, void* stream, co
     if (N <= 1) return SM_OK;
     keep_pool(st);
     if (!is_host_ptr(keys) && !is_host_ptr(vals)) return sort_any_device<K>(keys, vals, N, st, pdl);
+    if (is_host_ptr(keys) && (!vals || is_host_ptr(vals)) && N <= (int64_t)INT_MAX &&
+        N * (int64_t)(sizeof(K) + (vals ? 4 : 0)) >= (64ll << 20))
+        return sort_host_pipelined<K>(keys, vals, N, st, pdl);
     Stage sk, sv;
     sm_status s = stage_in(sk, keys, N * sizeof(K), true, true, st);
     if (s == SM_OK && vals) s = stage_in(sv, vals, N * 4, true, true, st);

@@ -115,3 +115,23 @@ def test_sort_full_size_config5():
     # bit-exact against the oracle on the full array
     want_k, want_v = oracle.sort(k0.cpu(), torch.arange(k0.numel(), dtype=torch.int32), "u32")
     assert_bit_exact(k.cpu(), dev.vals.cpu(), want_k, want_v, "u32")
+
+
+@pytest.mark.parametrize("kt,N,payload,pinned", [("u32", (8 << 20) + 12345, True, True),
+                                                  ("i64", (12 << 20) + 7, True, False),
+                                                  ("u32", (20 << 20) + 3, False, True),
+                                                  ("f32", (16 << 20) + 99, True, True)])
+def test_sort_host_pipelined(kt, N, payload, pinned):
+    """Host buffers of 64 MB or more: chunked uploads overlapped with the
+    chunk sorts, and the last merge round cut by the coarse Steps 1-4 into
+    sub-merges downloaded as they finish -- same bytes as the oracle."""
+    sm = lib()
+    inp = synth.sort_input(N, kt, "bounded:100000" if kt != "f32" else "special", seed=N % 101, payload=payload)
+    want = oracle.sort(inp.keys, inp.vals, kt)
+    k = inp.keys.clone()
+    v = None if inp.vals is None else inp.vals.clone()
+    if pinned:
+        k = k.pin_memory()
+        v = None if v is None else v.pin_memory()
+    sm.mergesort_stable(k, v, key_type=kt)
+    assert_bit_exact(k, v, *want, kt)
