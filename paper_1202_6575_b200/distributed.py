@@ -300,6 +300,46 @@ def _merge_tasks_peer(tasks, r, p, n, m, x, y, a_keys, a_vals, b_keys, b_vals, o
 # Result: rank r holds block r of the stably sorted whole (equal keys keep
 # their global input order: left runs play A).
 
+def _reblock_peer(plans, pieces, mypair, keys, vals, r, p, group):
+    """Sort round, peer access: every rank allocates its next-round block and
+    shares it (CUDA IPC); task owners copy their merged pieces' segments
+    straight into the destination blocks; a barrier ends the round."""
+    dev = keys.device
+    nk, nv = keys[:0], (None if vals is None else vals[:0])
+    if mypair is not None:
+        a0, b0, b1, n, m, x, y, owned = mypair
+        z = block_starts(n + m, b1 - a0)
+        L = z[r - a0 + 1] - z[r - a0]
+        nk = torch.empty((L,) + tuple(keys.shape[1:]), dtype=keys.dtype, device=dev)
+        nv = None if vals is None else torch.empty(L, dtype=vals.dtype, device=dev)
+    else:
+        nk, nv = keys, vals                           # odd trailing run: the block stays
+    torch.cuda.synchronize(dev)                       # this rank's merged pieces are complete
+    handles = [None] * p
+    dist.all_gather_object(handles, [_share(nk), _share(nv)] if mypair is not None else None, group=group)
+    for (a0, b0, b1, n, m, x, y, owned) in plans:
+        z = block_starts(n + m, b1 - a0)
+        for k, (owner, (ta0, ta1, tb0, tb1)) in enumerate(owned):
+            if owner != r:
+                continue
+            off, L = ta0 + tb0, ta1 - ta0 + tb1 - tb0
+            if L == 0:
+                continue
+            ck, cv = next((pk, pv) for (po, pk, pv) in pieces if po == off)
+            for blk in range(b1 - a0):
+                lo, hi = max(off, z[blk]), min(off + L, z[blk + 1])
+                if hi <= lo:
+                    continue
+                dest = a0 + blk
+                dk, dv = (nk, nv) if dest == r else [_open(h) for h in handles[dest]]
+                dk[lo - z[blk]:hi - z[blk]].copy_(ck[lo - off:hi - off])       # peer-to-peer over NVLink
+                if cv is not None:
+                    dv[lo - z[blk]:hi - z[blk]].copy_(cv[lo - off:hi - off])
+    torch.cuda.synchronize(dev)                       # every copy into the peers' blocks done
+    dist.barrier(group=group)
+    return nk, nv
+
+
 def _cat(parts, like):
     parts = [t for t in parts if t is not None and t.shape[0] > 0]
     if not parts:
@@ -308,13 +348,22 @@ def _cat(parts, like):
 
 
 def mergesort_stable_sharded(keys: torch.Tensor, vals: Optional[torch.Tensor], N: int, *, group=None,
-                             key_type: Optional[str] = None, descending: bool = False, ops=None):
+                             key_type: Optional[str] = None, descending: bool = False, ops=None,
+                             peer_access: Optional[bool] = None):
     """Stable sort of an array of N keys (+ uint32 payloads) sharded over the
     ranks of `group`: this rank passes block r of the input (PAPER.md block
     partition, p = world size) and gets back block r of the sorted array.
-    Returns (keys, vals)."""
+    Returns (keys, vals).
+
+    peer_access (default: on for CUDA shards in an NCCL group): both exchange
+    steps of a round go through CUDA IPC mappings instead of NCCL sends --
+    the merges read their foreign ranges in place from the holders' blocks,
+    and each task owner copies its merged piece straight into the
+    destination ranks' next-round blocks (peer-to-peer copies over NVLink)."""
     p = dist.get_world_size(group)
     r = dist.get_rank(group)
+    if peer_access is None:
+        peer_access = keys.is_cuda and dist.get_backend(group) == "nccl" and ops is None
     ops = ops or CudaOps(key_type, descending)
     xs = block_starts(N, p)
     if keys.shape[0] != xs[r + 1] - xs[r]:
@@ -360,6 +409,12 @@ def mergesort_stable_sharded(keys: torch.Tensor, vals: Optional[torch.Tensor], N
         ranks = part.cpu().tolist()
         ops_list, recv, mypair = [], {}, None
         plans = []
+        if peer_access:                                  # map every rank's current block (CUDA IPC)
+            torch.cuda.synchronize(dev)
+            handles = [None] * p
+            dist.all_gather_object(handles, [_share(keys), _share(vals)], group=group)
+            peers = {q: [_open(h) for h in handles[q]] for q in range(p) if q != r}
+            peers[r] = [keys, vals]
         for (a0, b0, b1, n, m) in pairs:
             pA, pB = b0 - a0, b1 - b0
             xbar = ranks[a0:b0] + [m]
@@ -377,6 +432,12 @@ def mergesort_stable_sharded(keys: torch.Tensor, vals: Optional[torch.Tensor], N
                         continue
                     holder = base + block_of(lo, length, len(st) - 1)
                     if holder == owner:
+                        continue
+                    if peer_access:                      # read in place from the holder's block
+                        if owner == r:
+                            s0, s1 = lo - st[holder - base], hi - st[holder - base]
+                            pk, pv = peers[holder]
+                            recv[(a0, k, side)] = (pk[s0:s1], None if pv is None else pv[s0:s1])
                         continue
                     if owner == r:
                         kt_ = torch.empty((hi - lo,) + tuple(keys.shape[1:]), dtype=keys.dtype, device=dev)
@@ -415,6 +476,12 @@ def mergesort_stable_sharded(keys: torch.Tensor, vals: Optional[torch.Tensor], N
                 ck, cv = ops.merge(ak.contiguous(), None if av is None else av.contiguous(), bk.contiguous(),
                                    None if bv is None else bv.contiguous())
                 pieces.append((ta0 + tb0, ck, cv))
+        if peer_access:
+            recv.clear()
+            peers.clear()                                # inputs read: release the mappings
+            keys, vals = _reblock_peer(plans, pieces, mypair, keys, vals, r, p, group)
+            h *= 2
+            continue
         # re-block every merged run over its ranks (one round of sends)
         ops_list, incoming = [], []
         for (a0, b0, b1, n, m, x, y, owned) in plans:

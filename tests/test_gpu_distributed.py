@@ -116,3 +116,45 @@ def test_sharded_merge_peer_access_ipc(world):
     mp.spawn(_peer_worker, args=(world, _port(), cases, out), nprocs=world, join=True)
     res = [out.get(timeout=5) for _ in cases]
     assert all(ok for _, ok in res), res
+
+
+def _peer_sort_worker(rank, world, port, cases, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1202_6575_b200 import distributed as D
+        for case in cases:
+            N, kt, dist_name = case
+            inp = synth.sort_input(N, kt, dist_name, seed=N + world, payload=True)
+            xs = D.block_starts(N, world)
+            k = inp.keys[xs[rank]:xs[rank + 1]].cuda()
+            v = inp.vals[xs[rank]:xs[rank + 1]].cuda()
+            sk, sv = D.mergesort_stable_sharded(k, v, N, key_type=kt, peer_access=True)
+            got = [None] * world
+            dist.all_gather_object(got, (sk.cpu(), sv.cpu()))
+            if rank == 0:
+                keys = torch.cat([g[0] for g in got])
+                vals = torch.cat([g[1] for g in got])
+                wk, wv = oracle.sort(inp.keys, inp.vals, kt)
+                ok = all(got[q][0].shape[0] == xs[q + 1] - xs[q] for q in range(world))
+                ok = ok and np.array_equal(oracle.as_np(keys, kt).view(np.uint8), wk.view(np.uint8)) and \
+                    np.array_equal(oracle.vals_np(vals), wv)
+                out.put((case, ok))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_sort_peer_access_ipc(world):
+    """peer_access=True for the sharded sort: foreign task inputs read in
+    place and merged pieces copied straight into the destination ranks'
+    next blocks through CUDA IPC (processes sharing cuda:0, gloo for the
+    small collectives)."""
+    lib()
+    import torch.multiprocessing as mp
+    cases = [(300001, "u32", "bounded:1048576"), (100003, "i64", "bounded:50"), (77777, "f32", "special")]
+    ctx = mp.get_context("spawn")
+    out = ctx.Queue()
+    mp.spawn(_peer_sort_worker, args=(world, _port(), cases, out), nprocs=world, join=True)
+    res = [out.get(timeout=5) for _ in cases]
+    assert all(ok for _, ok in res), res
