@@ -12,7 +12,8 @@
 //   --  k_batch_*       batched merges: segment table
 //   --  k_plan_dump     Steps 1-4 only: the task table for parity tests
 //
-// All in-kernel indices are 32-bit (the ABI rejects n+m or N > 2^31-1).
+// All in-kernel indices are 32-bit (larger calls are cut into sub-problems
+// below 2^31 on the host side: stablemerge.cu, merge_large_device).
 #pragma once
 #include "sm_device.cuh"
 
@@ -1075,13 +1076,18 @@ __global__ void __launch_bounds__(NT) k_block_sort(const K* __restrict__ in, con
             rowb[tid * ROW + 2 * i + 1] = wtot[w * ND + 2 * i + 1] + (ex >> 16);
         }
         __syncwarp();
-        // 5. scatter
+        // 5. scatter: every destination first (the shared loads of the bases
+        //    cannot be ordered behind the stores: the compiler does not know
+        //    rowb and kd never alias), then the stores
 #pragma unroll
         for (int k = 0; k < IPT; ++k) {
             const int d = (int)(key[k] >> sh) & 0xF;
-            const int pos = (int)(rowb[tid * ROW + d] + rank[k]);
-            kd[pos] = key[k];
-            if (HAS_V) vd[pos] = val[k];
+            rank[k] += rowb[tid * ROW + d];
+        }
+#pragma unroll
+        for (int k = 0; k < IPT; ++k) {
+            kd[rank[k]] = key[k];
+            if (HAS_V) vd[rank[k]] = val[k];
         }
         __syncthreads();
         cur ^= 1;
