@@ -209,6 +209,13 @@ __device__ __forceinline__ Task decode_task(const Geom& g, int task, const int* 
     int t;
     const int s = locate(g, task, false, t);
     sg = segment(g, s, (int*)xbar, (int*)ybar);
+    if (sg.pA == 0) {                                  // batched segment within one tile (R19)
+        Task w;
+        w.side = 0;
+        w.kase = (sg.n > 0 && sg.m > 0) ? CASE_B : CASE_A;
+        w.a0 = 0; w.a1 = sg.n; w.b0 = 0; w.b1 = sg.m;
+        return w;
+    }
     const Blocks xa(sg.n, sg.pA), yb(sg.m, sg.pB);
     return t < sg.pA ? classify_a_side(t, xa, yb, sg.xs, sg.ys) : classify_b_side(t - sg.pA, xa, yb, sg.xs, sg.ys);
 }
@@ -814,7 +821,7 @@ constexpr int BATCH_NT = 256;
 
 __global__ void __launch_bounds__(BATCH_NT) k_batch_count(const int64_t* __restrict__ a_off,
                                                           const int64_t* __restrict__ b_off, int S, int64_t n,
-                                                          int64_t m, int T, SegInfo* __restrict__ segs,
+                                                          int64_t m, int T, int NV, SegInfo* __restrict__ segs,
                                                           int2* __restrict__ blk) {
     __shared__ int2 wsum[BATCH_NT / 32];
     const int s = blockIdx.x * BATCH_NT + threadIdx.x;
@@ -825,10 +832,18 @@ __global__ void __launch_bounds__(BATCH_NT) k_batch_count(const int64_t* __restr
         const int64_t a0 = min(max(a_off[s], (int64_t)0), n), a1 = min(max(a_off[s + 1], a0), n);
         const int64_t b0 = min(max(b_off[s], (int64_t)0), m), b1 = min(max(b_off[s + 1], b0), m);
         e.aoff = (int)a0; e.n = (int)(a1 - a0); e.boff = (int)b0; e.m = (int)(b1 - b0); e.coff = (int)(a0 + b0);
-        e.pA = max(1, (e.n + T - 1) / T);
-        e.pB = max(1, (e.m + T - 1) / T);
-        tasks = e.pA + e.pB;
-        ranks = tasks + 2;
+        if (e.n + e.m <= NV) {
+            // the whole segment fits one tile: one task, no cross ranks (the
+            // two tasks of p_A = p_B = 1 concatenated: reading R19)
+            e.pA = e.pB = 0;
+            tasks = 1;
+            ranks = 0;
+        } else {
+            e.pA = max(1, (e.n + T - 1) / T);
+            e.pB = max(1, (e.m + T - 1) / T);
+            tasks = e.pA + e.pB;
+            ranks = tasks + 2;
+        }
     }
     int ti = tasks, ri = ranks;                         // block-inclusive scan
 #pragma unroll
@@ -891,8 +906,9 @@ __global__ void __launch_bounds__(BATCH_NT) k_batch_apply(const int2* __restrict
         e.rbase += b.y;
         segs[s] = e;
         // task -> segment and rank entry -> segment maps (K1/K2 locate in O(1))
-        for (int t = 0; t < e.pA + e.pB; ++t) task_seg[e.tbase + t] = s;
-        for (int t = 0; t < e.pA + e.pB + 2; ++t) rank_seg[e.rbase + t] = s;
+        const bool whole = e.pA == 0;
+        for (int t = 0; t < (whole ? 1 : e.pA + e.pB); ++t) task_seg[e.tbase + t] = s;
+        for (int t = 0; t < (whole ? 0 : e.pA + e.pB + 2); ++t) rank_seg[e.rbase + t] = s;
     }
     pdl_launch_dependents();
 }

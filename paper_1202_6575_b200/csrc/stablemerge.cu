@@ -752,7 +752,7 @@ static sm_status batch_entry(const K* A, const uint32_t* vA, int64_t n, const in
     int* ranks = totals + 4;
     int* rank_seg = ranks + gc.items;
     int* task_seg = rank_seg + gc.items;
-    k_batch_count<<<nblk, BATCH_NT, 0, st>>>(a_off, b_off, (int)S, n, m, (int)T, segs, blk);
+    k_batch_count<<<nblk, BATCH_NT, 0, st>>>(a_off, b_off, (int)S, n, m, (int)T, (int)(2 * T), segs, blk);
     s = check_launch("k_batch_count");
     if (s == SM_OK) {
         k_batch_scan<<<1, BATCH_NT, 0, st>>>(blk, nblk, totals);

@@ -117,3 +117,18 @@ def test_batched_malformed_offsets_stay_inside_output():
     sm.merge_stable_batched(a, None, aoff, b, None, boff, out_keys=out)
     torch.cuda.synchronize()
     assert bool((guard[1500:] == -12345).all())
+
+
+@pytest.mark.parametrize("kt,payload", [("u32", True), ("i64", False), ("f32", True)])
+def test_batched_segments_at_the_tile_boundary(kt, payload):
+    """Segments whose n + m is just below, at and just above the tile
+    capacity: the first two are single tasks (reading R19), the rest go
+    through cross ranks and cases (a)-(e)."""
+    sm = lib()
+    nv = sm.tile_capacity(kt, payload)
+    tot = np.array([nv - 1, nv, nv + 1, 2 * nv, 1, 0, nv - 2, nv + 7] * 5)
+    rng = np.random.default_rng(21)
+    la = np.array([int(rng.integers(0, t + 1)) for t in tot])
+    lb = tot - la
+    for dist in ("bounded:5", "full"):
+        _run(sm, _case(len(tot), la, lb, kt, dist, payload, seed=7), kt)
