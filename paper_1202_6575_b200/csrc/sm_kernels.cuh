@@ -9,7 +9,12 @@
 //                       copy (a, e) or stable merge (b, c, d) through a TMA
 //                       shared-memory ring, several tasks packed per stage
 //   K3  k_block_sort    row a8: stable LSD radix sort of one run per CTA
+//   --  k_cross_ranks_smp  K1 for one plain merge, top levels from a shared-
+//                       memory sample of the searched array
+//   --  k_classify      Steps 3-4 ahead of K2 for the segmented modes
 //   --  k_batch_*       batched merges: segment table
+//   --  k_iota, k_gather_rows   wide / struct payloads (§8(f) row 2)
+//   --  k_block_start_keys, k_rank_keys   coarse partition (>= 2^31), ranks
 //   --  k_plan_dump     Steps 1-4 only: the task table for parity tests
 //
 // All in-kernel indices are 32-bit (larger calls are cut into sub-problems

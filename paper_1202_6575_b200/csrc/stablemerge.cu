@@ -3,8 +3,11 @@
 //
 // Call sequence of merge_stable:
 //   validate -> choose p_A, p_B -> cudaMallocAsync the two rank arrays ->
-//   K1 (cross ranks) -> [single synchronisation: stream order / PDL] ->
-//   K2 (classify + copy/merge every task) -> cudaFreeAsync.  No host sync.
+//   K1 (cross ranks, PDL behind the previous kernel) -> [single
+//   synchronisation: PDL griddepcontrol.wait] -> K2 (classify + copy/merge
+//   every task) -> cudaFreeAsync.  No host sync.  Host buffers: staged, or
+//   pipelined over three streams from 64 MB; n + m >= 2^31: a coarse
+//   partition into sub-merges (one host sync).
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdio.h>
