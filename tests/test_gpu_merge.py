@@ -320,3 +320,35 @@ def test_config_merge_full_size(cfg):
     del dev
     want_k, want_v = oracle_merge(host)
     assert_bit_exact(ck.cpu(), None if cv is None else cv.cpu(), want_k, want_v, host.key_type)
+
+
+@pytest.mark.parametrize("kt", ["u32", "i64", "f32", "u64"])
+@pytest.mark.parametrize("shift", [(1, 3, 5, 7, 2, 9), (2, 1, 1, 3, 3, 1)])
+def test_merge_misaligned_views(kt, shift):
+    """Inputs, outputs and payloads as tensor views at element offsets that
+    are not 16-byte aligned: the TMA loads read 16-byte supersets inside the
+    same allocations and the stores write exactly the output range."""
+    sm = lib()
+    inp = synth.merge_input(70001, 50003, kt, "bounded:1000", seed=41, payload=True)
+    sa, sb, sc, sva, svb, svc = shift
+    ct = synth.KEY_TYPES[kt][0]
+
+    def view(t, s):
+        base = torch.zeros(t.numel() + s + 8, dtype=t.dtype, device="cuda")
+        v = base[s:s + t.numel()]
+        v.copy_(t.cuda())
+        return base, v
+
+    ba, a = view(inp.a_keys, sa)
+    bb, b = view(inp.b_keys, sb)
+    bva, va = view(inp.a_vals, sva)
+    bvb, vb = view(inp.b_vals, svb)
+    bc = torch.full((inp.n + inp.m + sc + 8,), -1, dtype=ct, device="cuda")
+    bvc = torch.full((inp.n + inp.m + svc + 8,), -1, dtype=torch.int32, device="cuda")
+    c, vc = bc[sc:sc + inp.n + inp.m], bvc[svc:svc + inp.n + inp.m]
+    sm.merge_stable(a, va, b, vb, c, vc, key_type=kt)
+    torch.cuda.synchronize()
+    assert_bit_exact(c.cpu(), vc.cpu(), *oracle_merge(inp), kt)
+    # nothing written outside the output views
+    assert bool((bc[:sc] == -1).all()) and bool((bc[sc + inp.n + inp.m:] == -1).all())
+    assert bool((bvc[:svc] == -1).all()) and bool((bvc[svc + inp.n + inp.m:] == -1).all())

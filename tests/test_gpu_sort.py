@@ -135,3 +135,19 @@ def test_sort_host_pipelined(kt, N, payload, pinned):
         v = None if v is None else v.pin_memory()
     sm.mergesort_stable(k, v, key_type=kt)
     assert_bit_exact(k, v, *want, kt)
+
+
+@pytest.mark.parametrize("kt,s", [("u32", 1), ("i64", 3), ("f64", 1)])
+def test_sort_misaligned_views(kt, s):
+    sm = lib()
+    inp = synth.sort_input(100003, kt, "bounded:1000", seed=5)
+    ct = synth.KEY_TYPES[kt][0]
+    bk = torch.full((inp.N + s + 8,), -1, dtype=ct, device="cuda")
+    bv = torch.full((inp.N + s + 8,), -1, dtype=torch.int32, device="cuda")
+    k, v = bk[s:s + inp.N], bv[s:s + inp.N]
+    k.copy_(inp.keys.cuda())
+    v.copy_(inp.vals.cuda())
+    sm.mergesort_stable(k, v, key_type=kt)
+    torch.cuda.synchronize()
+    assert_bit_exact(k.cpu(), v.cpu(), *oracle.sort(inp.keys, inp.vals, kt), kt)
+    assert bool((bk[:s] == -1).all()) and bool((bk[s + inp.N:] == -1).all())
