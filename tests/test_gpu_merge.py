@@ -208,7 +208,7 @@ def test_merge_host_buffers():
 def test_merge_host_pipelined(kt, payload, dist, pinned):
     """Host inputs above the pipelining threshold (>= 64 MB): the library
     cuts the call into sub-merges with the paper's Steps 1-4 on the host and
-    streams them over two CUDA streams -- same bytes as the oracle."""
+    streams them over three CUDA streams -- same bytes as the oracle."""
     sm = lib()
     eb = synth.elem_bytes(kt, payload)
     n = (100 << 20) // eb // 2 + 12345
@@ -352,3 +352,23 @@ def test_merge_misaligned_views(kt, shift):
     # nothing written outside the output views
     assert bool((bc[:sc] == -1).all()) and bool((bc[sc + inp.n + inp.m:] == -1).all())
     assert bool((bvc[:svc] == -1).all()) and bool((bvc[svc + inp.n + inp.m:] == -1).all())
+
+
+def test_merges_on_side_streams_concurrently():
+    """The library is stream-ordered: calls on two side streams (torch's
+    current stream, picked up by the binding) run concurrently and each is
+    complete after its own stream synchronises."""
+    sm = lib()
+    inps = [synth.merge_input(2_000_003, 1_500_007, kt, "full", seed=i, payload=True).to("cuda")
+            for i, kt in enumerate(("u32", "i64"))]
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    outs = []
+    torch.cuda.synchronize()
+    for inp, st in zip(inps, streams):
+        with torch.cuda.stream(st):
+            outs.append(sm.merge_stable(inp.a_keys, inp.a_vals, inp.b_keys, inp.b_vals, key_type=inp.key_type))
+    for (ck, cv), inp, st in zip(outs, inps, streams):
+        st.synchronize()
+        cpu = inp.to("cpu")
+        assert_bit_exact(ck.cpu(), cv.cpu(), *oracle.merge(cpu.a_keys, cpu.a_vals, cpu.b_keys, cpu.b_vals,
+                                                           inp.key_type), inp.key_type)
