@@ -489,7 +489,7 @@ __device__ __forceinline__ K lds(uint32_t addr);
 
 // NAME: specialisation tag; X_LE_Y / KA_LE_KB: the operand order of the key
 // compare ("x, y" / "%2, %3" ascending; reversed for the Desc<> types).
-#define SM_DEF_SMEM_OPS(K, NAME, CMP, BITS, RC, SZ, X_LE_Y, KA_LE_KB, XF_XY, XF_K, XF_0)                                \
+#define SM_DEF_SMEM_OPS(K, NAME, CMP, BITS, RC, SZ, X_LE_Y, KA_LE_KB, XF_XY, XF_K, XF_0, FAST_TAIL)                                \
     template <int STEP>                                                                                        \
     struct LiftProbe_##NAME {                                                                                  \
         __device__ __forceinline__ static void run(uint32_t& sa, uint32_t& sb, int& rem) {                     \
@@ -578,10 +578,7 @@ __device__ __forceinline__ K lds(uint32_t addr);
             "selp.b" BITS " %3, %3, %5, t;\n\t"                                                                \
             "@t add.u32 %0, %0, " #SZ ";\n\t"                                                                  \
             "@!t add.u32 %1, %1, " #SZ ";\n\t"                                                                 \
-            "selp.b32 ad, %0, %1, t;\n\t"                                                                      \
-            "ld.shared.b" BITS " k, [ad+" #SZ "];\n\t" XF_K                                                         \
-            "selp.b" BITS " %4, k, %4, t;\n\t"                                                                 \
-            "selp.b" BITS " %5, %5, k, t;\n\t}"                                                                \
+            FAST_TAIL "}"                                                                                      \
             : "+r"(pa), "+r"(pb), "+" RC(raw_ref(ka)), "+" RC(raw_ref(kb)), "+" RC(raw_ref(na)),              \
               "+" RC(raw_ref(nb)), "=" RC(raw_ref(out))                                                        \
             :                                                                                                  \
@@ -602,10 +599,7 @@ __device__ __forceinline__ K lds(uint32_t addr);
             "@!t add.u32 %1, %1, " #SZ ";\n\t"                                                                 \
             "@t add.s32 %7, %7, 1;\n\t"                                                                        \
             "@!t add.s32 %8, %8, 1;\n\t"                                                                       \
-            "selp.b32 ad, %0, %1, t;\n\t"                                                                      \
-            "ld.shared.b" BITS " k, [ad+" #SZ "];\n\t" XF_K                                                         \
-            "selp.b" BITS " %4, k, %4, t;\n\t"                                                                 \
-            "selp.b" BITS " %5, %5, k, t;\n\t}"                                                                \
+            FAST_TAIL "}"                                                                                      \
             : "+r"(pa), "+r"(pb), "+" RC(raw_ref(ka)), "+" RC(raw_ref(kb)), "+" RC(raw_ref(na)),              \
               "+" RC(raw_ref(nb)), "=" RC(raw_ref(out)), "+r"(ia), "+r"(ib), "=r"(src)                         \
             :                                                                                                  \
@@ -619,31 +613,43 @@ __device__ __forceinline__ K lds(uint32_t addr);
 template <typename K, int STEP>
 struct LiftSel;
 
-SM_DEF_SMEM_OPS(uint32_t, u32, u32, "32", "r", 4, "x, y", "%2, %3", "", "", "")
-SM_DEF_SMEM_OPS(int32_t, s32, s32, "32", "r", 4, "x, y", "%2, %3", "", "", "")
-SM_DEF_SMEM_OPS(uint64_t, u64, u64, "64", "l", 8, "x, y", "%2, %3", "", "", "")
-SM_DEF_SMEM_OPS(int64_t, s64, s64, "64", "l", 8, "x, y", "%2, %3", "", "", "")
-SM_DEF_SMEM_OPS(Desc<uint32_t>, du32, u32, "32", "r", 4, "y, x", "%3, %2", "", "", "")
-SM_DEF_SMEM_OPS(Desc<int32_t>, ds32, s32, "32", "r", 4, "y, x", "%3, %2", "", "", "")
-SM_DEF_SMEM_OPS(Desc<uint64_t>, du64, u64, "64", "l", 8, "y, x", "%3, %2", "", "", "")
-SM_DEF_SMEM_OPS(Desc<int64_t>, ds64, s64, "64", "l", 8, "y, x", "%3, %2", "", "", "")
+// The end of a fast merge step (pa / pb already advanced): integer keys
+// load the next key of the side taken straight into na / nb (predicated, so
+// nothing in the step waits for the load); floating-point keys load into a
+// temporary, map it to the order view and select (measured: predicating the
+// view as well is slower).
+#define SM_TAIL_PLD(BITS, SZ) "@t ld.shared.b" BITS " %4, [%0+" #SZ "];\n\t@!t ld.shared.b" BITS " %5, [%1+" #SZ "];\n\t"
+#define SM_TAIL_SEL(BITS, SZ, XF) "selp.b32 ad, %0, %1, t;\n\tld.shared.b" BITS " k, [ad+" #SZ "];\n\t" XF \
+    "selp.b" BITS " %4, k, %4, t;\n\tselp.b" BITS " %5, %5, k, t;\n\t"
+SM_DEF_SMEM_OPS(uint32_t, u32, u32, "32", "r", 4, "x, y", "%2, %3", "", "", "", SM_TAIL_PLD("32", 4))
+SM_DEF_SMEM_OPS(int32_t, s32, s32, "32", "r", 4, "x, y", "%2, %3", "", "", "", SM_TAIL_PLD("32", 4))
+SM_DEF_SMEM_OPS(uint64_t, u64, u64, "64", "l", 8, "x, y", "%2, %3", "", "", "", SM_TAIL_PLD("64", 8))
+SM_DEF_SMEM_OPS(int64_t, s64, s64, "64", "l", 8, "x, y", "%2, %3", "", "", "", SM_TAIL_PLD("64", 8))
+SM_DEF_SMEM_OPS(Desc<uint32_t>, du32, u32, "32", "r", 4, "y, x", "%3, %2", "", "", "", SM_TAIL_PLD("32", 4))
+SM_DEF_SMEM_OPS(Desc<int32_t>, ds32, s32, "32", "r", 4, "y, x", "%3, %2", "", "", "", SM_TAIL_PLD("32", 4))
+SM_DEF_SMEM_OPS(Desc<uint64_t>, du64, u64, "64", "l", 8, "y, x", "%3, %2", "", "", "", SM_TAIL_PLD("64", 8))
+SM_DEF_SMEM_OPS(Desc<int64_t>, ds64, s64, "64", "l", 8, "y, x", "%3, %2", "", "", "", SM_TAIL_PLD("64", 8))
 // Floating-point keys: every shared load is followed by the totalOrder view
 // (sign-magnitude -> two's complement: flip the magnitude bits of negative
 // values, an involution), compared as signed integers; the merged outputs
 // are mapped back by the same involution (FView below).
 #define SM_XF32(R) "shr.s32 xt, " R ", 31;\n\tand.b32 xt, xt, 0x7fffffff;\n\txor.b32 " R ", " R ", xt;\n\t"
 #define SM_XF64(R) "shr.s64 xt, " R ", 63;\n\tand.b64 xt, xt, 0x7fffffffffffffff;\n\txor.b64 " R ", " R ", xt;\n\t"
+
 SM_DEF_SMEM_OPS(FView<int32_t>, fs32, s32, "32", "r", 4, "x, y", "%2, %3", SM_XF32("x") SM_XF32("y"), SM_XF32("k"),
-                SM_XF32("%0"))
+                SM_XF32("%0"), SM_TAIL_SEL("32", 4, SM_XF32("k")))
 SM_DEF_SMEM_OPS(FView<int64_t>, fs64, s64, "64", "l", 8, "x, y", "%2, %3", SM_XF64("x") SM_XF64("y"), SM_XF64("k"),
-                SM_XF64("%0"))
+                SM_XF64("%0"), SM_TAIL_SEL("64", 8, SM_XF64("k")))
 SM_DEF_SMEM_OPS(Desc<FView<int32_t>>, dfs32, s32, "32", "r", 4, "y, x", "%3, %2", SM_XF32("x") SM_XF32("y"),
-                SM_XF32("k"), SM_XF32("%0"))
+                SM_XF32("k"), SM_XF32("%0"), SM_TAIL_SEL("32", 4, SM_XF32("k")))
 SM_DEF_SMEM_OPS(Desc<FView<int64_t>>, dfs64, s64, "64", "l", 8, "y, x", "%3, %2", SM_XF64("x") SM_XF64("y"),
-                SM_XF64("k"), SM_XF64("%0"))
+                SM_XF64("k"), SM_XF64("%0"), SM_TAIL_SEL("64", 8, SM_XF64("k")))
 #undef SM_XF32
 #undef SM_XF64
+
 #undef SM_DEF_SMEM_OPS
+#undef SM_TAIL_PLD
+#undef SM_TAIL_SEL
 
 template <typename K, int STEP>
 __device__ __forceinline__ void lift_probe(uint32_t& sa, uint32_t& sb, int& rem) {
