@@ -5,6 +5,7 @@ import glob
 import os
 import re
 import subprocess
+import sys
 
 import pytest
 
@@ -86,3 +87,37 @@ def test_host_validation_without_gpu(sm):
 def test_tile_constants(sm):
     cap = sm.tile_capacity("u32", True)
     assert cap >= 256 and sm.sort_run("u32", True) >= 256
+
+
+def test_product_path_never_imports_the_oracle():
+    """The oracle is test infrastructure: importing and using the product
+    package (and its distributed module) must not load `oracle` or `synth`,
+    and the package sources never mention them in an import."""
+    import glob as _glob
+    code = (
+        "import sys, build_native; build_native.build();"
+        "import paper_1202_6575_b200, paper_1202_6575_b200.distributed;"
+        "bad = [m for m in sys.modules if m == 'oracle' or m.startswith('oracle.') or m == 'synth'];"
+        "print(bad); sys.exit(1 if bad else 0)")
+    r = subprocess.run([sys.executable, "-c", code], cwd=ROOT, capture_output=True, text=True)
+    assert r.returncode == 0, r.stdout + r.stderr
+    for f in _glob.glob(os.path.join(ROOT, "paper_1202_6575_b200", "**", "*.py"), recursive=True):
+        src = open(f).read()
+        assert not re.search(r"^\s*(import|from)\s+(oracle|synth)\b", src, flags=re.M), f
+
+
+def test_oracle_and_cuda_sources_share_nothing():
+    """No include or import crosses between oracle/ and the CUDA library."""
+    inc = re.compile(r"^\s*(#\s*include|import|from)\s+\S*(paper_1202_6575_b200|sm_device|sm_kernels|stablemerge)",
+                     flags=re.M)
+    for f in _glob_all("oracle"):
+        assert not inc.search(open(f).read()), f
+    for f in _glob_all(os.path.join("paper_1202_6575_b200", "csrc")):
+        assert not re.search(r"^\s*#\s*include\s+\S*oracle", open(f).read(), flags=re.M), f
+
+
+def _glob_all(d):
+    out = []
+    for ext in ("*.c", "*.h", "*.cu", "*.cuh", "*.py"):
+        out += glob.glob(os.path.join(ROOT, d, "**", ext), recursive=True)
+    return out
