@@ -53,17 +53,17 @@
  *               pointers not all set or all NULL; invalid options; n + m > 2^31 - 1
  *               for the batched, wide-payload, plan and merge-path calls
  *               (32-bit in-kernel indices)
+ *   SM_EALIAS   output overlaps an input (the merge is not in place, S:L287)
+ *   SM_ENOMEM   scratch allocation failed
+ *   SM_ECUDA    a CUDA launch or copy failed (see sm_last_error())
+ * Unsorted inputs violate the precondition: the output is then unspecified
+ * (but every write stays inside C).
  * Sizes of 2^31 elements or more (merge_stable, mergesort_stable): the kernels
  * index 32-bit, so the library applies the paper's Steps 1-4 once more at
  * coarse granularity (p blocks of <= 2^29 elements per array, their
  * block-start keys ranked by the rank kernel, the cases on the host) and runs
  * 2p sub-merges below 2^31; a sort sorts chunks of 2^30 and merges them
  * pairwise.  One host synchronisation per coarse partition.
- *   SM_EALIAS   output overlaps an input (the merge is not in place, S:L287)
- *   SM_ENOMEM   scratch allocation failed
- *   SM_ECUDA    a CUDA launch or copy failed (see sm_last_error())
- * Unsorted inputs violate the precondition: the output is then unspecified
- * (but every write stays inside C).
  */
 #ifndef STABLEMERGE_H
 #define STABLEMERGE_H
