@@ -246,7 +246,7 @@ struct TaskDesc {
 // its bulk reads complete.  (A variant with per-warp output buffers, freeing
 // the stage as soon as it was read, measured 2-4% slower on C2: fewer stages
 // fit in shared memory.)
-template <typename K, bool HAS_V, int NC, int VT, int STAGES, int MAXT>
+template <typename K, bool HAS_V, int NC, int VT, int STAGES, int MAXT, typename PV = uint32_t>
 struct K2Layout {
     static constexpr int NV = NC * VT;                     // padded diagonals per stage
     static constexpr int KB = (int)sizeof(K);
@@ -256,7 +256,7 @@ struct K2Layout {
     // phase-aligned to the destination, and for the merge's look-ahead reads
     // past the end of a range.
     static constexpr int KREG = NV * KB + MAXT * 80;
-    static constexpr int VREG = HAS_V ? NV * 4 + MAXT * 80 : 0;
+    static constexpr int VREG = HAS_V ? NV * (int)sizeof(PV) + MAXT * 80 : 0;   // payloads (PV: 4 or 8 bytes)
     static constexpr int STAGE_BYTES = KREG + VREG;
     static constexpr int OFF_DESC = STAGES * STAGE_BYTES;
     static constexpr int OFF_PST = OFF_DESC + STAGES * MAXT * (int)sizeof(TaskDesc);
@@ -324,10 +324,10 @@ __device__ __forceinline__ void store_edge(T* dst, const T* sbuf, int o, int L, 
 // on C3/C4), else only when it runs low (8): the batched and sort-round
 // classifications take more dependent loads (mode 2/1: +46%/+19% when
 // refilled every stage).
-template <typename K, bool HAS_V, int VT, int STAGES, int MAXT, bool FIRSTFIT, typename Lay>
-__device__ __forceinline__ void k2_producer(const K* __restrict__ A, const uint32_t* __restrict__ vA,
-                                            const K* __restrict__ B, const uint32_t* __restrict__ vB,
-                                            const K* C, const uint32_t* vC, const Geom& g,
+template <typename K, bool HAS_V, int VT, int STAGES, int MAXT, bool FIRSTFIT, typename Lay, typename PV>
+__device__ __forceinline__ void k2_producer(const K* __restrict__ A, const PV* __restrict__ vA,
+                                            const K* __restrict__ B, const PV* __restrict__ vB,
+                                            const K* C, const PV* vC, const Geom& g,
                                             const int* __restrict__ xbar, const int* __restrict__ ybar, char* smem,
                                             TaskDesc* desc, int* pst, uint64_t* full, uint64_t* empty) {
     constexpr int NV = Lay::NV;
@@ -446,9 +446,10 @@ __device__ __forceinline__ void k2_producer(const K* __restrict__ A, const uint3
                 d.va_s = issue_span(vstage, vat, vA + ag, la, &full[st]);
                 d.vb_s = issue_span(vstage, vat + span_bytes(vA + ag, la), vB + bg, lb, &full[st]);
                 const int phV = phase_of(vC + off);
-                if (lb == 0 && (d.va_s & 3) == phV) d.obv = d.va_s;
-                else if (la == 0 && (d.vb_s & 3) == phV) d.obv = d.vb_s;
-                else d.obv = vat / 4 + phV;
+                constexpr int VM = 16 / (int)sizeof(PV) - 1;   // payload phase mask
+                if (lb == 0 && (d.va_s & VM) == phV) d.obv = d.va_s;
+                else if (la == 0 && (d.vb_s & VM) == phV) d.obv = d.vb_s;
+                else d.obv = vat / (int)sizeof(PV) + phV;
             }
             desc[st * MAXT + slot] = d;
             if (lane == last) {
@@ -506,10 +507,10 @@ __global__ void __launch_bounds__(256) k_classify(Geom g, const int* __restrict_
 // cnt <= VT outputs in registers.  Returns false when D lies in no task.
 //   copy = the task is a copy (cases a, e) and out/v were not filled because
 //          the in-place store needs no movement (INPLACE only).
-template <typename K, bool HAS_V, int VT, int MAXT, int LOG2NV, bool INPLACE>
-__device__ __forceinline__ bool k2_compute(const K* sk, const uint32_t* sv, const TaskDesc* desc_s, const int* ps,
+template <typename K, bool HAS_V, int VT, int MAXT, int LOG2NV, bool INPLACE, typename PV>
+__device__ __forceinline__ bool k2_compute(const K* sk, const PV* sv, const TaskDesc* desc_s, const int* ps,
                                            int nt, int D, TaskDesc& td, int& d, int& cnt, bool& write, K (&out)[VT],
-                                           uint32_t (&v)[HAS_V ? VT : 1]) {
+                                           PV (&v)[HAS_V ? VT : 1]) {
     constexpr int KB = (int)sizeof(K);
     write = false;
     cnt = 0;
@@ -618,18 +619,18 @@ __device__ __forceinline__ bool k2_compute(const K* sk, const uint32_t* sv, cons
 //   warp 1 (storer): bulk-stores each task's 16-byte-aligned middle,
 //     plain-stores the edge elements, and frees the stage once the bulk reads
 //     complete (empty[s]), so the consumers never wait on the stores.
-template <typename K, bool HAS_V, int NC, int VT, int STAGES, int MAXT, int MINB>
-__global__ void __launch_bounds__(K2Layout<K, HAS_V, NC, VT, STAGES, MAXT>::THREADS, MINB)
-    k_tasks(const K* __restrict__ A, const uint32_t* __restrict__ vA, const K* __restrict__ B,
-            const uint32_t* __restrict__ vB, K* __restrict__ C, uint32_t* __restrict__ vC, Geom g,
+template <typename K, bool HAS_V, int NC, int VT, int STAGES, int MAXT, int MINB, typename PV = uint32_t>
+__global__ void __launch_bounds__(K2Layout<K, HAS_V, NC, VT, STAGES, MAXT, PV>::THREADS, MINB)
+    k_tasks(const K* __restrict__ A, const PV* __restrict__ vA, const K* __restrict__ B,
+            const PV* __restrict__ vB, K* __restrict__ C, PV* __restrict__ vC, Geom g,
             const int* __restrict__ xbar, const int* __restrict__ ybar) {
-    using Lay = K2Layout<K, HAS_V, NC, VT, STAGES, MAXT>;
+    using Lay = K2Layout<K, HAS_V, NC, VT, STAGES, MAXT, PV>;
     static_assert(NC % 32 == 0 && MAXT <= 32 && STAGES >= 2, "warp-granular roles; one producer lane per task");
     constexpr int NV = Lay::NV;
     constexpr int LOG2NV = 31 - __builtin_clz(NV);   // 2^(LOG2NV+1) - 1 >= NV probes cover any range
     constexpr int EPV = Lay::EPV;
     constexpr int EK = 2 * (EPV - 1);                // key edge elements per store
-    constexpr int EV = HAS_V ? 6 : 0;                // payload edge elements per store
+    constexpr int EV = HAS_V ? 2 * (16 / (int)sizeof(PV) - 1) : 0;   // payload edge elements per store
     extern __shared__ __align__(128) char smem[];
     TaskDesc* desc = (TaskDesc*)(smem + Lay::OFF_DESC);
     int* pst = (int*)(smem + Lay::OFF_PST);          // [STAGES][MAXT + 2]: pst[0..nt], nt at MAXT+1
@@ -650,7 +651,7 @@ __global__ void __launch_bounds__(K2Layout<K, HAS_V, NC, VT, STAGES, MAXT>::THRE
     pdl_wait();   // the single synchronisation (L373-375): all ranks visible
 
     if (threadIdx.x < 32) {
-        k2_producer<K, HAS_V, VT, STAGES, MAXT, (sizeof(K) == 4 && !HAS_V), Lay>(A, vA, B, vB, C, vC, g, xbar, ybar,
+        k2_producer<K, HAS_V, VT, STAGES, MAXT, (sizeof(K) == 4 && !HAS_V), Lay, PV>(A, vA, B, vB, C, vC, g, xbar, ybar,
                                                                                smem, desc, pst, full, empty);
         return;
     }
@@ -664,13 +665,13 @@ __global__ void __launch_bounds__(K2Layout<K, HAS_V, NC, VT, STAGES, MAXT>::THRE
             const int nt = pst[s * (MAXT + 2) + MAXT + 1];
             if (nt < 0) break;
             const K* sk = (const K*)(smem + s * Lay::STAGE_BYTES);
-            const uint32_t* sv = (const uint32_t*)(smem + s * Lay::STAGE_BYTES + Lay::KREG);
+            const PV* sv = (const PV*)(smem + s * Lay::STAGE_BYTES + Lay::KREG);
             if (lane < nt) {
                 const TaskDesc& t = desc[s * MAXT + lane];
                 const int L = t.la + t.lb;
                 if (L > 0) {
                     store_middle<K>(C + t.off, sk, t.ob, L);
-                    if (HAS_V) store_middle<uint32_t>(vC + t.off, sv, t.obv, L);
+                    if (HAS_V) store_middle<PV>(vC + t.off, sv, t.obv, L);
                 }
                 bulk_commit();
             }
@@ -680,7 +681,7 @@ __global__ void __launch_bounds__(K2Layout<K, HAS_V, NC, VT, STAGES, MAXT>::THRE
                     const TaskDesc& t = desc[s * MAXT + k];
                     const int L = t.la + t.lb;
                     if (r < EK) store_edge<K>(C + t.off, sk, t.ob, L, r);
-                    else if (HAS_V) store_edge<uint32_t>(vC + t.off, sv, t.obv, L, r - EK);
+                    else if (HAS_V) store_edge<PV>(vC + t.off, sv, t.obv, L, r - EK);
                 }
             }
             bulk_wait_read<0>();                       // this lane's bulk stores have read the stage
@@ -703,13 +704,13 @@ __global__ void __launch_bounds__(K2Layout<K, HAS_V, NC, VT, STAGES, MAXT>::THRE
             break;
         }
         K* sk = (K*)(smem + s * Lay::STAGE_BYTES);
-        uint32_t* sv = (uint32_t*)(smem + s * Lay::STAGE_BYTES + Lay::KREG);
+        PV* sv = (PV*)(smem + s * Lay::STAGE_BYTES + Lay::KREG);
         TaskDesc td;
         int d = 0, cnt = 0;
         bool write = false;
         K out[VT];
-        uint32_t v[HAS_V ? VT : 1];
-        k2_compute<K, HAS_V, VT, MAXT, LOG2NV, true>(sk, sv, desc + s * MAXT, ps, nt, c * VT, td, d, cnt, write, out,
+        PV v[HAS_V ? VT : 1];
+        k2_compute<K, HAS_V, VT, MAXT, LOG2NV, true, PV>(sk, sv, desc + s * MAXT, ps, nt, c * VT, td, d, cnt, write, out,
                                                     v);
         named_sync(1, NC);                             // every input of the stage has been read
         if (write) {

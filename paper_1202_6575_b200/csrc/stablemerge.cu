@@ -45,9 +45,9 @@ struct K2Geo {
     static constexpr int NV = NC * VT;
     static constexpr int T = NV / 2;
 };
-template <typename K, bool HAS_V>
+template <typename K, bool HAS_V, typename PV = uint32_t>
 struct K2Shape {
-    static constexpr int bytes = (int)sizeof(K) + (HAS_V ? 4 : 0);
+    static constexpr int bytes = (int)sizeof(K) + (HAS_V ? (int)sizeof(PV) : 0);
     using type = typename std::conditional<
         bytes <= 4, K2Geo<352, 23, 3, 2>,
         typename std::conditional<bytes <= 8, K2Geo<256, 15, 3, 2>,
@@ -220,12 +220,12 @@ static sm_status launch_cross_ranks(const K* A, const K* B, const Geom& g, const
     return check_launch("k_cross_ranks");
 }
 
-template <typename K, bool HAS_V, typename Sh>
-static sm_status launch_tasks(const K* A, const uint32_t* vA, const K* B, const uint32_t* vB, K* C, uint32_t* vC,
+template <typename K, bool HAS_V, typename Sh, typename PV = uint32_t>
+static sm_status launch_tasks(const K* A, const PV* vA, const K* B, const PV* vB, K* C, PV* vC,
                               const Geom& g, const GeomCounts& gc, const int* xbar, const int* ybar, cudaStream_t st,
                               bool pdl) {
-    using Lay = K2Layout<K, HAS_V, Sh::NC, Sh::VT, Sh::STAGES, K2_MAXT>;
-    auto kern = k_tasks<K, HAS_V, Sh::NC, Sh::VT, Sh::STAGES, K2_MAXT, Sh::MINB>;
+    using Lay = K2Layout<K, HAS_V, Sh::NC, Sh::VT, Sh::STAGES, K2_MAXT, PV>;
+    auto kern = k_tasks<K, HAS_V, Sh::NC, Sh::VT, Sh::STAGES, K2_MAXT, Sh::MINB, PV>;
     static int per_sm = -1, n_sm = 0;
     if (per_sm < 0) {
         int dev = 0;
@@ -259,9 +259,9 @@ static sm_status launch_tasks(const K* A, const uint32_t* vA, const K* B, const 
     return SM_OK;
 }
 
-template <typename K, bool HAS_V>
-static sm_status launch_merge(const K* A, const uint32_t* vA, const K* B, const uint32_t* vB, K* C,
-                              uint32_t* vC, const Geom& g0, int* xbar, int* ybar, cudaStream_t st, bool pdl,
+template <typename K, bool HAS_V, typename PV = uint32_t>
+static sm_status launch_merge(const K* A, const PV* vA, const K* B, const PV* vB, K* C,
+                              PV* vC, const Geom& g0, int* xbar, int* ybar, cudaStream_t st, bool pdl,
                               const GeomCounts* counts = nullptr, int4* tdesc = nullptr) {
     const GeomCounts gc = counts ? *counts : geom_counts(g0);
     sm_status s = launch_cross_ranks<K>(A, B, g0, gc, xbar, ybar, st, pdl);
@@ -269,7 +269,7 @@ static sm_status launch_merge(const K* A, const uint32_t* vA, const K* B, const 
     Geom g = g0;
     if (tdesc && gc.tasks > 0) {
         // segmented modes: classify every task once, ahead of K2 (k_classify)
-        using Sh = typename K2Shape<K, HAS_V>::type;
+        using Sh = typename K2Shape<K, HAS_V, PV>::type;
         cudaLaunchConfig_t cfg;
         memset(&cfg, 0, sizeof(cfg));
         cfg.gridDim = dim3((unsigned)((gc.tasks + 255) / 256));
@@ -286,7 +286,8 @@ static sm_status launch_merge(const K* A, const uint32_t* vA, const K* B, const 
         if (s != SM_OK) return s;
         g.tdesc = tdesc;
     }
-    return launch_tasks<K, HAS_V, typename K2Shape<K, HAS_V>::type>(A, vA, B, vB, C, vC, g, gc, xbar, ybar, st, pdl);
+    return launch_tasks<K, HAS_V, typename K2Shape<K, HAS_V, PV>::type, PV>(A, vA, B, vB, C, vC, g, gc, xbar, ybar,
+                                                                          st, pdl);
 }
 
 // ------------------------------------------------ host-memory staging
@@ -342,9 +343,9 @@ static bool overlaps(const void* p, size_t pb, const void* q, size_t qb) {
 }
 
 // ------------------------------------------------------------ merge
-template <typename K>
-static sm_status merge_device(const K* A, const uint32_t* vA, int64_t n, const K* B, const uint32_t* vB, int64_t m,
-                              K* C, uint32_t* vC, cudaStream_t st, int64_t pA, int64_t pB, bool pdl,
+template <typename K, typename PV = uint32_t>
+static sm_status merge_device(const K* A, const PV* vA, int64_t n, const K* B, const PV* vB, int64_t m,
+                              K* C, PV* vC, cudaStream_t st, int64_t pA, int64_t pB, bool pdl,
                               int* ranks_given = nullptr) {
     Geom g{};
     g.S = 1; g.pA = (int)pA; g.pB = (int)pB; g.n = (int)n; g.m = (int)m; g.L = 0; g.N = 0; g.sort = 0;
@@ -352,8 +353,8 @@ static sm_status merge_device(const K* A, const uint32_t* vA, int64_t n, const K
     sm_status s = SM_OK;
     if (!ranks) s = dalloc(&ranks, (pA + 1) + (pB + 1), st);
     if (s != SM_OK) return s;
-    if (vC) s = launch_merge<K, true>(A, vA, B, vB, C, vC, g, ranks, ranks + pA + 1, st, pdl);
-    else s = launch_merge<K, false>(A, nullptr, B, nullptr, C, nullptr, g, ranks, ranks + pA + 1, st, pdl);
+    if (vC) s = launch_merge<K, true, PV>(A, vA, B, vB, C, vC, g, ranks, ranks + pA + 1, st, pdl);
+    else s = launch_merge<K, false, PV>(A, nullptr, B, nullptr, C, nullptr, g, ranks, ranks + pA + 1, st, pdl);
     if (!ranks_given) dfree(ranks, st);
     return s;
 }
@@ -379,8 +380,8 @@ static sm_status merge_path_device(const K* A, const uint32_t* vA, int64_t n, co
         g.S = 1; g.n = (int)n; g.m = (int)m; g.sort = 3; g.T = (int)W; g.pA = g.pB = 1;
         GeomCounts gc{tiles + 2, tiles};
         if (vC) s = launch_tasks<K, true, typename K2Shape<K, true>::type>(A, vA, B, vB, C, vC, g, gc, split, split, st, pdl);
-        else s = launch_tasks<K, false, typename K2Shape<K, false>::type>(A, nullptr, B, nullptr, C, nullptr, g, gc, split,
-                                                                         split, st, pdl);
+        else s = launch_tasks<K, false, typename K2Shape<K, false>::type, uint32_t>(A, nullptr, B, nullptr, C, nullptr, g,
+                                                                                   gc, split, split, st, pdl);
     }
     dfree(split, st);
     return s;
@@ -770,7 +771,8 @@ static sm_status batch_entry(const K* A, const uint32_t* vA, int64_t n, const in
         g.S = (int)S; g.sort = 2; g.T = (int)T; g.segs = segs; g.totals = totals;
         g.task_seg = task_seg; g.rank_seg = rank_seg;
         if (vC) s = launch_merge<K, true>(A, vA, B, vB, C, vC, g, ranks, ranks, st, true, &gc, tdesc);
-        else s = launch_merge<K, false>(A, nullptr, B, nullptr, C, nullptr, g, ranks, ranks, st, true, &gc, tdesc);
+        else s = launch_merge<K, false, uint32_t>(A, nullptr, B, nullptr, C, nullptr, g, ranks, ranks, st, true, &gc,
+                                                  tdesc);
     }
     dfree(scratch, st);
     return s;
@@ -886,8 +888,8 @@ static sm_status sort_device(K* keys, uint32_t* vals, int64_t N, cudaStream_t st
             int* xbar = ranks;
             int* ybar = ranks + (int64_t)g.S * (g.pA + 1);
             if (vals) s = launch_merge<K, true>(src, vsrc, src, vsrc, d2, vd2, g, xbar, ybar, st, pdl, nullptr, tdesc);
-            else s = launch_merge<K, false>(src, nullptr, src, nullptr, d2, nullptr, g, xbar, ybar, st, pdl, nullptr,
-                                            tdesc);
+            else s = launch_merge<K, false, uint32_t>(src, nullptr, src, nullptr, d2, nullptr, g, xbar, ybar, st, pdl,
+                                                      nullptr, tdesc);
             src = d2;
             vsrc = vd2;
         }
@@ -1188,6 +1190,14 @@ static sm_status merge_wide_entry(const K* A, const void* vA, int64_t n, const K
         return SM_EALIAS;
     if (n + m == 0) return SM_OK;
     keep_pool(st);
+    if (vbytes == 8 && (((uintptr_t)vA | (uintptr_t)vB | (uintptr_t)vC) & 7) == 0) {
+        // 8-byte rows (int64 / double / pairs of 32-bit): the fused path -- K2
+        // moves them as its payload type, no index payload and no gather
+        using Sh8 = typename K2Shape<K, true, uint64_t>::type;
+        return merge_device<K, uint64_t>(A, (const uint64_t*)vA, n, B, (const uint64_t*)vB, m, C, (uint64_t*)vC, st,
+                                         std::max<int64_t>(1, ceil_div(n, Sh8::T)),
+                                         std::max<int64_t>(1, ceil_div(m, Sh8::T)), true);
+    }
     uint32_t* idx = nullptr;
     s = dalloc(&idx, 2 * (n + m), st);
     if (s != SM_OK) return s;
