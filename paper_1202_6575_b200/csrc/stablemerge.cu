@@ -710,9 +710,9 @@ static sm_status merge_entry(const K* A, const uint32_t* vA, int64_t n, const K*
 // S independent stable merges in one call, through the
 // sort rounds' segmented machinery (§3) with a segment
 // table instead of equal runs.  Device pointers only.
-template <typename K>
-static sm_status batch_entry(const K* A, const uint32_t* vA, int64_t n, const int64_t* a_off, const K* B,
-                             const uint32_t* vB, int64_t m, const int64_t* b_off, int64_t S, K* C, uint32_t* vC,
+template <typename K, typename PV = uint32_t>
+static sm_status batch_entry(const K* A, const PV* vA, int64_t n, const int64_t* a_off, const K* B,
+                             const PV* vB, int64_t m, const int64_t* b_off, int64_t S, K* C, PV* vC,
                              void* stream) {
     g_launches = 0;
     g_err[0] = 0;
@@ -728,17 +728,17 @@ static sm_status batch_entry(const K* A, const uint32_t* vA, int64_t n, const in
     } else if (vA || vB) {
         return fail_inval("payload pointers must be all set or all NULL");
     }
-    const size_t kb = sizeof(K), cb = (size_t)(n + m);
-    if (overlaps(C, cb * kb, A, n * kb) || overlaps(C, cb * kb, B, m * kb) || overlaps(C, cb * kb, vA, n * 4) ||
-        overlaps(C, cb * kb, vB, m * 4) || overlaps(vC, cb * 4, A, n * kb) || overlaps(vC, cb * 4, B, m * kb) ||
-        overlaps(vC, cb * 4, vA, n * 4) || overlaps(vC, cb * 4, vB, m * 4) || overlaps(C, cb * kb, vC, cb * 4))
+    const size_t kb = sizeof(K), cb = (size_t)(n + m), vb = sizeof(PV);
+    if (overlaps(C, cb * kb, A, n * kb) || overlaps(C, cb * kb, B, m * kb) || overlaps(C, cb * kb, vA, n * vb) ||
+        overlaps(C, cb * kb, vB, m * vb) || overlaps(vC, cb * vb, A, n * kb) || overlaps(vC, cb * vb, B, m * kb) ||
+        overlaps(vC, cb * vb, vA, n * vb) || overlaps(vC, cb * vb, vB, m * vb) || overlaps(C, cb * kb, vC, cb * vb))
         return SM_EALIAS;
     if (S == 0 || n + m == 0) return SM_OK;
     if (is_host_ptr(A) || is_host_ptr(B) || is_host_ptr(vA) || is_host_ptr(vB) || is_host_ptr(C) || is_host_ptr(vC) ||
         is_host_ptr(a_off) || is_host_ptr(b_off))
         return fail_inval("merge_stable_batched takes device pointers only");
     keep_pool(st);
-    const int64_t T = tile_t((int)sizeof(K), vC != nullptr);
+    const int64_t T = vC ? K2Shape<K, true, PV>::type::T : K2Shape<K, false>::type::T;
     const int nblk = (int)ceil_div(S, BATCH_NT);
     GeomCounts gc;
     gc.tasks = ceil_div(n, T) + ceil_div(m, T) + 2 * S;      // sum over segments of p_A + p_B
@@ -770,9 +770,8 @@ static sm_status batch_entry(const K* A, const uint32_t* vA, int64_t n, const in
         Geom g{};
         g.S = (int)S; g.sort = 2; g.T = (int)T; g.segs = segs; g.totals = totals;
         g.task_seg = task_seg; g.rank_seg = rank_seg;
-        if (vC) s = launch_merge<K, true>(A, vA, B, vB, C, vC, g, ranks, ranks, st, true, &gc, tdesc);
-        else s = launch_merge<K, false, uint32_t>(A, nullptr, B, nullptr, C, nullptr, g, ranks, ranks, st, true, &gc,
-                                                  tdesc);
+        if (vC) s = launch_merge<K, true, PV>(A, vA, B, vB, C, vC, g, ranks, ranks, st, true, &gc, tdesc);
+        else s = launch_merge<K, false, PV>(A, nullptr, B, nullptr, C, nullptr, g, ranks, ranks, st, true, &gc, tdesc);
     }
     dfree(scratch, st);
     return s;
@@ -1229,7 +1228,10 @@ static sm_status batch_wide_entry(const K* A, const void* vA, int64_t n, const i
         overlaps(C, cb * kb, vB, m * vb))
         return SM_EALIAS;
     if (S == 0 || n + m == 0)
-        return batch_entry<K>(A, nullptr, n, a_off, B, nullptr, m, b_off, S, C, nullptr, stream);
+        return batch_entry<K, uint32_t>(A, nullptr, n, a_off, B, nullptr, m, b_off, S, C, nullptr, stream);
+    if (vbytes == 8 && (((uintptr_t)vA | (uintptr_t)vB | (uintptr_t)vC) & 7) == 0)   // fused 64-bit payload
+        return batch_entry<K, uint64_t>(A, (const uint64_t*)vA, n, a_off, B, (const uint64_t*)vB, m, b_off, S, C,
+                                        (uint64_t*)vC, stream);
     keep_pool(st);
     uint32_t* idx = nullptr;
     s = dalloc(&idx, 2 * (n + m), st);

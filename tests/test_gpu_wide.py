@@ -69,10 +69,11 @@ def test_wide_merge_misaligned_rows():
 
 @pytest.mark.parametrize("kt", ["u32", "i64", "f64"])
 @pytest.mark.parametrize("desc", [False, True])
-def test_wide_batched(kt, desc):
+@pytest.mark.parametrize("kind", ["f64x3", "i64"])          # i64: the fused 8-byte path
+def test_wide_batched(kt, desc, kind):
     sm = lib()
-    inp = synth.batch_input(257, 600, kt, DIST[kt], seed=31, payload=False, descending=desc)
-    va, vb = _rows("f64x3", inp.n, 7), _rows("f64x3", inp.m, 8)
+    inp = synth.batch_input(257, 2600, kt, DIST[kt], seed=31, payload=False, descending=desc)
+    va, vb = _rows(kind, inp.n, 7), _rows(kind, inp.m, 8)
     d = inp.to("cuda")
     ck, cv = sm.merge_stable_batched(d.a_keys, va.cuda(), d.a_offsets, d.b_keys, vb.cuda(), d.b_offsets,
                                      key_type=kt, descending=desc)
