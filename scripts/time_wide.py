@@ -34,3 +34,16 @@ for name, (dt, shp) in {"u32 payload (fused)": (None, None), "int64 rows": (torc
     ms = timed(lambda: sm.merge_stable(inp.a_keys, va, inp.b_keys, vb, key_type="u32"))
     gbs = 2 * (n + m) * (4 + pb) / ms / 1e6
     print(f"merge 2^25+2^25 u32 keys + {name}: {ms:.3f} ms, {gbs:.0f} GB/s algorithmic")
+
+N = 1 << 26
+src = synth.sort_input(N, "u32", "bounded:1048576", seed=2, payload=True)
+k0 = src.keys.cuda()
+for name, vals0 in (("u32 payload", src.vals.cuda()), ("int64 rows", src.vals.cuda().to(torch.int64))):
+    k, v = k0.clone(), vals0.clone()
+
+    def run():
+        k.copy_(k0)
+        v.copy_(vals0)
+        sm.mergesort_stable(k, v, key_type="u32")
+    ms = timed(run, 5)
+    print(f"sort 2^26 u32 keys + {name}: {ms:.3f} ms (incl. two input copies)")
