@@ -338,7 +338,7 @@ __device__ __forceinline__ void k2_producer(const K* __restrict__ A, const PV* _
     int la = 0, lb = 0, off = 0, ag = 0, bg = 0;   // window slot `lane`
     int cnt = 0;                                    // slots [0, cnt) hold tasks
     int next = blockIdx.x;                          // next task of this CTA
-    const int refill = (g.sort == 0 && KB + (HAS_V ? 4 : 0) > 8) ? 32 : 8;
+    const int refill = (g.sort == 0 && KB + (HAS_V ? (int)sizeof(PV) : 0) > 8) ? 32 : 8;
     for (int it = 0;; ++it) {
         if (cnt < refill && next < ntasks) {
             const int my = next + (lane - cnt) * (int)gridDim.x;
