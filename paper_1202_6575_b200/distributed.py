@@ -200,7 +200,7 @@ def merge_stable_sharded(a_keys: torch.Tensor, a_vals: Optional[torch.Tensor], b
 
     if peer_access is None:
         peer_access = a_keys.is_cuda and b_keys.is_cuda and dist.get_backend(group) == "nccl" and not custom_ops
-    if peer_access:
+    if peer_access and p > 1:
         return _merge_tasks_peer(tasks, r, p, n, m, x, y, a_keys, a_vals, b_keys, b_vals, ops, group)
 
     # exchange: every task's foreign range from its single holder
@@ -364,6 +364,7 @@ def mergesort_stable_sharded(keys: torch.Tensor, vals: Optional[torch.Tensor], N
     r = dist.get_rank(group)
     if peer_access is None:
         peer_access = keys.is_cuda and dist.get_backend(group) == "nccl" and ops is None
+    peer_access = peer_access and p > 1                  # one rank: nothing to exchange
     ops = ops or CudaOps(key_type, descending)
     xs = block_starts(N, p)
     if keys.shape[0] != xs[r + 1] - xs[r]:
