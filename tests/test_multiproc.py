@@ -71,3 +71,18 @@ def test_aggregate_value_is_whole_job():
     # 2 ranks x 1000 elements x 10 steps in 20 ms (max over ranks) = 1e6 elements/s
     assert bench.aggregate_value(1000, 2, 10, 20.0) == pytest.approx(1e6)
     assert bench.max_over_ranks(3.5, 1) == 3.5
+
+
+def test_reference_arm_prints_one_json_line():
+    """`bench.py --impl reference` (the CPU oracle as the reference arm) runs
+    without a GPU and prints the contract's JSON line."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--config", "1", "--steps", "1",
+                        "--warmup", "1"], cwd=root, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    line = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1])
+    assert line["impl"] == "reference" and line["value"] > 0 and line["cpu_baseline"]["kind"] == "oracle"
+    assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["higher_is_better"] is True
