@@ -486,10 +486,10 @@ sm_status mergesort_stable_ex_desc_f64(double *keys, uint32_t *vals, int64_t N, 
  * Device path: the method runs unchanged with a uint32 INDEX payload (the
  * position of each element in A||B, or in the sort input), then one gather
  * kernel moves row idx[k] to output row k.  merge_stable_wide and
- * merge_stable_batched_wide with 8-byte
- * rows and 8-byte-aligned payload pointers moves them directly as the merge
- * kernel's 64-bit payload (no index, no gather).  Scratch: 2 (n+m) uint32
- * (merge), N uint32 + N rows (sort), stream-ordered as above.
+ * merge_stable_batched_wide with 8-byte rows and 8-byte-aligned payload
+ * pointers move the rows directly as the merge kernel's 64-bit payload (no
+ * index, no gather).  Scratch: 2 (n+m) uint32 (merge), N uint32 + N rows
+ * (sort), stream-ordered as above.
  * ------------------------------------------------------------------- */
 sm_status merge_stable_wide_u32(const uint32_t *keys_A, const void *vals_A, int64_t n,
                                 const uint32_t *keys_B, const void *vals_B, int64_t m,
