@@ -179,11 +179,27 @@ def _sym(op: str, kt: str, descending: bool) -> str:
     return f"{op}_desc_{kt}" if descending else f"{op}_{kt}"
 
 
+_FN = {}
+
+
+def _fn(op: str, kt: str, descending: bool):
+    """(ctypes function, its name), cached per (op, key type, order)."""
+    k = (op, kt, descending)
+    f = _FN.get(k)
+    if f is None:
+        name = _sym(op, kt, descending)
+        f = _FN[k] = (getattr(_lib, name), name)
+    return f
+
+
+_raw_stream = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+
+
 def _stream_for(t: torch.Tensor, stream):
     if stream is not None:
         return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
-    if t.is_cuda:
-        return torch.cuda.current_stream(t.device).cuda_stream
+    if t.is_cuda:   # torch's current stream of the tensor's device (the raw handle: no Stream object)
+        return _raw_stream(t.device.index) if _raw_stream else torch.cuda.current_stream(t.device).cuda_stream
     return 0
 
 
@@ -260,12 +276,15 @@ def merge_stable(a_keys: torch.Tensor, a_vals: Optional[torch.Tensor], b_keys: t
     opt = _options(p_A, p_B, block, (0 if pdl else SM_FLAG_NO_PDL) | (SM_FLAG_MERGE_PATH if merge_path else 0))
     args = (_ptr(a_keys), _ptr(a_vals), n, _ptr(b_keys), _ptr(b_vals), m, _ptr(out_keys), _ptr(out_vals), s)
     if opt is None:
-        fn = _sym("merge_stable", kt, descending)
-        _check(getattr(_lib, fn)(*args), fn)
+        f, name = _fn("merge_stable", kt, descending)
+        st = f(*args)
     else:
-        fn = _sym("merge_stable_ex", kt, descending)
-        _check(getattr(_lib, fn)(*args, ctypes.byref(opt)), fn)
-    _sync_if_host(out_keys, s)
+        f, name = _fn("merge_stable_ex", kt, descending)
+        st = f(*args, ctypes.byref(opt))
+    if st:
+        _check(st, name)
+    if not out_keys.is_cuda:
+        _sync_if_host(out_keys, s)
     return out_keys, out_vals
 
 
