@@ -75,10 +75,13 @@ static bool keys_aligned(std::initializer_list<const void*> ptrs) {
     return true;
 }
 static int64_t tile_t(int key_bytes, bool has_v) { return tile_nv(key_bytes, has_v) / 2; }
-// K3 shape: one run of R = K3_NT * K3_IPT elements per CTA (radix block sort).
-constexpr int K3_NT = 256;
+// K3 shape: one run of R = k3_nt * K3_IPT elements per CTA (radix block sort).
+#ifndef SM_K3_NT_SMALL
+#define SM_K3_NT_SMALL 256
+#endif
 constexpr int K3_IPT = 17;
-constexpr int R_SORT = K3_NT * K3_IPT;
+constexpr int k3_nt(int key_bytes, bool has_v) { return key_bytes + (has_v ? 4 : 0) <= 8 ? SM_K3_NT_SMALL : 256; }
+constexpr int64_t k3_run(int key_bytes, bool has_v) { return (int64_t)k3_nt(key_bytes, has_v) * K3_IPT; }
 // K1: lanes per rank search (see k_cross_ranks).  Many searches: one lane
 // each (the DRAM-probe traffic of wider groups costs more than it saves);
 // for a plain merge the top levels come from a per-CTA shared-memory sample
@@ -838,20 +841,21 @@ static sm_status plan_entry(const K* A, int64_t n, const K* B, int64_t m, int64_
 template <typename K, bool HAS_V>
 static sm_status launch_block_sort(const K* in, const uint32_t* vin, K* out, uint32_t* vout, int64_t N,
                                    unsigned blocks, cudaStream_t st) {
-    using Lay = K3Layout<K, HAS_V, K3_NT, K3_IPT>;
-    auto kern = k_block_sort<K, HAS_V, K3_NT, K3_IPT>;
+    constexpr int NT = k3_nt((int)sizeof(K), HAS_V);
+    using Lay = K3Layout<K, HAS_V, NT, K3_IPT>;
+    auto kern = k_block_sort<K, HAS_V, NT, K3_IPT>;
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Lay::SMEM);
         attr = true;
     }
-    kern<<<blocks, K3_NT, Lay::SMEM, st>>>(in, vin, out, vout, (int)N);
+    kern<<<blocks, NT, Lay::SMEM, st>>>(in, vin, out, vout, (int)N);
     return SM_OK;
 }
 
 template <typename K>
 static sm_status sort_device(K* keys, uint32_t* vals, int64_t N, cudaStream_t st, bool pdl) {
-    const int R = R_SORT;   // initial run length: one K3 tile
+    const int R = (int)k3_run((int)sizeof(K), vals != nullptr);   // initial run length: one K3 tile
     int rounds = 0;
     for (int64_t L = R; L < N; L *= 2) ++rounds;
     K* aux = nullptr;
@@ -983,7 +987,8 @@ static sm_status sort_host_pipelined(K* keys, uint32_t* vals, int64_t N, cudaStr
         return evs[k];
     };
     const int64_t Q = 8;                                    // chunks
-    const int64_t Cs = ceil_div(ceil_div(N, Q), (int64_t)R_SORT) * R_SORT;
+    const int64_t R = k3_run((int)sizeof(K), vals != nullptr);
+    const int64_t Cs = ceil_div(ceil_div(N, Q), R) * R;
     const size_t kb = sizeof(K);
     K *dk = nullptr, *dk2 = nullptr;
     uint32_t *dv = nullptr, *dv2 = nullptr;
@@ -1113,7 +1118,7 @@ static sm_status sort_entry(K* keys, uint32_t* vals, int64_t N, void* stream, co
     if (N < 0) return fail_inval("negative size");
     if (N && !keys) return fail_inval("NULL key pointer with nonzero size");
     if (!keys_aligned<K>({keys})) return fail_inval("128-bit keys must be 16-byte aligned");
-    if (opt && opt->sort_run && opt->sort_run != R_SORT) return fail_inval("sort_run must equal the block-sort tile");
+    if (opt && opt->sort_run && opt->sort_run != k3_run((int)sizeof(K), vals != nullptr)) return fail_inval("sort_run must equal the block-sort tile");
     if (overlaps(keys, N * sizeof(K), vals, N * 4)) return SM_EALIAS;
     const bool pdl = !(opt && (opt->flags & SM_FLAG_NO_PDL));
     if (N <= 1) return SM_OK;
@@ -1355,9 +1360,7 @@ int64_t sm_tile_capacity(int32_t key_bytes, int32_t has_vals) {
 }
 
 int64_t sm_sort_run(int32_t key_bytes, int32_t has_vals) {
-    (void)key_bytes;
-    (void)has_vals;
-    return sm::R_SORT;
+    return sm::k3_run(key_bytes, has_vals != 0);
 }
 
 const char* sm_status_string(sm_status s) {
