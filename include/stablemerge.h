@@ -41,6 +41,12 @@
  * payloads) of 64 MB or more uploads in chunks sorted as they arrive and
  * downloads the last merge round in sub-merges as they finish (one host
  * synchronisation for that round's coarse partition).
+ * Device: a call runs on the device of `stream`, whatever the calling
+ * thread's current device (restored on return); with the NULL, legacy or
+ * per-thread default stream, or a stream under graph capture, it runs on the
+ * current device.  Device buffers must be accessible from that device.
+ * Device-pointer calls can be captured into a CUDA graph (the scratch
+ * allocations become graph memory nodes); host-pointer calls cannot.
  * Ownership: the caller owns every buffer; the library never frees or
  * retains them past the stream point of the call.  Scratch (the two
  * cross-rank arrays of p+1 entries, L373-375; the merge sort's auxiliary

@@ -138,20 +138,30 @@ static sm_status check_launch(const char* what) {
 
 static inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
+// One-time setup is per device: function attributes and memory pools belong
+// to a device's context, and one process may drive several devices.  Devices
+// past SM_MAX_DEV redo the setup at every call.  Concurrent first calls
+// repeat idempotent work only.
+constexpr int SM_MAX_DEV = 64;
+static int current_device() {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    return dev;
+}
+
 // The default memory pool keeps freed blocks (no release at every sync), so
 // the per-call rank arrays cost no cudaMalloc after the first call.
 static void keep_pool(cudaStream_t) {
-    static bool done = false;
-    if (done) return;
-    int dev = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess) return;
+    static bool done[SM_MAX_DEV];
+    const int dev = current_device();
+    if (dev < SM_MAX_DEV && done[dev]) return;
     cudaMemPool_t pool;
     if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
         uint64_t thr = UINT64_MAX;
         cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
     }
     cudaGetLastError();
-    done = true;
+    if (dev < SM_MAX_DEV) done[dev] = true;
 }
 
 template <typename T>
@@ -229,15 +239,19 @@ static sm_status launch_tasks(const K* A, const PV* vA, const K* B, const PV* vB
                               bool pdl) {
     using Lay = K2Layout<K, HAS_V, Sh::NC, Sh::VT, Sh::STAGES, K2_MAXT, PV>;
     auto kern = k_tasks<K, HAS_V, Sh::NC, Sh::VT, Sh::STAGES, K2_MAXT, Sh::MINB, PV>;
-    static int per_sm = -1, n_sm = 0;
-    if (per_sm < 0) {
-        int dev = 0;
-        cudaGetDevice(&dev);
+    static int per_sm_d[SM_MAX_DEV], n_sm_d[SM_MAX_DEV];   // 0: not yet set up on that device
+    const int dev = current_device();
+    int per_sm = dev < SM_MAX_DEV ? per_sm_d[dev] : 0, n_sm = dev < SM_MAX_DEV ? n_sm_d[dev] : 0;
+    if (per_sm == 0) {
         cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Lay::SMEM);
         cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, Lay::THREADS, Lay::SMEM);
         if (per_sm < 1) per_sm = 1;
+        if (dev < SM_MAX_DEV) {
+            n_sm_d[dev] = n_sm;
+            per_sm_d[dev] = per_sm;
+        }
     }
     const long long grid = std::max(1ll, std::min<long long>(gc.tasks, (long long)per_sm * n_sm));
     cudaLaunchConfig_t cfg;
@@ -304,6 +318,36 @@ static bool is_host_ptr(const void* p) {
     }
     return a.type == cudaMemoryTypeHost || a.type == cudaMemoryTypeUnregistered;
 }
+
+// A call runs on the device of its stream, whatever the calling thread's
+// current device (restored on return); the NULL, legacy and per-thread
+// default streams, and a stream under graph capture, mean the current device.
+struct DevGuard {
+    int prev = -1;
+    explicit DevGuard(void* stream) {
+        cudaStream_t st = (cudaStream_t)stream;
+        if (!st || st == cudaStreamLegacy || st == cudaStreamPerThread) return;
+        // a stream under graph capture is not queried (the query would
+        // invalidate the capture): the capturing thread's device is used
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) {
+            cudaGetLastError();
+            return;
+        }
+        int dev = 0, cur = 0;
+        if (cudaStreamGetDevice(st, &dev) != cudaSuccess) {
+            cudaGetLastError();
+            return;
+        }
+        cudaGetDevice(&cur);
+        if (dev != cur && cudaSetDevice(dev) == cudaSuccess) prev = cur;
+    }
+    ~DevGuard() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+    DevGuard(const DevGuard&) = delete;
+    DevGuard& operator=(const DevGuard&) = delete;
+};
 
 // One staged buffer: a device copy of a host range (in and/or out).
 struct Stage {
@@ -634,6 +678,7 @@ static sm_status merge_any_device(const K* A, const uint32_t* vA, int64_t n, con
 template <typename K>
 static sm_status merge_entry(const K* A, const uint32_t* vA, int64_t n, const K* B, const uint32_t* vB, int64_t m,
                              K* C, uint32_t* vC, void* stream, const sm_options* opt) {
+    DevGuard dev_guard(stream);
     g_launches = 0;
     g_err[0] = 0;
     cudaStream_t st = (cudaStream_t)stream;
@@ -717,6 +762,7 @@ template <typename K, typename PV = uint32_t>
 static sm_status batch_entry(const K* A, const PV* vA, int64_t n, const int64_t* a_off, const K* B,
                              const PV* vB, int64_t m, const int64_t* b_off, int64_t S, K* C, PV* vC,
                              void* stream) {
+    DevGuard dev_guard(stream);
     g_launches = 0;
     g_err[0] = 0;
     cudaStream_t st = (cudaStream_t)stream;
@@ -784,6 +830,7 @@ static sm_status batch_entry(const K* A, const PV* vA, int64_t n, const int64_t*
 template <typename K>
 static sm_status ranks_entry(const K* X, int64_t len, const K* keys, int64_t nkeys, int32_t high, int64_t* out,
                              void* stream) {
+    DevGuard dev_guard(stream);
     g_launches = 0;
     g_err[0] = 0;
     cudaStream_t st = (cudaStream_t)stream;
@@ -805,6 +852,7 @@ __global__ void k_widen(const int* __restrict__ in, int64_t* __restrict__ out, i
 template <typename K>
 static sm_status plan_entry(const K* A, int64_t n, const K* B, int64_t m, int64_t pA, int64_t pB, int64_t* xbar,
                             int64_t* ybar, int64_t* tasks, void* stream) {
+    DevGuard dev_guard(stream);
     g_launches = 0;
     g_err[0] = 0;
     cudaStream_t st = (cudaStream_t)stream;
@@ -844,10 +892,11 @@ static sm_status launch_block_sort(const K* in, const uint32_t* vin, K* out, uin
     constexpr int NT = k3_nt((int)sizeof(K), HAS_V);
     using Lay = K3Layout<K, HAS_V, NT, K3_IPT>;
     auto kern = k_block_sort<K, HAS_V, NT, K3_IPT>;
-    static bool attr = false;
-    if (!attr) {
+    static bool attr[SM_MAX_DEV];
+    const int dev = current_device();
+    if (dev >= SM_MAX_DEV || !attr[dev]) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Lay::SMEM);
-        attr = true;
+        if (dev < SM_MAX_DEV) attr[dev] = true;
     }
     kern<<<blocks, NT, Lay::SMEM, st>>>(in, vin, out, vout, (int)N);
     return SM_OK;
@@ -1112,6 +1161,7 @@ static sm_status sort_host_pipelined(K* keys, uint32_t* vals, int64_t N, cudaStr
 
 template <typename K>
 static sm_status sort_entry(K* keys, uint32_t* vals, int64_t N, void* stream, const sm_options* opt) {
+    DevGuard dev_guard(stream);
     g_launches = 0;
     g_err[0] = 0;
     cudaStream_t st = (cudaStream_t)stream;
@@ -1177,6 +1227,7 @@ static sm_status wide_check(int64_t vbytes, std::initializer_list<const void*> p
 template <typename K>
 static sm_status merge_wide_entry(const K* A, const void* vA, int64_t n, const K* B, const void* vB, int64_t m, K* C,
                                   void* vC, int64_t vbytes, void* stream) {
+    DevGuard dev_guard(stream);
     g_launches = 0;
     g_err[0] = 0;
     cudaStream_t st = (cudaStream_t)stream;
@@ -1219,6 +1270,7 @@ template <typename K>
 static sm_status batch_wide_entry(const K* A, const void* vA, int64_t n, const int64_t* a_off, const K* B,
                                   const void* vB, int64_t m, const int64_t* b_off, int64_t S, K* C, void* vC,
                                   int64_t vbytes, void* stream) {
+    DevGuard dev_guard(stream);
     cudaStream_t st = (cudaStream_t)stream;
     g_launches = 0;
     g_err[0] = 0;
@@ -1252,6 +1304,7 @@ static sm_status batch_wide_entry(const K* A, const void* vA, int64_t n, const i
 
 template <typename K>
 static sm_status sort_wide_entry(K* keys, void* vals, int64_t N, int64_t vbytes, void* stream) {
+    DevGuard dev_guard(stream);
     g_launches = 0;
     g_err[0] = 0;
     cudaStream_t st = (cudaStream_t)stream;
