@@ -949,6 +949,9 @@ __global__ void k_plan_dump(Geom g, const int* __restrict__ xbar, const int* __r
 //     thread's base offset per digit -- equal digits keep sequence order;
 //   - a partial last run is padded with the maximum unsigned view AFTER the
 //     real elements: stability keeps the padding last, and it is never stored.
+#ifndef SM_K3_NBUF
+#define SM_K3_NBUF 1
+#endif
 template <typename K, bool HAS_V, int NT, int IPT>
 struct K3Layout {
     using U = typename KeyOrd<K>::U;
@@ -956,8 +959,9 @@ struct K3Layout {
     static constexpr int NW = NT / 32;
     static constexpr int ND = 16;                        // 4-bit digits
     static constexpr int ROW = ND + 1;                   // padded per-thread base row
-    static constexpr int OFF_V = 2 * R * (int)sizeof(U);
-    static constexpr int OFF_ROW = OFF_V + (HAS_V ? 2 * R * 4 : 0);
+    static constexpr int NBUF = SM_K3_NBUF;              // 1: passes scatter in place
+    static constexpr int OFF_V = NBUF * R * (int)sizeof(U);
+    static constexpr int OFF_ROW = OFF_V + (HAS_V ? NBUF * R * 4 : 0);
     static constexpr int OFF_W = OFF_ROW + NT * ROW * 4; // warp totals [NW][ND]
     static constexpr int OFF_RED = OFF_W + NW * ND * 4;
     static constexpr int SMEM = OFF_RED + NW * (int)sizeof(U) + 16;
@@ -969,14 +973,18 @@ __device__ __forceinline__ uint32_t cnt_get(uint64_t lo, uint64_t hi, int d) {
     return (uint32_t)(w >> ((d & 7) * 8)) & 0xFFu;
 }
 
+#ifndef SM_K3_MINB
+#define SM_K3_MINB 2
+#endif
 template <typename K, bool HAS_V, int NT, int IPT>
-__global__ void __launch_bounds__(NT) k_block_sort(const K* __restrict__ in, const uint32_t* __restrict__ vin,
+__global__ void __launch_bounds__(NT, sizeof(K) <= 8 ? SM_K3_MINB : 1) k_block_sort(const K* __restrict__ in, const uint32_t* __restrict__ vin,
                                                    K* __restrict__ out, uint32_t* __restrict__ vout, int N) {
     using Lay = K3Layout<K, HAS_V, NT, IPT>;
     using U = typename Lay::U;
     constexpr int R = Lay::R, NW = Lay::NW, ND = Lay::ND, ROW = Lay::ROW;
     constexpr int NDIG = (int)sizeof(U) * 2;             // 4-bit digits per key
-    static_assert(IPT % 2 == 1 && IPT < 256 && NT % 32 == 0 && NT >= 32, "odd IPT; 8-bit counters");
+    static_assert(IPT % 2 == 1 && IPT < 256 && NT % 32 == 0 && NT >= 32 && R < 65536,
+                  "odd IPT; 8-bit counters; 16-bit scan fields");
     extern __shared__ __align__(128) char smem[];
     U* ku0 = (U*)smem;
     uint32_t* vv0 = (uint32_t*)(smem + Lay::OFF_V);
@@ -1029,21 +1037,29 @@ __global__ void __launch_bounds__(NT) k_block_sort(const K* __restrict__ in, con
     for (int dg = 0; dg < NDIG; ++dg) {
         const int sh = dg * 4;
         if (((diff >> sh) & 0xF) == 0) continue;       // every key of the run has this digit
+        // in place (NBUF = 1): every thread has read its items (step 1)
+        // before the first barrier of the pass, the scatter follows the second
         const U* ks = ku0 + cur * R;
-        U* kd = ku0 + (cur ^ 1) * R;
+        U* kd = ku0 + ((cur ^ 1) % Lay::NBUF) * R;
         const uint32_t* vs = vv0 + cur * R;
-        uint32_t* vd = vv0 + (cur ^ 1) * R;
+        uint32_t* vd = vv0 + ((cur ^ 1) % Lay::NBUF) * R;
         // 1. this thread's items (blocked) and in-thread ranks
+        // long runs (IPT > 17): ranks packed two 16-bit fields per register
+        // (every rank < R < 2^16), so the pass fits two CTAs per SM
+        constexpr bool PACK = IPT > 17;
         U key[IPT];
         uint32_t val[HAS_V ? IPT : 1];
-        uint32_t rank[IPT];
+        uint32_t rank[PACK ? (IPT + 1) / 2 : IPT];
         uint64_t clo = 0, chi = 0;
 #pragma unroll
         for (int k = 0; k < IPT; ++k) {
             key[k] = ks[tid * IPT + k];
             if (HAS_V) val[k] = vs[tid * IPT + k];
             const int d = (int)(key[k] >> sh) & 0xF;
-            rank[k] = cnt_get(clo, chi, d);
+            const uint32_t r0 = cnt_get(clo, chi, d);
+            if (!PACK) rank[k] = r0;
+            else if (k & 1) rank[k >> 1] |= r0 << 16;
+            else rank[k >> 1] = r0;
             const uint64_t inc = 1ull << ((d & 7) * 8);
             if (d < 8) clo += inc;
             else chi += inc;
@@ -1104,15 +1120,17 @@ __global__ void __launch_bounds__(NT) k_block_sort(const K* __restrict__ in, con
 #pragma unroll
         for (int k = 0; k < IPT; ++k) {
             const int d = (int)(key[k] >> sh) & 0xF;
-            rank[k] += rowb[tid * ROW + d];
+            if (PACK) rank[k >> 1] += rowb[tid * ROW + d] << (16 * (k & 1));
+            else rank[k] += rowb[tid * ROW + d];
         }
 #pragma unroll
         for (int k = 0; k < IPT; ++k) {
-            kd[rank[k]] = key[k];
-            if (HAS_V) vd[rank[k]] = val[k];
+            const uint32_t at = PACK ? (rank[k >> 1] >> (16 * (k & 1))) & 0xFFFFu : rank[k];
+            kd[at] = key[k];
+            if (HAS_V) vd[at] = val[k];
         }
         __syncthreads();
-        cur ^= 1;
+        cur = (cur ^ 1) % Lay::NBUF;
     }
     const U* kf = ku0 + cur * R;
     const uint32_t* vf = vv0 + cur * R;

@@ -75,13 +75,21 @@ static bool keys_aligned(std::initializer_list<const void*> ptrs) {
     return true;
 }
 static int64_t tile_t(int key_bytes, bool has_v) { return tile_nv(key_bytes, has_v) / 2; }
-// K3 shape: one run of R = k3_nt * K3_IPT elements per CTA (radix block sort).
+// K3 shape: one run of R = k3_nt * k3_ipt elements per CTA (radix block sort),
+// two CTAs per SM.  Key + payload slots of <= 8 bytes: 256 x 33 = 8448
+// (>= 2^13: one merge round fewer than 256 x 17 for N = 2^28; C5 14.96 vs
+// 15.92 ms); wider slots: 256 x 17 = 4352 (shared memory).
 #ifndef SM_K3_NT_SMALL
 #define SM_K3_NT_SMALL 256
 #endif
+#ifndef SM_K3_IPT_SMALL
+#define SM_K3_IPT_SMALL 33
+#endif
 constexpr int K3_IPT = 17;
-constexpr int k3_nt(int key_bytes, bool has_v) { return key_bytes + (has_v ? 4 : 0) <= 8 ? SM_K3_NT_SMALL : 256; }
-constexpr int64_t k3_run(int key_bytes, bool has_v) { return (int64_t)k3_nt(key_bytes, has_v) * K3_IPT; }
+constexpr bool k3_small(int key_bytes, bool has_v) { return key_bytes + (has_v ? 4 : 0) <= 8; }
+constexpr int k3_nt(int key_bytes, bool has_v) { return k3_small(key_bytes, has_v) ? SM_K3_NT_SMALL : 256; }
+constexpr int k3_ipt(int key_bytes, bool has_v) { return k3_small(key_bytes, has_v) ? SM_K3_IPT_SMALL : K3_IPT; }
+constexpr int64_t k3_run(int key_bytes, bool has_v) { return (int64_t)k3_nt(key_bytes, has_v) * k3_ipt(key_bytes, has_v); }
 // K1: lanes per rank search (see k_cross_ranks).  Many searches: one lane
 // each (the DRAM-probe traffic of wider groups costs more than it saves);
 // for a plain merge the top levels come from a per-CTA shared-memory sample
@@ -889,9 +897,9 @@ static sm_status plan_entry(const K* A, int64_t n, const K* B, int64_t m, int64_
 template <typename K, bool HAS_V>
 static sm_status launch_block_sort(const K* in, const uint32_t* vin, K* out, uint32_t* vout, int64_t N,
                                    unsigned blocks, cudaStream_t st) {
-    constexpr int NT = k3_nt((int)sizeof(K), HAS_V);
-    using Lay = K3Layout<K, HAS_V, NT, K3_IPT>;
-    auto kern = k_block_sort<K, HAS_V, NT, K3_IPT>;
+    constexpr int NT = k3_nt((int)sizeof(K), HAS_V), IPT = k3_ipt((int)sizeof(K), HAS_V);
+    using Lay = K3Layout<K, HAS_V, NT, IPT>;
+    auto kern = k_block_sort<K, HAS_V, NT, IPT>;
     static bool attr[SM_MAX_DEV];
     const int dev = current_device();
     if (dev >= SM_MAX_DEV || !attr[dev]) {
