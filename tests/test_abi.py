@@ -87,6 +87,9 @@ def test_host_validation_without_gpu(sm):
 def test_tile_constants(sm):
     cap = sm.tile_capacity("u32", True)
     assert cap >= 256 and sm.sort_run("u32", True) >= 256
+    # block-sort runs: 256 x 33 for key + payload slots of <= 8 bytes, else 256 x 17
+    assert [sm.sort_run(kt, v) for kt, v in (("u32", True), ("i32", False), ("i64", False), ("u64", True),
+                                             ("f64", True), ("u128", False))] == [8448, 8448, 8448, 4352, 4352, 4352]
 
 
 def test_product_path_never_imports_the_oracle():

@@ -28,16 +28,18 @@ def test_sort_ragged(kt, N):
         assert_bit_exact(*gpu_sort(sm, inp), *want, kt)
 
 
+@pytest.mark.parametrize("payload", [True, False])
 @pytest.mark.parametrize("kt", ["u32", "i32", "i64", "u64", "f32", "f64"])
-def test_sort_run_boundaries(kt):
-    """Sizes around the block-sort run length R and its powers of two
-    (the number of merge rounds changes there), full-range and narrow keys
-    (the block sort skips digits all keys of a run share)."""
+def test_sort_run_boundaries(kt, payload):
+    """Sizes around the block-sort run length R (which depends on the key +
+    payload width) and its powers of two (the number of merge rounds changes
+    there), full-range and narrow keys (the block sort skips digits all keys
+    of a run share)."""
     sm = lib()
-    R = sm.sort_run(kt, True)
+    R = sm.sort_run(kt, payload)
     for N in (R - 1, R, R + 1, 2 * R - 1, 2 * R + 3, 4 * R, 5 * R + 7):
         for dist in ("full", "bounded:3", "equal") + (("special",) if kt.startswith("f") else ()):
-            inp = synth.sort_input(N, kt, dist, seed=N, payload=True)
+            inp = synth.sort_input(N, kt, dist, seed=N, payload=payload)
             want = oracle.sort(inp.keys, inp.vals, kt)
             assert_bit_exact(*gpu_sort(sm, inp), *want, kt)
 
