@@ -18,7 +18,7 @@ LIB = os.path.join(LIBDIR, "libstablemerge.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "-shared", "--expt-relaxed-constexpr"]
+COMPILE_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "--expt-relaxed-constexpr"]
 
 
 def sources():
@@ -37,17 +37,30 @@ def up_to_date() -> bool:
     return all(os.path.getmtime(d) <= t for d in deps())
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and up_to_date():
+def build(force: bool = False, verbose: bool = False, out: str = LIB, extra_flags=None) -> str:
+    """One object per translation unit (sm_common.cu + one abi_<key>.cu per key
+    type), compiled in parallel, then linked into the shared library."""
+    if out == LIB and extra_flags is None and not force and up_to_date():
         return LIB
-    os.makedirs(LIBDIR, exist_ok=True)
-    extra = os.environ.get("SM_NVCC_EXTRA", "").split()     # tuning experiments (-D...)
-    cmd = [NVCC, *ARCH, *FLAGS, *extra, "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-o", LIB, *sources()]
-    if verbose:
-        cmd.insert(1, "-Xptxas=-v")
-        print(" ".join(cmd), flush=True)
-    subprocess.check_call(cmd)
-    return LIB
+    os.makedirs(os.path.dirname(out), exist_ok=True)
+    objdir = os.path.join(ROOT, "build", "obj_" + os.path.basename(out).replace(".so", ""))
+    os.makedirs(objdir, exist_ok=True)
+    extra = os.environ.get("SM_NVCC_EXTRA", "").split() if extra_flags is None else list(extra_flags)
+    inc = ["-I", os.path.join(ROOT, "include"), "-I", CSRC]
+    procs, objs = [], []
+    for src in sources():
+        obj = os.path.join(objdir, os.path.basename(src)[:-3] + ".o")
+        cmd = [NVCC, *ARCH, *COMPILE_FLAGS, *extra, *inc, "-c", "-o", obj, src]
+        if verbose:
+            cmd.insert(1, "-Xptxas=-v")
+            print(" ".join(cmd), flush=True)
+        procs.append((src, subprocess.Popen(cmd)))
+        objs.append(obj)
+    failed = [src for src, p in procs if p.wait() != 0]
+    if failed:
+        raise subprocess.CalledProcessError(1, f"nvcc {failed}")
+    subprocess.check_call([NVCC, *ARCH, "-shared", "-o", out, *objs])
+    return out
 
 
 def build_oracle() -> str:

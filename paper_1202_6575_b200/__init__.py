@@ -37,7 +37,9 @@ from typing import Optional
 import torch
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "lib", "libstablemerge.so")
+# SM_LIB_PATH: an alternative build of the same library (tuning experiments:
+# scripts/build_variants.py); the default is the in-tree build.
+LIB_PATH = os.environ.get("SM_LIB_PATH") or os.path.join(_PKG, "lib", "libstablemerge.so")
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"{LIB_PATH} is not built: run `python build_native.py` "

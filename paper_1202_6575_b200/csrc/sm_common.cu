@@ -1,0 +1,100 @@
+// sm_common.cu -- the library's globals (per-thread error text and launch
+// count, the CUDA-event profiler) and the C-ABI calls that do not depend on
+// the key type (include/stablemerge.h).
+#include "sm_host.cuh"
+
+namespace sm {
+
+thread_local char g_err[512] = "";
+thread_local int64_t g_launches = 0;
+
+sm_status fail_cuda(cudaError_t e, const char* what) {
+    snprintf(g_err, sizeof(g_err), "%s: %s", what, cudaGetErrorString(e));
+    return SM_ECUDA;
+}
+
+sm_status fail_inval(const char* what) {
+    snprintf(g_err, sizeof(g_err), "invalid argument: %s", what);
+    return SM_EINVAL;
+}
+
+bool g_prof_on = false;
+std::vector<ProfRec> g_prof_pool;
+size_t g_prof_used = 0;
+
+void prof_before(int kind, cudaStream_t st) {
+    if (!g_prof_on) return;
+    if (g_prof_used == g_prof_pool.size()) {
+        ProfRec r;
+        cudaEventCreate(&r.a);
+        cudaEventCreate(&r.b);
+        g_prof_pool.push_back(r);
+    }
+    g_prof_pool[g_prof_used].kind = kind;
+    cudaEventRecord(g_prof_pool[g_prof_used].a, st);
+}
+
+void prof_after(cudaStream_t st) {
+    if (!g_prof_on) return;
+    cudaEventRecord(g_prof_pool[g_prof_used].b, st);
+    ++g_prof_used;
+}
+
+sm_status check_launch(const char* what) {
+    ++g_launches;
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? SM_OK : fail_cuda(e, what);
+}
+
+}  // namespace sm
+
+extern "C" {
+
+int64_t sm_tile_capacity(int32_t key_bytes, int32_t has_vals) {
+    return sm::tile_nv(key_bytes, has_vals != 0);
+}
+
+int64_t sm_sort_run(int32_t key_bytes, int32_t has_vals) {
+    return sm::k3_run(key_bytes, has_vals != 0);
+}
+
+const char* sm_status_string(sm_status s) {
+    switch (s) {
+        case SM_OK: return "SM_OK";
+        case SM_EINVAL: return "SM_EINVAL: invalid argument";
+        case SM_EALIAS: return "SM_EALIAS: output overlaps an input";
+        case SM_ENOMEM: return "SM_ENOMEM: scratch allocation failed";
+        case SM_ECUDA: return "SM_ECUDA: CUDA error";
+    }
+    return "unknown status";
+}
+
+const char* sm_last_error(void) { return sm::g_err; }
+
+int64_t sm_last_launch_count(void) { return sm::g_launches; }
+
+void sm_profile_enable(int on) {
+    sm::g_prof_on = on != 0;
+    sm::g_prof_used = 0;
+}
+
+sm_status sm_profile_read(int kind, double* total_ms, int64_t* launches) {
+    double t = 0.0;
+    int64_t c = 0;
+    for (size_t i = 0; i < sm::g_prof_used; ++i) {
+        const sm::ProfRec& r = sm::g_prof_pool[i];
+        if (r.kind != kind) continue;
+        cudaError_t e = cudaEventSynchronize(r.b);
+        if (e != cudaSuccess) return sm::fail_cuda(e, "cudaEventSynchronize");
+        float ms = 0.f;
+        e = cudaEventElapsedTime(&ms, r.a, r.b);
+        if (e != cudaSuccess) return sm::fail_cuda(e, "cudaEventElapsedTime");
+        t += ms;
+        ++c;
+    }
+    if (total_ms) *total_ms = t;
+    if (launches) *launches = c;
+    return SM_OK;
+}
+
+}  // extern "C"

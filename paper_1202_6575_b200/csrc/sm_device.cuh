@@ -9,6 +9,7 @@
 #include <string.h>
 
 namespace sm {
+namespace {   // internal linkage: every translation unit keeps its own kernels
 
 // ---------------------------------------------------------------------------
 // Row a0: block partition.
@@ -365,6 +366,7 @@ __device__ __forceinline__ void st_stream(Desc<B>* p, Desc<B> v) { st_stream((B*
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;"); }
 
+}  // namespace
 }  // namespace sm
 
 // ===========================================================================
@@ -372,6 +374,7 @@ __device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepc
 // bulk copies (TMA engine, cp.async.bulk), async-proxy fence, named barriers.
 // ===========================================================================
 namespace sm {
+namespace {   // internal linkage: every translation unit keeps its own kernels
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -449,6 +452,7 @@ __device__ __forceinline__ void named_sync(int id, int count) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
 }
 
+}  // namespace
 }  // namespace sm
 
 // ===========================================================================
@@ -457,12 +461,14 @@ __device__ __forceinline__ void named_sync(int id, int count) {
 // type (signed compare for i32/i64, unsigned for u32/u64, reading R16).
 // ===========================================================================
 namespace sm {
+namespace {   // internal linkage: every translation unit keeps its own kernels
 
 // One binary-lifting probe of the merge-path split (reading R17): with
 // sa = &a[i0], sb = &b[d-1-i0] and `rem` candidates left, if STEP <= rem and
 // a[i0+STEP-1] <= b[d-1-i0-STEP+1] then advance i0 by STEP.
-template <typename K, int STEP>
-__device__ __forceinline__ void lift_probe(uint32_t& sa, uint32_t& sb, int& rem);
+#ifndef SM_SPLIT_SKEW_LEVEL
+#define SM_SPLIT_SKEW_LEVEL 32   // deep split levels probed in a per-thread skewed lattice (0: off)
+#endif
 
 // One output of the serial stable merge: take A when A is not exhausted and
 // (B is exhausted or ka <= kb) -- ties to A.  Advances
@@ -492,17 +498,45 @@ __device__ __forceinline__ K lds(uint32_t addr);
 #define SM_DEF_SMEM_OPS(K, NAME, CMP, BITS, RC, SZ, X_LE_Y, KA_LE_KB, XF_XY, XF_K, XF_0, FAST_TAIL)                                \
     template <int STEP>                                                                                        \
     struct LiftProbe_##NAME {                                                                                  \
-        __device__ __forceinline__ static void run(uint32_t& sa, uint32_t& sb, int& rem) {                     \
+        /* v: virtual candidates left below the range (see LiftProbeV); a step */                             \
+        /* taken here (STEP > v) leaves none */                                                               \
+        __device__ __forceinline__ static void run(uint32_t& sa, uint32_t& sb, int& rem, int& v) {             \
             asm volatile(                                                                                      \
                 "{\n\t.reg .pred p, q;\n\t.reg .b" BITS " x, y, xt;\n\t"                                          \
-                "setp.le.s32 p, %3, %2;\n\t"                                                                   \
-                "@p ld.shared.b" BITS " x, [%0+%4];\n\t"                                                       \
-                "@p ld.shared.b" BITS " y, [%1+%5];\n\t" XF_XY                                                 \
+                "setp.le.s32 p, %4, %2;\n\t"                                                                   \
+                "@p ld.shared.b" BITS " x, [%0+%5];\n\t"                                                       \
+                "@p ld.shared.b" BITS " y, [%1+%6];\n\t" XF_XY                                                 \
                 "setp.le.and." #CMP " q, " X_LE_Y ", p;\n\t"                                                   \
-                "@q add.u32 %0, %0, %6;\n\t"                                                                   \
-                "@q sub.u32 %1, %1, %6;\n\t"                                                                   \
-                "@q sub.s32 %2, %2, %3;\n\t}"                                                                  \
-                : "+r"(sa), "+r"(sb), "+r"(rem)                                                                \
+                "@q add.u32 %0, %0, %7;\n\t"                                                                   \
+                "@q sub.u32 %1, %1, %7;\n\t"                                                                   \
+                "@q sub.s32 %2, %2, %4;\n\t"                                                                   \
+                "@q mov.s32 %3, 0;\n\t}"                                                                       \
+                : "+r"(sa), "+r"(sb), "+r"(rem), "+r"(v)                                                       \
+                : "n"(STEP), "n"((STEP - 1) * SZ), "n"(-(STEP - 1) * SZ), "n"(STEP * SZ)                     \
+                : "memory");                                                                                   \
+        }                                                                                                      \
+    };                                                                                                         \
+    /* The same probe in a lattice shifted down by a per-thread skew: candidates */                       \
+    /* below the search range (v > 0 of them left) are "virtual" and pass without */                          \
+    /* a load.  Used for the deep levels (STEP <= 32), where the unshifted */                                 \
+    /* lattices of neighbouring threads share their residue mod 2*STEP and the */                             \
+    /* probes of a warp pile into two or three banks (measured 6-7-way). */                                   \
+    template <int STEP>                                                                                        \
+    struct LiftProbeV_##NAME {                                                                                 \
+        __device__ __forceinline__ static void run(uint32_t& sa, uint32_t& sb, int& rem, int& v) {             \
+            asm volatile(                                                                                      \
+                "{\n\t.reg .pred p, q, au;\n\t.reg .b" BITS " x, y, xt;\n\t"                                   \
+                "setp.le.s32 au, %4, %3;\n\t"                                                                 \
+                "setp.le.and.s32 p, %4, %2, !au;\n\t"                                                         \
+                "@p ld.shared.b" BITS " x, [%0+%5];\n\t"                                                       \
+                "@p ld.shared.b" BITS " y, [%1+%6];\n\t" XF_XY                                                 \
+                "setp.le.and." #CMP " q, " X_LE_Y ", p;\n\t"                                                   \
+                "or.pred q, q, au;\n\t"                                                                       \
+                "@q add.u32 %0, %0, %7;\n\t"                                                                   \
+                "@q sub.u32 %1, %1, %7;\n\t"                                                                   \
+                "@q sub.s32 %2, %2, %4;\n\t"                                                                   \
+                "@q sub.s32 %3, %3, %4;\n\t}"                                                                  \
+                : "+r"(sa), "+r"(sb), "+r"(rem), "+r"(v)                                                       \
                 : "n"(STEP), "n"((STEP - 1) * SZ), "n"(-(STEP - 1) * SZ), "n"(STEP * SZ)                     \
                 : "memory");                                                                                   \
         }                                                                                                      \
@@ -608,6 +642,7 @@ __device__ __forceinline__ K lds(uint32_t addr);
     template <int STEP>                                                                                        \
     struct LiftSel<K, STEP> {                                                                                  \
         using type = LiftProbe_##NAME<STEP>;                                                                   \
+        using vtype = LiftProbeV_##NAME<STEP>;                                                                 \
     };
 
 template <typename K, int STEP>
@@ -621,14 +656,34 @@ struct LiftSel;
 #define SM_TAIL_PLD(BITS, SZ) "@t ld.shared.b" BITS " %4, [%0+" #SZ "];\n\t@!t ld.shared.b" BITS " %5, [%1+" #SZ "];\n\t"
 #define SM_TAIL_SEL(BITS, SZ, XF) "selp.b32 ad, %0, %1, t;\n\tld.shared.b" BITS " k, [ad+" #SZ "];\n\t" XF \
     "selp.b" BITS " %4, k, %4, t;\n\tselp.b" BITS " %5, %5, k, t;\n\t"
-SM_DEF_SMEM_OPS(uint32_t, u32, u32, "32", "r", 4, "x, y", "%2, %3", "", "", "", SM_TAIL_PLD("32", 4))
-SM_DEF_SMEM_OPS(int32_t, s32, s32, "32", "r", 4, "x, y", "%2, %3", "", "", "", SM_TAIL_PLD("32", 4))
-SM_DEF_SMEM_OPS(uint64_t, u64, u64, "64", "l", 8, "x, y", "%2, %3", "", "", "", SM_TAIL_PLD("64", 8))
-SM_DEF_SMEM_OPS(int64_t, s64, s64, "64", "l", 8, "x, y", "%2, %3", "", "", "", SM_TAIL_PLD("64", 8))
-SM_DEF_SMEM_OPS(Desc<uint32_t>, du32, u32, "32", "r", 4, "y, x", "%3, %2", "", "", "", SM_TAIL_PLD("32", 4))
-SM_DEF_SMEM_OPS(Desc<int32_t>, ds32, s32, "32", "r", 4, "y, x", "%3, %2", "", "", "", SM_TAIL_PLD("32", 4))
-SM_DEF_SMEM_OPS(Desc<uint64_t>, du64, u64, "64", "l", 8, "y, x", "%3, %2", "", "", "", SM_TAIL_PLD("64", 8))
-SM_DEF_SMEM_OPS(Desc<int64_t>, ds64, s64, "64", "l", 8, "y, x", "%3, %2", "", "", "", SM_TAIL_PLD("64", 8))
+// The fast step's load: one load from the selected side (SEL) or two
+// predicated loads, one per side (PLD: off the select's latency, but each
+// costs its own shared-memory wavefronts: 4.6 per warp step against 2.9 for
+// SEL on 4-byte keys, ncu r2).  SM_FAST_PLD32 / SM_FAST_PLD64 pick PLD.
+#ifndef SM_FAST_PLD32
+#define SM_FAST_PLD32 0
+#endif
+#ifndef SM_FAST_PLD64
+#define SM_FAST_PLD64 1
+#endif
+#if SM_FAST_PLD32
+#define SM_TAIL32 SM_TAIL_PLD("32", 4)
+#else
+#define SM_TAIL32 SM_TAIL_SEL("32", 4, "")
+#endif
+#if SM_FAST_PLD64
+#define SM_TAIL64 SM_TAIL_PLD("64", 8)
+#else
+#define SM_TAIL64 SM_TAIL_SEL("64", 8, "")
+#endif
+SM_DEF_SMEM_OPS(uint32_t, u32, u32, "32", "r", 4, "x, y", "%2, %3", "", "", "", SM_TAIL32)
+SM_DEF_SMEM_OPS(int32_t, s32, s32, "32", "r", 4, "x, y", "%2, %3", "", "", "", SM_TAIL32)
+SM_DEF_SMEM_OPS(uint64_t, u64, u64, "64", "l", 8, "x, y", "%2, %3", "", "", "", SM_TAIL64)
+SM_DEF_SMEM_OPS(int64_t, s64, s64, "64", "l", 8, "x, y", "%2, %3", "", "", "", SM_TAIL64)
+SM_DEF_SMEM_OPS(Desc<uint32_t>, du32, u32, "32", "r", 4, "y, x", "%3, %2", "", "", "", SM_TAIL32)
+SM_DEF_SMEM_OPS(Desc<int32_t>, ds32, s32, "32", "r", 4, "y, x", "%3, %2", "", "", "", SM_TAIL32)
+SM_DEF_SMEM_OPS(Desc<uint64_t>, du64, u64, "64", "l", 8, "y, x", "%3, %2", "", "", "", SM_TAIL64)
+SM_DEF_SMEM_OPS(Desc<int64_t>, ds64, s64, "64", "l", 8, "y, x", "%3, %2", "", "", "", SM_TAIL64)
 // Floating-point keys: every shared load is followed by the totalOrder view
 // (sign-magnitude -> two's complement: flip the magnitude bits of negative
 // values, an involution), compared as signed integers; the merged outputs
@@ -650,36 +705,54 @@ SM_DEF_SMEM_OPS(Desc<FView<int64_t>>, dfs64, s64, "64", "l", 8, "y, x", "%3, %2"
 #undef SM_DEF_SMEM_OPS
 #undef SM_TAIL_PLD
 #undef SM_TAIL_SEL
+#undef SM_TAIL32
+#undef SM_TAIL64
 
 template <typename K, int STEP>
-__device__ __forceinline__ void lift_probe(uint32_t& sa, uint32_t& sb, int& rem) {
-    LiftSel<K, STEP>::type::run(sa, sb, rem);
+__device__ __forceinline__ void lift_probe(uint32_t& sa, uint32_t& sb, int& rem, int& v) {
+    if constexpr (STEP <= SM_SPLIT_SKEW_LEVEL) LiftSel<K, STEP>::vtype::run(sa, sb, rem, v);
+    else LiftSel<K, STEP>::type::run(sa, sb, rem, v);
+}
+
+template <typename K, int S>
+struct LiftAll {
+    __device__ __forceinline__ static void run(uint32_t& sa, uint32_t& sb, int& rem, int& v) {
+        lift_probe<K, (1 << S)>(sa, sb, rem, v);
+        LiftAll<K, S - 1>::run(sa, sb, rem, v);
+    }
+};
+template <typename K>
+struct LiftAll<K, -1> {
+    __device__ __forceinline__ static void run(uint32_t&, uint32_t&, int&, int&) {}
+};
+
+// Per-thread skew in [0, 2 * SM_SPLIT_SKEW_LEVEL) from the diagonal (a hash:
+// both the lattice of a[] and that of b[d-1-i] must differ between
+// neighbouring threads; simulated 79 -> 50 wavefronts per warp split).
+__device__ __forceinline__ int split_skew(int d) {
+    return SM_SPLIT_SKEW_LEVEL > 0 ? ((d * 37) >> 3) & (2 * SM_SPLIT_SKEW_LEVEL - 1) : 0;
 }
 
 // Merge-path split at diagonal d of sorted a[0, la) and b[0, lb) held in
 // shared memory at sa0 / sb0 (byte addresses): smallest i in
 // [max(0, d-lb), min(d, la)] with a[i] > b[d-1-i] (reading R17), by
 // LOG2+1 predicated probes (binary lifting; 2^(LOG2+1)-1 >= any range).
-template <typename K, int S>
-struct LiftAll {
-    __device__ __forceinline__ static void run(uint32_t& sa, uint32_t& sb, int& rem) {
-        lift_probe<K, (1 << S)>(sa, sb, rem);
-        LiftAll<K, S - 1>::run(sa, sb, rem);
-    }
-};
-template <typename K>
-struct LiftAll<K, -1> {
-    __device__ __forceinline__ static void run(uint32_t&, uint32_t&, int&) {}
-};
-
+// The lifting starts `skew` (< 2 * SM_SPLIT_SKEW_LEVEL) candidates below the
+// range; those virtual candidates pass without a load (they lie before the
+// split), so the result is unchanged while neighbouring threads probe
+// different residues at the deep levels (bank conflicts of the split: ncu r2
+// 14.5 M of K2's 40.6 M shared wavefronts on C2, ~6.5-way at STEP 4..16).
 template <typename K, int LOG2>
 __device__ __forceinline__ int split_smem(uint32_t sa0, int la, uint32_t sb0, int lb, int d) {
     const int lo = max(0, d - lb);
-    int rem = min(d, la) - lo;
-    uint32_t sa = sa0 + (uint32_t)lo * sizeof(K);
-    uint32_t sb = sb0 + (uint32_t)(d - 1 - lo) * sizeof(K);
-    LiftAll<K, LOG2>::run(sa, sb, rem);
+    const int skew = split_skew(d);
+    int rem = min(d, la) - lo + skew;
+    int v = skew;
+    uint32_t sa = sa0 + (uint32_t)(lo - skew) * sizeof(K);    // (wraps below sa0: never dereferenced there)
+    uint32_t sb = sb0 + (uint32_t)(d - 1 - lo + skew) * sizeof(K);
+    LiftAll<K, LOG2>::run(sa, sb, rem, v);
     return (int)((sa - sa0) / sizeof(K));
 }
 
+}  // namespace
 }  // namespace sm

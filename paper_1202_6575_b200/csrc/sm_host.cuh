@@ -1,5 +1,7 @@
-// stablemerge.cu -- host drivers and the C ABI (include/stablemerge.h) of the
-// B200 stable parallel merge / merge sort of arXiv 1202.6575.
+// sm_host.cuh -- host drivers of the B200 stable parallel merge / merge sort
+// of arXiv 1202.6575, shared by the per-key-type translation units abi_*.cu
+// (the library's globals and key-type-independent C-ABI calls live in
+// sm_common.cu).
 //
 // Call sequence of merge_stable:
 //   validate -> choose p_A, p_B -> cudaMallocAsync the two rank arrays ->
@@ -8,6 +10,7 @@
 //   every task) -> cudaFreeAsync.  No host sync.  Host buffers: staged, or
 //   pipelined over three streams from 64 MB; n + m >= 2^31: a coarse
 //   partition into sub-merges (one host sync).
+#pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdio.h>
@@ -25,8 +28,8 @@
 
 namespace sm {
 
-thread_local char g_err[512] = "";
-thread_local int64_t g_launches = 0;
+extern thread_local char g_err[512];
+extern thread_local int64_t g_launches;
 
 // K2 shape per element layout: NC consumer threads x VT diagonals per thread
 // = NV padded diagonals per ring stage, the largest task; block size
@@ -98,15 +101,8 @@ constexpr int64_t k3_run(int key_bytes, bool has_v) { return (int64_t)k3_nt(key_
 // whole warp each, ~log_33 dependent rounds.
 constexpr int K1_FEW = 4096;
 
-static sm_status fail_cuda(cudaError_t e, const char* what) {
-    snprintf(g_err, sizeof(g_err), "%s: %s", what, cudaGetErrorString(e));
-    return SM_ECUDA;
-}
-
-static sm_status fail_inval(const char* what) {
-    snprintf(g_err, sizeof(g_err), "invalid argument: %s", what);
-    return SM_EINVAL;
-}
+sm_status fail_cuda(cudaError_t e, const char* what);
+sm_status fail_inval(const char* what);
 
 // ------------------------------------------------------------ profiling
 // While enabled, every kernel launch is bracketed by two CUDA events on its
@@ -116,33 +112,13 @@ struct ProfRec {
     cudaEvent_t a, b;
     int kind;
 };
-static bool g_prof_on = false;
-static std::vector<ProfRec> g_prof_pool;
-static size_t g_prof_used = 0;
+extern bool g_prof_on;
+extern std::vector<ProfRec> g_prof_pool;
+extern size_t g_prof_used;
+void prof_before(int kind, cudaStream_t st);
+void prof_after(cudaStream_t st);
 
-static void prof_before(int kind, cudaStream_t st) {
-    if (!g_prof_on) return;
-    if (g_prof_used == g_prof_pool.size()) {
-        ProfRec r;
-        cudaEventCreate(&r.a);
-        cudaEventCreate(&r.b);
-        g_prof_pool.push_back(r);
-    }
-    g_prof_pool[g_prof_used].kind = kind;
-    cudaEventRecord(g_prof_pool[g_prof_used].a, st);
-}
-
-static void prof_after(cudaStream_t st) {
-    if (!g_prof_on) return;
-    cudaEventRecord(g_prof_pool[g_prof_used].b, st);
-    ++g_prof_used;
-}
-
-static sm_status check_launch(const char* what) {
-    ++g_launches;
-    cudaError_t e = cudaGetLastError();
-    return e == cudaSuccess ? SM_OK : fail_cuda(e, what);
-}
+sm_status check_launch(const char* what);
 
 static inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
@@ -852,7 +828,7 @@ static sm_status ranks_entry(const K* X, int64_t len, const K* keys, int64_t nke
 }
 
 // ------------------------------------------------------------ plan dump
-__global__ void k_widen(const int* __restrict__ in, int64_t* __restrict__ out, int count) {
+static __global__ void k_widen(const int* __restrict__ in, int64_t* __restrict__ out, int count) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < count) out[i] = in[i];
 }
@@ -1344,7 +1320,7 @@ static sm_status sort_wide_entry(K* keys, void* vals, int64_t N, int64_t vbytes,
 }  // namespace sm
 
 // ================================================================ C ABI
-extern "C" {
+// (instantiated per key type in abi_*.cu)
 
 // K: the key type the kernels see; C: its bits as the ABI type (C = K, or
 // the base type of Desc<C> for the descending-order entries).
@@ -1400,67 +1376,3 @@ extern "C" {
     sm_status mergesort_stable_wide_##SUF(C* keys, void* vals, int64_t N, int64_t val_bytes, void* stream) {   \
         return sm::sort_wide_entry<K>((K*)keys, vals, N, val_bytes, stream);                                    \
     }
-
-SM_DEFINE_ABI(u32, uint32_t, uint32_t)
-SM_DEFINE_ABI(i32, int32_t, int32_t)
-SM_DEFINE_ABI(i64, int64_t, int64_t)
-SM_DEFINE_ABI(u64, uint64_t, uint64_t)
-SM_DEFINE_ABI(f32, float, float)
-SM_DEFINE_ABI(f64, double, double)
-SM_DEFINE_ABI(desc_u32, sm::Desc<uint32_t>, uint32_t)
-SM_DEFINE_ABI(desc_i32, sm::Desc<int32_t>, int32_t)
-SM_DEFINE_ABI(desc_i64, sm::Desc<int64_t>, int64_t)
-SM_DEFINE_ABI(desc_u64, sm::Desc<uint64_t>, uint64_t)
-SM_DEFINE_ABI(desc_f32, sm::Desc<float>, float)
-SM_DEFINE_ABI(desc_f64, sm::Desc<double>, double)
-SM_DEFINE_ABI(u128, sm::u128, sm_u128)
-SM_DEFINE_ABI(desc_u128, sm::Desc<sm::u128>, sm_u128)
-
-int64_t sm_tile_capacity(int32_t key_bytes, int32_t has_vals) {
-    return sm::tile_nv(key_bytes, has_vals != 0);
-}
-
-int64_t sm_sort_run(int32_t key_bytes, int32_t has_vals) {
-    return sm::k3_run(key_bytes, has_vals != 0);
-}
-
-const char* sm_status_string(sm_status s) {
-    switch (s) {
-        case SM_OK: return "SM_OK";
-        case SM_EINVAL: return "SM_EINVAL: invalid argument";
-        case SM_EALIAS: return "SM_EALIAS: output overlaps an input";
-        case SM_ENOMEM: return "SM_ENOMEM: scratch allocation failed";
-        case SM_ECUDA: return "SM_ECUDA: CUDA error";
-    }
-    return "unknown status";
-}
-
-const char* sm_last_error(void) { return sm::g_err; }
-
-int64_t sm_last_launch_count(void) { return sm::g_launches; }
-
-void sm_profile_enable(int on) {
-    sm::g_prof_on = on != 0;
-    sm::g_prof_used = 0;
-}
-
-sm_status sm_profile_read(int kind, double* total_ms, int64_t* launches) {
-    double t = 0.0;
-    int64_t c = 0;
-    for (size_t i = 0; i < sm::g_prof_used; ++i) {
-        const sm::ProfRec& r = sm::g_prof_pool[i];
-        if (r.kind != kind) continue;
-        cudaError_t e = cudaEventSynchronize(r.b);
-        if (e != cudaSuccess) return sm::fail_cuda(e, "cudaEventSynchronize");
-        float ms = 0.f;
-        e = cudaEventElapsedTime(&ms, r.a, r.b);
-        if (e != cudaSuccess) return sm::fail_cuda(e, "cudaEventElapsedTime");
-        t += ms;
-        ++c;
-    }
-    if (total_ms) *total_ms = t;
-    if (launches) *launches = c;
-    return SM_OK;
-}
-
-}  // extern "C"

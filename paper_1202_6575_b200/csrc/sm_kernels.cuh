@@ -23,6 +23,7 @@
 #include "sm_device.cuh"
 
 namespace sm {
+namespace {   // internal linkage: every translation unit keeps its own kernels
 
 // ----------------------------------------------------------------- K1
 #ifndef K1_WAYS
@@ -525,6 +526,10 @@ __device__ __forceinline__ bool k2_compute(const K* sk, const PV* sv, const Task
     d = D - td.pst;
     cnt = min(VT, td.la + td.lb - d);
     if (cnt <= 0) return true;
+#ifdef SM_K2_NOCOMPUTE
+    // experiment only (wrong output): the same data movement without the merge
+    if (td.la > 0 && td.lb > 0) return true;
+#endif
     if (td.la > 0 && td.lb > 0) {
         // cases (b), (c), (d): stable merge (row a7), ties to A (R17)
         if constexpr (!KeyOrd<K>::PTX && !KeyOrd<K>::FLOAT) {
@@ -1144,4 +1149,5 @@ __global__ void __launch_bounds__(NT, sizeof(K) <= 8 ? SM_K3_MINB : 1) k_block_s
     }
 }
 
+}  // namespace
 }  // namespace sm
