@@ -208,10 +208,15 @@ sm_status ranks_stable_f64(const double *X, int64_t len, const double *keys, int
  *   keys[N], vals[N] (vals may be NULL: keys only), sorted IN PLACE from the
  *   caller's view; stable: equal keys keep their input order.
  *
- * Device path: runs of R consecutive elements are sorted stably inside one
- * CTA each ("sorting sequentially in parallel p consecutive blocks", L406-407;
- * a shared-memory LSD radix sort, stable by construction),
- * then ceil(log2(N/R)) rounds merge run pairs (2k, 2k+1) with the left run
+ * Device path, phase 1 ("sorting sequentially in parallel p consecutive
+ * blocks", L406-407): p blocks of R consecutive elements, each sorted
+ * stably by one CTA.  Keys of <= 8 bytes with 16-byte-aligned buffers and
+ * N / (SM count) >= 2^15: p = the SM count (the paper's p processing
+ * elements), each block radix-sorted through global memory (8-bit digits,
+ * one pass per byte on which the block's keys differ); otherwise runs of
+ * sm_sort_run() elements sorted in shared memory.  Either sort is stable
+ * by construction (sm_sort_run_n() gives R for a given N).
+ * Then ceil(log2(N/R)) rounds merge run pairs (2k, 2k+1) with the left run
  * playing A, every pair of a round in one segmented launch of the merge
  * above ("modifying the merge algorithm to work in parallel on the
  * ceil(p/2^i) pairs", L413-414); an odd trailing run is copied (L409-410).
@@ -234,8 +239,10 @@ sm_status mergesort_stable_f64(double *keys, uint32_t *vals, int64_t N, void *st
  *              has_vals), else SM_EINVAL.
  *   block      block size T (elements) when p_A/p_B are 0:
  *              p_A = ceil(n/T), p_B = ceil(m/T); 2T <= tile capacity.
- *   sort_run   merge sort initial run length R (0 = default; must equal
- *              the block-sort tile of the key type, or be rejected)
+ *   sort_run   merge sort initial run length R (0 = default): the
+ *              shared-memory block-sort tile sm_sort_run(), or any multiple
+ *              of 16 for one-CTA-per-block phase 1 (keys <= 8 bytes,
+ *              16-byte-aligned buffers); anything else: SM_EINVAL
  *   flags      bit 0 (SM_FLAG_NO_PDL): disable programmatic dependent launch
  *              between the cross-rank and task kernels; bit 1
  *              (SM_FLAG_MERGE_PATH): the merge-path comparison below.
@@ -326,8 +333,14 @@ sm_status mergesort_stable_ex_f64(double *keys, uint32_t *vals, int64_t N, void 
  * ceil(n/p_A) + ceil(m/p_B) <= 2T). */
 int64_t sm_tile_capacity(int32_t key_bytes, int32_t has_vals);
 
-/* Initial run length R of the merge sort for this key width / payload mode. */
+/* Run length of the shared-memory block sort (the merge sort's initial run
+ * length R for small N and 128-bit keys) for this key width / payload mode. */
 int64_t sm_sort_run(int32_t key_bytes, int32_t has_vals);
+
+/* The merge sort's initial run length R for N elements on the current
+ * device (16-byte-aligned buffers): ceil(N / SM count) rounded up to 16
+ * when that is >= 2^15 and keys have <= 8 bytes, else sm_sort_run(). */
+int64_t sm_sort_run_n(int32_t key_bytes, int32_t has_vals, int64_t n);
 
 /* Human-readable text for a status, and the last CUDA error message seen by
  * this library in the calling thread ("" if none). */

@@ -84,6 +84,8 @@ _lib.sm_tile_capacity.argtypes = [ctypes.c_int32, ctypes.c_int32]
 _lib.sm_tile_capacity.restype = ctypes.c_int64
 _lib.sm_sort_run.argtypes = [ctypes.c_int32, ctypes.c_int32]
 _lib.sm_sort_run.restype = ctypes.c_int64
+_lib.sm_sort_run_n.argtypes = [ctypes.c_int32, ctypes.c_int32, ctypes.c_int64]
+_lib.sm_sort_run_n.restype = ctypes.c_int64
 _lib.sm_status_string.argtypes = [ctypes.c_int]
 _lib.sm_status_string.restype = ctypes.c_char_p
 _lib.sm_last_error.argtypes = []
@@ -215,8 +217,13 @@ def tile_capacity(key_type: str = "u32", has_vals: bool = True) -> int:
     return int(_lib.sm_tile_capacity(_BYTES[key_type], int(has_vals)))
 
 
-def sort_run(key_type: str = "u32", has_vals: bool = True) -> int:
-    return int(_lib.sm_sort_run(_BYTES[key_type], int(has_vals)))
+def sort_run(key_type: str = "u32", has_vals: bool = True, n: Optional[int] = None) -> int:
+    """Initial run length of the merge sort: the shared-memory block-sort tile
+    (n None), or the run length a sort of n elements uses on the current
+    device (phase 1 with one block per SM when n is large)."""
+    if n is None:
+        return int(_lib.sm_sort_run(_BYTES[key_type], int(has_vals)))
+    return int(_lib.sm_sort_run_n(_BYTES[key_type], int(has_vals), int(n)))
 
 
 def last_launch_count() -> int:
@@ -345,8 +352,9 @@ def ranks_stable(X: torch.Tensor, keys: torch.Tensor, high: bool = False, *, key
 
 
 def mergesort_stable(keys: torch.Tensor, vals: Optional[torch.Tensor] = None, *, key_type: Optional[str] = None,
-                     stream=None, pdl: bool = True, descending: bool = False):
-    """Stable merge sort in place (equal keys keep input order).  Returns (keys, vals)."""
+                     stream=None, pdl: bool = True, descending: bool = False, run: Optional[int] = None):
+    """Stable merge sort in place (equal keys keep input order).  Returns (keys, vals).
+    run: the initial run length (tests; sm_options.sort_run)."""
     kt = _key_type(keys, key_type)
     N = _count(keys, kt)
     s = _stream_for(keys, stream)
@@ -361,11 +369,11 @@ def mergesort_stable(keys: torch.Tensor, vals: Optional[torch.Tensor] = None, *,
     if vals is not None and vals.numel() != N:
         raise ValueError("vals must have the same length as keys")
     args = (_ptr(keys), _ptr(vals), N, s)
-    if pdl:
+    if pdl and not run:
         fn = _sym("mergesort_stable", kt, descending)
         _check(getattr(_lib, fn)(*args), fn)
     else:
-        opt = SmOptions(0, 0, 0, 0, SM_FLAG_NO_PDL)
+        opt = SmOptions(0, 0, 0, int(run or 0), 0 if pdl else SM_FLAG_NO_PDL)
         fn = _sym("mergesort_stable_ex", kt, descending)
         _check(getattr(_lib, fn)(*args, ctypes.byref(opt)), fn)
     _sync_if_host(keys, s)

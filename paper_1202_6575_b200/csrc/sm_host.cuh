@@ -48,12 +48,39 @@ struct K2Geo {
     static constexpr int NV = NC * VT;
     static constexpr int T = NV / 2;
 };
+// (tuning experiments override the shapes with -DSM_K2S4_NC=... etc.)
+#ifndef SM_K2S4_NC
+#define SM_K2S4_NC 352
+#endif
+#ifndef SM_K2S4_VT
+#define SM_K2S4_VT 23
+#endif
+#ifndef SM_K2S4_ST
+#define SM_K2S4_ST 3
+#endif
+#ifndef SM_K2S4_MINB
+#define SM_K2S4_MINB 2
+#endif
+#ifndef SM_K2S8_NC
+#define SM_K2S8_NC 256
+#endif
+#ifndef SM_K2S8_VT
+#define SM_K2S8_VT 15
+#endif
+#ifndef SM_K2S8_ST
+#define SM_K2S8_ST 3
+#endif
+#ifndef SM_K2S8_MINB
+#define SM_K2S8_MINB 2
+#endif
+#define SM_K2S4 SM_K2S4_NC, SM_K2S4_VT, SM_K2S4_ST, SM_K2S4_MINB
+#define SM_K2S8 SM_K2S8_NC, SM_K2S8_VT, SM_K2S8_ST, SM_K2S8_MINB
 template <typename K, bool HAS_V, typename PV = uint32_t>
 struct K2Shape {
     static constexpr int bytes = (int)sizeof(K) + (HAS_V ? (int)sizeof(PV) : 0);
     using type = typename std::conditional<
-        bytes <= 4, K2Geo<352, 23, 3, 2>,
-        typename std::conditional<bytes <= 8, K2Geo<256, 15, 3, 2>,
+        bytes <= 4, K2Geo<SM_K2S4>,
+        typename std::conditional<bytes <= 8, K2Geo<SM_K2S8>,
                                   typename std::conditional<bytes <= 12, K2Geo<256, 15, 4>,
                                                             K2Geo<256, 11, 3>>::type>::type>::type;
 };
@@ -886,9 +913,68 @@ static sm_status launch_block_sort(const K* in, const uint32_t* vin, K* out, uin
     return SM_OK;
 }
 
+#ifndef SM_K3H_NT
+#define SM_K3H_NT 512
+#endif
+#ifndef SM_K3H_TILE
+#define SM_K3H_TILE 8192
+#endif
+// K3H (row a8 with p = the SM count): one CTA per block of the paper's
+// partition, radix-sorted through global memory (k_block_sort_hbm).
+template <typename K, bool HAS_V>
+static sm_status launch_block_sort_hbm(K* keys, uint32_t* vals, K* aux, uint32_t* vaux, int64_t N, int64_t L0,
+                                       bool dst1, cudaStream_t st) {
+    if constexpr (sizeof(K) > 8) {
+        return fail_inval("K3H takes keys of <= 8 bytes");
+    } else {
+        constexpr int NT = SM_K3H_NT;
+        constexpr int TILE = (int)sizeof(K) + (HAS_V ? 4 : 0) <= 8 ? SM_K3H_TILE : SM_K3H_TILE / 2;
+        using Lay = K3HLayout<K, HAS_V, NT, TILE>;
+        auto kern = k_block_sort_hbm<K, HAS_V, NT, TILE>;
+        static bool attr[SM_MAX_DEV];
+        const int dev = current_device();
+        if (dev >= SM_MAX_DEV || !attr[dev]) {
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Lay::SMEM);
+            if (dev < SM_MAX_DEV) attr[dev] = true;
+        }
+        kern<<<(unsigned)ceil_div(N, L0), NT, Lay::SMEM, st>>>(keys, vals, aux, vaux, N, L0, dst1 ? 1 : 0);
+        return SM_OK;
+    }
+}
+
+static int sm_count() {
+    static int n_d[SM_MAX_DEV];
+    const int dev = current_device();
+    int n = dev < SM_MAX_DEV ? n_d[dev] : 0;
+    if (n == 0) {
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        if (n < 1) n = 1;
+        if (dev < SM_MAX_DEV) n_d[dev] = n;
+    }
+    return n;
+}
+
+// Phase 1 (row a8): the initial run length of a sort of N elements.  Keys of
+// <= 8 bytes: the paper's p = the processing elements -- one block per SM
+// (K3H), so phase 2 takes ceil(log2 p) rounds -- when those blocks are long
+// enough to amortise the radix passes (>= K3H_MIN_RUN); else (and for
+// 128-bit keys, or buffers not 16-byte aligned) the shared-memory runs of K3.
+// `forced` (sm_options.sort_run, tests): k3_run selects K3, any other
+// multiple of 16 selects K3H with that run length.
+constexpr int64_t K3H_MIN_RUN = 1 << 15;
 template <typename K>
-static sm_status sort_device(K* keys, uint32_t* vals, int64_t N, cudaStream_t st, bool pdl) {
-    const int R = (int)k3_run((int)sizeof(K), vals != nullptr);   // initial run length: one K3 tile
+static int64_t phase1_run(int64_t N, const void* keys, const void* vals, int64_t forced) {
+    const int64_t r3 = k3_run((int)sizeof(K), vals != nullptr);
+    if (forced) return forced;
+    if (sizeof(K) > 8 || (((uintptr_t)keys | (uintptr_t)vals) & 15)) return r3;
+    const int64_t L0 = ceil_div(ceil_div(N, sm_count()), 16) * 16;
+    return L0 >= K3H_MIN_RUN ? L0 : r3;
+}
+
+template <typename K>
+static sm_status sort_device(K* keys, uint32_t* vals, int64_t N, cudaStream_t st, bool pdl, int64_t run_opt = 0) {
+    const int64_t R = phase1_run<K>(N, keys, vals, run_opt);   // initial run length
+    const bool hbm = R != k3_run((int)sizeof(K), vals != nullptr);
     int rounds = 0;
     for (int64_t L = R; L < N; L *= 2) ++rounds;
     K* aux = nullptr;
@@ -906,12 +992,17 @@ static sm_status sort_device(K* keys, uint32_t* vals, int64_t N, cudaStream_t st
         // ends in the caller's array (in place when rounds is even)
         K* dst = (rounds % 2 == 0) ? keys : aux;
         uint32_t* vdst = (rounds % 2 == 0) ? vals : vaux;
-        const unsigned blocks = (unsigned)ceil_div(N, R);
         prof_before(PROF_K3, st);
-        if (vals) s = launch_block_sort<K, true>(keys, vals, dst, vdst, N, blocks, st);
-        else s = launch_block_sort<K, false>(keys, nullptr, dst, nullptr, N, blocks, st);
+        if (hbm) {
+            if (vals) s = launch_block_sort_hbm<K, true>(keys, vals, aux, vaux, N, R, rounds % 2 == 1, st);
+            else s = launch_block_sort_hbm<K, false>(keys, nullptr, aux, nullptr, N, R, rounds % 2 == 1, st);
+        } else {
+            const unsigned blocks = (unsigned)ceil_div(N, R);
+            if (vals) s = launch_block_sort<K, true>(keys, vals, dst, vdst, N, blocks, st);
+            else s = launch_block_sort<K, false>(keys, nullptr, dst, nullptr, N, blocks, st);
+        }
         prof_after(st);
-        s = check_launch("k_block_sort");
+        if (s == SM_OK) s = check_launch(hbm ? "k_block_sort_hbm" : "k_block_sort");
         K* src = dst;
         uint32_t* vsrc = vdst;
         for (int64_t L = R; s == SM_OK && L < N; L *= 2) {
@@ -983,8 +1074,9 @@ static sm_status sort_large_device(K* keys, uint32_t* vals, int64_t N, cudaStrea
 }
 
 template <typename K>
-static sm_status sort_any_device(K* keys, uint32_t* vals, int64_t N, cudaStream_t st, bool pdl) {
-    return N > (int64_t)INT_MAX ? sort_large_device<K>(keys, vals, N, st, pdl) : sort_device<K>(keys, vals, N, st, pdl);
+static sm_status sort_any_device(K* keys, uint32_t* vals, int64_t N, cudaStream_t st, bool pdl, int64_t run_opt = 0) {
+    return N > (int64_t)INT_MAX ? sort_large_device<K>(keys, vals, N, st, pdl)
+                                : sort_device<K>(keys, vals, N, st, pdl, run_opt);
 }
 
 // Sort of host buffers (both keys and payloads on the host, N <= 2^31 - 1,
@@ -1152,19 +1244,24 @@ static sm_status sort_entry(K* keys, uint32_t* vals, int64_t N, void* stream, co
     if (N < 0) return fail_inval("negative size");
     if (N && !keys) return fail_inval("NULL key pointer with nonzero size");
     if (!keys_aligned<K>({keys})) return fail_inval("128-bit keys must be 16-byte aligned");
-    if (opt && opt->sort_run && opt->sort_run != k3_run((int)sizeof(K), vals != nullptr)) return fail_inval("sort_run must equal the block-sort tile");
+    const int64_t run_opt = opt ? opt->sort_run : 0;
+    if (run_opt && run_opt != k3_run((int)sizeof(K), vals != nullptr) &&
+        (sizeof(K) > 8 || run_opt < 16 || run_opt % 16 || run_opt > (int64_t)INT_MAX / 2 ||
+         (((uintptr_t)keys | (uintptr_t)vals) & 15)))
+        return fail_inval("sort_run: the block-sort tile (sm_sort_run), or a multiple of 16 for the one-block-per-SM "
+                          "phase 1 (keys <= 8 bytes, 16-byte-aligned buffers)");
     if (overlaps(keys, N * sizeof(K), vals, N * 4)) return SM_EALIAS;
     const bool pdl = !(opt && (opt->flags & SM_FLAG_NO_PDL));
     if (N <= 1) return SM_OK;
     keep_pool(st);
-    if (!is_host_ptr(keys) && !is_host_ptr(vals)) return sort_any_device<K>(keys, vals, N, st, pdl);
+    if (!is_host_ptr(keys) && !is_host_ptr(vals)) return sort_any_device<K>(keys, vals, N, st, pdl, run_opt);
     if (is_host_ptr(keys) && (!vals || is_host_ptr(vals)) && N <= (int64_t)INT_MAX &&
         N * (int64_t)(sizeof(K) + (vals ? 4 : 0)) >= (64ll << 20))
         return sort_host_pipelined<K>(keys, vals, N, st, pdl);
     Stage sk, sv;
     sm_status s = stage_in(sk, keys, N * sizeof(K), true, true, st);
     if (s == SM_OK && vals) s = stage_in(sv, vals, N * 4, true, true, st);
-    if (s == SM_OK) s = sort_any_device<K>((K*)sk.dev, (uint32_t*)sv.dev, N, st, pdl);
+    if (s == SM_OK) s = sort_any_device<K>((K*)sk.dev, (uint32_t*)sv.dev, N, st, pdl, run_opt);
     if (s != SM_OK) { sk.out = false; sv.out = false; }
     sm_status r1 = stage_out(sk, st), r2 = stage_out(sv, st);
     return s != SM_OK ? s : (r1 != SM_OK ? r1 : r2);

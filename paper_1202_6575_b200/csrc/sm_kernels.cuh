@@ -198,6 +198,9 @@ __global__ void __launch_bounds__(256) k_cross_ranks_smp(const K* __restrict__ A
     pdl_launch_dependents();
 }
 
+#ifndef SM_K2_INTERLEAVE
+#define SM_K2_INTERLEAVE 0    // 1: plain merges take A-side and B-side tasks alternately (experiment)
+#endif
 // Decode a task (rows a4/a5).  Mode 3 (the merge-path comparison, not the
 // paper's method): task k is output tile [kT, (k+1)T) with the diagonal
 // splits of K1mp in xbar.
@@ -223,6 +226,15 @@ __device__ __forceinline__ Task decode_task(const Geom& g, int task, const int* 
         return w;
     }
     const Blocks xa(sg.n, sg.pA), yb(sg.m, sg.pB);
+#if SM_K2_INTERLEAVE
+    if (g.sort == 0) {
+        // experiment: A-side and B-side tasks alternate (by block index), so
+        // the CTAs' reads and writes advance as one front through A, B and C
+        const int mn = min(sg.pA, sg.pB);
+        if (t < 2 * mn) t = (t & 1) ? sg.pA + (t >> 1) : (t >> 1);
+        else t = sg.pA >= sg.pB ? t - mn : sg.pA + t - mn;   // the rest of the larger side, in order
+    }
+#endif
     return t < sg.pA ? classify_a_side(t, xa, yb, sg.xs, sg.ys) : classify_b_side(t - sg.pA, xa, yb, sg.xs, sg.ys);
 }
 
@@ -266,6 +278,12 @@ struct K2Layout {
     static constexpr int THREADS = NC + 64;                 // producer + storer + consumers
 };
 
+#ifndef SM_BULK_CHUNK
+#define SM_BULK_CHUNK 0       // > 0: bulk loads cut into chunks of this many bytes (experiment)
+#endif
+#ifndef SM_BULK_CHUNK_ST
+#define SM_BULK_CHUNK_ST 0    // > 0: bulk stores cut likewise
+#endif
 // Bytes of the 16-byte-aligned superset of p[0, len).
 template <typename T>
 __device__ __forceinline__ int span_bytes(const T* p, int len) {
@@ -280,7 +298,14 @@ template <typename T>
 __device__ __forceinline__ int issue_span(char* base, int at, const T* p, int len, uint64_t* bar) {
     const uintptr_t g = (uintptr_t)p;
     const uintptr_t g0 = g & ~(uintptr_t)15;
+#if SM_BULK_CHUNK > 0
+    // experiment: cut each span into bulk copies of <= SM_BULK_CHUNK bytes
+    const int nb = len > 0 ? span_bytes(p, len) : 0;
+    for (int o = 0; o < nb; o += SM_BULK_CHUNK)
+        bulk_g2s(base + at + o, (const void*)(g0 + o), (uint32_t)min(SM_BULK_CHUNK, nb - o), bar);
+#else
     if (len > 0) bulk_g2s(base + at, (const void*)g0, (uint32_t)span_bytes(p, len), bar);
+#endif
     return (at + (int)(g - g0)) / (int)sizeof(T);
 }
 
@@ -296,7 +321,13 @@ __device__ __forceinline__ void store_middle(T* dst, const T* sbuf, int o, int L
     const uintptr_t g = (uintptr_t)dst;
     const uintptr_t gl = (g + 15) & ~(uintptr_t)15;
     const uintptr_t gh = (g + (uintptr_t)L * sizeof(T)) & ~(uintptr_t)15;
+#if SM_BULK_CHUNK_ST > 0
+    for (uintptr_t c = gl; c < gh; c += SM_BULK_CHUNK_ST)
+        bulk_s2g((void*)c, (const char*)(sbuf + o + (int)((gl - g) / sizeof(T))) + (c - gl),
+                 (uint32_t)min((uintptr_t)SM_BULK_CHUNK_ST, gh - c));
+#else
     if (gh > gl) bulk_s2g((void*)gl, sbuf + o + (int)((gl - g) / sizeof(T)), (uint32_t)(gh - gl));
+#endif
 }
 
 // Edge element r (0 <= r < 2*(16/sizeof(T)-1)) of the store above: the
@@ -1146,6 +1177,344 @@ __global__ void __launch_bounds__(NT, sizeof(K) <= 8 ? SM_K3_MINB : 1) k_block_s
             st_stream(out + base + e, KeyOrd<K>::from(kf[e]));
             if (HAS_V) st_stream(vout + base + e, vf[e]);
         }
+    }
+}
+
+// ---------------------------------------------------------------- K3H
+// Row a8 with the paper's own block count (§3: "sorting
+// sequentially in parallel p consecutive blocks", p = the processing
+// elements): one CTA per SM sorts one block of ~N/p elements, so phase 2
+// needs only ceil(log2 p) merge rounds (p = 148: 8 rounds for any N, against
+// 15 with the shared-memory runs of K3 for N = 2^28).  The CTA's sort is a
+// stable least-significant-digit radix sort of its block through global
+// memory (8-bit digits of the key's unsigned order view, KeyOrd), ping-
+// ponging between the caller's buffer (buf0) and the auxiliary one (buf1):
+//   pre-pass  one read of the block's keys: the 256-bucket histogram of every
+//             byte of the order view that varies, and the bytes on which keys
+//             differ (bytes every key of the block shares are skipped);
+//   pass      tiles of TILE elements in order, bulk-loaded (TMA) two tiles
+//             ahead: each warp ranks its items by digit (peers with the same
+//             digit from one ballot per digit bit, ranks in (item, lane)
+//             order = input order, warp counters in shared memory), a block
+//             scan over (digit, warp) places every item in the tile sorted by
+//             digit (stable), and the sorted tile is written to the other
+//             buffer at run[d] + (position - tile start of d), run[d] the
+//             block's running offset of digit d.
+// The result must land in the buffer the merge rounds start from (`dst1`:
+// buf1, else buf0): when the number of passes has the wrong parity, the
+// lowest varying byte is taken as two 4-bit digits (their histograms are
+// marginals of the byte's), and a block whose keys are all equal is copied.
+constexpr int K3H_NB = 256;          // buckets of an 8-bit digit
+
+template <typename K, bool HAS_V, int NT, int TILE>
+struct K3HLayout {
+    using U = typename KeyOrd<K>::U;
+    static constexpr int KB = (int)sizeof(K);
+    static constexpr int NW = NT / 32;
+    static constexpr int IPT = TILE / NT;
+    static constexpr int NPOS = (int)sizeof(U);
+    static constexpr int TILE_BYTES = TILE * (KB + (HAS_V ? 4 : 0));
+    static constexpr int OFF_IN = 0;                            // 2 TMA targets: keys[TILE], vals[TILE]
+    static constexpr int OFF_SORT = OFF_IN + 2 * TILE_BYTES;    // the tile sorted by digit
+    static constexpr int OFF_W = OFF_SORT + TILE_BYTES;         // warp counters [NW][256]
+    static constexpr int OFF_HIST = OFF_W + NW * K3H_NB * 4;    // [NPOS][256]
+    static constexpr int OFF_RUN = OFF_HIST + NPOS * 256 * 4;   // running offsets [256]
+    static constexpr int OFF_TOT = OFF_RUN + K3H_NB * 4;        // tile totals [256]
+    static constexpr int OFF_OFS = OFF_TOT + K3H_NB * 4;        // run[d] - tile start[d] [256]
+    static constexpr int OFF_TST = OFF_OFS + K3H_NB * 4;        // tile starts [256]
+    static constexpr int OFF_RED = OFF_TST + K3H_NB * 4;        // [NW] diff (U), [8] scan sums
+    static constexpr int OFF_BAR = (OFF_RED + NW * 16 + 64 + 15) & ~15;
+    static constexpr int SMEM = OFF_BAR + 16;
+    static_assert(TILE % NT == 0 && NT % 32 == 0 && NT >= K3H_NB && (TILE * KB) % 16 == 0, "tile shape");
+};
+
+// L2-coherent load of any 4/8/16-byte element (bypasses L1: the block's
+// other buffer is rewritten between passes)
+template <typename T>
+__device__ __forceinline__ T ld_cg(const T* p) {
+    T v;
+    if constexpr (sizeof(T) == 4) { const unsigned x = __ldcg((const unsigned*)p); memcpy(&v, &x, 4); }
+    else if constexpr (sizeof(T) == 8) { const unsigned long long x = __ldcg((const unsigned long long*)p); memcpy(&v, &x, 8); }
+    else { const ulonglong2 x = __ldcg((const ulonglong2*)p); memcpy(&v, &x, 16); }
+    return v;
+}
+
+// Bulk-load X[0, cnt) (16-byte-aligned start) into smem; the < 16-byte tail
+// with plain loads by the calling thread.  Returns the bytes for expect_tx.
+template <typename T>
+__device__ __forceinline__ uint32_t k3h_load(T* sdst, const T* X, int cnt, uint64_t* bar) {
+    const uint32_t bytes = (uint32_t)cnt * (uint32_t)sizeof(T);
+    const uint32_t body = bytes & ~15u;
+    if (body) bulk_g2s(sdst, X, body, bar);
+    for (uint32_t b = body / sizeof(T); b < (uint32_t)cnt; ++b) sdst[b] = ld_cg(X + b);
+    return body;
+}
+
+// Block exclusive scan of v over threads 0..255 (8 warps); `sums` holds 8
+// words; one barrier inside.  Returns the exclusive prefix of thread t < 256.
+__device__ __forceinline__ uint32_t k3h_scan256(uint32_t v, uint32_t* sums) {
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    uint32_t x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (tid < K3H_NB && lane == 31) sums[w] = x;
+    __syncthreads();
+    uint32_t pre = 0;
+    if (tid < K3H_NB)
+        for (int i = 0; i < w; ++i) pre += sums[i];
+    return pre + x - v;
+}
+
+template <typename K, bool HAS_V, int NT, int TILE>
+__global__ void __launch_bounds__(NT, 1) k_block_sort_hbm(K* buf0, uint32_t* vbuf0, K* buf1, uint32_t* vbuf1,
+                                                           int64_t N, int64_t L0, int dst1) {
+    using Lay = K3HLayout<K, HAS_V, NT, TILE>;
+    using U = typename Lay::U;
+    constexpr int NW = Lay::NW, IPT = Lay::IPT, NPOS = Lay::NPOS;
+    extern __shared__ __align__(128) char smem[];
+    K* so_k = (K*)(smem + Lay::OFF_SORT);
+    uint32_t* so_v = (uint32_t*)(smem + Lay::OFF_SORT + TILE * Lay::KB);
+    uint32_t* wcnt = (uint32_t*)(smem + Lay::OFF_W);
+    uint32_t* hist = (uint32_t*)(smem + Lay::OFF_HIST);
+    uint32_t* run = (uint32_t*)(smem + Lay::OFF_RUN);
+    uint32_t* tot = (uint32_t*)(smem + Lay::OFF_TOT);
+    uint32_t* ofs = (uint32_t*)(smem + Lay::OFF_OFS);
+    uint32_t* tst = (uint32_t*)(smem + Lay::OFF_TST);
+    U* red = (U*)(smem + Lay::OFF_RED);
+    uint32_t* sums = (uint32_t*)(smem + Lay::OFF_RED + NW * 16);
+    uint64_t* bar = (uint64_t*)(smem + Lay::OFF_BAR);      // [2]: one per TMA target
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const int64_t base = (int64_t)blockIdx.x * L0;
+    if (base >= N) return;
+    const int len = (int)min(L0, N - base);              // < 2^31 (host check)
+    const int ntiles = (len + TILE - 1) / TILE;
+    uint32_t ph[2] = {0u, 0u};
+    auto in_k = [&](int b) { return (K*)(smem + Lay::OFF_IN + b * Lay::TILE_BYTES); };
+    auto in_v = [&](int b) { return (uint32_t*)(smem + Lay::OFF_IN + b * Lay::TILE_BYTES + TILE * Lay::KB); };
+
+    if (tid == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        fence_barrier_init();
+    }
+    for (int i = tid; i < NPOS * 256; i += NT) hist[i] = 0;
+    for (int i = tid; i < NW * K3H_NB; i += NT) wcnt[i] = 0;
+    __syncthreads();
+
+    // tile t of the block in X (keys; payloads too when `vals`) -> TMA target t % 2
+    auto issue = [&](const K* X, const uint32_t* V, int t, bool vals) {
+        if (tid == 0 && t < ntiles) {
+            const int e0 = t * TILE, cnt = min(TILE, len - e0), b = t & 1;
+            uint32_t tx = k3h_load<K>(in_k(b), X + base + e0, cnt, &bar[b]);
+            if (HAS_V && vals) tx += k3h_load<uint32_t>(in_v(b), V + base + e0, cnt, &bar[b]);
+            mbar_arrive_expect_tx(&bar[b], tx);
+        }
+    };
+    auto wait = [&](int t) {
+        mbar_wait(&bar[t & 1], ph[t & 1]);
+        ph[t & 1] ^= 1u;
+    };
+
+    // ---- pre-pass: the varying bytes and their histograms
+    const U first = KeyOrd<K>::to(ld_cg(buf0 + base));
+    U diff = 0;
+    issue(buf0, vbuf0, 0, false);
+    issue(buf0, vbuf0, 1, false);
+    for (int t = 0; t < ntiles; ++t) {
+        wait(t);
+        const int cnt = min(TILE, len - t * TILE);
+        const K* ik = in_k(t & 1);
+        U u[IPT];
+#pragma unroll
+        for (int k = 0; k < IPT; ++k) {
+            const int e = k * NT + tid;
+            u[k] = e < cnt ? KeyOrd<K>::to(ik[e]) : first;
+        }
+        __syncthreads();                                 // TMA target t & 1 is free
+        issue(buf0, vbuf0, t + 2, false);
+#pragma unroll
+        for (int k = 0; k < IPT; ++k) {
+            const bool valid = k * NT + tid < cnt;
+            const U x = u[k] ^ first;                     // the bits where this key differs from the block's first
+            U m = x;                                      // ... OR-ed over the warp's valid lanes
+            if constexpr (sizeof(U) == 4) {
+                m = __reduce_or_sync(0xffffffffu, valid ? (uint32_t)x : 0u);
+            } else {
+                const uint32_t lo = __reduce_or_sync(0xffffffffu, valid ? (uint32_t)x : 0u);
+                const uint32_t hi = __reduce_or_sync(0xffffffffu, valid ? (uint32_t)(x >> 32) : 0u);
+                m = ((U)hi << 32) | lo;
+            }
+            diff |= m;
+            const uint32_t nv = __popc(__ballot_sync(0xffffffffu, valid));
+#pragma unroll
+            for (int pos = 0; pos < NPOS; ++pos) {
+                const uint32_t b = (uint32_t)(u[k] >> (8 * pos)) & 0xFFu;
+                if (((m >> (8 * pos)) & 0xFF) == 0) {     // warp-uniform: every valid lane has the first key's byte
+                    if (lane == 0 && nv) atomicAdd(&hist[pos * 256 + ((uint32_t)(first >> (8 * pos)) & 0xFFu)], nv);
+                } else if (valid) {
+                    atomicAdd(&hist[pos * 256 + b], 1u);
+                }
+            }
+        }
+    }
+    if (lane == 0) red[w] = diff;
+    __syncthreads();
+    diff = 0;
+#pragma unroll
+    for (int i = 0; i < NW; ++i) diff |= red[i];
+
+    // ---- the pass plan: varying bytes, low to high; parity fix-up
+    int np = 0, lowest = 0;
+#pragma unroll
+    for (int pos = NPOS - 1; pos >= 0; --pos)
+        if ((diff >> (8 * pos)) & 0xFF) { ++np; lowest = pos; }
+    const bool split = (np & 1) != dst1;                 // one more pass: the lowest byte as two nibbles
+    const int npass = np == 0 ? (dst1 ? 1 : 0) : np + (split ? 1 : 0);
+
+    const K* sk = buf0;
+    const uint32_t* sv = vbuf0;
+    K* dk = buf1;
+    uint32_t* dv = vbuf1;
+    int hpos = lowest;                                   // byte of the current pass
+    for (int ps = 0; ps < npass; ++ps) {
+        // digit of this pass: (shift, bits); bits = 0: a copy (all keys equal)
+        int bits = 0, nib = -1;
+        if (np > 0) {
+            if (split && ps < 2) { nib = ps; bits = 4; }
+            else {
+                if (ps >= (split ? 2 : 1))               // the next varying byte
+                    do { ++hpos; } while (((diff >> (8 * hpos)) & 0xFF) == 0);
+                bits = 8;
+            }
+        }
+        const int shift = 8 * hpos + (nib == 1 ? 4 : 0);
+        const uint32_t dmask = (1u << bits) - 1u;
+        // block exclusive prefix of this digit's histogram -> run[]
+        uint32_t c = 0;
+        if (tid < K3H_NB && tid <= (int)dmask) {
+            if (bits == 8) c = hist[hpos * 256 + tid];
+            else if (bits == 4)
+                for (int x = 0; x < 16; ++x) c += hist[hpos * 256 + (nib == 0 ? (x << 4) | tid : (tid << 4) | x)];
+            else c = (uint32_t)len;
+        }
+        const uint32_t r0 = k3h_scan256(c, sums);
+        if (tid < K3H_NB) run[tid] = r0;
+        // ---- tiles
+        issue(sk, sv, 0, true);
+        issue(sk, sv, 1, true);
+        K* dkb = dk + base;
+        uint32_t* dvb = HAS_V ? dv + base : nullptr;
+        for (int t = 0; t < ntiles; ++t) {
+            const int cnt = min(TILE, len - t * TILE);
+            wait(t);
+            const K* ik = in_k(t & 1);
+            const uint32_t* iv = in_v(t & 1);
+            K key[IPT];
+            uint32_t val[HAS_V ? IPT : 1];
+            uint32_t dig[IPT], rnk[IPT];
+            uint32_t* wc = wcnt + w * K3H_NB;
+            const uint32_t lt = (1u << lane) - 1u;
+            if (cnt == TILE) {
+#pragma unroll
+                for (int k = 0; k < IPT; ++k) {            // warp w: elements [w*32*IPT, ...), item k = k*32 + lane
+                    const int e = (w * IPT + k) * 32 + lane;
+                    key[k] = ik[e];
+                    if (HAS_V) val[k] = iv[e];
+                    dig[k] = (uint32_t)(KeyOrd<K>::to(key[k]) >> shift) & dmask;
+                }
+#pragma unroll
+                for (int k = 0; k < IPT; ++k) {
+                    uint32_t peers = 0xffffffffu;           // lanes with the same digit: one ballot per digit bit
+#pragma unroll
+                    for (int b = 0; b < 8; ++b) {
+                        if (b < bits) {
+                            const uint32_t bl = __ballot_sync(0xffffffffu, (dig[k] >> b) & 1u);
+                            peers &= ((dig[k] >> b) & 1u) ? bl : ~bl;
+                        }
+                    }
+                    const uint32_t cw = wc[dig[k]];
+                    rnk[k] = cw + __popc(peers & lt);
+                    __syncwarp();
+                    if ((peers & lt) == 0) wc[dig[k]] = cw + __popc(peers);
+                    __syncwarp();
+                }
+            } else {                                        // the ragged last tile: padding items rank nowhere
+#pragma unroll
+                for (int k = 0; k < IPT; ++k) {
+                    const int e = (w * IPT + k) * 32 + lane;
+                    const bool valid = e < cnt;
+                    if (valid) {
+                        key[k] = ik[e];
+                        if (HAS_V) val[k] = iv[e];
+                    }
+                    dig[k] = valid ? (uint32_t)(KeyOrd<K>::to(key[k]) >> shift) & dmask : 0xFFFFFFFFu;
+                    const uint32_t act = __ballot_sync(0xffffffffu, valid);
+                    uint32_t peers = act;
+#pragma unroll
+                    for (int b = 0; b < 8; ++b) {
+                        if (b < bits) {
+                            const uint32_t bl = __ballot_sync(0xffffffffu, (dig[k] >> b) & 1u);
+                            peers &= ((dig[k] >> b) & 1u) ? bl : ~bl;
+                        }
+                    }
+                    uint32_t cw = 0;
+                    if (valid) cw = wc[dig[k]];
+                    rnk[k] = cw + __popc(peers & lt);
+                    __syncwarp();
+                    if (valid && (peers & lt) == 0) wc[dig[k]] = cw + __popc(peers);
+                    __syncwarp();
+                }
+            }
+            __syncthreads();                                // counts done; TMA target t & 1 free
+            issue(sk, sv, t + 2, true);
+            // per digit: exclusive over warps (in place), tile total, tile start
+            uint32_t tc = 0;
+            if (tid < K3H_NB) {
+#pragma unroll
+                for (int i = 0; i < NW; ++i) {
+                    const uint32_t x = wcnt[i * K3H_NB + tid];
+                    wcnt[i * K3H_NB + tid] = tc;
+                    tc += x;
+                }
+            }
+            const uint32_t ts = k3h_scan256(tc, sums);
+            if (tid < K3H_NB) {
+                tst[tid] = ts;
+                ofs[tid] = run[tid] - ts;
+                run[tid] += tc;
+            }
+            __syncthreads();
+#pragma unroll
+            for (int k = 0; k < IPT; ++k) {
+                if (dig[k] < K3H_NB) {
+                    const uint32_t at = tst[dig[k]] + wc[dig[k]] + rnk[k];
+                    so_k[at] = key[k];
+                    if (HAS_V) so_v[at] = val[k];
+                }
+            }
+            __syncwarp();
+            for (int i = lane; i < K3H_NB; i += 32) wc[i] = 0;   // this warp's counters, for the next tile
+            __syncthreads();
+#pragma unroll
+            for (int k = 0; k < IPT; ++k) {
+                const int j = k * NT + tid;
+                if (j < cnt) {
+                    const K x = so_k[j];
+                    const uint32_t d = (uint32_t)(KeyOrd<K>::to(x) >> shift) & dmask;
+                    const uint32_t g = ofs[d] + (uint32_t)j;
+                    dkb[g] = x;
+                    if (HAS_V) dvb[g] = so_v[j];
+                }
+            }
+        }
+        // this pass's global writes before the next pass's bulk reads (async proxy)
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+        __syncthreads();
+        const K* tk = sk; sk = dk; dk = (K*)tk;
+        const uint32_t* tv = sv; sv = dv; dv = (uint32_t*)tv;
     }
 }
 

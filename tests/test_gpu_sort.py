@@ -153,3 +153,42 @@ def test_sort_misaligned_views(kt, s):
     torch.cuda.synchronize()
     assert_bit_exact(k.cpu(), v.cpu(), *oracle.sort(inp.keys, inp.vals, kt), kt)
     assert bool((bk[:s] == -1).all()) and bool((bk[s + inp.N:] == -1).all())
+
+
+@pytest.mark.parametrize("payload", [True, False])
+@pytest.mark.parametrize("kt", ["u32", "i32", "i64", "u64", "f32", "f64"])
+def test_sort_blocks_per_sm(kt, payload):
+    """Phase 1 with one CTA per block (k_block_sort_hbm), forced at small
+    sizes through the run length: blocks of one element-tile and of several
+    (ragged last tile, ragged last block), both parities of the round count
+    (the pass plan takes one more pass, or copies an all-equal block, to land
+    in the buffer the rounds start from), narrow and full-range keys (bytes
+    all keys of a block share are skipped)."""
+    sm = lib()
+    dists = ("full", "bounded:3", "bounded:300", "equal") + (("special",) if kt.startswith("f") else ())
+    for N, run in ((1000, 16), (5000, 1008), (20000, 8192 + 16), (40000, 20000), (70001, 70016),
+                   (100003, 3 * 8192 + 48), (250000, 17008)):
+        for dist in dists:
+            inp = synth.sort_input(N, kt, dist, seed=N + run, payload=payload)
+            want = oracle.sort(inp.keys, inp.vals, kt)
+            k = inp.keys.cuda()
+            v = None if inp.vals is None else inp.vals.cuda()
+            sm.mergesort_stable(k, v, key_type=kt, run=run)
+            torch.cuda.synchronize()
+            assert_bit_exact(k.cpu(), None if v is None else v.cpu(), *want, kt)
+
+
+@pytest.mark.parametrize("kt,payload", [("u32", True), ("i64", True), ("u64", False), ("f32", True)])
+def test_sort_default_blocks_per_sm(kt, payload):
+    """Sizes where the default phase 1 is one block per SM (sort_run(n) is
+    not the shared-memory tile), checked against the oracle."""
+    sm = lib()
+    for N in (sm.sort_run(kt, payload) * 0 + 148 * (1 << 15) + 5, (12 << 20) + 77):
+        assert sm.sort_run(kt, payload, N) != sm.sort_run(kt, payload)
+        inp = synth.sort_input(N, kt, "bounded:100000" if kt != "f32" else "special", seed=N % 97, payload=payload)
+        want = oracle.sort(inp.keys, inp.vals, kt)
+        k = inp.keys.cuda()
+        v = None if inp.vals is None else inp.vals.cuda()
+        sm.mergesort_stable(k, v, key_type=kt)
+        torch.cuda.synchronize()
+        assert_bit_exact(k.cpu(), None if v is None else v.cpu(), *want, kt)
