@@ -401,18 +401,32 @@ static bool overlaps(const void* p, size_t pb, const void* q, size_t qb) {
 }
 
 // ------------------------------------------------------------ merge
+static inline int64_t merge_scratch_ints(int64_t pA, int64_t pB) { return (pA + 1) + (pB + 1); }
+#ifndef SM_MODE0_CLASSIFY
+#define SM_MODE0_CLASSIFY 0      // 1: plain merges classify their tasks in a kernel ahead of K2 (experiment)
+#endif
+
 template <typename K, typename PV = uint32_t>
 static sm_status merge_device(const K* A, const PV* vA, int64_t n, const K* B, const PV* vB, int64_t m,
                               K* C, PV* vC, cudaStream_t st, int64_t pA, int64_t pB, bool pdl,
                               int* ranks_given = nullptr) {
     Geom g{};
     g.S = 1; g.pA = (int)pA; g.pB = (int)pB; g.n = (int)n; g.m = (int)m; g.L = 0; g.N = 0; g.sort = 0;
+    // scratch: x̄ (p_A + 1), ȳ (p_B + 1)
     int* ranks = ranks_given;
     sm_status s = SM_OK;
-    if (!ranks) s = dalloc(&ranks, (pA + 1) + (pB + 1), st);
+    if (!ranks) s = dalloc(&ranks, merge_scratch_ints(pA, pB), st);
     if (s != SM_OK) return s;
-    if (vC) s = launch_merge<K, true, PV>(A, vA, B, vB, C, vC, g, ranks, ranks + pA + 1, st, pdl);
-    else s = launch_merge<K, false, PV>(A, nullptr, B, nullptr, C, nullptr, g, ranks, ranks + pA + 1, st, pdl);
+    int4* tdesc = nullptr;
+#if SM_MODE0_CLASSIFY
+    s = dalloc(&tdesc, pA + pB, st);
+    if (s != SM_OK) return s;
+#endif
+
+    if (vC) s = launch_merge<K, true, PV>(A, vA, B, vB, C, vC, g, ranks, ranks + pA + 1, st, pdl, nullptr, tdesc);
+    else s = launch_merge<K, false, PV>(A, nullptr, B, nullptr, C, nullptr, g, ranks, ranks + pA + 1, st, pdl, nullptr,
+                                       tdesc);
+    dfree(tdesc, st);
     if (!ranks_given) dfree(ranks, st);
     return s;
 }
@@ -571,7 +585,8 @@ static sm_status merge_host_pipelined(const K* A, const uint32_t* vA, int64_t n,
     // every device buffer comes from `st` before the fork (stream-ordered pool)
     int64_t rank_ints = 0;
     for (const SubMerge& t : tasks)
-        rank_ints += std::max<int64_t>(1, ceil_div(t.a1 - t.a0, T)) + std::max<int64_t>(1, ceil_div(t.b1 - t.b0, T)) + 2;
+        rank_ints += merge_scratch_ints(std::max<int64_t>(1, ceil_div(t.a1 - t.a0, T)),
+                                        std::max<int64_t>(1, ceil_div(t.b1 - t.b0, T)));
     K *dA = nullptr, *dB = nullptr, *dC = nullptr;
     uint32_t *dvA = nullptr, *dvB = nullptr, *dvC = nullptr;
     int* dranks = nullptr;
@@ -610,7 +625,7 @@ static sm_status merge_host_pipelined(const K* A, const uint32_t* vA, int64_t n,
         const int64_t pa = std::max<int64_t>(1, ceil_div(la, T)), pb = std::max<int64_t>(1, ceil_div(lb, T));
         s = merge_device<K>(dA + t.a0, vC ? dvA + t.a0 : nullptr, la, dB + t.b0, vC ? dvB + t.b0 : nullptr, lb,
                             dC + off, vC ? dvC + off : nullptr, sM, pa, pb, pdl, dranks + rank_at);
-        rank_at += pa + pb + 2;
+        rank_at += merge_scratch_ints(pa, pb);
         if (s != SM_OK) break;
         cudaEventRecord(ev_mg[k], sM);
         cudaStreamWaitEvent(sD, ev_mg[k], 0);
@@ -922,8 +937,8 @@ static sm_status launch_block_sort(const K* in, const uint32_t* vin, K* out, uin
 // K3H (row a8 with p = the SM count): one CTA per block of the paper's
 // partition, radix-sorted through global memory (k_block_sort_hbm).
 template <typename K, bool HAS_V>
-static sm_status launch_block_sort_hbm(K* keys, uint32_t* vals, K* aux, uint32_t* vaux, int64_t N, int64_t L0,
-                                       bool dst1, cudaStream_t st) {
+static sm_status launch_block_sort_hbm(K* keys, uint32_t* vals, K* aux, uint32_t* vaux, K* aux2, uint32_t* vaux2,
+                                       int64_t N, int64_t L0, int final_buf, cudaStream_t st) {
     if constexpr (sizeof(K) > 8) {
         return fail_inval("K3H takes keys of <= 8 bytes");
     } else {
@@ -937,7 +952,7 @@ static sm_status launch_block_sort_hbm(K* keys, uint32_t* vals, K* aux, uint32_t
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Lay::SMEM);
             if (dev < SM_MAX_DEV) attr[dev] = true;
         }
-        kern<<<(unsigned)ceil_div(N, L0), NT, Lay::SMEM, st>>>(keys, vals, aux, vaux, N, L0, dst1 ? 1 : 0);
+        kern<<<(unsigned)ceil_div(N, L0), NT, Lay::SMEM, st>>>(keys, vals, aux, vaux, aux2, vaux2, N, L0, final_buf);
         return SM_OK;
     }
 }
@@ -977,54 +992,65 @@ static sm_status sort_device(K* keys, uint32_t* vals, int64_t N, cudaStream_t st
     const bool hbm = R != k3_run((int)sizeof(K), vals != nullptr);
     int rounds = 0;
     for (int64_t L = R; L < N; L *= 2) ++rounds;
-    K* aux = nullptr;
-    uint32_t* vaux = nullptr;
+    // buffers: the caller's (0), aux (1) and, for the one-block-per-SM phase 1,
+    // aux2 (2): phase 1 ends in aux2 whatever its pass count, and the merge
+    // rounds route through aux / aux2 so that the last one writes buffer 0
+    K* kb[3] = {keys, nullptr, nullptr};
+    uint32_t* vb[3] = {vals, nullptr, nullptr};
     int* ranks = nullptr;
     int4* tdesc = nullptr;
-    sm_status s = dalloc(&aux, N, st);
-    if (s == SM_OK && vals) s = dalloc(&vaux, N, st);
+    sm_status s = dalloc(&kb[1], N, st);
+    if (s == SM_OK && vals) s = dalloc(&vb[1], N, st);
+    if (s == SM_OK && hbm) s = dalloc(&kb[2], N, st);
+    if (s == SM_OK && hbm && vals) s = dalloc(&vb[2], N, st);
     // rank arrays for the largest round: S*(pA+1) + S*(pB+1) <= 2*(N/T + 2*S) entries
     const int64_t T = tile_t((int)sizeof(K), vals != nullptr);
     if (s == SM_OK) s = dalloc(&ranks, 2 * (ceil_div(N, T) + 2 * ceil_div(N, R) + 2), st);
     if (s == SM_OK) s = dalloc(&tdesc, ceil_div(N, T) + 2 * ceil_div(N, R) + 2, st);   // tasks of a round
     if (s == SM_OK) {
-        // phase 1 lands in the buffer from which an even number of rounds
-        // ends in the caller's array (in place when rounds is even)
-        K* dst = (rounds % 2 == 0) ? keys : aux;
-        uint32_t* vdst = (rounds % 2 == 0) ? vals : vaux;
+        int src;
         prof_before(PROF_K3, st);
         if (hbm) {
-            if (vals) s = launch_block_sort_hbm<K, true>(keys, vals, aux, vaux, N, R, rounds % 2 == 1, st);
-            else s = launch_block_sort_hbm<K, false>(keys, nullptr, aux, nullptr, N, R, rounds % 2 == 1, st);
+            src = rounds > 0 ? 2 : 0;
+            if (vals) s = launch_block_sort_hbm<K, true>(keys, vals, kb[1], vb[1], kb[2], vb[2], N, R, src, st);
+            else s = launch_block_sort_hbm<K, false>(keys, nullptr, kb[1], nullptr, kb[2], nullptr, N, R, src, st);
         } else {
+            // phase 1 lands in the buffer from which the rounds, alternating
+            // between 0 and 1, end in 0
+            src = rounds % 2;
             const unsigned blocks = (unsigned)ceil_div(N, R);
-            if (vals) s = launch_block_sort<K, true>(keys, vals, dst, vdst, N, blocks, st);
-            else s = launch_block_sort<K, false>(keys, nullptr, dst, nullptr, N, blocks, st);
+            if (vals) s = launch_block_sort<K, true>(keys, vals, kb[src], vb[src], N, blocks, st);
+            else s = launch_block_sort<K, false>(keys, nullptr, kb[src], nullptr, N, blocks, st);
         }
         prof_after(st);
         if (s == SM_OK) s = check_launch(hbm ? "k_block_sort_hbm" : "k_block_sort");
-        K* src = dst;
-        uint32_t* vsrc = vdst;
+        int left = rounds;
         for (int64_t L = R; s == SM_OK && L < N; L *= 2) {
-            K* d2 = (src == keys) ? aux : keys;
-            uint32_t* vd2 = (src == keys) ? vaux : vals;
+            --left;
+            // this round's target: buffer 0 when an even number of rounds
+            // follow, else a buffer that is neither 0 nor the source
+            const int dst = left % 2 == 0 ? 0 : (src == 1 ? 2 : 1);
             Geom g{};
             g.S = (int)ceil_div(N, 2 * L);
             g.pA = g.pB = (int)ceil_div(L, T);
             g.n = g.m = 0; g.L = (int)L; g.N = (int)N; g.sort = 1;
             int* xbar = ranks;
             int* ybar = ranks + (int64_t)g.S * (g.pA + 1);
-            if (vals) s = launch_merge<K, true>(src, vsrc, src, vsrc, d2, vd2, g, xbar, ybar, st, pdl, nullptr, tdesc);
-            else s = launch_merge<K, false, uint32_t>(src, nullptr, src, nullptr, d2, nullptr, g, xbar, ybar, st, pdl,
-                                                      nullptr, tdesc);
-            src = d2;
-            vsrc = vd2;
+            if (vals)
+                s = launch_merge<K, true>(kb[src], vb[src], kb[src], vb[src], kb[dst], vb[dst], g, xbar, ybar, st, pdl,
+                                          nullptr, tdesc);
+            else
+                s = launch_merge<K, false, uint32_t>(kb[src], nullptr, kb[src], nullptr, kb[dst], nullptr, g, xbar, ybar,
+                                                     st, pdl, nullptr, tdesc);
+            src = dst;
         }
     }
     dfree(tdesc, st);
     dfree(ranks, st);
-    dfree(vaux, st);
-    dfree(aux, st);
+    for (int b = 2; b >= 1; --b) {
+        dfree(vb[b], st);
+        dfree(kb[b], st);
+    }
     return s;
 }
 

@@ -193,11 +193,15 @@ __global__ void __launch_bounds__(256) k_cross_ranks_smp(const K* __restrict__ A
         const int c0 = lo * stride;
         r = c0 >= oth ? oth : c0 + rank_kary<K, K1_WAYS>(X[q] + c0, min(stride, oth - c0), x, high);
     }
-    if (sideA) xbar[idx] = (idx < plen && idx < own_len) ? r : m;
-    else ybar[idx] = (idx < plen && idx < own_len) ? r : n;
+    const int v = (idx < plen && idx < own_len) ? r : oth;
+    if (sideA) xbar[idx] = v;
+    else ybar[idx] = v;
     pdl_launch_dependents();
 }
 
+#ifndef SM_REFILL_TDESC
+#define SM_REFILL_TDESC 8     // window refill threshold when tasks come pre-classified (k_classify)
+#endif
 #ifndef SM_K2_INTERLEAVE
 #define SM_K2_INTERLEAVE 0    // 1: plain merges take A-side and B-side tasks alternately (experiment)
 #endif
@@ -370,7 +374,7 @@ __device__ __forceinline__ void k2_producer(const K* __restrict__ A, const PV* _
     int la = 0, lb = 0, off = 0, ag = 0, bg = 0;   // window slot `lane`
     int cnt = 0;                                    // slots [0, cnt) hold tasks
     int next = blockIdx.x;                          // next task of this CTA
-    const int refill = (g.sort == 0 && KB + (HAS_V ? (int)sizeof(PV) : 0) > 8) ? 32 : 8;
+    const int refill = g.tdesc ? SM_REFILL_TDESC : (g.sort == 0 && KB + (HAS_V ? (int)sizeof(PV) : 0) > 8) ? 32 : 8;
     for (int it = 0;; ++it) {
         if (cnt < refill && next < ntasks) {
             const int my = next + (lane - cnt) * (int)gridDim.x;
@@ -1200,10 +1204,8 @@ __global__ void __launch_bounds__(NT, sizeof(K) <= 8 ? SM_K3_MINB : 1) k_block_s
 //             digit (stable), and the sorted tile is written to the other
 //             buffer at run[d] + (position - tile start of d), run[d] the
 //             block's running offset of digit d.
-// The result must land in the buffer the merge rounds start from (`dst1`:
-// buf1, else buf0): when the number of passes has the wrong parity, the
-// lowest varying byte is taken as two 4-bit digits (their histograms are
-// marginals of the byte's), and a block whose keys are all equal is copied.
+// The result lands in the buffer the merge rounds start from (a third
+// buffer, so no pass is spent on the parity of the pass count).
 constexpr int K3H_NB = 256;          // buckets of an 8-bit digit
 
 template <typename K, bool HAS_V, int NT, int TILE>
@@ -1268,21 +1270,153 @@ __device__ __forceinline__ uint32_t k3h_scan256(uint32_t v, uint32_t* sums) {
     return pre + x - v;
 }
 
+// The lanes whose BITS-bit digit equals this lane's (within `act`): one
+// ballot per digit bit, each folded in with one predicated AND / AND-NOT.
+template <int BITS>
+__device__ __forceinline__ uint32_t k3h_peers(uint32_t d, uint32_t act) {
+    uint32_t peers = act;
+#pragma unroll
+    for (int b = 0; b < BITS; ++b) {
+        asm("{\n\t.reg .pred q;\n\t.reg .b32 bl, t;\n\t"
+            "and.b32 t, %1, %2;\n\t"
+            "setp.ne.u32 q, t, 0;\n\t"
+            "vote.sync.ballot.b32 bl, q, 0xffffffff;\n\t"
+            "@!q not.b32 bl, bl;\n\t"
+            "and.b32 %0, %0, bl;\n\t}"
+            : "+r"(peers)
+            : "r"(d), "r"(1u << b));
+    }
+    return peers;
+}
+
+// One pass of K3H over the block: tiles of TILE elements in order, stable
+// by the BITS-bit digit at `shift` (BITS = 0: a copy).  Per tile: each
+// warp ranks its items (warp w: elements [w*32*IPT, (w+1)*32*IPT), item k
+// of lane l = element (w*IPT + k)*32 + l, i.e. (item, lane) order = input
+// order): lanes with the same digit from one ballot per digit bit, the
+// warp's running count of each digit in shared memory, advanced by the
+// lowest lane of each group (atomicAdd returns the count before it; warp
+// barriers keep the items in order); then a scan over (digit, warp) places
+// every item in the tile sorted by digit, and the sorted tile is written at
+// run[d] + (position - tile start of d).
+template <typename K, bool HAS_V, int NT, int TILE, int BITS>
+__device__ __forceinline__ void k3h_pass(const K* sk, const uint32_t* sv, K* dk, uint32_t* dv, int64_t base, int len,
+                                         int shift, char* smem, uint64_t* bar, uint32_t (&ph)[2]) {
+    using Lay = K3HLayout<K, HAS_V, NT, TILE>;
+    constexpr int NW = Lay::NW, IPT = Lay::IPT;
+    constexpr uint32_t DMASK = (1u << BITS) - 1u;
+    K* so_k = (K*)(smem + Lay::OFF_SORT);
+    uint32_t* so_v = (uint32_t*)(smem + Lay::OFF_SORT + TILE * Lay::KB);
+    uint32_t* wcnt = (uint32_t*)(smem + Lay::OFF_W);
+    uint32_t* run = (uint32_t*)(smem + Lay::OFF_RUN);
+    uint32_t* ofs = (uint32_t*)(smem + Lay::OFF_OFS);
+    uint32_t* tst = (uint32_t*)(smem + Lay::OFF_TST);
+    uint32_t* sums = (uint32_t*)(smem + Lay::OFF_RED + NW * 16);
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const int ntiles = (len + TILE - 1) / TILE;
+    auto in_k = [&](int b) { return (K*)(smem + Lay::OFF_IN + b * Lay::TILE_BYTES); };
+    auto in_v = [&](int b) { return (uint32_t*)(smem + Lay::OFF_IN + b * Lay::TILE_BYTES + TILE * Lay::KB); };
+    auto issue = [&](int t) {
+        if (tid == 0 && t < ntiles) {
+            const int e0 = t * TILE, cnt = min(TILE, len - e0), b = t & 1;
+            uint32_t tx = k3h_load<K>(in_k(b), sk + base + e0, cnt, &bar[b]);
+            if (HAS_V) tx += k3h_load<uint32_t>(in_v(b), sv + base + e0, cnt, &bar[b]);
+            mbar_arrive_expect_tx(&bar[b], tx);
+        }
+    };
+    issue(0);
+    issue(1);
+    K* dkb = dk + base;
+    uint32_t* dvb = HAS_V ? dv + base : nullptr;
+    uint32_t* wc = wcnt + w * K3H_NB;
+    const uint32_t lt = (1u << lane) - 1u;
+    for (int t = 0; t < ntiles; ++t) {
+        const int cnt = min(TILE, len - t * TILE);
+        mbar_wait(&bar[t & 1], ph[t & 1]);
+        ph[t & 1] ^= 1u;
+        const K* ik = in_k(t & 1);
+        const uint32_t* iv = in_v(t & 1);
+        K key[IPT];
+        uint32_t val[HAS_V ? IPT : 1];
+        uint32_t dig[IPT], rnk[IPT];
+#pragma unroll
+        for (int k = 0; k < IPT; ++k) {
+            const int e = (w * IPT + k) * 32 + lane;
+            const bool valid = e < cnt;
+            if (valid) {
+                key[k] = ik[e];
+                if (HAS_V) val[k] = iv[e];
+            }
+            // padding items of a ragged last tile: digit 0xFFFFFFFF, ranked nowhere
+            dig[k] = valid ? (BITS ? (uint32_t)(KeyOrd<K>::to(key[k]) >> shift) & DMASK : 0u) : 0xFFFFFFFFu;
+        }
+        const bool full = cnt == TILE;
+#pragma unroll
+        for (int k = 0; k < IPT; ++k) {
+            const uint32_t d = dig[k];
+            const uint32_t peers = k3h_peers<BITS>(d, full ? 0xffffffffu : __ballot_sync(0xffffffffu, d != 0xFFFFFFFFu));
+            const uint32_t below = peers & lt;
+            uint32_t old = 0;
+            if (below == 0 && d != 0xFFFFFFFFu) old = atomicAdd(&wc[d], (uint32_t)__popc(peers));
+            old = __shfl_sync(0xffffffffu, old, __ffs(peers) - 1);
+            rnk[k] = old + __popc(below);
+            __syncwarp();                               // the next item's counts after this one's
+        }
+        __syncthreads();                                // counts done; TMA target t & 1 free
+        issue(t + 2);
+        // per digit: exclusive over warps (in place), tile total, tile start
+        uint32_t tc = 0;
+        if (tid < K3H_NB) {
+#pragma unroll
+            for (int i = 0; i < NW; ++i) {
+                const uint32_t x = wcnt[i * K3H_NB + tid];
+                wcnt[i * K3H_NB + tid] = tc;
+                tc += x;
+            }
+        }
+        const uint32_t ts = k3h_scan256(tc, sums);
+        if (tid < K3H_NB) {
+            tst[tid] = ts;
+            ofs[tid] = run[tid] - ts;
+            run[tid] += tc;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < IPT; ++k) {
+            if (dig[k] != 0xFFFFFFFFu) {
+                const uint32_t at = tst[dig[k]] + wc[dig[k]] + rnk[k];
+                so_k[at] = key[k];
+                if (HAS_V) so_v[at] = val[k];
+            }
+        }
+        __syncwarp();
+        for (int i = lane; i < K3H_NB; i += 32) wc[i] = 0;   // this warp's counters, for the next tile
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < IPT; ++k) {
+            const int j = k * NT + tid;
+            if (j < cnt) {
+                const K x = so_k[j];
+                const uint32_t d = BITS ? (uint32_t)(KeyOrd<K>::to(x) >> shift) & DMASK : 0u;
+                const uint32_t g = ofs[d] + (uint32_t)j;
+                dkb[g] = x;
+                if (HAS_V) dvb[g] = so_v[j];
+            }
+        }
+    }
+}
+
 template <typename K, bool HAS_V, int NT, int TILE>
 __global__ void __launch_bounds__(NT, 1) k_block_sort_hbm(K* buf0, uint32_t* vbuf0, K* buf1, uint32_t* vbuf1,
-                                                           int64_t N, int64_t L0, int dst1) {
+                                                           K* buf2, uint32_t* vbuf2, int64_t N, int64_t L0,
+                                                           int final_buf) {
     using Lay = K3HLayout<K, HAS_V, NT, TILE>;
     using U = typename Lay::U;
     constexpr int NW = Lay::NW, IPT = Lay::IPT, NPOS = Lay::NPOS;
     extern __shared__ __align__(128) char smem[];
-    K* so_k = (K*)(smem + Lay::OFF_SORT);
-    uint32_t* so_v = (uint32_t*)(smem + Lay::OFF_SORT + TILE * Lay::KB);
     uint32_t* wcnt = (uint32_t*)(smem + Lay::OFF_W);
     uint32_t* hist = (uint32_t*)(smem + Lay::OFF_HIST);
     uint32_t* run = (uint32_t*)(smem + Lay::OFF_RUN);
-    uint32_t* tot = (uint32_t*)(smem + Lay::OFF_TOT);
-    uint32_t* ofs = (uint32_t*)(smem + Lay::OFF_OFS);
-    uint32_t* tst = (uint32_t*)(smem + Lay::OFF_TST);
     U* red = (U*)(smem + Lay::OFF_RED);
     uint32_t* sums = (uint32_t*)(smem + Lay::OFF_RED + NW * 16);
     uint64_t* bar = (uint64_t*)(smem + Lay::OFF_BAR);      // [2]: one per TMA target
@@ -1366,155 +1500,38 @@ __global__ void __launch_bounds__(NT, 1) k_block_sort_hbm(K* buf0, uint32_t* vbu
 #pragma unroll
     for (int i = 0; i < NW; ++i) diff |= red[i];
 
-    // ---- the pass plan: varying bytes, low to high; parity fix-up
-    int np = 0, lowest = 0;
+    // ---- the pass plan: one pass per varying byte, low to high.  Three
+    // buffers: pass i writes the buffer that is neither its source nor the
+    // final one (final_buf: 2 = buf2, the merge rounds' start; 0 = buf0,
+    // a sort that is one block), the last pass writes the final buffer; a
+    // block whose keys are all equal is copied (a pass on a 0-bit digit)
+    int np = 0, hpos = 0;
 #pragma unroll
     for (int pos = NPOS - 1; pos >= 0; --pos)
-        if ((diff >> (8 * pos)) & 0xFF) { ++np; lowest = pos; }
-    const bool split = (np & 1) != dst1;                 // one more pass: the lowest byte as two nibbles
-    const int npass = np == 0 ? (dst1 ? 1 : 0) : np + (split ? 1 : 0);
-
-    const K* sk = buf0;
-    const uint32_t* sv = vbuf0;
-    K* dk = buf1;
-    uint32_t* dv = vbuf1;
-    int hpos = lowest;                                   // byte of the current pass
+        if ((diff >> (8 * pos)) & 0xFF) { ++np; hpos = pos; }
+    int npass = max(np, 1);
+    if (final_buf == 0) npass = np == 0 ? 0 : max(np, 2);   // (one block: in place, or one more copying pass)
+    K* const bk[3] = {buf0, buf1, buf2};
+    uint32_t* const bv[3] = {vbuf0, vbuf1, vbuf2};
+    int src = 0;
     for (int ps = 0; ps < npass; ++ps) {
-        // digit of this pass: (shift, bits); bits = 0: a copy (all keys equal)
-        int bits = 0, nib = -1;
-        if (np > 0) {
-            if (split && ps < 2) { nib = ps; bits = 4; }
-            else {
-                if (ps >= (split ? 2 : 1))               // the next varying byte
-                    do { ++hpos; } while (((diff >> (8 * hpos)) & 0xFF) == 0);
-                bits = 8;
-            }
-        }
-        const int shift = 8 * hpos + (nib == 1 ? 4 : 0);
-        const uint32_t dmask = (1u << bits) - 1u;
+        const int dst = ps == npass - 1 ? final_buf : (src != 1 && final_buf != 1 ? 1 : (src != 2 && final_buf != 2 ? 2 : 0));
+        const bool digit_pass = ps < np;               // else: a copying pass
+        if (digit_pass && ps > 0)
+            do { ++hpos; } while (((diff >> (8 * hpos)) & 0xFF) == 0);
+        const int bits = digit_pass ? 8 : 0;
+        const int shift = 8 * hpos;
         // block exclusive prefix of this digit's histogram -> run[]
         uint32_t c = 0;
-        if (tid < K3H_NB && tid <= (int)dmask) {
-            if (bits == 8) c = hist[hpos * 256 + tid];
-            else if (bits == 4)
-                for (int x = 0; x < 16; ++x) c += hist[hpos * 256 + (nib == 0 ? (x << 4) | tid : (tid << 4) | x)];
-            else c = (uint32_t)len;
-        }
+        if (tid < K3H_NB) c = bits ? hist[hpos * 256 + tid] : (tid == 0 ? (uint32_t)len : 0u);
         const uint32_t r0 = k3h_scan256(c, sums);
         if (tid < K3H_NB) run[tid] = r0;
-        // ---- tiles
-        issue(sk, sv, 0, true);
-        issue(sk, sv, 1, true);
-        K* dkb = dk + base;
-        uint32_t* dvb = HAS_V ? dv + base : nullptr;
-        for (int t = 0; t < ntiles; ++t) {
-            const int cnt = min(TILE, len - t * TILE);
-            wait(t);
-            const K* ik = in_k(t & 1);
-            const uint32_t* iv = in_v(t & 1);
-            K key[IPT];
-            uint32_t val[HAS_V ? IPT : 1];
-            uint32_t dig[IPT], rnk[IPT];
-            uint32_t* wc = wcnt + w * K3H_NB;
-            const uint32_t lt = (1u << lane) - 1u;
-            if (cnt == TILE) {
-#pragma unroll
-                for (int k = 0; k < IPT; ++k) {            // warp w: elements [w*32*IPT, ...), item k = k*32 + lane
-                    const int e = (w * IPT + k) * 32 + lane;
-                    key[k] = ik[e];
-                    if (HAS_V) val[k] = iv[e];
-                    dig[k] = (uint32_t)(KeyOrd<K>::to(key[k]) >> shift) & dmask;
-                }
-#pragma unroll
-                for (int k = 0; k < IPT; ++k) {
-                    uint32_t peers = 0xffffffffu;           // lanes with the same digit: one ballot per digit bit
-#pragma unroll
-                    for (int b = 0; b < 8; ++b) {
-                        if (b < bits) {
-                            const uint32_t bl = __ballot_sync(0xffffffffu, (dig[k] >> b) & 1u);
-                            peers &= ((dig[k] >> b) & 1u) ? bl : ~bl;
-                        }
-                    }
-                    const uint32_t cw = wc[dig[k]];
-                    rnk[k] = cw + __popc(peers & lt);
-                    __syncwarp();
-                    if ((peers & lt) == 0) wc[dig[k]] = cw + __popc(peers);
-                    __syncwarp();
-                }
-            } else {                                        // the ragged last tile: padding items rank nowhere
-#pragma unroll
-                for (int k = 0; k < IPT; ++k) {
-                    const int e = (w * IPT + k) * 32 + lane;
-                    const bool valid = e < cnt;
-                    if (valid) {
-                        key[k] = ik[e];
-                        if (HAS_V) val[k] = iv[e];
-                    }
-                    dig[k] = valid ? (uint32_t)(KeyOrd<K>::to(key[k]) >> shift) & dmask : 0xFFFFFFFFu;
-                    const uint32_t act = __ballot_sync(0xffffffffu, valid);
-                    uint32_t peers = act;
-#pragma unroll
-                    for (int b = 0; b < 8; ++b) {
-                        if (b < bits) {
-                            const uint32_t bl = __ballot_sync(0xffffffffu, (dig[k] >> b) & 1u);
-                            peers &= ((dig[k] >> b) & 1u) ? bl : ~bl;
-                        }
-                    }
-                    uint32_t cw = 0;
-                    if (valid) cw = wc[dig[k]];
-                    rnk[k] = cw + __popc(peers & lt);
-                    __syncwarp();
-                    if (valid && (peers & lt) == 0) wc[dig[k]] = cw + __popc(peers);
-                    __syncwarp();
-                }
-            }
-            __syncthreads();                                // counts done; TMA target t & 1 free
-            issue(sk, sv, t + 2, true);
-            // per digit: exclusive over warps (in place), tile total, tile start
-            uint32_t tc = 0;
-            if (tid < K3H_NB) {
-#pragma unroll
-                for (int i = 0; i < NW; ++i) {
-                    const uint32_t x = wcnt[i * K3H_NB + tid];
-                    wcnt[i * K3H_NB + tid] = tc;
-                    tc += x;
-                }
-            }
-            const uint32_t ts = k3h_scan256(tc, sums);
-            if (tid < K3H_NB) {
-                tst[tid] = ts;
-                ofs[tid] = run[tid] - ts;
-                run[tid] += tc;
-            }
-            __syncthreads();
-#pragma unroll
-            for (int k = 0; k < IPT; ++k) {
-                if (dig[k] < K3H_NB) {
-                    const uint32_t at = tst[dig[k]] + wc[dig[k]] + rnk[k];
-                    so_k[at] = key[k];
-                    if (HAS_V) so_v[at] = val[k];
-                }
-            }
-            __syncwarp();
-            for (int i = lane; i < K3H_NB; i += 32) wc[i] = 0;   // this warp's counters, for the next tile
-            __syncthreads();
-#pragma unroll
-            for (int k = 0; k < IPT; ++k) {
-                const int j = k * NT + tid;
-                if (j < cnt) {
-                    const K x = so_k[j];
-                    const uint32_t d = (uint32_t)(KeyOrd<K>::to(x) >> shift) & dmask;
-                    const uint32_t g = ofs[d] + (uint32_t)j;
-                    dkb[g] = x;
-                    if (HAS_V) dvb[g] = so_v[j];
-                }
-            }
-        }
+        if (bits) k3h_pass<K, HAS_V, NT, TILE, 8>(bk[src], bv[src], bk[dst], bv[dst], base, len, shift, smem, bar, ph);
+        else k3h_pass<K, HAS_V, NT, TILE, 0>(bk[src], bv[src], bk[dst], bv[dst], base, len, shift, smem, bar, ph);
         // this pass's global writes before the next pass's bulk reads (async proxy)
         asm volatile("fence.proxy.async.global;" ::: "memory");
         __syncthreads();
-        const K* tk = sk; sk = dk; dk = (K*)tk;
-        const uint32_t* tv = sv; sv = dv; dv = (uint32_t*)tv;
+        src = dst;
     }
 }
 
