@@ -3,21 +3,33 @@
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config 2]
 
-A step is one pass of the hot path over one batch of synthetic input: for the
-default workload (BASELINE.json configs[1], the one its metric is quoted on:
-stable merge keys-only, n = m = 2^26 int32 full range) a step is one
-merge_stable call = K1 cross ranks + K2 classify/copy/merge (rows a0-a7).
---config 5 benches the merge sort (rows a8-a9); configs 1, 3, 4 the other
-merges.  Inputs are seeded and synthetic (synth/), resident in HBM before the
-timed region.  Multi-GPU (torchrun): every rank merges its own replica
-(different seed), no collective on the data path ("replicas only",
-DESIGN.md); value = all ranks' elements / max-over-ranks time.
+A step is one pass of the hot path over one batch of synthetic input.  The
+headline workload (--config 2, the default) is BASELINE.json configs[1],
+the configuration this tier's bench convention designates (BASELINE.json's
+metric names no config itself): stable merge keys-only, n = m = 2^26 int32
+full range; a step is one merge_stable call = K1 cross ranks + K2
+classify/copy/merge (rows a0-a7).  --config 5 benches the merge sort (rows
+a8-a9); configs 1, 3, 4 the other merges.  Inputs are seeded and synthetic
+(synth/), resident in HBM before the timed region.  In the same run, after
+the headline, `per_config` measures all five BASELINE configs (ms per step,
+elements/s, achieved GB/s, the dominant kernels' per-launch times and
+roofline fractions, clocks) -- skipped with --no-per-config / --no-extras.
+
+Multi-GPU (torchrun, N > 1): the paper's BSP form (§3,
+SURVEY §8(e)) -- rank r holds block r of A and of B (C2-class shards,
+2^26 + 2^26 int32 per rank, so the global merge grows with N: weak
+scaling), and a step is one distributed.merge_stable_sharded call: one
+all-gather of block-start keys, the local rank kernels, ONE all-reduce (the
+single synchronisation), the task plan, one NCCL exchange of each task's
+foreign range, the local merges.  value = all ranks' elements / the
+max-over-ranks device time.
 
 Rank 0 prints ONE JSON line.  `roofline` is for the dominant kernel (K2,
-k_tasks), timed live with CUDA events on its launch stream (sm_profile_*);
-`cpu_baseline` is the CPU oracle (oracle/, single thread) on a bounded sample
-of the same workload; `e2e` is the same metric through the C ABI with pinned
-HOST buffers (host->device and device->host copies inside the timed region).
+k_tasks; K3H k_block_sort_hbm for the sort when it dominates), timed live
+with CUDA events on its launch stream (sm_profile_*); `cpu_baseline` is the
+CPU oracle (oracle/, single thread) on a bounded sample of the same
+workload; `e2e` is the same metric through the C ABI with pinned HOST
+buffers (host->device and device->host copies inside the timed region).
 `--impl reference` times the oracle instead (the reference arm of this tier).
 """
 from __future__ import annotations
@@ -73,6 +85,9 @@ def args_():
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--cpu-seconds", type=float, default=10.0, help="bounded CPU-oracle sample budget")
     ap.add_argument("--no-extras", action="store_true", help="timed loop only (for ncu launch lists)")
+    ap.add_argument("--no-per-config", action="store_true", help="skip the per-config measurements of C1-C5")
+    ap.add_argument("--peer-access", action="store_true",
+                    help="N > 1: the sharded merge reads foreign ranges through CUDA IPC instead of the NCCL exchange")
     ap.add_argument("--merge-path", action="store_true",
                     help="merges only: time the equal-output merge-path COMPARISON instead of the paper's method")
     return ap.parse_args()
@@ -203,7 +218,7 @@ class Workload:
 
     passes = 1                                  # HBM passes of the algorithmic bytes
 
-    def k2_launch_bytes(self):
+    def k2_launch_bytes(self):  # noqa: E301
         """Algorithmic bytes of one launch of the dominant kernel K2 (SURVEY
         §8(d): read A+B + write C, keys + payload)."""
         return 2 * self.elems * self.eb
@@ -270,7 +285,7 @@ class SortWork(Workload):
         self.work_v = self.src.vals.clone() if self.src.vals is not None else None
         self.sm = sm
         import math
-        R = sm.sort_run(kt, c["payload"])
+        R = sm.sort_run(kt, c["payload"], c["N"])     # phase 1's run length for this N
         self.passes = 1 + max(0, math.ceil(math.log2(c["N"] / R)))   # block sort + merge rounds
 
     def prep(self):                              # restore the unsorted input (untimed)
@@ -377,7 +392,149 @@ def make_workload(cfg, seed, dev, sm):
     return {"merge": MergeWork, "sort": SortWork, "batch": BatchWork}[kind](cfg, seed, dev, sm)
 
 
+# ------------------------------------------------------------ N > 1: sharded
+class ShardedMergeWork(Workload):
+    """N > 1: the paper's BSP form (§3).  Rank
+    r holds block r of A and of B (C2-class: n_per = 2^26 int32 full-range
+    keys per array per rank; the global merge is n = m = world * n_per); one
+    step is one distributed.merge_stable_sharded call.  `ops` is the test
+    seam of distributed.py (None: the CUDA library); `peer_access` selects
+    the CUDA-IPC path instead of the NCCL exchange."""
+
+    def __init__(self, rank, world, dev, n_per=1 << 26, ops=None, peer_access=False, group=None):
+        from paper_1202_6575_b200 import distributed as D
+        self.cfg, self.c, self.dev = 2, dict(synth.CONFIGS[2]), dev
+        self.kt = "i32"
+        self.eb = synth.elem_bytes("i32", False)
+        self.rank, self.world, self.n_per = rank, world, n_per
+        a, b = synth.sharded_merge_blocks(n_per, world, rank, synth.BASE_SEED + 2, device=dev)
+        self.a_keys, self.b_keys = a, b
+        self.n = self.m = n_per * world
+        self.elems = 2 * n_per                      # per rank
+        self.ops = ops if ops is not None else D.CudaOps("i32")
+        self.peer_access, self.group = peer_access, group
+        self.pieces, self.stats = [], {}
+
+    def call(self):
+        from paper_1202_6575_b200 import distributed as D
+        self.stats = {}
+        self.pieces = D.merge_stable_sharded(self.a_keys, None, self.b_keys, None, self.n, self.m, key_type=self.kt,
+                                             ops=self.ops, peer_access=self.peer_access, group=self.group,
+                                             stats=self.stats)
+
+
 # ------------------------------------------------------------------ ours
+def _time_steps(wl, steps, stream, dev, prep, per_step_events, world):
+    """Device time of `steps` steps (CUDA events on the launch stream),
+    max over ranks; back-to-back when the inputs exceed L2, else one event
+    pair per step with L2 flushed in between (prep)."""
+    barrier(world)
+    torch.cuda.synchronize(dev)
+    t_wall0 = time.time()
+    if not per_step_events:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(steps):
+            wl.call()
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        t_ms = e0.elapsed_time(e1)
+    else:
+        evs = []
+        for _ in range(steps):
+            prep()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            wl.call()
+            e1.record(stream)
+            evs.append((e0, e1))
+        torch.cuda.synchronize(dev)
+        t_ms = sum(x.elapsed_time(y) for x, y in evs)
+    t_wall1 = time.time()
+    barrier(world)
+    return max_over_ranks(t_ms, world), t_wall0, t_wall1
+
+
+def _kernel_profile(wl, sm, steps, prep, dev):
+    """Per-kernel durations (the library's CUDA-event profiler, events on
+    each kernel's own launch stream; profiling turns PDL off)."""
+    sm.profile_enable(True)
+    for _ in range(steps):
+        prep()
+        wl.call()
+    torch.cuda.synchronize(dev)
+    k = {"k_cross_ranks": sm.profile_read(sm.PROF_K1), "k_tasks": sm.profile_read(sm.PROF_K2),
+         "k_block_sort": sm.profile_read(sm.PROF_K3), "steps": steps}
+    sm.profile_enable(False)
+    return k
+
+
+def _roofline(wl, kernels, peak, peak_src, cfg):
+    """The dominant kernel's roofline: algorithmic bytes per launch (SURVEY
+    §8(d): read + write, keys + payload) over its average launch time."""
+    k2_ms, k2_n = kernels["k_tasks"]
+    k1_ms, k1_n = kernels["k_cross_ranks"]
+    k3_ms, k3_n = kernels["k_block_sort"]
+    steps = kernels["steps"]
+    per_launch_bytes = wl.k2_launch_bytes()
+    k2_avg = k2_ms / max(1, k2_n)
+    achieved = per_launch_bytes / (k2_avg * 1e-3) / 1e9
+    traffic, tsrc = traffic_from_profiles(cfg)
+    out = {"bound": "hbm", "kernel": "k_tasks (K2: classify + copy/merge)",
+           "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+           "traffic": traffic, "traffic_source": tsrc, "peak_source": peak_src,
+           "algorithmic_bytes_per_launch": per_launch_bytes,
+           "avg_launch_ms": k2_avg,
+           "share_of_step": k2_ms / max(1e-9, k1_ms + k2_ms + k3_ms),
+           "k_cross_ranks_avg_ms": k1_ms / max(1, k1_n),
+           "k_cross_ranks_ms_per_step": k1_ms / steps,
+           "k_tasks_ms_per_step": k2_ms / steps,
+           "k_block_sort_avg_ms": (k3_ms / k3_n) if k3_n else None}
+    if k3_n:
+        # phase 1 (row a8): its algorithmic bytes are one read + one write of
+        # the input (its radix passes move more: that is the kernel's cost)
+        k3_avg = k3_ms / k3_n
+        b3 = 2 * wl.elems * wl.eb
+        out["k_block_sort"] = {"avg_launch_ms": k3_avg, "algorithmic_bytes_per_launch": b3,
+                               "achieved": b3 / (k3_avg * 1e-3) / 1e9, "frac": b3 / (k3_avg * 1e-3) / 1e9 / peak}
+    return out
+
+
+def _measure_config(cfg, sm, dev, stream, steps, warmup, peak, peak_src, clocks):
+    """One BASELINE config at N = 1 (per_config): time, kernels, roofline."""
+    wl = make_workload(cfg, rank_seed(cfg, 0), dev, sm)
+    per_step_events = wl.c["kind"] == "sort" or wl.step_bytes() < 4 * L2_BYTES
+    flush = torch.empty(2 * L2_BYTES // 4, dtype=torch.int32, device=dev) if per_step_events else None
+
+    def prep():
+        wl.prep()
+        if flush is not None:
+            flush.add_(1)
+
+    for _ in range(warmup):
+        prep()
+        wl.call()
+    t_ms, w0, w1 = _time_steps(wl, steps, stream, dev, prep, per_step_events, 1)
+    kern = _kernel_profile(wl, sm, max(3, steps), prep, dev)
+    ms = t_ms / steps
+    roof = _roofline(wl, kern, peak, peak_src, cfg)
+    out = {"workload": CONFIG_NAMES[cfg], "steps": steps, "ms_per_step": ms,
+           "elements_per_s": wl.elems / (ms * 1e-3),
+           "achieved_hbm_gbs": wl.step_bytes() / (ms * 1e-3) / 1e9,
+           "achieved_hbm_frac": wl.step_bytes() / (ms * 1e-3) / 1e9 / peak,
+           "algorithmic_bytes_per_step": wl.step_bytes(),
+           "k_tasks_avg_ms": roof["avg_launch_ms"], "k_tasks_frac": roof["frac"],
+           "k_tasks_ms_per_step": roof["k_tasks_ms_per_step"],
+           "k_cross_ranks_ms_per_step": roof["k_cross_ranks_ms_per_step"],
+           "clocks": clocks.summary(w0, w1)}
+    if "k_block_sort" in roof:
+        out["k_block_sort_ms"] = roof["k_block_sort"]["avg_launch_ms"]
+        out["merge_rounds"] = wl.passes - 1
+    del wl, flush
+    torch.cuda.empty_cache()
+    return out
+
+
 def run_ours(a, world, rank, local):
     import paper_1202_6575_b200 as sm
 
@@ -385,9 +542,12 @@ def run_ours(a, world, rank, local):
     torch.cuda.set_device(dev)
     cfg = a.config
     clocks = ClockSampler(local).start()
-    wl = make_workload(cfg, rank_seed(cfg, rank), dev, sm)     # inputs resident in HBM
-    wl.merge_path = a.merge_path
-    per_step_events = wl.c["kind"] == "sort" or wl.step_bytes() < 4 * L2_BYTES
+    if world > 1:
+        wl = ShardedMergeWork(rank, world, dev, peer_access=a.peer_access)   # inputs resident in HBM
+    else:
+        wl = make_workload(cfg, rank_seed(cfg, rank), dev, sm)
+        wl.merge_path = a.merge_path
+    per_step_events = world == 1 and (wl.c["kind"] == "sort" or wl.step_bytes() < 4 * L2_BYTES)
     flush = torch.empty(2 * L2_BYTES // 4, dtype=torch.int32, device=dev) if per_step_events else None
 
     def prep():
@@ -399,53 +559,35 @@ def run_ours(a, world, rank, local):
     for _ in range(a.warmup):
         prep()
         wl.call()
-    wl.call()
-    launches_per_step = sm.last_launch_count()
-    torch.cuda.synchronize(dev)
-    barrier(world)
-    torch.cuda.synchronize(dev)
-
-    t_wall0 = time.time()
-    if not per_step_events:
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        for _ in range(a.steps):
-            wl.call()
-        e1.record(stream)
-        torch.cuda.synchronize(dev)
-        t_ms = e0.elapsed_time(e1)
+    if world > 1:
+        l0 = wl.ops.launches
+        wl.call()
+        launches_per_step = wl.ops.launches - l0     # this rank's library launches in one sharded step
     else:
-        evs = []
-        for _ in range(a.steps):
-            prep()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            wl.call()
-            e1.record(stream)
-            evs.append((e0, e1))
-        torch.cuda.synchronize(dev)
-        t_ms = sum(x.elapsed_time(y) for x, y in evs)
-    t_wall1 = time.time()
-    barrier(world)
-    t_ms = max_over_ranks(t_ms, world)
+        wl.call()
+        launches_per_step = sm.last_launch_count()
+    torch.cuda.synchronize(dev)
+    t_ms, t_wall0, t_wall1 = _time_steps(wl, a.steps, stream, dev, prep, per_step_events, world)
     clk = clocks.summary(t_wall0, t_wall1)
 
     res = dict(value=aggregate_value(wl.elems, world, a.steps, t_ms), ms_per_step=t_ms / a.steps,
-               launches=launches_per_step * a.steps, clocks=clk, per_step_events=per_step_events, wl=wl)
+               launches=None if launches_per_step is None else launches_per_step * a.steps, clocks=clk,
+               per_step_events=per_step_events, wl=wl)
+    if world > 1:
+        # exchange volume of the sharded merge: max over ranks, against the
+        # ~half-of-the-local-input bound of the paper's one exchange step
+        st = wl.stats
+        res["sharded"] = {"recv_bytes_max": int(max_over_ranks(float(st.get("recv_bytes", 0)), world)),
+                          "local_input_bytes": int(st.get("local_bytes", 0)), "tasks": st.get("tasks"),
+                          "peer_access": bool(a.peer_access),
+                          "global_n": wl.n, "global_m": wl.m}
+        clocks.stop()
+        return res
     if a.no_extras:
         clocks.stop()
         return res
 
-    # ---- per-kernel durations (CUDA events on the launch stream)
-    prof_steps = max(3, min(a.steps, 50 if wl.c["kind"] == "sort" else 200))
-    sm.profile_enable(True)
-    for _ in range(prof_steps):
-        prep()
-        wl.call()
-    torch.cuda.synchronize(dev)
-    res["kernels"] = {"k_cross_ranks": sm.profile_read(sm.PROF_K1), "k_tasks": sm.profile_read(sm.PROF_K2),
-                      "k_block_sort": sm.profile_read(sm.PROF_K3), "steps": prof_steps}
-    sm.profile_enable(False)
+    res["kernels"] = _kernel_profile(wl, sm, max(3, min(a.steps, 50 if wl.c["kind"] == "sort" else 200)), prep, dev)
 
     # ---- end to end through the public API with pinned host buffers
     h2d, d2h = wl.e2e_setup(stream)
@@ -461,10 +603,24 @@ def run_ours(a, world, rank, local):
         e1.record(stream)
         torch.cuda.synchronize(dev)
         e2e_ms += e0.elapsed_time(e1)
-    e2e_ms = max_over_ranks(e2e_ms, world)
     res["e2e"] = {"value": aggregate_value(wl.elems, world, a.e2e_steps, e2e_ms), "unit": "elements/s",
                   "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": a.e2e_steps,
                   "path": "public API with pinned host buffers (H2D, kernels, D2H inside the timed region)"}
+    res["cpu_baseline"] = cpu_oracle_sample(wl, a.cpu_seconds)
+
+    # ---- every BASELINE config in the same run (per_config)
+    if not a.no_per_config:
+        peak, peak_src = hbm_peak()
+        for attr in ("inp", "src", "work_k", "work_v", "out_k", "out_v", "h_args", "host", "hk", "hv", "hwk", "hwv"):
+            if hasattr(wl, attr):
+                setattr(wl, attr, None)
+        del flush
+        torch.cuda.empty_cache()
+        per = {}
+        for c in (1, 2, 3, 4, 5):
+            steps = 5 if synth.CONFIGS[c]["kind"] == "sort" else 20
+            per[f"C{c}"] = _measure_config(c, sm, dev, stream, steps, 3, peak, peak_src, clocks)
+        res["per_config"] = per
     clocks.stop()
     return res
 
@@ -555,17 +711,26 @@ def main():
     wl = r["wl"]
     c = wl.c
     peak, peak_src = hbm_peak()
+    sharded = "sharded" in r
+    if sharded:
+        parallelism = (f"sharded over {world} ranks: the paper's BSP form (rank r holds block r of A and B, "
+                       f"one all-reduce of cross ranks, one {'CUDA-IPC' if a.peer_access else 'NCCL'} exchange)")
+        workload = (f"C2-class sharded stable merge keys-only: n = m = {world} x 2^26 int32 full range "
+                    f"(each rank: its 2^26 + 2^26 block pair)")
+    else:
+        parallelism = "1 GPU"
+        workload = CONFIG_NAMES[cfg]
     line = {
         "metric": load_json("BASELINE.json")["metric"],
         "value": r["value"], "unit": "elements/s", "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
         "ms_per_step": r["ms_per_step"], "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": c["key_type"] + ("+u32" if c["payload"] else ""), "data": "synthetic",
-        "config": {"workload": CONFIG_NAMES[cfg], "elements_per_gpu_step": wl.elems, "key_type": c["key_type"],
+        "config": {"workload": workload, "elements_per_gpu_step": wl.elems, "key_type": c["key_type"],
                    "payload": c["payload"], "dist": c["dist"], "seed": f"{synth.BASE_SEED + cfg:#x} + 1000*rank",
                    "l2": ("per-step events, L2 flushed (2x L2 write) and sort input restored between timed steps"
                           if r["per_step_events"] else
                           f"inputs+output {wl.step_bytes() / 1e9:.2f} GB > 126 MB L2: no flush, back-to-back steps"),
-                   "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
+                   "parallelism": parallelism,
                    "method": ("merge-path comparison (equal output tiles; NOT the paper's method)" if a.merge_path
                               else "paper: cross ranks + cases (a)-(e)")},
         "achieved_hbm_gbs": wl.step_bytes() / (r["ms_per_step"] * 1e-3) / 1e9,
@@ -574,29 +739,14 @@ def main():
         "clocks": r["clocks"],
     }
     line["achieved_hbm_frac"] = line["achieved_hbm_gbs"] / peak
+    if sharded:
+        line["sharded"] = r["sharded"]
+        line["achieved_hbm_gbs_note"] = "per GPU: local elements x 8 B / max-over-ranks step time"
     if "kernels" in r:
-        k2_ms, k2_n = r["kernels"]["k_tasks"]
-        k1_ms, k1_n = r["kernels"]["k_cross_ranks"]
-        k3_ms, k3_n = r["kernels"]["k_block_sort"]
-        steps = r["kernels"]["steps"]
-        per_launch_bytes = wl.k2_launch_bytes()
-        k2_avg = k2_ms / max(1, k2_n)
-        achieved = per_launch_bytes / (k2_avg * 1e-3) / 1e9
-        traffic, tsrc = traffic_from_profiles(cfg)
-        line["roofline"] = {"bound": "hbm", "kernel": "k_tasks (K2: classify + copy/merge)",
-                            "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                            "traffic": traffic, "traffic_source": tsrc, "peak_source": peak_src,
-                            "algorithmic_bytes_per_launch": per_launch_bytes,
-                            "avg_launch_ms": k2_avg,
-                            "share_of_step": k2_ms / max(1e-9, k1_ms + k2_ms + k3_ms),
-                            "k_cross_ranks_avg_ms": k1_ms / max(1, k1_n),
-                            "k_cross_ranks_ms_per_step": k1_ms / steps,
-                            "k_tasks_ms_per_step": k2_ms / steps,
-                            "k_block_sort_avg_ms": (k3_ms / k3_n) if k3_n else None}
-    if "e2e" in r:
-        line["e2e"] = r["e2e"]
-    if world == 1 and not a.no_extras:
-        line["cpu_baseline"] = cpu_oracle_sample(wl, a.cpu_seconds)
+        line["roofline"] = _roofline(wl, r["kernels"], peak, peak_src, cfg)
+    for key in ("e2e", "cpu_baseline", "per_config"):
+        if key in r:
+            line[key] = r[key]
     print(json.dumps(line), flush=True)
     if world > 1:
         import torch.distributed as dist

@@ -1289,6 +1289,36 @@ __device__ __forceinline__ uint32_t k3h_peers(uint32_t d, uint32_t act) {
     return peers;
 }
 
+// The stable rank of this lane's item in its warp's running count: the
+// group of lanes with the same digit (`peers`) advances the warp counter of
+// the digit once -- its highest lane adds the group size with one shared
+// atomic, and every lane gets the count before it by a shuffle -- and the
+// item's place is that count plus its peers in lower lanes.  A warp barrier
+// orders the next item's atomic after this one's.
+__device__ __forceinline__ uint32_t k3h_rank(uint32_t wc_s, uint32_t d, uint32_t peers, int lane, bool valid) {
+    uint32_t r;
+    asm volatile(
+        "{\n\t.reg .pred lead, v;\n\t.reg .b32 hi, cnt, addr, old, src, lt, below;\n\t"
+        "setp.ne.u32 v, %5, 0;\n\t"
+        "shr.b32 hi, %2, %3;\n\t"
+        "setp.eq.and.u32 lead, hi, 1, v;\n\t"
+        "popc.b32 cnt, %2;\n\t"
+        "mad.lo.u32 addr, %1, 4, %4;\n\t"
+        "mov.u32 old, 0;\n\t"
+        "@lead atom.shared.add.u32 old, [addr], cnt;\n\t"
+        "bfind.u32 src, %2;\n\t"
+        "shfl.sync.idx.b32 old, old, src, 0x1f, 0xffffffff;\n\t"
+        "mov.u32 lt, %%lanemask_lt;\n\t"
+        "and.b32 below, %2, lt;\n\t"
+        "popc.b32 below, below;\n\t"
+        "add.u32 %0, old, below;\n\t"
+        "bar.warp.sync 0xffffffff;\n\t}"
+        : "=r"(r)
+        : "r"(d), "r"(peers), "r"(lane), "r"(wc_s), "r"((uint32_t)valid)
+        : "memory");
+    return r;
+}
+
 // One pass of K3H over the block: tiles of TILE elements in order, stable
 // by the BITS-bit digit at `shift` (BITS = 0: a copy).  Per tile: each
 // warp ranks its items (warp w: elements [w*32*IPT, (w+1)*32*IPT), item k
@@ -1351,16 +1381,12 @@ __device__ __forceinline__ void k3h_pass(const K* sk, const uint32_t* sv, K* dk,
             dig[k] = valid ? (BITS ? (uint32_t)(KeyOrd<K>::to(key[k]) >> shift) & DMASK : 0u) : 0xFFFFFFFFu;
         }
         const bool full = cnt == TILE;
+        const uint32_t wc_s = smem_addr(wc);
 #pragma unroll
         for (int k = 0; k < IPT; ++k) {
             const uint32_t d = dig[k];
             const uint32_t peers = k3h_peers<BITS>(d, full ? 0xffffffffu : __ballot_sync(0xffffffffu, d != 0xFFFFFFFFu));
-            const uint32_t below = peers & lt;
-            uint32_t old = 0;
-            if (below == 0 && d != 0xFFFFFFFFu) old = atomicAdd(&wc[d], (uint32_t)__popc(peers));
-            old = __shfl_sync(0xffffffffu, old, __ffs(peers) - 1);
-            rnk[k] = old + __popc(below);
-            __syncwarp();                               // the next item's counts after this one's
+            rnk[k] = k3h_rank(wc_s, d, peers, lane, full || d != 0xFFFFFFFFu);
         }
         __syncthreads();                                // counts done; TMA target t & 1 free
         issue(t + 2);

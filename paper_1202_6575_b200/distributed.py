@@ -48,22 +48,30 @@ class CudaOps:
     """The local primitives on this rank's GPU (the library's kernels)."""
 
     def __init__(self, key_type: Optional[str] = None, descending: bool = False):
-        from . import merge_stable, mergesort_stable, ranks_stable
+        from . import last_launch_count, merge_stable, mergesort_stable, ranks_stable
         self._merge, self._ranks, self._sort = merge_stable, ranks_stable, mergesort_stable
+        self._count = last_launch_count
         self.key_type, self.descending = key_type, descending
+        self.launches = 0                          # the library's kernel launches through this object
 
     def ranks(self, X: torch.Tensor, keys: torch.Tensor, high: bool) -> torch.Tensor:
         if X.numel() == 0 or keys.numel() == 0:
             return torch.zeros(keys.numel(), dtype=torch.int64, device=keys.device)
-        return self._ranks(X, keys, high, key_type=self.key_type, descending=self.descending)
+        r = self._ranks(X, keys, high, key_type=self.key_type, descending=self.descending)
+        self.launches += self._count()
+        return r
 
     def merge(self, ak, av, bk, bv):
-        return self._merge(ak, av, bk, bv, key_type=self.key_type, descending=self.descending)
+        r = self._merge(ak, av, bk, bv, key_type=self.key_type, descending=self.descending)
+        self.launches += self._count()
+        return r
 
     def sort(self, keys, vals):
         keys = keys.clone()
         vals = None if vals is None else vals.clone()
-        return self._sort(keys, vals, key_type=self.key_type, descending=self.descending)
+        r = self._sort(keys, vals, key_type=self.key_type, descending=self.descending)
+        self.launches += self._count()
+        return r
 
 
 def block_starts(length: int, p: int) -> List[int]:
@@ -148,23 +156,29 @@ def _open(shared) -> Optional[torch.Tensor]:
 def merge_stable_sharded(a_keys: torch.Tensor, a_vals: Optional[torch.Tensor], b_keys: torch.Tensor,
                          b_vals: Optional[torch.Tensor], n: int, m: int, *, group=None,
                          key_type: Optional[str] = None, ops=None,
-                         peer_access: Optional[bool] = None) -> List[Piece]:
+                         peer_access: bool = False, stats: Optional[dict] = None) -> List[Piece]:
     """Stable merge (ties: A first) of A (n) and B (m) sharded over the ranks
     of `group`: this rank passes its blocks A[x_r, x_{r+1}) and B[y_r, y_{r+1})
     (PAPER.md block partition, p = world size).  Returns this rank's output
-    pieces.
+    pieces.  `stats` (optional dict) receives this rank's exchange volume:
+    recv_bytes (foreign input ranges this rank's tasks read) and
+    local_bytes (its own shards).
 
-    peer_access (default: on for CUDA shards in an NCCL group -- the GPUs of
-    one NVLink/NVSwitch node, reachable by CUDA IPC): no exchange step at all -- every rank maps the
-    other ranks' shards (CUDA IPC handles, one all-gather) and the merge
-    kernel's TMA loads read each task's foreign range straight from the
-    holder's memory over NVLink, so the transfer overlaps the merge stage by
-    stage inside ONE kernel; a barrier before the merges (inputs complete)
-    and after them (no rank frees its shard while peers read it)."""
+    peer_access (opt-in; CUDA shards in an NCCL group, all ranks' GPUs
+    peer-accessible): no exchange step at all -- every rank maps the other
+    ranks' shards (CUDA IPC handles, one all-gather) and the merge kernel's
+    TMA loads read each task's foreign range straight from the holder's
+    memory over NVLink, so the transfer overlaps the merge stage by stage
+    inside ONE kernel; a barrier before the merges (inputs complete) and
+    after them (no rank frees its shard while peers read it).  A mapped
+    shard that does not land on this rank's device (torch opens an IPC
+    handle on the sender's device index) makes the call fall back to the
+    NCCL exchange: the library launches on the inputs' device only.  The
+    NVLink path has been exercised with processes sharing one GPU only."""
     p = dist.get_world_size(group)
     r = dist.get_rank(group)
-    custom_ops = ops is not None
     ops = ops or CudaOps(key_type)
+    custom_ops = not isinstance(ops, CudaOps)
     x, y = block_starts(n, p), block_starts(m, p)
     if a_keys.numel() != x[r + 1] - x[r] or b_keys.numel() != y[r + 1] - y[r]:
         raise ValueError("shards must be the paper's blocks: A[x_r, x_r+1) and B[y_r, y_r+1)")
@@ -198,10 +212,23 @@ def merge_stable_sharded(a_keys: torch.Tensor, a_vals: Optional[torch.Tensor], b
     ybar = ranks[p:] + [n]
     tasks = plan_tasks(n, m, p, xbar, ybar)
 
-    if peer_access is None:
-        peer_access = a_keys.is_cuda and b_keys.is_cuda and dist.get_backend(group) == "nccl" and not custom_ops
+    if stats is not None:
+        eb = a_keys.element_size() + (0 if a_vals is None else a_vals.element_size())
+        fb = b_keys.element_size() + (0 if b_vals is None else b_vals.element_size())
+        recv = 0
+        for (owner, a0, a1, b0, b1) in tasks:
+            if owner != r:
+                continue
+            if a1 > a0 and _holder(a0, a1, n, p) != r:
+                recv += (a1 - a0) * eb
+            if b1 > b0 and _holder(b0, b1, m, p) != r:
+                recv += (b1 - b0) * fb
+        stats.update(recv_bytes=recv, local_bytes=a_keys.numel() * eb + b_keys.numel() * fb, tasks=len(tasks))
+    peer_access = bool(peer_access) and a_keys.is_cuda and b_keys.is_cuda and not custom_ops
     if peer_access and p > 1:
-        return _merge_tasks_peer(tasks, r, p, n, m, x, y, a_keys, a_vals, b_keys, b_vals, ops, group)
+        pieces = _merge_tasks_peer(tasks, r, p, n, m, x, y, a_keys, a_vals, b_keys, b_vals, ops, group)
+        if pieces is not None:
+            return pieces
 
     # exchange: every task's foreign range from its single holder
     ops_list, recv = [], {}
@@ -262,6 +289,15 @@ def _merge_tasks_peer(tasks, r, p, n, m, x, y, a_keys, a_vals, b_keys, b_vals, o
         if q not in mapped:
             mapped[q] = [_open(h) for h in handles[q]]
         return mapped[q]
+
+    # every rank must be able to read every peer shard on its own device
+    ok = all(t is None or t.device == a_keys.device for q in range(p) for t in shard(q))
+    flags = torch.tensor([1 if ok else 0], dtype=torch.int32, device=_coll_device(a_keys, group))
+    dist.all_reduce(flags, op=dist.ReduceOp.MIN, group=group)
+    if not int(flags.item()):
+        mapped.clear()
+        dist.barrier(group=group)
+        return None                                      # the caller takes the NCCL exchange
 
     pieces = []
     for k, (owner, a0, a1, b0, b1) in enumerate(tasks):
@@ -349,22 +385,21 @@ def _cat(parts, like):
 
 def mergesort_stable_sharded(keys: torch.Tensor, vals: Optional[torch.Tensor], N: int, *, group=None,
                              key_type: Optional[str] = None, descending: bool = False, ops=None,
-                             peer_access: Optional[bool] = None):
+                             peer_access: bool = False):
     """Stable sort of an array of N keys (+ uint32 payloads) sharded over the
     ranks of `group`: this rank passes block r of the input (PAPER.md block
     partition, p = world size) and gets back block r of the sorted array.
     Returns (keys, vals).
 
-    peer_access (default: on for CUDA shards in an NCCL group): both exchange
-    steps of a round go through CUDA IPC mappings instead of NCCL sends --
-    the merges read their foreign ranges in place from the holders' blocks,
-    and each task owner copies its merged piece straight into the
-    destination ranks' next-round blocks (peer-to-peer copies over NVLink)."""
+    peer_access (opt-in, CUDA shards): both exchange steps of a round go
+    through CUDA IPC mappings instead of NCCL sends -- the merges read their
+    foreign ranges in place from the holders' blocks, and each task owner
+    copies its merged piece straight into the destination ranks' next-round
+    blocks (peer-to-peer copies over NVLink).  If a mapped block does not
+    land on this rank's device, the sort continues with the NCCL exchange."""
     p = dist.get_world_size(group)
     r = dist.get_rank(group)
-    if peer_access is None:
-        peer_access = keys.is_cuda and dist.get_backend(group) == "nccl" and ops is None
-    peer_access = peer_access and p > 1                  # one rank: nothing to exchange
+    peer_access = bool(peer_access) and keys.is_cuda and ops is None and p > 1   # one rank: nothing to exchange
     ops = ops or CudaOps(key_type, descending)
     xs = block_starts(N, p)
     if keys.shape[0] != xs[r + 1] - xs[r]:
@@ -416,6 +451,13 @@ def mergesort_stable_sharded(keys: torch.Tensor, vals: Optional[torch.Tensor], N
             dist.all_gather_object(handles, [_share(keys), _share(vals)], group=group)
             peers = {q: [_open(h) for h in handles[q]] for q in range(p) if q != r}
             peers[r] = [keys, vals]
+            ok = all(t is None or t.device == dev for q in range(p) for t in peers[q])
+            flags = torch.tensor([1 if ok else 0], dtype=torch.int32, device=_coll_device(keys, group))
+            dist.all_reduce(flags, op=dist.ReduceOp.MIN, group=group)
+            if not int(flags.item()):                    # mapped on another device: NCCL from here on
+                peers = None
+                peer_access = False
+                dist.barrier(group=group)
         for (a0, b0, b1, n, m) in pairs:
             pA, pB = b0 - a0, b1 - b0
             xbar = ranks[a0:b0] + [m]

@@ -249,6 +249,24 @@ def merge_input(n: int, m: int, key_type: str, dist: str, seed: int, payload: bo
     return MergeInput(key_type, a, b, av, bv)
 
 
+def sharded_merge_blocks(n_per: int, world: int, rank: int, seed: int, device="cpu"):
+    """Rank `rank`'s blocks of a C2-class sharded merge (bench.py at N > 1):
+    A and B of n_per * world int32 keys each, uniform over the full int32
+    range, sorted, split into the paper's blocks of n_per (p = world).  The
+    blocks are drawn stratified -- block r holds n_per keys uniform in the
+    r-th 1/world of the key range, sorted -- so every rank makes its own
+    blocks and their concatenation is the sorted array.  Returns (A_r, B_r)."""
+    W = (1 << 32) // world
+    lo = -(1 << 31) + rank * W
+    width = W if rank < world - 1 else (1 << 32) - rank * W
+    out = []
+    for stream in (STREAM_A, STREAM_B):
+        r = splitmix_stream(seed, 64 * stream + rank, n_per, device)
+        k = (bounded(r, width) + lo).to(torch.int32)
+        out.append(torch.sort(k).values)
+    return out[0], out[1]
+
+
 def sort_input(N: int, key_type: str, dist: str, seed: int, payload: bool = True, device="cpu") -> SortInput:
     keys = u128_keys(dist, seed, STREAM_SORT, N, device) if key_type == "u128" else \
         _keys(dist, key_type, seed, STREAM_SORT, N, device)

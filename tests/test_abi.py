@@ -37,7 +37,7 @@ def test_header_declares_entry_points():
             assert f"{f}_desc_{kt}" in names          # descending order
         for f in ("merge_stable_wide", "merge_stable_batched_wide", "mergesort_stable_wide"):
             assert f"{f}_{kt}" in names and f"{f}_desc_{kt}" in names   # wide payloads (row 2)
-    assert len(names) == 147
+    assert len(names) == 148          # + sm_sort_run_n
 
 
 def test_library_exports_every_declared_symbol(sm):
