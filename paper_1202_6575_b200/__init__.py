@@ -250,6 +250,18 @@ def _options(p_A, p_B, block, flags, sort_run_=None):
     return SmOptions(p_A or 0, p_B or 0, block or 0, sort_run_ or 0, flags or 0)
 
 
+def _check_args(pairs, tensors):
+    """Every (tensor, expected rows, what) holds exactly that many rows, and
+    every tensor lives on one device: the C ABI trusts the sizes it is given
+    (a short buffer would be read or written past its end on the GPU)."""
+    for t, want, what in pairs:
+        if t is not None and int(t.shape[0] if t.dim() else 1) != want:
+            raise ValueError(f"{what} must hold {want} rows, has {int(t.shape[0]) if t.dim() else 1}")
+    devs = {t.device for t in tensors if t is not None}
+    if len(devs) > 1:
+        raise ValueError(f"all tensors must be on one device, got {sorted(map(str, devs))}")
+
+
 def merge_stable(a_keys: torch.Tensor, a_vals: Optional[torch.Tensor], b_keys: torch.Tensor,
                  b_vals: Optional[torch.Tensor], out_keys: Optional[torch.Tensor] = None,
                  out_vals: Optional[torch.Tensor] = None, *, key_type: Optional[str] = None, stream=None,
@@ -269,6 +281,10 @@ def merge_stable(a_keys: torch.Tensor, a_vals: Optional[torch.Tensor], b_keys: t
             out_keys = _empty_keys(n + m, a_keys, kt)
         if out_vals is None:
             out_vals = torch.empty((n + m,) + tuple(a_vals.shape[1:]), dtype=a_vals.dtype, device=a_keys.device)
+        _check_args([(a_vals, n, "a_vals"), (b_vals, m, "b_vals"), (out_vals, n + m, "out_vals")],
+                    [a_keys, b_keys, a_vals, b_vals, out_keys, out_vals])
+        if _count(out_keys, kt) != n + m or (n + m and out_vals.element_size() * out_vals[0:1].numel() != vb):
+            raise ValueError("outputs must hold n + m keys and rows of the payloads' width")
         s = _stream_for(a_keys, stream)
         fn = _sym("merge_stable_wide", kt, descending)
         _check(getattr(_lib, fn)(_ptr(a_keys), _ptr(a_vals), n, _ptr(b_keys), _ptr(b_vals), m, _ptr(out_keys),
@@ -281,6 +297,7 @@ def merge_stable(a_keys: torch.Tensor, a_vals: Optional[torch.Tensor], b_keys: t
         out_vals = torch.empty(n + m, dtype=a_vals.dtype, device=a_keys.device)
     if _count(out_keys, kt) != n + m or (out_vals is not None and out_vals.numel() != n + m):
         raise ValueError("output length must be n + m")
+    _check_args([(a_vals, n, "a_vals"), (b_vals, m, "b_vals")], [a_keys, b_keys, a_vals, b_vals, out_keys, out_vals])
     s = _stream_for(a_keys, stream)
     opt = _options(p_A, p_B, block, (0 if pdl else SM_FLAG_NO_PDL) | (SM_FLAG_MERGE_PATH if merge_path else 0))
     args = (_ptr(a_keys), _ptr(a_vals), n, _ptr(b_keys), _ptr(b_vals), m, _ptr(out_keys), _ptr(out_vals), s)
@@ -320,6 +337,10 @@ def merge_stable_batched(a_keys: torch.Tensor, a_vals: Optional[torch.Tensor], a
     n, m = _count(a_keys, kt), _count(b_keys, kt)
     if out_keys is None:
         out_keys = _empty_keys(n + m, a_keys, kt)
+    if _count(out_keys, kt) != n + m:
+        raise ValueError("out_keys must hold n + m keys")
+    _check_args([(a_vals, n, "a_vals"), (b_vals, m, "b_vals"), (out_vals, n + m, "out_vals")],
+                [a_keys, b_keys, a_vals, b_vals, a_offsets, b_offsets, out_keys, out_vals])
     s = _stream_for(a_keys, stream)
     if wide:
         vb = _wide_args(a_vals, b_vals)
@@ -368,6 +389,7 @@ def mergesort_stable(keys: torch.Tensor, vals: Optional[torch.Tensor] = None, *,
     _vals_ok(vals)
     if vals is not None and vals.numel() != N:
         raise ValueError("vals must have the same length as keys")
+    _check_args([], [keys, vals])
     args = (_ptr(keys), _ptr(vals), N, s)
     if pdl and not run:
         fn = _sym("mergesort_stable", kt, descending)

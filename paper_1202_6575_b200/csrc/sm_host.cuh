@@ -22,6 +22,7 @@
 #include <vector>
 #include <climits>
 #include <initializer_list>
+#include <mutex>
 
 #include "stablemerge.h"
 #include "sm_kernels.cuh"
@@ -160,26 +161,42 @@ static int current_device() {
     return dev;
 }
 
-// The default memory pool keeps freed blocks (no release at every sync), so
-// the per-call rank arrays cost no cudaMalloc after the first call.
-static void keep_pool(cudaStream_t) {
-    static bool done[SM_MAX_DEV];
+// The library's scratch (rank arrays, task descriptors, the sort's auxiliary
+// buffers, staging copies) comes from a private stream-ordered memory pool per
+// device that keeps freed blocks (release threshold: never), so steady-state
+// calls allocate nothing new -- without changing the release behaviour of the
+// device's default pool for the rest of the process.
+static cudaMemPool_t lib_pool() {
+    static cudaMemPool_t pools[SM_MAX_DEV];
+    static std::mutex mu;
     const int dev = current_device();
-    if (dev < SM_MAX_DEV && done[dev]) return;
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-        uint64_t thr = UINT64_MAX;
-        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    if (dev < SM_MAX_DEV && pools[dev]) return pools[dev];
+    std::lock_guard<std::mutex> lock(mu);
+    if (dev < SM_MAX_DEV && pools[dev]) return pools[dev];
+    cudaMemPoolProps props;
+    memset(&props, 0, sizeof(props));
+    props.allocType = cudaMemAllocationTypePinned;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = dev;
+    cudaMemPool_t pool = nullptr;
+    if (cudaMemPoolCreate(&pool, &props) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;                                  // dalloc falls back to the default pool
     }
-    cudaGetLastError();
-    if (dev < SM_MAX_DEV) done[dev] = true;
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    if (dev < SM_MAX_DEV) pools[dev] = pool;
+    return pool;
 }
+static void keep_pool(cudaStream_t) { lib_pool(); }
 
 template <typename T>
 static sm_status dalloc(T** p, int64_t count, cudaStream_t st) {
     *p = nullptr;
     if (count <= 0) return SM_OK;
-    cudaError_t e = cudaMallocAsync((void**)p, (size_t)count * sizeof(T), st);
+    cudaMemPool_t pool = lib_pool();
+    cudaError_t e = pool ? cudaMallocFromPoolAsync((void**)p, (size_t)count * sizeof(T), pool, st)
+                         : cudaMallocAsync((void**)p, (size_t)count * sizeof(T), st);
     if (e != cudaSuccess) {
         cudaGetLastError();
         snprintf(g_err, sizeof(g_err), "cudaMallocAsync(%lld bytes): %s", (long long)(count * sizeof(T)),
@@ -459,6 +476,31 @@ static sm_status merge_path_device(const K* A, const uint32_t* vA, int64_t n, co
     return s;
 }
 
+// The host pipelines' three streams and their events belong to one device:
+// one set per (host thread, device), created on first use.
+struct PipeStreams {
+    cudaStream_t sH = nullptr, sM = nullptr, sD = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    std::vector<cudaEvent_t> ev_a, ev_b;
+};
+static PipeStreams* pipe_streams() {
+    thread_local PipeStreams sets[SM_MAX_DEV];
+    const int dev = current_device();
+    if (dev >= SM_MAX_DEV) return nullptr;
+    PipeStreams& ps = sets[dev];
+    if (!ps.sH) {
+        if (cudaStreamCreateWithFlags(&ps.sH, cudaStreamNonBlocking) != cudaSuccess ||
+            cudaStreamCreateWithFlags(&ps.sM, cudaStreamNonBlocking) != cudaSuccess ||
+            cudaStreamCreateWithFlags(&ps.sD, cudaStreamNonBlocking) != cudaSuccess ||
+            cudaEventCreateWithFlags(&ps.ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&ps.ev_join, cudaEventDisableTiming) != cudaSuccess) {
+            ps.sH = nullptr;
+            return nullptr;
+        }
+    }
+    return &ps;
+}
+
 // ----------------------------------------------- pipelined host staging
 // A call with HOST inputs is cut into independent sub-merges with the paper's
 // own Steps 1-4 at coarse granularity (p_h blocks per array, PAPER.md
@@ -559,17 +601,12 @@ static sm_status merge_host_pipelined(const K* A, const uint32_t* vA, int64_t n,
     // break, sM merges each task once its upload event fires, sD downloads
     // each task once its merge event fires -- the two copy engines stay busy
     // concurrently and no download waits behind the next task's kernels
-    thread_local cudaStream_t sH = nullptr, sM = nullptr, sD = nullptr;
-    thread_local cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
-    thread_local std::vector<cudaEvent_t> ev_up, ev_mg;
-    if (!sH) {
-        if (cudaStreamCreateWithFlags(&sH, cudaStreamNonBlocking) != cudaSuccess ||
-            cudaStreamCreateWithFlags(&sM, cudaStreamNonBlocking) != cudaSuccess ||
-            cudaStreamCreateWithFlags(&sD, cudaStreamNonBlocking) != cudaSuccess ||
-            cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming) != cudaSuccess ||
-            cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming) != cudaSuccess)
-            return fail_cuda(cudaGetLastError(), "stream/event create");
-    }
+    PipeStreams* ps = pipe_streams();
+    if (!ps) return fail_cuda(cudaGetLastError(), "stream/event create");
+    cudaStream_t sH = ps->sH, sM = ps->sM, sD = ps->sD;
+    cudaEvent_t ev_fork = ps->ev_fork, ev_join = ps->ev_join;
+    std::vector<cudaEvent_t>& ev_up = ps->ev_a;
+    std::vector<cudaEvent_t>& ev_mg = ps->ev_b;
     std::vector<SubMerge> tasks;
     host_plan<K>(A, n, B, m, host_pipeline_blocks<K>(n, m, vC != nullptr), tasks);
     while (ev_up.size() < tasks.size()) {
@@ -1118,17 +1155,11 @@ static sm_status sort_any_device(K* keys, uint32_t* vals, int64_t N, cudaStream_
 // so the uploads overlap the chunk sorts and the downloads the last round.
 template <typename K>
 static sm_status sort_host_pipelined(K* keys, uint32_t* vals, int64_t N, cudaStream_t st, bool pdl) {
-    thread_local cudaStream_t sH = nullptr, sM = nullptr, sD = nullptr;
-    thread_local cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
-    thread_local std::vector<cudaEvent_t> evs;
-    if (!sH) {
-        if (cudaStreamCreateWithFlags(&sH, cudaStreamNonBlocking) != cudaSuccess ||
-            cudaStreamCreateWithFlags(&sM, cudaStreamNonBlocking) != cudaSuccess ||
-            cudaStreamCreateWithFlags(&sD, cudaStreamNonBlocking) != cudaSuccess ||
-            cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming) != cudaSuccess ||
-            cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming) != cudaSuccess)
-            return fail_cuda(cudaGetLastError(), "stream/event create");
-    }
+    PipeStreams* ps = pipe_streams();
+    if (!ps) return fail_cuda(cudaGetLastError(), "stream/event create");
+    cudaStream_t sH = ps->sH, sM = ps->sM, sD = ps->sD;
+    cudaEvent_t ev_fork = ps->ev_fork, ev_join = ps->ev_join;
+    std::vector<cudaEvent_t>& evs = ps->ev_a;
     auto event = [&](size_t k) -> cudaEvent_t {
         while (evs.size() <= k) {
             cudaEvent_t e;

@@ -1017,8 +1017,10 @@ __device__ __forceinline__ uint32_t cnt_get(uint64_t lo, uint64_t hi, int d) {
 #define SM_K3_MINB 2
 #endif
 template <typename K, bool HAS_V, int NT, int IPT>
-__global__ void __launch_bounds__(NT, sizeof(K) <= 8 ? SM_K3_MINB : 1) k_block_sort(const K* __restrict__ in, const uint32_t* __restrict__ vin,
-                                                   K* __restrict__ out, uint32_t* __restrict__ vout, int N) {
+// (in and out may be the same array -- phase 1 in place -- so they are not
+// __restrict__: every load of the run completes before the first barrier)
+__global__ void __launch_bounds__(NT, sizeof(K) <= 8 ? SM_K3_MINB : 1) k_block_sort(const K* in, const uint32_t* vin,
+                                                                                  K* out, uint32_t* vout, int N) {
     using Lay = K3Layout<K, HAS_V, NT, IPT>;
     using U = typename Lay::U;
     constexpr int R = Lay::R, NW = Lay::NW, ND = Lay::ND, ROW = Lay::ROW;
