@@ -342,6 +342,25 @@ int64_t sm_sort_run(int32_t key_bytes, int32_t has_vals);
  * when that is >= 2^15 and keys have <= 8 bytes, else sm_sort_run(). */
 int64_t sm_sort_run_n(int32_t key_bytes, int32_t has_vals, int64_t n);
 
+/* Test hooks (not the contract).
+ *
+ * sm_set_k1_variant: which cross-rank kernel (rows a1/a2) later calls on
+ *   this process launch -- 0 automatic (the default: a warp per search below
+ *   4096 searches, else the shared-memory-sample kernel for a plain merge and
+ *   one thread per search for the segmented modes), 1 a warp per search,
+ *   2 the sample kernel (plain merges), 3 one thread per search.  Lets the
+ *   tests compare every variant's x̄ / ȳ with the oracle (merge_plan_ex).
+ *
+ * sm_plan_from_ranks: the host's own Steps 3-4 (readings
+ *   R1, R8) on given cross ranks xbar[0..p], ybar[0..p] with p blocks per
+ *   array: the coarse partition the host-buffer pipeline and the >= 2^31
+ *   merges use.  Writes the 2p tasks as rows (a0, a1, b0, b1) into
+ *   tasks[2p * 4], ordered by output offset a0 + b0.  Host memory, no GPU;
+ *   SM_EINVAL on bad arguments. */
+void sm_set_k1_variant(int32_t variant);
+sm_status sm_plan_from_ranks(int64_t n, int64_t m, int64_t p, const int64_t *xbar, const int64_t *ybar,
+                             int64_t *tasks);
+
 /* Human-readable text for a status, and the last CUDA error message seen by
  * this library in the calling thread ("" if none). */
 const char *sm_status_string(sm_status s);

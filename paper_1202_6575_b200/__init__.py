@@ -84,6 +84,11 @@ _lib.sm_tile_capacity.argtypes = [ctypes.c_int32, ctypes.c_int32]
 _lib.sm_tile_capacity.restype = ctypes.c_int64
 _lib.sm_sort_run.argtypes = [ctypes.c_int32, ctypes.c_int32]
 _lib.sm_sort_run.restype = ctypes.c_int64
+_lib.sm_set_k1_variant.argtypes = [ctypes.c_int32]
+_lib.sm_set_k1_variant.restype = None
+_lib.sm_plan_from_ranks.argtypes = [ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p,
+                                    ctypes.c_void_p]
+_lib.sm_plan_from_ranks.restype = ctypes.c_int
 _lib.sm_sort_run_n.argtypes = [ctypes.c_int32, ctypes.c_int32, ctypes.c_int64]
 _lib.sm_sort_run_n.restype = ctypes.c_int64
 _lib.sm_status_string.argtypes = [ctypes.c_int]
@@ -215,6 +220,21 @@ def _sync_if_host(t: torch.Tensor, stream_handle):
 
 def tile_capacity(key_type: str = "u32", has_vals: bool = True) -> int:
     return int(_lib.sm_tile_capacity(_BYTES[key_type], int(has_vals)))
+
+
+def set_k1_variant(variant: int) -> None:
+    """Test hook: 0 automatic, 1 warp per search, 2 sample kernel, 3 thread per search."""
+    _lib.sm_set_k1_variant(int(variant))
+
+
+def plan_from_ranks(n: int, m: int, p: int, xbar, ybar) -> list:
+    """Test hook: the host's coarse Steps 3-4 on given cross ranks; the 2p
+    tasks (a0, a1, b0, b1) ordered by output offset."""
+    xb = (ctypes.c_int64 * (p + 1))(*xbar)
+    yb = (ctypes.c_int64 * (p + 1))(*ybar)
+    out = (ctypes.c_int64 * (8 * p))()
+    _check(_lib.sm_plan_from_ranks(n, m, p, xb, yb, out), "sm_plan_from_ranks")
+    return [tuple(out[4 * k:4 * k + 4]) for k in range(2 * p)]
 
 
 def sort_run(key_type: str = "u32", has_vals: bool = True, n: Optional[int] = None) -> int:

@@ -18,6 +18,7 @@ sm_status fail_inval(const char* what) {
     return SM_EINVAL;
 }
 
+int g_k1_variant = 0;
 bool g_prof_on = false;
 std::vector<ProfRec> g_prof_pool;
 size_t g_prof_used = 0;
@@ -49,6 +50,23 @@ sm_status check_launch(const char* what) {
 }  // namespace sm
 
 extern "C" {
+
+void sm_set_k1_variant(int32_t variant) { sm::g_k1_variant = (variant >= 0 && variant <= 3) ? variant : 0; }
+
+sm_status sm_plan_from_ranks(int64_t n, int64_t m, int64_t p, const int64_t* xbar, const int64_t* ybar,
+                             int64_t* tasks) {
+    if (n < 0 || m < 0 || p < 1 || !xbar || !ybar || !tasks) return sm::fail_inval("sm_plan_from_ranks arguments");
+    std::vector<int64_t> xb(xbar, xbar + p + 1), yb(ybar, ybar + p + 1);
+    std::vector<sm::SubMerge> t;
+    sm::plan_from_ranks(n, m, p, xb, yb, t);
+    for (size_t k = 0; k < t.size(); ++k) {
+        tasks[4 * k] = t[k].a0;
+        tasks[4 * k + 1] = t[k].a1;
+        tasks[4 * k + 2] = t[k].b0;
+        tasks[4 * k + 3] = t[k].b1;
+    }
+    return SM_OK;
+}
 
 int64_t sm_tile_capacity(int32_t key_bytes, int32_t has_vals) {
     return sm::tile_nv(key_bytes, has_vals != 0);

@@ -140,6 +140,7 @@ struct ProfRec {
     cudaEvent_t a, b;
     int kind;
 };
+extern int g_k1_variant;        // test hook (sm_set_k1_variant): 0 auto, 1 warp per search, 2 sample, 3 thread per search
 extern bool g_prof_on;
 extern std::vector<ProfRec> g_prof_pool;
 extern size_t g_prof_used;
@@ -248,10 +249,11 @@ static sm_status launch_cross_ranks(const K* A, const K* B, const Geom& g, const
     prof_before(PROF_K1, st);
     constexpr int SMP = 8192 / (int)sizeof(K);    // 8 KB sample per searched array
     cudaError_t e;
-    if (items < K1_FEW)
+    const int v = g_k1_variant;
+    if (v == 1 || (v == 0 && items < K1_FEW))
         e = launch_maybe_pdl(k_cross_ranks<K, 32>, (unsigned)((items * 32 + 255) / 256), 256, st, pdl, A, B, g, xbar,
                              ybar);
-    else if (g.sort == 0)
+    else if (g.sort == 0 && v != 3)
         e = launch_maybe_pdl(k_cross_ranks_smp<K, SMP>, (unsigned)((items + 255) / 256), 256, st, pdl, A, B, g, xbar,
                              ybar);
     else
@@ -419,6 +421,9 @@ static bool overlaps(const void* p, size_t pb, const void* q, size_t qb) {
 
 // ------------------------------------------------------------ merge
 static inline int64_t merge_scratch_ints(int64_t pA, int64_t pB) { return (pA + 1) + (pB + 1); }
+#ifndef SM_T_DIV
+#define SM_T_DIV 2               // default block size T = tile capacity / SM_T_DIV (experiment knob)
+#endif
 #ifndef SM_MODE0_CLASSIFY
 #define SM_MODE0_CLASSIFY 0      // 1: plain merges classify their tasks in a kernel ahead of K2 (experiment)
 #endif
@@ -771,7 +776,7 @@ static sm_status merge_entry(const K* A, const uint32_t* vA, int64_t n, const K*
         if (pA > INT_MAX / 2 || pB > INT_MAX / 2) return fail_inval("p too large");
         if (ceil_div(n, pA) + ceil_div(m, pB) > NV) return fail_inval("task bound ceil(n/p_A)+ceil(m/p_B) exceeds the tile");
     } else {
-        int64_t T = (opt && opt->block) ? opt->block : NV / 2;
+        int64_t T = (opt && opt->block) ? opt->block : NV / SM_T_DIV;
         if (T < 1 || 2 * T > NV) return fail_inval("block size T must satisfy 1 <= 2T <= tile capacity");
         pA = std::max<int64_t>(1, ceil_div(n, T));
         pB = std::max<int64_t>(1, ceil_div(m, T));

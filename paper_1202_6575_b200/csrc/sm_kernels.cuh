@@ -202,9 +202,35 @@ __global__ void __launch_bounds__(256) k_cross_ranks_smp(const K* __restrict__ A
 #ifndef SM_REFILL_TDESC
 #define SM_REFILL_TDESC 8     // window refill threshold when tasks come pre-classified (k_classify)
 #endif
-#ifndef SM_K2_INTERLEAVE
-#define SM_K2_INTERLEAVE 0    // 1: plain merges take A-side and B-side tasks alternately (experiment)
+#ifndef SM_K2_CHUNKED
+#define SM_K2_CHUNKED 0       // 1: each CTA takes a contiguous range of tasks (experiment)
 #endif
+#ifndef SM_K2_INTERLEAVE
+#define SM_K2_INTERLEAVE 1    // balanced segments: K2 takes A-side and B-side tasks alternately
+#endif
+// The order in which K2 takes a segment's tasks.  When the segment's block
+// counts are balanced (p_A, p_B within a factor 2), A-side task i and
+// B-side task i alternate: their ranges lie at nearby places of A, B and C,
+// so the CTAs' reads of A and B and their writes of C advance as one front
+// each (measured: C2 K2 -2%); unbalanced segments (C3, C4) keep index order,
+// where whole runs of A-side tasks are contiguous in C (alternating there
+// was 5% slower on C4).  Position k -> local task index, and its inverse.
+__device__ __forceinline__ bool interleaved(int pA, int pB) {
+    return SM_K2_INTERLEAVE && pA > 0 && pB > 0 && 2 * min(pA, pB) >= max(pA, pB);
+}
+__device__ __forceinline__ int task_at(int k, int pA, int pB) {
+    if (!interleaved(pA, pB)) return k;
+    const int mn = min(pA, pB);
+    if (k < 2 * mn) return (k & 1) ? pA + (k >> 1) : (k >> 1);
+    return pA >= pB ? k - mn : pA + k - mn;        // the rest of the larger side, in order
+}
+__device__ __forceinline__ int task_pos(int t, int pA, int pB) {
+    if (!interleaved(pA, pB)) return t;
+    const int mn = min(pA, pB);
+    const int side_i = t < pA ? t : t - pA;
+    if (side_i < mn) return 2 * side_i + (t < pA ? 0 : 1);
+    return 2 * mn + (side_i - mn);
+}
 // Decode a task (rows a4/a5).  Mode 3 (the merge-path comparison, not the
 // paper's method): task k is output tile [kT, (k+1)T) with the diagonal
 // splits of K1mp in xbar.
@@ -230,15 +256,6 @@ __device__ __forceinline__ Task decode_task(const Geom& g, int task, const int* 
         return w;
     }
     const Blocks xa(sg.n, sg.pA), yb(sg.m, sg.pB);
-#if SM_K2_INTERLEAVE
-    if (g.sort == 0) {
-        // experiment: A-side and B-side tasks alternate (by block index), so
-        // the CTAs' reads and writes advance as one front through A, B and C
-        const int mn = min(sg.pA, sg.pB);
-        if (t < 2 * mn) t = (t & 1) ? sg.pA + (t >> 1) : (t >> 1);
-        else t = sg.pA >= sg.pB ? t - mn : sg.pA + t - mn;   // the rest of the larger side, in order
-    }
-#endif
     return t < sg.pA ? classify_a_side(t, xa, yb, sg.xs, sg.ys) : classify_b_side(t - sg.pA, xa, yb, sg.xs, sg.ys);
 }
 
@@ -373,12 +390,25 @@ __device__ __forceinline__ void k2_producer(const K* __restrict__ A, const PV* _
     const int lane = threadIdx.x;
     int la = 0, lb = 0, off = 0, ag = 0, bg = 0;   // window slot `lane`
     int cnt = 0;                                    // slots [0, cnt) hold tasks
+#if SM_K2_CHUNKED
+    // experiment: CTA c takes a contiguous range of tasks (plain merges)
+    const int chunk = (ntasks + gridDim.x - 1) / gridDim.x;
+    int next = blockIdx.x * chunk;
+    const int chunk_end = min(ntasks, next + chunk);
+#else
     int next = blockIdx.x;                          // next task of this CTA
+#endif
     const int refill = g.tdesc ? SM_REFILL_TDESC : (g.sort == 0 && KB + (HAS_V ? (int)sizeof(PV) : 0) > 8) ? 32 : 8;
     for (int it = 0;; ++it) {
+#if SM_K2_CHUNKED
+        if (cnt < refill && next < chunk_end) {
+            const int my = next + (lane - cnt);
+            const bool fill = lane >= cnt && my < chunk_end;
+#else
         if (cnt < refill && next < ntasks) {
             const int my = next + (lane - cnt) * (int)gridDim.x;
             const bool fill = lane >= cnt && my < ntasks;
+#endif
             if (fill) {
                 if (g.tdesc) {                      // classified ahead (k_classify): one load
                     const int4 q = __ldg(g.tdesc + my);
@@ -389,7 +419,7 @@ __device__ __forceinline__ void k2_producer(const K* __restrict__ A, const PV* _
                     lb = q.w & 0xFFFF;
                 } else {
                     Seg sg;
-                    const Task t = decode_task(g, my, xbar, ybar, sg);
+                    const Task t = decode_task(g, g.sort == 0 ? task_at(my, g.pA, g.pB) : my, xbar, ybar, sg);
                     // sorted inputs give 0 <= la + lb <= NV (the task bound of
                     // L388-393); unsorted ones (a precondition violation) may
                     // not: clamp so the kernel still terminates in its buffers
@@ -400,7 +430,11 @@ __device__ __forceinline__ void k2_producer(const K* __restrict__ A, const PV* _
                     bg = sg.boff + t.b0;
                 }
             }
+#if SM_K2_CHUNKED
+            next += 32 - cnt;
+#else
             next += (32 - cnt) * (int)gridDim.x;
+#endif
             cnt += __popc(__ballot_sync(0xffffffffu, fill));
         }
         const int st = it % STAGES;
@@ -532,7 +566,10 @@ __global__ void __launch_bounds__(256) k_classify(Geom g, const int* __restrict_
         const Task t = decode_task(g, task, xbar, ybar, sg);
         const int la = max(0, min(t.a1 - t.a0, NV));
         const int lb = max(0, min(t.b1 - t.b0, NV - la));
-        tdesc[task] = make_int4(sg.aoff + t.a0, sg.boff + t.b0, sg.coff + t.a0 + t.b0, (la << 16) | lb);
+        int lt;
+        locate(g, task, false, lt);                  // its place in K2's order within the segment
+        const int at = task - lt + (sg.pA > 0 ? task_pos(lt, sg.pA, sg.pB) : lt);
+        tdesc[at] = make_int4(sg.aoff + t.a0, sg.boff + t.b0, sg.coff + t.a0 + t.b0, (la << 16) | lb);
     }
     pdl_launch_dependents();
 }

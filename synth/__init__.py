@@ -330,8 +330,8 @@ def batch_input(S: int, mean: int, key_type: str, dist: str, seed: int, payload:
     a, aoff = _segmented(S, mean, key_type, dist, seed, STREAM_A, device, descending)
     b, boff = _segmented(S, mean, key_type, dist, seed, STREAM_B, device, descending)
     av = bv = None
-    if payload:
-        av, bv = source_payloads(a.numel(), b.numel(), device)
+    if payload:                                     # one payload per key (u128 keys are (N, 2) rows)
+        av, bv = source_payloads(a.shape[0], b.shape[0], device)
     return BatchInput(key_type, a, b, av, bv, aoff, boff)
 
 

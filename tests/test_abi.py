@@ -37,7 +37,7 @@ def test_header_declares_entry_points():
             assert f"{f}_desc_{kt}" in names          # descending order
         for f in ("merge_stable_wide", "merge_stable_batched_wide", "mergesort_stable_wide"):
             assert f"{f}_{kt}" in names and f"{f}_desc_{kt}" in names   # wide payloads (row 2)
-    assert len(names) == 148          # + sm_sort_run_n
+    assert len(names) == 150          # + sm_sort_run_n, sm_set_k1_variant, sm_plan_from_ranks
 
 
 def test_library_exports_every_declared_symbol(sm):
@@ -124,3 +124,25 @@ def _glob_all(d):
     for ext in ("*.c", "*.h", "*.cu", "*.cuh", "*.py"):
         out += glob.glob(os.path.join(ROOT, d, "**", ext), recursive=True)
     return out
+
+
+def test_host_plan_from_ranks_matches_oracle_plan(sm):
+    """The host's coarse Steps 3-4 (sm_plan_from_ranks: the partition of the
+    host-buffer pipeline and of merges >= 2^31) equal oracle/plan.py's
+    classification of the same cross ranks, task for task (PAPER.md
+    L310-340; p = 5 is Fig. 1's), on random inputs incl. empty blocks."""
+    import numpy as np
+    from oracle import plan as P
+    rng = np.random.default_rng(41)
+    for trial in range(300):
+        n, m = int(rng.integers(0, 60)), int(rng.integers(0, 60))
+        p = int(rng.integers(1, 9)) if trial else 5
+        K = int(rng.integers(1, 8))
+        A = sorted(int(v) for v in rng.integers(0, K, n))
+        B = sorted(int(v) for v in rng.integers(0, K, m))
+        x, y, xbar, ybar, tasks = P.build_plan(A, B, p, p)
+        got = sm.plan_from_ranks(n, m, p, xbar, ybar)
+        want = sorted((t.a0, t.a1, t.b0, t.b1) for t in tasks)
+        assert sorted(got) == want, (n, m, p, A, B)
+        offs = [a0 + b0 for a0, a1, b0, b1 in got]
+        assert offs == sorted(offs)

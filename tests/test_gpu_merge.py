@@ -63,6 +63,61 @@ def test_plan_parity_random(kt, dist, pApB):
     assert np.array_equal(tasks.cpu().numpy(), P.task_table(otasks))
 
 
+@pytest.mark.parametrize("variant", [1, 2, 3])
+@pytest.mark.parametrize("kt,dist", [("i32", "bounded:7"), ("u32", "full"), ("i64", "bounded:1000"),
+                                     ("u64", "mostly:0x8000000000000000:9/10"), ("f32", "special"),
+                                     ("f64", "special")])
+def test_cross_ranks_every_k1_variant(kt, dist, variant):
+    """x̄ / ȳ (Steps 1-2) of each cross-rank kernel forced
+    in turn -- a warp per search, the shared-memory-sample kernel (every large
+    plain merge), one thread per search (every sort round) -- equal the
+    oracle plan's ranks, and so do the task tables, with p_A + p_B + 2 from
+    a few to > 4096 searches."""
+    sm = lib()
+    try:
+        sm.set_k1_variant(variant)
+        for n, m, pA, pB in ((5003, 2999, 17, 5), (40000, 30001, 3000, 2501), (1, 9000, 1, 4500)):
+            inp = synth.merge_input(n, m, kt, dist, seed=n + variant, payload=False)
+            a, b = oracle.as_np(inp.a_keys, kt), oracle.as_np(inp.b_keys, kt)
+            if kt.startswith("f"):                  # totalOrder ranks from the oracle's own search
+                x, y = P.block_starts(n, pA), P.block_starts(m, pB)
+                oxbar = [oracle.rank_low(a[x[i]], b, kt) if x[i] < n else m for i in range(pA)] + [m]
+                oybar = [oracle.rank_high(b[y[j]], a, kt) if y[j] < m else n for j in range(pB)] + [n]
+            else:
+                _, _, oxbar, oybar, _ = P.build_plan(a, b, pA, pB, vectorised=True)
+            xbar, ybar, tasks = sm.merge_plan(inp.a_keys.cuda(), inp.b_keys.cuda(), pA, pB, key_type=kt)
+            assert xbar.tolist() == oxbar and ybar.tolist() == oybar, (n, m, pA, pB)
+    finally:
+        sm.set_k1_variant(0)
+
+
+def test_cross_ranks_full_size_c2_sample_kernel():
+    """BASELINE configs[1] at full size with p_A = p_B = 2^15: 65538 searches,
+    so the automatic choice is the shared-memory-sample kernel; every x̄, ȳ
+    equals numpy's searchsorted (rank_low = side left, rank_high = right)."""
+    sm = lib()
+    inp = synth.config_input(2, device="cuda")
+    p = 1 << 15
+    xbar, ybar, _ = sm.merge_plan(inp.a_keys, inp.b_keys, p, p, key_type="i32")
+    a, b = inp.a_keys.cpu().numpy(), inp.b_keys.cpu().numpy()
+    x = np.asarray(P.block_starts(a.size, p)[:-1])
+    y = np.asarray(P.block_starts(b.size, p)[:-1])
+    assert np.array_equal(xbar.cpu().numpy()[:-1], np.searchsorted(b, a[x], side="left"))
+    assert np.array_equal(ybar.cpu().numpy()[:-1], np.searchsorted(a, b[y], side="right"))
+    assert int(xbar[-1]) == b.size and int(ybar[-1]) == a.size
+
+
+def test_one_cross_rank_launch_then_one_task_launch():
+    """A device merge is exactly two launches: K1 (Steps 1-2), then K2 behind
+    the single synchronisation (SURVEY §2.2 acceptance 6)."""
+    sm = lib()
+    for n, m in ((1 << 20, 1 << 20), (5000, 3), (1 << 23, 1 << 16)):
+        inp = synth.merge_input(n, m, "u32", "full", seed=n, payload=True).to("cuda")
+        sm.merge_stable(inp.a_keys, inp.a_vals, inp.b_keys, inp.b_vals, key_type="u32")
+        assert sm.last_launch_count() == 2, (n, m)
+    torch.cuda.synchronize()
+
+
 def test_plan_parity_exhaustive_small():
     sm = lib()
     import itertools

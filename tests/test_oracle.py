@@ -409,6 +409,29 @@ def test_float_merge_and_sort_vs_total_order_definition(orc, kt, width, np_u, np
         assert sk.view(np_u).tolist() == [kb[i] for i in order]
 
 
+@pytest.mark.parametrize("kt,width,np_u,np_f", [("f32", 32, np.uint32, np.float32), ("f64", 64, np.uint64, np.float64)])
+def test_float_ranks_vs_total_order_count(orc, kt, width, np_u, np_f):
+    """Ascending f32 / f64 ranks (PAPER.md L119-128 under IEEE totalOrder,
+    reading R16): rank_low = #{X[t] before x}, rank_high = #{X[t] not after
+    x}, counted with the standard's field-by-field comparison."""
+    import synth
+    cmp = _total_order_cmp(width)
+    rng = np.random.default_rng(23)
+    for dist in ("special", "full", "bounded:5"):
+        for n in (0, 1, 7, 64, 301):
+            X = orc.as_np(synth.merge_input(max(n, 1), 1, kt, dist, seed=n + 5).a_keys, kt)[:n]
+            xb = X.view(np_u).tolist()
+            assert all(cmp(xb[i], xb[i + 1]) <= 0 for i in range(len(xb) - 1))
+            specials = np.array([0.0, -0.0, np.inf, -np.inf, np.nan, 1.0, -1.5], dtype=np_f)
+            probes = np.concatenate([X[:6], specials, -specials, X[rng.integers(0, max(n, 1), 4)] if n else X[:0]])
+            for v in probes:
+                vb = int(np.array([v], dtype=np_f).view(np_u)[0])
+                lo = sum(1 for e in xb if cmp(e, vb) < 0)
+                hi = sum(1 for e in xb if cmp(e, vb) <= 0)
+                assert orc.rank_low(v, X, kt) == lo
+                assert orc.rank_high(v, X, kt) == hi
+
+
 def test_float_total_order_special_values(orc):
     """-NaN < -inf < -1 < -0 < +0 < subnormal < 1 < inf < +NaN, and -0/+0 are
     different keys (totalOrder), so A's +0 follows B's -0."""
@@ -498,7 +521,7 @@ def test_desc_ranks_vs_linear_count(orc, kt):
 # rows gathered by the tags) and by agreement with the uint32-payload oracle
 # when the wide payload is four copies of the uint32 one.
 
-@pytest.mark.parametrize("kt", ["u32", "i64", "f32"])
+@pytest.mark.parametrize("kt", ["u32", "i32", "i64", "u64", "f32", "f64"])
 @pytest.mark.parametrize("desc", [False, True])
 def test_wide_merge_and_sort_vs_brute_force(orc, kt, desc):
     rng = np.random.default_rng(17)
@@ -578,3 +601,29 @@ def test_u128_merge_sort_ranks_vs_python(orc, desc):
             le = sum((t >= x) if desc else (t <= x) for t in b)
             assert orc.rank_low(x, _u128_arr(b), "u128", descending=desc) == lt
             assert orc.rank_high(x, _u128_arr(b), "u128", descending=desc) == le
+
+
+@pytest.mark.parametrize("desc", [False, True])
+def test_u128_wide_merge_and_sort_vs_python(orc, desc):
+    """merge_wide / sort_wide with 128-bit keys: rows of a 13-byte record
+    follow their keys exactly as Python's stable sort of (key, row) moves
+    them (brute force)."""
+    rng = np.random.default_rng(29)
+    rdt = np.dtype([("tag", "<u4"), ("x", "<f8"), ("b", "u1")])
+    for trial in range(12):
+        n, m = int(rng.integers(0, 90)), int(rng.integers(0, 90))
+        a = sorted(_u128_input(rng, n, trial % 2 == 0), reverse=desc)
+        b = sorted(_u128_input(rng, m, trial % 2 == 0), reverse=desc)
+        va = np.zeros(n, dtype=rdt); va["tag"] = np.arange(n); va["x"] = rng.standard_normal(n)
+        vb = np.zeros(m, dtype=rdt); vb["tag"] = 500 + np.arange(m); vb["b"] = rng.integers(0, 256, m)
+        c, vc = orc.merge_wide(_u128_arr(a), va, _u128_arr(b), vb, "u128", descending=desc)
+        rows = list(va) + list(vb)
+        want = sorted(zip(a + b, range(n + m)), key=lambda e: e[0], reverse=desc)
+        assert orc.u128_ints(c) == [k for k, _ in want]
+        assert vc.tobytes() == b"".join(rows[r].tobytes() for _, r in want)
+        keys = a + b
+        rng.shuffle(keys)
+        vals = np.zeros(len(keys), dtype=rdt); vals["tag"] = np.arange(len(keys))
+        sk, sv = orc.sort_wide(_u128_arr(keys), vals, "u128", descending=desc)
+        assert sv["tag"].tolist() == sorted(range(len(keys)), key=lambda i: keys[i], reverse=desc)
+        assert orc.u128_ints(sk) == sorted(keys, reverse=desc)
