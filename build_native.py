@@ -63,6 +63,20 @@ def build(force: bool = False, verbose: bool = False, out: str = LIB, extra_flag
     return out
 
 
+DEBUG_LIB = os.path.join(LIBDIR, "libstablemerge_debug.so")
+
+
+def build_debug(force: bool = False) -> str:
+    """The SM_DEBUG build (device-side store-range checks and K2's output
+    coverage counters, include/stablemerge.h sm_debug_cover): a separate
+    library beside the product one, loaded only when asked for
+    (SM_LIB_PATH)."""
+    if not force and os.path.exists(DEBUG_LIB) and all(os.path.getmtime(d) <= os.path.getmtime(DEBUG_LIB)
+                                                       for d in deps()):
+        return DEBUG_LIB
+    return build(out=DEBUG_LIB, extra_flags=["-DSM_DEBUG"])
+
+
 def build_oracle() -> str:
     """The CPU oracle (test infrastructure) -- building the checker is not using it."""
     sys.path.insert(0, ROOT)
@@ -73,4 +87,6 @@ def build_oracle() -> str:
 if __name__ == "__main__":
     build(force=True, verbose="--verbose" in sys.argv)
     print(LIB)
+    if "--debug" in sys.argv:
+        print(build_debug(force=True))
     print(build_oracle())

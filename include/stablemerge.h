@@ -358,6 +358,18 @@ int64_t sm_sort_run_n(int32_t key_bytes, int32_t has_vals, int64_t n);
  *   tasks[2p * 4], ordered by output offset a0 + b0.  Host memory, no GPU;
  *   SM_EINVAL on bad arguments. */
 void sm_set_k1_variant(int32_t variant);
+
+/* SM_DEBUG builds (build_native.build_debug(): lib/libstablemerge_debug.so)
+ * check the paper's disjoint-write invariant on the device (PAPER.md
+ * L343-361): every K2 store lies inside its task's output range and inside
+ * C, every K3 / K3H store inside its run, else the kernel traps (printf +
+ * __trap).  sm_debug_cover(cover, len): later K2 launches add 1 to
+ * cover[i] for every output element i they store (cover: device memory the
+ * caller zeroed, len >= the output length; NULL stops counting) -- a merge
+ * must leave exactly 1 everywhere.  Release builds: SM_EINVAL.
+ * sm_is_debug_build: 1 in SM_DEBUG builds, else 0. */
+sm_status sm_debug_cover(uint32_t *cover, int64_t len);
+int32_t sm_is_debug_build(void);
 sm_status sm_plan_from_ranks(int64_t n, int64_t m, int64_t p, const int64_t *xbar, const int64_t *ybar,
                              int64_t *tasks);
 

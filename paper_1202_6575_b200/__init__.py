@@ -84,6 +84,10 @@ _lib.sm_tile_capacity.argtypes = [ctypes.c_int32, ctypes.c_int32]
 _lib.sm_tile_capacity.restype = ctypes.c_int64
 _lib.sm_sort_run.argtypes = [ctypes.c_int32, ctypes.c_int32]
 _lib.sm_sort_run.restype = ctypes.c_int64
+_lib.sm_debug_cover.argtypes = [ctypes.c_void_p, ctypes.c_int64]
+_lib.sm_debug_cover.restype = ctypes.c_int
+_lib.sm_is_debug_build.argtypes = []
+_lib.sm_is_debug_build.restype = ctypes.c_int32
 _lib.sm_set_k1_variant.argtypes = [ctypes.c_int32]
 _lib.sm_set_k1_variant.restype = None
 _lib.sm_plan_from_ranks.argtypes = [ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p,
@@ -220,6 +224,19 @@ def _sync_if_host(t: torch.Tensor, stream_handle):
 
 def tile_capacity(key_type: str = "u32", has_vals: bool = True) -> int:
     return int(_lib.sm_tile_capacity(_BYTES[key_type], int(has_vals)))
+
+
+def is_debug_build() -> bool:
+    return bool(_lib.sm_is_debug_build())
+
+
+def debug_cover(cover: Optional[torch.Tensor]) -> None:
+    """SM_DEBUG builds: K2 counts every output element it stores in `cover`
+    (a zeroed int32 CUDA tensor at least as long as the output); None stops."""
+    if cover is None:
+        _check(_lib.sm_debug_cover(None, 0), "sm_debug_cover")
+    else:
+        _check(_lib.sm_debug_cover(_ptr(cover), cover.numel()), "sm_debug_cover")
 
 
 def set_k1_variant(variant: int) -> None:

@@ -19,6 +19,7 @@ sm_status fail_inval(const char* what) {
 }
 
 int g_k1_variant = 0;
+uint32_t* g_dbg_cover = nullptr;
 bool g_prof_on = false;
 std::vector<ProfRec> g_prof_pool;
 size_t g_prof_used = 0;
@@ -50,6 +51,26 @@ sm_status check_launch(const char* what) {
 }  // namespace sm
 
 extern "C" {
+
+sm_status sm_debug_cover(uint32_t* cover, int64_t len) {
+#ifdef SM_DEBUG
+    if (cover && len <= 0) return sm::fail_inval("sm_debug_cover: length");
+    sm::g_dbg_cover = cover;
+    return SM_OK;
+#else
+    (void)cover;
+    (void)len;
+    return sm::fail_inval("sm_debug_cover: not an SM_DEBUG build");
+#endif
+}
+
+int32_t sm_is_debug_build(void) {
+#ifdef SM_DEBUG
+    return 1;
+#else
+    return 0;
+#endif
+}
 
 void sm_set_k1_variant(int32_t variant) { sm::g_k1_variant = (variant >= 0 && variant <= 3) ? variant : 0; }
 

@@ -222,7 +222,24 @@ struct Geom {
     const int* task_seg;  // mode 2: segment of every task
     const int* rank_seg;  // mode 2: segment of every rank entry
     const int4* tdesc;    // modes 1, 2: tasks classified ahead by k_classify (or null)
+    uint32_t* cover;      // SM_DEBUG builds: K2 counts every output element it stores here (or null)
 };
+
+// SM_DEBUG builds: device-side checks of the disjoint-write invariant of the
+// paper's tasks: every store of K2 falls inside its
+// task's range [off, off + L) and inside C, and (sm_debug_cover) every
+// output element is stored exactly once; K3 / K3H stores stay in their run.
+#ifdef SM_DEBUG
+#define SM_DCHECK(cond, what)                                                                        \
+    do {                                                                                             \
+        if (!(cond)) {                                                                               \
+            printf("SM_DEBUG check failed: %s (block %d thread %d)\n", what, blockIdx.x, threadIdx.x); \
+            __trap();                                                                                \
+        }                                                                                            \
+    } while (0)
+#else
+#define SM_DCHECK(cond, what) do {} while (0)
+#endif
 
 // One segment, located: its ranges, block counts and rank arrays.
 struct Seg {

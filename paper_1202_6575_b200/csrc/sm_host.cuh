@@ -140,6 +140,7 @@ struct ProfRec {
     cudaEvent_t a, b;
     int kind;
 };
+extern uint32_t* g_dbg_cover;  // SM_DEBUG builds: K2's coverage counters (sm_debug_cover), or null
 extern int g_k1_variant;        // test hook (sm_set_k1_variant): 0 auto, 1 warp per search, 2 sample, 3 thread per search
 extern bool g_prof_on;
 extern std::vector<ProfRec> g_prof_pool;
@@ -284,6 +285,8 @@ static sm_status launch_tasks(const K* A, const PV* vA, const K* B, const PV* vB
         }
     }
     const long long grid = std::max(1ll, std::min<long long>(gc.tasks, (long long)per_sm * n_sm));
+    Geom gk = g;
+    gk.cover = g_dbg_cover;
     cudaLaunchConfig_t cfg;
     memset(&cfg, 0, sizeof(cfg));
     cfg.gridDim = dim3((unsigned)grid);
@@ -296,7 +299,7 @@ static sm_status launch_tasks(const K* A, const PV* vA, const K* B, const PV* vB
     cfg.attrs = attr;
     cfg.numAttrs = (pdl && !g_prof_on) ? 1 : 0;
     prof_before(PROF_K2, st);
-    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, A, vA, B, vB, C, vC, g, xbar, ybar);
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, A, vA, B, vB, C, vC, gk, xbar, ybar);
     prof_after(st);
     ++g_launches;
     if (e != cudaSuccess) {

@@ -342,6 +342,7 @@ __device__ __forceinline__ void store_middle(T* dst, const T* sbuf, int o, int L
     const uintptr_t g = (uintptr_t)dst;
     const uintptr_t gl = (g + 15) & ~(uintptr_t)15;
     const uintptr_t gh = (g + (uintptr_t)L * sizeof(T)) & ~(uintptr_t)15;
+    SM_DCHECK(gh <= gl || (gl >= g && gh <= g + (uintptr_t)L * sizeof(T)), "K2 bulk store outside its task range");
 #if SM_BULK_CHUNK_ST > 0
     for (uintptr_t c = gl; c < gh; c += SM_BULK_CHUNK_ST)
         bulk_s2g((void*)c, (const char*)(sbuf + o + (int)((gl - g) / sizeof(T))) + (c - gl),
@@ -362,7 +363,10 @@ __device__ __forceinline__ void store_edge(T* dst, const T* sbuf, int o, int L, 
     if (head > L) head = L;
     const int tail0 = gh > gl ? (int)((gh - g) / sizeof(T)) : head;
     const int e = r < head ? r : tail0 + (r - head);
-    if (e < L && (r < head || e >= tail0)) dst[e] = sbuf[o + e];
+    if (e < L && (r < head || e >= tail0)) {
+        SM_DCHECK(e >= 0 && e < L, "K2 edge store outside its task range");
+        dst[e] = sbuf[o + e];
+    }
 }
 
 // ---- producer (warp 0): classify, pack, bulk-load (rows a4/a5) ----------
@@ -743,6 +747,19 @@ __global__ void __launch_bounds__(K2Layout<K, HAS_V, NC, VT, STAGES, MAXT, PV>::
             if (nt < 0) break;
             const K* sk = (const K*)(smem + s * Lay::STAGE_BYTES);
             const PV* sv = (const PV*)(smem + s * Lay::STAGE_BYTES + Lay::KREG);
+#ifdef SM_DEBUG
+            {   // every task's output range inside C; every element counted once
+                const long long lim = g.sort == 1 ? g.N : (g.sort == 2 ? -1 : (long long)g.n + g.m);
+                for (int k = 0; k < nt; ++k) {
+                    const TaskDesc& t = desc[s * MAXT + k];
+                    const int L = t.la + t.lb;
+                    SM_DCHECK(t.off >= 0 && L >= 0 && (lim < 0 || (long long)t.off + L <= lim),
+                              "K2 task range outside C");
+                    if (g.cover)
+                        for (int e = lane; e < L; e += 32) atomicAdd(&g.cover[t.off + e], 1u);
+                }
+            }
+#endif
             if (lane < nt) {
                 const TaskDesc& t = desc[s * MAXT + lane];
                 const int L = t.la + t.lb;
@@ -1217,6 +1234,7 @@ __global__ void __launch_bounds__(NT, sizeof(K) <= 8 ? SM_K3_MINB : 1) k_block_s
     for (int k = 0; k < IPT; ++k) {
         const int e = k * NT + tid;
         if (e < len) {
+            SM_DCHECK(base + e < N, "K3 store outside the input");
             st_stream(out + base + e, KeyOrd<K>::from(kf[e]));
             if (HAS_V) st_stream(vout + base + e, vf[e]);
         }
@@ -1464,6 +1482,7 @@ __device__ __forceinline__ void k3h_pass(const K* sk, const uint32_t* sv, K* dk,
                 const K x = so_k[j];
                 const uint32_t d = BITS ? (uint32_t)(KeyOrd<K>::to(x) >> shift) & DMASK : 0u;
                 const uint32_t g = ofs[d] + (uint32_t)j;
+                SM_DCHECK(g < (uint32_t)len, "K3H store outside its block");
                 dkb[g] = x;
                 if (HAS_V) dvb[g] = so_v[j];
             }

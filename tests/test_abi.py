@@ -16,7 +16,7 @@ def declared_functions():
     names = []
     for h in glob.glob(os.path.join(ROOT, "include", "*.h")):
         text = re.sub(r"/\*.*?\*/", "", open(h).read(), flags=re.S)
-        names += re.findall(r"^\s*(?:sm_status|int64_t|void|const\s+char\s*\*)\s*\*?\s*(\w+)\s*\(", text, flags=re.M)
+        names += re.findall(r"^\s*(?:sm_status|int64_t|int32_t|void|const\s+char\s*\*)\s*\*?\s*(\w+)\s*\(", text, flags=re.M)
     return names
 
 
@@ -37,7 +37,8 @@ def test_header_declares_entry_points():
             assert f"{f}_desc_{kt}" in names          # descending order
         for f in ("merge_stable_wide", "merge_stable_batched_wide", "mergesort_stable_wide"):
             assert f"{f}_{kt}" in names and f"{f}_desc_{kt}" in names   # wide payloads (row 2)
-    assert len(names) == 150          # + sm_sort_run_n, sm_set_k1_variant, sm_plan_from_ranks
+    assert len(names) == 152          # + sm_sort_run_n, sm_set_k1_variant, sm_plan_from_ranks, sm_debug_cover,
+    #                                     sm_is_debug_build
 
 
 def test_library_exports_every_declared_symbol(sm):
