@@ -2,6 +2,7 @@
 // count, the CUDA-event profiler) and the C-ABI calls that do not depend on
 // the key type (include/stablemerge.h).
 #include "sm_host.cuh"
+#include <nvtx3/nvToolsExt.h>
 
 namespace sm {
 
@@ -24,7 +25,13 @@ bool g_prof_on = false;
 std::vector<ProfRec> g_prof_pool;
 size_t g_prof_used = 0;
 
+// NVTX ranges around the launches of the method's kernels (host side; a
+// tool such as nsys / ncu --nvtx shows them, otherwise a pointer test each)
+static const char* const kKernelRange[PROF_KINDS] = {"sm K1 cross ranks (Steps 1-2)",
+                                                     "sm K2 tasks (Steps 3-4, copy / merge)",
+                                                     "sm K3 block sort (phase 1)"};
 void prof_before(int kind, cudaStream_t st) {
+    nvtxRangePushA(kind >= 0 && kind < PROF_KINDS ? kKernelRange[kind] : "sm kernel");
     if (!g_prof_on) return;
     if (g_prof_used == g_prof_pool.size()) {
         ProfRec r;
@@ -37,6 +44,7 @@ void prof_before(int kind, cudaStream_t st) {
 }
 
 void prof_after(cudaStream_t st) {
+    nvtxRangePop();
     if (!g_prof_on) return;
     cudaEventRecord(g_prof_pool[g_prof_used].b, st);
     ++g_prof_used;

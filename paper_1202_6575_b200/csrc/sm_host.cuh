@@ -24,6 +24,8 @@
 #include <initializer_list>
 #include <mutex>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "stablemerge.h"
 #include "sm_kernels.cuh"
 
@@ -351,6 +353,14 @@ static bool is_host_ptr(const void* p) {
     }
     return a.type == cudaMemoryTypeHost || a.type == cudaMemoryTypeUnregistered;
 }
+
+// An NVTX range for the whole C-ABI call (the kernels' own ranges nest in it)
+struct NvtxCall {
+    explicit NvtxCall(const char* name) { nvtxRangePushA(name); }
+    ~NvtxCall() { nvtxRangePop(); }
+    NvtxCall(const NvtxCall&) = delete;
+    NvtxCall& operator=(const NvtxCall&) = delete;
+};
 
 // A call runs on the device of its stream, whatever the calling thread's
 // current device (restored on return); the NULL, legacy and per-thread
@@ -750,6 +760,7 @@ template <typename K>
 static sm_status merge_entry(const K* A, const uint32_t* vA, int64_t n, const K* B, const uint32_t* vB, int64_t m,
                              K* C, uint32_t* vC, void* stream, const sm_options* opt) {
     DevGuard dev_guard(stream);
+    NvtxCall nvtx_call("sm merge_stable");
     g_launches = 0;
     g_err[0] = 0;
     cudaStream_t st = (cudaStream_t)stream;
@@ -834,6 +845,7 @@ static sm_status batch_entry(const K* A, const PV* vA, int64_t n, const int64_t*
                              const PV* vB, int64_t m, const int64_t* b_off, int64_t S, K* C, PV* vC,
                              void* stream) {
     DevGuard dev_guard(stream);
+    NvtxCall nvtx_call("sm merge_stable_batched");
     g_launches = 0;
     g_err[0] = 0;
     cudaStream_t st = (cudaStream_t)stream;
@@ -902,6 +914,7 @@ template <typename K>
 static sm_status ranks_entry(const K* X, int64_t len, const K* keys, int64_t nkeys, int32_t high, int64_t* out,
                              void* stream) {
     DevGuard dev_guard(stream);
+    NvtxCall nvtx_call("sm ranks_stable");
     g_launches = 0;
     g_err[0] = 0;
     cudaStream_t st = (cudaStream_t)stream;
@@ -1303,6 +1316,7 @@ static sm_status sort_host_pipelined(K* keys, uint32_t* vals, int64_t N, cudaStr
 template <typename K>
 static sm_status sort_entry(K* keys, uint32_t* vals, int64_t N, void* stream, const sm_options* opt) {
     DevGuard dev_guard(stream);
+    NvtxCall nvtx_call("sm mergesort_stable");
     g_launches = 0;
     g_err[0] = 0;
     cudaStream_t st = (cudaStream_t)stream;
@@ -1374,6 +1388,7 @@ template <typename K>
 static sm_status merge_wide_entry(const K* A, const void* vA, int64_t n, const K* B, const void* vB, int64_t m, K* C,
                                   void* vC, int64_t vbytes, void* stream) {
     DevGuard dev_guard(stream);
+    NvtxCall nvtx_call("sm merge_stable_wide");
     g_launches = 0;
     g_err[0] = 0;
     cudaStream_t st = (cudaStream_t)stream;
@@ -1451,6 +1466,7 @@ static sm_status batch_wide_entry(const K* A, const void* vA, int64_t n, const i
 template <typename K>
 static sm_status sort_wide_entry(K* keys, void* vals, int64_t N, int64_t vbytes, void* stream) {
     DevGuard dev_guard(stream);
+    NvtxCall nvtx_call("sm mergesort_stable_wide");
     g_launches = 0;
     g_err[0] = 0;
     cudaStream_t st = (cudaStream_t)stream;

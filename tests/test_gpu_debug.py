@@ -36,11 +36,11 @@ def covered(n_out, fn):
 for cfg, scale in ((1, 16), (2, 256), (3, 512), (4, 256)):
     inp = synth.config_input(cfg, scale=scale)
     d = inp.to(dev)
-    for p in (None, 3):
-        kw = {} if p is None else dict(p_A=p, p_B=p + 2)
+    for blk in (None, 500):
+        kw = {} if blk is None else dict(block=blk)
         cover, (ck, cv) = covered(inp.n + inp.m, lambda: sm.merge_stable(d.a_keys, d.a_vals, d.b_keys, d.b_vals,
                                                                         key_type=inp.key_type, **kw))
-        assert bool((cover == 1).all()), ("merge coverage", cfg, p, int(cover.min()), int(cover.max()))
+        assert bool((cover == 1).all()), ("merge coverage", cfg, blk, int(cover.min()), int(cover.max()))
         want = oracle.merge(inp.a_keys, inp.a_vals, inp.b_keys, inp.b_vals, inp.key_type)
         assert_bit_exact(ck.cpu(), None if cv is None else cv.cpu(), *want, inp.key_type)
 # batched merges
