@@ -109,7 +109,7 @@ int64_t sm_sort_run_n(int32_t key_bytes, int32_t has_vals, int64_t n) {
     // phase1_run's rule for 16-byte-aligned buffers, on the current device
     const int64_t r3 = sm::k3_run(key_bytes, has_vals != 0);
     if (key_bytes > 8 || n <= 0) return r3;
-    const int64_t L0 = sm::ceil_div(sm::ceil_div(n, sm::sm_count()), 16) * 16;
+    const int64_t L0 = sm::ceil_div(sm::ceil_div(n, sm::k3h_blocks()), 16) * 16;
     return L0 >= sm::K3H_MIN_RUN ? L0 : r3;
 }
 

@@ -1027,6 +1027,21 @@ static int sm_count() {
     return n;
 }
 
+// The block count p of the one-block-per-SM phase 1: the SM count times
+// SM_K3H_CTAS (CTAs per SM), optionally rounded down to a power of two.
+#ifndef SM_K3H_CTAS
+#define SM_K3H_CTAS 1
+#endif
+#ifndef SM_K3H_POW2
+#define SM_K3H_POW2 0
+#endif
+static int64_t k3h_blocks() {
+    int64_t p = (int64_t)sm_count() * SM_K3H_CTAS;
+    if (SM_K3H_POW2)
+        while (p & (p - 1)) p &= p - 1;
+    return p;
+}
+
 // Phase 1 (row a8): the initial run length of a sort of N elements.  Keys of
 // <= 8 bytes: the paper's p = the processing elements -- one block per SM
 // (K3H), so phase 2 takes ceil(log2 p) rounds -- when those blocks are long
@@ -1040,7 +1055,7 @@ static int64_t phase1_run(int64_t N, const void* keys, const void* vals, int64_t
     const int64_t r3 = k3_run((int)sizeof(K), vals != nullptr);
     if (forced) return forced;
     if (sizeof(K) > 8 || (((uintptr_t)keys | (uintptr_t)vals) & 15)) return r3;
-    const int64_t L0 = ceil_div(ceil_div(N, sm_count()), 16) * 16;
+    const int64_t L0 = ceil_div(ceil_div(N, k3h_blocks()), 16) * 16;
     return L0 >= K3H_MIN_RUN ? L0 : r3;
 }
 

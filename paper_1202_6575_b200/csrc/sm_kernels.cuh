@@ -1264,6 +1264,9 @@ __global__ void __launch_bounds__(NT, sizeof(K) <= 8 ? SM_K3_MINB : 1) k_block_s
 // The result lands in the buffer the merge rounds start from (a third
 // buffer, so no pass is spent on the parity of the pass count).
 constexpr int K3H_NB = 256;          // buckets of an 8-bit digit
+#ifndef SM_K3H_REGKEYS
+#define SM_K3H_REGKEYS 1     // items stay in registers from the ranking to the scatter (0: re-read from smem)
+#endif
 
 template <typename K, bool HAS_V, int NT, int TILE>
 struct K3HLayout {
@@ -1376,6 +1379,119 @@ __device__ __forceinline__ uint32_t k3h_rank(uint32_t wc_s, uint32_t d, uint32_t
     return r;
 }
 
+// L2-only store of any 4/8-byte element (K3H's sorted-tile write-out: the
+// runs of a digit are short, L2 merges them into full lines)
+template <typename T>
+__device__ __forceinline__ void st_cg(T* p, T v) {
+    if constexpr (sizeof(T) == 4) { unsigned x; memcpy(&x, &v, 4); __stcg((unsigned*)p, x); }
+    else { unsigned long long x; memcpy(&x, &v, 8); __stcg((unsigned long long*)p, x); }
+}
+
+// One tile of a K3H pass (FULL: TILE elements, no padding items): rank the
+// warps' items, scan over (digit, warp), scatter into the tile sorted by
+// digit, write the sorted tile to dkb at run[d] + (position - tile start).
+// Registers hold one word per item -- (rank << 9) | digit -- and the keys
+// and payloads are re-read from the TMA target for the scatter, so the
+// target is released (`release`: the next-but-one tile's load is issued
+// there) only after the scatter.
+template <typename K, bool HAS_V, int NT, int TILE, int BITS, bool FULL, typename F>
+__device__ __forceinline__ void k3h_tile(const K* ik, const uint32_t* iv, int cnt, int shift, char* smem, K* dkb,
+                                         uint32_t* dvb, int len, F release) {
+    using Lay = K3HLayout<K, HAS_V, NT, TILE>;
+    constexpr int NW = Lay::NW, IPT = Lay::IPT;
+    constexpr uint32_t DMASK = (1u << BITS) - 1u;
+    constexpr uint32_t PAD = 256u;                         // digit of a padding item (ranked nowhere)
+    static_assert(TILE <= (1 << 22), "rank field");
+    K* so_k = (K*)(smem + Lay::OFF_SORT);
+    uint32_t* so_v = (uint32_t*)(smem + Lay::OFF_SORT + TILE * Lay::KB);
+    uint32_t* wcnt = (uint32_t*)(smem + Lay::OFF_W);
+    uint32_t* run = (uint32_t*)(smem + Lay::OFF_RUN);
+    uint32_t* ofs = (uint32_t*)(smem + Lay::OFF_OFS);
+    uint32_t* sums = (uint32_t*)(smem + Lay::OFF_RED + NW * 16);
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    uint32_t* wc = wcnt + w * K3H_NB;
+    const uint32_t wc_s = smem_addr(wc);
+    uint32_t dr[IPT];                                      // (rank in the warp << 9) | digit
+#if SM_K3H_REGKEYS
+    K key[IPT];
+    uint32_t val[HAS_V ? IPT : 1];
+#endif
+#pragma unroll
+    for (int k = 0; k < IPT; ++k) {                        // warp w: elements [w*32*IPT, ...), item k = k*32 + lane
+        const int e = (w * IPT + k) * 32 + lane;
+        const bool valid = FULL || e < cnt;
+#if SM_K3H_REGKEYS
+        if (valid) {
+            key[k] = ik[e];
+            if (HAS_V) val[k] = iv[e];
+        }
+        const uint32_t d = valid ? (BITS ? (uint32_t)(KeyOrd<K>::to(key[k]) >> shift) & DMASK : 0u) : PAD;
+#else
+        const uint32_t d = valid ? (BITS ? (uint32_t)(KeyOrd<K>::to(ik[e]) >> shift) & DMASK : 0u) : PAD;
+#endif
+        const uint32_t peers = k3h_peers<BITS>(d, FULL ? 0xffffffffu : __ballot_sync(0xffffffffu, valid));
+        dr[k] = (k3h_rank(wc_s, d, peers, lane, valid) << 9) | d;
+    }
+    __syncthreads();                                       // every warp's counts are in wcnt
+#if SM_K3H_REGKEYS
+    release();                                             // (the items are in registers)
+#endif
+    // per digit: the tile total, its exclusive scan (tile start), then every
+    // warp's first place of that digit in the sorted tile (start + earlier warps)
+    uint32_t tc = 0;
+    if (tid < K3H_NB) {
+#pragma unroll
+        for (int i = 0; i < NW; ++i) tc += wcnt[i * K3H_NB + tid];
+    }
+    const uint32_t ts = k3h_scan256(tc, sums);
+    if (tid < K3H_NB) {
+        uint32_t at = ts;
+#pragma unroll
+        for (int i = 0; i < NW; ++i) {
+            const uint32_t x = wcnt[i * K3H_NB + tid];
+            wcnt[i * K3H_NB + tid] = at;
+            at += x;
+        }
+        ofs[tid] = run[tid] - ts;
+        run[tid] += tc;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < IPT; ++k) {
+        const uint32_t d = dr[k] & 511u;
+        if (FULL || d != PAD) {
+            const int e = (w * IPT + k) * 32 + lane;
+            const uint32_t at = wc[d] + (dr[k] >> 9);
+#if SM_K3H_REGKEYS
+            (void)e;
+            so_k[at] = key[k];
+            if (HAS_V) so_v[at] = val[k];
+#else
+            so_k[at] = ik[e];
+            if (HAS_V) so_v[at] = iv[e];
+#endif
+        }
+    }
+    __syncwarp();
+    for (int i = lane; i < K3H_NB; i += 32) wc[i] = 0;     // this warp's counters, for the next tile
+    __syncthreads();                                       // sorted tile complete; the TMA target is free
+#if !SM_K3H_REGKEYS
+    release();
+#endif
+#pragma unroll
+    for (int k = 0; k < IPT; ++k) {
+        const int j = k * NT + tid;
+        if (FULL || j < cnt) {
+            const K x = so_k[j];
+            const uint32_t d = BITS ? (uint32_t)(KeyOrd<K>::to(x) >> shift) & DMASK : 0u;
+            const uint32_t g = ofs[d] + (uint32_t)j;
+            SM_DCHECK(g < (uint32_t)len, "K3H store outside its block");
+            st_cg(dkb + g, x);
+            if (HAS_V) st_cg(dvb + g, so_v[j]);
+        }
+    }
+}
+
 // One pass of K3H over the block: tiles of TILE elements in order, stable
 // by the BITS-bit digit at `shift` (BITS = 0: a copy).  Per tile: each
 // warp ranks its items (warp w: elements [w*32*IPT, (w+1)*32*IPT), item k
@@ -1388,18 +1504,9 @@ __device__ __forceinline__ uint32_t k3h_rank(uint32_t wc_s, uint32_t d, uint32_t
 // run[d] + (position - tile start of d).
 template <typename K, bool HAS_V, int NT, int TILE, int BITS>
 __device__ __forceinline__ void k3h_pass(const K* sk, const uint32_t* sv, K* dk, uint32_t* dv, int64_t base, int len,
-                                         int shift, char* smem, uint64_t* bar, uint32_t (&ph)[2]) {
+                                         int shift, char* smem, uint64_t* bar, uint32_t& ph) {
     using Lay = K3HLayout<K, HAS_V, NT, TILE>;
-    constexpr int NW = Lay::NW, IPT = Lay::IPT;
-    constexpr uint32_t DMASK = (1u << BITS) - 1u;
-    K* so_k = (K*)(smem + Lay::OFF_SORT);
-    uint32_t* so_v = (uint32_t*)(smem + Lay::OFF_SORT + TILE * Lay::KB);
-    uint32_t* wcnt = (uint32_t*)(smem + Lay::OFF_W);
-    uint32_t* run = (uint32_t*)(smem + Lay::OFF_RUN);
-    uint32_t* ofs = (uint32_t*)(smem + Lay::OFF_OFS);
-    uint32_t* tst = (uint32_t*)(smem + Lay::OFF_TST);
-    uint32_t* sums = (uint32_t*)(smem + Lay::OFF_RED + NW * 16);
-    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const int tid = threadIdx.x;
     const int ntiles = (len + TILE - 1) / TILE;
     auto in_k = [&](int b) { return (K*)(smem + Lay::OFF_IN + b * Lay::TILE_BYTES); };
     auto in_v = [&](int b) { return (uint32_t*)(smem + Lay::OFF_IN + b * Lay::TILE_BYTES + TILE * Lay::KB); };
@@ -1415,83 +1522,24 @@ __device__ __forceinline__ void k3h_pass(const K* sk, const uint32_t* sv, K* dk,
     issue(1);
     K* dkb = dk + base;
     uint32_t* dvb = HAS_V ? dv + base : nullptr;
-    uint32_t* wc = wcnt + w * K3H_NB;
-    const uint32_t lt = (1u << lane) - 1u;
     for (int t = 0; t < ntiles; ++t) {
         const int cnt = min(TILE, len - t * TILE);
-        mbar_wait(&bar[t & 1], ph[t & 1]);
-        ph[t & 1] ^= 1u;
-        const K* ik = in_k(t & 1);
-        const uint32_t* iv = in_v(t & 1);
-        K key[IPT];
-        uint32_t val[HAS_V ? IPT : 1];
-        uint32_t dig[IPT], rnk[IPT];
-#pragma unroll
-        for (int k = 0; k < IPT; ++k) {
-            const int e = (w * IPT + k) * 32 + lane;
-            const bool valid = e < cnt;
-            if (valid) {
-                key[k] = ik[e];
-                if (HAS_V) val[k] = iv[e];
-            }
-            // padding items of a ragged last tile: digit 0xFFFFFFFF, ranked nowhere
-            dig[k] = valid ? (BITS ? (uint32_t)(KeyOrd<K>::to(key[k]) >> shift) & DMASK : 0u) : 0xFFFFFFFFu;
-        }
-        const bool full = cnt == TILE;
-        const uint32_t wc_s = smem_addr(wc);
-#pragma unroll
-        for (int k = 0; k < IPT; ++k) {
-            const uint32_t d = dig[k];
-            const uint32_t peers = k3h_peers<BITS>(d, full ? 0xffffffffu : __ballot_sync(0xffffffffu, d != 0xFFFFFFFFu));
-            rnk[k] = k3h_rank(wc_s, d, peers, lane, full || d != 0xFFFFFFFFu);
-        }
-        __syncthreads();                                // counts done; TMA target t & 1 free
-        issue(t + 2);
-        // per digit: exclusive over warps (in place), tile total, tile start
-        uint32_t tc = 0;
-        if (tid < K3H_NB) {
-#pragma unroll
-            for (int i = 0; i < NW; ++i) {
-                const uint32_t x = wcnt[i * K3H_NB + tid];
-                wcnt[i * K3H_NB + tid] = tc;
-                tc += x;
-            }
-        }
-        const uint32_t ts = k3h_scan256(tc, sums);
-        if (tid < K3H_NB) {
-            tst[tid] = ts;
-            ofs[tid] = run[tid] - ts;
-            run[tid] += tc;
-        }
-        __syncthreads();
-#pragma unroll
-        for (int k = 0; k < IPT; ++k) {
-            if (dig[k] != 0xFFFFFFFFu) {
-                const uint32_t at = tst[dig[k]] + wc[dig[k]] + rnk[k];
-                so_k[at] = key[k];
-                if (HAS_V) so_v[at] = val[k];
-            }
-        }
-        __syncwarp();
-        for (int i = lane; i < K3H_NB; i += 32) wc[i] = 0;   // this warp's counters, for the next tile
-        __syncthreads();
-#pragma unroll
-        for (int k = 0; k < IPT; ++k) {
-            const int j = k * NT + tid;
-            if (j < cnt) {
-                const K x = so_k[j];
-                const uint32_t d = BITS ? (uint32_t)(KeyOrd<K>::to(x) >> shift) & DMASK : 0u;
-                const uint32_t g = ofs[d] + (uint32_t)j;
-                SM_DCHECK(g < (uint32_t)len, "K3H store outside its block");
-                dkb[g] = x;
-                if (HAS_V) dvb[g] = so_v[j];
-            }
-        }
+        mbar_wait(&bar[t & 1], (ph >> (t & 1)) & 1u);
+        ph ^= 1u << (t & 1);
+        if (cnt == TILE)
+            k3h_tile<K, HAS_V, NT, TILE, BITS, true>(in_k(t & 1), in_v(t & 1), TILE, shift, smem, dkb, dvb, len,
+                                                     [&] { issue(t + 2); });
+        else
+            k3h_tile<K, HAS_V, NT, TILE, BITS, false>(in_k(t & 1), in_v(t & 1), cnt, shift, smem, dkb, dvb, len,
+                                                      [&] { issue(t + 2); });
     }
 }
 
 template <typename K, bool HAS_V, int NT, int TILE>
-__global__ void __launch_bounds__(NT, 1) k_block_sort_hbm(K* buf0, uint32_t* vbuf0, K* buf1, uint32_t* vbuf1,
+#ifndef SM_K3H_MINB
+#define SM_K3H_MINB 1
+#endif
+__global__ void __launch_bounds__(NT, SM_K3H_MINB) k_block_sort_hbm(K* buf0, uint32_t* vbuf0, K* buf1, uint32_t* vbuf1,
                                                            K* buf2, uint32_t* vbuf2, int64_t N, int64_t L0,
                                                            int final_buf) {
     using Lay = K3HLayout<K, HAS_V, NT, TILE>;
@@ -1509,7 +1557,7 @@ __global__ void __launch_bounds__(NT, 1) k_block_sort_hbm(K* buf0, uint32_t* vbu
     if (base >= N) return;
     const int len = (int)min(L0, N - base);              // < 2^31 (host check)
     const int ntiles = (len + TILE - 1) / TILE;
-    uint32_t ph[2] = {0u, 0u};
+    uint32_t ph = 0u;                                   // bit b: the phase of TMA target b
     auto in_k = [&](int b) { return (K*)(smem + Lay::OFF_IN + b * Lay::TILE_BYTES); };
     auto in_v = [&](int b) { return (uint32_t*)(smem + Lay::OFF_IN + b * Lay::TILE_BYTES + TILE * Lay::KB); };
 
@@ -1532,8 +1580,8 @@ __global__ void __launch_bounds__(NT, 1) k_block_sort_hbm(K* buf0, uint32_t* vbu
         }
     };
     auto wait = [&](int t) {
-        mbar_wait(&bar[t & 1], ph[t & 1]);
-        ph[t & 1] ^= 1u;
+        mbar_wait(&bar[t & 1], (ph >> (t & 1)) & 1u);
+        ph ^= 1u << (t & 1);
     };
 
     // ---- pre-pass: the varying bytes and their histograms
@@ -1595,8 +1643,8 @@ __global__ void __launch_bounds__(NT, 1) k_block_sort_hbm(K* buf0, uint32_t* vbu
         if ((diff >> (8 * pos)) & 0xFF) { ++np; hpos = pos; }
     int npass = max(np, 1);
     if (final_buf == 0) npass = np == 0 ? 0 : max(np, 2);   // (one block: in place, or one more copying pass)
-    K* const bk[3] = {buf0, buf1, buf2};
-    uint32_t* const bv[3] = {vbuf0, vbuf1, vbuf2};
+    auto bk = [&](int b) { return b == 0 ? buf0 : (b == 1 ? buf1 : buf2); };
+    auto bv = [&](int b) { return b == 0 ? vbuf0 : (b == 1 ? vbuf1 : vbuf2); };
     int src = 0;
     for (int ps = 0; ps < npass; ++ps) {
         const int dst = ps == npass - 1 ? final_buf : (src != 1 && final_buf != 1 ? 1 : (src != 2 && final_buf != 2 ? 2 : 0));
@@ -1610,8 +1658,8 @@ __global__ void __launch_bounds__(NT, 1) k_block_sort_hbm(K* buf0, uint32_t* vbu
         if (tid < K3H_NB) c = bits ? hist[hpos * 256 + tid] : (tid == 0 ? (uint32_t)len : 0u);
         const uint32_t r0 = k3h_scan256(c, sums);
         if (tid < K3H_NB) run[tid] = r0;
-        if (bits) k3h_pass<K, HAS_V, NT, TILE, 8>(bk[src], bv[src], bk[dst], bv[dst], base, len, shift, smem, bar, ph);
-        else k3h_pass<K, HAS_V, NT, TILE, 0>(bk[src], bv[src], bk[dst], bv[dst], base, len, shift, smem, bar, ph);
+        if (bits) k3h_pass<K, HAS_V, NT, TILE, 8>(bk(src), bv(src), bk(dst), bv(dst), base, len, shift, smem, bar, ph);
+        else k3h_pass<K, HAS_V, NT, TILE, 0>(bk(src), bv(src), bk(dst), bv(dst), base, len, shift, smem, bar, ph);
         // this pass's global writes before the next pass's bulk reads (async proxy)
         asm volatile("fence.proxy.async.global;" ::: "memory");
         __syncthreads();
