@@ -130,6 +130,9 @@ constexpr int64_t k3_run(int key_bytes, bool has_v) { return (int64_t)k3_nt(key_
 // them through L1/L2 on C2-C4, within 0.3%).  Few searches (< K1_FEW): a
 // whole warp each, ~log_33 dependent rounds.
 constexpr int K1_FEW = 4096;
+#ifndef SM_K1_SMP_BYTES
+#define SM_K1_SMP_BYTES 8192     // the sample kernel's shared-memory sample per searched array
+#endif
 
 sm_status fail_cuda(cudaError_t e, const char* what);
 sm_status fail_inval(const char* what);
@@ -230,12 +233,13 @@ static GeomCounts geom_counts(const Geom& g) {
 // action is griddepcontrol.wait, so it reads nothing that kernel writes
 // before it completes.
 template <typename... KA, typename... Args>
-static cudaError_t launch_maybe_pdl(void (*kern)(KA...), unsigned grid, unsigned block, cudaStream_t st, bool pdl,
-                                    Args... args) {
+static cudaError_t launch_maybe_pdl_smem(void (*kern)(KA...), unsigned grid, unsigned block, size_t smem,
+                                         cudaStream_t st, bool pdl, Args... args) {
     cudaLaunchConfig_t cfg;
     memset(&cfg, 0, sizeof(cfg));
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(block);
+    cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -244,21 +248,34 @@ static cudaError_t launch_maybe_pdl(void (*kern)(KA...), unsigned grid, unsigned
     cfg.numAttrs = (pdl && !g_prof_on) ? 1 : 0;
     return cudaLaunchKernelEx(&cfg, kern, args...);
 }
+template <typename... KA, typename... Args>
+static cudaError_t launch_maybe_pdl(void (*kern)(KA...), unsigned grid, unsigned block, cudaStream_t st, bool pdl,
+                                    Args... args) {
+    return launch_maybe_pdl_smem(kern, grid, block, 0, st, pdl, args...);
+}
 
 template <typename K>
 static sm_status launch_cross_ranks(const K* A, const K* B, const Geom& g, const GeomCounts& gc, int* xbar, int* ybar,
                                     cudaStream_t st, bool pdl = false) {
     const long long items = gc.items;
     prof_before(PROF_K1, st);
-    constexpr int SMP = 8192 / (int)sizeof(K);    // 8 KB sample per searched array
+    constexpr int SMP = SM_K1_SMP_BYTES / (int)sizeof(K);   // sample keys per searched array
     cudaError_t e;
     const int v = g_k1_variant;
     if (v == 1 || (v == 0 && items < K1_FEW))
         e = launch_maybe_pdl(k_cross_ranks<K, 32>, (unsigned)((items * 32 + 255) / 256), 256, st, pdl, A, B, g, xbar,
                              ybar);
-    else if (g.sort == 0 && v != 3)
-        e = launch_maybe_pdl(k_cross_ranks_smp<K, SMP>, (unsigned)((items + 255) / 256), 256, st, pdl, A, B, g, xbar,
-                             ybar);
+    else if (g.sort == 0 && v != 3) {
+        auto kern = k_cross_ranks_smp<K, SMP>;
+        constexpr size_t smem = 2 * SMP * sizeof(K);
+        static bool attr[SM_MAX_DEV];
+        const int dev = current_device();
+        if (dev >= SM_MAX_DEV || !attr[dev]) {
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            if (dev < SM_MAX_DEV) attr[dev] = true;
+        }
+        e = launch_maybe_pdl_smem(kern, (unsigned)((items + 255) / 256), 256, smem, st, pdl, A, B, g, xbar, ybar);
+    }
     else
         e = launch_maybe_pdl(k_cross_ranks<K, 1>, (unsigned)((items + 255) / 256), 256, st, pdl, A, B, g, xbar, ybar);
     prof_after(st);

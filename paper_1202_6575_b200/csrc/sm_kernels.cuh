@@ -150,7 +150,8 @@ __global__ void __launch_bounds__(256) k_cross_ranks(const K* __restrict__ A, co
 template <typename K, int SMP>
 __global__ void __launch_bounds__(256) k_cross_ranks_smp(const K* __restrict__ A, const K* __restrict__ B, Geom g,
                                                          int* __restrict__ xbar, int* __restrict__ ybar) {
-    __shared__ K smp[2][SMP];                          // [0]: sample of B (A-side searches), [1]: of A
+    extern __shared__ __align__(16) char k1_smem[];
+    K (*smp)[SMP] = reinterpret_cast<K (*)[SMP]>(k1_smem);   // [0]: sample of B (A-side searches), [1]: of A
     pdl_wait();
     const int n = g.n, m = g.m, pA = g.pA, pB = g.pB;
     const int items = pA + 1 + pB + 1;
