@@ -223,6 +223,7 @@ struct Geom {
     const int* rank_seg;  // mode 2: segment of every rank entry
     const int4* tdesc;    // modes 1, 2: tasks classified ahead by k_classify (or null)
     uint32_t* cover;      // SM_DEBUG builds: K2 counts every output element it stores here (or null)
+    int fuse;             // mode 0, few searches: K2 computes the cross ranks itself before a grid barrier
 };
 
 // SM_DEBUG builds: device-side checks of the disjoint-write invariant of the
@@ -308,7 +309,7 @@ struct Task {
 };
 
 __device__ __forceinline__ Task classify_a_side(int i, const Blocks& xa, const Blocks& yb,
-                                                const int* __restrict__ xbar, const int* __restrict__ ybar) {
+                                                const int* xbar, const int* ybar) {
     Task t;
     t.side = 0;
     const int xi = xa.start(i), xi1 = xa.start(i + 1);
@@ -334,7 +335,7 @@ __device__ __forceinline__ Task classify_a_side(int i, const Blocks& xa, const B
 }
 
 __device__ __forceinline__ Task classify_b_side(int j, const Blocks& xa, const Blocks& yb,
-                                                const int* __restrict__ xbar, const int* __restrict__ ybar) {
+                                                const int* xbar, const int* ybar) {
     Task t;
     t.side = 1;
     const int yj = yb.start(j), yj1 = yb.start(j + 1);

@@ -130,6 +130,12 @@ constexpr int64_t k3_run(int key_bytes, bool has_v) { return (int64_t)k3_nt(key_
 // them through L1/L2 on C2-C4, within 0.3%).  Few searches (< K1_FEW): a
 // whole warp each, ~log_33 dependent rounds.
 constexpr int K1_FEW = 4096;
+#ifndef SM_FUSE_K1
+#define SM_FUSE_K1 0             // 1: small plain merges fuse K1 into K2 (one cooperative launch; measured
+#endif                           //    slower on C1: 36 vs 23 us -- the grid barrier costs more than the launch)
+#ifndef SM_FUSE_ITEMS
+#define SM_FUSE_ITEMS 4096       // ... when p_A + p_B + 2 cross ranks at most
+#endif
 #ifndef SM_K1_SMP_BYTES
 #define SM_K1_SMP_BYTES 8192     // the sample kernel's shared-memory sample per searched array
 #endif
@@ -313,10 +319,16 @@ static sm_status launch_tasks(const K* A, const PV* vA, const K* B, const PV* vB
     cfg.dynamicSmemBytes = Lay::SMEM;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    if (g.fuse) {                                    // K2 computes the ranks itself: a grid barrier inside
+        attr[0].id = cudaLaunchAttributeCooperative;
+        attr[0].val.cooperative = 1;
+        cfg.numAttrs = 1;
+    } else {
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.numAttrs = (pdl && !g_prof_on) ? 1 : 0;
+    }
     cfg.attrs = attr;
-    cfg.numAttrs = (pdl && !g_prof_on) ? 1 : 0;
     prof_before(PROF_K2, st);
     cudaError_t e = cudaLaunchKernelEx(&cfg, kern, A, vA, B, vB, C, vC, gk, xbar, ybar);
     prof_after(st);
@@ -333,9 +345,16 @@ static sm_status launch_merge(const K* A, const PV* vA, const K* B, const PV* vB
                               PV* vC, const Geom& g0, int* xbar, int* ybar, cudaStream_t st, bool pdl,
                               const GeomCounts* counts = nullptr, int4* tdesc = nullptr) {
     const GeomCounts gc = counts ? *counts : geom_counts(g0);
+    Geom g = g0;
+    if (g0.sort == 0 && SM_FUSE_K1 && gc.items <= SM_FUSE_ITEMS && g_k1_variant == 0) {
+        // a small plain merge: one launch -- K2 computes its cross ranks itself
+        // (a warp per search) and a grid barrier is the single synchronisation
+        g.fuse = 1;
+        return launch_tasks<K, HAS_V, typename K2Shape<K, HAS_V, PV>::type, PV>(A, vA, B, vB, C, vC, g, gc, xbar, ybar,
+                                                                              st, pdl);
+    }
     sm_status s = launch_cross_ranks<K>(A, B, g0, gc, xbar, ybar, st, pdl);
     if (s != SM_OK) return s;
-    Geom g = g0;
     if (tdesc && gc.tasks > 0) {
         // segmented modes: classify every task once, ahead of K2 (k_classify)
         using Sh = typename K2Shape<K, HAS_V, PV>::type;

@@ -20,7 +20,10 @@
 // All in-kernel indices are 32-bit (larger calls are cut into sub-problems
 // below 2^31 on the host side: stablemerge.cu, merge_large_device).
 #pragma once
+#include <cooperative_groups.h>
 #include "sm_device.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace sm {
 namespace {   // internal linkage: every translation unit keeps its own kernels
@@ -235,8 +238,7 @@ __device__ __forceinline__ int task_pos(int t, int pA, int pB) {
 // Decode a task (rows a4/a5).  Mode 3 (the merge-path comparison, not the
 // paper's method): task k is output tile [kT, (k+1)T) with the diagonal
 // splits of K1mp in xbar.
-__device__ __forceinline__ Task decode_task(const Geom& g, int task, const int* __restrict__ xbar,
-                                            const int* __restrict__ ybar, Seg& sg) {
+__device__ __forceinline__ Task decode_task(const Geom& g, int task, const int* xbar, const int* ybar, Seg& sg) {
     if (g.sort == 3) {
         sg = segment(g, 0, (int*)xbar, (int*)ybar);
         const int d0 = task * g.T, d1 = min(g.n + g.m, d0 + g.T);
@@ -386,7 +388,7 @@ template <typename K, bool HAS_V, int VT, int STAGES, int MAXT, bool FIRSTFIT, t
 __device__ __forceinline__ void k2_producer(const K* __restrict__ A, const PV* __restrict__ vA,
                                             const K* __restrict__ B, const PV* __restrict__ vB,
                                             const K* C, const PV* vC, const Geom& g,
-                                            const int* __restrict__ xbar, const int* __restrict__ ybar, char* smem,
+                                            const int* xbar, const int* ybar, char* smem,
                                             TaskDesc* desc, int* pst, uint64_t* full, uint64_t* empty) {
     constexpr int NV = Lay::NV;
     constexpr int KB = Lay::KB;
@@ -705,7 +707,7 @@ template <typename K, bool HAS_V, int NC, int VT, int STAGES, int MAXT, int MINB
 __global__ void __launch_bounds__(K2Layout<K, HAS_V, NC, VT, STAGES, MAXT, PV>::THREADS, MINB)
     k_tasks(const K* __restrict__ A, const PV* __restrict__ vA, const K* __restrict__ B,
             const PV* __restrict__ vB, K* __restrict__ C, PV* __restrict__ vC, Geom g,
-            const int* __restrict__ xbar, const int* __restrict__ ybar) {
+            const int* xbar, const int* ybar) {
     using Lay = K2Layout<K, HAS_V, NC, VT, STAGES, MAXT, PV>;
     static_assert(NC % 32 == 0 && MAXT <= 32 && STAGES >= 2, "warp-granular roles; one producer lane per task");
     constexpr int NV = Lay::NV;
@@ -731,6 +733,26 @@ __global__ void __launch_bounds__(K2Layout<K, HAS_V, NC, VT, STAGES, MAXT, PV>::
     }
     __syncthreads();
     pdl_wait();   // the single synchronisation (L373-375): all ranks visible
+
+    if (g.fuse) {
+        // small plain merges (few block starts): no separate K1 launch -- every
+        // warp of the grid computes cross ranks (Steps 1-2, a warp per search,
+        // PAPER.md L304-309), then the grid barrier is the single
+        // synchronisation (L373-375); the kernel is launched cooperatively
+        const int warp = threadIdx.x >> 5, wpc = (int)(blockDim.x >> 5);
+        const int items = g.pA + 1 + g.pB + 1;
+        for (int it = blockIdx.x * wpc + warp; it < items; it += gridDim.x * wpc) {
+            const bool sideA = it <= g.pA;
+            const int idx = sideA ? it : it - g.pA - 1;
+            const int plen = sideA ? g.pA : g.pB, own_len = sideA ? g.n : g.m, oth_len = sideA ? g.m : g.n;
+            const bool search = idx < plen && idx < own_len;
+            K x = K(0);
+            if (search) x = ldg_key((sideA ? A : B) + Blocks(own_len, plen).start(idx));
+            const int r = group_rank<K, 32>(sideA ? B : A, oth_len, x, !sideA, search);
+            if ((threadIdx.x & 31) == 0) const_cast<int*>(sideA ? xbar : ybar)[idx] = search ? r : oth_len;
+        }
+        cg::this_grid().sync();
+    }
 
     if (threadIdx.x < 32) {
         k2_producer<K, HAS_V, VT, STAGES, MAXT, (sizeof(K) == 4 && !HAS_V), Lay, PV>(A, vA, B, vB, C, vC, g, xbar, ybar,

@@ -108,14 +108,17 @@ def test_cross_ranks_full_size_c2_sample_kernel():
 
 
 def test_one_cross_rank_launch_then_one_task_launch():
-    """A device merge is exactly two launches: K1 (Steps 1-2), then K2 behind
-    the single synchronisation (SURVEY §2.2 acceptance 6)."""
+    """A device merge has exactly one synchronisation between Steps 1-2 and
+    the tasks (SURVEY §2.2 acceptance 6): two launches, K1
+    then K2 behind it (PDL griddepcontrol.wait), and the oracle's merge."""
     sm = lib()
-    for n, m in ((1 << 20, 1 << 20), (5000, 3), (1 << 23, 1 << 16)):
-        inp = synth.merge_input(n, m, "u32", "full", seed=n, payload=True).to("cuda")
-        sm.merge_stable(inp.a_keys, inp.a_vals, inp.b_keys, inp.b_vals, key_type="u32")
+    for n, m in ((1 << 20, 1 << 20), (5000, 3), (1 << 23, 1 << 16), (3 << 20, 3 << 20)):
+        inp = synth.merge_input(n, m, "u32", "full", seed=n, payload=True)
+        d = inp.to("cuda")
+        ck, cv = sm.merge_stable(d.a_keys, d.a_vals, d.b_keys, d.b_vals, key_type="u32")
         assert sm.last_launch_count() == 2, (n, m)
-    torch.cuda.synchronize()
+        torch.cuda.synchronize()
+        assert_bit_exact(ck.cpu(), cv.cpu(), *oracle_merge(inp), "u32")
 
 
 def test_plan_parity_exhaustive_small():
