@@ -1026,7 +1026,7 @@ static sm_status launch_block_sort(const K* in, const uint32_t* vin, K* out, uin
 #define SM_K3H_NT 512
 #endif
 #ifndef SM_K3H_TILE
-#define SM_K3H_TILE 8192
+#define SM_K3H_TILE (SM_K3H_GROUPS == 2 ? 4096 : 8192)
 #endif
 // K3H (row a8 with p = the SM count): one CTA per block of the paper's
 // partition, radix-sorted through global memory (k_block_sort_hbm).

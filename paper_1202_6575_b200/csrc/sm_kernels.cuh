@@ -1287,6 +1287,9 @@ __global__ void __launch_bounds__(NT, sizeof(K) <= 8 ? SM_K3_MINB : 1) k_block_s
 // The result lands in the buffer the merge rounds start from (a third
 // buffer, so no pass is spent on the parity of the pass count).
 constexpr int K3H_NB = 256;          // buckets of an 8-bit digit
+#ifndef SM_K3H_GROUPS
+#define SM_K3H_GROUPS 2      // 2: two warp groups take alternate tiles (one ranks while the other writes)
+#endif
 #ifndef SM_K3H_REGKEYS
 #define SM_K3H_REGKEYS 1     // items stay in registers from the ranking to the scatter (0: re-read from smem)
 #endif
@@ -1299,18 +1302,22 @@ struct K3HLayout {
     static constexpr int IPT = TILE / NT;
     static constexpr int NPOS = (int)sizeof(U);
     static constexpr int TILE_BYTES = TILE * (KB + (HAS_V ? 4 : 0));
+    static constexpr int GROUPS = SM_K3H_GROUPS;                 // warp groups working on alternate tiles
+    static constexpr int GT = NT / GROUPS;                       // threads per group
+    static constexpr int GIPT = TILE / GT;                       // items per thread of a group's tile
     static constexpr int OFF_IN = 0;                            // 2 TMA targets: keys[TILE], vals[TILE]
-    static constexpr int OFF_SORT = OFF_IN + 2 * TILE_BYTES;    // the tile sorted by digit
-    static constexpr int OFF_W = OFF_SORT + TILE_BYTES;         // warp counters [NW][256]
+    static constexpr int OFF_SORT = OFF_IN + 2 * TILE_BYTES;    // per group: the tile sorted by digit
+    static constexpr int OFF_W = OFF_SORT + GROUPS * TILE_BYTES;  // warp counters [NW][256]
     static constexpr int OFF_HIST = OFF_W + NW * K3H_NB * 4;    // [NPOS][256]
     static constexpr int OFF_RUN = OFF_HIST + NPOS * 256 * 4;   // running offsets [256]
     static constexpr int OFF_TOT = OFF_RUN + K3H_NB * 4;        // tile totals [256]
-    static constexpr int OFF_OFS = OFF_TOT + K3H_NB * 4;        // run[d] - tile start[d] [256]
-    static constexpr int OFF_TST = OFF_OFS + K3H_NB * 4;        // tile starts [256]
+    static constexpr int OFF_OFS = OFF_TOT + K3H_NB * 4;        // per group: run[d] - tile start[d] [256]
+    static constexpr int OFF_TST = OFF_OFS + GROUPS * K3H_NB * 4;  // tile starts [256]
     static constexpr int OFF_RED = OFF_TST + K3H_NB * 4;        // [NW] diff (U), [8] scan sums
     static constexpr int OFF_BAR = (OFF_RED + NW * 16 + 64 + 15) & ~15;
     static constexpr int SMEM = OFF_BAR + 16;
     static_assert(TILE % NT == 0 && NT % 32 == 0 && NT >= K3H_NB && (TILE * KB) % 16 == 0, "tile shape");
+    static_assert(GROUPS == 1 || (GROUPS == 2 && GT == K3H_NB), "two groups of 256 threads");
 };
 
 // L2-coherent load of any 4/8/16-byte element (bypasses L1: the block's
@@ -1558,6 +1565,144 @@ __device__ __forceinline__ void k3h_pass(const K* sk, const uint32_t* sv, K* dk,
     }
 }
 
+// ---- K3H with two warp groups (SM_K3H_GROUPS = 2): group g (threads
+// 256g .. 256g+255) takes tiles t = g, g+2, ... of a pass, so one group ranks
+// its tile while the other scatters and writes its own (their barriers are
+// named barriers of 256 threads).  The block's running digit offsets run[]
+// advance in tile order: the group of tile t waits (bar.sync, 512 threads)
+// for the group of tile t-1 to have added that tile's counts (bar.arrive).
+__device__ __forceinline__ void k3h_gbar(int g) { named_sync(1 + g, 256); }
+__device__ __forceinline__ void k3h_hand_arrive(int id) {
+    asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(512) : "memory");
+}
+
+// Exclusive scan of v over the 256 threads of group g (one group barrier).
+__device__ __forceinline__ uint32_t k3h_scan_group(uint32_t v, uint32_t* sums, int g) {
+    const int tg = threadIdx.x & 255, lane = tg & 31, wg = tg >> 5;
+    uint32_t x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) sums[wg] = x;
+    k3h_gbar(g);
+    uint32_t pre = 0;
+    for (int i = 0; i < wg; ++i) pre += sums[i];
+    return pre + x - v;
+}
+
+template <typename K, bool HAS_V, int NT, int TILE, int BITS, bool FULL, typename F>
+__device__ __forceinline__ void k3h_tile_group(const K* ik, const uint32_t* iv, int cnt, int shift, char* smem, K* dkb,
+                                               uint32_t* dvb, int len, int g, int t, int ntiles, F release) {
+    using Lay = K3HLayout<K, HAS_V, NT, TILE>;
+    constexpr int IPT = Lay::GIPT;
+    constexpr uint32_t DMASK = (1u << BITS) - 1u;
+    constexpr uint32_t PAD = 256u;
+    K* so_k = (K*)(smem + Lay::OFF_SORT + g * Lay::TILE_BYTES);
+    uint32_t* so_v = (uint32_t*)(smem + Lay::OFF_SORT + g * Lay::TILE_BYTES + TILE * Lay::KB);
+    uint32_t* wcnt = (uint32_t*)(smem + Lay::OFF_W);
+    uint32_t* run = (uint32_t*)(smem + Lay::OFF_RUN);
+    uint32_t* ofs = (uint32_t*)(smem + Lay::OFF_OFS) + g * K3H_NB;
+    uint32_t* sums = (uint32_t*)(smem + Lay::OFF_RED + Lay::NW * 16) + 8 * g;
+    const int tid = threadIdx.x, tg = tid & 255, lane = tid & 31, w = tid >> 5, wg = tg >> 5;
+    uint32_t* wc = wcnt + w * K3H_NB;
+    const uint32_t wc_s = smem_addr(wc);
+    uint32_t dr[IPT];
+    K key[IPT];
+    uint32_t val[HAS_V ? IPT : 1];
+#pragma unroll
+    for (int k = 0; k < IPT; ++k) {                        // group warp wg: elements [wg*32*IPT, ...)
+        const int e = (wg * IPT + k) * 32 + lane;
+        const bool valid = FULL || e < cnt;
+        if (valid) {
+            key[k] = ik[e];
+            if (HAS_V) val[k] = iv[e];
+        }
+        const uint32_t d = valid ? (BITS ? (uint32_t)(KeyOrd<K>::to(key[k]) >> shift) & DMASK : 0u) : PAD;
+        const uint32_t peers = k3h_peers<BITS>(d, FULL ? 0xffffffffu : __ballot_sync(0xffffffffu, valid));
+        dr[k] = (k3h_rank(wc_s, d, peers, lane, valid) << 9) | d;
+    }
+    k3h_gbar(g);                                           // the group's counts are in wcnt
+    release();                                             // (the items are in registers)
+    uint32_t tc = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) tc += wcnt[(8 * g + i) * K3H_NB + tg];
+    const uint32_t ts = k3h_scan_group(tc, sums, g);
+    {
+        uint32_t at = ts;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const uint32_t x = wcnt[(8 * g + i) * K3H_NB + tg];
+            wcnt[(8 * g + i) * K3H_NB + tg] = at;
+            at += x;
+        }
+    }
+    if (t > 0) named_sync(3 + ((t - 1) & 1), 512);        // run[] holds tiles < t
+    ofs[tg] = run[tg] - ts;
+    run[tg] += tc;
+    if (t + 1 < ntiles) k3h_hand_arrive(3 + (t & 1));     // ... and now tile t too
+    k3h_gbar(g);
+#pragma unroll
+    for (int k = 0; k < IPT; ++k) {
+        const uint32_t d = dr[k] & 511u;
+        if (FULL || d != PAD) {
+            const uint32_t at = wc[d] + (dr[k] >> 9);
+            so_k[at] = key[k];
+            if (HAS_V) so_v[at] = val[k];
+        }
+    }
+    __syncwarp();
+    for (int i = lane; i < K3H_NB; i += 32) wc[i] = 0;
+    k3h_gbar(g);
+#pragma unroll
+    for (int k = 0; k < IPT; ++k) {
+        const int j = k * 256 + tg;
+        if (FULL || j < cnt) {
+            const K x = so_k[j];
+            const uint32_t d = BITS ? (uint32_t)(KeyOrd<K>::to(x) >> shift) & DMASK : 0u;
+            const uint32_t gi = ofs[d] + (uint32_t)j;
+            SM_DCHECK(gi < (uint32_t)len, "K3H store outside its block");
+            st_cg(dkb + gi, x);
+            if (HAS_V) st_cg(dvb + gi, so_v[j]);
+        }
+    }
+}
+
+template <typename K, bool HAS_V, int NT, int TILE, int BITS>
+__device__ __forceinline__ void k3h_pass_group(const K* sk, const uint32_t* sv, K* dk, uint32_t* dv, int64_t base,
+                                               int len, int shift, char* smem, uint64_t* bar, uint32_t& ph) {
+    using Lay = K3HLayout<K, HAS_V, NT, TILE>;
+    const int g = threadIdx.x >> 8, tg = threadIdx.x & 255;
+    const int ntiles = (len + TILE - 1) / TILE;
+    auto issue = [&](int t) {
+        if (tg == 0 && t < ntiles) {
+            const int e0 = t * TILE, cnt = min(TILE, len - e0), b = t & 1;
+            K* ik = (K*)(smem + Lay::OFF_IN + b * Lay::TILE_BYTES);
+            uint32_t* iv = (uint32_t*)(smem + Lay::OFF_IN + b * Lay::TILE_BYTES + TILE * Lay::KB);
+            uint32_t tx = k3h_load<K>(ik, sk + base + e0, cnt, &bar[b]);
+            if (HAS_V) tx += k3h_load<uint32_t>(iv, sv + base + e0, cnt, &bar[b]);
+            mbar_arrive_expect_tx(&bar[b], tx);
+        }
+    };
+    issue(g);
+    K* dkb = dk + base;
+    uint32_t* dvb = HAS_V ? dv + base : nullptr;
+    for (int t = g; t < ntiles; t += 2) {
+        const int cnt = min(TILE, len - t * TILE);
+        mbar_wait(&bar[g], (ph >> g) & 1u);
+        ph ^= 1u << g;
+        const K* ik = (const K*)(smem + Lay::OFF_IN + g * Lay::TILE_BYTES);
+        const uint32_t* iv = (const uint32_t*)(smem + Lay::OFF_IN + g * Lay::TILE_BYTES + TILE * Lay::KB);
+        if (cnt == TILE)
+            k3h_tile_group<K, HAS_V, NT, TILE, BITS, true>(ik, iv, TILE, shift, smem, dkb, dvb, len, g, t, ntiles,
+                                                           [&] { issue(t + 2); });
+        else
+            k3h_tile_group<K, HAS_V, NT, TILE, BITS, false>(ik, iv, cnt, shift, smem, dkb, dvb, len, g, t, ntiles,
+                                                            [&] { issue(t + 2); });
+    }
+}
+
 template <typename K, bool HAS_V, int NT, int TILE>
 #ifndef SM_K3H_MINB
 #define SM_K3H_MINB 1
@@ -1681,8 +1826,14 @@ __global__ void __launch_bounds__(NT, SM_K3H_MINB) k_block_sort_hbm(K* buf0, uin
         if (tid < K3H_NB) c = bits ? hist[hpos * 256 + tid] : (tid == 0 ? (uint32_t)len : 0u);
         const uint32_t r0 = k3h_scan256(c, sums);
         if (tid < K3H_NB) run[tid] = r0;
-        if (bits) k3h_pass<K, HAS_V, NT, TILE, 8>(bk(src), bv(src), bk(dst), bv(dst), base, len, shift, smem, bar, ph);
-        else k3h_pass<K, HAS_V, NT, TILE, 0>(bk(src), bv(src), bk(dst), bv(dst), base, len, shift, smem, bar, ph);
+        if constexpr (Lay::GROUPS == 2) {
+            __syncthreads();                               // run[] of every digit before either group reads it
+            if (bits) k3h_pass_group<K, HAS_V, NT, TILE, 8>(bk(src), bv(src), bk(dst), bv(dst), base, len, shift, smem, bar, ph);
+            else k3h_pass_group<K, HAS_V, NT, TILE, 0>(bk(src), bv(src), bk(dst), bv(dst), base, len, shift, smem, bar, ph);
+        } else {
+            if (bits) k3h_pass<K, HAS_V, NT, TILE, 8>(bk(src), bv(src), bk(dst), bv(dst), base, len, shift, smem, bar, ph);
+            else k3h_pass<K, HAS_V, NT, TILE, 0>(bk(src), bv(src), bk(dst), bv(dst), base, len, shift, smem, bar, ph);
+        }
         // this pass's global writes before the next pass's bulk reads (async proxy)
         asm volatile("fence.proxy.async.global;" ::: "memory");
         __syncthreads();

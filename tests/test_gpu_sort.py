@@ -192,3 +192,23 @@ def test_sort_default_blocks_per_sm(kt, payload):
         sm.mergesort_stable(k, v, key_type=kt)
         torch.cuda.synchronize()
         assert_bit_exact(k.cpu(), None if v is None else v.cpu(), *want, kt)
+
+
+@pytest.mark.parametrize("kt", ["u32", "i32", "i64", "u64", "f32", "f64"])
+def test_sort_blocks_per_sm_descending(kt):
+    """The one-block-per-SM phase 1 under the reversed order (Desc<> keys:
+    the complemented order view drives the radix digits), forced at small
+    sizes, and at a size where it is the default: equal to the oracle's
+    descending stable sort."""
+    sm = lib()
+    cases = [(30001, 8192 + 16, "bounded:300"), (50000, 4096, "full"), (9000, 16, "equal")]
+    if kt in ("u32", "f32"):
+        cases.append((148 * (1 << 15) + 3, None, "bounded:100000" if kt == "u32" else "special"))
+    for N, run, dist in cases:
+        inp = synth.sort_input(N, kt, dist if not (kt.startswith("f") and dist == "full") else "special",
+                               seed=N + 1, payload=True)
+        want = oracle.sort(inp.keys, inp.vals, kt, descending=True)
+        k, v = inp.keys.cuda(), inp.vals.cuda()
+        sm.mergesort_stable(k, v, key_type=kt, descending=True, run=run)
+        torch.cuda.synchronize()
+        assert_bit_exact(k.cpu(), v.cpu(), *want, kt)
