@@ -29,6 +29,9 @@ namespace sm {
 namespace {   // internal linkage: every translation unit keeps its own kernels
 
 // ----------------------------------------------------------------- K1
+#ifndef K1_WAYS_SEG
+#define K1_WAYS_SEG 4    // fan-out of the one-thread-per-search kernel (sort rounds, batches)
+#endif
 #ifndef K1_WAYS
 #define K1_WAYS 4
 #endif
@@ -129,7 +132,7 @@ __global__ void __launch_bounds__(256) k_cross_ranks(const K* __restrict__ A, co
     if (search) x = ldg_key((sideA ? A + sg.aoff : B + sg.boff) + Blocks(own_len, plen).start(idx));
     int r;
     if constexpr (G == 1) {
-        r = search ? rank_kary<K, K1_WAYS>(sideA ? B + sg.boff : A + sg.aoff, oth_len, x, !sideA) : 0;
+        r = search ? rank_kary<K, K1_WAYS_SEG>(sideA ? B + sg.boff : A + sg.aoff, oth_len, x, !sideA) : 0;
     } else {
         r = group_rank<K, G>(sideA ? B + sg.boff : A + sg.aoff, oth_len, x, !sideA, search);
     }

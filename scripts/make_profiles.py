@@ -109,7 +109,7 @@ def main(tag):
         path = os.path.join(EV, rep + ".ncu-rep")
         if os.path.exists(path):
             kern = name.split("_c")[0]
-            text, tr, dur = summarize_ncu(path, 2 if "c2" in name else 5, tag, kern, 3 if "c2" in name else 2)
+            text, tr, dur = summarize_ncu(path, 2 if "c2" in name else 5, tag, kern, 3 if "c2" in name else 1)
             text = text.replace("K2 (k_tasks)", name.split("_c")[0])
             open(os.path.join(OUT, f"{tag}_ncu_{name}.md"), "w").write(text)
     mp = os.path.join(EV, "bench_c2_mergepath.log")
