@@ -21,6 +21,7 @@ sm_status fail_inval(const char* what) {
 
 int g_k1_variant = 0;
 uint32_t* g_dbg_cover = nullptr;
+unsigned long long* g_dbg_ts = nullptr;
 bool g_prof_on = false;
 std::vector<ProfRec> g_prof_pool;
 size_t g_prof_used = 0;
@@ -71,6 +72,12 @@ sm_status sm_debug_cover(uint32_t* cover, int64_t len) {
     return sm::fail_inval("sm_debug_cover: not an SM_DEBUG build");
 #endif
 }
+
+#ifdef SM_K2_TSTAMP
+// experiment builds only (not in the header): later K2 launches record their
+// per-CTA event times into ts[8 * CTA + slot] (device memory; NULL stops)
+void sm_debug_k2_timestamps(unsigned long long* ts) { sm::g_dbg_ts = ts; }
+#endif
 
 int32_t sm_is_debug_build(void) {
 #ifdef SM_DEBUG

@@ -224,7 +224,16 @@ struct Geom {
     const int4* tdesc;    // modes 1, 2: tasks classified ahead by k_classify (or null)
     uint32_t* cover;      // SM_DEBUG builds: K2 counts every output element it stores here (or null)
     int fuse;             // mode 0, few searches: K2 computes the cross ranks itself before a grid barrier
+    int* ctr;             // K2's task counter (dynamic assignment): zeroed by the kernel launched before K2
+    unsigned long long* ts;   // SM_K2_TSTAMP builds: per-CTA event times of K2 (or null)
 };
+
+// The kernel launched right before K2 (K1, k_classify, k_diag_splits) zeroes
+// K2's task counter, after its own griddepcontrol.wait: the counter lives in
+// the call's scratch, which a previous call's K2 may have used.
+__device__ __forceinline__ void zero_task_counter(int* ctr) {
+    if (ctr && blockIdx.x == 0 && threadIdx.x == 0) *ctr = 0;
+}
 
 // SM_DEBUG builds: device-side checks of the disjoint-write invariant of the
 // paper's tasks: every store of K2 falls inside its
@@ -460,6 +469,8 @@ __device__ __forceinline__ void bulk_s2g(void* dst_gmem, const void* src_smem, u
 }
 
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
 template <int N>
 __device__ __forceinline__ void bulk_wait_read() {

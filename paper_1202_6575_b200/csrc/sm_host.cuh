@@ -152,6 +152,7 @@ struct ProfRec {
     int kind;
 };
 extern uint32_t* g_dbg_cover;  // SM_DEBUG builds: K2's coverage counters (sm_debug_cover), or null
+extern unsigned long long* g_dbg_ts;   // SM_K2_TSTAMP builds: K2's per-CTA event times (sm_debug_k2_timestamps)
 extern int g_k1_variant;        // test hook (sm_set_k1_variant): 0 auto, 1 warp per search, 2 sample, 3 thread per search
 extern bool g_prof_on;
 extern std::vector<ProfRec> g_prof_pool;
@@ -312,6 +313,7 @@ static sm_status launch_tasks(const K* A, const PV* vA, const K* B, const PV* vB
     const long long grid = std::max(1ll, std::min<long long>(gc.tasks, (long long)per_sm * n_sm));
     Geom gk = g;
     gk.cover = g_dbg_cover;
+    gk.ts = g_dbg_ts;
     cudaLaunchConfig_t cfg;
     memset(&cfg, 0, sizeof(cfg));
     cfg.gridDim = dim3((unsigned)grid);
@@ -469,7 +471,8 @@ static bool overlaps(const void* p, size_t pb, const void* q, size_t qb) {
 }
 
 // ------------------------------------------------------------ merge
-static inline int64_t merge_scratch_ints(int64_t pA, int64_t pB) { return (pA + 1) + (pB + 1); }
+// x̄ (p_A + 1), ȳ (p_B + 1) and K2's task counter
+static inline int64_t merge_scratch_ints(int64_t pA, int64_t pB) { return (pA + 1) + (pB + 1) + 1; }
 #ifndef SM_T_DIV
 #define SM_T_DIV 2               // default block size T = tile capacity / SM_T_DIV (experiment knob)
 #endif
@@ -483,11 +486,12 @@ static sm_status merge_device(const K* A, const PV* vA, int64_t n, const K* B, c
                               int* ranks_given = nullptr) {
     Geom g{};
     g.S = 1; g.pA = (int)pA; g.pB = (int)pB; g.n = (int)n; g.m = (int)m; g.L = 0; g.N = 0; g.sort = 0;
-    // scratch: x̄ (p_A + 1), ȳ (p_B + 1)
+    // scratch: x̄ (p_A + 1), ȳ (p_B + 1), task counter
     int* ranks = ranks_given;
     sm_status s = SM_OK;
     if (!ranks) s = dalloc(&ranks, merge_scratch_ints(pA, pB), st);
     if (s != SM_OK) return s;
+    g.ctr = ranks + (pA + 1) + (pB + 1);
     int4* tdesc = nullptr;
 #if SM_MODE0_CLASSIFY
     s = dalloc(&tdesc, pA + pB, st);
@@ -512,15 +516,17 @@ static sm_status merge_path_device(const K* A, const uint32_t* vA, int64_t n, co
     const int64_t W = tile_nv((int)sizeof(K), vC != nullptr);
     const int64_t tiles = ceil_div(n + m, W);
     int* split = nullptr;
-    sm_status s = dalloc(&split, tiles + 1, st);
+    sm_status s = dalloc(&split, tiles + 2, st);    // splits, task counter
     if (s != SM_OK) return s;
     prof_before(PROF_K1, st);
-    k_diag_splits<K><<<(unsigned)((tiles + 1 + 255) / 256), 256, 0, st>>>(A, B, (int)n, (int)m, (int)W, split);
+    k_diag_splits<K><<<(unsigned)((tiles + 1 + 255) / 256), 256, 0, st>>>(A, B, (int)n, (int)m, (int)W, split,
+                                                                          split + tiles + 1);
     prof_after(st);
     s = check_launch("k_diag_splits");
     if (s == SM_OK) {
         Geom g{};
         g.S = 1; g.n = (int)n; g.m = (int)m; g.sort = 3; g.T = (int)W; g.pA = g.pB = 1;
+        g.ctr = split + tiles + 1;
         GeomCounts gc{tiles + 2, tiles};
         if (vC) s = launch_tasks<K, true, typename K2Shape<K, true>::type>(A, vA, B, vB, C, vC, g, gc, split, split, st, pdl);
         else s = launch_tasks<K, false, typename K2Shape<K, false>::type, uint32_t>(A, nullptr, B, nullptr, C, nullptr, g,
@@ -937,6 +943,7 @@ static sm_status batch_entry(const K* A, const PV* vA, int64_t n, const int64_t*
     if (s == SM_OK) {
         Geom g{};
         g.S = (int)S; g.sort = 2; g.T = (int)T; g.segs = segs; g.totals = totals;
+        g.ctr = totals + 2;                           // (totals[0..1]: tasks, rank entries)
         g.task_seg = task_seg; g.rank_seg = rank_seg;
         if (vC) s = launch_merge<K, true, PV>(A, vA, B, vB, C, vC, g, ranks, ranks, st, true, &gc, tdesc);
         else s = launch_merge<K, false, PV>(A, nullptr, B, nullptr, C, nullptr, g, ranks, ranks, st, true, &gc, tdesc);
@@ -1114,7 +1121,8 @@ static sm_status sort_device(K* keys, uint32_t* vals, int64_t N, cudaStream_t st
     if (s == SM_OK && hbm && vals) s = dalloc(&vb[2], N, st);
     // rank arrays for the largest round: S*(pA+1) + S*(pB+1) <= 2*(N/T + 2*S) entries
     const int64_t T = tile_t((int)sizeof(K), vals != nullptr);
-    if (s == SM_OK) s = dalloc(&ranks, 2 * (ceil_div(N, T) + 2 * ceil_div(N, R) + 2), st);
+    const int64_t rank_ints = 2 * (ceil_div(N, T) + 2 * ceil_div(N, R) + 2);
+    if (s == SM_OK) s = dalloc(&ranks, rank_ints + 1, st);     // + K2's task counter
     if (s == SM_OK) s = dalloc(&tdesc, ceil_div(N, T) + 2 * ceil_div(N, R) + 2, st);   // tasks of a round
     if (s == SM_OK) {
         int src;
@@ -1143,6 +1151,7 @@ static sm_status sort_device(K* keys, uint32_t* vals, int64_t N, cudaStream_t st
             g.S = (int)ceil_div(N, 2 * L);
             g.pA = g.pB = (int)ceil_div(L, T);
             g.n = g.m = 0; g.L = (int)L; g.N = (int)N; g.sort = 1;
+            g.ctr = ranks + rank_ints;
             int* xbar = ranks;
             int* ybar = ranks + (int64_t)g.S * (g.pA + 1);
             if (vals)

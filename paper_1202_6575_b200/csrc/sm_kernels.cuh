@@ -117,6 +117,7 @@ template <typename K, int G>
 __global__ void __launch_bounds__(256) k_cross_ranks(const K* __restrict__ A, const K* __restrict__ B, Geom g,
                                                      int* __restrict__ xbar, int* __restrict__ ybar) {
     pdl_wait();   // a batch's segment table (no-op for plain launches)
+    zero_task_counter(g.ctr);
     const long long item = ((long long)blockIdx.x * blockDim.x + threadIdx.x) / G;
     const bool valid = item < (long long)total_rank_items(g);
     int s = 0, t = 0;
@@ -159,6 +160,7 @@ __global__ void __launch_bounds__(256) k_cross_ranks_smp(const K* __restrict__ A
     extern __shared__ __align__(16) char k1_smem[];
     K (*smp)[SMP] = reinterpret_cast<K (*)[SMP]>(k1_smem);   // [0]: sample of B (A-side searches), [1]: of A
     pdl_wait();
+    zero_task_counter(g.ctr);
     const int n = g.n, m = g.m, pA = g.pA, pB = g.pB;
     const int items = pA + 1 + pB + 1;
     const int i0 = blockIdx.x * blockDim.x;
@@ -209,8 +211,21 @@ __global__ void __launch_bounds__(256) k_cross_ranks_smp(const K* __restrict__ A
 #ifndef SM_REFILL_TDESC
 #define SM_REFILL_TDESC 8     // window refill threshold when tasks come pre-classified (k_classify)
 #endif
-#ifndef SM_K2_CHUNKED
-#define SM_K2_CHUNKED 0       // 1: each CTA takes a contiguous range of tasks (experiment)
+#ifndef SM_K2_CHUNK
+#define SM_K2_CHUNK 8         // tasks per reservation of the dynamic assignment, at most (<= 8-byte elements;
+#endif                        //   measured: 4 and 16 within 1% on C2 / C5)
+#ifndef SM_K2_CHUNK_WIDE
+#define SM_K2_CHUNK_WIDE 4    // ... wider elements (C3 / C4: 4 measured 0.5% faster than 8)
+#endif
+#ifndef SM_K2_TAILWIN
+#define SM_K2_TAILWIN 16      // the shortest refill threshold near the end of the dynamic part (4 / 8 / 32
+                              //   measured within 0.5%; a fixed static share first: no gain)
+#endif
+#ifndef SM_K2_DYN_MIN
+#define SM_K2_DYN_MIN 8       // dynamic assignment only above this many tasks per CTA
+#endif
+#ifndef SM_K2_DYN
+#define SM_K2_DYN 1           // 0: static round-robin task assignment (experiment)
 #endif
 #ifndef SM_K2_INTERLEAVE
 #define SM_K2_INTERLEAVE 1    // balanced segments: K2 takes A-side and B-side tasks alternately
@@ -266,6 +281,21 @@ __device__ __forceinline__ Task decode_task(const Geom& g, int task, const int* 
 }
 
 // ----------------------------------------------------------------- K2
+// SM_K2_TSTAMP builds (experiments, scripts/k2_timeline.py): K2 records
+// per-CTA event times (%globaltimer, ns) in g.ts[8 * CTA + slot]: 0 entry,
+// 1 first stage issued, 2 producer done, 3 storer done.
+#ifdef SM_K2_TSTAMP
+#define K2_TS(slot)                                                                    \
+    do {                                                                               \
+        if (g.ts) {                                                                    \
+            unsigned long long t_;                                                     \
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                   \
+            g.ts[8 * blockIdx.x + (slot)] = t_;                                        \
+        }                                                                              \
+    } while (0)
+#else
+#define K2_TS(slot) do {} while (0)
+#endif
 // A ring stage holds the input ranges of up to MAXT tasks ("packing"): the
 // paper's subproblems range from O(1) to ~2T elements (L388-393), so one task
 // per tile would leave half the consumer threads idle on average.  The
@@ -381,12 +411,18 @@ __device__ __forceinline__ void store_edge(T* dst, const T* sbuf, int o, int L, 
 // goes into the next ring stage; every packed task's lane issues the TMA bulk
 // loads of its A and B ranges (keys, payloads).  A stage with task count -1
 // terminates the consumers.
-// The window is refilled (up to 32 tasks classified in parallel, one per
-// lane) whenever fewer than `refill` tasks are left in it: after every stage
-// (32) for plain merges of wide elements (mode 0, > 8 bytes: measured -10%
-// on C3/C4), else only when it runs low (8): the batched and sort-round
-// classifications take more dependent loads (mode 2/1: +46%/+19% when
-// refilled every stage).
+// Tasks are handed out dynamically: the producer takes chunks of consecutive
+// positions of K2's order from the launch's task counter, so the CTAs
+// advance as one front and finish together -- a static round-robin left the
+// CTAs' finishing times 50 us apart on C2 (per-CTA timelines,
+// scripts/k2_timeline.py).  Each refill uses the chunk reserved at the
+// previous one and reserves the next (one atomicAdd, whose latency overlaps
+// the stages in between).  The window is refilled (classified in parallel,
+// one task per lane) whenever fewer than `refill` tasks are left: after every
+// stage for plain merges of wide elements (mode 0, > 8 bytes), else when it
+// runs low (8); chunks shrink to half a fair share of what is left
+// (remaining / (2 x grid)) and, near the end, windows to ~4 tasks, so no CTA
+// is left holding a long queue.
 template <typename K, bool HAS_V, int VT, int STAGES, int MAXT, bool FIRSTFIT, typename Lay, typename PV>
 __device__ __forceinline__ void k2_producer(const K* __restrict__ A, const PV* __restrict__ vA,
                                             const K* __restrict__ B, const PV* __restrict__ vB,
@@ -398,27 +434,51 @@ __device__ __forceinline__ void k2_producer(const K* __restrict__ A, const PV* _
     constexpr int EPV = Lay::EPV;
     const int ntasks = total_tasks(g);
     const int lane = threadIdx.x;
+    const int G = (int)gridDim.x;
     int la = 0, lb = 0, off = 0, ag = 0, bg = 0;   // window slot `lane`
     int cnt = 0;                                    // slots [0, cnt) hold tasks
-#if SM_K2_CHUNKED
-    // experiment: CTA c takes a contiguous range of tasks (plain merges)
-    const int chunk = (ntasks + gridDim.x - 1) / gridDim.x;
-    int next = blockIdx.x * chunk;
-    const int chunk_end = min(ntasks, next + chunk);
-#else
-    int next = blockIdx.x;                          // next task of this CTA
-#endif
-    const int refill = g.tdesc ? SM_REFILL_TDESC : (g.sort == 0 && KB + (HAS_V ? (int)sizeof(PV) : 0) > 8) ? 32 : 8;
+    int seen = 0;                                   // end of this CTA's last reservation (progress estimate)
+    bool more = ntasks > 0;
+    // few tasks per CTA (C1): static round-robin -- one refill takes them all
+    int* const ctr = (SM_K2_DYN && ntasks > SM_K2_DYN_MIN * G) ? g.ctr : nullptr;
+    const int refill =
+        g.tdesc ? SM_REFILL_TDESC : (g.sort == 0 && KB + (HAS_V ? (int)sizeof(PV) : 0) > 8) ? 32 : 8;
+    constexpr int CH = KB + (HAS_V ? (int)sizeof(PV) : 0) > 8 ? SM_K2_CHUNK_WIDE : SM_K2_CHUNK;
+    int resv = 0, resv_n = 0;                       // (lane 0) positions reserved for the next refill
+    int next = blockIdx.x;                          // (no counter: static round-robin, CTA b takes b, b+G, ...)
     for (int it = 0;; ++it) {
-#if SM_K2_CHUNKED
-        if (cnt < refill && next < chunk_end) {
-            const int my = next + (lane - cnt);
-            const bool fill = lane >= cnt && my < chunk_end;
-#else
-        if (cnt < refill && next < ntasks) {
-            const int my = next + (lane - cnt) * (int)gridDim.x;
-            const bool fill = lane >= cnt && my < ntasks;
-#endif
+        // dynamic: refill while the window has room for a chunk; near the end
+        // (fewer than SM_K2_TAILWIN tasks per CTA left) keep the window short
+        const bool dyn = ctr != nullptr;
+        const int thr = dyn ? min(min(refill, 33 - CH), max(SM_K2_TAILWIN, (ntasks - seen) / G)) : refill;
+        if (cnt < thr && more) {
+            int base, stride, take = 32;
+            if (dyn) {
+                if (resv_n == 0) {                  // first refill: reserve now
+                    resv_n = max(1, min(CH, ntasks / (2 * G)));
+                    if (lane == 0) resv = atomicAdd(ctr, resv_n);
+                }
+                base = __shfl_sync(0xffffffffu, resv, 0);   // (waits for the reservation)
+                take = resv_n;
+                seen = base + take;
+                more = seen < ntasks;
+                if (more) {
+                    // reserve the next chunk now: the atomic's latency overlaps
+                    // the stages until the next refill.  Chunks shrink to half
+                    // a fair share of what is left, down to single tasks.
+                    resv_n = max(1, min(CH, (ntasks - seen) / (2 * G)));
+                    if (lane == 0) resv = atomicAdd(ctr, resv_n);
+                }
+                stride = 1;
+                base -= cnt;                        // lane l in [cnt, cnt + take) takes position base + l
+            } else {
+                base = next;
+                stride = G;
+                next += (32 - cnt) * G;
+                more = next < ntasks;
+            }
+            const int my = base + (lane - (dyn ? 0 : cnt)) * stride;
+            const bool fill = lane >= cnt && lane < cnt + take && my < ntasks;
             if (fill) {
                 if (g.tdesc) {                      // classified ahead (k_classify): one load
                     const int4 q = __ldg(g.tdesc + my);
@@ -440,11 +500,6 @@ __device__ __forceinline__ void k2_producer(const K* __restrict__ A, const PV* _
                     bg = sg.boff + t.b0;
                 }
             }
-#if SM_K2_CHUNKED
-            next += 32 - cnt;
-#else
-            next += (32 - cnt) * (int)gridDim.x;
-#endif
             cnt += __popc(__ballot_sync(0xffffffffu, fill));
         }
         const int st = it % STAGES;
@@ -454,6 +509,7 @@ __device__ __forceinline__ void k2_producer(const K* __restrict__ A, const PV* _
             if (lane == 0) {
                 ps[MAXT + 1] = -1;
                 mbar_arrive(&full[st]);
+                K2_TS(2);
             }
             return;
         }
@@ -541,8 +597,10 @@ __device__ __forceinline__ void k2_producer(const K* __restrict__ A, const PV* _
         // the descriptors are released by the arrive; the bulk loads may
         // complete_tx before the expect_tx (the phase needs both)
         __syncwarp();
-        if (lane == 0)
+        if (lane == 0) {
             mbar_arrive_expect_tx(&full[st], (uint32_t)(ktot - 16 * take + (HAS_V ? vtot - 16 * take : 0)));
+            if (it == 0) K2_TS(1);
+        }
         // drop the packed tasks from the window, keeping the order of the rest
         int sl = lane + take;                            // prefix packed: shift down
         if constexpr (FIRSTFIT) {
@@ -570,6 +628,7 @@ template <int NV>
 __global__ void __launch_bounds__(256) k_classify(Geom g, const int* __restrict__ xbar, const int* __restrict__ ybar,
                                                   int4* __restrict__ tdesc) {
     pdl_wait();
+    zero_task_counter(g.ctr);
     const int task = blockIdx.x * blockDim.x + threadIdx.x;
     if (task < total_tasks(g)) {
         Seg sg;
@@ -736,6 +795,7 @@ __global__ void __launch_bounds__(K2Layout<K, HAS_V, NC, VT, STAGES, MAXT, PV>::
     }
     __syncthreads();
     pdl_wait();   // the single synchronisation (L373-375): all ranks visible
+    if (threadIdx.x == 0) K2_TS(0);
 
     if (g.fuse) {
         // small plain merges (few block starts): no separate K1 launch -- every
@@ -770,7 +830,13 @@ __global__ void __launch_bounds__(K2Layout<K, HAS_V, NC, VT, STAGES, MAXT, PV>::
             const int s = it % STAGES;
             mbar_wait_sleep(&written[s], (it / STAGES) & 1);
             const int nt = pst[s * (MAXT + 2) + MAXT + 1];
-            if (nt < 0) break;
+            if (nt < 0) {
+#ifdef SM_K2_TSTAMP
+                bulk_wait_all();
+                if (lane == 0) K2_TS(3);
+#endif
+                break;
+            }
             const K* sk = (const K*)(smem + s * Lay::STAGE_BYTES);
             const PV* sv = (const PV*)(smem + s * Lay::STAGE_BYTES + Lay::KREG);
 #ifdef SM_DEBUG
@@ -918,7 +984,8 @@ __global__ void __launch_bounds__(256) k_rank_keys(const K* __restrict__ X, int6
 // memory.  Same output bytes as the method; no factor-two imbalance.
 template <typename K>
 __global__ void __launch_bounds__(256) k_diag_splits(const K* __restrict__ A, const K* __restrict__ B, int n, int m,
-                                                     int T, int* __restrict__ split) {
+                                                     int T, int* __restrict__ split, int* ctr) {
+    zero_task_counter(ctr);
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     const int tiles = (n + m + T - 1) / T;
     if (k <= tiles) {
