@@ -350,6 +350,15 @@ int64_t sm_sort_run_n(int32_t key_bytes, int32_t has_vals, int64_t n);
  *   one thread per search for the segmented modes), 1 a warp per search,
  *   2 the sample kernel (plain merges), 3 one thread per search.  Lets the
  *   tests compare every variant's x̄ / ȳ with the oracle (merge_plan_ex).
+ *   A variant other than 0 also turns the one-launch small merges off.
+ *
+ * sm_set_small_fuse: 1 -- a plain merge on device buffers with at most 8
+ *   tasks per resident K2 CTA (C1's size) is ONE launch: each CTA computes
+ *   the cross ranks its own tasks read (Steps 1-2, L304-309; a warp per
+ *   search) before classifying them, so every rank a task reads is final
+ *   first (L373-375, per CTA); 0 (the default) -- K1 then K2 as for larger
+ *   merges (measured faster when the inputs are not in L2: K2's launch then
+ *   overlaps K1 under PDL).  Both give the same output.
  *
  * sm_plan_from_ranks: the host's own Steps 3-4 (readings
  *   R1, R8) on given cross ranks xbar[0..p], ybar[0..p] with p blocks per
@@ -358,6 +367,7 @@ int64_t sm_sort_run_n(int32_t key_bytes, int32_t has_vals, int64_t n);
  *   tasks[2p * 4], ordered by output offset a0 + b0.  Host memory, no GPU;
  *   SM_EINVAL on bad arguments. */
 void sm_set_k1_variant(int32_t variant);
+void sm_set_small_fuse(int32_t on);
 
 /* SM_DEBUG builds (build_native.build_debug(): lib/libstablemerge_debug.so)
  * check the paper's disjoint-write invariant on the device (PAPER.md
@@ -372,6 +382,19 @@ sm_status sm_debug_cover(uint32_t *cover, int64_t len);
 int32_t sm_is_debug_build(void);
 sm_status sm_plan_from_ranks(int64_t n, int64_t m, int64_t p, const int64_t *xbar, const int64_t *ybar,
                              int64_t *tasks);
+
+/* Steps 3-4 on the host (readings R1, R7, R8) for cross
+ * ranks computed elsewhere -- the sharded merge ranks block
+ * starts across GPUs and classifies the p_A + p_B tasks here.
+ *   xbar[0..pA], ybar[0..pB]: x̄ (rank_low of A's block starts in B, the
+ *   sentinel x̄_pA = m, m for empty block starts) and ȳ likewise (n).
+ *   tasks[(pA + pB) * 4]: rows (a0, a1, b0, b1) in task order -- A-side task
+ *   i = 0..pA-1, then B-side task j = 0..pB-1 -- the ranges A[a0, a1) and
+ *   B[b0, b1) merged into C[a0 + b0, a1 + b1).
+ * The same classification code as the device's K2 (64-bit indices).  Host
+ * memory, no GPU; caller-owned arrays; SM_EINVAL on bad arguments. */
+sm_status sm_plan_tasks(int64_t n, int64_t m, int64_t pA, int64_t pB, const int64_t *xbar, const int64_t *ybar,
+                        int64_t *tasks);
 
 /* Human-readable text for a status, and the last CUDA error message seen by
  * this library in the calling thread ("" if none). */

@@ -90,9 +90,14 @@ _lib.sm_is_debug_build.argtypes = []
 _lib.sm_is_debug_build.restype = ctypes.c_int32
 _lib.sm_set_k1_variant.argtypes = [ctypes.c_int32]
 _lib.sm_set_k1_variant.restype = None
+_lib.sm_set_small_fuse.argtypes = [ctypes.c_int32]
+_lib.sm_set_small_fuse.restype = None
 _lib.sm_plan_from_ranks.argtypes = [ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p,
                                     ctypes.c_void_p]
 _lib.sm_plan_from_ranks.restype = ctypes.c_int
+_lib.sm_plan_tasks.argtypes = [ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p,
+                               ctypes.c_void_p, ctypes.c_void_p]
+_lib.sm_plan_tasks.restype = ctypes.c_int
 _lib.sm_sort_run_n.argtypes = [ctypes.c_int32, ctypes.c_int32, ctypes.c_int64]
 _lib.sm_sort_run_n.restype = ctypes.c_int64
 _lib.sm_status_string.argtypes = [ctypes.c_int]
@@ -244,6 +249,12 @@ def set_k1_variant(variant: int) -> None:
     _lib.sm_set_k1_variant(int(variant))
 
 
+def set_small_fuse(on: bool) -> None:
+    """Small plain merges in one launch (each K2 CTA ranks its own tasks) or
+    K1 then K2 (the default)."""
+    _lib.sm_set_small_fuse(int(bool(on)))
+
+
 def plan_from_ranks(n: int, m: int, p: int, xbar, ybar) -> list:
     """Test hook: the host's coarse Steps 3-4 on given cross ranks; the 2p
     tasks (a0, a1, b0, b1) ordered by output offset."""
@@ -252,6 +263,17 @@ def plan_from_ranks(n: int, m: int, p: int, xbar, ybar) -> list:
     out = (ctypes.c_int64 * (8 * p))()
     _check(_lib.sm_plan_from_ranks(n, m, p, xb, yb, out), "sm_plan_from_ranks")
     return [tuple(out[4 * k:4 * k + 4]) for k in range(2 * p)]
+
+
+def plan_tasks(n: int, m: int, pA: int, pB: int, xbar, ybar) -> list:
+    """Steps 3-4 on the host for given cross ranks x̄[0..pA], ȳ[0..pB]: the
+    pA + pB tasks (a0, a1, b0, b1) in task order (A-side task i, then B-side
+    task j), by the library's classification (sm_plan_tasks)."""
+    xb = (ctypes.c_int64 * (pA + 1))(*[int(v) for v in xbar])
+    yb = (ctypes.c_int64 * (pB + 1))(*[int(v) for v in ybar])
+    out = (ctypes.c_int64 * (4 * (pA + pB)))()
+    _check(_lib.sm_plan_tasks(n, m, pA, pB, xb, yb, out), "sm_plan_tasks")
+    return [tuple(out[4 * k:4 * k + 4]) for k in range(pA + pB)]
 
 
 def sort_run(key_type: str = "u32", has_vals: bool = True, n: Optional[int] = None) -> int:
@@ -459,6 +481,6 @@ def merge_plan(a_keys: torch.Tensor, b_keys: torch.Tensor, p_A: int, p_B: Option
     return xbar, ybar, tasks
 
 
-__all__ = ["merge_stable", "merge_stable_batched", "mergesort_stable", "ranks_stable", "merge_plan", "tile_capacity", "sort_run", "last_launch_count",
+__all__ = ["merge_stable", "merge_stable_batched", "mergesort_stable", "ranks_stable", "merge_plan", "plan_tasks", "tile_capacity", "sort_run", "last_launch_count",
            "StableMergeError", "KEY_TYPES", "LIB_PATH", "profile_enable", "profile_read", "PROF_K1", "PROF_K2",
            "PROF_K3"]

@@ -20,6 +20,7 @@ sm_status fail_inval(const char* what) {
 }
 
 int g_k1_variant = 0;
+int g_small_fuse = 0;
 uint32_t* g_dbg_cover = nullptr;
 unsigned long long* g_dbg_ts = nullptr;
 bool g_prof_on = false;
@@ -89,12 +90,29 @@ int32_t sm_is_debug_build(void) {
 
 void sm_set_k1_variant(int32_t variant) { sm::g_k1_variant = (variant >= 0 && variant <= 3) ? variant : 0; }
 
+void sm_set_small_fuse(int32_t on) { sm::g_small_fuse = on != 0; }
+
 sm_status sm_plan_from_ranks(int64_t n, int64_t m, int64_t p, const int64_t* xbar, const int64_t* ybar,
                              int64_t* tasks) {
     if (n < 0 || m < 0 || p < 1 || !xbar || !ybar || !tasks) return sm::fail_inval("sm_plan_from_ranks arguments");
     std::vector<int64_t> xb(xbar, xbar + p + 1), yb(ybar, ybar + p + 1);
     std::vector<sm::SubMerge> t;
     sm::plan_from_ranks(n, m, p, xb, yb, t);
+    for (size_t k = 0; k < t.size(); ++k) {
+        tasks[4 * k] = t[k].a0;
+        tasks[4 * k + 1] = t[k].a1;
+        tasks[4 * k + 2] = t[k].b0;
+        tasks[4 * k + 3] = t[k].b1;
+    }
+    return SM_OK;
+}
+
+sm_status sm_plan_tasks(int64_t n, int64_t m, int64_t pA, int64_t pB, const int64_t* xbar, const int64_t* ybar,
+                        int64_t* tasks) {
+    if (n < 0 || m < 0 || pA < 1 || pB < 1 || !xbar || !ybar || !tasks) return sm::fail_inval("sm_plan_tasks arguments");
+    std::vector<int64_t> xb(xbar, xbar + pA + 1), yb(ybar, ybar + pB + 1);
+    std::vector<sm::SubMerge> t;
+    sm::plan_tasks_host(n, m, pA, pB, xb, yb, t);
     for (size_t k = 0; k < t.size(); ++k) {
         tasks[4 * k] = t[k].a0;
         tasks[4 * k + 1] = t[k].a1;

@@ -19,16 +19,20 @@ namespace {   // internal linkage: every translation unit keeps its own kernels
 //               = floor((k - r*ceil(len/p)) / floor(len/p)) + r   otherwise
 //   block_of(len) = p  (reading R3: the virtual block after the last one)
 // ---------------------------------------------------------------------------
-struct Blocks {
-    int len, p, q, r;   // q = floor(len/p), r = len mod p
-    __device__ __forceinline__ Blocks(int len_, int p_) : len(len_), p(p_), q(len_ / p_), r(len_ % p_) {}
-    __device__ __forceinline__ int start(int i) const { return i < r ? i * (q + 1) : i * q + r; }
-    __device__ __forceinline__ int of(int k) const {
+// I: the index type -- int on the device (calls below 2^31), int64_t for the
+// host's coarse partition (merges of >= 2^31 elements, host pipelines).
+template <typename I>
+struct BlocksT {
+    I len, p, q, r;     // q = floor(len/p), r = len mod p
+    __host__ __device__ __forceinline__ BlocksT(I len_, I p_) : len(len_), p(p_), q(len_ / p_), r(len_ % p_) {}
+    __host__ __device__ __forceinline__ I start(I i) const { return i < r ? i * (q + 1) : i * q + r; }
+    __host__ __device__ __forceinline__ I of(I k) const {
         if (k >= len) return p;
-        const int big = r * (q + 1);
+        const I big = r * (q + 1);
         return k < big ? k / (q + 1) : (k - big) / q + r;   // q > 0 whenever k >= big and k < len
     }
 };
+using Blocks = BlocksT<int>;
 
 // ---------------------------------------------------------------------------
 // The key order "<=" of PAPER.md L63 ("ordered by a relation <="): natural
@@ -223,7 +227,7 @@ struct Geom {
     const int* rank_seg;  // mode 2: segment of every rank entry
     const int4* tdesc;    // modes 1, 2: tasks classified ahead by k_classify (or null)
     uint32_t* cover;      // SM_DEBUG builds: K2 counts every output element it stores here (or null)
-    int fuse;             // mode 0, few searches: K2 computes the cross ranks itself before a grid barrier
+    int fuse;             // mode 0, few tasks per CTA: K2 computes the ranks of its own tasks (no K1 launch)
     int* ctr;             // K2's task counter (dynamic assignment): zeroed by the kernel launched before K2
     unsigned long long* ts;   // SM_K2_TSTAMP builds: per-CTA event times of K2 (or null)
 };
@@ -313,28 +317,36 @@ __device__ __forceinline__ int locate(const Geom& g, int idx, bool ranks, int& l
 // ---------------------------------------------------------------------------
 enum { CASE_A = 0, CASE_B = 1, CASE_C = 2, CASE_D = 3, CASE_E = 4 };
 
-struct Task {
-    int side, kase, a0, a1, b0, b1;
+template <typename I>
+struct TaskT {
+    int side, kase;
+    I a0, a1, b0, b1;
 };
+using Task = TaskT<int>;
 
-__device__ __forceinline__ Task classify_a_side(int i, const Blocks& xa, const Blocks& yb,
-                                                const int* xbar, const int* ybar) {
-    Task t;
+// XR / YR: the rank arrays x̄, ȳ -- plain pointers, or (small merges in one
+// launch) a view of the entries a CTA computed itself (LocalView).
+// One implementation for the device (K2, k_classify, the small-merge
+// prologue) and the host (the coarse plans of sm_plan_tasks / the pipelines).
+template <typename I, typename XR, typename YR>
+__host__ __device__ __forceinline__ TaskT<I> classify_a_side(I i, const BlocksT<I>& xa, const BlocksT<I>& yb,
+                                                             const XR& xbar, const YR& ybar) {
+    TaskT<I> t;
     t.side = 0;
-    const int xi = xa.start(i), xi1 = xa.start(i + 1);
-    const int xb0 = xbar[i], xb1 = xbar[i + 1];
+    const I xi = xa.start(i), xi1 = xa.start(i + 1);
+    const I xb0 = xbar[i], xb1 = xbar[i + 1];
     if (xb0 == xb1) {                                         // (a) copy A[x_i, x_{i+1})
         t.kase = CASE_A; t.a0 = xi; t.a1 = xi1; t.b0 = t.b1 = xb0; return t;
     }
-    const int j = yb.of(xb0);
-    const int yj = yb.start(j);
+    const I j = yb.of(xb0);
+    const I yj = yb.start(j);
     if (xb0 == yj) {                                          // (e) copy A[x_i, ybar_j)
         t.kase = CASE_E; t.a0 = xi; t.a1 = ybar[j]; t.b0 = t.b1 = xb0; return t;
     }
     if (yb.of(xb1) == j) {                                    // (b) A block with B[xbar_i, xbar_{i+1})
         t.kase = CASE_B; t.a0 = xi; t.a1 = xi1; t.b0 = xb0; t.b1 = xb1; return t;
     }
-    const int yj1 = yb.start(j + 1);
+    const I yj1 = yb.start(j + 1);
     if (xb1 == yj1) {                                         // (d) A block with B[xbar_i, y_{j+1})
         t.kase = CASE_D; t.a0 = xi; t.a1 = xi1; t.b0 = xb0; t.b1 = yj1; return t;
     }
@@ -343,24 +355,25 @@ __device__ __forceinline__ Task classify_a_side(int i, const Blocks& xa, const B
     return t;
 }
 
-__device__ __forceinline__ Task classify_b_side(int j, const Blocks& xa, const Blocks& yb,
-                                                const int* xbar, const int* ybar) {
-    Task t;
+template <typename I, typename XR, typename YR>
+__host__ __device__ __forceinline__ TaskT<I> classify_b_side(I j, const BlocksT<I>& xa, const BlocksT<I>& yb,
+                                                             const XR& xbar, const YR& ybar) {
+    TaskT<I> t;
     t.side = 1;
-    const int yj = yb.start(j), yj1 = yb.start(j + 1);
-    const int yb0 = ybar[j], yb1 = ybar[j + 1];
+    const I yj = yb.start(j), yj1 = yb.start(j + 1);
+    const I yb0 = ybar[j], yb1 = ybar[j + 1];
     if (yb0 == yb1) {                                         // (a) copy B[y_j, y_{j+1})
         t.kase = CASE_A; t.b0 = yj; t.b1 = yj1; t.a0 = t.a1 = yb0; return t;
     }
-    const int i = xa.of(yb0);
-    const int xi = xa.start(i);
+    const I i = xa.of(yb0);
+    const I xi = xa.start(i);
     if (yb0 == xi) {                                          // (e) copy B[y_j, xbar_i)
         t.kase = CASE_E; t.b0 = yj; t.b1 = xbar[i]; t.a0 = t.a1 = yb0; return t;
     }
     if (xa.of(yb1) == i) {                                    // (b) B block with A[ybar_j, ybar_{j+1})
         t.kase = CASE_B; t.b0 = yj; t.b1 = yj1; t.a0 = yb0; t.a1 = yb1; return t;
     }
-    const int xi1 = xa.start(i + 1);
+    const I xi1 = xa.start(i + 1);
     if (yb1 == xi1) {                                         // (d) B block with A[ybar_j, x_{i+1})
         t.kase = CASE_D; t.b0 = yj; t.b1 = yj1; t.a0 = yb0; t.a1 = xi1; return t;
     }
@@ -469,6 +482,15 @@ __device__ __forceinline__ void bulk_s2g(void* dst_gmem, const void* src_smem, u
 }
 
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+
+// L2 prefetch of the 16-byte-aligned interior of p[0, len) (a hint: no data
+// lands in shared memory, nothing is written)
+template <typename T>
+__device__ __forceinline__ void prefetch_l2(const T* p, int len) {
+    const uintptr_t a = ((uintptr_t)p + 15) & ~(uintptr_t)15, e = ((uintptr_t)(p + len)) & ~(uintptr_t)15;
+    if (len > 0 && e > a)
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"((uint32_t)(e - a)) : "memory");
+}
 
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 

@@ -130,11 +130,8 @@ constexpr int64_t k3_run(int key_bytes, bool has_v) { return (int64_t)k3_nt(key_
 // them through L1/L2 on C2-C4, within 0.3%).  Few searches (< K1_FEW): a
 // whole warp each, ~log_33 dependent rounds.
 constexpr int K1_FEW = 4096;
-#ifndef SM_FUSE_K1
-#define SM_FUSE_K1 0             // 1: small plain merges fuse K1 into K2 (one cooperative launch; measured
-#endif                           //    slower on C1: 36 vs 23 us -- the grid barrier costs more than the launch)
-#ifndef SM_FUSE_ITEMS
-#define SM_FUSE_ITEMS 4096       // ... when p_A + p_B + 2 cross ranks at most
+#ifndef SM_SMALL_FUSE
+#define SM_SMALL_FUSE 1          // small plain merges: one launch, each CTA ranks its own tasks (k2_local_prologue)
 #endif
 #ifndef SM_K1_SMP_BYTES
 #define SM_K1_SMP_BYTES 8192     // the sample kernel's shared-memory sample per searched array
@@ -154,6 +151,8 @@ struct ProfRec {
 extern uint32_t* g_dbg_cover;  // SM_DEBUG builds: K2's coverage counters (sm_debug_cover), or null
 extern unsigned long long* g_dbg_ts;   // SM_K2_TSTAMP builds: K2's per-CTA event times (sm_debug_k2_timestamps)
 extern int g_k1_variant;        // test hook (sm_set_k1_variant): 0 auto, 1 warp per search, 2 sample, 3 thread per search
+extern int g_small_fuse;        // sm_set_small_fuse: small plain merges in one launch (default 0: measured slower
+                                //   with L2 flushed between calls, C1 24.1 vs 22.9 us; back to back 21.0 vs 21.9)
 extern bool g_prof_on;
 extern std::vector<ProfRec> g_prof_pool;
 extern size_t g_prof_used;
@@ -290,10 +289,10 @@ static sm_status launch_cross_ranks(const K* A, const K* B, const Geom& g, const
     return check_launch("k_cross_ranks");
 }
 
+// CTAs of K2 resident on the device at once (the persistent grid); the
+// function attributes are set once per device.
 template <typename K, bool HAS_V, typename Sh, typename PV = uint32_t>
-static sm_status launch_tasks(const K* A, const PV* vA, const K* B, const PV* vB, K* C, PV* vC,
-                              const Geom& g, const GeomCounts& gc, const int* xbar, const int* ybar, cudaStream_t st,
-                              bool pdl) {
+static long long k2_resident() {
     using Lay = K2Layout<K, HAS_V, Sh::NC, Sh::VT, Sh::STAGES, K2_MAXT, PV>;
     auto kern = k_tasks<K, HAS_V, Sh::NC, Sh::VT, Sh::STAGES, K2_MAXT, Sh::MINB, PV>;
     static int per_sm_d[SM_MAX_DEV], n_sm_d[SM_MAX_DEV];   // 0: not yet set up on that device
@@ -310,7 +309,17 @@ static sm_status launch_tasks(const K* A, const PV* vA, const K* B, const PV* vB
             per_sm_d[dev] = per_sm;
         }
     }
-    const long long grid = std::max(1ll, std::min<long long>(gc.tasks, (long long)per_sm * n_sm));
+    return (long long)per_sm * n_sm;
+}
+
+template <typename K, bool HAS_V, typename Sh, typename PV = uint32_t>
+static sm_status launch_tasks(const K* A, const PV* vA, const K* B, const PV* vB, K* C, PV* vC,
+                              const Geom& g, const GeomCounts& gc, const int* xbar, const int* ybar, cudaStream_t st,
+                              bool pdl) {
+    using Lay = K2Layout<K, HAS_V, Sh::NC, Sh::VT, Sh::STAGES, K2_MAXT, PV>;
+    auto kern = k_tasks<K, HAS_V, Sh::NC, Sh::VT, Sh::STAGES, K2_MAXT, Sh::MINB, PV>;
+    const long long resident = k2_resident<K, HAS_V, Sh, PV>();
+    const long long grid = std::max(1ll, std::min<long long>(gc.tasks, resident));
     Geom gk = g;
     gk.cover = g_dbg_cover;
     gk.ts = g_dbg_ts;
@@ -321,15 +330,9 @@ static sm_status launch_tasks(const K* A, const PV* vA, const K* B, const PV* vB
     cfg.dynamicSmemBytes = Lay::SMEM;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
-    if (g.fuse) {                                    // K2 computes the ranks itself: a grid barrier inside
-        attr[0].id = cudaLaunchAttributeCooperative;
-        attr[0].val.cooperative = 1;
-        cfg.numAttrs = 1;
-    } else {
-        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-        attr[0].val.programmaticStreamSerializationAllowed = 1;
-        cfg.numAttrs = (pdl && !g_prof_on) ? 1 : 0;
-    }
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.numAttrs = (pdl && !g_prof_on) ? 1 : 0;
     cfg.attrs = attr;
     prof_before(PROF_K2, st);
     cudaError_t e = cudaLaunchKernelEx(&cfg, kern, A, vA, B, vB, C, vC, gk, xbar, ybar);
@@ -348,9 +351,11 @@ static sm_status launch_merge(const K* A, const PV* vA, const K* B, const PV* vB
                               const GeomCounts* counts = nullptr, int4* tdesc = nullptr) {
     const GeomCounts gc = counts ? *counts : geom_counts(g0);
     Geom g = g0;
-    if (g0.sort == 0 && SM_FUSE_K1 && gc.items <= SM_FUSE_ITEMS && g_k1_variant == 0) {
-        // a small plain merge: one launch -- K2 computes its cross ranks itself
-        // (a warp per search) and a grid barrier is the single synchronisation
+    using Sh0 = typename K2Shape<K, HAS_V, PV>::type;
+    if (g0.sort == 0 && SM_SMALL_FUSE && g_small_fuse && g_k1_variant == 0 &&
+        gc.tasks <= (long long)K2L_MAXP * k2_resident<K, HAS_V, Sh0, PV>()) {
+        // a small plain merge: one launch -- each CTA of K2 computes the cross
+        // ranks its own tasks read (k2_local_prologue)
         g.fuse = 1;
         return launch_tasks<K, HAS_V, typename K2Shape<K, HAS_V, PV>::type, PV>(A, vA, B, vB, C, vC, g, gc, xbar, ybar,
                                                                               st, pdl);
@@ -587,14 +592,7 @@ static int64_t host_pipeline_blocks(int64_t n, int64_t m, bool has_v) {
 }
 
 static inline int64_t hblock_start(int64_t len, int64_t p, int64_t i) {    // x_i, L168-182; x_p = len
-    const int64_t q = len / p, r = len % p;
-    return i < r ? i * (q + 1) : i * q + r;
-}
-
-static inline int64_t hblock_of(int64_t len, int64_t p, int64_t k) {       // L294-300; block_of(len) = p (R3)
-    if (k >= len) return p;
-    const int64_t q = len / p, r = len % p, big = r * (q + 1);
-    return k < big ? k / (q + 1) : (k - big) / q + r;
+    return BlocksT<int64_t>(len, p).start(i);
 }
 
 template <typename K>
@@ -611,40 +609,27 @@ static void host_plan(const K* A, int64_t n, const K* B, int64_t m, int64_t p, s
     plan_from_ranks(n, m, p, xb, yb, tasks);
 }
 
-// Steps 3-4 at coarse granularity from the cross ranks xb[0..p], yb[0..p].
+// Steps 3-4 on the host: the p_A + p_B tasks in task
+// order (A-side task i, then B-side task j) from the cross ranks
+// xb[0..p_A], yb[0..p_B], by the classification the device runs
+// (classify_a_side / classify_b_side, 64-bit indices).
+static void plan_tasks_host(int64_t n, int64_t m, int64_t pA, int64_t pB, const std::vector<int64_t>& xb,
+                            const std::vector<int64_t>& yb, std::vector<SubMerge>& tasks) {
+    const BlocksT<int64_t> xa(n, pA), ybl(m, pB);
+    for (int64_t i = 0; i < pA; ++i) {
+        const TaskT<int64_t> t = classify_a_side<int64_t>(i, xa, ybl, xb.data(), yb.data());
+        tasks.push_back({t.a0, t.a1, t.b0, t.b1});
+    }
+    for (int64_t j = 0; j < pB; ++j) {
+        const TaskT<int64_t> t = classify_b_side<int64_t>(j, xa, ybl, xb.data(), yb.data());
+        tasks.push_back({t.a0, t.a1, t.b0, t.b1});
+    }
+}
+
+// Steps 3-4 at coarse granularity (p blocks per array), ordered by output offset.
 static void plan_from_ranks(int64_t n, int64_t m, int64_t p, const std::vector<int64_t>& xb,
                             const std::vector<int64_t>& yb, std::vector<SubMerge>& tasks) {
-    std::vector<int64_t> x(p + 1), y(p + 1);
-    for (int64_t i = 0; i <= p; ++i) {
-        x[i] = hblock_start(n, p, i);
-        y[i] = hblock_start(m, p, i);
-    }
-    for (int64_t i = 0; i < p; ++i) {      // Step 3, cases tested (a), (e), (b), (d), (c) (R8, R1)
-        SubMerge t;
-        if (xb[i] == xb[i + 1]) {
-            t = {x[i], x[i + 1], xb[i], xb[i]};
-        } else {
-            const int64_t j = hblock_of(m, p, xb[i]);
-            if (xb[i] == y[j]) t = {x[i], yb[j], xb[i], xb[i]};
-            else if (hblock_of(m, p, xb[i + 1]) == j) t = {x[i], x[i + 1], xb[i], xb[i + 1]};
-            else if (xb[i + 1] == y[j + 1]) t = {x[i], x[i + 1], xb[i], y[j + 1]};
-            else t = {x[i], yb[j + 1], xb[i], y[j + 1]};
-        }
-        tasks.push_back(t);
-    }
-    for (int64_t j = 0; j < p; ++j) {      // Step 4: the mirror (ties still to A, R2)
-        SubMerge t;
-        if (yb[j] == yb[j + 1]) {
-            t = {yb[j], yb[j], y[j], y[j + 1]};
-        } else {
-            const int64_t i = hblock_of(n, p, yb[j]);
-            if (yb[j] == x[i]) t = {yb[j], yb[j], y[j], xb[i]};
-            else if (hblock_of(n, p, yb[j + 1]) == i) t = {yb[j], yb[j + 1], y[j], y[j + 1]};
-            else if (yb[j + 1] == x[i + 1]) t = {yb[j], x[i + 1], y[j], y[j + 1]};
-            else t = {yb[j], x[i + 1], y[j], xb[i + 1]};
-        }
-        tasks.push_back(t);
-    }
+    plan_tasks_host(n, m, p, p, xb, yb, tasks);
     for (SubMerge& t : tasks) {            // unsorted inputs (a precondition violation): never negative
         t.a1 = std::max(t.a0, std::min(t.a1, n));
         t.b1 = std::max(t.b0, std::min(t.b1, m));

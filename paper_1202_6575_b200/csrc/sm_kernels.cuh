@@ -20,10 +20,7 @@
 // All in-kernel indices are 32-bit (larger calls are cut into sub-problems
 // below 2^31 on the host side: stablemerge.cu, merge_large_device).
 #pragma once
-#include <cooperative_groups.h>
 #include "sm_device.cuh"
-
-namespace cg = cooperative_groups;
 
 namespace sm {
 namespace {   // internal linkage: every translation unit keeps its own kernels
@@ -280,6 +277,128 @@ __device__ __forceinline__ Task decode_task(const Geom& g, int task, const int* 
     return t < sg.pA ? classify_a_side(t, xa, yb, sg.xs, sg.ys) : classify_b_side(t - sg.pA, xa, yb, sg.xs, sg.ys);
 }
 
+// ---- small plain merges in one launch (g.fuse) ----------------------------
+// When every CTA has at most K2L_MAXP tasks (C1: 2^20 + 2^20 elements,
+// 1094 tasks on 296 CTAs), K1 is a latency-bound launch of its own (~10 of
+// the call's 23 µs).  Then no K1 runs: CTA b takes the consecutive positions
+// [bP, (b+1)P) of K2's order and its warps compute the cross ranks its
+// tasks read (Steps 1-2: x̄ over the A-side tasks' block
+// starts and the next one, ȳ likewise, plus a margin), a warp per search;
+// then each task is classified (Steps 3-4); the one rank of the other side
+// a case (c) or (e) task may still need (ȳ_j / x̄_i)
+// comes from a second round of searches.  Every rank a task reads is final
+// before the task is classified -- the single synchronisation of L373-375,
+// per CTA -- and no CTA depends on another.
+constexpr int K2L_MAXP = 8;                 // tasks per CTA at most in this mode
+#ifndef SM_SMALL_PREFETCH
+#define SM_SMALL_PREFETCH 1                 // own blocks prefetched to L2 while the ranks are searched
+#endif
+constexpr int K2L_MAXR = K2L_MAXP + 4;      // local x̄ / ȳ entries
+struct K2Local {
+    int k0, k1;                             // the CTA's positions
+    int ia0, nx, jb0, ny;                   // x̄ over [ia0, ia0 + nx), ȳ over [jb0, jb0 + ny)
+    int xl[K2L_MAXR], yl[K2L_MAXR];
+    int miss_side[K2L_MAXP], miss_idx[K2L_MAXP], miss_val[K2L_MAXP];
+    int4 desc[K2L_MAXP];                    // the tasks, classified: A start, B start, C start, la << 16 | lb
+};
+// A rank array as classification reads it: the local entries, the sentinel
+// and empty block starts (the other length, R4), the second round's extras;
+// an entry not there is recorded in *miss (first one only) and reads as 0.
+struct LocalView {
+    const K2Local* L;
+    int side;                               // 0: x̄ (A's block starts in B), 1: ȳ
+    int p, own_len, oth_len;
+    int* miss;
+    __device__ __forceinline__ int operator[](int i) const {
+        if (i >= p || i >= own_len) return oth_len;
+        const int lo = side ? L->jb0 : L->ia0, cnt = side ? L->ny : L->nx;
+        if (i >= lo && i < lo + cnt) return side ? L->yl[i - lo] : L->xl[i - lo];
+        for (int k = 0; k < L->k1 - L->k0; ++k)
+            if (L->miss_side[k] == side && L->miss_idx[k] == i) return L->miss_val[k];
+        if (miss && *miss < 0) *miss = i;
+        return 0;
+    }
+};
+template <typename K>
+__device__ __forceinline__ int warp_rank(const K* A, const K* B, const Geom& g, const Blocks& xa, const Blocks& yb,
+                                         int side, int i) {
+    // x̄_i = rank_low(A[x_i], B) (side 0) or ȳ_i = rank_high(B[y_i], A) (side 1), a whole warp per search
+    const int p = side ? g.pB : g.pA, own_len = side ? g.m : g.n, oth_len = side ? g.n : g.m;
+    const bool search = i < p && i < own_len;
+    K x = K(0);
+    if (search) x = ldg_key(side ? B + yb.start(i) : A + xa.start(i));
+    const int r = group_rank<K, 32>(side ? A : B, oth_len, x, side == 1, search);
+    return search ? r : oth_len;
+}
+template <typename K, int NV>
+__device__ void k2_local_prologue(const K* A, const K* B, const Geom& g, K2Local* L) {
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, NW = (int)(blockDim.x >> 5);
+    const int ntasks = g.pA + g.pB;
+    const int P = (ntasks + (int)gridDim.x - 1) / (int)gridDim.x;
+    const Blocks xa(g.n, g.pA), yb(g.m, g.pB);
+    if (tid == 0) {
+        const int k0 = min(ntasks, (int)blockIdx.x * P), k1 = min(ntasks, k0 + P);
+        int a_lo = INT_MAX, a_hi = -1, b_lo = INT_MAX, b_hi = -1;
+        for (int k = k0; k < k1; ++k) {
+            const int t = task_at(k, g.pA, g.pB);
+            if (t < g.pA) { a_lo = min(a_lo, t); a_hi = max(a_hi, t); }
+            else { b_lo = min(b_lo, t - g.pA); b_hi = max(b_hi, t - g.pA); }
+        }
+        // own tasks' entries i, i + 1 and a margin of one before, two after
+        // (balanced inputs: the other side's entries case (c) / (e) reads)
+        if (a_hi < 0) { a_lo = b_lo; a_hi = b_hi; }
+        if (b_hi < 0) { b_lo = a_lo; b_hi = a_hi; }
+        L->k0 = k0;
+        L->k1 = k1;
+        L->ia0 = max(0, a_lo - 1);
+        L->nx = min(g.pA - 1, a_hi + 2) - L->ia0 + 1;
+        L->jb0 = max(0, b_lo - 1);
+        L->ny = min(g.pB - 1, b_hi + 2) - L->jb0 + 1;
+        if (k0 >= k1) L->nx = L->ny = 0;
+    }
+    __syncthreads();
+    const int nx = max(0, L->nx), ny = max(0, L->ny), np = L->k1 - L->k0;
+    for (int e = w; e < nx + ny; e += NW) {                 // round 1: a warp per entry
+        const int side = e < nx ? 0 : 1;
+        const int i = side ? L->jb0 + e - nx : L->ia0 + e;
+        const int r = warp_rank<K>(A, B, g, xa, yb, side, i);
+        if (lane == 0) (side ? L->yl : L->xl)[i - (side ? L->jb0 : L->ia0)] = r;
+    }
+    if (tid < K2L_MAXP) L->miss_side[tid] = -1;
+    __syncthreads();
+    int miss = -1, side = 0;
+    if (tid < np) {                                          // classify; note the entry it lacks, if any
+        const int t0 = task_at(L->k0 + tid, g.pA, g.pB);
+        side = t0 < g.pA ? 1 : 0;                            // an A-side task reads ȳ, a B-side task x̄
+        const LocalView xv{L, 0, g.pA, g.n, g.m, side == 0 ? &miss : nullptr};
+        const LocalView yv{L, 1, g.pB, g.m, g.n, side == 1 ? &miss : nullptr};
+        if (t0 < g.pA) classify_a_side(t0, xa, yb, xv, yv);
+        else classify_b_side(t0 - g.pA, xa, yb, xv, yv);
+        if (miss >= 0) {
+            L->miss_side[tid] = side;
+            L->miss_idx[tid] = miss;
+        }
+    }
+    __syncthreads();
+    for (int k = w; k < np; k += NW) {                      // round 2: the missing entries
+        if (L->miss_side[k] < 0) continue;
+        const int r = warp_rank<K>(A, B, g, xa, yb, L->miss_side[k], L->miss_idx[k]);
+        if (lane == 0) L->miss_val[k] = r;
+    }
+    __syncthreads();
+    if (tid < np) {
+        const int t0 = task_at(L->k0 + tid, g.pA, g.pB);
+        const LocalView xv{L, 0, g.pA, g.n, g.m, nullptr};
+        const LocalView yv{L, 1, g.pB, g.m, g.n, nullptr};
+        const Task t = t0 < g.pA ? classify_a_side(t0, xa, yb, xv, yv) : classify_b_side(t0 - g.pA, xa, yb, xv, yv);
+        // clamped as in the producer (unsorted inputs, a precondition violation)
+        const int la = max(0, min(t.a1 - t.a0, NV));
+        const int lb = max(0, min(t.b1 - t.b0, NV - la));
+        L->desc[tid] = make_int4(t.a0, t.b0, t.a0 + t.b0, (la << 16) | lb);
+    }
+    __syncthreads();
+}
+
 // ----------------------------------------------------------------- K2
 // SM_K2_TSTAMP builds (experiments, scripts/k2_timeline.py): K2 records
 // per-CTA event times (%globaltimer, ns) in g.ts[8 * CTA + slot]: 0 entry,
@@ -331,7 +450,8 @@ struct K2Layout {
     static constexpr int OFF_DESC = STAGES * STAGE_BYTES;
     static constexpr int OFF_PST = OFF_DESC + STAGES * MAXT * (int)sizeof(TaskDesc);
     static constexpr int OFF_BAR = ((OFF_PST + STAGES * (MAXT + 2) * 4) + 15) & ~15;
-    static constexpr int SMEM = OFF_BAR + 3 * STAGES * 8;   // full, empty, written
+    static constexpr int OFF_LOC = (OFF_BAR + 3 * STAGES * 8 + 15) & ~15;   // full, empty, written; then
+    static constexpr int SMEM = OFF_LOC + (int)sizeof(K2Local);              //   the small-merge ranks (g.fuse)
     static constexpr int THREADS = NC + 64;                 // producer + storer + consumers
 };
 
@@ -440,12 +560,17 @@ __device__ __forceinline__ void k2_producer(const K* __restrict__ A, const PV* _
     int seen = 0;                                   // end of this CTA's last reservation (progress estimate)
     bool more = ntasks > 0;
     // few tasks per CTA (C1): static round-robin -- one refill takes them all
-    int* const ctr = (SM_K2_DYN && ntasks > SM_K2_DYN_MIN * G) ? g.ctr : nullptr;
+    int* const ctr = (SM_K2_DYN && !g.fuse && ntasks > SM_K2_DYN_MIN * G) ? g.ctr : nullptr;
     const int refill =
         g.tdesc ? SM_REFILL_TDESC : (g.sort == 0 && KB + (HAS_V ? (int)sizeof(PV) : 0) > 8) ? 32 : 8;
     constexpr int CH = KB + (HAS_V ? (int)sizeof(PV) : 0) > 8 ? SM_K2_CHUNK_WIDE : SM_K2_CHUNK;
     int resv = 0, resv_n = 0;                       // (lane 0) positions reserved for the next refill
     int next = blockIdx.x;                          // (no counter: static round-robin, CTA b takes b, b+G, ...)
+    const K2Local* loc = (const K2Local*)(smem + Lay::OFF_LOC);
+    if (g.fuse) {                                   // small merge: this CTA's positions, classified (prologue)
+        next = loc->k0;
+        more = loc->k0 < loc->k1;
+    }
     for (int it = 0;; ++it) {
         // dynamic: refill while the window has room for a chunk; near the end
         // (fewer than SM_K2_TAILWIN tasks per CTA left) keep the window short
@@ -471,6 +596,11 @@ __device__ __forceinline__ void k2_producer(const K* __restrict__ A, const PV* _
                 }
                 stride = 1;
                 base -= cnt;                        // lane l in [cnt, cnt + take) takes position base + l
+            } else if (g.fuse) {
+                base = next;
+                stride = 1;
+                take = loc->k1 - loc->k0;                   // <= K2L_MAXP: one refill
+                more = false;
             } else {
                 base = next;
                 stride = G;
@@ -480,8 +610,8 @@ __device__ __forceinline__ void k2_producer(const K* __restrict__ A, const PV* _
             const int my = base + (lane - (dyn ? 0 : cnt)) * stride;
             const bool fill = lane >= cnt && lane < cnt + take && my < ntasks;
             if (fill) {
-                if (g.tdesc) {                      // classified ahead (k_classify): one load
-                    const int4 q = __ldg(g.tdesc + my);
+                if (g.tdesc || g.fuse) {            // classified ahead (k_classify / the prologue): one load
+                    const int4 q = g.fuse ? loc->desc[my - loc->k0] : __ldg(g.tdesc + my);
                     ag = q.x;
                     bg = q.y;
                     off = q.z;
@@ -797,26 +927,24 @@ __global__ void __launch_bounds__(K2Layout<K, HAS_V, NC, VT, STAGES, MAXT, PV>::
     pdl_wait();   // the single synchronisation (L373-375): all ranks visible
     if (threadIdx.x == 0) K2_TS(0);
 
-    if (g.fuse) {
-        // small plain merges (few block starts): no separate K1 launch -- every
-        // warp of the grid computes cross ranks (Steps 1-2, a warp per search,
-        // PAPER.md L304-309), then the grid barrier is the single
-        // synchronisation (L373-375); the kernel is launched cooperatively
-        const int warp = threadIdx.x >> 5, wpc = (int)(blockDim.x >> 5);
-        const int items = g.pA + 1 + g.pB + 1;
-        for (int it = blockIdx.x * wpc + warp; it < items; it += gridDim.x * wpc) {
-            const bool sideA = it <= g.pA;
-            const int idx = sideA ? it : it - g.pA - 1;
-            const int plen = sideA ? g.pA : g.pB, own_len = sideA ? g.n : g.m, oth_len = sideA ? g.m : g.n;
-            const bool search = idx < plen && idx < own_len;
-            K x = K(0);
-            if (search) x = ldg_key((sideA ? A : B) + Blocks(own_len, plen).start(idx));
-            const int r = group_rank<K, 32>(sideA ? B : A, oth_len, x, !sideA, search);
-            if ((threadIdx.x & 31) == 0) const_cast<int*>(sideA ? xbar : ybar)[idx] = search ? r : oth_len;
+    if (g.fuse) {                                    // small plain merge
+#if SM_SMALL_PREFETCH
+        // each task's own block (its A range starts at x_i, a B-side task's
+        // B range at y_j) to L2 while the ranks are searched
+        const int ntasks = g.pA + g.pB, P = (ntasks + (int)gridDim.x - 1) / (int)gridDim.x;
+        const int k = (int)blockIdx.x * P + (int)threadIdx.x;
+        if ((int)threadIdx.x < P && k < ntasks) {
+            const int t = task_at(k, g.pA, g.pB);
+            const bool sa = t < g.pA;
+            const Blocks bl = sa ? Blocks(g.n, g.pA) : Blocks(g.m, g.pB);
+            const int i = sa ? t : t - g.pA;
+            const int s0 = min(bl.start(i), bl.len), s1 = i + 1 < bl.p ? bl.start(i + 1) : bl.len;
+            prefetch_l2((sa ? A : B) + s0, s1 - s0);
+            if (HAS_V) prefetch_l2((sa ? vA : vB) + s0, s1 - s0);
         }
-        cg::this_grid().sync();
+#endif
+        k2_local_prologue<K, NV>(A, B, g, (K2Local*)(smem + Lay::OFF_LOC));
     }
-
     if (threadIdx.x < 32) {
         k2_producer<K, HAS_V, VT, STAGES, MAXT, (sizeof(K) == 4 && !HAS_V), Lay, PV>(A, vA, B, vB, C, vC, g, xbar, ybar,
                                                                                smem, desc, pst, full, empty);

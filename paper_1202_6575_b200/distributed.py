@@ -92,39 +92,12 @@ def block_of(k: int, length: int, p: int) -> int:
 def plan_tasks(n: int, m: int, p: int, xbar: Sequence[int], ybar: Sequence[int], pB: Optional[int] = None):
     """Steps 3-4 (L310-340; readings R1, R8): the p_A + p_B tasks as
     (owner, a0, a1, b0, b1), A-side task q then B-side task q for every q
-    (p_A = p, p_B = pB or p: reading R7)."""
+    (p_A = p, p_B = pB or p: reading R7) -- the library's classification
+    (sm_plan_tasks, the same code as the device's K2), on the host."""
+    from . import plan_tasks as _plan
     pA, pB = p, (p if pB is None else pB)
-    x, y = block_starts(n, pA), block_starts(m, pB)
-    tasks = []
-    for i in range(pA):
-        if xbar[i] == xbar[i + 1]:
-            t = (x[i], x[i + 1], xbar[i], xbar[i])
-        else:
-            j = block_of(xbar[i], m, pB)
-            if xbar[i] == y[j]:
-                t = (x[i], ybar[j], xbar[i], xbar[i])
-            elif block_of(xbar[i + 1], m, pB) == j:
-                t = (x[i], x[i + 1], xbar[i], xbar[i + 1])
-            elif xbar[i + 1] == y[j + 1]:
-                t = (x[i], x[i + 1], xbar[i], y[j + 1])
-            else:
-                t = (x[i], ybar[j + 1], xbar[i], y[j + 1])
-        tasks.append((i,) + t)
-    for j in range(pB):
-        if ybar[j] == ybar[j + 1]:
-            t = (ybar[j], ybar[j], y[j], y[j + 1])
-        else:
-            i = block_of(ybar[j], n, pA)
-            if ybar[j] == x[i]:
-                t = (ybar[j], ybar[j], y[j], xbar[i])
-            elif block_of(ybar[j + 1], n, pA) == i:
-                t = (ybar[j], ybar[j + 1], y[j], y[j + 1])
-            elif ybar[j + 1] == x[i + 1]:
-                t = (ybar[j], x[i + 1], y[j], y[j + 1])
-            else:
-                t = (ybar[j], x[i + 1], y[j], xbar[i + 1])
-        tasks.append((j,) + t)
-    return tasks
+    rows = _plan(n, m, pA, pB, xbar, ybar)
+    return [(i,) + rows[i] for i in range(pA)] + [(j,) + rows[pA + j] for j in range(pB)]
 
 
 def _holder(lo: int, hi: int, length: int, p: int) -> int:

@@ -37,8 +37,8 @@ def test_header_declares_entry_points():
             assert f"{f}_desc_{kt}" in names          # descending order
         for f in ("merge_stable_wide", "merge_stable_batched_wide", "mergesort_stable_wide"):
             assert f"{f}_{kt}" in names and f"{f}_desc_{kt}" in names   # wide payloads (row 2)
-    assert len(names) == 152          # + sm_sort_run_n, sm_set_k1_variant, sm_plan_from_ranks, sm_debug_cover,
-    #                                     sm_is_debug_build
+    assert len(names) == 154          # + sm_sort_run_n, sm_set_k1_variant, sm_plan_from_ranks, sm_debug_cover,
+    #                                     sm_is_debug_build, sm_set_small_fuse, sm_plan_tasks
 
 
 def test_library_exports_every_declared_symbol(sm):
@@ -147,3 +147,27 @@ def test_host_plan_from_ranks_matches_oracle_plan(sm):
         assert sorted(got) == want, (n, m, p, A, B)
         offs = [a0 + b0 for a0, a1, b0, b1 in got]
         assert offs == sorted(offs)
+
+
+def test_host_plan_tasks_matches_oracle_plan(sm):
+    """sm_plan_tasks -- the classification the device's K2 runs, compiled for
+    the host with 64-bit indices (the sharded merge's Steps 3-4) -- equals
+    oracle/plan.py task for task and in task order (A side, then B side),
+    with p_A != p_B (reading R7), on Fig. 1 and random
+    inputs with heavy ties and empty blocks."""
+    import json
+    import os
+    import numpy as np
+    from oracle import plan as P
+    fig = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "fig1.json")))
+    cases = [(fig["A"], fig["B"], 5, 5)]
+    rng = np.random.default_rng(43)
+    for _ in range(400):
+        n, m = int(rng.integers(0, 70)), int(rng.integers(0, 70))
+        K = int(rng.integers(1, 9))
+        cases.append((sorted(int(v) for v in rng.integers(0, K, n)), sorted(int(v) for v in rng.integers(0, K, m)),
+                      int(rng.integers(1, 10)), int(rng.integers(1, 10))))
+    for A, B, pA, pB in cases:
+        _, _, xbar, ybar, tasks = P.build_plan(A, B, pA, pB)
+        got = sm.plan_tasks(len(A), len(B), pA, pB, xbar, ybar)
+        assert got == [(t.a0, t.a1, t.b0, t.b1) for t in tasks], (A, B, pA, pB)

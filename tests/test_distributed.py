@@ -107,7 +107,7 @@ def test_sharded_merge_gloo(world):
 
 
 def test_plan_tasks_tile_the_output():
-    """The distributed plan (its own implementation of Steps 3-4) tiles
+    """The distributed plan (the library's host Steps 3-4, sm_plan_tasks) tiles
     [0, n+m) and partitions A and B, checked against the ranks of the oracle."""
     from paper_1202_6575_b200 import distributed as D
     for n, m, p in ((18, 15, 5), (1000, 37, 4), (7, 2000, 3), (0, 5, 2), (3, 1, 8)):

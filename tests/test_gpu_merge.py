@@ -107,18 +107,64 @@ def test_cross_ranks_full_size_c2_sample_kernel():
     assert int(xbar[-1]) == b.size and int(ybar[-1]) == a.size
 
 
-def test_one_cross_rank_launch_then_one_task_launch():
+def _one_launch(sm, n, m, kt="u32", payload=True):
+    """The library's rule for a one-launch small merge: at most 8 tasks per
+    resident K2 CTA (two per SM for <= 8-byte elements)."""
+    T = sm.tile_capacity(kt, payload) // 2
+    tasks = max(1, -(-n // T)) + max(1, -(-m // T))
+    return tasks <= 8 * 2 * torch.cuda.get_device_properties(0).multi_processor_count
+
+
+@pytest.mark.parametrize("small_fuse", [True, False])
+def test_launches_per_device_merge(small_fuse):
     """A device merge has exactly one synchronisation between Steps 1-2 and
     the tasks (SURVEY §2.2 acceptance 6): two launches, K1
-    then K2 behind it (PDL griddepcontrol.wait), and the oracle's merge."""
+    then K2 behind it (PDL griddepcontrol.wait); or, for a small merge, ONE
+    launch in which every CTA computes the ranks its own tasks read before
+    classifying them.  Either way, the oracle's merge."""
     sm = lib()
-    for n, m in ((1 << 20, 1 << 20), (5000, 3), (1 << 23, 1 << 16), (3 << 20, 3 << 20)):
-        inp = synth.merge_input(n, m, "u32", "full", seed=n, payload=True)
-        d = inp.to("cuda")
-        ck, cv = sm.merge_stable(d.a_keys, d.a_vals, d.b_keys, d.b_vals, key_type="u32")
-        assert sm.last_launch_count() == 2, (n, m)
-        torch.cuda.synchronize()
-        assert_bit_exact(ck.cpu(), cv.cpu(), *oracle_merge(inp), "u32")
+    try:
+        sm.set_small_fuse(small_fuse)
+        for n, m in ((1 << 20, 1 << 20), (5000, 3), (1 << 23, 1 << 16), (3 << 20, 3 << 20)):
+            inp = synth.merge_input(n, m, "u32", "full", seed=n, payload=True)
+            d = inp.to("cuda")
+            ck, cv = sm.merge_stable(d.a_keys, d.a_vals, d.b_keys, d.b_vals, key_type="u32")
+            assert sm.last_launch_count() == (1 if small_fuse and _one_launch(sm, n, m) else 2), (n, m)
+            torch.cuda.synchronize()
+            assert_bit_exact(ck.cpu(), cv.cpu(), *oracle_merge(inp), "u32")
+    finally:
+        sm.set_small_fuse(False)
+
+
+@pytest.mark.parametrize("small_fuse", [True, False])
+@pytest.mark.parametrize("kt,dist,payload", [("i32", "full", False), ("u32", "bounded:3", True),
+                                             ("u32", "bounded:65536", True), ("i64", "bounded:1000", True),
+                                             ("u64", "mostly:7:9/10", True), ("f32", "special", True),
+                                             ("f64", "bounded:50", False), ("u128", "tuple:5", True)])
+@pytest.mark.parametrize("nm", [(1, 0), (0, 7), (5, 3), (1921, 3839), (70001, 12345), (3, 200003),
+                                (1_000_003, 999_999), (2_000_000, 4099), (17, 2_000_000), (1 << 20, 1 << 20)])
+def test_small_merge_one_launch_parity(small_fuse, kt, dist, payload, nm):
+    """One-launch small merges (each CTA ranks its own tasks: balanced,
+    unbalanced -- where the other side's entries come from the second round
+    of searches -- and degenerate sizes) and the two-launch path give the
+    oracle's merge, bit for bit."""
+    sm = lib()
+    n, m = nm
+    inp = synth.merge_input(n, m, kt, dist, seed=n + 3 * m + small_fuse, payload=payload)
+    try:
+        sm.set_small_fuse(small_fuse)
+        got = gpu_merge(sm, inp)
+        got_desc = None
+        if kt in ("u32", "i64"):
+            dinp = synth.merge_input(n, m, kt, dist, seed=n + 5 * m, payload=payload, descending=True)
+            got_desc = (gpu_merge(sm, dinp, descending=True), dinp)
+    finally:
+        sm.set_small_fuse(False)
+    assert_bit_exact(*got, *oracle_merge(inp), kt)
+    if got_desc is not None:
+        (gk, gv), dinp = got_desc
+        want = oracle.merge(dinp.a_keys, dinp.a_vals, dinp.b_keys, dinp.b_vals, kt, descending=True)
+        assert_bit_exact(gk, gv, *want, kt)
 
 
 def test_plan_parity_exhaustive_small():
