@@ -1038,7 +1038,8 @@ static sm_status launch_block_sort_hbm(K* keys, uint32_t* vals, K* aux, uint32_t
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Lay::SMEM);
             if (dev < SM_MAX_DEV) attr[dev] = true;
         }
-        kern<<<(unsigned)ceil_div(N, L0), NT, Lay::SMEM, st>>>(keys, vals, aux, vaux, aux2, vaux2, N, L0, final_buf);
+        kern<<<(unsigned)ceil_div(N, L0), NT, Lay::SMEM, st>>>(keys, vals, aux, vaux, aux2, vaux2, N, L0, final_buf,
+                                                               g_dbg_ts);
         return SM_OK;
     }
 }

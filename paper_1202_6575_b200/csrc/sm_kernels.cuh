@@ -1907,7 +1907,7 @@ template <typename K, bool HAS_V, int NT, int TILE>
 #endif
 __global__ void __launch_bounds__(NT, SM_K3H_MINB) k_block_sort_hbm(K* buf0, uint32_t* vbuf0, K* buf1, uint32_t* vbuf1,
                                                            K* buf2, uint32_t* vbuf2, int64_t N, int64_t L0,
-                                                           int final_buf) {
+                                                           int final_buf, unsigned long long* ts) {
     using Lay = K3HLayout<K, HAS_V, NT, TILE>;
     using U = typename Lay::U;
     constexpr int NW = Lay::NW, IPT = Lay::IPT, NPOS = Lay::NPOS;
@@ -1950,6 +1950,21 @@ __global__ void __launch_bounds__(NT, SM_K3H_MINB) k_block_sort_hbm(K* buf0, uin
         ph ^= 1u << (t & 1);
     };
 
+    // SM_K2_TSTAMP builds: per-CTA event times at ts[8 * (4096 + CTA) + slot]:
+    // 0 entry, 1 pre-pass done, 2 + i pass i done
+#ifdef SM_K2_TSTAMP
+    auto k3_ts = [&](int slot) {
+        if (ts && tid == 0) {
+            unsigned long long t_;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
+            ts[8 * (4096 + blockIdx.x) + slot] = t_;
+        }
+    };
+#else
+    auto k3_ts = [](int) {};
+    (void)ts;
+#endif
+    k3_ts(0);
     // ---- pre-pass: the varying bytes and their histograms
     const U first = KeyOrd<K>::to(ld_cg(buf0 + base));
     U diff = 0;
@@ -1997,6 +2012,7 @@ __global__ void __launch_bounds__(NT, SM_K3H_MINB) k_block_sort_hbm(K* buf0, uin
     diff = 0;
 #pragma unroll
     for (int i = 0; i < NW; ++i) diff |= red[i];
+    k3_ts(1);
 
     // ---- the pass plan: one pass per varying byte, low to high.  Three
     // buffers: pass i writes the buffer that is neither its source nor the
@@ -2036,6 +2052,7 @@ __global__ void __launch_bounds__(NT, SM_K3H_MINB) k_block_sort_hbm(K* buf0, uin
         asm volatile("fence.proxy.async.global;" ::: "memory");
         __syncthreads();
         src = dst;
+        if (ps < 6) k3_ts(2 + ps);
     }
 }
 

@@ -33,7 +33,7 @@ def main():
     dev = torch.device("cuda", 0)
     fn = sm._lib.sm_debug_k2_timestamps
     fn.argtypes = [ctypes.c_void_p]
-    ts = torch.zeros(8 * 4096, dtype=torch.int64, device=dev)
+    ts = torch.zeros(16 * 4096, dtype=torch.int64, device=dev)
     for cfg in [int(x) for x in a.configs.split(",")]:
         wl = bench.make_workload(cfg, bench.rank_seed(cfg, 0), dev, sm)
         for _ in range(5):
@@ -46,7 +46,16 @@ def main():
         wl.call()           # the previous call's K2 is still draining when this one's starts (PDL)
         torch.cuda.synchronize()
         fn(None)
-        t = ts.view(-1, 8).cpu().numpy().astype(np.float64)
+        allt = ts.view(-1, 8).cpu().numpy().astype(np.float64)
+        k3 = allt[4096:]
+        k3 = k3[k3[:, 0] > 0]
+        if k3.size:                                  # the sort's phase 1 (K3H): entry, pre-pass, passes
+            r3 = (k3 - k3[:, 0].min()) / 1e3
+            print(json.dumps({"tag": a.tag, "cfg": cfg, "k3h_ctas": int(k3.shape[0]),
+                              **{f"k3h_slot{s}": {"p50": pct(r3[:, s][k3[:, s] > 0], 50),
+                                                  "max": pct(r3[:, s][k3[:, s] > 0], 100)}
+                                 for s in range(8) if (k3[:, s] > 0).any()}}), flush=True)
+        t = allt[:4096]
         t = t[t[:, 0] > 0]
         t0 = t[:, 0].min()
         rel = (t - t0) / 1e3
