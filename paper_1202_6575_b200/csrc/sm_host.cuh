@@ -654,13 +654,14 @@ static sm_status merge_host_pipelined(const K* A, const uint32_t* vA, int64_t n,
     std::vector<cudaEvent_t>& ev_mg = ps->ev_b;
     std::vector<SubMerge> tasks;
     host_plan<K>(A, n, B, m, host_pipeline_blocks<K>(n, m, vC != nullptr), tasks);
-    while (ev_up.size() < tasks.size()) {
-        cudaEvent_t e, f;
-        if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess ||
-            cudaEventCreateWithFlags(&f, cudaEventDisableTiming) != cudaSuccess)
-            return fail_cuda(cudaGetLastError(), "event create");
-        ev_up.push_back(e);
-        ev_mg.push_back(f);
+    // (the two lists grow independently: the sort's host pipeline uses ev_a alone)
+    for (std::vector<cudaEvent_t>* v : {&ev_up, &ev_mg}) {
+        while (v->size() < tasks.size()) {
+            cudaEvent_t e;
+            if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess)
+                return fail_cuda(cudaGetLastError(), "event create");
+            v->push_back(e);
+        }
     }
     const size_t kb = sizeof(K);
     const int64_t T = tile_t((int)kb, vC != nullptr);

@@ -1513,7 +1513,11 @@ struct K3HLayout {
     static constexpr int OFF_TST = OFF_OFS + GROUPS * K3H_NB * 4;  // tile starts [256]
     static constexpr int OFF_RED = OFF_TST + K3H_NB * 4;        // [NW] diff (U), [8] scan sums
     static constexpr int OFF_BAR = (OFF_RED + NW * 16 + 64 + 15) & ~15;
-    static constexpr int SMEM = OFF_BAR + 16;
+    static constexpr int SMEM = OFF_BAR + 4 * 8;                // 4 mbarriers (the pre-pass's 4 TMA targets)
+    // the pre-pass reads keys only, four TMA targets deep: the two input
+    // targets and the two sorted-tile buffers, PT keys each
+    static constexpr int PT = TILE_BYTES / KB;
+    static constexpr int PIPT = PT / NT;
     static_assert(TILE % NT == 0 && NT % 32 == 0 && NT >= K3H_NB && (TILE * KB) % 16 == 0, "tile shape");
     static_assert(GROUPS == 1 || (GROUPS == 2 && GT == K3H_NB), "two groups of 256 threads");
 };
@@ -1910,44 +1914,41 @@ __global__ void __launch_bounds__(NT, SM_K3H_MINB) k_block_sort_hbm(K* buf0, uin
                                                            int final_buf, unsigned long long* ts) {
     using Lay = K3HLayout<K, HAS_V, NT, TILE>;
     using U = typename Lay::U;
-    constexpr int NW = Lay::NW, IPT = Lay::IPT, NPOS = Lay::NPOS;
+    constexpr int NW = Lay::NW, NPOS = Lay::NPOS;
     extern __shared__ __align__(128) char smem[];
     uint32_t* wcnt = (uint32_t*)(smem + Lay::OFF_W);
     uint32_t* hist = (uint32_t*)(smem + Lay::OFF_HIST);
     uint32_t* run = (uint32_t*)(smem + Lay::OFF_RUN);
     U* red = (U*)(smem + Lay::OFF_RED);
     uint32_t* sums = (uint32_t*)(smem + Lay::OFF_RED + NW * 16);
-    uint64_t* bar = (uint64_t*)(smem + Lay::OFF_BAR);      // [2]: one per TMA target
+    uint64_t* bar = (uint64_t*)(smem + Lay::OFF_BAR);      // [4]: one per TMA target (passes: 0, 1)
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
     const int64_t base = (int64_t)blockIdx.x * L0;
     if (base >= N) return;
     const int len = (int)min(L0, N - base);              // < 2^31 (host check)
-    const int ntiles = (len + TILE - 1) / TILE;
     uint32_t ph = 0u;                                   // bit b: the phase of TMA target b
-    auto in_k = [&](int b) { return (K*)(smem + Lay::OFF_IN + b * Lay::TILE_BYTES); };
-    auto in_v = [&](int b) { return (uint32_t*)(smem + Lay::OFF_IN + b * Lay::TILE_BYTES + TILE * Lay::KB); };
 
     if (tid == 0) {
-        mbar_init(&bar[0], 1);
-        mbar_init(&bar[1], 1);
+        for (int b = 0; b < 4; ++b) mbar_init(&bar[b], 1);
         fence_barrier_init();
     }
     for (int i = tid; i < NPOS * 256; i += NT) hist[i] = 0;
     for (int i = tid; i < NW * K3H_NB; i += NT) wcnt[i] = 0;
     __syncthreads();
 
-    // tile t of the block in X (keys; payloads too when `vals`) -> TMA target t % 2
-    auto issue = [&](const K* X, const uint32_t* V, int t, bool vals) {
-        if (tid == 0 && t < ntiles) {
-            const int e0 = t * TILE, cnt = min(TILE, len - e0), b = t & 1;
-            uint32_t tx = k3h_load<K>(in_k(b), X + base + e0, cnt, &bar[b]);
-            if (HAS_V && vals) tx += k3h_load<uint32_t>(in_v(b), V + base + e0, cnt, &bar[b]);
-            mbar_arrive_expect_tx(&bar[b], tx);
+    // pre-pass tile t (PT keys of the block) -> TMA target t % 4
+    constexpr int PT = Lay::PT, PIPT = Lay::PIPT;
+    const int ntp = (len + PT - 1) / PT;
+    auto pissue = [&](int t) {
+        if (tid == 0 && t < ntp) {
+            const int e0 = t * PT, cnt = min(PT, len - e0), b = t & 3;
+            K* dst = (K*)(smem + Lay::OFF_IN + b * Lay::TILE_BYTES);
+            mbar_arrive_expect_tx(&bar[b], k3h_load<K>(dst, buf0 + base + e0, cnt, &bar[b]));
         }
     };
-    auto wait = [&](int t) {
-        mbar_wait(&bar[t & 1], (ph >> (t & 1)) & 1u);
-        ph ^= 1u << (t & 1);
+    auto pwait = [&](int t) {
+        mbar_wait(&bar[t & 3], (ph >> (t & 3)) & 1u);
+        ph ^= 1u << (t & 3);
     };
 
     // SM_K2_TSTAMP builds: per-CTA event times at ts[8 * (4096 + CTA) + slot]:
@@ -1965,25 +1966,25 @@ __global__ void __launch_bounds__(NT, SM_K3H_MINB) k_block_sort_hbm(K* buf0, uin
     (void)ts;
 #endif
     k3_ts(0);
-    // ---- pre-pass: the varying bytes and their histograms
+    // ---- pre-pass: the varying bytes and their histograms (keys only, four
+    // targets of PT keys in flight: measured 0.81 -> see DESIGN with two of TILE)
     const U first = KeyOrd<K>::to(ld_cg(buf0 + base));
     U diff = 0;
-    issue(buf0, vbuf0, 0, false);
-    issue(buf0, vbuf0, 1, false);
-    for (int t = 0; t < ntiles; ++t) {
-        wait(t);
-        const int cnt = min(TILE, len - t * TILE);
-        const K* ik = in_k(t & 1);
-        U u[IPT];
+    for (int t = 0; t < 4; ++t) pissue(t);
+    for (int t = 0; t < ntp; ++t) {
+        pwait(t);
+        const int cnt = min(PT, len - t * PT);
+        const K* ik = (const K*)(smem + Lay::OFF_IN + (t & 3) * Lay::TILE_BYTES);
+        U u[PIPT];
 #pragma unroll
-        for (int k = 0; k < IPT; ++k) {
+        for (int k = 0; k < PIPT; ++k) {
             const int e = k * NT + tid;
             u[k] = e < cnt ? KeyOrd<K>::to(ik[e]) : first;
         }
-        __syncthreads();                                 // TMA target t & 1 is free
-        issue(buf0, vbuf0, t + 2, false);
+        __syncthreads();                                 // TMA target t & 3 is free
+        pissue(t + 4);
 #pragma unroll
-        for (int k = 0; k < IPT; ++k) {
+        for (int k = 0; k < PIPT; ++k) {
             const bool valid = k * NT + tid < cnt;
             const U x = u[k] ^ first;                     // the bits where this key differs from the block's first
             U m = x;                                      // ... OR-ed over the warp's valid lanes

@@ -139,6 +139,22 @@ def test_sort_host_pipelined(kt, N, payload, pinned):
     assert_bit_exact(k, v, *want, kt)
 
 
+def test_host_pipelines_sort_then_merge_same_thread():
+    """The sort's and the merge's host pipelines share one per-(thread,
+    device) set of streams and events: a host-buffer sort (which grows one
+    event list) followed by a pipelined host-buffer merge (which needs two)
+    on the same thread -- a regression test for an event list read past its
+    end -- both as the oracle."""
+    sm = lib()
+    s = synth.sort_input((20 << 20) + 3, "u32", "bounded:100000", seed=7, payload=False)
+    k = s.keys.clone().pin_memory()
+    sm.mergesort_stable(k, None, key_type="u32")
+    assert_bit_exact(k, None, *oracle.sort(s.keys, None, "u32"), "u32")
+    m = synth.merge_input(3 << 20, 3 << 20, "i64", "bounded:1000", seed=9, payload=True)
+    ck, cv = sm.merge_stable(m.a_keys, m.a_vals, m.b_keys, m.b_vals, key_type="i64")
+    assert_bit_exact(ck, cv, *oracle.merge(m.a_keys, m.a_vals, m.b_keys, m.b_vals, "i64"), "i64")
+
+
 @pytest.mark.parametrize("kt,s", [("u32", 1), ("i64", 3), ("f64", 1)])
 def test_sort_misaligned_views(kt, s):
     sm = lib()
