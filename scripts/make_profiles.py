@@ -172,7 +172,7 @@ def write_readme(tag, rows, traffic):
             f"`{tag}_ncu_k_cross_ranks_c2.md` (K1) and `{tag}_ncu_k_block_sort_c5.md` (K3).",
             "- `traffic.json` -- DRAM read+write bytes per K2 launch from those captures (bench.py `roofline.traffic`).",
             f"- `{tag}_bench_reference.json` -- `bench.py --impl reference`: the CPU oracle as the reference arm.",
-            f"- `{tag}_size_sweep.md` -- merge throughput against size (`scripts/size_sweep.sh`, written by hand).",
+            "- `r01_size_sweep.md` -- merge throughput against size (`scripts/size_sweep.sh`, round 1, written by hand).",
             f"- `{tag}_pytest_gpu.log` -- the full `pytest -m gpu` run on the B200."]
     open(os.path.join(OUT, "README.md"), "w").write("\n".join(out) + "\n")
 
