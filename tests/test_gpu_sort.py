@@ -228,3 +228,19 @@ def test_sort_blocks_per_sm_descending(kt):
         sm.mergesort_stable(k, v, key_type=kt, descending=True, run=run)
         torch.cuda.synchronize()
         assert_bit_exact(k.cpu(), v.cpu(), *want, kt)
+
+
+@pytest.mark.parametrize("dist,desc", [("bounded:3", False), ("equal", False), ("full", True), ("bounded:3", True)])
+def test_sort_rounds_ties_across_chunks(dist, desc):
+    """A 12.6 M sort (one block per SM in phase 1, then eight rounds whose runs
+    grow past 255 blocks per side): heavy ties, all-equal keys, both orders --
+    the oracle's stable sort.  (A shared-memory-sample cross-rank kernel for
+    these rounds was measured slower than the plain searches: DESIGN §12.)"""
+    sm = lib()
+    N = (12 << 20) + 77
+    inp = synth.sort_input(N, "u32", dist, seed=N % 89, payload=True)
+    want = oracle.sort(inp.keys, inp.vals, "u32", descending=desc)
+    k, v = inp.keys.cuda(), inp.vals.cuda()
+    sm.mergesort_stable(k, v, key_type="u32", descending=desc)
+    torch.cuda.synchronize()
+    assert_bit_exact(k.cpu(), v.cpu(), *want, "u32")
