@@ -1485,6 +1485,9 @@ __global__ void __launch_bounds__(NT, sizeof(K) <= 8 ? SM_K3_MINB : 1) k_block_s
 // The result lands in the buffer the merge rounds start from (a third
 // buffer, so no pass is spent on the parity of the pass count).
 constexpr int K3H_NB = 256;          // buckets of an 8-bit digit
+#ifndef SM_K3H_VREG
+#define SM_K3H_VREG 0         // 1: payloads held in registers from the load to the scatter (128 regs: spills)
+#endif
 #ifndef SM_K3H_GROUPS
 #define SM_K3H_GROUPS 2      // 2: two warp groups take alternate tiles (one ranks while the other writes)
 #endif
@@ -1794,9 +1797,13 @@ __device__ __forceinline__ uint32_t k3h_scan_group(uint32_t v, uint32_t* sums, i
     return pre + x - v;
 }
 
+// hnext (or null): the histogram of the next pass's byte at nshift, counted
+// here as the sorted tile is written out (the pre-pass counts the first
+// pass's byte only)
 template <typename K, bool HAS_V, int NT, int TILE, int BITS, bool FULL, typename F>
 __device__ __forceinline__ void k3h_tile_group(const K* ik, const uint32_t* iv, int cnt, int shift, char* smem, K* dkb,
-                                               uint32_t* dvb, int len, int g, int t, int ntiles, F release) {
+                                               uint32_t* dvb, int len, int g, int t, int ntiles, F release,
+                                               uint32_t* hnext, int nshift) {
     using Lay = K3HLayout<K, HAS_V, NT, TILE>;
     constexpr int IPT = Lay::GIPT;
     constexpr uint32_t DMASK = (1u << BITS) - 1u;
@@ -1810,23 +1817,24 @@ __device__ __forceinline__ void k3h_tile_group(const K* ik, const uint32_t* iv, 
     const int tid = threadIdx.x, tg = tid & 255, lane = tid & 31, w = tid >> 5, wg = tg >> 5;
     uint32_t* wc = wcnt + w * K3H_NB;
     const uint32_t wc_s = smem_addr(wc);
+    constexpr bool VREG = HAS_V && SM_K3H_VREG;            // payloads held in registers (else re-read)
     uint32_t dr[IPT];
     K key[IPT];
-    uint32_t val[HAS_V ? IPT : 1];
+    uint32_t val[VREG ? IPT : 1];
 #pragma unroll
     for (int k = 0; k < IPT; ++k) {                        // group warp wg: elements [wg*32*IPT, ...)
         const int e = (wg * IPT + k) * 32 + lane;
         const bool valid = FULL || e < cnt;
         if (valid) {
             key[k] = ik[e];
-            if (HAS_V) val[k] = iv[e];
+            if (VREG) val[k] = iv[e];
         }
         const uint32_t d = valid ? (BITS ? (uint32_t)(KeyOrd<K>::to(key[k]) >> shift) & DMASK : 0u) : PAD;
         const uint32_t peers = k3h_peers<BITS>(d, FULL ? 0xffffffffu : __ballot_sync(0xffffffffu, valid));
         dr[k] = (k3h_rank(wc_s, d, peers, lane, valid) << 9) | d;
     }
     k3h_gbar(g);                                           // the group's counts are in wcnt
-    release();                                             // (the items are in registers)
+    if (!HAS_V || VREG) release();                         // (the items are in registers)
     uint32_t tc = 0;
 #pragma unroll
     for (int i = 0; i < 8; ++i) tc += wcnt[(8 * g + i) * K3H_NB + tg];
@@ -1851,12 +1859,14 @@ __device__ __forceinline__ void k3h_tile_group(const K* ik, const uint32_t* iv, 
         if (FULL || d != PAD) {
             const uint32_t at = wc[d] + (dr[k] >> 9);
             so_k[at] = key[k];
-            if (HAS_V) so_v[at] = val[k];
+            if (VREG) so_v[at] = val[k];
+            else if (HAS_V) so_v[at] = iv[(wg * IPT + k) * 32 + lane];
         }
     }
     __syncwarp();
     for (int i = lane; i < K3H_NB; i += 32) wc[i] = 0;
     k3h_gbar(g);
+    if (HAS_V && !VREG) release();                         // the payloads were read from the TMA target
 #pragma unroll
     for (int k = 0; k < IPT; ++k) {
         const int j = k * 256 + tg;
@@ -1867,13 +1877,15 @@ __device__ __forceinline__ void k3h_tile_group(const K* ik, const uint32_t* iv, 
             SM_DCHECK(gi < (uint32_t)len, "K3H store outside its block");
             st_cg(dkb + gi, x);
             if (HAS_V) st_cg(dvb + gi, so_v[j]);
+            if (hnext) atomicAdd(&hnext[(uint32_t)(KeyOrd<K>::to(x) >> nshift) & 0xFFu], 1u);
         }
     }
 }
 
 template <typename K, bool HAS_V, int NT, int TILE, int BITS>
 __device__ __forceinline__ void k3h_pass_group(const K* sk, const uint32_t* sv, K* dk, uint32_t* dv, int64_t base,
-                                               int len, int shift, char* smem, uint64_t* bar, uint32_t& ph) {
+                                               int len, int shift, char* smem, uint64_t* bar, uint32_t& ph,
+                                               uint32_t* hnext = nullptr, int nshift = 0) {
     using Lay = K3HLayout<K, HAS_V, NT, TILE>;
     const int g = threadIdx.x >> 8, tg = threadIdx.x & 255;
     const int ntiles = (len + TILE - 1) / TILE;
@@ -1898,16 +1910,19 @@ __device__ __forceinline__ void k3h_pass_group(const K* sk, const uint32_t* sv, 
         const uint32_t* iv = (const uint32_t*)(smem + Lay::OFF_IN + g * Lay::TILE_BYTES + TILE * Lay::KB);
         if (cnt == TILE)
             k3h_tile_group<K, HAS_V, NT, TILE, BITS, true>(ik, iv, TILE, shift, smem, dkb, dvb, len, g, t, ntiles,
-                                                           [&] { issue(t + 2); });
+                                                           [&] { issue(t + 2); }, hnext, nshift);
         else
             k3h_tile_group<K, HAS_V, NT, TILE, BITS, false>(ik, iv, cnt, shift, smem, dkb, dvb, len, g, t, ntiles,
-                                                            [&] { issue(t + 2); });
+                                                            [&] { issue(t + 2); }, hnext, nshift);
     }
 }
 
 template <typename K, bool HAS_V, int NT, int TILE>
 #ifndef SM_K3H_MINB
 #define SM_K3H_MINB 1
+#endif
+#ifndef SM_K3H_DEFER
+#define SM_K3H_DEFER 1        // the pre-pass counts the first pass's byte only; each pass counts the next one's
 #endif
 __global__ void __launch_bounds__(NT, SM_K3H_MINB) k_block_sort_hbm(K* buf0, uint32_t* vbuf0, K* buf1, uint32_t* vbuf1,
                                                            K* buf2, uint32_t* vbuf2, int64_t N, int64_t L0,
@@ -1966,53 +1981,76 @@ __global__ void __launch_bounds__(NT, SM_K3H_MINB) k_block_sort_hbm(K* buf0, uin
     (void)ts;
 #endif
     k3_ts(0);
-    // ---- pre-pass: the varying bytes and their histograms (keys only, four
-    // targets of PT keys in flight: measured 0.81 -> see DESIGN with two of TILE)
+    // ---- pre-pass: the bytes on which the block's keys differ, and the
+    // histograms of the bytes in `posmask` (keys only, four targets of PT keys
+    // in flight).  With two warp groups (SM_K3H_DEFER) it counts the first
+    // pass's byte only -- byte 0, or after a second read the lowest varying
+    // byte when byte 0 is shared -- and each pass counts the next pass's byte
+    // as it writes its tiles out.
     const U first = KeyOrd<K>::to(ld_cg(buf0 + base));
-    U diff = 0;
-    for (int t = 0; t < 4; ++t) pissue(t);
-    for (int t = 0; t < ntp; ++t) {
-        pwait(t);
-        const int cnt = min(PT, len - t * PT);
-        const K* ik = (const K*)(smem + Lay::OFF_IN + (t & 3) * Lay::TILE_BYTES);
-        U u[PIPT];
+    auto prepass = [&](uint32_t posmask) -> U {
+        U diff = 0;
+        for (int t = 0; t < 4; ++t) pissue(t);
+        for (int t = 0; t < ntp; ++t) {
+            pwait(t);
+            const int cnt = min(PT, len - t * PT);
+            const K* ik = (const K*)(smem + Lay::OFF_IN + (t & 3) * Lay::TILE_BYTES);
+            U u[PIPT];
 #pragma unroll
-        for (int k = 0; k < PIPT; ++k) {
-            const int e = k * NT + tid;
-            u[k] = e < cnt ? KeyOrd<K>::to(ik[e]) : first;
-        }
-        __syncthreads();                                 // TMA target t & 3 is free
-        pissue(t + 4);
-#pragma unroll
-        for (int k = 0; k < PIPT; ++k) {
-            const bool valid = k * NT + tid < cnt;
-            const U x = u[k] ^ first;                     // the bits where this key differs from the block's first
-            U m = x;                                      // ... OR-ed over the warp's valid lanes
-            if constexpr (sizeof(U) == 4) {
-                m = __reduce_or_sync(0xffffffffu, valid ? (uint32_t)x : 0u);
-            } else {
-                const uint32_t lo = __reduce_or_sync(0xffffffffu, valid ? (uint32_t)x : 0u);
-                const uint32_t hi = __reduce_or_sync(0xffffffffu, valid ? (uint32_t)(x >> 32) : 0u);
-                m = ((U)hi << 32) | lo;
+            for (int k = 0; k < PIPT; ++k) {
+                const int e = k * NT + tid;
+                u[k] = e < cnt ? KeyOrd<K>::to(ik[e]) : first;
             }
-            diff |= m;
-            const uint32_t nv = __popc(__ballot_sync(0xffffffffu, valid));
+            __syncthreads();                             // TMA target t & 3 is free
+            pissue(t + 4);
 #pragma unroll
-            for (int pos = 0; pos < NPOS; ++pos) {
-                const uint32_t b = (uint32_t)(u[k] >> (8 * pos)) & 0xFFu;
-                if (((m >> (8 * pos)) & 0xFF) == 0) {     // warp-uniform: every valid lane has the first key's byte
-                    if (lane == 0 && nv) atomicAdd(&hist[pos * 256 + ((uint32_t)(first >> (8 * pos)) & 0xFFu)], nv);
-                } else if (valid) {
-                    atomicAdd(&hist[pos * 256 + b], 1u);
+            for (int k = 0; k < PIPT; ++k) {
+                const bool valid = k * NT + tid < cnt;
+                const U x = u[k] ^ first;                 // the bits where this key differs from the block's first
+                U m = x;                                  // ... OR-ed over the warp's valid lanes
+                if constexpr (sizeof(U) == 4) {
+                    m = __reduce_or_sync(0xffffffffu, valid ? (uint32_t)x : 0u);
+                } else {
+                    const uint32_t lo = __reduce_or_sync(0xffffffffu, valid ? (uint32_t)x : 0u);
+                    const uint32_t hi = __reduce_or_sync(0xffffffffu, valid ? (uint32_t)(x >> 32) : 0u);
+                    m = ((U)hi << 32) | lo;
+                }
+                diff |= m;
+                const uint32_t nv = __popc(__ballot_sync(0xffffffffu, valid));
+#pragma unroll
+                for (int pos = 0; pos < NPOS; ++pos) {
+                    if (!((posmask >> pos) & 1u)) continue;
+                    const uint32_t b = (uint32_t)(u[k] >> (8 * pos)) & 0xFFu;
+                    if (((m >> (8 * pos)) & 0xFF) == 0) { // warp-uniform: every valid lane has the first key's byte
+                        if (lane == 0 && nv) atomicAdd(&hist[pos * 256 + ((uint32_t)(first >> (8 * pos)) & 0xFFu)], nv);
+                    } else if (valid) {
+                        atomicAdd(&hist[pos * 256 + b], 1u);
+                    }
                 }
             }
         }
-    }
-    if (lane == 0) red[w] = diff;
-    __syncthreads();
-    diff = 0;
+        if (lane == 0) red[w] = diff;
+        __syncthreads();
+        diff = 0;
 #pragma unroll
-    for (int i = 0; i < NW; ++i) diff |= red[i];
+        for (int i = 0; i < NW; ++i) diff |= red[i];
+        __syncthreads();                                 // (red[] reused by a second read)
+        return diff;
+    };
+    // (keys-only sorts count every byte in the pre-pass: with the deferred counts
+    // ptxas fails to allocate their kernel, C7600, around the R2P multisplit)
+    constexpr bool DEFER = SM_K3H_DEFER && Lay::GROUPS == 2 && HAS_V;
+    U diff = 0;
+    uint32_t posmask = DEFER ? 1u : 0xFFu;
+#pragma unroll 1
+    for (int rd = 0; rd < 2; ++rd) {                     // (one call site: one inlined copy)
+        const U d = prepass(posmask);
+        if (rd == 0) diff = d;
+        if (!DEFER || (diff & 0xFF) != 0 || diff == 0) break;
+        int p0 = 1;                                      // byte 0 shared: count the lowest varying byte
+        while (((diff >> (8 * p0)) & 0xFF) == 0) ++p0;
+        posmask = 1u << p0;
+    }
     k3_ts(1);
 
     // ---- the pass plan: one pass per varying byte, low to high.  Three
@@ -2043,7 +2081,15 @@ __global__ void __launch_bounds__(NT, SM_K3H_MINB) k_block_sort_hbm(K* buf0, uin
         if (tid < K3H_NB) run[tid] = r0;
         if constexpr (Lay::GROUPS == 2) {
             __syncthreads();                               // run[] of every digit before either group reads it
-            if (bits) k3h_pass_group<K, HAS_V, NT, TILE, 8>(bk(src), bv(src), bk(dst), bv(dst), base, len, shift, smem, bar, ph);
+            // the next pass's byte, counted during this one (DEFER)
+            int npos = -1;
+            if (DEFER && digit_pass && ps + 1 < np) {
+                npos = hpos + 1;
+                while (((diff >> (8 * npos)) & 0xFF) == 0) ++npos;
+            }
+            uint32_t* hn = npos >= 0 ? hist + npos * 256 : nullptr;
+            if (bits) k3h_pass_group<K, HAS_V, NT, TILE, 8>(bk(src), bv(src), bk(dst), bv(dst), base, len, shift, smem, bar, ph,
+                                                            hn, 8 * max(npos, 0));
             else k3h_pass_group<K, HAS_V, NT, TILE, 0>(bk(src), bv(src), bk(dst), bv(dst), base, len, shift, smem, bar, ph);
         } else {
             if (bits) k3h_pass<K, HAS_V, NT, TILE, 8>(bk(src), bv(src), bk(dst), bv(dst), base, len, shift, smem, bar, ph);
