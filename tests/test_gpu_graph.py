@@ -93,3 +93,34 @@ def test_call_keeps_current_device_and_runs_on_stream_device():
     cpu = inp.to("cpu")
     assert_bit_exact(ck.cpu(), cv.cpu(), *oracle.merge(cpu.a_keys, cpu.a_vals, cpu.b_keys, cpu.b_vals, "u32"),
                      "u32")
+
+
+@pytest.mark.parametrize("kind", ["merge", "sort"])
+def test_graph_replay_dynamic_task_assignment(kind):
+    """Sizes where K2 hands its tasks out from a task counter (more than 8 tasks
+    per resident CTA): the counter lives in the call's scratch and is zeroed
+    by the kernel launched before K2 -- inside the graph, so every replay
+    starts from zero -- each replay the oracle's result."""
+    sm = lib()
+    if kind == "merge":
+        n = m = (1 << 23) + 17
+        st = synth.merge_input(n, m, "i32", "full", seed=1, payload=False).to("cuda")
+        g, (ck, _) = _capture(lambda: sm.merge_stable(st.a_keys, None, st.b_keys, None, key_type="i32"))
+        for seed in (2, 3, 4):
+            inp = synth.merge_input(n, m, "i32", "bounded:1000" if seed == 3 else "full", seed=seed, payload=False)
+            st.a_keys.copy_(inp.a_keys)
+            st.b_keys.copy_(inp.b_keys)
+            g.replay()
+            torch.cuda.synchronize()
+            assert_bit_exact(ck.cpu(), None, *oracle.merge(inp.a_keys, None, inp.b_keys, None, "i32"), "i32")
+    else:
+        N = (12 << 20) + 5
+        st = synth.sort_input(N, "u32", "full", seed=3, payload=True, device="cuda")
+        g, _ = _capture(lambda: sm.mergesort_stable(st.keys, st.vals, key_type="u32"))
+        for seed in (4, 5):
+            inp = synth.sort_input(N, "u32", "bounded:100" if seed == 5 else "full", seed=seed, payload=True)
+            st.keys.copy_(inp.keys)
+            st.vals.copy_(inp.vals)
+            g.replay()
+            torch.cuda.synchronize()
+            assert_bit_exact(st.keys.cpu(), st.vals.cpu(), *oracle.sort(inp.keys, inp.vals, "u32"), "u32")

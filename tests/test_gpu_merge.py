@@ -476,3 +476,26 @@ def test_merges_on_side_streams_concurrently():
         cpu = inp.to("cpu")
         assert_bit_exact(ck.cpu(), cv.cpu(), *oracle.merge(cpu.a_keys, cpu.a_vals, cpu.b_keys, cpu.b_vals,
                                                            inp.key_type), inp.key_type)
+
+
+def test_concurrent_merges_dynamic_task_assignment():
+    """Two merges large enough for K2's task counter (more than 8 tasks per
+    resident CTA) on two side streams at once: each call's counter is its
+    own (per-call scratch), so the concurrent K2 grids never take each
+    other's tasks -- both the oracle's merge."""
+    sm = lib()
+    inps = [synth.merge_input((1 << 23) + 5, (1 << 23) - 3, "i32", "full", seed=20 + i, payload=False).to("cuda")
+            for i in range(2)]
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    torch.cuda.synchronize()
+    outs = []
+    for rep in range(3):
+        outs = []
+        for inp, st in zip(inps, streams):
+            with torch.cuda.stream(st):
+                outs.append(sm.merge_stable(inp.a_keys, None, inp.b_keys, None, key_type="i32"))
+        for st in streams:
+            st.synchronize()
+    for (ck, _), inp in zip(outs, inps):
+        cpu = inp.to("cpu")
+        assert_bit_exact(ck.cpu(), None, *oracle.merge(cpu.a_keys, None, cpu.b_keys, None, "i32"), "i32")
