@@ -26,8 +26,11 @@ namespace sm {
 namespace {   // internal linkage: every translation unit keeps its own kernels
 
 // ----------------------------------------------------------------- K1
+#ifndef K1_WAYS_SORT
+#define K1_WAYS_SORT 2   // fan-out of the one-thread-per-search kernel in the sort rounds (binary: C5 K1 -10%)
+#endif
 #ifndef K1_WAYS_SEG
-#define K1_WAYS_SEG 4    // fan-out of the one-thread-per-search kernel (sort rounds, batches)
+#define K1_WAYS_SEG 4    // ... for the batched merges (4-ary: binary measured +18%)
 #endif
 #ifndef K1_WAYS
 #define K1_WAYS 4
@@ -130,7 +133,9 @@ __global__ void __launch_bounds__(256) k_cross_ranks(const K* __restrict__ A, co
     if (search) x = ldg_key((sideA ? A + sg.aoff : B + sg.boff) + Blocks(own_len, plen).start(idx));
     int r;
     if constexpr (G == 1) {
-        r = search ? rank_kary<K, K1_WAYS_SEG>(sideA ? B + sg.boff : A + sg.aoff, oth_len, x, !sideA) : 0;
+        const K* X = sideA ? B + sg.boff : A + sg.aoff;
+        r = !search ? 0
+            : g.sort == 1 ? rank_kary<K, K1_WAYS_SORT>(X, oth_len, x, !sideA) : rank_kary<K, K1_WAYS_SEG>(X, oth_len, x, !sideA);
     } else {
         r = group_rank<K, G>(sideA ? B + sg.boff : A + sg.aoff, oth_len, x, !sideA, search);
     }
