@@ -88,6 +88,8 @@ def args_():
     ap.add_argument("--no-per-config", action="store_true", help="skip the per-config measurements of C1-C5")
     ap.add_argument("--peer-access", action="store_true",
                     help="N > 1: the sharded merge reads foreign ranges through CUDA IPC instead of the NCCL exchange")
+    ap.add_argument("--sort-ways", type=int, choices=[2, 4], default=4,
+                    help="merge sort phase 2: 4 = two merge rounds per HBM pass (default), 2 = one round per pass")
     ap.add_argument("--merge-path", action="store_true",
                     help="merges only: time the equal-output merge-path COMPARISON instead of the paper's method")
     return ap.parse_args()
@@ -286,7 +288,12 @@ class SortWork(Workload):
         self.sm = sm
         import math
         R = sm.sort_run(kt, c["payload"], c["N"])     # phase 1's run length for this N
-        self.passes = 1 + max(0, math.ceil(math.log2(c["N"] / R)))   # block sort + merge rounds
+        self.rounds = max(0, math.ceil(math.log2(c["N"] / R)))      # the paper's merge rounds
+        # HBM passes: the block sort + one per merge pass (two rounds per
+        # pass with sort_ways 4, an odd round on its own)
+        four = SORT_WAYS == 4 and synth.KEY_TYPES[kt][2] <= 8
+        self.merge_passes = self.rounds - (self.rounds // 2 if four else 0)
+        self.passes = 1 + self.merge_passes
 
     def prep(self):                              # restore the unsorted input (untimed)
         self.work_k.copy_(self.src.keys)
@@ -529,7 +536,8 @@ def _measure_config(cfg, sm, dev, stream, steps, warmup, peak, peak_src, clocks)
            "clocks": clocks.summary(w0, w1)}
     if "k_block_sort" in roof:
         out["k_block_sort_ms"] = roof["k_block_sort"]["avg_launch_ms"]
-        out["merge_rounds"] = wl.passes - 1
+        out["merge_rounds"] = wl.rounds
+        out["merge_passes"] = wl.merge_passes
     del wl, flush
     torch.cuda.empty_cache()
     return out
@@ -537,6 +545,7 @@ def _measure_config(cfg, sm, dev, stream, steps, warmup, peak, peak_src, clocks)
 
 def run_ours(a, world, rank, local):
     import paper_1202_6575_b200 as sm
+    sm.set_sort_ways(a.sort_ways)
 
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
@@ -692,8 +701,13 @@ def run_reference(a):
     }
 
 
+SORT_WAYS = 4          # --sort-ways (set in main, read by SortWork)
+
+
 def main():
+    global SORT_WAYS
     a = args_()
+    SORT_WAYS = a.sort_ways
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     if a.impl == "reference":

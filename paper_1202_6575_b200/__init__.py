@@ -92,6 +92,8 @@ _lib.sm_set_k1_variant.argtypes = [ctypes.c_int32]
 _lib.sm_set_k1_variant.restype = None
 _lib.sm_set_small_fuse.argtypes = [ctypes.c_int32]
 _lib.sm_set_small_fuse.restype = None
+_lib.sm_set_sort_ways.argtypes = [ctypes.c_int32]
+_lib.sm_set_sort_ways.restype = None
 _lib.sm_plan_from_ranks.argtypes = [ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p,
                                     ctypes.c_void_p]
 _lib.sm_plan_from_ranks.restype = ctypes.c_int
@@ -253,6 +255,12 @@ def set_small_fuse(on: bool) -> None:
     """Small plain merges in one launch (each K2 CTA ranks its own tasks) or
     K1 then K2 (the default)."""
     _lib.sm_set_small_fuse(int(bool(on)))
+
+
+def set_sort_ways(ways: int) -> None:
+    """Merge sort phase 2: 4 (default) -- two merge rounds per HBM pass;
+    2 -- one round per pass.  Same output."""
+    _lib.sm_set_sort_ways(int(ways))
 
 
 def plan_from_ranks(n: int, m: int, p: int, xbar, ybar) -> list:

@@ -21,6 +21,7 @@ sm_status fail_inval(const char* what) {
 
 int g_k1_variant = 0;
 int g_small_fuse = 0;
+int g_sort_ways = 4;
 uint32_t* g_dbg_cover = nullptr;
 unsigned long long* g_dbg_ts = nullptr;
 bool g_prof_on = false;
@@ -91,6 +92,8 @@ int32_t sm_is_debug_build(void) {
 void sm_set_k1_variant(int32_t variant) { sm::g_k1_variant = (variant >= 0 && variant <= 3) ? variant : 0; }
 
 void sm_set_small_fuse(int32_t on) { sm::g_small_fuse = on != 0; }
+
+void sm_set_sort_ways(int32_t ways) { sm::g_sort_ways = ways == 2 ? 2 : 4; }
 
 sm_status sm_plan_from_ranks(int64_t n, int64_t m, int64_t p, const int64_t* xbar, const int64_t* ybar,
                              int64_t* tasks) {

@@ -28,6 +28,7 @@
 
 #include "stablemerge.h"
 #include "sm_kernels.cuh"
+#include "sm_kernels4.cuh"
 
 namespace sm {
 
@@ -151,6 +152,8 @@ struct ProfRec {
 extern uint32_t* g_dbg_cover;  // SM_DEBUG builds: K2's coverage counters (sm_debug_cover), or null
 extern unsigned long long* g_dbg_ts;   // SM_K2_TSTAMP builds: K2's per-CTA event times (sm_debug_k2_timestamps)
 extern int g_k1_variant;        // test hook (sm_set_k1_variant): 0 auto, 1 warp per search, 2 sample, 3 thread per search
+extern int g_sort_ways;         // sm_set_sort_ways: 4 (default) -- two merge rounds per HBM pass
+                                //   (k_tasks4) for keys <= 8 bytes; 2 -- one round per pass (K2)
 extern int g_small_fuse;        // sm_set_small_fuse: small plain merges in one launch (default 0: measured slower
                                 //   with L2 flushed between calls, C1 24.1 vs 22.9 us; back to back 21.0 vs 21.9)
 extern bool g_prof_on;
@@ -383,6 +386,81 @@ static sm_status launch_merge(const K* A, const PV* vA, const K* B, const PV* vB
     }
     return launch_tasks<K, HAS_V, typename K2Shape<K, HAS_V, PV>::type, PV>(A, vA, B, vB, C, vC, g, gc, xbar, ybar,
                                                                           st, pdl);
+}
+
+// ------------------------------------------------ two rounds per pass
+// The merge sort's rounds L -> 2L -> 4L in one HBM pass (sm_kernels4.cuh):
+// k4_sample, k4_ranks, k4_order (the paper's Steps 1-2 and the order of the
+// subproblems, for four runs), then k_tasks4; PDL between them.
+struct Pass4Scratch {
+    void* spl;        // block-start keys   [G * 4 * cmax]
+    int4* rk;         // their ranks        [G * 4 * cmax]
+    int* fv;          // their places       [G * 4 * cmax]
+    int4* bnd;        // boundaries         [G * (4 * cmax + 2)]
+    int* ctr;         // k_tasks4's task counter
+};
+template <typename K, bool HAS_V>
+struct K4Shape {
+    using Sh = typename K2Shape<K, HAS_V>::type;
+    using Lay = K4Layout<K, HAS_V, Sh::NC, Sh::VT, Sh::STAGES, K2_MAXT>;
+};
+template <typename K, bool HAS_V>
+static Geom4 geom4(int64_t N, int64_t L) {
+    Geom4 g{};
+    g.N = (int)N;
+    g.L = (int)L;
+    g.S = K4Shape<K, HAS_V>::Lay::S;
+    g.cmax = (int)ceil_div(L, g.S);
+    g.TPG = 4 * g.cmax + 1;
+    g.G = (int)ceil_div(N, 4 * L);
+    return g;
+}
+template <typename K, bool HAS_V>
+static sm_status launch_pass4(const K* in, const uint32_t* vin, K* out, uint32_t* vout, int64_t N, int64_t L,
+                              const Pass4Scratch& sc, cudaStream_t st, bool pdl) {
+    using Sh = typename K4Shape<K, HAS_V>::Sh;
+    using Lay = typename K4Shape<K, HAS_V>::Lay;
+    Geom4 g = geom4<K, HAS_V>(N, L);
+    g.ctr = sc.ctr;
+    g.bnd = sc.bnd;
+    g.cover = g_dbg_cover;
+    const long long ids = (long long)g.G * 4 * g.cmax;
+    const long long nb = (long long)g.G * (g.TPG + 1);
+    K* spl = (K*)sc.spl;
+    prof_before(PROF_K1, st);
+    cudaError_t e = launch_maybe_pdl(k4_sample<K>, (unsigned)ceil_div(ids, 256), 256, st, pdl, in, g, spl);
+    if (e == cudaSuccess)
+        e = launch_maybe_pdl(k4_ranks<K>, (unsigned)ceil_div(ids, 256), 256, st, pdl, in, g, (const K*)spl, sc.rk,
+                             sc.fv);
+    if (e == cudaSuccess)
+        e = launch_maybe_pdl(k4_order, (unsigned)ceil_div(std::max(ids, nb), 256), 256, st, pdl, g,
+                             (const int4*)sc.rk, (const int*)sc.fv, sc.bnd);
+    prof_after(st);
+    if (e != cudaSuccess) return fail_cuda(e, "k4 partition");
+    g_launches += 2;
+    sm_status s = check_launch("k4 partition");
+    if (s != SM_OK) return s;
+    auto kern = k_tasks4<K, HAS_V, Sh::NC, Sh::VT, Sh::STAGES, K2_MAXT, Sh::MINB>;
+    static int per_sm_d[SM_MAX_DEV], n_sm_d[SM_MAX_DEV];
+    const int dev = current_device();
+    int per_sm = dev < SM_MAX_DEV ? per_sm_d[dev] : 0, n_sm = dev < SM_MAX_DEV ? n_sm_d[dev] : 0;
+    if (per_sm == 0) {
+        cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Lay::SMEM);
+        cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, Lay::THREADS, Lay::SMEM);
+        if (per_sm < 1) per_sm = 1;
+        if (dev < SM_MAX_DEV) {
+            n_sm_d[dev] = n_sm;
+            per_sm_d[dev] = per_sm;
+        }
+    }
+    const long long grid = std::max(1ll, std::min<long long>((long long)g.G * g.TPG, (long long)per_sm * n_sm));
+    prof_before(PROF_K2, st);
+    e = launch_maybe_pdl_smem(kern, (unsigned)grid, Lay::THREADS, Lay::SMEM, st, pdl, in, vin, out, vout, g);
+    prof_after(st);
+    if (e != cudaSuccess) return fail_cuda(e, "k_tasks4");
+    return check_launch("k_tasks4");
 }
 
 // ------------------------------------------------ host-memory staging
@@ -1095,6 +1173,11 @@ static sm_status sort_device(K* keys, uint32_t* vals, int64_t N, cudaStream_t st
     const bool hbm = R != k3_run((int)sizeof(K), vals != nullptr);
     int rounds = 0;
     for (int64_t L = R; L < N; L *= 2) ++rounds;
+    // phase 2 as HBM passes: with sm_set_sort_ways(4) (the default) two
+    // rounds per pass (k_tasks4), an odd round first as a plain round (K2)
+    const bool four = g_sort_ways == 4 && sizeof(K) <= 8;
+    const int n4 = four ? rounds / 2 : 0;
+    const int passes = rounds - n4;
     // buffers: the caller's (0), aux (1) and, for the one-block-per-SM phase 1,
     // aux2 (2): phase 1 ends in aux2 whatever its pass count, and the merge
     // rounds route through aux / aux2 so that the last one writes buffer 0
@@ -1111,29 +1194,63 @@ static sm_status sort_device(K* keys, uint32_t* vals, int64_t N, cudaStream_t st
     const int64_t rank_ints = 2 * (ceil_div(N, T) + 2 * ceil_div(N, R) + 2);
     if (s == SM_OK) s = dalloc(&ranks, rank_ints + 1, st);     // + K2's task counter
     if (s == SM_OK) s = dalloc(&tdesc, ceil_div(N, T) + 2 * ceil_div(N, R) + 2, st);   // tasks of a round
+    // scratch of the two-rounds-per-pass partition, sized for its largest pass
+    Pass4Scratch sc4{};
+    void* sc4_mem = nullptr;
+    if (s == SM_OK && n4 > 0) {
+        int64_t ids = 0, nb = 0;
+        for (int64_t L = R << (rounds - 2 * n4), k = 0; k < n4; ++k, L *= 4) {
+            if constexpr (sizeof(K) <= 8) {
+                const Geom4 g4 = vals ? geom4<K, true>(N, L) : geom4<K, false>(N, L);
+                ids = std::max(ids, (int64_t)g4.G * 4 * g4.cmax);
+                nb = std::max(nb, (int64_t)g4.G * (g4.TPG + 1));
+            }
+        }
+        const int64_t b_spl = ceil_div(ids * (int64_t)sizeof(K), 16) * 16, b_rk = ids * 16,
+                      b_fv = ceil_div(ids * 4, 16) * 16, b_bnd = nb * 16;
+        s = dalloc((char**)&sc4_mem, b_spl + b_rk + b_fv + b_bnd + 16, st);
+        if (s == SM_OK) {
+            char* p = (char*)sc4_mem;
+            sc4.rk = (int4*)p;
+            sc4.bnd = (int4*)(p + b_rk);
+            sc4.spl = p + b_rk + b_bnd;
+            sc4.fv = (int*)(p + b_rk + b_bnd + b_spl);
+            sc4.ctr = (int*)(p + b_rk + b_bnd + b_spl + b_fv);
+        }
+    }
     if (s == SM_OK) {
         int src;
         prof_before(PROF_K3, st);
         if (hbm) {
-            src = rounds > 0 ? 2 : 0;
+            src = passes > 0 ? 2 : 0;
             if (vals) s = launch_block_sort_hbm<K, true>(keys, vals, kb[1], vb[1], kb[2], vb[2], N, R, src, st);
             else s = launch_block_sort_hbm<K, false>(keys, nullptr, kb[1], nullptr, kb[2], nullptr, N, R, src, st);
         } else {
             // phase 1 lands in the buffer from which the rounds, alternating
             // between 0 and 1, end in 0
-            src = rounds % 2;
+            src = passes % 2;
             const unsigned blocks = (unsigned)ceil_div(N, R);
             if (vals) s = launch_block_sort<K, true>(keys, vals, kb[src], vb[src], N, blocks, st);
             else s = launch_block_sort<K, false>(keys, nullptr, kb[src], nullptr, N, blocks, st);
         }
         prof_after(st);
         if (s == SM_OK) s = check_launch(hbm ? "k_block_sort_hbm" : "k_block_sort");
-        int left = rounds;
+        int left = passes;
         for (int64_t L = R; s == SM_OK && L < N; L *= 2) {
             --left;
+            const bool pass4 = left < n4;         // the last n4 passes take two rounds each
             // this round's target: buffer 0 when an even number of rounds
             // follow, else a buffer that is neither 0 nor the source
             const int dst = left % 2 == 0 ? 0 : (src == 1 ? 2 : 1);
+            if (pass4) {
+                if constexpr (sizeof(K) <= 8) {
+                    if (vals) s = launch_pass4<K, true>(kb[src], vb[src], kb[dst], vb[dst], N, L, sc4, st, pdl);
+                    else s = launch_pass4<K, false>(kb[src], nullptr, kb[dst], nullptr, N, L, sc4, st, pdl);
+                }
+                src = dst;
+                L *= 2;                           // (the loop doubles it again)
+                continue;
+            }
             Geom g{};
             g.S = (int)ceil_div(N, 2 * L);
             g.pA = g.pB = (int)ceil_div(L, T);
@@ -1150,6 +1267,7 @@ static sm_status sort_device(K* keys, uint32_t* vals, int64_t N, cudaStream_t st
             src = dst;
         }
     }
+    dfree(sc4_mem, st);
     dfree(tdesc, st);
     dfree(ranks, st);
     for (int b = 2; b >= 1; --b) {

@@ -50,7 +50,7 @@ cover, (ck, cv) = covered(b.n + b.m, lambda: sm.merge_stable_batched(db.a_keys, 
                                                                      db.b_vals, db.b_offsets, key_type="u32"))
 assert bool((cover == 1).all()), "batched coverage"
 # sorts: the shared-memory block sort and the one-block-per-SM phase 1; every
-# merge round stores every element once
+# merge pass stores every element once
 for kt, N, run in (("u32", 300007, None), ("i64", 200003, 16400), ("f32", 150001, 8192 + 16), ("u64", 70001, 1008)):
     s = synth.sort_input(N, kt, "bounded:100000" if kt != "f32" else "special", seed=N, payload=True)
     k, v = s.keys.to(dev), s.vals.to(dev)
@@ -60,9 +60,17 @@ for kt, N, run in (("u32", 300007, None), ("i64", 200003, 16400), ("f32", 150001
     while L < N:
         rounds += 1
         L *= 2
-    cover, _ = covered(N, lambda: sm.mergesort_stable(k, v, key_type=kt, run=run))
-    assert bool((cover == rounds).all()), ("sort coverage", kt, N, rounds, int(cover.min()), int(cover.max()))
-    assert_bit_exact(k.cpu(), v.cpu(), *oracle.sort(s.keys, s.vals, kt), kt)
+    # one store per element per HBM pass: two rounds per pass (k_tasks4,
+    # ways 4, an odd round on its own) or one (ways 2)
+    for ways in (4, 2):
+        k, v = s.keys.to(dev), s.vals.to(dev)
+        sm.set_sort_ways(ways)
+        cover, _ = covered(N, lambda: sm.mergesort_stable(k, v, key_type=kt, run=run))
+        sm.set_sort_ways(4)
+        passes = rounds - (rounds // 2 if ways == 4 else 0)
+        assert bool((cover == passes).all()), ("sort coverage", kt, N, ways, passes, int(cover.min()),
+                                               int(cover.max()))
+        assert_bit_exact(k.cpu(), v.cpu(), *oracle.sort(s.keys, s.vals, kt), kt)
 print("debug build: store ranges and exact coverage ok")
 """
 
