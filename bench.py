@@ -88,8 +88,9 @@ def args_():
     ap.add_argument("--no-per-config", action="store_true", help="skip the per-config measurements of C1-C5")
     ap.add_argument("--peer-access", action="store_true",
                     help="N > 1: the sharded merge reads foreign ranges through CUDA IPC instead of the NCCL exchange")
-    ap.add_argument("--sort-ways", type=int, choices=[2, 4], default=4,
-                    help="merge sort phase 2: 4 = two merge rounds per HBM pass (default), 2 = one round per pass")
+    ap.add_argument("--sort-ways", type=int, choices=[0, 2, 4], default=0,
+                    help="merge sort phase 2: 0 = automatic (default), 4 = two merge rounds per HBM pass, "
+                         "2 = one round per pass")
     ap.add_argument("--merge-path", action="store_true",
                     help="merges only: time the equal-output merge-path COMPARISON instead of the paper's method")
     return ap.parse_args()
@@ -289,10 +290,9 @@ class SortWork(Workload):
         import math
         R = sm.sort_run(kt, c["payload"], c["N"])     # phase 1's run length for this N
         self.rounds = max(0, math.ceil(math.log2(c["N"] / R)))      # the paper's merge rounds
-        # HBM passes: the block sort + one per merge pass (two rounds per
-        # pass with sort_ways 4, an odd round on its own)
-        four = SORT_WAYS == 4 and synth.KEY_TYPES[kt][2] <= 8
-        self.merge_passes = self.rounds - (self.rounds // 2 if four else 0)
+        # HBM passes: the block sort + one per merge pass (the library's plan:
+        # two rounds per pass where sm_set_sort_ways selects it)
+        self.merge_passes = sm.sort_merge_passes(kt, c["payload"], c["N"])
         self.passes = 1 + self.merge_passes
 
     def prep(self):                              # restore the unsorted input (untimed)
@@ -701,13 +701,8 @@ def run_reference(a):
     }
 
 
-SORT_WAYS = 4          # --sort-ways (set in main, read by SortWork)
-
-
 def main():
-    global SORT_WAYS
     a = args_()
-    SORT_WAYS = a.sort_ways
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     if a.impl == "reference":

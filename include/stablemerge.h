@@ -362,14 +362,20 @@ int64_t sm_sort_run_n(int32_t key_bytes, int32_t has_vals, int64_t n);
  *
  * sm_set_sort_ways: how the merge sort's phase 2 (§3,
  *   row a9) runs its ceil(log2 p) rounds on later calls of this process --
- *   4 (the default, keys of <= 8 bytes): two rounds per HBM pass: the four
- *   runs R0..R3 of two consecutive rounds are partitioned at once (every
- *   block start of a run ranked in the three others: Steps 1-2 of L304-309
- *   for four arrays, reading R19 in DESIGN.md) and each subproblem is merged
- *   twice in shared memory (R0 with R1, R2 with R3, then the two results),
- *   an odd round first as a plain round; 2: one round per pass (the paper's
- *   rounds as they stand).  Any other value selects 4.  Same output, bit for
- *   bit; 128-bit keys always take one round per pass.
+ *   4: two rounds per HBM pass (keys of <= 8 bytes): the four runs R0..R3
+ *   of two consecutive rounds are partitioned at once (every block start of
+ *   a run ranked in the three others: Steps 1-2 of L304-309 for four
+ *   arrays, reading R19 in DESIGN.md) and each subproblem is merged twice in
+ *   shared memory (R0 with R1, R2 with R3, then the two results), an odd
+ *   round first as a plain round; 2: one round per pass (the paper's rounds
+ *   as they stand); 0 (the default, also any other value): 4 where it
+ *   measured faster -- key + payload slots of >= 8 bytes and N >= 2^23 --
+ *   else 2.  Same output, bit for bit; 128-bit keys always take one round
+ *   per pass.
+ *
+ * sm_sort_merge_passes: the number of phase-2 HBM passes (k_tasks / k_tasks4
+ *   launches) a sort of n elements takes on the current device under the
+ *   current sm_set_sort_ways setting (16-byte-aligned buffers).
  *
  * sm_plan_from_ranks: the host's own Steps 3-4 (readings
  *   R1, R8) on given cross ranks xbar[0..p], ybar[0..p] with p blocks per
@@ -380,6 +386,7 @@ int64_t sm_sort_run_n(int32_t key_bytes, int32_t has_vals, int64_t n);
 void sm_set_k1_variant(int32_t variant);
 void sm_set_small_fuse(int32_t on);
 void sm_set_sort_ways(int32_t ways);
+int32_t sm_sort_merge_passes(int32_t key_bytes, int32_t has_vals, int64_t n);
 
 /* SM_DEBUG builds (build_native.build_debug(): lib/libstablemerge_debug.so)
  * check the paper's disjoint-write invariant on the device (PAPER.md

@@ -94,6 +94,8 @@ _lib.sm_set_small_fuse.argtypes = [ctypes.c_int32]
 _lib.sm_set_small_fuse.restype = None
 _lib.sm_set_sort_ways.argtypes = [ctypes.c_int32]
 _lib.sm_set_sort_ways.restype = None
+_lib.sm_sort_merge_passes.argtypes = [ctypes.c_int32, ctypes.c_int32, ctypes.c_int64]
+_lib.sm_sort_merge_passes.restype = ctypes.c_int32
 _lib.sm_plan_from_ranks.argtypes = [ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p,
                                     ctypes.c_void_p]
 _lib.sm_plan_from_ranks.restype = ctypes.c_int
@@ -258,9 +260,14 @@ def set_small_fuse(on: bool) -> None:
 
 
 def set_sort_ways(ways: int) -> None:
-    """Merge sort phase 2: 4 (default) -- two merge rounds per HBM pass;
-    2 -- one round per pass.  Same output."""
+    """Merge sort phase 2: 0 (default) automatic, 4 -- two merge rounds per
+    HBM pass, 2 -- one round per pass.  Same output."""
     _lib.sm_set_sort_ways(int(ways))
+
+
+def sort_merge_passes(key_type: str, has_vals: bool, n: int) -> int:
+    """Phase-2 HBM passes of a sort of n elements under the current setting."""
+    return int(_lib.sm_sort_merge_passes(_BYTES[key_type], int(has_vals), int(n)))
 
 
 def plan_from_ranks(n: int, m: int, p: int, xbar, ybar) -> list:

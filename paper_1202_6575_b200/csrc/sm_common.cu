@@ -21,7 +21,7 @@ sm_status fail_inval(const char* what) {
 
 int g_k1_variant = 0;
 int g_small_fuse = 0;
-int g_sort_ways = 4;
+int g_sort_ways = 0;
 uint32_t* g_dbg_cover = nullptr;
 unsigned long long* g_dbg_ts = nullptr;
 bool g_prof_on = false;
@@ -93,7 +93,7 @@ void sm_set_k1_variant(int32_t variant) { sm::g_k1_variant = (variant >= 0 && va
 
 void sm_set_small_fuse(int32_t on) { sm::g_small_fuse = on != 0; }
 
-void sm_set_sort_ways(int32_t ways) { sm::g_sort_ways = ways == 2 ? 2 : 4; }
+void sm_set_sort_ways(int32_t ways) { sm::g_sort_ways = (ways == 2 || ways == 4) ? ways : 0; }
 
 sm_status sm_plan_from_ranks(int64_t n, int64_t m, int64_t p, const int64_t* xbar, const int64_t* ybar,
                              int64_t* tasks) {
@@ -139,6 +139,15 @@ int64_t sm_sort_run_n(int32_t key_bytes, int32_t has_vals, int64_t n) {
     if (key_bytes > 8 || n <= 0) return r3;
     const int64_t L0 = sm::ceil_div(sm::ceil_div(n, sm::k3h_blocks()), 16) * 16;
     return L0 >= sm::K3H_MIN_RUN ? L0 : r3;
+}
+
+int32_t sm_sort_merge_passes(int32_t key_bytes, int32_t has_vals, int64_t n) {
+    // sort_device's phase-2 plan: ceil(log2(n / R)) rounds, two per pass
+    // where sort_four_ways holds (an odd round on its own)
+    const int64_t R = sm_sort_run_n(key_bytes, has_vals, n);
+    int32_t rounds = 0;
+    for (int64_t L = R; L < n; L *= 2) ++rounds;
+    return sm::sort_four_ways(key_bytes, has_vals != 0, n) ? rounds - rounds / 2 : rounds;
 }
 
 const char* sm_status_string(sm_status s) {

@@ -152,8 +152,8 @@ struct ProfRec {
 extern uint32_t* g_dbg_cover;  // SM_DEBUG builds: K2's coverage counters (sm_debug_cover), or null
 extern unsigned long long* g_dbg_ts;   // SM_K2_TSTAMP builds: K2's per-CTA event times (sm_debug_k2_timestamps)
 extern int g_k1_variant;        // test hook (sm_set_k1_variant): 0 auto, 1 warp per search, 2 sample, 3 thread per search
-extern int g_sort_ways;         // sm_set_sort_ways: 4 (default) -- two merge rounds per HBM pass
-                                //   (k_tasks4) for keys <= 8 bytes; 2 -- one round per pass (K2)
+extern int g_sort_ways;         // sm_set_sort_ways: 0 (default) automatic, 4 -- two merge rounds per
+                                //   HBM pass (k_tasks4) for keys <= 8 bytes, 2 -- one round per pass (K2)
 extern int g_small_fuse;        // sm_set_small_fuse: small plain merges in one launch (default 0: measured slower
                                 //   with L2 flushed between calls, C1 24.1 vs 22.9 us; back to back 21.0 vs 21.9)
 extern bool g_prof_on;
@@ -399,9 +399,28 @@ struct Pass4Scratch {
     int4* bnd;        // boundaries         [G * (4 * cmax + 2)]
     int* ctr;         // k_tasks4's task counter
 };
+#ifndef SM_K4_MIN_N
+#define SM_K4_MIN_N (1 << 23)   // sorts below this size keep one round per pass
+#endif
+// k_tasks4 shapes (tuning experiments override them with -DSM_K4S8_NC=...):
+// 4-byte elements as K2's, <= 8-byte elements SM_K4S8, wider as K2's.
+#ifndef SM_K4S8_NC
+#define SM_K4S8_NC SM_K2S8_NC
+#endif
+#ifndef SM_K4S8_VT
+#define SM_K4S8_VT SM_K2S8_VT
+#endif
+#ifndef SM_K4S8_ST
+#define SM_K4S8_ST SM_K2S8_ST
+#endif
+#ifndef SM_K4S8_MINB
+#define SM_K4S8_MINB SM_K2S8_MINB
+#endif
 template <typename K, bool HAS_V>
 struct K4Shape {
-    using Sh = typename K2Shape<K, HAS_V>::type;
+    static constexpr int bytes = (int)sizeof(K) + (HAS_V ? 4 : 0);
+    using Sh = typename std::conditional<bytes == 8, K2Geo<SM_K4S8_NC, SM_K4S8_VT, SM_K4S8_ST, SM_K4S8_MINB>,
+                                         typename K2Shape<K, HAS_V>::type>::type;
     using Lay = K4Layout<K, HAS_V, Sh::NC, Sh::VT, Sh::STAGES, K2_MAXT>;
 };
 template <typename K, bool HAS_V>
@@ -1167,6 +1186,14 @@ static int64_t phase1_run(int64_t N, const void* keys, const void* vals, int64_t
     return L0 >= K3H_MIN_RUN ? L0 : r3;
 }
 
+// Phase 2 with two rounds per HBM pass?  sm_set_sort_ways: 2 never, 4
+// always (keys <= 8 bytes), 0 (the default) where measured faster.
+static inline bool sort_four_ways(int key_bytes, bool has_vals, int64_t N) {
+    if (key_bytes > 8 || g_sort_ways == 2) return false;
+    if (g_sort_ways == 4) return true;
+    return (key_bytes > 4 || has_vals) && N >= SM_K4_MIN_N;
+}
+
 template <typename K>
 static sm_status sort_device(K* keys, uint32_t* vals, int64_t N, cudaStream_t st, bool pdl, int64_t run_opt = 0) {
     const int64_t R = phase1_run<K>(N, keys, vals, run_opt);   // initial run length
@@ -1174,8 +1201,13 @@ static sm_status sort_device(K* keys, uint32_t* vals, int64_t N, cudaStream_t st
     int rounds = 0;
     for (int64_t L = R; L < N; L *= 2) ++rounds;
     // phase 2 as HBM passes: with sm_set_sort_ways(4) (the default) two
-    // rounds per pass (k_tasks4), an odd round first as a plain round (K2)
-    const bool four = g_sort_ways == 4 && sizeof(K) <= 8;
+    // rounds per pass (k_tasks4), an odd round first as a plain round (K2).
+    // Measured (scripts/gpu_sort_ways.sh): faster for key + payload slots of
+    // >= 8 bytes from N ~ 2^23 on (C5 -4%, i64 / f64 + payload -3%); slower
+    // for 4-byte keys without payload (+1%: their DRAM pass is half as long
+    // against the same shared-memory merges) and for small N (2M: +18%,
+    // the partition's four launches), which keep one round per pass.
+    const bool four = sort_four_ways((int)sizeof(K), vals != nullptr, N);
     const int n4 = four ? rounds / 2 : 0;
     const int passes = rounds - n4;
     // buffers: the caller's (0), aux (1) and, for the one-block-per-SM phase 1,

@@ -42,6 +42,10 @@
 namespace sm {
 namespace {   // internal linkage: every translation unit keeps its own kernels
 
+#ifndef SM_K4_LOG2_NV
+#define SM_K4_LOG2_NV 0       // 1: split probes sized by the stage (NV) instead of the task bound (2S)
+#endif
+
 struct Geom4 {
     int N;            // elements
     int L;            // input run length (a multiple of 16 or the whole input)
@@ -406,8 +410,14 @@ __global__ void __launch_bounds__(K4Layout<K, HAS_V, NC, VT, STAGES, MAXT>::THRE
     k_tasks4(const K* __restrict__ in, const uint32_t* __restrict__ vin, K* __restrict__ out,
              uint32_t* __restrict__ vout, Geom4 g) {
     using Lay = K4Layout<K, HAS_V, NC, VT, STAGES, MAXT>;
-    constexpr int NV = Lay::NV;
-    constexpr int LOG2NV = 31 - __builtin_clz(NV);
+    // merge-path splits: a level-1 range holds <= S elements, a level-2
+    // range (X) <= 2S, plus the split's skew (< 2 * SM_SPLIT_SKEW_LEVEL
+    // virtual candidates): 2^(LOG2+1) - 1 covers them
+#if SM_K4_LOG2_NV
+    constexpr int LOG2NV = 31 - __builtin_clz(Lay::NV);
+#else
+    constexpr int LOG2NV = 31 - __builtin_clz(2 * Lay::S + 2 * SM_SPLIT_SKEW_LEVEL);
+#endif
     constexpr int EK = 2 * (Lay::EPV - 1);
     constexpr int EV = HAS_V ? 2 * 3 : 0;
     extern __shared__ __align__(128) char smem[];

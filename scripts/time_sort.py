@@ -1,5 +1,5 @@
 """Device time of one stable merge sort (CUDA events, inputs restored between
-calls outside the timed region): python scripts/time_sort.py KT N PAYLOAD DIST"""
+calls outside the timed region): python scripts/time_sort.py KT N PAYLOAD DIST [WAYS]"""
 import os
 import sys
 
@@ -10,6 +10,8 @@ import paper_1202_6575_b200 as sm  # noqa: E402
 import synth  # noqa: E402
 
 kt, N, payload, dist = sys.argv[1], int(sys.argv[2]), sys.argv[3] == "1", sys.argv[4] if len(sys.argv) > 4 else "full"
+ways = int(sys.argv[5]) if len(sys.argv) > 5 else 4
+sm.set_sort_ways(ways)
 inp = synth.sort_input(N, kt, dist, seed=1, payload=payload, device="cuda")
 k, v = inp.keys.clone(), None if inp.vals is None else inp.vals.clone()
 ts = []
@@ -25,4 +27,4 @@ for i in range(13):
     if i >= 3:
         ts.append(e0.elapsed_time(e1))
 ts.sort()
-print(f"sort {kt} N={N} payload={payload} {dist}: median {ts[len(ts) // 2]:.3f} ms")
+print(f"sort {kt} N={N} payload={payload} {dist} ways={ways}: median {ts[len(ts) // 2]:.3f} ms")

@@ -37,8 +37,9 @@ def test_header_declares_entry_points():
             assert f"{f}_desc_{kt}" in names          # descending order
         for f in ("merge_stable_wide", "merge_stable_batched_wide", "mergesort_stable_wide"):
             assert f"{f}_{kt}" in names and f"{f}_desc_{kt}" in names   # wide payloads (row 2)
-    assert len(names) == 155          # + sm_sort_run_n, sm_set_k1_variant, sm_plan_from_ranks, sm_debug_cover,
-    #                                     sm_is_debug_build, sm_set_small_fuse, sm_plan_tasks, sm_set_sort_ways
+    assert len(names) == 156          # + sm_sort_run_n, sm_set_k1_variant, sm_plan_from_ranks, sm_debug_cover,
+    #                                     sm_is_debug_build, sm_set_small_fuse, sm_plan_tasks, sm_set_sort_ways,
+    #                                     sm_sort_merge_passes
 
 
 def test_library_exports_every_declared_symbol(sm):

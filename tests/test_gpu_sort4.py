@@ -24,7 +24,7 @@ def gpu_sort(sm, inp: synth.SortInput, ways: int, run=None, descending=False):
         sm.mergesort_stable(k, v, key_type=inp.key_type, run=run, descending=descending)
         torch.cuda.synchronize()
     finally:
-        sm.set_sort_ways(4)
+        sm.set_sort_ways(0)
     return k.cpu(), (None if v is None else v.cpu())
 
 
@@ -82,8 +82,8 @@ def test_sort4_default_run_matches_oracle(kt, payload):
 def test_sort4_equals_two_way_full_c5():
     """BASELINE config 5 at full size (N = 2^28): two rounds per pass and one
     round per pass give the same bytes, and the result is sorted and stable
-    (payload = original index, increasing within equal keys); a sample of
-    positions checked against the oracle's rank of the key."""
+    (payload = original index, increasing within equal keys) and carries
+    every key with its index (a permutation of the input)."""
     sm = lib()
     inp = synth.config_input(5)
     k4, v4 = gpu_sort(sm, inp, 4)
@@ -96,3 +96,33 @@ def test_sort4_equals_two_way_full_c5():
     assert np.all(v[1:][tie] > v[:-1][tie])
     src = inp.keys.numpy().view(np.uint32)
     assert np.array_equal(src[v], k)                  # a permutation carried with its keys
+
+
+def test_sort_merge_passes_plan():
+    """The pass plan the library reports (bench.py's algorithmic bytes use it):
+    ceil(log2(N / R)) rounds, two per HBM pass where selected."""
+    sm = lib()
+    N = 1 << 28
+    R = sm.sort_run("u32", True, N)
+    rounds = 0
+    while R << rounds < N:
+        rounds += 1
+    try:
+        sm.set_sort_ways(2)
+        assert sm.sort_merge_passes("u32", True, N) == rounds
+        sm.set_sort_ways(4)
+        assert sm.sort_merge_passes("u32", True, N) == rounds - rounds // 2
+        assert sm.sort_merge_passes("u32", False, N) == rounds - rounds // 2
+        r128 = 0
+        while sm.sort_run("u128", True, 1 << 20) << r128 < 1 << 20:
+            r128 += 1
+        assert sm.sort_merge_passes("u128", True, 1 << 20) == r128   # 128-bit keys: one round per pass
+        sm.set_sort_ways(0)                          # automatic: key + payload >= 8 bytes, N >= 2^23
+        assert sm.sort_merge_passes("u32", True, N) == rounds - rounds // 2
+        assert sm.sort_merge_passes("u32", False, N) == rounds
+        r_small = 0
+        while sm.sort_run("u64", True, 1 << 20) << r_small < 1 << 20:
+            r_small += 1
+        assert sm.sort_merge_passes("u64", True, 1 << 20) == r_small
+    finally:
+        sm.set_sort_ways(0)
