@@ -365,7 +365,7 @@ int64_t sm_sort_run_n(int32_t key_bytes, int32_t has_vals, int64_t n);
  *   4: two rounds per HBM pass (keys of <= 8 bytes): the four runs R0..R3
  *   of two consecutive rounds are partitioned at once (every block start of
  *   a run ranked in the three others: Steps 1-2 of L304-309 for four
- *   arrays, reading R19 in DESIGN.md) and each subproblem is merged twice in
+ *   arrays, reading R20 in DESIGN.md) and each subproblem is merged twice in
  *   shared memory (R0 with R1, R2 with R3, then the two results), an odd
  *   round first as a plain round; 2: one round per pass (the paper's rounds
  *   as they stand); 0 (the default, also any other value): 4 where it

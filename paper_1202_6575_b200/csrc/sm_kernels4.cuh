@@ -23,7 +23,7 @@
 //   of that run lies strictly inside), so a subproblem holds at most 4S --
 //   the paper's task bound (L388-393) for four arrays.  The subproblems are
 //   disjoint and cover the group; their output offset is f of their first
-//   block start (reading R19 in DESIGN.md).
+//   block start (reading R20 in DESIGN.md).
 //
 //   k4_sample   the block-start keys of every run, contiguous (L2-resident)
 //   k4_ranks    one thread per block start: its three ranks, each by a

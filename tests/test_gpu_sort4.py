@@ -1,5 +1,5 @@
 """GPU parity of the merge sort's phase 2 with two rounds per HBM pass
-(sm_set_sort_ways(4), k4_* + k_tasks4; reading R19) against the
+(sm_set_sort_ways(4), k4_* + k_tasks4; reading R20) against the
 CPU oracle, and against the one-round-per-pass path (ways = 2).
 
 The run length is forced small (sm_options.sort_run) so that many passes
