@@ -402,25 +402,65 @@ struct Pass4Scratch {
 #ifndef SM_K4_MIN_N
 #define SM_K4_MIN_N (1 << 23)   // sorts below this size keep one round per pass
 #endif
-// k_tasks4 shapes (tuning experiments override them with -DSM_K4S8_NC=...):
-// 4-byte elements as K2's, <= 8-byte elements SM_K4S8, wider as K2's.
+// k_tasks4 shapes by slot size (tuning experiments override them with
+// -DSM_K4S8_NC=... etc.).  8-byte slots: one CTA of 512 x 17 per SM -- the
+// split's probes amortise over 17 outputs instead of 15 and S doubles (half
+// the block starts to rank and order); measured on C5 (scripts/gpu_ab.sh,
+// pass / partition ms per sort): 256 x 15 x 2 CTAs 4.81 / 0.48, 288 x 13 x 2
+// 4.76 / 0.48, 384 x 10 x 2 5.21 / 0.48, 512 x 15 4.83 / 0.35, 480 x 17 4.66 /
+// 0.34, 576 x 15 4.67 / 0.33, 640 x 13 4.64 / 0.33, 512 x 19 with two stages
+// 4.68 / 0.32, 384 x 19 4.89 / 0.35, 512 x 17 4.53 / 0.33 (C5 9.90 -> 9.45 ms;
+// f32 + payload 2^28 12.24 -> 11.80 ms; i64 keys-only 2^27 unchanged, 9.23 ->
+// 9.26).  12-byte slots: 448 x 13 with three stages instead of K2's 256 x 15
+// with four (i64 + payload 2^27 14.11 -> 13.27 ms, f64 + payload 14.87 ->
+// 14.06; scripts/gpu_k4_types.sh).  4-byte keys without payload keep K2's
+// shape and one round per pass (704 x 23 at one CTA per SM: 8.29 ms against
+// 8.28 for one round per pass on 2^28 u32 keys).
+#ifndef SM_K4S4_NC
+#define SM_K4S4_NC SM_K2S4_NC
+#endif
+#ifndef SM_K4S4_VT
+#define SM_K4S4_VT SM_K2S4_VT
+#endif
+#ifndef SM_K4S4_ST
+#define SM_K4S4_ST SM_K2S4_ST
+#endif
+#ifndef SM_K4S4_MINB
+#define SM_K4S4_MINB SM_K2S4_MINB
+#endif
 #ifndef SM_K4S8_NC
-#define SM_K4S8_NC SM_K2S8_NC
+#define SM_K4S8_NC 512
 #endif
 #ifndef SM_K4S8_VT
-#define SM_K4S8_VT SM_K2S8_VT
+#define SM_K4S8_VT 17
 #endif
 #ifndef SM_K4S8_ST
-#define SM_K4S8_ST SM_K2S8_ST
+#define SM_K4S8_ST 3
 #endif
 #ifndef SM_K4S8_MINB
-#define SM_K4S8_MINB SM_K2S8_MINB
+#define SM_K4S8_MINB 1
+#endif
+#ifndef SM_K4S12_NC
+#define SM_K4S12_NC 448
+#endif
+#ifndef SM_K4S12_VT
+#define SM_K4S12_VT 13
+#endif
+#ifndef SM_K4S12_ST
+#define SM_K4S12_ST 3
+#endif
+#ifndef SM_K4S12_MINB
+#define SM_K4S12_MINB 1
 #endif
 template <typename K, bool HAS_V>
 struct K4Shape {
     static constexpr int bytes = (int)sizeof(K) + (HAS_V ? 4 : 0);
-    using Sh = typename std::conditional<bytes == 8, K2Geo<SM_K4S8_NC, SM_K4S8_VT, SM_K4S8_ST, SM_K4S8_MINB>,
-                                         typename K2Shape<K, HAS_V>::type>::type;
+    using Sh = typename std::conditional<
+        bytes <= 4, K2Geo<SM_K4S4_NC, SM_K4S4_VT, SM_K4S4_ST, SM_K4S4_MINB>,
+        typename std::conditional<bytes <= 8, K2Geo<SM_K4S8_NC, SM_K4S8_VT, SM_K4S8_ST, SM_K4S8_MINB>,
+                                  typename std::conditional<bytes <= 12,
+                                                            K2Geo<SM_K4S12_NC, SM_K4S12_VT, SM_K4S12_ST, SM_K4S12_MINB>,
+                                                            typename K2Shape<K, HAS_V>::type>::type>::type>::type;
     using Lay = K4Layout<K, HAS_V, Sh::NC, Sh::VT, Sh::STAGES, K2_MAXT>;
 };
 template <typename K, bool HAS_V>
