@@ -1549,6 +1549,7 @@ struct K3HLayout {
     static constexpr int PT = TILE_BYTES / KB;
     static constexpr int PIPT = PT / NT;
     static_assert(TILE % NT == 0 && NT % 32 == 0 && NT >= K3H_NB && (TILE * KB) % 16 == 0, "tile shape");
+    static_assert(PT % NT == 0, "the pre-pass reads whole TMA targets: PT keys over NT threads");
     static_assert(GROUPS == 1 || (GROUPS == 2 && GT == K3H_NB), "two groups of 256 threads");
 };
 
