@@ -1158,6 +1158,12 @@ static sm_status launch_block_sort(const K* in, const uint32_t* vin, K* out, uin
 #ifndef SM_K3H_TILE
 #define SM_K3H_TILE (SM_K3H_GROUPS == 2 ? 4096 : 8192)
 #endif
+#ifndef SM_K3H_TILE12
+#define SM_K3H_TILE12 4096     // 8-byte integer keys + payload
+#endif
+#ifndef SM_K3H_TILE12F
+#define SM_K3H_TILE12F 3072    // f64 keys + payload (4096 spills more there)
+#endif
 #ifndef SM_K3H_TILE4
 #define SM_K3H_TILE4 (SM_K3H_GROUPS == 2 ? 5120 : 8192)
 #endif
@@ -1172,9 +1178,11 @@ static sm_status launch_block_sort_hbm(K* keys, uint32_t* vals, K* aux, uint32_t
         constexpr int NT = SM_K3H_NT;
         // 4-byte keys: tiles of 5120 per warp group (measured, C5 K3H 4.65 -> 4.43 ms, u32 keys-only
         // 2^28 8.29 -> 8.05 ms; 3072: 5.09; 6144 spills); 8-byte keys keep 4096 (keys-only: 5120 measured
-        // 6% slower) and 2048 with a payload
+        // 6% slower, 3584 / 4608 4-7%); with a payload 4096 for integer keys and 3072 for f64 (2^27 i64 +
+        // payload 13.27 ms with 2048, 12.09 with 3072, 11.77 with 4096; f64 + payload 14.07 / 12.95 / 13.30)
         constexpr int TILE = sizeof(K) == 4 ? SM_K3H_TILE4
-                                            : ((int)sizeof(K) + (HAS_V ? 4 : 0) <= 8 ? SM_K3H_TILE : SM_K3H_TILE / 2);
+                                            : ((int)sizeof(K) + (HAS_V ? 4 : 0) <= 8 ? SM_K3H_TILE
+                                               : (KeyOrd<K>::FLOAT ? SM_K3H_TILE12F : SM_K3H_TILE12));
         using Lay = K3HLayout<K, HAS_V, NT, TILE>;
         auto kern = k_block_sort_hbm<K, HAS_V, NT, TILE>;
         static bool attr[SM_MAX_DEV];
