@@ -489,10 +489,10 @@ static sm_status launch_pass4(const K* in, const uint32_t* vin, K* out, uint32_t
     prof_before(PROF_K1, st);
     cudaError_t e = launch_maybe_pdl(k4_sample<K>, (unsigned)ceil_div(ids, 256), 256, st, pdl, in, g, spl);
     if (e == cudaSuccess)
-        e = launch_maybe_pdl(k4_ranks<K>, (unsigned)ceil_div(ids, 256), 256, st, pdl, in, g, (const K*)spl, sc.rk,
+        e = launch_maybe_pdl(k4_ranks<K>, (unsigned)ceil_div(4 * ids, 256), 256, st, pdl, in, g, (const K*)spl, sc.rk,
                              sc.fv);
     if (e == cudaSuccess)
-        e = launch_maybe_pdl(k4_order, (unsigned)ceil_div(std::max(ids, nb), 256), 256, st, pdl, g,
+        e = launch_maybe_pdl(k4_order, (unsigned)ceil_div(std::max(4 * ids, nb), 256), 256, st, pdl, g,
                              (const int4*)sc.rk, (const int*)sc.fv, sc.bnd);
     prof_after(st);
     if (e != cudaSuccess) return fail_cuda(e, "k4 partition");

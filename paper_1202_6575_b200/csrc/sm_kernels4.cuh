@@ -26,12 +26,12 @@
 //   block start (reading R20 in DESIGN.md).
 //
 //   k4_sample   the block-start keys of every run, contiguous (L2-resident)
-//   k4_ranks    one thread per block start: its three ranks, each by a
+//   k4_ranks    four lanes per block start, one per run: its three ranks, each by a
 //               binary search over the other run's block-start keys (L2),
 //               then one inside the block that search names (S elements,
 //               HBM)
 //   --  single synchronisation (PDL griddepcontrol.wait, L373-375)
-//   k4_order    one thread per block start: its place among the group's
+//   k4_order    four lanes per block start: its place among the group's
 //               block starts (three searches over the f values, L2), and
 //               the group's sentinel boundaries
 //   k_tasks4    K2's persistent warp-specialised TMA ring, four ranges per
@@ -95,36 +95,42 @@ __device__ __forceinline__ int count_before(const K* X, int len, K e, bool high)
 }
 
 // ---- k4_ranks: Steps 1-2 for four runs ------------------------------------
+// Four lanes per block start, one per run: lane jj ranks e in run jj (its own
+// run: qS), so the three searches run side by side instead of one after the
+// other (each is ~25 dependent loads); the quad's lane 0 writes the ranks.
 template <typename K>
 __global__ void __launch_bounds__(256) k4_ranks(const K* __restrict__ in, Geom4 g, const K* __restrict__ spl,
                                                 int4* __restrict__ rk, int* __restrict__ fv) {
     pdl_wait();
-    const int id = blockIdx.x * blockDim.x + threadIdx.x;
+    const int tid = blockIdx.x * blockDim.x + threadIdx.x;
+    const int id = tid >> 2, jj = tid & 3;
+    int r = 0;
+    bool valid = false;
     if (id < g.G * 4 * g.cmax) {
         const int q = id % g.cmax, j = (id / g.cmax) & 3, grp = id / (4 * g.cmax);
-        if ((int64_t)q * g.S < run_len(g, grp, j)) {
-            const K e = spl[id];
-            int r[4];
-#pragma unroll
-            for (int jj = 0; jj < 4; ++jj) {
-                if (jj == j) {
-                    r[jj] = q * g.S;
-                    continue;
-                }
+        valid = (int64_t)q * g.S < run_len(g, grp, j);
+        if (valid) {
+            if (jj == j) {
+                r = q * g.S;
+            } else {
+                const K e = spl[id];
                 const int len = run_len(g, grp, jj);
                 const bool high = jj < j;
                 // the block of run jj holding the rank: c block starts lie before e
                 const int c = count_before(spl + (grp * 4 + jj) * g.cmax, run_starts(g, len), e, high);
-                if (c == 0) {
-                    r[jj] = 0;
-                } else {
+                if (c > 0) {
                     const int lo = (c - 1) * g.S + 1, hi = min(c * g.S, len);
-                    r[jj] = lo + count_before(in + run_base(g, grp, jj) + lo, hi - lo, e, high);
+                    r = lo + count_before(in + run_base(g, grp, jj) + lo, hi - lo, e, high);
                 }
             }
-            rk[id] = make_int4(r[0], r[1], r[2], r[3]);
-            fv[id] = r[0] + r[1] + r[2] + r[3];
         }
+    }
+    const int lane = threadIdx.x & 31, q0 = lane & ~3;
+    const int r0 = __shfl_sync(0xffffffffu, r, q0), r1 = __shfl_sync(0xffffffffu, r, q0 + 1),
+              r2 = __shfl_sync(0xffffffffu, r, q0 + 2), r3 = __shfl_sync(0xffffffffu, r, q0 + 3);
+    if (valid && jj == 0) {
+        rk[id] = make_int4(r0, r1, r2, r3);
+        fv[id] = r0 + r1 + r2 + r3;
     }
     pdl_launch_dependents();
 }
@@ -132,20 +138,24 @@ __global__ void __launch_bounds__(256) k4_ranks(const K* __restrict__ in, Geom4 
 // ---- k4_order: the block starts of a group in output order ----------------
 // bnd[grp][0] = (0,0,0,0); bnd[grp][1 + k] = the k-th block start by f;
 // bnd[grp][1 + tot ..] = (len0, len1, len2, len3): the tasks past the
-// group's last block start are empty.
+// group's last block start are empty.  Four lanes per block start as in
+// k4_ranks (lane jj: the block starts of run jj before it).
 __global__ void __launch_bounds__(256) k4_order(Geom4 g, const int4* __restrict__ rk, const int* __restrict__ fv,
                                                 int4* __restrict__ bnd) {
     pdl_wait();
     if (g.ctr && blockIdx.x == 0 && threadIdx.x == 0) *g.ctr = 0;   // k_tasks4's counter (after the wait)
-    const int id = blockIdx.x * blockDim.x + threadIdx.x;
+    const int tid = blockIdx.x * blockDim.x + threadIdx.x;
+    const int id = tid >> 2, jj = tid & 3;
+    int cntb = 0;
+    bool valid = false;
     if (id < g.G * 4 * g.cmax) {
         const int q = id % g.cmax, j = (id / g.cmax) & 3, grp = id / (4 * g.cmax);
-        if ((int64_t)q * g.S < run_len(g, grp, j)) {
-            const int f = fv[id];
-            int pos = q;
-#pragma unroll
-            for (int jj = 0; jj < 4; ++jj) {
-                if (jj == j) continue;
+        valid = (int64_t)q * g.S < run_len(g, grp, j);
+        if (valid) {
+            if (jj == j) {
+                cntb = q;
+            } else {
+                const int f = fv[id];
                 const int* F = fv + (grp * 4 + jj) * g.cmax;
                 int lo = 0, n = run_starts(g, run_len(g, grp, jj));
                 while (n > 0) {                        // f values of distinct elements differ
@@ -154,21 +164,27 @@ __global__ void __launch_bounds__(256) k4_order(Geom4 g, const int4* __restrict_
                     lo = before ? lo + h + 1 : lo;
                     n = before ? n - h - 1 : h;
                 }
-                pos += lo;
+                cntb = lo;
             }
-            bnd[(int64_t)grp * (g.TPG + 1) + 1 + pos] = rk[id];
         }
     }
-    if (id < g.G * (g.TPG + 1)) {                     // sentinels
-        const int s = id % (g.TPG + 1), grp = id / (g.TPG + 1);
+    int pos = cntb;
+    pos += __shfl_xor_sync(0xffffffffu, pos, 1);
+    pos += __shfl_xor_sync(0xffffffffu, pos, 2);
+    if (valid && jj == 0) {
+        const int grp = id / (4 * g.cmax);
+        bnd[(int64_t)grp * (g.TPG + 1) + 1 + pos] = rk[id];
+    }
+    if (tid < g.G * (g.TPG + 1)) {                    // sentinels
+        const int s = tid % (g.TPG + 1), grp = tid / (g.TPG + 1);
         int len[4], tot = 0;
 #pragma unroll
-        for (int jj = 0; jj < 4; ++jj) {
-            len[jj] = run_len(g, grp, jj);
-            tot += run_starts(g, len[jj]);
+        for (int k = 0; k < 4; ++k) {
+            len[k] = run_len(g, grp, k);
+            tot += run_starts(g, len[k]);
         }
-        if (s == 0) bnd[id] = make_int4(0, 0, 0, 0);
-        else if (s > tot) bnd[id] = make_int4(len[0], len[1], len[2], len[3]);
+        if (s == 0) bnd[tid] = make_int4(0, 0, 0, 0);
+        else if (s > tot) bnd[tid] = make_int4(len[0], len[1], len[2], len[3]);
     }
     pdl_launch_dependents();
 }
