@@ -369,8 +369,8 @@ int64_t sm_sort_run_n(int32_t key_bytes, int32_t has_vals, int64_t n);
  *   shared memory (R0 with R1, R2 with R3, then the two results), an odd
  *   round first as a plain round; 2: one round per pass (the paper's rounds
  *   as they stand); 0 (the default, also any other value): 4 where it
- *   measured faster -- key + payload slots of >= 8 bytes and N >= 2^23 --
- *   else 2.  Same output, bit for bit; 128-bit keys always take one round
+ *   measured faster -- N >= 3 * 2^19 (~1.5 M) elements, except 4-byte
+ *   keys without a payload from N = 2^28 on -- else 2.  Same output, bit for bit; 128-bit keys always take one round
  *   per pass.
  *
  * sm_sort_merge_passes: the number of phase-2 HBM passes (k_tasks / k_tasks4

@@ -400,7 +400,7 @@ struct Pass4Scratch {
     int* ctr;         // k_tasks4's task counter
 };
 #ifndef SM_K4_MIN_N
-#define SM_K4_MIN_N (1 << 23)   // sorts below this size keep one round per pass
+#define SM_K4_MIN_N (3 << 19)   // sorts below ~1.5 M elements keep one round per pass (2^20: 0.148 / 0.143 ms)
 #endif
 // k_tasks4 shapes by slot size (tuning experiments override them with
 // -DSM_K4S8_NC=... etc.).  8-byte slots: one CTA of 512 x 17 per SM -- the
@@ -1246,7 +1246,12 @@ static int64_t phase1_run(int64_t N, const void* keys, const void* vals, int64_t
 static inline bool sort_four_ways(int key_bytes, bool has_vals, int64_t N) {
     if (key_bytes > 8 || g_sort_ways == 2) return false;
     if (g_sort_ways == 4) return true;
-    return (key_bytes > 4 || has_vals) && N >= SM_K4_MIN_N;
+    // measured (scripts/time_sort.py, ways 4 against 2): faster from N ~ 1.5 M on for every
+    // slot size (u32 + payload 2^21 0.200 / 0.210 ms, 2^24 0.851 / 0.993; i64 + payload 2^22
+    // 0.509 / 0.565; u32 keys 2^24 0.636 / 0.728, 2^27 4.12 / 4.15) except 4-byte keys without
+    // a payload at 2^28 (8.36 / 8.28: their HBM pass is half as long against the same merges)
+    if (key_bytes <= 4 && !has_vals && N >= (1ll << 28)) return false;
+    return N >= SM_K4_MIN_N;
 }
 
 template <typename K>
@@ -1255,13 +1260,8 @@ static sm_status sort_device(K* keys, uint32_t* vals, int64_t N, cudaStream_t st
     const bool hbm = R != k3_run((int)sizeof(K), vals != nullptr);
     int rounds = 0;
     for (int64_t L = R; L < N; L *= 2) ++rounds;
-    // phase 2 as HBM passes: with sm_set_sort_ways(4) (the default) two
-    // rounds per pass (k_tasks4), an odd round first as a plain round (K2).
-    // Measured (scripts/gpu_sort_ways.sh): faster for key + payload slots of
-    // >= 8 bytes from N ~ 2^23 on (C5 -4%, i64 / f64 + payload -3%); slower
-    // for 4-byte keys without payload (+1%: their DRAM pass is half as long
-    // against the same shared-memory merges) and for small N (2M: +18%,
-    // the partition's four launches), which keep one round per pass.
+    // phase 2 as HBM passes: two rounds per pass (k_tasks4) where
+    // sort_four_ways says so, an odd round first as a plain round (K2)
     const bool four = sort_four_ways((int)sizeof(K), vals != nullptr, N);
     const int n4 = four ? rounds / 2 : 0;
     const int passes = rounds - n4;

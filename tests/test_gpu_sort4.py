@@ -117,9 +117,14 @@ def test_sort_merge_passes_plan():
         while sm.sort_run("u128", True, 1 << 20) << r128 < 1 << 20:
             r128 += 1
         assert sm.sort_merge_passes("u128", True, 1 << 20) == r128   # 128-bit keys: one round per pass
-        sm.set_sort_ways(0)                          # automatic: key + payload >= 8 bytes, N >= 2^23
+        sm.set_sort_ways(0)                          # automatic: N >= ~1.5 M, but 4-byte keys alone < 2^28
         assert sm.sort_merge_passes("u32", True, N) == rounds - rounds // 2
         assert sm.sort_merge_passes("u32", False, N) == rounds
+        for kt, payload, n in (("u32", False, 1 << 27), ("u64", True, 1 << 22), ("i64", False, 1 << 21)):
+            r = 0
+            while sm.sort_run(kt, payload, n) << r < n:
+                r += 1
+            assert sm.sort_merge_passes(kt, payload, n) == r - r // 2
         r_small = 0
         while sm.sort_run("u64", True, 1 << 20) << r_small < 1 << 20:
             r_small += 1
