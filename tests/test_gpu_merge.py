@@ -499,3 +499,37 @@ def test_concurrent_merges_dynamic_task_assignment():
     for (ck, _), inp in zip(outs, inps):
         cpu = inp.to("cpu")
         assert_bit_exact(ck.cpu(), None, *oracle.merge(cpu.a_keys, None, cpu.b_keys, None, "i32"), "i32")
+
+
+@pytest.mark.parametrize("kt,payload", [("i32", False), ("u32", True), ("i64", True), ("f32", False)])
+def test_chained_merges_search_ahead(kt, payload):
+    """Back-to-back calls on one stream where the second merge reads what the
+    first one writes (pre-filled with zeros, so a kernel that read its inputs
+    ahead of the stream order -- K1 and K2 are chained by programmatic
+    dependent launches -- would rank against wrong data): both outputs must be
+    the oracle's, every time.  Also the regression test of the search-ahead
+    experiment (scripts/experiments/k1_search_ahead.patch)."""
+    sm = lib()
+    n = 1 << 23
+    a = synth.merge_input(n, n, kt, "full", seed=5, payload=payload)
+    d2 = synth.merge_input(2 * n, 2 * n, kt, "full", seed=6, payload=payload)   # its B is merge 2's B
+    da, dd = a.to("cuda"), d2.to("cuda")
+    w1k, w1v = oracle_merge(a)
+    w1k_t = torch.from_numpy(np.ascontiguousarray(w1k).view({4: np.int32, 8: np.int64}[w1k.dtype.itemsize]))
+    w1v_t = None if w1v is None else torch.from_numpy(np.ascontiguousarray(w1v).view(np.int32))
+    w2k, w2v = oracle.merge(w1k_t, w1v_t, d2.b_keys, d2.b_vals, kt)
+    c1k = torch.empty(2 * n, dtype=da.a_keys.dtype, device="cuda")
+    c1v = torch.empty(2 * n, dtype=torch.int32, device="cuda") if payload else None
+    c2k = torch.empty(4 * n, dtype=da.a_keys.dtype, device="cuda")
+    c2v = torch.empty(4 * n, dtype=torch.int32, device="cuda") if payload else None
+    for rep in range(6):
+        c1k.zero_()
+        if payload:
+            c1v.zero_()
+        sm.merge_stable(da.a_keys, da.a_vals, da.b_keys, da.b_vals, c1k, c1v, key_type=kt)
+        sm.merge_stable(c1k, c1v, dd.b_keys, dd.b_vals, c2k, c2v, key_type=kt)
+        if rep % 2:                                  # a third call queued behind, reading the first's output again
+            sm.merge_stable(c1k, c1v, dd.b_keys, dd.b_vals, c2k, c2v, key_type=kt)
+        torch.cuda.synchronize()
+        assert_bit_exact(c1k.cpu(), None if c1v is None else c1v.cpu(), w1k, w1v, kt)
+        assert_bit_exact(c2k.cpu(), None if c2v is None else c2v.cpu(), w2k, w2v, kt)
