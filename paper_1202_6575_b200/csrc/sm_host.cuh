@@ -88,6 +88,26 @@ struct K2Shape {
                                   typename std::conditional<bytes <= 12, K2Geo<256, 15, 4>,
                                                             K2Geo<256, 11, 3>>::type>::type>::type;
 };
+// Large plain merges of 8-byte slots: one CTA per SM with a larger tile
+// (the split's probes amortise over 17 outputs, half the cross ranks);
+// measured (scripts/gpu_k2s8.sh, ms, 256 x 15 x 2 CTAs against the large
+// shape): u32 + payload 2^26 + 2^26 0.379 / 0.366 with 512 x 17, f32 +
+// payload 2^25 + 2^25 0.206 / 0.198, u32 + payload 2^27 + 2^20 0.410 / 0.388,
+// 2^22 + 2^22 0.0433 / 0.0402; i64 keys 2^26 + 2^26 0.429 / 0.397 with
+// 448 x 17 (0.443 with 512 x 17).  Small merges keep two small CTAs per SM
+// (C1, 2^20 + 2^20: 23.5 us against 26.6) and so do the sort rounds and the
+// batched merges' segments.
+#ifndef SM_K2_BIG_MIN
+#define SM_K2_BIG_MIN (1ll << 23)     // n + m from which a default plain merge takes the large shape
+#endif
+template <typename K, bool HAS_V, typename PV = uint32_t>
+struct K2ShapeBig {
+    static constexpr int bytes = (int)sizeof(K) + (HAS_V ? (int)sizeof(PV) : 0);
+    static constexpr bool differs = bytes == 8;
+    using type = typename std::conditional<
+        !differs, typename K2Shape<K, HAS_V, PV>::type,
+        typename std::conditional<sizeof(K) == 4, K2Geo<512, 17, 3, 1>, K2Geo<448, 17, 3, 1>>::type>::type;
+};
 // Tasks packed per ring stage at most.
 constexpr int K2_MAXT = 16;
 
@@ -109,6 +129,12 @@ static bool keys_aligned(std::initializer_list<const void*> ptrs) {
     return true;
 }
 static int64_t tile_t(int key_bytes, bool has_v) { return tile_nv(key_bytes, has_v) / 2; }
+// ... of the large shape (8-byte slots; else the same)
+static int64_t tile_nv_big(int key_bytes, bool has_v) {
+    if (key_bytes == 4 && has_v) return K2ShapeBig<uint32_t, true>::type::NV;
+    if (key_bytes == 8 && !has_v) return K2ShapeBig<uint64_t, false>::type::NV;
+    return tile_nv(key_bytes, has_v);
+}
 // K3 shape: one run of R = k3_nt * k3_ipt elements per CTA (radix block sort),
 // two CTAs per SM.  Key + payload slots of <= 8 bytes: 256 x 33 = 8448
 // (>= 2^13: one merge round fewer than 256 x 17 for N = 2^28; C5 14.96 vs
@@ -351,10 +377,18 @@ static sm_status launch_tasks(const K* A, const PV* vA, const K* B, const PV* vB
 template <typename K, bool HAS_V, typename PV = uint32_t>
 static sm_status launch_merge(const K* A, const PV* vA, const K* B, const PV* vB, K* C,
                               PV* vC, const Geom& g0, int* xbar, int* ybar, cudaStream_t st, bool pdl,
-                              const GeomCounts* counts = nullptr, int4* tdesc = nullptr) {
+                              const GeomCounts* counts = nullptr, int4* tdesc = nullptr, bool big = false) {
     const GeomCounts gc = counts ? *counts : geom_counts(g0);
     Geom g = g0;
     using Sh0 = typename K2Shape<K, HAS_V, PV>::type;
+    if constexpr (K2ShapeBig<K, HAS_V, PV>::differs) {
+        if (big && g0.sort == 0 && !tdesc) {            // a large plain merge: the large shape
+            sm_status sb = launch_cross_ranks<K>(A, B, g0, gc, xbar, ybar, st, pdl);
+            if (sb != SM_OK) return sb;
+            return launch_tasks<K, HAS_V, typename K2ShapeBig<K, HAS_V, PV>::type, PV>(A, vA, B, vB, C, vC, g, gc, xbar,
+                                                                                     ybar, st, pdl);
+        }
+    }
     if (g0.sort == 0 && SM_SMALL_FUSE && g_small_fuse && g_k1_variant == 0 &&
         gc.tasks <= (long long)K2L_MAXP * k2_resident<K, HAS_V, Sh0, PV>()) {
         // a small plain merge: one launch -- each CTA of K2 computes the cross
@@ -625,7 +659,7 @@ static inline int64_t merge_scratch_ints(int64_t pA, int64_t pB) { return (pA + 
 template <typename K, typename PV = uint32_t>
 static sm_status merge_device(const K* A, const PV* vA, int64_t n, const K* B, const PV* vB, int64_t m,
                               K* C, PV* vC, cudaStream_t st, int64_t pA, int64_t pB, bool pdl,
-                              int* ranks_given = nullptr) {
+                              int* ranks_given = nullptr, bool big = false) {
     Geom g{};
     g.S = 1; g.pA = (int)pA; g.pB = (int)pB; g.n = (int)n; g.m = (int)m; g.L = 0; g.N = 0; g.sort = 0;
     // scratch: x̄ (p_A + 1), ȳ (p_B + 1), task counter
@@ -640,9 +674,9 @@ static sm_status merge_device(const K* A, const PV* vA, int64_t n, const K* B, c
     if (s != SM_OK) return s;
 #endif
 
-    if (vC) s = launch_merge<K, true, PV>(A, vA, B, vB, C, vC, g, ranks, ranks + pA + 1, st, pdl, nullptr, tdesc);
+    if (vC) s = launch_merge<K, true, PV>(A, vA, B, vB, C, vC, g, ranks, ranks + pA + 1, st, pdl, nullptr, tdesc, big);
     else s = launch_merge<K, false, PV>(A, nullptr, B, nullptr, C, nullptr, g, ranks, ranks + pA + 1, st, pdl, nullptr,
-                                       tdesc);
+                                       tdesc, big);
     dfree(tdesc, st);
     if (!ranks_given) dfree(ranks, st);
     return s;
@@ -916,9 +950,10 @@ static sm_status merge_large_device(const K* A, const uint32_t* vA, int64_t n, c
 // Any size, device buffers.
 template <typename K>
 static sm_status merge_any_device(const K* A, const uint32_t* vA, int64_t n, const K* B, const uint32_t* vB, int64_t m,
-                                  K* C, uint32_t* vC, cudaStream_t st, int64_t pA, int64_t pB, bool pdl) {
+                                  K* C, uint32_t* vC, cudaStream_t st, int64_t pA, int64_t pB, bool pdl,
+                                  bool big = false) {
     if (n + m > (int64_t)INT_MAX) return merge_large_device<K>(A, vA, n, B, vB, m, C, vC, st, pdl);
-    return merge_device<K>(A, vA, n, B, vB, m, C, vC, st, pA, pB, pdl);
+    return merge_device<K>(A, vA, n, B, vB, m, C, vC, st, pA, pB, pdl, nullptr, big);
 }
 
 template <typename K>
@@ -947,7 +982,10 @@ static sm_status merge_entry(const K* A, const uint32_t* vA, int64_t n, const K*
         overlaps(vC, cb * 4, vA, n * 4) || overlaps(vC, cb * 4, vB, m * 4) || overlaps(C, cb * kb, vC, cb * 4))
         return SM_EALIAS;
 
-    const int64_t NV = tile_nv((int)sizeof(K), vC != nullptr);
+    // a default plain merge of >= SM_K2_BIG_MIN elements takes the large tile shape (8-byte slots)
+    const bool big = !(opt && (opt->p_A || opt->p_B || opt->block || (opt->flags & SM_FLAG_MERGE_PATH))) && !large &&
+                     n + m >= SM_K2_BIG_MIN && !g_small_fuse;
+    const int64_t NV = big ? tile_nv_big((int)sizeof(K), vC != nullptr) : tile_nv((int)sizeof(K), vC != nullptr);
     int64_t pA, pB;
     if (opt && (opt->p_A || opt->p_B)) {
         if (opt->p_A < 1 || opt->p_B < 1) return fail_inval("p_A and p_B must both be >= 1");
@@ -973,7 +1011,7 @@ static sm_status merge_entry(const K* A, const uint32_t* vA, int64_t n, const K*
 
     const bool host = is_host_ptr(A) || is_host_ptr(B) || is_host_ptr(vA) || is_host_ptr(vB) || is_host_ptr(C) ||
                       is_host_ptr(vC);
-    if (!host) return merge_any_device<K>(A, vA, n, B, vB, m, C, vC, st, pA, pB, pdl);
+    if (!host) return merge_any_device<K>(A, vA, n, B, vB, m, C, vC, st, pA, pB, pdl, big);
 
     // Host inputs large enough to pipeline: sub-merges over two streams.
     const bool host_inputs = is_host_ptr(A) && is_host_ptr(B) && (!vC || (is_host_ptr(vA) && is_host_ptr(vB)));
@@ -991,7 +1029,7 @@ static sm_status merge_entry(const K* A, const uint32_t* vA, int64_t n, const K*
     if (s == SM_OK && vC) s = stage_in(svC, vC, cb * 4, true, false, st);
     if (s == SM_OK)
         s = merge_any_device<K>((const K*)sA.dev, (const uint32_t*)svA.dev, n, (const K*)sB.dev,
-                                (const uint32_t*)svB.dev, m, (K*)sC.dev, (uint32_t*)svC.dev, st, pA, pB, pdl);
+                                (const uint32_t*)svB.dev, m, (K*)sC.dev, (uint32_t*)svC.dev, st, pA, pB, pdl, big);
     sm_status s2 = SM_OK;
     for (Stage* x : {&sC, &svC, &sA, &sB, &svA, &svB}) {
         if (s != SM_OK) x->out = false;

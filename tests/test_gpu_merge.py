@@ -533,3 +533,25 @@ def test_chained_merges_search_ahead(kt, payload):
         torch.cuda.synchronize()
         assert_bit_exact(c1k.cpu(), None if c1v is None else c1v.cpu(), w1k, w1v, kt)
         assert_bit_exact(c2k.cpu(), None if c2v is None else c2v.cpu(), w2k, w2v, kt)
+
+
+@pytest.mark.parametrize("kt,payload,dist", [("u32", True, "bounded:65536"), ("f32", True, "special"),
+                                             ("i32", True, "full"), ("i64", False, "bounded:1000"),
+                                             ("u64", False, "mostly:7:9/10"), ("f64", False, "full")])
+@pytest.mark.parametrize("nm", [((1 << 22) + 5, (1 << 22) - 5), ((1 << 23) + 12345, 70001), (333, (1 << 23) + 77)])
+def test_large_default_merges_take_the_large_shape(kt, payload, dist, nm):
+    """Default plain merges of >= 2^23 elements with 8-byte slots run K2 with
+    its large tile (512 x 17 / 448 x 17 at one CTA per SM): the
+    oracle's merge, bit for bit, and the same as with an explicit block size
+    (which keeps the small shape)."""
+    sm = lib()
+    n, m = nm
+    inp = synth.merge_input(n, m, kt, dist, seed=n % 1000 + m % 7, payload=payload)
+    want = oracle_merge(inp)
+    assert_bit_exact(*gpu_merge(sm, inp), *want, kt)
+    assert_bit_exact(*gpu_merge(sm, inp, block=sm.tile_capacity(kt, payload) // 2), *want, kt)
+    if kt in ("u32", "i64"):
+        dinp = synth.merge_input(n, m, kt, dist, seed=n % 1000 + 3, payload=payload, descending=True)
+        gk, gv = gpu_merge(sm, dinp, descending=True)
+        assert_bit_exact(gk, gv, *oracle.merge(dinp.a_keys, dinp.a_vals, dinp.b_keys, dinp.b_vals, kt,
+                                               descending=True), kt)
