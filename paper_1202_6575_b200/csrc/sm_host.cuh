@@ -374,34 +374,15 @@ static sm_status launch_tasks(const K* A, const PV* vA, const K* B, const PV* vB
     return SM_OK;
 }
 
-template <typename K, bool HAS_V, typename PV = uint32_t>
-static sm_status launch_merge(const K* A, const PV* vA, const K* B, const PV* vB, K* C,
-                              PV* vC, const Geom& g0, int* xbar, int* ybar, cudaStream_t st, bool pdl,
-                              const GeomCounts* counts = nullptr, int4* tdesc = nullptr, bool big = false) {
-    const GeomCounts gc = counts ? *counts : geom_counts(g0);
+// K1, (segmented modes) k_classify, K2 -- with the tile shape Sh.
+template <typename K, bool HAS_V, typename Sh, typename PV>
+static sm_status launch_merge_sh(const K* A, const PV* vA, const K* B, const PV* vB, K* C, PV* vC, const Geom& g0,
+                                 const GeomCounts& gc, int* xbar, int* ybar, cudaStream_t st, bool pdl, int4* tdesc) {
     Geom g = g0;
-    using Sh0 = typename K2Shape<K, HAS_V, PV>::type;
-    if constexpr (K2ShapeBig<K, HAS_V, PV>::differs) {
-        if (big && g0.sort == 0 && !tdesc) {            // a large plain merge: the large shape
-            sm_status sb = launch_cross_ranks<K>(A, B, g0, gc, xbar, ybar, st, pdl);
-            if (sb != SM_OK) return sb;
-            return launch_tasks<K, HAS_V, typename K2ShapeBig<K, HAS_V, PV>::type, PV>(A, vA, B, vB, C, vC, g, gc, xbar,
-                                                                                     ybar, st, pdl);
-        }
-    }
-    if (g0.sort == 0 && SM_SMALL_FUSE && g_small_fuse && g_k1_variant == 0 &&
-        gc.tasks <= (long long)K2L_MAXP * k2_resident<K, HAS_V, Sh0, PV>()) {
-        // a small plain merge: one launch -- each CTA of K2 computes the cross
-        // ranks its own tasks read (k2_local_prologue)
-        g.fuse = 1;
-        return launch_tasks<K, HAS_V, typename K2Shape<K, HAS_V, PV>::type, PV>(A, vA, B, vB, C, vC, g, gc, xbar, ybar,
-                                                                              st, pdl);
-    }
     sm_status s = launch_cross_ranks<K>(A, B, g0, gc, xbar, ybar, st, pdl);
     if (s != SM_OK) return s;
     if (tdesc && gc.tasks > 0) {
         // segmented modes: classify every task once, ahead of K2 (k_classify)
-        using Sh = typename K2Shape<K, HAS_V, PV>::type;
         cudaLaunchConfig_t cfg;
         memset(&cfg, 0, sizeof(cfg));
         cfg.gridDim = dim3((unsigned)((gc.tasks + 255) / 256));
@@ -418,8 +399,31 @@ static sm_status launch_merge(const K* A, const PV* vA, const K* B, const PV* vB
         if (s != SM_OK) return s;
         g.tdesc = tdesc;
     }
-    return launch_tasks<K, HAS_V, typename K2Shape<K, HAS_V, PV>::type, PV>(A, vA, B, vB, C, vC, g, gc, xbar, ybar,
-                                                                          st, pdl);
+    return launch_tasks<K, HAS_V, Sh, PV>(A, vA, B, vB, C, vC, g, gc, xbar, ybar, st, pdl);
+}
+
+// big: the large tile shape (K2ShapeBig: large plain merges and batches of
+// 8-byte slots; the caller's block counts / block size must match it).
+template <typename K, bool HAS_V, typename PV = uint32_t>
+static sm_status launch_merge(const K* A, const PV* vA, const K* B, const PV* vB, K* C,
+                              PV* vC, const Geom& g0, int* xbar, int* ybar, cudaStream_t st, bool pdl,
+                              const GeomCounts* counts = nullptr, int4* tdesc = nullptr, bool big = false) {
+    const GeomCounts gc = counts ? *counts : geom_counts(g0);
+    using Sh0 = typename K2Shape<K, HAS_V, PV>::type;
+    if constexpr (K2ShapeBig<K, HAS_V, PV>::differs) {
+        if (big && g0.sort != 1)
+            return launch_merge_sh<K, HAS_V, typename K2ShapeBig<K, HAS_V, PV>::type, PV>(A, vA, B, vB, C, vC, g0, gc, xbar,
+                                                                                        ybar, st, pdl, tdesc);
+    }
+    if (g0.sort == 0 && SM_SMALL_FUSE && g_small_fuse && g_k1_variant == 0 &&
+        gc.tasks <= (long long)K2L_MAXP * k2_resident<K, HAS_V, Sh0, PV>()) {
+        // a small plain merge: one launch -- each CTA of K2 computes the cross
+        // ranks its own tasks read (k2_local_prologue)
+        Geom g = g0;
+        g.fuse = 1;
+        return launch_tasks<K, HAS_V, Sh0, PV>(A, vA, B, vB, C, vC, g, gc, xbar, ybar, st, pdl);
+    }
+    return launch_merge_sh<K, HAS_V, Sh0, PV>(A, vA, B, vB, C, vC, g0, gc, xbar, ybar, st, pdl, tdesc);
 }
 
 // ------------------------------------------------ two rounds per pass
@@ -1073,7 +1077,10 @@ static sm_status batch_entry(const K* A, const PV* vA, int64_t n, const int64_t*
         is_host_ptr(a_off) || is_host_ptr(b_off))
         return fail_inval("merge_stable_batched takes device pointers only");
     keep_pool(st);
-    const int64_t T = vC ? K2Shape<K, true, PV>::type::T : K2Shape<K, false>::type::T;
+    // large batches of 8-byte slots take K2's large tile shape (C6 / B1: K2 0.338 -> 0.330 ms)
+    const bool big = n + m >= SM_K2_BIG_MIN;
+    const int64_t T = big ? (vC ? K2ShapeBig<K, true, PV>::type::T : K2ShapeBig<K, false>::type::T)
+                          : (vC ? K2Shape<K, true, PV>::type::T : K2Shape<K, false>::type::T);
     const int nblk = (int)ceil_div(S, BATCH_NT);
     GeomCounts gc;
     gc.tasks = ceil_div(n, T) + ceil_div(m, T) + 2 * S;      // sum over segments of p_A + p_B
@@ -1106,8 +1113,9 @@ static sm_status batch_entry(const K* A, const PV* vA, int64_t n, const int64_t*
         g.S = (int)S; g.sort = 2; g.T = (int)T; g.segs = segs; g.totals = totals;
         g.ctr = totals + 2;                           // (totals[0..1]: tasks, rank entries)
         g.task_seg = task_seg; g.rank_seg = rank_seg;
-        if (vC) s = launch_merge<K, true, PV>(A, vA, B, vB, C, vC, g, ranks, ranks, st, true, &gc, tdesc);
-        else s = launch_merge<K, false, PV>(A, nullptr, B, nullptr, C, nullptr, g, ranks, ranks, st, true, &gc, tdesc);
+        if (vC) s = launch_merge<K, true, PV>(A, vA, B, vB, C, vC, g, ranks, ranks, st, true, &gc, tdesc, big);
+        else s = launch_merge<K, false, PV>(A, nullptr, B, nullptr, C, nullptr, g, ranks, ranks, st, true, &gc, tdesc,
+                                            big);
     }
     dfree(scratch, st);
     return s;
