@@ -44,7 +44,7 @@ extern thread_local int64_t g_launches;
 // best of the shapes tried is 352 x 23 (2 CTAs/SM: T = 4048, half the
 // cross-rank searches of VT = 15); 8-byte elements 256 x 15 (2 CTAs/SM,
 // requested: 8-byte keys-only merges of random keys +25% over 1 CTA/SM);
-// 12-byte elements 256 x 15 with a 4-deep ring (1 CTA/SM); 16-20-byte
+// 12-byte elements 320 x 17 with a 3-deep ring (1 CTA/SM; see SM_K2S12); 16-20-byte
 // elements (128-bit keys) 256 x 11 (three stages fit).
 template <int NC_, int VT_, int STAGES_, int MINB_ = 1>
 struct K2Geo {
@@ -77,6 +77,21 @@ struct K2Geo {
 #ifndef SM_K2S8_MINB
 #define SM_K2S8_MINB 2
 #endif
+// 12-byte slots (8-byte keys + payload), one CTA per SM: 320 x 17 with three
+// stages -- measured (scripts/gpu_k2s12.sh) against 256 x 15 with four: random
+// i64 + payload 2^26 + 2^26 0.655 -> 0.560 ms, f64 + payload 2^25 + 2^25 0.373
+// -> 0.319, C4 0.617 -> 0.612, C3 0.954 -> 0.959 (448 x 13: 0.559 / 0.318 /
+// 0.613 / 0.964, spills 8 bytes; 384 x 15: 0.590 / 0.336 / 0.616 / 0.968)
+#ifndef SM_K2S12_NC
+#define SM_K2S12_NC 320
+#endif
+#ifndef SM_K2S12_VT
+#define SM_K2S12_VT 17
+#endif
+#ifndef SM_K2S12_ST
+#define SM_K2S12_ST 3
+#endif
+#define SM_K2S12 SM_K2S12_NC, SM_K2S12_VT, SM_K2S12_ST, 1
 #define SM_K2S4 SM_K2S4_NC, SM_K2S4_VT, SM_K2S4_ST, SM_K2S4_MINB
 #define SM_K2S8 SM_K2S8_NC, SM_K2S8_VT, SM_K2S8_ST, SM_K2S8_MINB
 template <typename K, bool HAS_V, typename PV = uint32_t>
@@ -85,7 +100,7 @@ struct K2Shape {
     using type = typename std::conditional<
         bytes <= 4, K2Geo<SM_K2S4>,
         typename std::conditional<bytes <= 8, K2Geo<SM_K2S8>,
-                                  typename std::conditional<bytes <= 12, K2Geo<256, 15, 4>,
+                                  typename std::conditional<bytes <= 12, K2Geo<SM_K2S12>,
                                                             K2Geo<256, 11, 3>>::type>::type>::type;
 };
 // Large plain merges of 8-byte slots: one CTA per SM with a larger tile
