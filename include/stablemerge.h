@@ -346,7 +346,7 @@ int64_t sm_sort_run_n(int32_t key_bytes, int32_t has_vals, int64_t n);
  *
  * sm_set_k1_variant: which cross-rank kernel (rows a1/a2) later calls on
  *   this process launch -- 0 automatic (the default: a warp per search below
- *   4096 searches, else the shared-memory-sample kernel for a plain merge and
+ *   10240 searches, else the shared-memory-sample kernel for a plain merge and
  *   one thread per search for the segmented modes), 1 a warp per search,
  *   2 the sample kernel (plain merges), 3 one thread per search.  Lets the
  *   tests compare every variant's x̄ / ȳ with the oracle (merge_plan_ex).

@@ -171,7 +171,14 @@ constexpr int64_t k3_run(int key_bytes, bool has_v) { return (int64_t)k3_nt(key_
 // (k_cross_ranks_smp, the north_star's design; measured equal to searching
 // them through L1/L2 on C2-C4, within 0.3%).  Few searches (< K1_FEW): a
 // whole warp each, ~log_33 dependent rounds.
-constexpr int K1_FEW = 4096;
+// Measured (i32 keys, n = m, ms per call, threshold 4096 / 16384): 8 M
+// (4148 searches) 0.0440 / 0.0397, 12 M (6200) 0.0554 / 0.0512, 16 M (8290)
+// 0.0642 / 0.0616, 24 M (12434) 0.0864 / 0.0871: a warp per search up to ~10 K
+// searches (one wave of warps), the sample kernel above.
+#ifndef SM_K1_FEW
+#define SM_K1_FEW 10240
+#endif
+constexpr int K1_FEW = SM_K1_FEW;
 #ifndef SM_SMALL_FUSE
 #define SM_SMALL_FUSE 1          // small plain merges: one launch, each CTA ranks its own tasks (k2_local_prologue)
 #endif
