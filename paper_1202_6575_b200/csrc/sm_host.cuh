@@ -113,7 +113,8 @@ struct K2Shape {
 // (C1, 2^20 + 2^20: 23.5 us against 26.6) and so do the sort rounds and the
 // batched merges' segments.
 #ifndef SM_K2_BIG_MIN
-#define SM_K2_BIG_MIN (1ll << 23)     // n + m from which a default plain merge takes the large shape
+#define SM_K2_BIG_MIN (1ll << 23)     // n + m from which a default plain merge takes the large shape (from 2^22:
+                                      //   u32 + payload 2^21 + 2^21 0.0219 -> 0.0229 ms, i64 keys 0.0238 -> 0.0263)
 #endif
 template <typename K, bool HAS_V, typename PV = uint32_t>
 struct K2ShapeBig {
